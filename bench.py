@@ -1,0 +1,317 @@
+"""bench.py -- SGD rating-updates/s of the BGMF epoch on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C4] [--nnz NNZ]
+
+A "step" is one outer step (epoch) of train_blocked: every stratum of
+plan_step, G=1 sweep over each block, plus the per-block post-sweep SSE the
+convergence trace needs.  Workload: BASELINE.json configs[3] (synthetic
+Netflix-shaped, 480k x 17.8k, 100M ratings, k=128, 16x16 blocks), fp32.
+
+Printed JSON (rank 0, one line):
+  value        nnz * K / device time of K epochs, inputs resident in HBM
+               (CUDA events on the engine's stream, barrier + sync around)
+  e2e          same metric through the public API train_blocked() with the
+               dataset in HOST memory: H2D of the ratings + factors, GPU
+               partition, K epochs, D2H of the model, all in the timed region
+  roofline     dominant kernel = the SGD stratum kernel; achieved = its
+               algorithmic bytes (12 + 16k per rating update) / its CUDA-event
+               time, vs the measured HBM copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline the oracle's C restatement of the reference epoch, on the host
+               cores (bounded sample), kind "port"
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def make_workload(name: str, nnz: int | None):
+    from paper_2304_13724_b200 import workloads
+
+    w = workloads.CONFIGS[name]
+    t0 = time.perf_counter()
+    if name == "C1":
+        r, c, v = workloads.ml100k_standin()
+        v = v.astype(np.float64)
+    else:
+        r, c, v = workloads.lowrank(w.n, w.m, nnz or w.nnz, seed=w.seed)
+    return w, r, c, v, time.perf_counter() - t0
+
+
+class CpuReference:
+    """The oracle's C restatement of the reference epoch (trainer.py:138-152 +
+    _kernels.sgd_sweeps), partitioned once, timed per epoch on host cores."""
+
+    def __init__(self, w, r, c, v):
+        from oracle import oracle as O
+
+        self.O, self.w = O, w
+        t0 = time.perf_counter()
+        self.P = O.partition(r, c, v, w.n, w.m, w.grid, w.grid)
+        self.t_partition = time.perf_counter() - t0
+        self.u, self.v = O.init_factors(w.n, w.m, w.k, w.seed)
+        self.step = 0
+
+    def epoch(self, threads: int, max_batches: int | None):
+        O, w, P = self.O, self.w, self.P
+        batches, ids, off = O.flat_plan(w.grid, w.grid, self.step % w.grid)
+        nb = len(batches) if max_batches is None else min(max_batches, len(batches))
+        sse = np.zeros(w.grid * w.grid)
+        bad = np.full((w.grid * w.grid, 2), -1, np.int64)
+        t0 = time.perf_counter()
+        O.lib().oracle_run_step(
+            O._p(P["offsets"], O._i64p), O._p(P["rows"], O._i64p), O._p(P["cols"], O._i64p),
+            O._p(P["values"], O._f64p), O._p(P["row_bounds"], O._i64p),
+            O._p(P["col_bounds"], O._i64p), w.grid, w.grid, O._p(self.u, O._f64p),
+            O._p(self.v, O._f64p), w.k, O._p(ids, O._i32p), O._p(off, O._i32p), nb, 1,
+            w.alpha, w.beta, threads, O._p(sse, O._f64p), O._p(bad, O._i64p))
+        dt = time.perf_counter() - t0
+        self.step += 1
+        updates = int(sum(P["offsets"][b + 1] - P["offsets"][b] for b in ids[: off[nb]]))
+        return updates / dt, updates, dt, nb, len(batches)
+
+
+def run_reference(args):
+    """--impl reference: the oracle's C port of the reference epoch on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w, r, c, v, _ = make_workload(args.config, args.nnz)
+    threads = min(os.cpu_count() or 1, w.grid)
+    ref = CpuReference(w, r, c, v)
+    rates = []
+    for i in range(args.warmup + args.steps):
+        rate, updates, dt, nb, ntot = ref.epoch(threads, args.ref_batches)
+        if i >= args.warmup:
+            rates.append(rate)
+    value = float(np.median(rates))
+    sample = (f"{nb} of {ntot} strata of a {args.config} epoch per step "
+              f"({updates} rating updates), oracle C port, {threads} threads")
+    line = {
+        "impl": "reference", "metric": "SGD rating-updates/sec (epoch)", "value": value,
+        "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": updates / value * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(w, args), "e2e": {"value": value, "unit": "updates/s",
+                                                    "h2d_bytes_per_step": 0,
+                                                    "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+    }
+    print(json.dumps(line))
+
+
+def workload_config(w, args):
+    return {"workload": w.description, "n": w.n, "m": w.m, "nnz": args.nnz or w.nnz, "k": w.k,
+            "grid": f"{w.grid}x{w.grid}", "alpha": w.alpha, "beta": w.beta, "inner_iters": 1,
+            "parallelism": f"stratum-parallel x{args.gpus} GPU",
+            "l2": "inputs larger than L2 (ratings 12 B x nnz + U n x k fp32 >> 126 MB)"}
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2304_13724_b200 as bm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        from paper_2304_13724_b200 import distributed as D
+
+        return D.bench_main(args)
+    torch.cuda.set_device(local)
+    dev = torch.cuda.current_device()
+    w, r, c, v, t_gen = make_workload(args.config, args.nnz)
+    nnz = len(r)
+    d = bm.RatingsDataset(w.n, w.m, r, c, v)
+    cfg = bm.TrainConfig(k=w.k, alpha=w.alpha, beta=w.beta, grid_i=w.grid, grid_j=w.grid,
+                         seed=w.seed, outer_steps=args.steps)
+
+    # ---- e2e through the public API: host dataset in, host model out
+    e2e_val = None
+    h2d = d2h = 0
+    if not args.no_e2e:
+        bm.train_blocked(d, bm.TrainConfig(k=w.k, grid_i=w.grid, grid_j=w.grid, outer_steps=1),
+                         early_stop=False)  # warm the CUDA context / allocator
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = bm.train_blocked(d, cfg, early_stop=False)
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        e2e_val = nnz * args.steps / t_e2e
+        h2d = (nnz * 24 + (w.n + w.m) * w.k * 8) / args.steps
+        d2h = ((w.n + w.m) * w.k * 8 + args.steps * w.grid * w.grid * 8) / args.steps
+        del res
+
+    # ---- device-resident epochs
+    stream = torch.cuda.current_stream()
+    # the engine launches on torch's current stream so torch events bracket the work
+    eng2 = bm.Engine(bm.EngineOptions(device=dev), stream=stream.cuda_stream)
+    eng2.partition(d.rows, d.cols, d.values, w.n, w.m, w.grid, w.grid)
+    m0 = bm.init_factors(w.n, w.m, w.k, w.seed)
+    eng2.set_factors(m0.u, m0.v)
+    del m0
+    plans = [eng2.plan_arrays(bm.plan_step(w.grid, w.grid, s)) for s in range(w.grid)]
+    step = 0
+    for _ in range(args.warmup):
+        ids, off = plans[step % w.grid]
+        eng2.run_step(ids, off, 1, w.alpha, w.beta)
+        step += 1
+    torch.cuda.synchronize()
+    eng2.set_timing(True)
+    eng2.kernel_stats(reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    trace = []
+    with ClockSampler(dev) as clocks:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            ids, off = plans[step % w.grid]
+            sse, bad = eng2.run_step(ids, off, 1, w.alpha, w.beta)
+            assert bad is None
+            trace.append(math.sqrt(float(sse[ids].sum()) / nnz))
+            step += 1
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    total_ms = ev0.elapsed_time(ev1)
+    st = eng2.kernel_stats(reset=True)
+    eng2.set_timing(False)
+    ms_per_step = total_ms / args.steps
+    value = nnz * args.steps / (total_ms / 1e3)
+    hbm, hbm_kind = peaks()
+    sgd_launch_ms = st["sgd_ms"] / max(st["sgd_launches"], 1)
+    alg_per_launch = st["sgd_alg_bytes"] / max(st["sgd_launches"], 1)
+    achieved = alg_per_launch / (sgd_launch_ms / 1e3) / 1e9
+    launches_per_step = (st["sgd_launches"] + st["sse_launches"]) / args.steps
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        threads = min(os.cpu_count() or 1, w.grid)
+        ref = CpuReference(w, r, c, v)
+        rate, updates, dt, nb, ntot = ref.epoch(threads, args.ref_batches)
+        cpu = {"value": rate, "unit": "updates/s", "cores": threads, "kind": "port",
+               "sample": f"{nb} of {ntot} strata of one {args.config} epoch "
+                         f"({updates} updates, {dt:.2f} s), oracle C port of the reference "
+                         f"epoch (_kernels.sgd_sweeps + post-sweep SSE)"}
+        del ref
+
+    line = {
+        "metric": "SGD rating-updates/sec (epoch)", "value": value, "unit": "updates/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded low-rank generator, workloads.lowrank)",
+        "config": workload_config(w, args),
+        "e2e": {"value": e2e_val, "unit": "updates/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "what": "train_blocked(host RatingsDataset) incl. H2D, GPU partition, "
+                        "init upload, K epochs, D2H model"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None, "peak_kind": hbm_kind,
+                     "kernel": "sgd_fast_kernel<32,1>",
+                     "alg_bytes_per_launch": alg_per_launch, "avg_launch_ms": sgd_launch_ms,
+                     "sgd_share_of_step": st["sgd_ms"] / total_ms,
+                     "sse_ms_per_step": st["sse_ms"] / args.steps},
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+        "gpu_launches": int(round(launches_per_step * args.steps)),
+        "train_rmse_trace": trace,
+        "gen_seconds": t_gen,
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--nnz", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-batches", type=int, default=None,
+                    help="strata per CPU sample (default: the whole epoch)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,170 @@
+/*
+ * bgmf.h -- C ABI of libbgmf.so, the B200 (sm_100a) implementation of the
+ * blocked-SGD matrix-factorization hot path of the reference `blockmf`
+ * package (arXiv 2304.13724).  Paths below are relative to
+ * /root/reference/pkg/src/blockmf/.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; every host buffer is caller-owned and is
+ *     only read/written during the call; device buffers are owned by the
+ *     context (bgmf_ctx) or, for bgmf_bind_factors, by the caller;
+ *   - return 0 (BGMF_OK) on success, a negative BGMF_ERR_* code otherwise, with
+ *     a message from bgmf_last_error(ctx) (ctx may be NULL for the stateless
+ *     entry points: the message is then thread-local);
+ *   - numeric divergence is NOT an error code: like the reference
+ *     (_kernels.py:5-7,49-50) it is reported through out-parameters
+ *     (bad_entry / bad_iter >= 0, sse_after = NaN);
+ *   - one host thread per context at a time; distinct contexts (and the
+ *     stateless calls, which use a thread-local scratch context) may be used
+ *     concurrently from different threads.  The GIL is released by ctypes.
+ */
+#ifndef BGMF_H
+#define BGMF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BGMF_OK 0
+#define BGMF_ERR_CUDA (-1)   /* CUDA runtime error (message has details) */
+#define BGMF_ERR_ARG (-2)    /* invalid argument (shape, range, NULL)    */
+#define BGMF_ERR_STATE (-3)  /* call order: e.g. run_step before partition */
+#define BGMF_ERR_DATA (-4)   /* dataset violates its contract (index range) */
+#define BGMF_ERR_NOMEM (-5)  /* device allocation failed                  */
+
+typedef struct bgmf_ctx bgmf_ctx;
+
+/* ABI version (major*100 + minor). */
+int bgmf_version(void);
+
+/* Create a context on CUDA device `device`.  `stream` is a cudaStream_t to
+ * launch on (NULL: the context creates its own non-blocking stream). */
+int bgmf_create(int device, void* stream, bgmf_ctx** out);
+void bgmf_destroy(bgmf_ctx* ctx);
+const char* bgmf_last_error(const bgmf_ctx* ctx);
+
+/* Tunables (B200 knobs; none changes the reference's semantics):
+ *   "exact"      0/1   1 = fp64 sequential-per-block kernels, bit-identical to
+ *                      the reference (_kernels.py fastmath=False order);
+ *                      0 = fp32 warp-per-rating lossless kernels (default).
+ *   "min_chunk"  int   minimum ratings per worker group in fast mode
+ *                      (bounds per-block concurrency on small blocks; 48).
+ *   "timing"     0/1   record CUDA events around every kernel launch.
+ *   "warps_per_sm" int resident-warp target used to size chunks (0 = occupancy). */
+int bgmf_set_option(bgmf_ctx* ctx, const char* key, double value);
+
+/* Bucket the ratings into the I x J block grid on the GPU.
+ * Replaces BlockedDataset.__init__ (partition.py:112-136) and make_grid /
+ * split_bounds (partition.py:18-71): balanced slabs, entries sorted by
+ * (block, row, col) with ties in input order -- bit-exact with np.lexsort.
+ * rows/cols are global int64 indices, vals fp64 (RatingsDataset layout,
+ * core.py:53-108).  Returns BGMF_ERR_DATA when an index is outside n x m. */
+int bgmf_partition(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
+                   const double* vals, int64_t nnz, int64_t n, int64_t m,
+                   int grid_i, int grid_j);
+
+/* Copy the partition back (any pointer may be NULL):
+ *   offsets[I*J+1]    BlockedDataset._offsets            (partition.py:134-136)
+ *   order[nnz]        source index of each sorted entry (values = vals[order],
+ *                     BlockedDataset._values, partition.py:131)
+ *   lrows/lcols[nnz]  block-local coordinates (BlockedDataset._rows/_cols,
+ *                     partition.py:125-130). */
+int bgmf_partition_export(bgmf_ctx* ctx, int64_t* offsets, int64_t* order,
+                          int32_t* lrows, int32_t* lcols);
+
+/* Upload U (n x k) and V (m x k), row-major fp64 as FactorModel.u/.v
+ * (core.py:139-176).  Fast mode stores fp32 rows padded to a multiple of 4. */
+int bgmf_set_factors(bgmf_ctx* ctx, const double* u, const double* v,
+                     int64_t n, int64_t m, int k);
+/* Download the factors into caller fp64 buffers (n x k, m x k). */
+int bgmf_get_factors(bgmf_ctx* ctx, double* u, double* v);
+
+/* Use caller-owned device factor buffers (fp32, row stride kp >= k, kp % 4 ==
+ * 0, zero padding) instead of context-owned ones -- e.g. torch tensors that
+ * NCCL moves between GPUs.  Fast mode only. */
+int bgmf_bind_factors(bgmf_ctx* ctx, void* u_dev, void* v_dev, int64_t n,
+                      int64_t m, int k, int kp);
+
+/* One outer step (trainer.py:125-158): for each batch (plan_step order,
+ * scheduler.py:45-75) run `inner_iters` SGD sweeps over every block of the
+ * batch concurrently, then each block's post-sweep SSE (_kernels.py:56).
+ *   plan[batch_off[t] .. batch_off[t+1]) = flat block ids bi*J+bj of batch t
+ *   sse_out[I*J]  per-block post-sweep SSE (blocks not in the plan: 0)
+ *   bad_out[3]    {plan position, entry, inner iteration} of the first
+ *                 diverged block in plan order, or {-1,-1,-1}.
+ * Equivalent to `_kernels.sgd_sweeps` on every block of the plan followed by
+ * the trainer's merge.  Synchronous: returns after sse_out is on the host. */
+int bgmf_run_step(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
+                  int nbatch, int inner_iters, double alpha, double beta,
+                  double* sse_out, int64_t* bad_out);
+
+/* Converge mode (ConvergeEachBlock, kernel.py:108-126, _kernels.py:62-100):
+ * every block of every batch sweeps until its RMSE improvement < tol or
+ * `cap` sweeps.  iters_out[I*J] sweeps used, capped_out[I*J] 0/1. */
+int bgmf_run_step_converge(bgmf_ctx* ctx, const int32_t* plan,
+                           const int32_t* batch_off, int nbatch, double tol,
+                           int64_t cap, double alpha, double beta,
+                           double* sse_out, int64_t* iters_out,
+                           int32_t* capped_out, int64_t* bad_out);
+
+/* SSE of the current factors over all partitioned training entries
+ * (metrics.py:39-52 numerator, for AdaptiveDecreasing's RMSE_0). */
+int bgmf_train_sse(bgmf_ctx* ctx, double* sse_out);
+
+/* Held-out set for per-step test RMSE (HoldoutEvaluator, metrics.py:55-81):
+ * global int64 rows/cols, fp64 values, cold[count] (1 = predict `fallback`). */
+int bgmf_holdout_set(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
+                     const double* vals, const uint8_t* cold, int64_t count,
+                     double fallback);
+int bgmf_holdout_sse(bgmf_ctx* ctx, double* sse_out);
+
+/* Accumulated kernel time since the last reset (requires "timing"=1):
+ * out[0] sgd ms, out[1] sse ms, out[2] sgd launches, out[3] sse launches,
+ * out[4] algorithmic bytes of the timed sgd launches (ratings*(12+16k)). */
+int bgmf_kernel_stats(bgmf_ctx* ctx, double* out5, int reset);
+
+/* ---- stateless drop-ins for the reference's native loops ---------------
+ * Same arguments and results as the numba functions they replace; all
+ * arrays are host memory, u/v are updated in place.  Computed on the GPU
+ * in fp64 sequential order (bit-identical with the reference). */
+
+/* _kernels.py:31-59 sgd_sweeps(rows, cols, vals, u, v, alpha, beta, iters) */
+int bgmf_sgd_sweeps(const int64_t* rows, const int64_t* cols,
+                    const double* vals, int64_t count, double* u,
+                    int64_t u_rows, double* v, int64_t v_rows, int k,
+                    double alpha, double beta, int iters, double* sse_before,
+                    double* sse_after, int64_t* bad_entry, int64_t* bad_iter);
+
+/* _kernels.py:62-100 sgd_converge(rows, cols, vals, u, v, alpha, beta, tol, cap) */
+int bgmf_sgd_converge(const int64_t* rows, const int64_t* cols,
+                      const double* vals, int64_t count, double* u,
+                      int64_t u_rows, double* v, int64_t v_rows, int k,
+                      double alpha, double beta, double tol, int64_t cap,
+                      double* sse_before, double* sse_after,
+                      int64_t* iters_used, int32_t* capped,
+                      int64_t* bad_entry, int64_t* bad_iter);
+
+/* _kernels.py:16-28 block_sse(rows, cols, vals, u, v) */
+int bgmf_block_sse(const int64_t* rows, const int64_t* cols,
+                   const double* vals, int64_t count, const double* u,
+                   int64_t u_rows, const double* v, int64_t v_rows, int k,
+                   double* sse);
+
+/* FactorModel.predict (core.py:163-165): out[i] = u[rows[i]] . v[cols[i]] */
+int bgmf_predict(const double* u, int64_t n, const double* v, int64_t m, int k,
+                 const int64_t* rows, const int64_t* cols, int64_t count,
+                 double* out);
+
+/* rmse / HoldoutEvaluator numerator (metrics.py:51,78-80): sum of squared
+ * errors, cold[i] != 0 predicts `fallback` (cold may be NULL). */
+int bgmf_sse(const double* u, int64_t n, const double* v, int64_t m, int k,
+             const int64_t* rows, const int64_t* cols, const double* vals,
+             const uint8_t* cold, double fallback, int64_t count, double* sse);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BGMF_H */

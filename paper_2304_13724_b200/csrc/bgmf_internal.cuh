@@ -1,0 +1,155 @@
+// bgmf_internal.cuh -- shared declarations of libbgmf.so (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/bgmf.h"
+
+namespace bgmf {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// One block of one batch (fast path).  Entries [begin, end) of the
+// partition arrays are cut into chunks of chunk_len; chunk c of the batch
+// belongs to the work item whose [first_chunk, first_chunk + nchunks)
+// contains c.
+struct BlockWork {
+  int64_t begin, end;           // entry range in the partition arrays
+  int64_t row_start, col_start; // factor slice offsets (rows of U / V)
+  int32_t chunk_len;            // ratings per worker group
+  int32_t first_chunk;          // exclusive prefix of chunk counts in batch
+  int32_t block_id;             // bi * J + bj
+  int32_t pos;                  // position in the step plan
+};
+
+// Divergence record: smaller = earlier in the reference's order
+// (plan position, then inner iteration, then entry).
+__host__ __device__ inline unsigned long long pack_bad(int64_t pos, int64_t iter,
+                                                       int64_t entry) {
+  return ((unsigned long long)pos << 48) | ((unsigned long long)(iter & 0xFFFF) << 32) |
+         (unsigned long long)(entry & 0xFFFFFFFFll);
+}
+constexpr unsigned long long kNoBad = ~0ull;
+
+struct TimedLaunch {
+  cudaEvent_t a, b;
+  int kind;        // 0 sgd, 1 sse
+  double bytes;    // algorithmic bytes (sgd)
+};
+
+}  // namespace bgmf
+
+struct bgmf_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int num_sms = 148;
+
+  // options
+  bool exact = false;
+  int min_chunk = 48;
+  bool timing = false;
+  int warps_per_sm = 0;
+
+  // grid + partition
+  int64_t n = 0, m = 0, nnz = 0;
+  int I = 0, J = 0;
+  std::vector<int64_t> row_bounds, col_bounds, h_offsets;
+  bool partitioned = false;
+  int32_t* d_lrow = nullptr;
+  int32_t* d_lcol = nullptr;
+  float* d_val = nullptr;
+  double* d_val64 = nullptr;
+  uint32_t* d_order = nullptr;
+
+  // factors
+  int k = 0, kp = 0;
+  bool have_factors = false, bound = false;
+  float* d_u = nullptr;
+  float* d_v = nullptr;
+  double* d_u64 = nullptr;
+  double* d_v64 = nullptr;
+
+  // step scratch
+  double* d_sse = nullptr;               // [I*J]
+  unsigned long long* d_bad = nullptr;   // [1]
+  bgmf::BlockWork* d_work = nullptr;
+  bgmf::BlockWork* h_work = nullptr;     // pinned
+  size_t work_cap = 0;
+  double* h_sse = nullptr;               // pinned [I*J]
+  unsigned long long* h_bad = nullptr;   // pinned [1]
+
+  // holdout
+  int32_t* d_hrow = nullptr;
+  int32_t* d_hcol = nullptr;
+  float* d_hval = nullptr;
+  double* d_hval64 = nullptr;
+  uint8_t* d_hcold = nullptr;
+  int64_t hcount = 0;
+  double hfallback = 0.0;
+  double* d_partials = nullptr;          // eval partial sums
+  double* h_scalar = nullptr;            // pinned
+
+  // timing
+  std::vector<bgmf::TimedLaunch> events;
+  size_t events_used = 0;
+  double t_sgd_ms = 0, t_sse_ms = 0, t_bytes = 0;
+  int64_t n_sgd = 0, n_sse = 0;
+};
+
+namespace bgmf {
+
+// error helpers --------------------------------------------------------
+int fail(bgmf_ctx* ctx, int code, const std::string& msg);
+int cuda_fail(bgmf_ctx* ctx, cudaError_t e, const char* what);
+
+#define BGMF_CK(ctx, call)                                   \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) return bgmf::cuda_fail((ctx), _e, #call); \
+  } while (0)
+
+// partition.cu
+int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
+                     const double* vals, int64_t nnz, int64_t n, int64_t m, int I, int J);
+
+// sgd.cu
+int run_step_fast(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
+                  int nbatch, int iters, float alpha, float beta);
+int run_step_exact(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
+                   int nbatch, int iters, double alpha, double beta);
+int run_step_converge_exact(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
+                            int nbatch, double tol, int64_t cap, double alpha, double beta,
+                            int64_t* iters_out, int32_t* capped_out);
+int run_step_converge_fast(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
+                           int nbatch, double tol, int64_t cap, double alpha, double beta,
+                           int64_t* iters_out, int32_t* capped_out);
+int train_sse_fast(bgmf_ctx* ctx, double* out);
+int train_sse_exact(bgmf_ctx* ctx, double* out);
+int ensure_step_scratch(bgmf_ctx* ctx, size_t nwork);
+// single-block exact kernel used by the stateless drop-ins
+int block_exact(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const double* vals,
+                int64_t count, double* u, int64_t u_rows, double* v, int64_t v_rows, int k,
+                double alpha, double beta, int mode, int iters, double tol, int64_t cap,
+                double* out6);
+
+// eval.cu
+int eval_sse_f32(bgmf_ctx* ctx, const int32_t* rows, const int32_t* cols, const float* vals,
+                 const uint8_t* cold, double fallback, int64_t count, double* out);
+int eval_sse_f64(bgmf_ctx* ctx, const double* u, const double* v, int k, const int32_t* rows,
+                 const int32_t* cols, const double* vals, const uint8_t* cold, double fallback,
+                 int64_t count, double* out);
+int predict_f64(bgmf_ctx* ctx, const double* u, const double* v, int k, const int32_t* rows,
+                const int32_t* cols, int64_t count, double* out_dev);
+
+// timing
+void record_begin(bgmf_ctx* ctx, int kind, double bytes, TimedLaunch** slot);
+void record_end(bgmf_ctx* ctx, TimedLaunch* slot);
+void harvest_timing(bgmf_ctx* ctx);
+
+}  // namespace bgmf

@@ -1,0 +1,580 @@
+// capi.cu -- the extern "C" boundary of libbgmf.so (declared in
+// include/bgmf.h).  Host-side orchestration only; kernels live in
+// partition.cu / sgd.cu / eval.cu.
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+
+#include "bgmf_internal.cuh"
+
+namespace bgmf {
+
+thread_local std::string g_err;  // errors of calls without a context
+
+int fail(bgmf_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg; else g_err = msg;
+  return code;
+}
+
+int cuda_fail(bgmf_ctx* ctx, cudaError_t e, const char* what) {
+  std::string msg = std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                    cudaGetErrorString(e) + ") in " + what;
+  cudaGetLastError();  // clear sticky-free errors
+  return fail(ctx, e == cudaErrorMemoryAllocation ? BGMF_ERR_NOMEM : BGMF_ERR_CUDA, msg);
+}
+
+void record_begin(bgmf_ctx* c, int kind, double bytes, TimedLaunch** slot) {
+  if (c->events_used == c->events.size()) {
+    TimedLaunch t;
+    cudaEventCreate(&t.a);
+    cudaEventCreate(&t.b);
+    c->events.push_back(t);
+  }
+  TimedLaunch* t = &c->events[c->events_used++];
+  t->kind = kind;
+  t->bytes = bytes;
+  cudaEventRecord(t->a, c->stream);
+  *slot = t;
+}
+
+void record_end(bgmf_ctx* c, TimedLaunch* slot) { cudaEventRecord(slot->b, c->stream); }
+
+void harvest_timing(bgmf_ctx* c) {
+  for (size_t i = 0; i < c->events_used; ++i) {
+    TimedLaunch& t = c->events[i];
+    float ms = 0.f;
+    cudaEventSynchronize(t.b);
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    if (t.kind == 0) { c->t_sgd_ms += ms; c->n_sgd++; c->t_bytes += t.bytes; }
+    else { c->t_sse_ms += ms; c->n_sse++; }
+  }
+  c->events_used = 0;
+}
+
+namespace {
+
+__global__ void f64_to_f32_rows(const double* __restrict__ src, float* __restrict__ dst,
+                                int64_t rows, int k, int kp) {
+  const int64_t total = rows * kp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / kp;
+    const int g = (int)(i - r * kp);
+    dst[i] = g < k ? (float)src[r * k + g] : 0.f;
+  }
+}
+
+__global__ void f32_to_f64_rows(const float* __restrict__ src, double* __restrict__ dst,
+                                int64_t rows, int k, int kp) {
+  const int64_t total = rows * k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / k;
+    const int g = (int)(i - r * k);
+    dst[i] = (double)src[r * kp + g];
+  }
+}
+
+constexpr int64_t kStageRows = 1 << 16;
+
+// fp64 host (rows x k) -> fp32 device (rows x kp) through a staging buffer.
+int upload_rows(bgmf_ctx* c, const double* h, float* d, int64_t rows, int k, int kp) {
+  if (rows == 0) return BGMF_OK;
+  double* stage = nullptr;
+  const int64_t chunk = rows < kStageRows ? rows : kStageRows;
+  BGMF_CK(c, cudaMalloc(&stage, (size_t)chunk * k * 8));
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const int64_t nr = rows - r0 < chunk ? rows - r0 : chunk;
+    cudaError_t e = cudaMemcpyAsync(stage, h + r0 * k, (size_t)nr * k * 8,
+                                    cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) { cudaFree(stage); return cuda_fail(c, e, "upload_rows"); }
+    f64_to_f32_rows<<<c->num_sms * 4, 256, 0, c->stream>>>(stage, d + r0 * kp, nr, k, kp);
+  }
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  cudaFree(stage);
+  if (e != cudaSuccess) return cuda_fail(c, e, "upload_rows sync");
+  return BGMF_OK;
+}
+
+int download_rows(bgmf_ctx* c, const float* d, double* h, int64_t rows, int k, int kp) {
+  if (rows == 0) return BGMF_OK;
+  double* stage = nullptr;
+  const int64_t chunk = rows < kStageRows ? rows : kStageRows;
+  BGMF_CK(c, cudaMalloc(&stage, (size_t)chunk * k * 8));
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const int64_t nr = rows - r0 < chunk ? rows - r0 : chunk;
+    f32_to_f64_rows<<<c->num_sms * 4, 256, 0, c->stream>>>(d + r0 * kp, stage, nr, k, kp);
+    cudaError_t e = cudaMemcpyAsync(h + r0 * k, stage, (size_t)nr * k * 8,
+                                    cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) { cudaFree(stage); return cuda_fail(c, e, "download_rows"); }
+  }
+  cudaFree(stage);
+  return BGMF_OK;
+}
+
+void free_factors(bgmf_ctx* c) {
+  if (!c->bound) {
+    if (c->d_u) cudaFree(c->d_u);
+    if (c->d_v) cudaFree(c->d_v);
+  }
+  if (c->d_u64) cudaFree(c->d_u64);
+  if (c->d_v64) cudaFree(c->d_v64);
+  c->d_u = c->d_v = nullptr;
+  c->d_u64 = c->d_v64 = nullptr;
+  c->bound = false;
+  c->have_factors = false;
+}
+
+void free_holdout(bgmf_ctx* c) {
+  if (c->d_hrow) cudaFree(c->d_hrow);
+  if (c->d_hcol) cudaFree(c->d_hcol);
+  if (c->d_hval) cudaFree(c->d_hval);
+  if (c->d_hval64) cudaFree(c->d_hval64);
+  if (c->d_hcold) cudaFree(c->d_hcold);
+  c->d_hrow = c->d_hcol = nullptr;
+  c->d_hval = nullptr;
+  c->d_hval64 = nullptr;
+  c->d_hcold = nullptr;
+  c->hcount = 0;
+}
+
+int check_step_ready(bgmf_ctx* c) {
+  if (!c->partitioned) return fail(c, BGMF_ERR_STATE, "bgmf_partition has not been called");
+  if (!c->have_factors) return fail(c, BGMF_ERR_STATE, "bgmf_set_factors has not been called");
+  if (c->exact && (!c->d_val64 || !c->d_u64))
+    return fail(c, BGMF_ERR_STATE, "exact mode must be enabled before partition and set_factors");
+  if (!c->exact && !c->d_u) return fail(c, BGMF_ERR_STATE, "fast-mode factors missing");
+  return BGMF_OK;
+}
+
+void fill_bad(bgmf_ctx* c, int64_t* bad_out) {
+  const unsigned long long b = *c->h_bad;
+  if (b == kNoBad) {
+    bad_out[0] = bad_out[1] = bad_out[2] = -1;
+  } else {
+    bad_out[0] = (int64_t)(b >> 48);
+    bad_out[1] = (int64_t)(b & 0xFFFFFFFFull);
+    bad_out[2] = (int64_t)((b >> 32) & 0xFFFF);
+  }
+}
+
+// Per-thread scratch context for the stateless drop-in entry points.
+bgmf_ctx* scratch_ctx(int* rc) {
+  thread_local std::unique_ptr<bgmf_ctx, void (*)(bgmf_ctx*)> ctx(nullptr, bgmf_destroy);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) { *rc = cuda_fail(nullptr, e, "cudaGetDevice"); return nullptr; }
+  if (!ctx || ctx->device != dev) {
+    bgmf_ctx* c = nullptr;
+    *rc = bgmf_create(dev, nullptr, &c);
+    if (*rc) return nullptr;
+    ctx.reset(c);
+  }
+  *rc = BGMF_OK;
+  return ctx.get();
+}
+
+}  // namespace
+}  // namespace bgmf
+
+using namespace bgmf;
+
+extern "C" {
+
+int bgmf_version(void) { return 100; }
+
+int bgmf_create(int device, void* stream, bgmf_ctx** out) {
+  if (!out) return fail(nullptr, BGMF_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) return fail(nullptr, BGMF_ERR_ARG, "no such CUDA device");
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+  auto* c = new bgmf_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+  } else {
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete c; return cuda_fail(nullptr, e, "cudaStreamCreate"); }
+    c->own_stream = true;
+  }
+  *out = c;
+  return BGMF_OK;
+}
+
+void bgmf_destroy(bgmf_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  free_factors(c);
+  free_holdout(c);
+  cudaFree(c->d_lrow); cudaFree(c->d_lcol); cudaFree(c->d_val); cudaFree(c->d_val64);
+  cudaFree(c->d_order); cudaFree(c->d_sse); cudaFree(c->d_bad); cudaFree(c->d_work);
+  cudaFree(c->d_partials);
+  if (c->h_work) cudaFreeHost(c->h_work);
+  if (c->h_sse) cudaFreeHost(c->h_sse);
+  if (c->h_bad) cudaFreeHost(c->h_bad);
+  for (auto& t : c->events) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* bgmf_last_error(const bgmf_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
+  if (!c || !key) return fail(c, BGMF_ERR_ARG, "NULL argument");
+  if (!strcmp(key, "exact")) c->exact = value != 0.0;
+  else if (!strcmp(key, "min_chunk")) c->min_chunk = value < 1 ? 1 : (int)value;
+  else if (!strcmp(key, "timing")) c->timing = value != 0.0;
+  else if (!strcmp(key, "warps_per_sm")) c->warps_per_sm = value < 0 ? 0 : (int)value;
+  else return fail(c, BGMF_ERR_ARG, std::string("unknown option ") + key);
+  return BGMF_OK;
+}
+
+int bgmf_partition(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const double* vals,
+                   int64_t nnz, int64_t n, int64_t m, int grid_i, int grid_j) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  cudaSetDevice(c->device);
+  // the step scratch is sized by the grid
+  cudaFree(c->d_sse); cudaFreeHost(c->h_sse); cudaFree(c->d_bad); cudaFreeHost(c->h_bad);
+  c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
+  return partition_device(c, rows, cols, vals, nnz, n, m, grid_i, grid_j);
+}
+
+int bgmf_partition_export(bgmf_ctx* c, int64_t* offsets, int64_t* order, int32_t* lrows,
+                          int32_t* lcols) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (!c->partitioned) return fail(c, BGMF_ERR_STATE, "bgmf_partition has not been called");
+  cudaSetDevice(c->device);
+  if (offsets) memcpy(offsets, c->h_offsets.data(), c->h_offsets.size() * 8);
+  const int64_t n = c->nnz;
+  if (n == 0) return BGMF_OK;
+  if (lrows) BGMF_CK(c, cudaMemcpyAsync(lrows, c->d_lrow, n * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (lcols) BGMF_CK(c, cudaMemcpyAsync(lcols, c->d_lcol, n * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (order) {
+    std::vector<uint32_t> o((size_t)n);
+    BGMF_CK(c, cudaMemcpyAsync(o.data(), c->d_order, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    BGMF_CK(c, cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < n; ++i) order[i] = (int64_t)o[i];
+  }
+  BGMF_CK(c, cudaStreamSynchronize(c->stream));
+  return BGMF_OK;
+}
+
+int bgmf_set_factors(bgmf_ctx* c, const double* u, const double* v, int64_t n, int64_t m, int k) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (!u || !v || k < 1 || n < 1 || m < 1) return fail(c, BGMF_ERR_ARG, "bad factor arguments");
+  if (c->partitioned && (n != c->n || m != c->m))
+    return fail(c, BGMF_ERR_ARG, "factor shapes do not match the partitioned dataset");
+  cudaSetDevice(c->device);
+  if (c->exact) {
+    free_factors(c);
+    c->k = k; c->kp = k;
+    BGMF_CK(c, cudaMalloc(&c->d_u64, (size_t)n * k * 8));
+    BGMF_CK(c, cudaMalloc(&c->d_v64, (size_t)m * k * 8));
+    BGMF_CK(c, cudaMemcpyAsync(c->d_u64, u, (size_t)n * k * 8, cudaMemcpyHostToDevice, c->stream));
+    BGMF_CK(c, cudaMemcpyAsync(c->d_v64, v, (size_t)m * k * 8, cudaMemcpyHostToDevice, c->stream));
+    BGMF_CK(c, cudaStreamSynchronize(c->stream));
+    c->have_factors = true;
+    return BGMF_OK;
+  }
+  const int kp = (k + 3) / 4 * 4;
+  if (!(c->bound && c->k == k)) {
+    free_factors(c);
+    c->k = k; c->kp = kp;
+    BGMF_CK(c, cudaMalloc(&c->d_u, (size_t)n * kp * 4));
+    BGMF_CK(c, cudaMalloc(&c->d_v, (size_t)m * kp * 4));
+  }
+  int rc = upload_rows(c, u, c->d_u, n, k, c->kp);
+  if (!rc) rc = upload_rows(c, v, c->d_v, m, k, c->kp);
+  if (rc) return rc;
+  c->have_factors = true;
+  return BGMF_OK;
+}
+
+int bgmf_bind_factors(bgmf_ctx* c, void* u_dev, void* v_dev, int64_t n, int64_t m, int k, int kp) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (c->exact) return fail(c, BGMF_ERR_STATE, "bind_factors is fast-mode only");
+  if (!u_dev || !v_dev || k < 1 || kp < k || kp % 4) return fail(c, BGMF_ERR_ARG, "bad bind");
+  if (((uintptr_t)u_dev | (uintptr_t)v_dev) & 15) return fail(c, BGMF_ERR_ARG, "unaligned factors");
+  if (c->partitioned && (n != c->n || m != c->m))
+    return fail(c, BGMF_ERR_ARG, "factor shapes do not match the partitioned dataset");
+  free_factors(c);
+  c->d_u = (float*)u_dev;
+  c->d_v = (float*)v_dev;
+  c->k = k; c->kp = kp;
+  c->bound = true;
+  c->have_factors = true;
+  return BGMF_OK;
+}
+
+int bgmf_get_factors(bgmf_ctx* c, double* u, double* v) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (!c->have_factors) return fail(c, BGMF_ERR_STATE, "no factors on the device");
+  cudaSetDevice(c->device);
+  const int64_t n = c->n, m = c->m;
+  if (c->exact) {
+    if (u) BGMF_CK(c, cudaMemcpyAsync(u, c->d_u64, (size_t)n * c->k * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (v) BGMF_CK(c, cudaMemcpyAsync(v, c->d_v64, (size_t)m * c->k * 8, cudaMemcpyDeviceToHost, c->stream));
+    BGMF_CK(c, cudaStreamSynchronize(c->stream));
+    return BGMF_OK;
+  }
+  int rc = BGMF_OK;
+  if (u) rc = download_rows(c, c->d_u, u, n, c->k, c->kp);
+  if (!rc && v) rc = download_rows(c, c->d_v, v, m, c->k, c->kp);
+  return rc;
+}
+
+int bgmf_run_step(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
+                  int inner_iters, double alpha, double beta, double* sse_out, int64_t* bad_out) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (!plan || !batch_off || nbatch < 0 || !sse_out || !bad_out)
+    return fail(c, BGMF_ERR_ARG, "NULL argument");
+  if (inner_iters < 1 || inner_iters > 65535) return fail(c, BGMF_ERR_ARG, "inner_iters out of range");
+  int rc = check_step_ready(c);
+  if (rc) return rc;
+  cudaSetDevice(c->device);
+  rc = c->exact ? run_step_exact(c, plan, batch_off, nbatch, inner_iters, alpha, beta)
+                : run_step_fast(c, plan, batch_off, nbatch, inner_iters, (float)alpha, (float)beta);
+  if (rc) return rc;
+  const int nb = c->I * c->J;
+  for (int b = 0; b < nb; ++b) sse_out[b] = c->h_sse[b];
+  fill_bad(c, bad_out);
+  return BGMF_OK;
+}
+
+int bgmf_run_step_converge(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off,
+                           int nbatch, double tol, int64_t cap, double alpha, double beta,
+                           double* sse_out, int64_t* iters_out, int32_t* capped_out,
+                           int64_t* bad_out) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (!plan || !batch_off || !sse_out || !iters_out || !capped_out || !bad_out)
+    return fail(c, BGMF_ERR_ARG, "NULL argument");
+  if (!(tol > 0) || cap < 1) return fail(c, BGMF_ERR_ARG, "converge mode needs tol > 0, cap >= 1");
+  int rc = check_step_ready(c);
+  if (rc) return rc;
+  cudaSetDevice(c->device);
+  rc = c->exact ? run_step_converge_exact(c, plan, batch_off, nbatch, tol, cap, alpha, beta,
+                                          iters_out, capped_out)
+                : run_step_converge_fast(c, plan, batch_off, nbatch, tol, cap, alpha, beta,
+                                         iters_out, capped_out);
+  if (rc) return rc;
+  const int nb = c->I * c->J;
+  for (int b = 0; b < nb; ++b) sse_out[b] = c->h_sse[b];
+  fill_bad(c, bad_out);
+  return BGMF_OK;
+}
+
+int bgmf_train_sse(bgmf_ctx* c, double* sse_out) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  int rc = check_step_ready(c);
+  if (rc) return rc;
+  cudaSetDevice(c->device);
+  rc = ensure_step_scratch(c, 1);
+  if (rc) return rc;
+  return c->exact ? train_sse_exact(c, sse_out) : train_sse_fast(c, sse_out);
+}
+
+int bgmf_holdout_set(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const double* vals,
+                     const uint8_t* cold, int64_t count, double fallback) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (count < 0 || (count > 0 && (!rows || !cols || !vals)))
+    return fail(c, BGMF_ERR_ARG, "bad holdout arguments");
+  cudaSetDevice(c->device);
+  free_holdout(c);
+  const size_t N = (size_t)(count > 0 ? count : 1);
+  std::vector<int32_t> r(N), q(N);
+  for (int64_t i = 0; i < count; ++i) {
+    if (rows[i] < 0 || rows[i] >= c->n || cols[i] < 0 || cols[i] >= c->m)
+      return fail(c, BGMF_ERR_DATA, "holdout index outside the matrix");
+    r[i] = (int32_t)rows[i];
+    q[i] = (int32_t)cols[i];
+  }
+  std::vector<float> vf(N);
+  for (int64_t i = 0; i < count; ++i) vf[i] = (float)vals[i];
+  BGMF_CK(c, cudaMalloc(&c->d_hrow, N * 4));
+  BGMF_CK(c, cudaMalloc(&c->d_hcol, N * 4));
+  BGMF_CK(c, cudaMalloc(&c->d_hval, N * 4));
+  BGMF_CK(c, cudaMalloc(&c->d_hval64, N * 8));
+  BGMF_CK(c, cudaMalloc(&c->d_hcold, N));
+  if (count > 0) {
+    BGMF_CK(c, cudaMemcpyAsync(c->d_hrow, r.data(), count * 4, cudaMemcpyHostToDevice, c->stream));
+    BGMF_CK(c, cudaMemcpyAsync(c->d_hcol, q.data(), count * 4, cudaMemcpyHostToDevice, c->stream));
+    BGMF_CK(c, cudaMemcpyAsync(c->d_hval, vf.data(), count * 4, cudaMemcpyHostToDevice, c->stream));
+    BGMF_CK(c, cudaMemcpyAsync(c->d_hval64, vals, count * 8, cudaMemcpyHostToDevice, c->stream));
+    if (cold) BGMF_CK(c, cudaMemcpyAsync(c->d_hcold, cold, count, cudaMemcpyHostToDevice, c->stream));
+    else BGMF_CK(c, cudaMemsetAsync(c->d_hcold, 0, count, c->stream));
+  }
+  BGMF_CK(c, cudaStreamSynchronize(c->stream));
+  c->hcount = count;
+  c->hfallback = fallback;
+  return BGMF_OK;
+}
+
+int bgmf_holdout_sse(bgmf_ctx* c, double* sse_out) {
+  if (!c || !sse_out) return fail(c, BGMF_ERR_ARG, "NULL argument");
+  if (!c->have_factors) return fail(c, BGMF_ERR_STATE, "no factors on the device");
+  if (!c->d_hrow) return fail(c, BGMF_ERR_STATE, "bgmf_holdout_set has not been called");
+  cudaSetDevice(c->device);
+  if (c->hcount == 0) { *sse_out = 0.0; return BGMF_OK; }
+  if (c->exact)
+    return eval_sse_f64(c, c->d_u64, c->d_v64, c->k, c->d_hrow, c->d_hcol, c->d_hval64, c->d_hcold,
+                        c->hfallback, c->hcount, sse_out);
+  return eval_sse_f32(c, c->d_hrow, c->d_hcol, c->d_hval, c->d_hcold, c->hfallback, c->hcount,
+                      sse_out);
+}
+
+int bgmf_kernel_stats(bgmf_ctx* c, double* out5, int reset) {
+  if (!c || !out5) return fail(c, BGMF_ERR_ARG, "NULL argument");
+  out5[0] = c->t_sgd_ms;
+  out5[1] = c->t_sse_ms;
+  out5[2] = (double)c->n_sgd;
+  out5[3] = (double)c->n_sse;
+  out5[4] = c->t_bytes;
+  if (reset) { c->t_sgd_ms = c->t_sse_ms = c->t_bytes = 0; c->n_sgd = c->n_sse = 0; }
+  return BGMF_OK;
+}
+
+// ---------------------------------------------------------------- stateless
+
+int bgmf_sgd_sweeps(const int64_t* rows, const int64_t* cols, const double* vals, int64_t count,
+                    double* u, int64_t u_rows, double* v, int64_t v_rows, int k, double alpha,
+                    double beta, int iters, double* sse_before, double* sse_after,
+                    int64_t* bad_entry, int64_t* bad_iter) {
+  int rc;
+  bgmf_ctx* c = scratch_ctx(&rc);
+  if (!c) return rc;
+  if (iters < 0) return fail(nullptr, BGMF_ERR_ARG, "iters must be >= 0");
+  double o[6];
+  rc = block_exact(c, rows, cols, vals, count, u, u_rows, v, v_rows, k, alpha, beta, 0, iters,
+                   0.0, 0, o);
+  if (rc) { g_err = c->err; return rc; }
+  *sse_before = o[0]; *sse_after = o[1];
+  *bad_entry = (int64_t)o[4]; *bad_iter = (int64_t)o[5];
+  return BGMF_OK;
+}
+
+int bgmf_sgd_converge(const int64_t* rows, const int64_t* cols, const double* vals, int64_t count,
+                      double* u, int64_t u_rows, double* v, int64_t v_rows, int k, double alpha,
+                      double beta, double tol, int64_t cap, double* sse_before, double* sse_after,
+                      int64_t* iters_used, int32_t* capped, int64_t* bad_entry,
+                      int64_t* bad_iter) {
+  int rc;
+  bgmf_ctx* c = scratch_ctx(&rc);
+  if (!c) return rc;
+  double o[6];
+  rc = block_exact(c, rows, cols, vals, count, u, u_rows, v, v_rows, k, alpha, beta, 1, 0, tol,
+                   cap, o);
+  if (rc) { g_err = c->err; return rc; }
+  *sse_before = o[0]; *sse_after = o[1];
+  *iters_used = (int64_t)o[2]; *capped = (int32_t)o[3];
+  *bad_entry = (int64_t)o[4]; *bad_iter = (int64_t)o[5];
+  return BGMF_OK;
+}
+
+int bgmf_block_sse(const int64_t* rows, const int64_t* cols, const double* vals, int64_t count,
+                   const double* u, int64_t u_rows, const double* v, int64_t v_rows, int k,
+                   double* sse) {
+  int rc;
+  bgmf_ctx* c = scratch_ctx(&rc);
+  if (!c) return rc;
+  double o[6];
+  rc = block_exact(c, rows, cols, vals, count, const_cast<double*>(u), u_rows,
+                   const_cast<double*>(v), v_rows, k, 0.0, 0.0, 2, 0, 0.0, 0, o);
+  if (rc) { g_err = c->err; return rc; }
+  *sse = o[0];
+  return BGMF_OK;
+}
+
+namespace {
+
+// upload u, v (f64) and int32 copies of rows/cols; caller frees via cleanup
+struct EvalBufs {
+  double *u = nullptr, *v = nullptr, *vals = nullptr, *pred = nullptr;
+  int32_t *r = nullptr, *q = nullptr;
+  uint8_t* cold = nullptr;
+  ~EvalBufs() {
+    cudaFree(u); cudaFree(v); cudaFree(vals); cudaFree(pred); cudaFree(r); cudaFree(q);
+    cudaFree(cold);
+  }
+};
+
+int eval_upload(bgmf_ctx* c, EvalBufs& b, const double* u, int64_t n, const double* v, int64_t m,
+                int k, const int64_t* rows, const int64_t* cols, int64_t count) {
+  if (!u || !v || k < 1 || n < 1 || m < 1 || count < 0 || n >= INT32_MAX || m >= INT32_MAX)
+    return fail(c, BGMF_ERR_ARG, "bad model/dataset shapes");
+  const size_t N = (size_t)(count > 0 ? count : 1);
+  std::vector<int32_t> r(N), q(N);
+  for (int64_t i = 0; i < count; ++i) {
+    if (rows[i] < 0 || rows[i] >= n || cols[i] < 0 || cols[i] >= m)
+      return fail(c, BGMF_ERR_DATA, "index outside the model");
+    r[i] = (int32_t)rows[i];
+    q[i] = (int32_t)cols[i];
+  }
+  BGMF_CK(c, cudaMalloc(&b.u, (size_t)n * k * 8));
+  BGMF_CK(c, cudaMalloc(&b.v, (size_t)m * k * 8));
+  BGMF_CK(c, cudaMalloc(&b.r, N * 4));
+  BGMF_CK(c, cudaMalloc(&b.q, N * 4));
+  BGMF_CK(c, cudaMemcpyAsync(b.u, u, (size_t)n * k * 8, cudaMemcpyHostToDevice, c->stream));
+  BGMF_CK(c, cudaMemcpyAsync(b.v, v, (size_t)m * k * 8, cudaMemcpyHostToDevice, c->stream));
+  if (count > 0) {
+    BGMF_CK(c, cudaMemcpyAsync(b.r, r.data(), count * 4, cudaMemcpyHostToDevice, c->stream));
+    BGMF_CK(c, cudaMemcpyAsync(b.q, q.data(), count * 4, cudaMemcpyHostToDevice, c->stream));
+  }
+  BGMF_CK(c, cudaStreamSynchronize(c->stream));
+  return BGMF_OK;
+}
+
+}  // namespace
+
+int bgmf_predict(const double* u, int64_t n, const double* v, int64_t m, int k,
+                 const int64_t* rows, const int64_t* cols, int64_t count, double* out) {
+  int rc;
+  bgmf_ctx* c = scratch_ctx(&rc);
+  if (!c) return rc;
+  EvalBufs b;
+  rc = eval_upload(c, b, u, n, v, m, k, rows, cols, count);
+  if (rc) { g_err = c->err; return rc; }
+  if (count == 0) return BGMF_OK;
+  cudaError_t e = cudaMalloc(&b.pred, (size_t)count * 8);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMalloc");
+  rc = predict_f64(c, b.u, b.v, k, b.r, b.q, count, b.pred);
+  if (rc) { g_err = c->err; return rc; }
+  e = cudaMemcpyAsync(out, b.pred, (size_t)count * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "predict download");
+  return BGMF_OK;
+}
+
+int bgmf_sse(const double* u, int64_t n, const double* v, int64_t m, int k, const int64_t* rows,
+             const int64_t* cols, const double* vals, const uint8_t* cold, double fallback,
+             int64_t count, double* sse) {
+  int rc;
+  bgmf_ctx* c = scratch_ctx(&rc);
+  if (!c) return rc;
+  EvalBufs b;
+  rc = eval_upload(c, b, u, n, v, m, k, rows, cols, count);
+  if (rc) { g_err = c->err; return rc; }
+  if (count == 0) { *sse = 0.0; return BGMF_OK; }
+  const size_t N = (size_t)count;
+  cudaError_t e = cudaMalloc(&b.vals, N * 8);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(b.vals, vals, N * 8, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess && cold) {
+    e = cudaMalloc(&b.cold, N);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(b.cold, cold, N, cudaMemcpyHostToDevice, c->stream);
+  }
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "sse upload");
+  rc = eval_sse_f64(c, b.u, b.v, k, b.r, b.q, b.vals, b.cold, fallback, count, sse);
+  if (rc) { g_err = c->err; return rc; }
+  return BGMF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,377 @@
+// partition.cu -- GPU block partitioner, bit-exact with the reference
+// BlockedDataset (reference pkg/src/blockmf/partition.py:112-136).
+//
+// The reference computes block ids with searchsorted over balanced slab
+// bounds (partition.py:18-37,120-122) and orders entries with
+// np.lexsort((cols, rows, block_id)) -- (block, row, col), ties in input
+// order.  Here:
+//   1. make_keys: closed-form slab index (first n % P slabs are one longer),
+//      one 64-bit key per rating = block | local row | local col, payload =
+//      source index.  Within a block, (local row, local col) orders exactly
+//      like (row, col).
+//   2. LSD radix sort, 8-bit digits, stable (hist -> per-digit tile scan ->
+//      warp-ranked stable scatter with __match_any_sync), so duplicate cells
+//      keep input order like lexsort.
+//   3. decode: local coords from the key, fp64 value gathered by source index
+//      (fp32 copy for the fast kernels), block offsets by binary search.
+// HBM-bound integer work: every pass streams key+index (12 B/rating) in and
+// out; grid sized to tiles of 4096 ratings.
+
+#include "bgmf_internal.cuh"
+
+namespace bgmf {
+namespace {
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
+constexpr int RS_WARPS = RS_THREADS / 32;
+
+__device__ __forceinline__ int64_t slab_index(int64_t x, int64_t base, int64_t extra) {
+  const int64_t big = extra * (base + 1);
+  return x < big ? x / (base + 1) : extra + (x - big) / base;
+}
+__device__ __forceinline__ int64_t slab_start(int64_t s, int64_t base, int64_t extra) {
+  return s * base + (s < extra ? s : extra);
+}
+
+__global__ void make_keys(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols,
+                          int64_t nnz, int64_t n, int64_t m, int64_t rbase, int64_t rextra,
+                          int64_t cbase, int64_t cextra, int J, int rbits, int cbits,
+                          uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
+                          unsigned long long* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rows[i], c = cols[i];
+    idx[i] = (uint32_t)i;
+    if (r < 0 || r >= n || c < 0 || c >= m) {
+      atomicMin(bad, (unsigned long long)i);
+      keys[i] = 0;
+      continue;
+    }
+    const int64_t bi = slab_index(r, rbase, rextra);
+    const int64_t bj = slab_index(c, cbase, cextra);
+    const uint64_t lr = (uint64_t)(r - slab_start(bi, rbase, rextra));
+    const uint64_t lc = (uint64_t)(c - slab_start(bj, cbase, cextra));
+    keys[i] = ((uint64_t)(bi * J + bj) << (rbits + cbits)) | (lr << cbits) | lc;
+  }
+}
+
+// Per-tile digit histogram, written digit-major: hist[d * ntiles + tile].
+__global__ void __launch_bounds__(RS_THREADS)
+radix_hist(const uint64_t* __restrict__ keys, int64_t n, int shift, int64_t ntiles,
+           uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+#pragma unroll 4
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    const int64_t i = base + (int64_t)j * RS_THREADS + threadIdx.x;
+    const bool valid = i < n;
+    const unsigned vm = __ballot_sync(kFull, valid);
+    if (valid) {
+      const unsigned d = (unsigned)(keys[i] >> shift) & 0xFFu;
+      const unsigned peers = __match_any_sync(vm, d);
+      if (lane == __ffs(peers) - 1) atomicAdd(&h[d], (uint32_t)__popc(peers));
+    }
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// One CTA per digit: exclusive scan of hist[d * ntiles + 0 .. ntiles) in
+// place; digit total to totals[d].
+__global__ void __launch_bounds__(1024)
+radix_scan_tiles(uint32_t* __restrict__ hist, int64_t ntiles, uint32_t* __restrict__ totals) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t chunk_total;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* row = hist + (int64_t)blockIdx.x * ntiles;
+  uint32_t carry = 0;
+  for (int64_t t0 = 0; t0 < ntiles; t0 += 1024) {
+    const int64_t t = t0 + threadIdx.x;
+    const uint32_t x = t < ntiles ? row[t] : 0u;
+    uint32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t s = wsum[lane];
+      uint32_t si = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, si, o);
+        if (lane >= o) si += y;
+      }
+      wsum[lane] = si - s;
+      if (lane == 31) chunk_total = si;
+    }
+    __syncthreads();
+    if (t < ntiles) row[t] = carry + wsum[warp] + incl - x;
+    carry += chunk_total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+}
+
+// Stable scatter of one tile.  Warp w owns tile items [w*512, (w+1)*512),
+// walked 32 at a time in order; ranks within a round come from
+// __match_any_sync, across rounds/warps/tiles/digits from the prefix sums.
+__global__ void __launch_bounds__(RS_THREADS)
+radix_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+              uint64_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift,
+              const uint32_t* __restrict__ hist, int64_t ntiles,
+              const uint32_t* __restrict__ totals) {
+  __shared__ uint32_t woff[RS_WARPS][256];
+  __shared__ uint32_t wsum[RS_WARPS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
+
+  // digit base = exclusive scan of totals (256 threads, one digit each)
+  uint32_t dbase;
+  {
+    const uint32_t x = totals[tid];
+    uint32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    dbase = before + incl - x + hist[(int64_t)tid * ntiles + blockIdx.x];
+  }
+#pragma unroll
+  for (int w = 0; w < RS_WARPS; ++w) woff[w][tid] = 0;
+  __syncthreads();
+
+  const int64_t wbase = (int64_t)blockIdx.x * RS_TILE + (int64_t)warp * (32 * RS_ITEMS);
+  uint64_t key[RS_ITEMS];
+  uint32_t val[RS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    const int64_t i = wbase + j * 32 + lane;
+    key[j] = i < n ? kin[i] : 0ull;
+    val[j] = i < n ? vin[i] : 0u;
+  }
+  // count this warp's digits
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    const bool valid = wbase + j * 32 + lane < n;
+    const unsigned vm = __ballot_sync(kFull, valid);
+    if (valid) {
+      const unsigned d = (unsigned)(key[j] >> shift) & 0xFFu;
+      const unsigned peers = __match_any_sync(vm, d);
+      if (lane == __ffs(peers) - 1) woff[warp][d] += (uint32_t)__popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    uint32_t run = dbase;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) {
+      const uint32_t c = woff[w][tid];
+      woff[w][tid] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    const bool valid = wbase + j * 32 + lane < n;
+    const unsigned vm = __ballot_sync(kFull, valid);
+    unsigned d = 0, peers = 0;
+    if (valid) {
+      d = (unsigned)(key[j] >> shift) & 0xFFu;
+      peers = __match_any_sync(vm, d);
+      const uint32_t p = woff[warp][d] + (uint32_t)__popc(peers & lt);
+      kout[p] = key[j];
+      vout[p] = val[j];
+    }
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) woff[warp][d] += (uint32_t)__popc(peers);
+    __syncwarp();
+  }
+}
+
+__global__ void block_offsets(const uint64_t* __restrict__ keys, int64_t n, int nblocks,
+                              int shift, int64_t* __restrict__ off) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > nblocks) return;
+  if (b == nblocks) {
+    off[b] = n;
+    return;
+  }
+  const uint64_t target = (uint64_t)b << shift;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  off[b] = lo;
+}
+
+__global__ void decode(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                       const double* __restrict__ vin, int64_t n, int cbits, uint64_t rmask,
+                       uint64_t cmask, int32_t* __restrict__ lrow, int32_t* __restrict__ lcol,
+                       float* __restrict__ val, double* __restrict__ val64,
+                       uint32_t* __restrict__ order) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    const uint32_t o = idx[i];
+    lrow[i] = (int32_t)((k >> cbits) & rmask);
+    lcol[i] = (int32_t)(k & cmask);
+    order[i] = o;
+    const double x = vin[o];
+    val[i] = (float)x;
+    if (val64) val64[i] = x;
+  }
+}
+
+int bits_for(uint64_t maxval) {  // bits to represent 0..maxval
+  int b = 0;
+  while (b < 64 && (maxval >> b) != 0) ++b;
+  return b;
+}
+
+template <typename T>
+void free_dev(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+}  // namespace
+
+int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
+                     const double* vals, int64_t nnz, int64_t n, int64_t m, int I, int J) {
+  if (n < 1 || m < 1) return fail(ctx, BGMF_ERR_ARG, "n and m must be >= 1");
+  if (I < 1 || I > n) return fail(ctx, BGMF_ERR_ARG, "grid_i must be in [1, n]");
+  if (J < 1 || J > m) return fail(ctx, BGMF_ERR_ARG, "grid_j must be in [1, m]");
+  if (nnz < 0 || nnz >= (int64_t)0xFFFFFFFFll)
+    return fail(ctx, BGMF_ERR_ARG, "nnz must be in [0, 2^32-1)");
+  if ((int64_t)I * J > 65535) return fail(ctx, BGMF_ERR_ARG, "grid_i*grid_j must be <= 65535");
+  if (nnz > 0 && (!rows || !cols || !vals)) return fail(ctx, BGMF_ERR_ARG, "NULL input");
+
+  const int64_t rbase = n / I, rextra = n % I, cbase = m / J, cextra = m % J;
+  const int rbits = bits_for((uint64_t)(rbase + (rextra ? 1 : 0)) - 1);
+  const int cbits = bits_for((uint64_t)(cbase + (cextra ? 1 : 0)) - 1);
+  const int bbits = bits_for((uint64_t)I * J - 1);
+  if (rbits + cbits + bbits > 64) return fail(ctx, BGMF_ERR_ARG, "grid too large for 64-bit keys");
+  if (rbits > 31 || cbits > 31) return fail(ctx, BGMF_ERR_ARG, "block slab wider than 2^31");
+
+  // release any previous partition
+  free_dev(ctx->d_lrow); free_dev(ctx->d_lcol); free_dev(ctx->d_val);
+  free_dev(ctx->d_val64); free_dev(ctx->d_order);
+  ctx->partitioned = false;
+
+  cudaStream_t s = ctx->stream;
+  ctx->n = n; ctx->m = m; ctx->I = I; ctx->J = J; ctx->nnz = nnz;
+  ctx->row_bounds.assign(I + 1, 0);
+  ctx->col_bounds.assign(J + 1, 0);
+  for (int p = 0; p < I; ++p) ctx->row_bounds[p + 1] = ctx->row_bounds[p] + rbase + (p < rextra);
+  for (int p = 0; p < J; ++p) ctx->col_bounds[p + 1] = ctx->col_bounds[p] + cbase + (p < cextra);
+  const int nb = I * J;
+  ctx->h_offsets.assign(nb + 1, 0);
+
+  const size_t N = (size_t)(nnz > 0 ? nnz : 1);
+  int64_t *d_rows = nullptr, *d_cols = nullptr, *d_off = nullptr;
+  double* d_vin = nullptr;
+  uint64_t *ka = nullptr, *kb = nullptr;
+  uint32_t *ia = nullptr, *ib = nullptr, *hist = nullptr, *tot = nullptr;
+  unsigned long long* d_bad = nullptr;
+  int rc = BGMF_OK;
+  auto cleanup = [&]() {
+    free_dev(d_rows); free_dev(d_cols); free_dev(d_vin); free_dev(ka); free_dev(kb);
+    free_dev(ia); free_dev(ib); free_dev(hist); free_dev(tot); free_dev(d_bad); free_dev(d_off);
+  };
+#define PCK(call)                                           \
+  do {                                                      \
+    cudaError_t _e = (call);                                \
+    if (_e != cudaSuccess) { rc = cuda_fail(ctx, _e, #call); cleanup(); return rc; } \
+  } while (0)
+
+  PCK(cudaMalloc(&d_rows, N * 8));
+  PCK(cudaMalloc(&d_cols, N * 8));
+  PCK(cudaMalloc(&d_vin, N * 8));
+  PCK(cudaMalloc(&ka, N * 8));
+  PCK(cudaMalloc(&ia, N * 4));
+  PCK(cudaMalloc(&d_bad, 8));
+  PCK(cudaMalloc(&d_off, (nb + 1) * 8));
+  if (nnz > 0) {
+    PCK(cudaMemcpyAsync(d_rows, rows, nnz * 8, cudaMemcpyHostToDevice, s));
+    PCK(cudaMemcpyAsync(d_cols, cols, nnz * 8, cudaMemcpyHostToDevice, s));
+    PCK(cudaMemcpyAsync(d_vin, vals, nnz * 8, cudaMemcpyHostToDevice, s));
+  }
+  PCK(cudaMemsetAsync(d_bad, 0xFF, 8, s));
+  const int grid = ctx->num_sms * 8;
+  if (nnz > 0)
+    make_keys<<<grid, 256, 0, s>>>(d_rows, d_cols, nnz, n, m, rbase, rextra, cbase, cextra, J,
+                                   rbits, cbits, ka, ia, d_bad);
+  PCK(cudaGetLastError());
+  unsigned long long hbad = 0;
+  PCK(cudaMemcpyAsync(&hbad, d_bad, 8, cudaMemcpyDeviceToHost, s));
+  PCK(cudaStreamSynchronize(s));
+  if (hbad != ~0ull) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "entry %lld: index (%lld, %lld) outside %lldx%lld matrix",
+             (long long)hbad, (long long)rows[hbad], (long long)cols[hbad], (long long)n,
+             (long long)m);
+    cleanup();
+    return fail(ctx, BGMF_ERR_DATA, buf);
+  }
+  free_dev(d_rows);
+  free_dev(d_cols);
+
+  const int total_bits = rbits + cbits + bbits;
+  const int passes = (total_bits + 7) / 8;
+  const int64_t ntiles = (nnz + RS_TILE - 1) / RS_TILE;
+  if (passes > 0 && nnz > 1) {
+    PCK(cudaMalloc(&kb, N * 8));
+    PCK(cudaMalloc(&ib, N * 4));
+    PCK(cudaMalloc(&hist, (size_t)256 * ntiles * 4));
+    PCK(cudaMalloc(&tot, 256 * 4));
+    for (int p = 0; p < passes; ++p) {
+      const int shift = 8 * p;
+      radix_hist<<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, nnz, shift, ntiles, hist);
+      radix_scan_tiles<<<256, 1024, 0, s>>>(hist, ntiles, tot);
+      radix_scatter<<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, ia, kb, ib, nnz, shift, hist,
+                                                            ntiles, tot);
+      PCK(cudaGetLastError());
+      uint64_t* tk = ka; ka = kb; kb = tk;
+      uint32_t* ti = ia; ia = ib; ib = ti;
+    }
+    free_dev(kb); free_dev(ib); free_dev(hist); free_dev(tot);
+  }
+
+  PCK(cudaMalloc(&ctx->d_lrow, N * 4));
+  PCK(cudaMalloc(&ctx->d_lcol, N * 4));
+  PCK(cudaMalloc(&ctx->d_val, N * 4));
+  PCK(cudaMalloc(&ctx->d_order, N * 4));
+  if (ctx->exact) PCK(cudaMalloc(&ctx->d_val64, N * 8));
+  if (nnz > 0) {
+    decode<<<grid, 256, 0, s>>>(ka, ia, d_vin, nnz, cbits, (1ull << rbits) - 1,
+                                (1ull << cbits) - 1, ctx->d_lrow, ctx->d_lcol, ctx->d_val,
+                                ctx->d_val64, ctx->d_order);
+  }
+  block_offsets<<<(nb + 1 + 255) / 256, 256, 0, s>>>(ka, nnz, nb, rbits + cbits, d_off);
+  PCK(cudaGetLastError());
+  PCK(cudaMemcpyAsync(ctx->h_offsets.data(), d_off, (nb + 1) * 8, cudaMemcpyDeviceToHost, s));
+  PCK(cudaStreamSynchronize(s));
+  cleanup();
+#undef PCK
+  ctx->partitioned = true;
+  return BGMF_OK;
+}
+
+}  // namespace bgmf

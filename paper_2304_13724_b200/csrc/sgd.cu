@@ -1,0 +1,830 @@
+// sgd.cu -- per-stratum SGD kernels (reference pkg/src/blockmf/_kernels.py).
+//
+// Fast path (default, fp32):  a "group" of L lanes owns one rating at a time;
+// each lane holds V4 float4 of the (padded) latent vector, so kp = 4*L*V4.
+// The blocks of one batch (a stratum of plan_step, scheduler.py:45-75) are
+// cut into contiguous row-major chunks, one chunk per group:
+//   * rating triples are read coalesced, L at a time, and broadcast with shfl;
+//   * u_r stays in registers for the whole run of ratings of user r (entries
+//     are sorted row-major, partition.py:124), so within a chunk the U updates
+//     are exactly sequential; the run is written back with a plain store, or
+//     -- when the run crosses a chunk boundary -- with red.add of its delta;
+//   * v_c is read with 128-bit loads and its delta alpha*(2e*u - beta*v) is
+//     applied with red.global.add.v4.f32 (lossless: no update is ever lost,
+//     reads may be stale by the few concurrent groups on the same block);
+//   * the dot product is a butterfly xor-shuffle over the L lanes;
+//   * factor rows are read with ld.global.cg (L2, never a stale L1 line):
+//     V is L2-resident (C4: 9.1 MB of 126 MB) and the reds resolve in L2.
+// Update rule per entry (_kernels.py:44-55): e = x - u.v;
+//   u <- u + a(2e v - b u);  v <- v + a(2e u_old - b v)  (both pre-update).
+// The post-sweep SSE of every block (_kernels.py:56, consumed by the trace,
+// trainer.py:149-158) is a second kernel over the same chunks.
+//
+// Exact path (fp64, opt-in): one thread walks a whole block sequentially
+// with explicitly rounded __dmul_rn/__dsub_rn/__dadd_rn in the reference's
+// operation order -- bit-identical to numba's fastmath=False loops.  Blocks of
+// a batch are independent, so the batch is still parallel across blocks.
+
+#include <cmath>
+
+#include "bgmf_internal.cuh"
+
+namespace bgmf {
+namespace {
+
+__device__ __forceinline__ void red_add_v4(float* p, float4 d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(d.x), "f"(d.y),
+               "f"(d.z), "f"(d.w)
+               : "memory");
+}
+
+__device__ __forceinline__ int find_work(const BlockWork* __restrict__ work, int nwork, int c) {
+  int lo = 0, hi = nwork - 1;  // last w with first_chunk <= c
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (work[mid].first_chunk <= c) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int L>
+__device__ __forceinline__ float group_sum(float x) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+  return x;
+}
+
+// Chunk geometry shared by the sweep and SSE kernels.
+struct Chunk {
+  int64_t begin, end, bbeg, bend;
+  int64_t row_start, col_start;
+  int block_id, pos;
+};
+
+__device__ __forceinline__ Chunk locate_chunk(const BlockWork* __restrict__ work, int nwork,
+                                              int total_chunks, int chunk) {
+  Chunk ch{0, 0, 0, 0, 0, 0, 0, 0};
+  if (chunk < total_chunks) {
+    const int w = find_work(work, nwork, chunk);
+    const BlockWork bw = work[w];
+    ch.begin = bw.begin + (int64_t)(chunk - bw.first_chunk) * bw.chunk_len;
+    ch.end = min(ch.begin + (int64_t)bw.chunk_len, bw.end);
+    ch.bbeg = bw.begin;
+    ch.bend = bw.end;
+    ch.row_start = bw.row_start;
+    ch.col_start = bw.col_start;
+    ch.block_id = bw.block_id;
+    ch.pos = bw.pos;
+  }
+  return ch;
+}
+
+template <int L, int V4>
+__global__ void __launch_bounds__(256)
+sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
+                const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
+                const float* __restrict__ val, float* __restrict__ U, float* __restrict__ V,
+                int kp, float alpha, float beta, int iter, unsigned long long* __restrict__ bad) {
+  constexpr int GPW = 32 / L;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (L - 1);
+  const int gbase = lane & ~(L - 1);
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int chunk = warp * GPW + lane / L;
+  const Chunk ch = locate_chunk(work, nwork, total_chunks, chunk);
+  const int len = (int)(ch.end - ch.begin);
+  const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
+  if (maxlen == 0) return;
+
+  float* Ub = U + ch.row_start * kp;
+  float* Vb = V + ch.col_start * kp;
+  // runs that continue into a neighbouring chunk are shared with another group
+  int first_row = -1, last_row = -1;
+  if (len > 0) {
+    const int fr = lrow[ch.begin], lr = lrow[ch.end - 1];
+    if (ch.begin > ch.bbeg && lrow[ch.begin - 1] == fr) first_row = fr;
+    if (ch.end < ch.bend && lrow[ch.end] == lr) last_row = lr;
+  }
+
+  float4 u[V4], u0[V4];
+  int cur = -1;
+  bool shared = false, dead = false;
+  const float two_a = 2.0f * alpha, ab = alpha * beta;
+
+  for (int t0 = 0; t0 < maxlen; t0 += L) {
+    int r_l = 0, c_l = 0;
+    float x_l = 0.f;
+    if (t0 + gl < len) {
+      const int64_t i = ch.begin + t0 + gl;
+      r_l = __ldg(lrow + i);
+      c_l = __ldg(lcol + i);
+      x_l = __ldg(val + i);
+    }
+#pragma unroll 2
+    for (int j = 0; j < L; ++j) {
+      const int r = __shfl_sync(kFull, r_l, gbase + j);
+      const int c = __shfl_sync(kFull, c_l, gbase + j);
+      const float x = __shfl_sync(kFull, x_l, gbase + j);
+      const bool valid = (t0 + j < len) && !dead;
+      if (valid && r != cur) {
+        if (cur >= 0) {
+          float* p = Ub + (int64_t)cur * kp;
+#pragma unroll
+          for (int q = 0; q < V4; ++q) {
+            float* pq = p + 4 * (q * L + gl);
+            if (shared)
+              red_add_v4(pq, make_float4(u[q].x - u0[q].x, u[q].y - u0[q].y, u[q].z - u0[q].z,
+                                         u[q].w - u0[q].w));
+            else
+              *reinterpret_cast<float4*>(pq) = u[q];
+          }
+        }
+        const float* p = Ub + (int64_t)r * kp;
+#pragma unroll
+        for (int q = 0; q < V4; ++q) {
+          u[q] = __ldcg(reinterpret_cast<const float4*>(p + 4 * (q * L + gl)));
+          u0[q] = u[q];
+        }
+        cur = r;
+        shared = (r == first_row) || (r == last_row);
+      }
+      float4 v[V4];
+      float dot = 0.f;
+      float* vp = Vb + (int64_t)c * kp;
+      if (valid) {
+#pragma unroll
+        for (int q = 0; q < V4; ++q) {
+          v[q] = __ldcg(reinterpret_cast<const float4*>(vp + 4 * (q * L + gl)));
+          dot = fmaf(u[q].x, v[q].x, dot);
+          dot = fmaf(u[q].y, v[q].y, dot);
+          dot = fmaf(u[q].z, v[q].z, dot);
+          dot = fmaf(u[q].w, v[q].w, dot);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < V4; ++q) v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      dot = group_sum<L>(dot);
+      const float e = x - dot;
+      if (valid) {
+        if (!isfinite(e)) {
+          if (gl == 0) atomicMin(bad, pack_bad(ch.pos, iter, ch.begin + t0 + j - ch.bbeg));
+          dead = true;
+        } else {
+          const float g = two_a * e;
+#pragma unroll
+          for (int q = 0; q < V4; ++q) {
+            float4 dv;
+            dv.x = g * u[q].x - ab * v[q].x;
+            dv.y = g * u[q].y - ab * v[q].y;
+            dv.z = g * u[q].z - ab * v[q].z;
+            dv.w = g * u[q].w - ab * v[q].w;
+            u[q].x += g * v[q].x - ab * u[q].x;
+            u[q].y += g * v[q].y - ab * u[q].y;
+            u[q].z += g * v[q].z - ab * u[q].z;
+            u[q].w += g * v[q].w - ab * u[q].w;
+            red_add_v4(vp + 4 * (q * L + gl), dv);
+          }
+        }
+      }
+    }
+  }
+  if (cur >= 0) {
+    float* p = Ub + (int64_t)cur * kp;
+#pragma unroll
+    for (int q = 0; q < V4; ++q) {
+      float* pq = p + 4 * (q * L + gl);
+      if (shared)
+        red_add_v4(pq, make_float4(u[q].x - u0[q].x, u[q].y - u0[q].y, u[q].z - u0[q].z,
+                                   u[q].w - u0[q].w));
+      else
+        *reinterpret_cast<float4*>(pq) = u[q];
+    }
+  }
+}
+
+// Post-sweep SSE of each block: sum over the chunk of (x - u.v)^2 in fp64,
+// one atomicAdd per group into sse[block_id].
+template <int L, int V4>
+__global__ void __launch_bounds__(256)
+sse_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
+                const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
+                const float* __restrict__ val, const float* __restrict__ U,
+                const float* __restrict__ V, int kp, double* __restrict__ sse) {
+  constexpr int GPW = 32 / L;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (L - 1);
+  const int gbase = lane & ~(L - 1);
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int chunk = warp * GPW + lane / L;
+  const Chunk ch = locate_chunk(work, nwork, total_chunks, chunk);
+  const int len = (int)(ch.end - ch.begin);
+  const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
+  if (maxlen == 0) return;
+  const float* Ub = U + ch.row_start * kp;
+  const float* Vb = V + ch.col_start * kp;
+  float4 u[V4];
+  int cur = -1;
+  double acc = 0.0;
+  for (int t0 = 0; t0 < maxlen; t0 += L) {
+    int r_l = 0, c_l = 0;
+    float x_l = 0.f;
+    if (t0 + gl < len) {
+      const int64_t i = ch.begin + t0 + gl;
+      r_l = __ldg(lrow + i);
+      c_l = __ldg(lcol + i);
+      x_l = __ldg(val + i);
+    }
+#pragma unroll 2
+    for (int j = 0; j < L; ++j) {
+      const int r = __shfl_sync(kFull, r_l, gbase + j);
+      const int c = __shfl_sync(kFull, c_l, gbase + j);
+      const float x = __shfl_sync(kFull, x_l, gbase + j);
+      const bool valid = t0 + j < len;
+      if (valid && r != cur) {
+        const float* p = Ub + (int64_t)r * kp;
+#pragma unroll
+        for (int q = 0; q < V4; ++q) u[q] = __ldg(reinterpret_cast<const float4*>(p + 4 * (q * L + gl)));
+        cur = r;
+      }
+      float dot = 0.f;
+      if (valid) {
+        const float* vp = Vb + (int64_t)c * kp;
+#pragma unroll
+        for (int q = 0; q < V4; ++q) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(vp + 4 * (q * L + gl)));
+          dot = fmaf(u[q].x, v.x, dot);
+          dot = fmaf(u[q].y, v.y, dot);
+          dot = fmaf(u[q].z, v.z, dot);
+          dot = fmaf(u[q].w, v.w, dot);
+        }
+      }
+      dot = group_sum<L>(dot);
+      if (valid) {
+        const double e = (double)x - (double)dot;
+        acc += e * e;
+      }
+    }
+  }
+  if (gl == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
+}
+
+// ---------------------------------------------------------------- exact
+// Sequential fp64 sweep of one block in the reference's operation order.
+// Returns the first non-finite entry index or -1 (_kernels.py:43-55).
+__device__ int64_t sweep_exact(const int32_t* rows, const int32_t* cols, const double* vals,
+                               int64_t count, double* u, double* v, int k, double alpha,
+                               double beta) {
+  for (int64_t i = 0; i < count; ++i) {
+    double* ur = u + (int64_t)rows[i] * k;
+    double* vc = v + (int64_t)cols[i] * k;
+    double e = vals[i];
+    for (int g = 0; g < k; ++g) e = __dsub_rn(e, __dmul_rn(ur[g], vc[g]));
+    if (!isfinite(e)) return i;
+    const double e2 = __dmul_rn(2.0, e);
+    for (int g = 0; g < k; ++g) {
+      const double ug = ur[g], vg = vc[g];
+      ur[g] = __dadd_rn(ug, __dmul_rn(alpha, __dsub_rn(__dmul_rn(e2, vg), __dmul_rn(beta, ug))));
+      vc[g] = __dadd_rn(vg, __dmul_rn(alpha, __dsub_rn(__dmul_rn(e2, ug), __dmul_rn(beta, vg))));
+    }
+  }
+  return -1;
+}
+
+__device__ double sse_exact(const int32_t* rows, const int32_t* cols, const double* vals,
+                            int64_t count, const double* u, const double* v, int k) {
+  double s = 0.0;
+  for (int64_t i = 0; i < count; ++i) {
+    const double* ur = u + (int64_t)rows[i] * k;
+    const double* vc = v + (int64_t)cols[i] * k;
+    double e = vals[i];
+    for (int g = 0; g < k; ++g) e = __dsub_rn(e, __dmul_rn(ur[g], vc[g]));
+    s = __dadd_rn(s, __dmul_rn(e, e));
+  }
+  return s;
+}
+
+// mode 0: sweeps (sgd_sweeps), mode 1: converge (sgd_converge).
+// out[8*w + 0..5] = sse_before, sse_after, iters_used, capped, bad_entry, bad_iter
+__global__ void block_exact_kernel(const BlockWork* __restrict__ work, int nwork,
+                                   const int32_t* __restrict__ lrow,
+                                   const int32_t* __restrict__ lcol,
+                                   const double* __restrict__ val, double* U, double* V, int k,
+                                   double alpha, double beta, int mode, int iters, double tol,
+                                   int64_t cap, int want_before, double* __restrict__ out) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nwork) return;
+  const BlockWork bw = work[w];
+  const int32_t* rows = lrow + bw.begin;
+  const int32_t* cols = lcol + bw.begin;
+  const double* vals = val + bw.begin;
+  const int64_t count = bw.end - bw.begin;
+  double* u = U + bw.row_start * k;
+  double* v = V + bw.col_start * k;
+  double* o = out + 8 * w;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  const bool before = want_before || mode == 1;
+  const double sb = before ? sse_exact(rows, cols, vals, count, u, v, k) : 0.0;
+  o[0] = sb; o[3] = 0.0; o[4] = -1.0; o[5] = -1.0;
+  if (mode == 0) {
+    for (int it = 0; it < iters; ++it) {
+      const int64_t b = sweep_exact(rows, cols, vals, count, u, v, k, alpha, beta);
+      if (b >= 0) { o[1] = nan; o[2] = iters; o[4] = (double)b; o[5] = it; return; }
+    }
+    const double sa = sse_exact(rows, cols, vals, count, u, v, k);
+    o[2] = iters;
+    if (!isfinite(sa)) { o[1] = nan; o[4] = (double)(count - 1); o[5] = iters - 1; return; }
+    o[1] = sa;
+    return;
+  }
+  // converge (_kernels.py:62-100)
+  if (count == 0) { o[0] = 0.0; o[1] = 0.0; o[2] = 0.0; return; }
+  double prev = sqrt(sb / (double)count);
+  double s = sb;
+  int64_t it = 0;
+  while (it < cap) {
+    const int64_t b = sweep_exact(rows, cols, vals, count, u, v, k, alpha, beta);
+    if (b >= 0) { o[1] = nan; o[2] = (double)(it + 1); o[4] = (double)b; o[5] = (double)it; return; }
+    ++it;
+    s = sse_exact(rows, cols, vals, count, u, v, k);
+    if (!isfinite(s)) {
+      o[1] = nan; o[2] = (double)it; o[4] = (double)(count - 1); o[5] = (double)(it - 1);
+      return;
+    }
+    const double now = sqrt(s / (double)count);
+    if (prev - now < tol) { o[1] = s; o[2] = (double)it; return; }
+    prev = now;
+  }
+  o[1] = s; o[2] = (double)it; o[3] = 1.0;
+}
+
+// ------------------------------------------------------------ dispatch
+struct Shape {
+  int L, V4;
+};
+
+Shape shape_for(int kp) {
+  // smallest power-of-two group with V4 = 1 up to 32 lanes, then V4 > 1
+  const int f4 = kp / 4;  // float4 per row
+  if (f4 <= 32) {
+    int L = 1;
+    while (L < f4) L <<= 1;
+    return {L, 1};
+  }
+  if (f4 <= 64) return {32, 2};
+  if (f4 <= 128) return {32, 4};
+  return {32, 8};
+}
+
+template <int L, int V4>
+void launch_pair(bool sweep, dim3 grid, cudaStream_t s, const BlockWork* w, int nwork, int total,
+                 bgmf_ctx* c, float a, float b, int it) {
+  if (sweep)
+    sgd_fast_kernel<L, V4><<<grid, 256, 0, s>>>(w, nwork, total, c->d_lrow, c->d_lcol, c->d_val,
+                                                c->d_u, c->d_v, c->kp, a, b, it, c->d_bad);
+  else
+    sse_fast_kernel<L, V4><<<grid, 256, 0, s>>>(w, nwork, total, c->d_lrow, c->d_lcol, c->d_val,
+                                                c->d_u, c->d_v, c->kp, c->d_sse);
+}
+
+void launch_fast(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, const BlockWork* w,
+                 int nwork, int total, bgmf_ctx* c, float a, float b, int it) {
+#define BGMF_CASE(LL, VV)                                          \
+  if (sh.L == LL && sh.V4 == VV) {                                 \
+    launch_pair<LL, VV>(sweep, grid, s, w, nwork, total, c, a, b, it); \
+    return;                                                        \
+  }
+  BGMF_CASE(1, 1) BGMF_CASE(2, 1) BGMF_CASE(4, 1) BGMF_CASE(8, 1) BGMF_CASE(16, 1)
+  BGMF_CASE(32, 1) BGMF_CASE(32, 2) BGMF_CASE(32, 4) BGMF_CASE(32, 8)
+#undef BGMF_CASE
+}
+
+template <int L, int V4>
+int occupancy_warps(bgmf_ctx*) {
+  int blocks = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, sgd_fast_kernel<L, V4>, 256, 0);
+  return blocks * 8;
+}
+
+int resident_warps(bgmf_ctx* c, const Shape& sh) {
+  if (c->warps_per_sm > 0) return c->warps_per_sm;
+#define BGMF_OCC(LL, VV) if (sh.L == LL && sh.V4 == VV) return occupancy_warps<LL, VV>(c);
+  BGMF_OCC(1, 1) BGMF_OCC(2, 1) BGMF_OCC(4, 1) BGMF_OCC(8, 1) BGMF_OCC(16, 1)
+  BGMF_OCC(32, 1) BGMF_OCC(32, 2) BGMF_OCC(32, 4) BGMF_OCC(32, 8)
+#undef BGMF_OCC
+  return 32;
+}
+
+// Fill h_work for every batch; returns per-batch (work offset, total chunks).
+struct BatchRange {
+  int w0, nw, chunks;
+};
+
+int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
+               int64_t chunk_len_base, std::vector<BatchRange>& ranges,
+               const std::vector<char>* active = nullptr) {
+  const int total = batch_off[nbatch];
+  int rc = ensure_step_scratch(c, (size_t)total);
+  if (rc) return rc;
+  ranges.assign(nbatch, BatchRange{0, 0, 0});
+  int w = 0;
+  for (int t = 0; t < nbatch; ++t) {
+    ranges[t].w0 = w;
+    int chunks = 0;
+    for (int q = batch_off[t]; q < batch_off[t + 1]; ++q) {
+      const int b = plan[q];
+      if (b < 0 || b >= c->I * c->J) return fail(c, BGMF_ERR_ARG, "plan block id out of range");
+      if (active && !(*active)[q]) continue;
+      const int64_t beg = c->h_offsets[b], end = c->h_offsets[b + 1];
+      const int64_t cnt = end - beg;
+      if (cnt == 0) continue;
+      int64_t cl = chunk_len_base;
+      if (cl < c->min_chunk) cl = c->min_chunk;
+      if (cl > cnt) cl = cnt;
+      if (cl > (1 << 30)) cl = 1 << 30;
+      BlockWork& bw = c->h_work[w++];
+      bw.begin = beg;
+      bw.end = end;
+      bw.row_start = c->row_bounds[b / c->J];
+      bw.col_start = c->col_bounds[b % c->J];
+      bw.chunk_len = (int32_t)cl;
+      bw.first_chunk = chunks;
+      bw.block_id = b;
+      bw.pos = q;
+      chunks += (int)((cnt + cl - 1) / cl);
+    }
+    ranges[t].nw = w - ranges[t].w0;
+    ranges[t].chunks = chunks;
+  }
+  return BGMF_OK;
+}
+
+int64_t base_chunk_len(bgmf_ctx* c, const Shape& sh, int nbatch) {
+  const int64_t groups = (int64_t)c->num_sms * resident_warps(c, sh) * (32 / sh.L);
+  const int64_t per_batch = nbatch > 0 ? (c->nnz + nbatch - 1) / nbatch : c->nnz;
+  int64_t cl = groups > 0 ? (per_batch + groups - 1) / groups : per_batch;
+  return cl < 1 ? 1 : cl;
+}
+
+}  // namespace
+
+int ensure_step_scratch(bgmf_ctx* c, size_t nwork) {
+  const int nb = c->I * c->J;
+  if (!c->d_sse) {
+    BGMF_CK(c, cudaMalloc(&c->d_sse, sizeof(double) * (nb > 0 ? nb : 1)));
+    BGMF_CK(c, cudaMallocHost(&c->h_sse, sizeof(double) * (nb > 0 ? nb : 1)));
+    BGMF_CK(c, cudaMalloc(&c->d_bad, 8));
+    BGMF_CK(c, cudaMallocHost(&c->h_bad, 8));
+  }
+  if (nwork > c->work_cap) {
+    if (c->d_work) cudaFree(c->d_work);
+    if (c->h_work) cudaFreeHost(c->h_work);
+    c->d_work = nullptr;
+    c->h_work = nullptr;
+    size_t cap = nwork < 64 ? 64 : nwork;
+    BGMF_CK(c, cudaMalloc(&c->d_work, sizeof(BlockWork) * cap * 8));  // 8x: exact out slots
+    BGMF_CK(c, cudaMallocHost(&c->h_work, sizeof(BlockWork) * cap));
+    c->work_cap = cap;
+  }
+  return BGMF_OK;
+}
+
+int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
+                  int iters, float alpha, float beta) {
+  cudaStream_t s = c->stream;
+  const Shape sh = shape_for(c->kp);
+  std::vector<BatchRange> ranges;
+  int rc = build_work(c, plan, batch_off, nbatch, base_chunk_len(c, sh, nbatch), ranges);
+  if (rc) return rc;
+  const int nw = ranges.empty() ? 0 : ranges.back().w0 + ranges.back().nw;
+  const int nb = c->I * c->J;
+  if (nw > 0)
+    BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * nw,
+                               cudaMemcpyHostToDevice, s));
+  BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, s));
+  BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+  const int gpw = 32 / sh.L;
+  for (int t = 0; t < nbatch; ++t) {
+    const BatchRange& r = ranges[t];
+    if (r.chunks == 0) continue;
+    const int warps = (r.chunks + gpw - 1) / gpw;
+    const dim3 grid((warps + 7) / 8);
+    const BlockWork* w = c->d_work + r.w0;
+    double ratings = 0;
+    for (int q = 0; q < r.nw; ++q) ratings += (double)(c->h_work[r.w0 + q].end - c->h_work[r.w0 + q].begin);
+    for (int it = 0; it < iters; ++it) {
+      TimedLaunch* slot = nullptr;
+      if (c->timing) record_begin(c, 0, ratings * (12.0 + 16.0 * c->k), &slot);
+      launch_fast(true, sh, grid, s, w, r.nw, r.chunks, c, alpha, beta, it);
+      if (slot) record_end(c, slot);
+    }
+    TimedLaunch* slot = nullptr;
+    if (c->timing) record_begin(c, 1, 0.0, &slot);
+    launch_fast(false, sh, grid, s, w, r.nw, r.chunks, c, alpha, beta, 0);
+    if (slot) record_end(c, slot);
+  }
+  BGMF_CK(c, cudaGetLastError());
+  BGMF_CK(c, cudaMemcpyAsync(c->h_sse, c->d_sse, sizeof(double) * nb, cudaMemcpyDeviceToHost, s));
+  BGMF_CK(c, cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, s));
+  BGMF_CK(c, cudaStreamSynchronize(s));
+  if (c->timing) harvest_timing(c);
+  return BGMF_OK;
+}
+
+int run_step_exact(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
+                   int iters, double alpha, double beta) {
+  cudaStream_t s = c->stream;
+  std::vector<BatchRange> ranges;
+  int rc = build_work(c, plan, batch_off, nbatch, INT32_MAX, ranges);
+  if (rc) return rc;
+  const int nw = ranges.empty() ? 0 : ranges.back().w0 + ranges.back().nw;
+  const int nb = c->I * c->J;
+  double* d_out = reinterpret_cast<double*>(c->d_work + c->work_cap);  // scratch after work
+  if (nw > 0)
+    BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * nw,
+                               cudaMemcpyHostToDevice, s));
+  for (int t = 0; t < nbatch; ++t) {
+    const BatchRange& r = ranges[t];
+    if (r.nw == 0) continue;
+    block_exact_kernel<<<(r.nw + 31) / 32, 32, 0, s>>>(
+        c->d_work + r.w0, r.nw, c->d_lrow, c->d_lcol, c->d_val64, c->d_u64, c->d_v64, c->k,
+        alpha, beta, 0, iters, 0.0, 0, 0, d_out + 8 * r.w0);
+  }
+  BGMF_CK(c, cudaGetLastError());
+  std::vector<double> out((size_t)8 * (nw > 0 ? nw : 1));
+  if (nw > 0)
+    BGMF_CK(c, cudaMemcpyAsync(out.data(), d_out, sizeof(double) * 8 * nw,
+                               cudaMemcpyDeviceToHost, s));
+  BGMF_CK(c, cudaStreamSynchronize(s));
+  for (int b = 0; b < nb; ++b) c->h_sse[b] = 0.0;
+  unsigned long long best = kNoBad;
+  for (int q = 0; q < nw; ++q) {
+    const BlockWork& bw = c->h_work[q];
+    const double* o = &out[8 * q];
+    c->h_sse[bw.block_id] = o[1];
+    if (o[4] >= 0) {
+      const unsigned long long key = pack_bad(bw.pos, (int64_t)o[5], (int64_t)o[4]);
+      if (key < best) best = key;
+    }
+  }
+  *c->h_bad = best;
+  return BGMF_OK;
+}
+
+int run_step_converge_exact(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off,
+                            int nbatch, double tol, int64_t cap, double alpha, double beta,
+                            int64_t* iters_out, int32_t* capped_out) {
+  cudaStream_t s = c->stream;
+  std::vector<BatchRange> ranges;
+  int rc = build_work(c, plan, batch_off, nbatch, INT32_MAX, ranges);
+  if (rc) return rc;
+  const int nw = ranges.empty() ? 0 : ranges.back().w0 + ranges.back().nw;
+  const int nb = c->I * c->J;
+  double* d_out = reinterpret_cast<double*>(c->d_work + c->work_cap);
+  if (nw > 0)
+    BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * nw,
+                               cudaMemcpyHostToDevice, s));
+  for (int t = 0; t < nbatch; ++t) {
+    const BatchRange& r = ranges[t];
+    if (r.nw == 0) continue;
+    block_exact_kernel<<<(r.nw + 31) / 32, 32, 0, s>>>(
+        c->d_work + r.w0, r.nw, c->d_lrow, c->d_lcol, c->d_val64, c->d_u64, c->d_v64, c->k,
+        alpha, beta, 1, 0, tol, cap, 1, d_out + 8 * r.w0);
+  }
+  BGMF_CK(c, cudaGetLastError());
+  std::vector<double> out((size_t)8 * (nw > 0 ? nw : 1));
+  if (nw > 0)
+    BGMF_CK(c, cudaMemcpyAsync(out.data(), d_out, sizeof(double) * 8 * nw,
+                               cudaMemcpyDeviceToHost, s));
+  BGMF_CK(c, cudaStreamSynchronize(s));
+  for (int b = 0; b < nb; ++b) { c->h_sse[b] = 0.0; iters_out[b] = 0; capped_out[b] = 0; }
+  unsigned long long best = kNoBad;
+  for (int q = 0; q < nw; ++q) {
+    const BlockWork& bw = c->h_work[q];
+    const double* o = &out[8 * q];
+    c->h_sse[bw.block_id] = o[1];
+    iters_out[bw.block_id] = (int64_t)o[2];
+    capped_out[bw.block_id] = (int32_t)o[3];
+    if (o[4] >= 0) {
+      const unsigned long long key = pack_bad(bw.pos, (int64_t)o[5], (int64_t)o[4]);
+      if (key < best) best = key;
+    }
+  }
+  *c->h_bad = best;
+  return BGMF_OK;
+}
+
+// Fast converge mode: per batch, sweep the still-active blocks, measure each
+// block's post-sweep SSE, deactivate blocks whose RMSE improvement < tol.
+int run_step_converge_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off,
+                           int nbatch, double tol, int64_t cap, double alpha, double beta,
+                           int64_t* iters_out, int32_t* capped_out) {
+  cudaStream_t s = c->stream;
+  const Shape sh = shape_for(c->kp);
+  const int nb = c->I * c->J;
+  const int64_t cl = base_chunk_len(c, sh, nbatch);
+  std::vector<double> sse_final(nb, 0.0);
+  for (int b = 0; b < nb; ++b) { iters_out[b] = 0; capped_out[b] = 0; }
+  unsigned long long best = kNoBad;
+  BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+  const int gpw = 32 / sh.L;
+  for (int t = 0; t < nbatch; ++t) {
+    const int q0 = batch_off[t], q1 = batch_off[t + 1];
+    std::vector<char> active(batch_off[nbatch], 0);
+    std::vector<double> prev(nb, 0.0);
+    int n_active = 0;
+    for (int q = q0; q < q1; ++q) {
+      const int b = plan[q];
+      if (c->h_offsets[b + 1] > c->h_offsets[b]) { active[q] = 1; ++n_active; }
+    }
+    // sse_before of the active blocks
+    auto measure = [&](std::vector<double>& out) -> int {
+      std::vector<BatchRange> rg;
+      int rc = build_work(c, plan + 0, batch_off, nbatch, cl, rg, &active);
+      if (rc) return rc;
+      const BatchRange& r = rg[t];
+      BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, s));
+      if (r.chunks > 0) {
+        BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work + r.w0, sizeof(BlockWork) * r.nw,
+                                   cudaMemcpyHostToDevice, s));
+        const int warps = (r.chunks + gpw - 1) / gpw;
+        launch_fast(false, sh, dim3((warps + 7) / 8), s, c->d_work, r.nw, r.chunks, c,
+                    (float)alpha, (float)beta, 0);
+      }
+      BGMF_CK(c, cudaMemcpyAsync(c->h_sse, c->d_sse, sizeof(double) * nb,
+                                 cudaMemcpyDeviceToHost, s));
+      BGMF_CK(c, cudaStreamSynchronize(s));
+      for (int b = 0; b < nb; ++b) out[b] = c->h_sse[b];
+      return BGMF_OK;
+    };
+    std::vector<double> cur(nb, 0.0);
+    int rc = measure(cur);
+    if (rc) return rc;
+    for (int q = q0; q < q1; ++q) {
+      const int b = plan[q];
+      const double cnt = (double)(c->h_offsets[b + 1] - c->h_offsets[b]);
+      if (active[q]) prev[b] = std::sqrt(cur[b] / cnt);
+    }
+    int64_t it = 0;
+    while (n_active > 0 && it < cap) {
+      std::vector<BatchRange> rg;
+      rc = build_work(c, plan, batch_off, nbatch, cl, rg, &active);
+      if (rc) return rc;
+      const BatchRange& r = rg[t];
+      if (r.chunks > 0) {
+        BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work + r.w0, sizeof(BlockWork) * r.nw,
+                                   cudaMemcpyHostToDevice, s));
+        const int warps = (r.chunks + gpw - 1) / gpw;
+        launch_fast(true, sh, dim3((warps + 7) / 8), s, c->d_work, r.nw, r.chunks, c,
+                    (float)alpha, (float)beta, (int)(it & 0xFFFF));
+      }
+      BGMF_CK(c, cudaGetLastError());
+      ++it;
+      rc = measure(cur);
+      if (rc) return rc;
+      BGMF_CK(c, cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, s));
+      BGMF_CK(c, cudaStreamSynchronize(s));
+      for (int q = q0; q < q1; ++q) {
+        if (!active[q]) continue;
+        const int b = plan[q];
+        const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
+        iters_out[b] = it;
+        sse_final[b] = cur[b];
+        const double now = std::sqrt(cur[b] / (double)cnt);
+        if (!std::isfinite(cur[b])) {
+          const unsigned long long key = pack_bad(q, it - 1, cnt - 1);
+          if (key < best) best = key;
+          active[q] = 0; --n_active;
+        } else if (prev[b] - now < tol) {
+          active[q] = 0; --n_active;
+        } else {
+          prev[b] = now;
+        }
+      }
+      if (*c->h_bad != kNoBad) break;
+    }
+    for (int q = q0; q < q1; ++q)
+      if (active[q]) capped_out[plan[q]] = 1;
+    if (*c->h_bad != kNoBad) break;
+  }
+  for (int b = 0; b < nb; ++b) c->h_sse[b] = sse_final[b];
+  if (*c->h_bad < best) best = *c->h_bad;
+  *c->h_bad = best;
+  return BGMF_OK;
+}
+
+int train_sse_fast(bgmf_ctx* c, double* out) {
+  const int nb = c->I * c->J;
+  std::vector<int32_t> plan(nb), off{0, nb};
+  for (int b = 0; b < nb; ++b) plan[b] = b;
+  const Shape sh = shape_for(c->kp);
+  std::vector<BatchRange> ranges;
+  int rc = build_work(c, plan.data(), off.data(), 1, base_chunk_len(c, sh, 1), ranges);
+  if (rc) return rc;
+  cudaStream_t s = c->stream;
+  BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, s));
+  const BatchRange& r = ranges[0];
+  if (r.chunks > 0) {
+    BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * r.nw,
+                               cudaMemcpyHostToDevice, s));
+    const int gpw = 32 / sh.L;
+    const int warps = (r.chunks + gpw - 1) / gpw;
+    launch_fast(false, sh, dim3((warps + 7) / 8), s, c->d_work, r.nw, r.chunks, c, 0.f, 0.f, 0);
+  }
+  BGMF_CK(c, cudaGetLastError());
+  BGMF_CK(c, cudaMemcpyAsync(c->h_sse, c->d_sse, sizeof(double) * nb, cudaMemcpyDeviceToHost, s));
+  BGMF_CK(c, cudaStreamSynchronize(s));
+  double acc = 0.0;
+  for (int b = 0; b < nb; ++b) acc += c->h_sse[b];
+  *out = acc;
+  return BGMF_OK;
+}
+
+int train_sse_exact(bgmf_ctx* c, double* out) {
+  const int nb = c->I * c->J;
+  std::vector<int32_t> plan(nb), off{0, nb};
+  for (int b = 0; b < nb; ++b) plan[b] = b;
+  std::vector<BatchRange> ranges;
+  int rc = build_work(c, plan.data(), off.data(), 1, INT32_MAX, ranges);
+  if (rc) return rc;
+  cudaStream_t s = c->stream;
+  const int nw = ranges[0].nw;
+  double* d_out = reinterpret_cast<double*>(c->d_work + c->work_cap);
+  double acc = 0.0;
+  if (nw > 0) {
+    BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * nw,
+                               cudaMemcpyHostToDevice, s));
+    // iters = 0 sweeps: o[1] = post-"sweep" SSE of the untouched block
+    block_exact_kernel<<<(nw + 31) / 32, 32, 0, s>>>(c->d_work, nw, c->d_lrow, c->d_lcol,
+                                                     c->d_val64, c->d_u64, c->d_v64, c->k, 0.0,
+                                                     0.0, 0, 0, 0.0, 0, 0, d_out);
+    BGMF_CK(c, cudaGetLastError());
+    std::vector<double> o((size_t)8 * nw);
+    BGMF_CK(c, cudaMemcpyAsync(o.data(), d_out, sizeof(double) * 8 * nw, cudaMemcpyDeviceToHost, s));
+    BGMF_CK(c, cudaStreamSynchronize(s));
+    for (int q = 0; q < nw; ++q) acc += o[8 * q + 1];
+  }
+  *out = acc;
+  return BGMF_OK;
+}
+
+int block_exact(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const double* vals,
+                int64_t count, double* u, int64_t u_rows, double* v, int64_t v_rows, int k,
+                double alpha, double beta, int mode, int iters, double tol, int64_t cap,
+                double* out6) {
+  if (k < 1 || count < 0 || u_rows < 0 || v_rows < 0)
+    return fail(c, BGMF_ERR_ARG, "bad block shape");
+  for (int64_t i = 0; i < count; ++i) {
+    if (rows[i] < 0 || rows[i] >= u_rows || cols[i] < 0 || cols[i] >= v_rows)
+      return fail(c, BGMF_ERR_ARG, "block entry index outside its factor slice");
+  }
+  cudaStream_t s = c->stream;
+  const size_t N = (size_t)(count > 0 ? count : 1);
+  std::vector<int32_t> r32(N), c32(N);
+  for (int64_t i = 0; i < count; ++i) { r32[i] = (int32_t)rows[i]; c32[i] = (int32_t)cols[i]; }
+  int32_t *dr = nullptr, *dc = nullptr;
+  double *dv = nullptr, *du = nullptr, *dV = nullptr, *dout = nullptr;
+  BlockWork* dw = nullptr;
+  int rc = BGMF_OK;
+  auto cleanup = [&]() {
+    cudaFree(dr); cudaFree(dc); cudaFree(dv); cudaFree(du); cudaFree(dV); cudaFree(dout);
+    cudaFree(dw);
+  };
+#define XCK(call)                                                                       \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess) { rc = cuda_fail(c, _e, #call); cleanup(); return rc; }      \
+  } while (0)
+  XCK(cudaMalloc(&dr, N * 4));
+  XCK(cudaMalloc(&dc, N * 4));
+  XCK(cudaMalloc(&dv, N * 8));
+  XCK(cudaMalloc(&du, (size_t)(u_rows > 0 ? u_rows : 1) * k * 8));
+  XCK(cudaMalloc(&dV, (size_t)(v_rows > 0 ? v_rows : 1) * k * 8));
+  XCK(cudaMalloc(&dout, 8 * 8));
+  XCK(cudaMalloc(&dw, sizeof(BlockWork)));
+  BlockWork w{0, count, 0, 0, 0, 0, 0, 0};
+  XCK(cudaMemcpyAsync(dw, &w, sizeof w, cudaMemcpyHostToDevice, s));
+  if (count > 0) {
+    XCK(cudaMemcpyAsync(dr, r32.data(), count * 4, cudaMemcpyHostToDevice, s));
+    XCK(cudaMemcpyAsync(dc, c32.data(), count * 4, cudaMemcpyHostToDevice, s));
+    XCK(cudaMemcpyAsync(dv, vals, count * 8, cudaMemcpyHostToDevice, s));
+  }
+  if (u_rows > 0) XCK(cudaMemcpyAsync(du, u, (size_t)u_rows * k * 8, cudaMemcpyHostToDevice, s));
+  if (v_rows > 0) XCK(cudaMemcpyAsync(dV, v, (size_t)v_rows * k * 8, cudaMemcpyHostToDevice, s));
+  block_exact_kernel<<<1, 32, 0, s>>>(dw, 1, dr, dc, dv, du, dV, k, alpha, beta,
+                                      mode == 1 ? 1 : 0, iters, tol, cap, 1, dout);
+  XCK(cudaGetLastError());
+  double o[8];
+  XCK(cudaMemcpyAsync(o, dout, 8 * 8, cudaMemcpyDeviceToHost, s));
+  if (mode != 2) {  // mode 2: block_sse, factors untouched
+    if (u_rows > 0) XCK(cudaMemcpyAsync(u, du, (size_t)u_rows * k * 8, cudaMemcpyDeviceToHost, s));
+    if (v_rows > 0) XCK(cudaMemcpyAsync(v, dV, (size_t)v_rows * k * 8, cudaMemcpyDeviceToHost, s));
+  }
+  XCK(cudaStreamSynchronize(s));
+#undef XCK
+  for (int i = 0; i < 6; ++i) out6[i] = o[i];
+  cleanup();
+  return BGMF_OK;
+}
+
+}  // namespace bgmf

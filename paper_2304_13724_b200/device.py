@@ -1,0 +1,189 @@
+"""Engine: one libbgmf device context (partition + factors + step scratch).
+
+This is the host-side owner of everything that lives in HBM for one GPU:
+
+* the partitioned ratings, SoA ``int32 lrow | int32 lcol | fp32 value``
+  (12 B/rating), blocks contiguous in row-major block order, entries of a
+  block row-major (the reference's BlockedDataset order);
+* U (n x kp) and V (m x kp) fp32, rows padded to kp = ceil(k/4)*4 so every
+  row is a whole number of 16-byte vectors (exact mode: fp64, kp = k);
+* the per-block SSE array and the divergence word of the current step.
+
+Numbers only ever come back through :meth:`run_step` (P^2 doubles) and the
+explicit download calls.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+
+@dataclass(frozen=True)
+class EngineOptions:
+    """B200 knobs.  None of them changes the reference's semantics.
+
+    exact      fp64 sequential-per-block kernels, bit-identical to the
+               reference (slow; parity/verification mode).
+    min_chunk  minimum ratings per worker group (bounds concurrency on tiny
+               blocks, which keeps the lossless-Hogwild drift far below 1e-3).
+    device     CUDA ordinal; default $BGMF_DEVICE, else $LOCAL_RANK, else 0.
+    timing     record CUDA events around every kernel launch.
+    """
+
+    exact: bool = False
+    min_chunk: int = 48
+    device: int | None = None
+    timing: bool = False
+    warps_per_sm: int = 0
+
+
+def default_device() -> int:
+    for var in ("BGMF_DEVICE", "LOCAL_RANK"):
+        v = os.environ.get(var)
+        if v:
+            return int(v)
+    return 0
+
+
+class Engine:
+    def __init__(self, options: EngineOptions | None = None, *, stream: int | None = None):
+        self.options = options or EngineOptions()
+        self._L = N.load()
+        dev = self.options.device if self.options.device is not None else default_device()
+        h = ctypes.c_void_p()
+        N.check(self._L.bgmf_create(dev, ctypes.c_void_p(stream or 0), ctypes.byref(h)))
+        self._h = h
+        self.device = dev
+        self._opt("exact", 1.0 if self.options.exact else 0.0)
+        self._opt("min_chunk", float(self.options.min_chunk))
+        self._opt("timing", 1.0 if self.options.timing else 0.0)
+        self._opt("warps_per_sm", float(self.options.warps_per_sm))
+        self.n = self.m = self.nnz = 0
+        self.I = self.J = 0
+        self.k = 0
+        self.offsets: np.ndarray | None = None
+
+    # ------------------------------------------------------------ plumbing
+    def _opt(self, key: str, value: float):
+        N.check(self._L.bgmf_set_option(self._h, key.encode(), value), self._h)
+
+    def _check(self, rc: int, **kw):
+        N.check(rc, self._h, **kw)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._L.bgmf_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_timing(self, on: bool):
+        self._opt("timing", 1.0 if on else 0.0)
+
+    # ------------------------------------------------------------ partition
+    def partition(self, rows, cols, values, n: int, m: int, grid_i: int, grid_j: int,
+                  data_error=None):
+        rows, cols, values = N.i64(rows), N.i64(cols), N.f64(values)
+        self._check(self._L.bgmf_partition(
+            self._h, N.ptr(rows, N._i64p), N.ptr(cols, N._i64p), N.ptr(values, N._f64p),
+            len(rows), n, m, grid_i, grid_j), data_error=data_error)
+        self.n, self.m, self.nnz, self.I, self.J = n, m, len(rows), grid_i, grid_j
+        off = np.zeros(grid_i * grid_j + 1, np.int64)
+        self._check(self._L.bgmf_partition_export(self._h, N.ptr(off, N._i64p), None, None, None))
+        self.offsets = off
+
+    def export_partition(self):
+        """(offsets, order, local rows, local cols) as int64 host arrays."""
+        nnz = self.nnz
+        off = np.zeros(self.I * self.J + 1, np.int64)
+        order = np.empty(nnz, np.int64)
+        lr = np.empty(nnz, np.int32)
+        lc = np.empty(nnz, np.int32)
+        self._check(self._L.bgmf_partition_export(
+            self._h, N.ptr(off, N._i64p), N.ptr(order, N._i64p), N.ptr(lr, N._i32p),
+            N.ptr(lc, N._i32p)))
+        return off, order, lr.astype(np.int64), lc.astype(np.int64)
+
+    # ------------------------------------------------------------ factors
+    def set_factors(self, u: np.ndarray, v: np.ndarray):
+        u, v = N.f64(u), N.f64(v)
+        self._check(self._L.bgmf_set_factors(self._h, N.ptr(u, N._f64p), N.ptr(v, N._f64p),
+                                             u.shape[0], v.shape[0], u.shape[1]))
+        self.k = u.shape[1]
+
+    def bind_factors(self, u_ptr: int, v_ptr: int, n: int, m: int, k: int, kp: int):
+        self._check(self._L.bgmf_bind_factors(self._h, ctypes.c_void_p(u_ptr),
+                                              ctypes.c_void_p(v_ptr), n, m, k, kp))
+        self.k = k
+
+    def get_factors(self):
+        u = np.empty((self.n, self.k), np.float64)
+        v = np.empty((self.m, self.k), np.float64)
+        self._check(self._L.bgmf_get_factors(self._h, N.ptr(u, N._f64p), N.ptr(v, N._f64p)))
+        return u, v
+
+    # ------------------------------------------------------------ steps
+    def plan_arrays(self, batches):
+        """Plan batches of (bi, bj) -> (flat block ids, batch offsets)."""
+        J = self.J
+        ids = np.array([bi * J + bj for b in batches for bi, bj in b], np.int32)
+        off = np.zeros(len(batches) + 1, np.int32)
+        off[1:] = np.cumsum([len(b) for b in batches])
+        return ids, off
+
+    def run_step(self, ids: np.ndarray, off: np.ndarray, iters: int, alpha: float, beta: float):
+        """Returns (sse[I*J], bad) where bad = (plan_pos, entry, iteration) or None."""
+        sse = np.zeros(self.I * self.J, np.float64)
+        bad = np.zeros(3, np.int64)
+        self._check(self._L.bgmf_run_step(self._h, N.ptr(ids, N._i32p), N.ptr(off, N._i32p),
+                                          len(off) - 1, int(iters), float(alpha), float(beta),
+                                          N.ptr(sse, N._f64p), N.ptr(bad, N._i64p)))
+        return sse, (None if bad[0] < 0 else tuple(int(x) for x in bad))
+
+    def run_step_converge(self, ids, off, tol: float, cap: int, alpha: float, beta: float):
+        nb = self.I * self.J
+        sse = np.zeros(nb, np.float64)
+        iters = np.zeros(nb, np.int64)
+        capped = np.zeros(nb, np.int32)
+        bad = np.zeros(3, np.int64)
+        self._check(self._L.bgmf_run_step_converge(
+            self._h, N.ptr(ids, N._i32p), N.ptr(off, N._i32p), len(off) - 1, float(tol),
+            int(cap), float(alpha), float(beta), N.ptr(sse, N._f64p), N.ptr(iters, N._i64p),
+            N.ptr(capped, N._i32p), N.ptr(bad, N._i64p)))
+        return sse, iters, capped, (None if bad[0] < 0 else tuple(int(x) for x in bad))
+
+    def train_sse(self) -> float:
+        out = ctypes.c_double()
+        self._check(self._L.bgmf_train_sse(self._h, ctypes.byref(out)))
+        return out.value
+
+    # ------------------------------------------------------------ holdout
+    def holdout_set(self, rows, cols, values, cold: np.ndarray, fallback: float):
+        rows, cols, values = N.i64(rows), N.i64(cols), N.f64(values)
+        cold = np.ascontiguousarray(cold, np.uint8)
+        self._check(self._L.bgmf_holdout_set(self._h, N.ptr(rows, N._i64p), N.ptr(cols, N._i64p),
+                                             N.ptr(values, N._f64p), N.ptr(cold, N._u8p),
+                                             len(rows), float(fallback)))
+        self._hcount = len(rows)
+
+    def holdout_sse(self) -> float:
+        out = ctypes.c_double()
+        self._check(self._L.bgmf_holdout_sse(self._h, ctypes.byref(out)))
+        return out.value
+
+    # ------------------------------------------------------------ timing
+    def kernel_stats(self, reset: bool = False) -> dict:
+        out = np.zeros(5, np.float64)
+        self._check(self._L.bgmf_kernel_stats(self._h, N.ptr(out, N._f64p), 1 if reset else 0))
+        return dict(sgd_ms=out[0], sse_ms=out[1], sgd_launches=int(out[2]),
+                    sse_launches=int(out[3]), sgd_alg_bytes=out[4])

@@ -1,0 +1,218 @@
+"""End-to-end training on the GPU against the reference.
+
+* exact mode (fp64 sequential-per-block kernels): bit-identical traces and
+  factors to the reference golden runs;
+* fast mode (fp32 lossless warp-per-rating kernels, the throughput path):
+  per-epoch train/test RMSE within 1e-3 absolute of the reference/oracle
+  (BASELINE.md tolerance), on C1 (golden) and C2/C3 (oracle, same inputs).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2304_13724_b200 as bm
+from helpers import config_of, sha, trace_inputs
+from oracle import oracle as O
+from paper_2304_13724_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3  # absolute, per epoch (BASELINE.md "RMSE parity")
+EXACT = bm.EngineOptions(exact=True)
+
+TRACES = ["dense64_const1", "dense64_const3", "dense64_dec4", "dense64_inc", "dense64_adaptive",
+          "dense64_converge", "dense64_early", "dense64_wide_2x5", "dense64_tall_5x2",
+          "dense64_holdout", "c1_k30", "c1_k10", "c1_split"]
+
+
+@pytest.mark.parametrize("name", TRACES)
+def test_exact_mode_bit_identical(golden, name):
+    meta = golden["traces"][name]
+    d, te = trace_inputs(name)
+    res = bm.train_blocked(d, config_of(meta), te, early_stop=meta["early_stop"], timing=False,
+                           options=EXACT)
+    assert [s.train_rmse for s in res.trace] == meta["train"]
+    assert [s.inner_iters for s in res.trace] == meta["inner"]
+    assert [s.capped_blocks for s in res.trace] == meta["capped"]
+    assert res.stop_reason == meta["stop"]
+    assert sha(res.model.u) == meta["u_sha"] and sha(res.model.v) == meta["v_sha"]
+    if meta["test"][0] is not None:  # GPU reduction order vs numpy pairwise sum
+        for a, b in zip([s.test_rmse for s in res.trace], meta["test"]):
+            assert a == pytest.approx(b, rel=1e-12)
+    assert bm.rmse(res.model, d) == pytest.approx(meta["final_rmse"], rel=1e-12)
+
+
+@pytest.mark.parametrize("name", TRACES)
+def test_fast_mode_within_tolerance(golden, name):
+    meta = golden["traces"][name]
+    d, te = trace_inputs(name)
+    res = bm.train_blocked(d, config_of(meta), te, early_stop=meta["early_stop"], timing=False)
+    got = [s.train_rmse for s in res.trace]
+    assert len(got) == len(meta["train"])
+    assert np.max(np.abs(np.array(got) - np.array(meta["train"]))) <= TOL
+    if meta["test"][0] is not None:
+        got_t = np.array([s.test_rmse for s in res.trace])
+        assert np.max(np.abs(got_t - np.array(meta["test"]))) <= TOL
+    assert abs(bm.rmse(res.model, d) - meta["final_rmse"]) <= TOL
+    if not name.endswith("converge"):
+        assert [s.inner_iters for s in res.trace] == meta["inner"]
+
+
+def test_c1_parity_per_epoch_detail(golden):
+    """C1 (north-star parity config): 20 epochs, k=30, 4x4 -- report the drift."""
+    meta = golden["traces"]["c1_k30"]
+    d, _ = trace_inputs("c1_k30")
+    res = bm.train_blocked(d, config_of(meta), early_stop=False, timing=False)
+    drift = np.abs(np.array([s.train_rmse for s in res.trace]) - np.array(meta["train"]))
+    print("C1 max |d train_rmse| over 20 epochs:", drift.max())
+    assert drift.max() <= TOL
+    assert np.all(np.diff([s.train_rmse for s in res.trace]) < 0)
+
+
+def _oracle_vs_gpu(name, epochs, nnz=None, k=None, grid=None):
+    w = workloads.CONFIGS[name]
+    k = k or w.k
+    grid = grid or w.grid
+    r, c, v = workloads.lowrank(w.n, w.m, nnz or w.nnz, seed=0)
+    d = bm.RatingsDataset(w.n, w.m, r, c, v)
+    tr, te = bm.split(d, 0.2, seed=0)
+    cfg = bm.TrainConfig(k=k, alpha=w.alpha, beta=w.beta, outer_steps=epochs, grid_i=grid,
+                         grid_j=grid, seed=0)
+    res = bm.train_blocked(tr, cfg, te, early_stop=False, timing=False)
+    _, _, otr, _ = O.train_blocked(tr.n, tr.m, tr.rows, tr.cols, tr.values, k=k, alpha=w.alpha,
+                                   beta=w.beta, outer_steps=epochs, grid_i=grid, grid_j=grid,
+                                   seed=0, test=(te.rows, te.cols, te.values), early_stop=False,
+                                   nthreads=8)
+    dtr = np.abs(np.array([s.train_rmse for s in res.trace]) - [s["train_rmse"] for s in otr])
+    dte = np.abs(np.array([s.test_rmse for s in res.trace]) - [s["test_rmse"] for s in otr])
+    print(f"{name}: max |d train| {dtr.max():.3e}  max |d test| {dte.max():.3e}")
+    return dtr, dte
+
+
+def test_c2_parity_vs_oracle():
+    dtr, dte = _oracle_vs_gpu("C2", epochs=10)
+    assert dtr.max() <= TOL and dte.max() <= TOL
+
+
+@pytest.mark.slow
+def test_c3_parity_vs_oracle():
+    dtr, dte = _oracle_vs_gpu("C3", epochs=3)
+    assert dtr.max() <= TOL and dte.max() <= TOL
+
+
+class TestReferenceTrainerBehaviour:
+    def cfg64(self, **kw):
+        base = dict(k=10, alpha=1e-4, beta=1e-2, delta=1e-2, seed=0, outer_steps=10,
+                    inner_schedule=bm.Constant(1), grid_i=4, grid_j=4)
+        base.update(kw)
+        return bm.TrainConfig(**base)
+
+    def test_early_stop_and_budget(self, dense64):
+        r = bm.train_blocked(dense64, self.cfg64(delta=10.0, outer_steps=50))
+        assert r.stop_reason == "converged" and len(r.trace) == 2
+        r = bm.train_blocked(dense64, self.cfg64(outer_steps=7), early_stop=False)
+        assert r.stop_reason == "max_steps" and [s.step for s in r.trace] == list(range(1, 8))
+
+    def test_empty_dataset(self):
+        r = bm.train_blocked(bm.RatingsDataset.from_triples(4, 4, []), self.cfg64(grid_i=2,
+                                                                                 grid_j=2))
+        assert r.stop_reason == "converged" and len(r.trace) == 1
+        assert r.trace.last().train_rmse == 0.0
+
+    def test_holdout_only_when_given(self, dense64):
+        tr, te = bm.split(dense64, 0.2, seed=1)
+        a = bm.train_blocked(tr, self.cfg64(outer_steps=2), te, early_stop=False)
+        b = bm.train_blocked(tr, self.cfg64(outer_steps=2), early_stop=False)
+        assert all(s.test_rmse is not None for s in a.trace)
+        assert all(s.test_rmse is None for s in b.trace)
+
+    def test_hooks_and_slice_exclusivity(self, dense64):
+        events, active, violations = [], {}, []
+
+        def hook(phase, task):
+            events.append((phase, task.bi, task.bj))
+            if phase == "start":
+                for bi, bj in active.values():
+                    if bi == task.bi or bj == task.bj:
+                        violations.append(((bi, bj), (task.bi, task.bj)))
+                active[id(task)] = (task.bi, task.bj)
+            else:
+                active.pop(id(task), None)
+
+        bm.train_blocked(dense64, self.cfg64(outer_steps=2), early_stop=False, block_hook=hook)
+        starts = [(bi, bj) for p, bi, bj in events if p == "start"]
+        assert len(starts) == 32 and set(starts) == {(i, j) for i in range(4) for j in range(4)}
+        assert violations == []
+
+    def test_divergence(self, dense64):
+        with pytest.raises(bm.DivergenceError) as info:
+            bm.train_blocked(dense64, self.cfg64(alpha=10.0), early_stop=False)
+        err = info.value
+        assert err.step == 1 and err.block is not None
+        assert isinstance(err.partial_trace, bm.ConvergenceTrace)
+        assert "reduce alpha" in str(err)
+
+    def test_more_inner_iterations_hurt_at_equal_budget(self, dense256):
+        finals = {}
+        for g in (1, 8):
+            cfg = self.cfg64(grid_i=8, grid_j=8, outer_steps=400 // g,
+                             inner_schedule=bm.Constant(g))
+            finals[g] = bm.rmse(bm.train_blocked(dense256, cfg, early_stop=False).model, dense256)
+        assert finals[1] < finals[8]
+
+    def test_fast_repeat_runs_close(self, dense64):
+        a = bm.train_blocked(dense64, self.cfg64(), early_stop=False)
+        b = bm.train_blocked(dense64, self.cfg64(), early_stop=False)
+        da = np.abs(np.array([s.train_rmse for s in a.trace]) - [s.train_rmse for s in b.trace])
+        assert da.max() <= 1e-5
+
+    def test_exact_repeat_runs_bit_identical(self, dense64):
+        a = bm.train_blocked(dense64, self.cfg64(), early_stop=False, options=EXACT)
+        b = bm.train_blocked(dense64, self.cfg64(), early_stop=False, options=EXACT)
+        assert a.model == b.model
+
+
+def test_metrics_on_gpu(dense32):
+    model = bm.FactorModel(np.array([[1.0], [2.0]]), np.array([[1.0], [2.0]]))
+    d = bm.RatingsDataset.from_triples(2, 2, [(0, 0, 4.0), (1, 1, 8.0)])
+    assert bm.rmse(model, d) == pytest.approx(3.5355339059327378, rel=1e-15)
+    assert bm.rmse(bm.FactorModel(np.array([[2.0]]), np.array([[3.0]])),
+                   bm.RatingsDataset.from_triples(1, 1, [(0, 0, 6.0)])) == 0.0
+    with pytest.raises(bm.DataError, match="empty"):
+        bm.rmse(bm.init_factors(2, 2, 1, 0), bm.RatingsDataset.from_triples(2, 2, []))
+    with pytest.raises(bm.DataError, match="3x3"):
+        bm.rmse(bm.init_factors(3, 3, 1, 0), bm.RatingsDataset.from_triples(2, 2, [(0, 0, 1.0)]))
+    train = bm.RatingsDataset.from_triples(3, 3, [(0, 0, 2.0), (1, 1, 4.0)])
+    ev = bm.HoldoutEvaluator(train, bm.RatingsDataset.from_triples(3, 3, [(2, 2, 3.0)]))
+    assert ev.cold_entries == 1 and ev.fallback == 3.0
+    assert ev.rmse(bm.init_factors(3, 3, 2, seed=0)) == 0.0
+    m = bm.init_factors(32, 32, 4, seed=1)
+    ref = O.rmse(m.u, m.v, dense32.rows, dense32.cols, dense32.values)
+    assert bm.rmse(m, dense32) == pytest.approx(ref, rel=1e-13)
+    pred = m.predict(dense32.rows, dense32.cols)
+    assert np.allclose(pred, np.einsum("ij,ij->i", m.u[dense32.rows], m.v[dense32.cols]),
+                       rtol=1e-14, atol=0)
+    tr, te = bm.split(dense32, 0.25, seed=3)
+    assert bm.test_rmse(m, tr, te) == bm.HoldoutEvaluator(tr, te).rmse(m)
+    with pytest.raises(ValueError, match="share global dimensions"):
+        bm.HoldoutEvaluator(dense32, bm.RatingsDataset.from_triples(8, 8, [(0, 0, 1.0)]))
+    with pytest.raises(bm.DataError, match="non-empty"):
+        bm.HoldoutEvaluator(dense32, bm.RatingsDataset.from_triples(32, 32, []))
+
+
+@pytest.mark.slow
+def test_c4_one_epoch_properties():
+    """C4 at full size (100M ratings, k=128, 16x16): one epoch through the
+    public API; size-independent checks (finite, monotone descent, trace ==
+    recomputed per-block SSE merge)."""
+    w = workloads.CONFIGS["C4"]
+    r, c, v = workloads.lowrank(w.n, w.m, w.nnz, seed=0)
+    d = bm.RatingsDataset(w.n, w.m, r, c, v)
+    blocked = bm.partition(d, 16, 16)
+    cfg = bm.TrainConfig(k=128, outer_steps=2, grid_i=16, grid_j=16)
+    res = bm.train_blocked(d, cfg, early_stop=False, blocked=blocked)
+    tr = [s.train_rmse for s in res.trace]
+    assert all(math.isfinite(x) for x in tr) and tr[1] < tr[0]
+    assert np.all(np.isfinite(res.model.u)) and np.all(np.isfinite(res.model.v))
