@@ -218,7 +218,8 @@ def run_ours(args):
     # ---- device-resident epochs
     stream = torch.cuda.current_stream()
     # the engine launches on torch's current stream so torch events bracket the work
-    eng2 = bm.Engine(bm.EngineOptions(device=dev), stream=stream.cuda_stream)
+    eng2 = bm.Engine(bm.EngineOptions(device=dev, fused=not args.unfused),
+                     stream=stream.cuda_stream)
     eng2.partition(d.rows, d.cols, d.values, w.n, w.m, w.grid, w.grid)
     m0 = bm.init_factors(w.n, w.m, w.k, w.seed)
     eng2.set_factors(m0.u, m0.v)
@@ -279,7 +280,8 @@ def run_ours(args):
                         "init upload, K epochs, D2H model"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": None, "peak_kind": hbm_kind,
-                     "kernel": "sgd_fast_kernel<32,1>",
+                     "kernel": ("sgd_fast_kernel<32,1>" if args.unfused else
+                                "epoch_fast_kernel<32,1> (sweeps + SSE, fused)"),
                      "alg_bytes_per_launch": alg_per_launch, "avg_launch_ms": sgd_launch_ms,
                      "sgd_share_of_step": st["sgd_ms"] / total_ms,
                      "sse_ms_per_step": st["sse_ms"] / args.steps},
@@ -301,6 +303,8 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--nnz", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--unfused", action="store_true",
+                    help="one launch per stratum sweep / SSE pass (default: one per epoch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-batches", type=int, default=None,
                     help="strata per CPU sample (default: the whole epoch)")

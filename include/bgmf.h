@@ -50,9 +50,12 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      the reference (_kernels.py fastmath=False order);
  *                      0 = fp32 warp-per-rating lossless kernels (default).
  *   "min_chunk"  int   minimum ratings per worker group in fast mode
- *                      (bounds per-block concurrency on small blocks; 48).
+ *                      (bounds per-block concurrency on small blocks; 256).
  *   "timing"     0/1   record CUDA events around every kernel launch.
- *   "warps_per_sm" int resident-warp target used to size chunks (0 = occupancy). */
+ *   "warps_per_sm" int resident-warp target used to size chunks (0 = occupancy).
+ *   "fused"      0/1   1 = one cooperative launch per outer step (all strata,
+ *                      sweeps and SSE passes separated by grid barriers;
+ *                      default); 0 = one launch per stratum sweep / SSE pass. */
 int bgmf_set_option(bgmf_ctx* ctx, const char* key, double value);
 
 /* Bucket the ratings into the I x J block grid on the GPU.

@@ -52,9 +52,10 @@ struct bgmf_ctx {
 
   // options
   bool exact = false;
-  int min_chunk = 48;
+  int min_chunk = 256;
   bool timing = false;
   int warps_per_sm = 0;
+  bool fused = true;   // one cooperative launch per outer step
 
   // grid + partition
   int64_t n = 0, m = 0, nnz = 0;

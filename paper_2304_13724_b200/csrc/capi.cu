@@ -235,6 +235,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "min_chunk")) c->min_chunk = value < 1 ? 1 : (int)value;
   else if (!strcmp(key, "timing")) c->timing = value != 0.0;
   else if (!strcmp(key, "warps_per_sm")) c->warps_per_sm = value < 0 ? 0 : (int)value;
+  else if (!strcmp(key, "fused")) c->fused = value != 0.0;
   else return fail(c, BGMF_ERR_ARG, std::string("unknown option ") + key);
   return BGMF_OK;
 }
@@ -287,6 +288,7 @@ int bgmf_set_factors(bgmf_ctx* c, const double* u, const double* v, int64_t n, i
     return BGMF_OK;
   }
   const int kp = (k + 3) / 4 * 4;
+  if (kp > 512) return fail(c, BGMF_ERR_ARG, "fast mode supports k <= 512 (use exact mode)");
   if (!(c->bound && c->k == k)) {
     free_factors(c);
     c->k = k; c->kp = kp;
@@ -303,7 +305,8 @@ int bgmf_set_factors(bgmf_ctx* c, const double* u, const double* v, int64_t n, i
 int bgmf_bind_factors(bgmf_ctx* c, void* u_dev, void* v_dev, int64_t n, int64_t m, int k, int kp) {
   if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
   if (c->exact) return fail(c, BGMF_ERR_STATE, "bind_factors is fast-mode only");
-  if (!u_dev || !v_dev || k < 1 || kp < k || kp % 4) return fail(c, BGMF_ERR_ARG, "bad bind");
+  if (!u_dev || !v_dev || k < 1 || kp < k || kp % 4 || kp > 512)
+    return fail(c, BGMF_ERR_ARG, "bad bind (need k <= kp <= 512, kp % 4 == 0)");
   if (((uintptr_t)u_dev | (uintptr_t)v_dev) & 15) return fail(c, BGMF_ERR_ARG, "unaligned factors");
   if (c->partitioned && (n != c->n || m != c->m))
     return fail(c, BGMF_ERR_ARG, "factor shapes do not match the partitioned dataset");

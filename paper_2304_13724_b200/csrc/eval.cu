@@ -51,6 +51,7 @@ eval_f32_kernel(const int32_t* __restrict__ rows, const int32_t* __restrict__ co
       const float* vp = V + (int64_t)cols[i] * kp;
 #pragma unroll
       for (int q = 0; q < V4; ++q) {
+        if (4 * (q * L + gl) >= kp) continue;  // lane past the padded row
         const float4 a = __ldg(reinterpret_cast<const float4*>(up + 4 * (q * L + gl)));
         const float4 b = __ldg(reinterpret_cast<const float4*>(vp + 4 * (q * L + gl)));
         dot = fmaf(a.x, b.x, dot);

@@ -25,12 +25,16 @@
 // operation order -- bit-identical to numba's fastmath=False loops.  Blocks of
 // a batch are independent, so the batch is still parallel across blocks.
 
+#include <cooperative_groups.h>
+
 #include <cmath>
 
 #include "bgmf_internal.cuh"
 
 namespace bgmf {
 namespace {
+
+namespace cg = cooperative_groups;
 
 __device__ __forceinline__ void red_add_v4(float* p, float4 d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(d.x), "f"(d.y),
@@ -79,128 +83,199 @@ __device__ __forceinline__ Chunk locate_chunk(const BlockWork* __restrict__ work
   return ch;
 }
 
+// Per-thread masks: lanes past the padded row (kp < 4*L*V4) do nothing.
 template <int L, int V4>
-__global__ void __launch_bounds__(256)
+struct Lanes {
+  int gl, gbase;
+  bool on[V4];
+  __device__ __forceinline__ Lanes(int kp) {
+    const int lane = threadIdx.x & 31;
+    gl = lane & (L - 1);
+    gbase = lane & ~(L - 1);
+#pragma unroll
+    for (int q = 0; q < V4; ++q) on[q] = 4 * (q * L + gl) < kp;
+  }
+  __device__ __forceinline__ int off(int q) const { return 4 * (q * L + gl); }
+};
+
+__device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+// L2-coherent 128-bit load (the factors are written by other SMs during the
+// kernel; ld.global.cg never returns a stale L1 line).
+__device__ __forceinline__ float4 ld_cg(const float* p) {
+  return __ldcg(reinterpret_cast<const float4*>(p));
+}
+
+template <int L, int V4>
+__device__ __forceinline__ void load_row(float4 (&dst)[V4], const float* row, const Lanes<L, V4>& ln) {
+#pragma unroll
+  for (int q = 0; q < V4; ++q) dst[q] = ln.on[q] ? ld_cg(row + ln.off(q)) : zero4();
+}
+
+// Write a finished user run back with a plain store.  (A run shared with a
+// neighbour chunk is never stored: its per-rating deltas went out as reds.)
+template <int L, int V4>
+__device__ __forceinline__ void store_row(float* row, const float4 (&u)[V4],
+                                          const Lanes<L, V4>& ln) {
+#pragma unroll
+  for (int q = 0; q < V4; ++q)
+    if (ln.on[q]) *reinterpret_cast<float4*>(row + ln.off(q)) = u[q];
+}
+
+// Software-pipelined walk over one chunk.  While rating t is computed, the
+// triple of t+1 is already in registers (the next L triples are prefetched a
+// batch ahead), its V row is in flight, and -- when t+1 starts a new user run
+// -- so is its U row.  kSweep: SGD update; else: accumulate (x - u.v)^2.
+// A user run that continues into a neighbour chunk ("shared") applies each
+// rating's U delta with red.add as it goes; an interior run is stored once.
+// All lanes of the warp execute the same trip count (maxlen) so the shuffles
+// stay converged; groups past their chunk end are predicated off.
+template <int L, int V4, bool kSweep>
+__device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
+                                             const int32_t* __restrict__ lrow,
+                                             const int32_t* __restrict__ lcol,
+                                             const float* __restrict__ val, float* U, float* V,
+                                             int kp, float alpha, float beta, int iter,
+                                             unsigned long long* bad) {
+  const Lanes<L, V4> ln(kp);
+  const int len = (int)(ch.end - ch.begin);
+  float* Ub = U + ch.row_start * kp;
+  float* Vb = V + ch.col_start * kp;
+  int first_row = -1, last_row = -1;
+  if (kSweep && len > 0) {
+    const int fr = __ldg(lrow + ch.begin), lr = __ldg(lrow + ch.end - 1);
+    if (ch.begin > ch.bbeg && __ldg(lrow + ch.begin - 1) == fr) first_row = fr;
+    if (ch.end < ch.bend && __ldg(lrow + ch.end) == lr) last_row = lr;
+  }
+  // triple batches A (current) and B (next)
+  int rA = 0, cA = 0, rB = 0, cB = 0;
+  float xA = 0.f, xB = 0.f;
+  if (ln.gl < len) {
+    rA = __ldg(lrow + ch.begin + ln.gl);
+    cA = __ldg(lcol + ch.begin + ln.gl);
+    xA = __ldg(val + ch.begin + ln.gl);
+  }
+  if (L + ln.gl < len) {
+    rB = __ldg(lrow + ch.begin + L + ln.gl);
+    cB = __ldg(lcol + ch.begin + L + ln.gl);
+    xB = __ldg(val + ch.begin + L + ln.gl);
+  }
+  int r = __shfl_sync(kFull, rA, ln.gbase);
+  int c = __shfl_sync(kFull, cA, ln.gbase);
+  float x = __shfl_sync(kFull, xA, ln.gbase);
+  float4 u[V4], v[V4];
+  if (len > 0) {
+    load_row<L, V4>(u, Ub + (int64_t)r * kp, ln);
+    load_row<L, V4>(v, Vb + (int64_t)c * kp, ln);
+  } else {
+#pragma unroll
+    for (int q = 0; q < V4; ++q) u[q] = v[q] = zero4();
+  }
+  bool shared = kSweep && (r == first_row || r == last_row);
+  bool dead = false;
+  double acc = 0.0;
+  const float two_a = 2.0f * alpha, ab = alpha * beta;
+
+  for (int t0 = 0; t0 < maxlen; t0 += L) {
+#pragma unroll 1
+    for (int j = 0; j < L; ++j) {
+      const int t = t0 + j;
+      // look ahead: triple of t+1 (from batch A, or B at the batch edge)
+      const bool last_in_batch = (j + 1 == L);
+      const int src = ln.gbase + ((j + 1) & (L - 1));
+      const int rn = __shfl_sync(kFull, last_in_batch ? rB : rA, src);
+      const int cn = __shfl_sync(kFull, last_in_batch ? cB : cA, src);
+      const float xn = __shfl_sync(kFull, last_in_batch ? xB : xA, src);
+      const bool valid = t < len && !dead;
+      const bool nvalid = t + 1 < len && !dead;
+      const bool newrun = nvalid && rn != r;
+      float4 vn[V4], un[V4];
+      if (nvalid) load_row<L, V4>(vn, Vb + (int64_t)cn * kp, ln);
+      if (newrun) load_row<L, V4>(un, Ub + (int64_t)rn * kp, ln);
+
+      float dot = 0.f;
+#pragma unroll
+      for (int q = 0; q < V4; ++q) {
+        dot = fmaf(u[q].x, v[q].x, dot);
+        dot = fmaf(u[q].y, v[q].y, dot);
+        dot = fmaf(u[q].z, v[q].z, dot);
+        dot = fmaf(u[q].w, v[q].w, dot);
+      }
+      dot = group_sum<L>(dot);
+      const float e = x - dot;
+      if (valid) {
+        if (!kSweep) {
+          const double ed = (double)x - (double)dot;
+          acc += ed * ed;
+        } else if (!isfinite(e)) {
+          if (ln.gl == 0) atomicMin(bad, pack_bad(ch.pos, iter, ch.begin + t - ch.bbeg));
+          dead = true;
+        } else {
+          const float g = two_a * e;
+          float* vp = Vb + (int64_t)c * kp;
+          float* up = Ub + (int64_t)r * kp;
+#pragma unroll
+          for (int q = 0; q < V4; ++q) {
+            float4 dv, du;
+            dv.x = g * u[q].x - ab * v[q].x;
+            dv.y = g * u[q].y - ab * v[q].y;
+            dv.z = g * u[q].z - ab * v[q].z;
+            dv.w = g * u[q].w - ab * v[q].w;
+            du.x = g * v[q].x - ab * u[q].x;
+            du.y = g * v[q].y - ab * u[q].y;
+            du.z = g * v[q].z - ab * u[q].z;
+            du.w = g * v[q].w - ab * u[q].w;
+            u[q].x += du.x;
+            u[q].y += du.y;
+            u[q].z += du.z;
+            u[q].w += du.w;
+            if (ln.on[q]) {
+              red_add_v4(vp + ln.off(q), dv);
+              if (shared) red_add_v4(up + ln.off(q), du);
+            }
+          }
+        }
+      }
+      if (kSweep && valid && !dead && !shared && (newrun || !nvalid))
+        store_row<L, V4>(Ub + (int64_t)r * kp, u, ln);
+      if (newrun) {
+#pragma unroll
+        for (int q = 0; q < V4; ++q) u[q] = un[q];
+        shared = kSweep && (rn == first_row || rn == last_row);
+      }
+      if (nvalid) {
+#pragma unroll
+        for (int q = 0; q < V4; ++q) v[q] = vn[q];
+      }
+      r = rn;
+      c = cn;
+      x = xn;
+    }
+    // advance the triple batches
+    rA = rB; cA = cB; xA = xB;
+    const int nb = t0 + 2 * L + ln.gl;
+    if (nb < len) {
+      rB = __ldg(lrow + ch.begin + nb);
+      cB = __ldg(lcol + ch.begin + nb);
+      xB = __ldg(val + ch.begin + nb);
+    }
+  }
+  return acc;
+}
+
+template <int L, int V4>
+__global__ void __launch_bounds__(256, 2)
 sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
                 const float* __restrict__ val, float* __restrict__ U, float* __restrict__ V,
                 int kp, float alpha, float beta, int iter, unsigned long long* __restrict__ bad) {
   constexpr int GPW = 32 / L;
   const int lane = threadIdx.x & 31;
-  const int gl = lane & (L - 1);
-  const int gbase = lane & ~(L - 1);
   const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  const int chunk = warp * GPW + lane / L;
-  const Chunk ch = locate_chunk(work, nwork, total_chunks, chunk);
-  const int len = (int)(ch.end - ch.begin);
-  const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
+  const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
+  const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
   if (maxlen == 0) return;
-
-  float* Ub = U + ch.row_start * kp;
-  float* Vb = V + ch.col_start * kp;
-  // runs that continue into a neighbouring chunk are shared with another group
-  int first_row = -1, last_row = -1;
-  if (len > 0) {
-    const int fr = lrow[ch.begin], lr = lrow[ch.end - 1];
-    if (ch.begin > ch.bbeg && lrow[ch.begin - 1] == fr) first_row = fr;
-    if (ch.end < ch.bend && lrow[ch.end] == lr) last_row = lr;
-  }
-
-  float4 u[V4], u0[V4];
-  int cur = -1;
-  bool shared = false, dead = false;
-  const float two_a = 2.0f * alpha, ab = alpha * beta;
-
-  for (int t0 = 0; t0 < maxlen; t0 += L) {
-    int r_l = 0, c_l = 0;
-    float x_l = 0.f;
-    if (t0 + gl < len) {
-      const int64_t i = ch.begin + t0 + gl;
-      r_l = __ldg(lrow + i);
-      c_l = __ldg(lcol + i);
-      x_l = __ldg(val + i);
-    }
-#pragma unroll 2
-    for (int j = 0; j < L; ++j) {
-      const int r = __shfl_sync(kFull, r_l, gbase + j);
-      const int c = __shfl_sync(kFull, c_l, gbase + j);
-      const float x = __shfl_sync(kFull, x_l, gbase + j);
-      const bool valid = (t0 + j < len) && !dead;
-      if (valid && r != cur) {
-        if (cur >= 0) {
-          float* p = Ub + (int64_t)cur * kp;
-#pragma unroll
-          for (int q = 0; q < V4; ++q) {
-            float* pq = p + 4 * (q * L + gl);
-            if (shared)
-              red_add_v4(pq, make_float4(u[q].x - u0[q].x, u[q].y - u0[q].y, u[q].z - u0[q].z,
-                                         u[q].w - u0[q].w));
-            else
-              *reinterpret_cast<float4*>(pq) = u[q];
-          }
-        }
-        const float* p = Ub + (int64_t)r * kp;
-#pragma unroll
-        for (int q = 0; q < V4; ++q) {
-          u[q] = __ldcg(reinterpret_cast<const float4*>(p + 4 * (q * L + gl)));
-          u0[q] = u[q];
-        }
-        cur = r;
-        shared = (r == first_row) || (r == last_row);
-      }
-      float4 v[V4];
-      float dot = 0.f;
-      float* vp = Vb + (int64_t)c * kp;
-      if (valid) {
-#pragma unroll
-        for (int q = 0; q < V4; ++q) {
-          v[q] = __ldcg(reinterpret_cast<const float4*>(vp + 4 * (q * L + gl)));
-          dot = fmaf(u[q].x, v[q].x, dot);
-          dot = fmaf(u[q].y, v[q].y, dot);
-          dot = fmaf(u[q].z, v[q].z, dot);
-          dot = fmaf(u[q].w, v[q].w, dot);
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < V4; ++q) v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      dot = group_sum<L>(dot);
-      const float e = x - dot;
-      if (valid) {
-        if (!isfinite(e)) {
-          if (gl == 0) atomicMin(bad, pack_bad(ch.pos, iter, ch.begin + t0 + j - ch.bbeg));
-          dead = true;
-        } else {
-          const float g = two_a * e;
-#pragma unroll
-          for (int q = 0; q < V4; ++q) {
-            float4 dv;
-            dv.x = g * u[q].x - ab * v[q].x;
-            dv.y = g * u[q].y - ab * v[q].y;
-            dv.z = g * u[q].z - ab * v[q].z;
-            dv.w = g * u[q].w - ab * v[q].w;
-            u[q].x += g * v[q].x - ab * u[q].x;
-            u[q].y += g * v[q].y - ab * u[q].y;
-            u[q].z += g * v[q].z - ab * u[q].z;
-            u[q].w += g * v[q].w - ab * u[q].w;
-            red_add_v4(vp + 4 * (q * L + gl), dv);
-          }
-        }
-      }
-    }
-  }
-  if (cur >= 0) {
-    float* p = Ub + (int64_t)cur * kp;
-#pragma unroll
-    for (int q = 0; q < V4; ++q) {
-      float* pq = p + 4 * (q * L + gl);
-      if (shared)
-        red_add_v4(pq, make_float4(u[q].x - u0[q].x, u[q].y - u0[q].y, u[q].z - u0[q].z,
-                                   u[q].w - u0[q].w));
-      else
-        *reinterpret_cast<float4*>(pq) = u[q];
-    }
-  }
+  walk_chunk<L, V4, true>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter, bad);
 }
 
 // Post-sweep SSE of each block: sum over the chunk of (x - u.v)^2 in fp64,
@@ -213,60 +288,59 @@ sse_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const float* __restrict__ V, int kp, double* __restrict__ sse) {
   constexpr int GPW = 32 / L;
   const int lane = threadIdx.x & 31;
-  const int gl = lane & (L - 1);
-  const int gbase = lane & ~(L - 1);
   const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  const int chunk = warp * GPW + lane / L;
-  const Chunk ch = locate_chunk(work, nwork, total_chunks, chunk);
+  const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
   const int len = (int)(ch.end - ch.begin);
   const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
   if (maxlen == 0) return;
-  const float* Ub = U + ch.row_start * kp;
-  const float* Vb = V + ch.col_start * kp;
-  float4 u[V4];
-  int cur = -1;
-  double acc = 0.0;
-  for (int t0 = 0; t0 < maxlen; t0 += L) {
-    int r_l = 0, c_l = 0;
-    float x_l = 0.f;
-    if (t0 + gl < len) {
-      const int64_t i = ch.begin + t0 + gl;
-      r_l = __ldg(lrow + i);
-      c_l = __ldg(lcol + i);
-      x_l = __ldg(val + i);
+  const double acc = walk_chunk<L, V4, false>(ch, maxlen, lrow, lcol, val, const_cast<float*>(U),
+                                              const_cast<float*>(V), kp, 0.f, 0.f, 0, nullptr);
+  if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
+}
+
+// Whole outer step in one cooperative launch: for every batch, `iters`
+// sweeps, then the per-block SSE, separated by grid-wide barriers (a stratum
+// must finish before its SSE, and the SSE before the next stratum touches the
+// same U/V slices).  Groups loop over the batch's chunks (normally one each).
+struct BatchDesc {
+  int w0, nw, chunks, pad;
+};
+
+template <int L, int V4>
+__global__ void __launch_bounds__(256, 2)
+epoch_fast_kernel(const BlockWork* __restrict__ work, const BatchDesc* __restrict__ batches,
+                  int nbatch, int iters, const int32_t* __restrict__ lrow,
+                  const int32_t* __restrict__ lcol, const float* __restrict__ val,
+                  float* __restrict__ U, float* __restrict__ V, int kp, float alpha, float beta,
+                  double* __restrict__ sse, unsigned long long* __restrict__ bad) {
+  constexpr int GPW = 32 / L;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int stride = (int)(gridDim.x * (blockDim.x >> 5)) * GPW;
+  for (int t = 0; t < nbatch; ++t) {
+    const BatchDesc bd = batches[t];
+    const BlockWork* w = work + bd.w0;
+    for (int it = 0; it < iters; ++it) {
+      for (int base = warp * GPW; base < bd.chunks; base += stride) {
+        const Chunk ch = locate_chunk(w, bd.nw, bd.chunks, base + lane / L);
+        const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
+        if (maxlen > 0)
+          walk_chunk<L, V4, true>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, it, bad);
+      }
+      grid.sync();
     }
-#pragma unroll 2
-    for (int j = 0; j < L; ++j) {
-      const int r = __shfl_sync(kFull, r_l, gbase + j);
-      const int c = __shfl_sync(kFull, c_l, gbase + j);
-      const float x = __shfl_sync(kFull, x_l, gbase + j);
-      const bool valid = t0 + j < len;
-      if (valid && r != cur) {
-        const float* p = Ub + (int64_t)r * kp;
-#pragma unroll
-        for (int q = 0; q < V4; ++q) u[q] = __ldg(reinterpret_cast<const float4*>(p + 4 * (q * L + gl)));
-        cur = r;
-      }
-      float dot = 0.f;
-      if (valid) {
-        const float* vp = Vb + (int64_t)c * kp;
-#pragma unroll
-        for (int q = 0; q < V4; ++q) {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(vp + 4 * (q * L + gl)));
-          dot = fmaf(u[q].x, v.x, dot);
-          dot = fmaf(u[q].y, v.y, dot);
-          dot = fmaf(u[q].z, v.z, dot);
-          dot = fmaf(u[q].w, v.w, dot);
-        }
-      }
-      dot = group_sum<L>(dot);
-      if (valid) {
-        const double e = (double)x - (double)dot;
-        acc += e * e;
-      }
+    for (int base = warp * GPW; base < bd.chunks; base += stride) {
+      const Chunk ch = locate_chunk(w, bd.nw, bd.chunks, base + lane / L);
+      const int len = (int)(ch.end - ch.begin);
+      const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
+      if (maxlen == 0) continue;
+      const double acc =
+          walk_chunk<L, V4, false>(ch, maxlen, lrow, lcol, val, U, V, kp, 0.f, 0.f, 0, nullptr);
+      if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
     }
+    if (t + 1 < nbatch) grid.sync();
   }
-  if (gl == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
 }
 
 // ---------------------------------------------------------------- exact
@@ -364,55 +438,60 @@ struct Shape {
 };
 
 Shape shape_for(int kp) {
-  // smallest power-of-two group with V4 = 1 up to 32 lanes, then V4 > 1
+  // each lane holds up to 4 float4 (16 floats) of the row: several
+  // independent groups per warp, few shuffles per rating
   const int f4 = kp / 4;  // float4 per row
-  if (f4 <= 32) {
-    int L = 1;
-    while (L < f4) L <<= 1;
-    return {L, 1};
+  if (f4 <= 4) {
+    int v4 = 1;
+    while (v4 < f4) v4 <<= 1;
+    return {1, v4};
   }
-  if (f4 <= 64) return {32, 2};
-  if (f4 <= 128) return {32, 4};
-  return {32, 8};
+  int L = 1;
+  while (L * 4 < f4) L <<= 1;
+  return {L, 4};
 }
 
-template <int L, int V4>
-void launch_pair(bool sweep, dim3 grid, cudaStream_t s, const BlockWork* w, int nwork, int total,
-                 bgmf_ctx* c, float a, float b, int it) {
-  if (sweep)
-    sgd_fast_kernel<L, V4><<<grid, 256, 0, s>>>(w, nwork, total, c->d_lrow, c->d_lcol, c->d_val,
-                                                c->d_u, c->d_v, c->kp, a, b, it, c->d_bad);
-  else
-    sse_fast_kernel<L, V4><<<grid, 256, 0, s>>>(w, nwork, total, c->d_lrow, c->d_lcol, c->d_val,
-                                                c->d_u, c->d_v, c->kp, c->d_sse);
-}
+#define BGMF_SHAPES(X) X(1, 1) X(1, 2) X(1, 4) X(2, 4) X(4, 4) X(8, 4) X(16, 4) X(32, 4)
 
 void launch_fast(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, const BlockWork* w,
                  int nwork, int total, bgmf_ctx* c, float a, float b, int it) {
-#define BGMF_CASE(LL, VV)                                          \
-  if (sh.L == LL && sh.V4 == VV) {                                 \
-    launch_pair<LL, VV>(sweep, grid, s, w, nwork, total, c, a, b, it); \
-    return;                                                        \
+#define BGMF_CASE(LL, VV)                                                                     \
+  if (sh.L == LL && sh.V4 == VV) {                                                            \
+    if (sweep)                                                                                \
+      sgd_fast_kernel<LL, VV><<<grid, 256, 0, s>>>(w, nwork, total, c->d_lrow, c->d_lcol,     \
+                                                   c->d_val, c->d_u, c->d_v, c->kp, a, b, it, \
+                                                   c->d_bad);                                 \
+    else                                                                                      \
+      sse_fast_kernel<LL, VV><<<grid, 256, 0, s>>>(w, nwork, total, c->d_lrow, c->d_lcol,     \
+                                                   c->d_val, c->d_u, c->d_v, c->kp, c->d_sse); \
+    return;                                                                                   \
   }
-  BGMF_CASE(1, 1) BGMF_CASE(2, 1) BGMF_CASE(4, 1) BGMF_CASE(8, 1) BGMF_CASE(16, 1)
-  BGMF_CASE(32, 1) BGMF_CASE(32, 2) BGMF_CASE(32, 4) BGMF_CASE(32, 8)
+  BGMF_SHAPES(BGMF_CASE)
 #undef BGMF_CASE
 }
 
-template <int L, int V4>
-int occupancy_warps(bgmf_ctx*) {
-  int blocks = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, sgd_fast_kernel<L, V4>, 256, 0);
-  return blocks * 8;
+const void* epoch_kernel_ptr(const Shape& sh) {
+#define BGMF_EP(LL, VV) \
+  if (sh.L == LL && sh.V4 == VV) return reinterpret_cast<const void*>(&epoch_fast_kernel<LL, VV>);
+  BGMF_SHAPES(BGMF_EP)
+#undef BGMF_EP
+  return nullptr;
 }
 
-int resident_warps(bgmf_ctx* c, const Shape& sh) {
-  if (c->warps_per_sm > 0) return c->warps_per_sm;
-#define BGMF_OCC(LL, VV) if (sh.L == LL && sh.V4 == VV) return occupancy_warps<LL, VV>(c);
-  BGMF_OCC(1, 1) BGMF_OCC(2, 1) BGMF_OCC(4, 1) BGMF_OCC(8, 1) BGMF_OCC(16, 1)
-  BGMF_OCC(32, 1) BGMF_OCC(32, 2) BGMF_OCC(32, 4) BGMF_OCC(32, 8)
-#undef BGMF_OCC
-  return 32;
+const void* sweep_kernel_ptr(const Shape& sh) {
+#define BGMF_SW(LL, VV) \
+  if (sh.L == LL && sh.V4 == VV) return reinterpret_cast<const void*>(&sgd_fast_kernel<LL, VV>);
+  BGMF_SHAPES(BGMF_SW)
+#undef BGMF_SW
+  return nullptr;
+}
+
+// Resident 256-thread CTAs per SM of a kernel (the one-wave capacity).
+int resident_ctas(bgmf_ctx* c, const void* fn) {
+  if (c->warps_per_sm > 0) return (c->warps_per_sm + 7) / 8;
+  int blocks = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 256, 0);
+  return blocks > 0 ? blocks : 1;
 }
 
 // Fill h_work for every batch; returns per-batch (work offset, total chunks).
@@ -420,8 +499,12 @@ struct BatchRange {
   int w0, nw, chunks;
 };
 
+// Chunking: each batch's ratings are cut into equal chunks, at most `groups`
+// of them (groups = worker groups resident in one wave; 0 = one chunk per
+// block, the exact path).  chunk = ceil(batch_nnz / (groups - B)) so the
+// per-block rounding can never spill into a second wave.
 int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
-               int64_t chunk_len_base, std::vector<BatchRange>& ranges,
+               int64_t groups, std::vector<BatchRange>& ranges,
                const std::vector<char>* active = nullptr) {
   const int total = batch_off[nbatch];
   int rc = ensure_step_scratch(c, (size_t)total);
@@ -429,29 +512,41 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
   ranges.assign(nbatch, BatchRange{0, 0, 0});
   int w = 0;
   for (int t = 0; t < nbatch; ++t) {
-    ranges[t].w0 = w;
-    int chunks = 0;
+    int64_t batch_nnz = 0;
+    int nonempty = 0;
     for (int q = batch_off[t]; q < batch_off[t + 1]; ++q) {
       const int b = plan[q];
       if (b < 0 || b >= c->I * c->J) return fail(c, BGMF_ERR_ARG, "plan block id out of range");
       if (active && !(*active)[q]) continue;
+      const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
+      batch_nnz += cnt;
+      nonempty += cnt > 0;
+    }
+    int64_t cl = INT32_MAX;
+    if (groups > 0) {
+      const int64_t slots = groups - nonempty > 0 ? groups - nonempty : 1;
+      cl = (batch_nnz + slots - 1) / slots;
+      if (cl < c->min_chunk) cl = c->min_chunk;
+    }
+    ranges[t].w0 = w;
+    int chunks = 0;
+    for (int q = batch_off[t]; q < batch_off[t + 1]; ++q) {
+      const int b = plan[q];
+      if (active && !(*active)[q]) continue;
       const int64_t beg = c->h_offsets[b], end = c->h_offsets[b + 1];
       const int64_t cnt = end - beg;
       if (cnt == 0) continue;
-      int64_t cl = chunk_len_base;
-      if (cl < c->min_chunk) cl = c->min_chunk;
-      if (cl > cnt) cl = cnt;
-      if (cl > (1 << 30)) cl = 1 << 30;
+      const int64_t bl = cl < cnt ? cl : cnt;
       BlockWork& bw = c->h_work[w++];
       bw.begin = beg;
       bw.end = end;
       bw.row_start = c->row_bounds[b / c->J];
       bw.col_start = c->col_bounds[b % c->J];
-      bw.chunk_len = (int32_t)cl;
+      bw.chunk_len = (int32_t)bl;
       bw.first_chunk = chunks;
       bw.block_id = b;
       bw.pos = q;
-      chunks += (int)((cnt + cl - 1) / cl);
+      chunks += (int)((cnt + bl - 1) / bl);
     }
     ranges[t].nw = w - ranges[t].w0;
     ranges[t].chunks = chunks;
@@ -459,11 +554,8 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
   return BGMF_OK;
 }
 
-int64_t base_chunk_len(bgmf_ctx* c, const Shape& sh, int nbatch) {
-  const int64_t groups = (int64_t)c->num_sms * resident_warps(c, sh) * (32 / sh.L);
-  const int64_t per_batch = nbatch > 0 ? (c->nnz + nbatch - 1) / nbatch : c->nnz;
-  int64_t cl = groups > 0 ? (per_batch + groups - 1) / groups : per_batch;
-  return cl < 1 ? 1 : cl;
+int64_t sweep_groups(bgmf_ctx* c, const Shape& sh) {
+  return (int64_t)c->num_sms * resident_ctas(c, sweep_kernel_ptr(sh)) * 8 * (32 / sh.L);
 }
 
 }  // namespace
@@ -482,46 +574,86 @@ int ensure_step_scratch(bgmf_ctx* c, size_t nwork) {
     c->d_work = nullptr;
     c->h_work = nullptr;
     size_t cap = nwork < 64 ? 64 : nwork;
-    BGMF_CK(c, cudaMalloc(&c->d_work, sizeof(BlockWork) * cap * 8));  // 8x: exact out slots
+    // device: work table, then exact-mode output slots / batch descriptors
+    BGMF_CK(c, cudaMalloc(&c->d_work, sizeof(BlockWork) * cap * 8));
     BGMF_CK(c, cudaMallocHost(&c->h_work, sizeof(BlockWork) * cap));
     c->work_cap = cap;
   }
   return BGMF_OK;
 }
 
+// One outer step, fast path.  Default: ONE cooperative launch of
+// epoch_fast_kernel for the whole step (grid = one wave of resident CTAs).
+// Option fused=0: per batch, `iters` sgd launches + one sse launch.
 int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
                   int iters, float alpha, float beta) {
   cudaStream_t s = c->stream;
   const Shape sh = shape_for(c->kp);
+  const int gpw = 32 / sh.L;
+  const int nb = c->I * c->J;
+  const void* ep = epoch_kernel_ptr(sh);
+  const int ctas_per_sm = c->fused ? resident_ctas(c, ep) : resident_ctas(c, sweep_kernel_ptr(sh));
+  const int64_t groups = (int64_t)c->num_sms * ctas_per_sm * 8 * gpw;
   std::vector<BatchRange> ranges;
-  int rc = build_work(c, plan, batch_off, nbatch, base_chunk_len(c, sh, nbatch), ranges);
+  int rc = build_work(c, plan, batch_off, nbatch, groups, ranges);
   if (rc) return rc;
   const int nw = ranges.empty() ? 0 : ranges.back().w0 + ranges.back().nw;
-  const int nb = c->I * c->J;
+  BatchDesc* bdesc = reinterpret_cast<BatchDesc*>(c->d_work + c->work_cap);
+  std::vector<BatchDesc> hb(nbatch > 0 ? nbatch : 1);
+  int max_chunks = 0;
+  double ratings = 0;
+  for (int t = 0; t < nbatch; ++t) {
+    hb[t] = BatchDesc{ranges[t].w0, ranges[t].nw, ranges[t].chunks, 0};
+    if (ranges[t].chunks > max_chunks) max_chunks = ranges[t].chunks;
+  }
+  for (int q = 0; q < nw; ++q) ratings += (double)(c->h_work[q].end - c->h_work[q].begin);
   if (nw > 0)
     BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * nw,
                                cudaMemcpyHostToDevice, s));
   BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, s));
   BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
-  const int gpw = 32 / sh.L;
-  for (int t = 0; t < nbatch; ++t) {
-    const BatchRange& r = ranges[t];
-    if (r.chunks == 0) continue;
-    const int warps = (r.chunks + gpw - 1) / gpw;
-    const dim3 grid((warps + 7) / 8);
-    const BlockWork* w = c->d_work + r.w0;
-    double ratings = 0;
-    for (int q = 0; q < r.nw; ++q) ratings += (double)(c->h_work[r.w0 + q].end - c->h_work[r.w0 + q].begin);
-    for (int it = 0; it < iters; ++it) {
+  if (c->fused && max_chunks > 0) {
+    BGMF_CK(c, cudaMemcpyAsync(bdesc, hb.data(), sizeof(BatchDesc) * nbatch,
+                               cudaMemcpyHostToDevice, s));
+    const int need = (max_chunks + gpw * 8 - 1) / (gpw * 8);
+    const int cap = c->num_sms * ctas_per_sm;
+    const dim3 grid(need < cap ? need : cap);
+    const BlockWork* dw = c->d_work;
+    const BatchDesc* db = bdesc;
+    int nbt = nbatch, its = iters, kp = c->kp;
+    const int32_t* lr = c->d_lrow;
+    const int32_t* lc = c->d_lcol;
+    const float* vv = c->d_val;
+    float* U = c->d_u;
+    float* V = c->d_v;
+    double* sse = c->d_sse;
+    unsigned long long* bad = c->d_bad;
+    void* args[] = {&dw, &db, &nbt, &its, &lr, &lc, &vv, &U, &V, &kp, &alpha, &beta, &sse, &bad};
+    TimedLaunch* slot = nullptr;
+    if (c->timing) record_begin(c, 0, ratings * iters * (12.0 + 16.0 * c->k), &slot);
+    BGMF_CK(c, cudaLaunchCooperativeKernel(ep, grid, dim3(256), args, 0, s));
+    if (slot) record_end(c, slot);
+  } else {
+    for (int t = 0; t < nbatch; ++t) {
+      const BatchRange& r = ranges[t];
+      if (r.chunks == 0) continue;
+      const int warps = (r.chunks + gpw - 1) / gpw;
+      const dim3 grid((warps + 7) / 8);
+      const BlockWork* w = c->d_work + r.w0;
+      double br = 0;
+      for (int q = 0; q < r.nw; ++q)
+        br += (double)(c->h_work[r.w0 + q].end - c->h_work[r.w0 + q].begin);
+      for (int it = 0; it < iters; ++it) {
+        TimedLaunch* slot = nullptr;
+        if (c->timing) record_begin(c, 0, br * (12.0 + 16.0 * c->k), &slot);
+        launch_fast(true, sh, grid, s, w, r.nw, r.chunks, c, alpha, beta, it);
+        if (slot) record_end(c, slot);
+      }
       TimedLaunch* slot = nullptr;
-      if (c->timing) record_begin(c, 0, ratings * (12.0 + 16.0 * c->k), &slot);
-      launch_fast(true, sh, grid, s, w, r.nw, r.chunks, c, alpha, beta, it);
+      if (c->timing) record_begin(c, 1, 0.0, &slot);
+      launch_fast(false, sh, grid, s, w, r.nw, r.chunks, c, alpha, beta, 0);
       if (slot) record_end(c, slot);
     }
-    TimedLaunch* slot = nullptr;
-    if (c->timing) record_begin(c, 1, 0.0, &slot);
-    launch_fast(false, sh, grid, s, w, r.nw, r.chunks, c, alpha, beta, 0);
-    if (slot) record_end(c, slot);
   }
   BGMF_CK(c, cudaGetLastError());
   BGMF_CK(c, cudaMemcpyAsync(c->h_sse, c->d_sse, sizeof(double) * nb, cudaMemcpyDeviceToHost, s));
@@ -535,7 +667,7 @@ int run_step_exact(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, i
                    int iters, double alpha, double beta) {
   cudaStream_t s = c->stream;
   std::vector<BatchRange> ranges;
-  int rc = build_work(c, plan, batch_off, nbatch, INT32_MAX, ranges);
+  int rc = build_work(c, plan, batch_off, nbatch, 0, ranges);
   if (rc) return rc;
   const int nw = ranges.empty() ? 0 : ranges.back().w0 + ranges.back().nw;
   const int nb = c->I * c->J;
@@ -576,7 +708,7 @@ int run_step_converge_exact(bgmf_ctx* c, const int32_t* plan, const int32_t* bat
                             int64_t* iters_out, int32_t* capped_out) {
   cudaStream_t s = c->stream;
   std::vector<BatchRange> ranges;
-  int rc = build_work(c, plan, batch_off, nbatch, INT32_MAX, ranges);
+  int rc = build_work(c, plan, batch_off, nbatch, 0, ranges);
   if (rc) return rc;
   const int nw = ranges.empty() ? 0 : ranges.back().w0 + ranges.back().nw;
   const int nb = c->I * c->J;
@@ -622,7 +754,7 @@ int run_step_converge_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batc
   cudaStream_t s = c->stream;
   const Shape sh = shape_for(c->kp);
   const int nb = c->I * c->J;
-  const int64_t cl = base_chunk_len(c, sh, nbatch);
+  const int64_t cl = sweep_groups(c, sh);
   std::vector<double> sse_final(nb, 0.0);
   for (int b = 0; b < nb; ++b) { iters_out[b] = 0; capped_out[b] = 0; }
   unsigned long long best = kNoBad;
@@ -719,7 +851,7 @@ int train_sse_fast(bgmf_ctx* c, double* out) {
   for (int b = 0; b < nb; ++b) plan[b] = b;
   const Shape sh = shape_for(c->kp);
   std::vector<BatchRange> ranges;
-  int rc = build_work(c, plan.data(), off.data(), 1, base_chunk_len(c, sh, 1), ranges);
+  int rc = build_work(c, plan.data(), off.data(), 1, sweep_groups(c, sh), ranges);
   if (rc) return rc;
   cudaStream_t s = c->stream;
   BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, s));
@@ -745,7 +877,7 @@ int train_sse_exact(bgmf_ctx* c, double* out) {
   std::vector<int32_t> plan(nb), off{0, nb};
   for (int b = 0; b < nb; ++b) plan[b] = b;
   std::vector<BatchRange> ranges;
-  int rc = build_work(c, plan.data(), off.data(), 1, INT32_MAX, ranges);
+  int rc = build_work(c, plan.data(), off.data(), 1, 0, ranges);
   if (rc) return rc;
   cudaStream_t s = c->stream;
   const int nw = ranges[0].nw;

@@ -34,13 +34,16 @@ class EngineOptions:
                blocks, which keeps the lossless-Hogwild drift far below 1e-3).
     device     CUDA ordinal; default $BGMF_DEVICE, else $LOCAL_RANK, else 0.
     timing     record CUDA events around every kernel launch.
+    fused      one cooperative launch per outer step (default) instead of one
+               launch per stratum sweep / SSE pass.
     """
 
     exact: bool = False
-    min_chunk: int = 48
+    min_chunk: int = 256
     device: int | None = None
     timing: bool = False
     warps_per_sm: int = 0
+    fused: bool = True
 
 
 def default_device() -> int:
@@ -64,6 +67,7 @@ class Engine:
         self._opt("min_chunk", float(self.options.min_chunk))
         self._opt("timing", 1.0 if self.options.timing else 0.0)
         self._opt("warps_per_sm", float(self.options.warps_per_sm))
+        self._opt("fused", 1.0 if self.options.fused else 0.0)
         self.n = self.m = self.nnz = 0
         self.I = self.J = 0
         self.k = 0

@@ -1,0 +1,321 @@
+"""Multi-GPU BGMF: one process per GPU, U resident, V blocks rotating.
+
+SURVEY §8(e).  A stratum's blocks own pairwise-disjoint U and V slices, so the
+result does not depend on which GPU computes which block.  Rank g owns the
+contiguous U row-blocks ``[g*R, (g+1)*R)`` (R = ceil(I / G)) and all rating
+blocks of those rows (≈ nnz/G ratings and n/G U rows stay in its HBM).  For the
+square rotating plan, batch t of step s pairs row-block r with column
+(r - s - t) mod P, so after every batch each V block moves one row down: G
+blocks per batch cross to rank g+1, and at a step boundary every block moves
+two rows.  :class:`RingSchedule` derives those transfers generically from any
+plan (`plan_step` of any I x J grid), so wide grids work too.
+
+Transfers are NCCL point-to-point (``torch.distributed`` batch_isend_irecv of V
+slices that the engine uses in place via ``bgmf_bind_factors``) ordered on the
+engine's CUDA stream.  Per-block SSEs are summed across ranks (all-reduce of
+P^2 doubles) and merged in plan order on every rank, exactly like the
+single-GPU trainer.  The same schedule code drives the CPU/gloo tests, where
+the per-block compute is the oracle (tests only).
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .scheduler import plan_step
+
+
+@dataclass(frozen=True)
+class Transfer:
+    col: int   # V column-block
+    src: int   # rank holding its latest version
+    dst: int   # rank that needs it for the next batch
+
+
+class RingSchedule:
+    """Row-block ownership and the V-block moves implied by the plans."""
+
+    def __init__(self, grid_i: int, grid_j: int, world: int):
+        if world < 1:
+            raise ValueError("world must be >= 1")
+        self.I, self.J, self.G = grid_i, grid_j, world
+        self.R = math.ceil(grid_i / world)
+        # holder[j]: rank with the latest V_j; None = every rank (initial replicas)
+        self.holder: list[int | None] = [None] * grid_j
+
+    def owner(self, bi: int) -> int:
+        return min(bi // self.R, self.G - 1)
+
+    def rows_of(self, rank: int) -> range:
+        lo = min(rank * self.R, self.I)
+        hi = self.I if rank == self.G - 1 else min((rank + 1) * self.R, self.I)
+        return range(lo, hi)
+
+    def batches(self, step0: int):
+        return [list(b) for b in plan_step(self.I, self.J, step0)]
+
+    def transfers_for(self, batch) -> list[Transfer]:
+        """Moves needed before ``batch`` runs; updates the holders."""
+        moves = []
+        for bi, bj in batch:
+            dst = self.owner(bi)
+            src = self.holder[bj]
+            if src is not None and src != dst:
+                moves.append(Transfer(bj, src, dst))
+            self.holder[bj] = dst
+        return moves
+
+    def local_blocks(self, batch, rank: int):
+        return [(bi, bj) for bi, bj in batch if self.owner(bi) == rank]
+
+
+def exchange(moves, rank: int, v_slice, dist) -> None:
+    """Run one batch's V moves: isend what this rank holds, irecv what it needs."""
+    ops = []
+    for mv in moves:
+        if mv.src == rank:
+            ops.append(dist.P2POp(dist.isend, v_slice(mv.col), mv.dst))
+        elif mv.dst == rank:
+            ops.append(dist.P2POp(dist.irecv, v_slice(mv.col), mv.src))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+def sync_all_v(sched: RingSchedule, rank: int, v_slice, dist) -> None:
+    """Give every rank the latest version of every V block (broadcast from holders)."""
+    for j in range(sched.J):
+        src = sched.holder[j]
+        if src is not None:
+            dist.broadcast(v_slice(j), src=src)
+
+
+def shard_rows(rows: np.ndarray, row_bounds: np.ndarray, sched: RingSchedule, rank: int):
+    """Mask of the ratings whose row-block this rank owns."""
+    r = sched.rows_of(rank)
+    lo, hi = row_bounds[r.start], row_bounds[r.stop]
+    return (rows >= lo) & (rows < hi)
+
+
+def run_epoch(sched: RingSchedule, shard, rank: int, dist, step0: int, g: int,
+              alpha: float, beta: float, nb: int, J: int):
+    """One outer step on this rank: before each batch move the V blocks it
+    needs, then run the batch's blocks whose rows this rank owns.  Returns
+    (local per-block SSE [nb], plan order of block ids, first local divergence
+    as (block, entry, iter) or None).  ``shard`` provides ``v_slice(j)`` and
+    ``run_batch(blocks, g, alpha, beta) -> (sse[nb], bad, ids)``."""
+    sse_all = np.zeros(nb, np.float64)
+    order: list[int] = []
+    bad_any = None
+    for batch in sched.batches(step0):
+        exchange(sched.transfers_for(batch), rank, shard.v_slice, dist)
+        order.extend(bi * J + bj for bi, bj in batch)
+        mine = sched.local_blocks(batch, rank)
+        if mine:
+            sse, bad, ids = shard.run_batch(mine, g, alpha, beta)
+            sse_all[ids] = sse[ids]
+            if bad is not None and bad_any is None:
+                bad_any = (int(ids[bad[0]]), bad[1], bad[2])
+    return sse_all, order, bad_any
+
+
+# ---------------------------------------------------------------------------- GPU
+
+
+class GpuShard:
+    """This rank's engine: its ratings, full-size U/V buffers (torch-allocated
+    so NCCL can move V slices), bound into libbgmf with bgmf_bind_factors."""
+
+    def __init__(self, d, cfg, sched: RingSchedule, rank: int, device: int, options=None):
+        import torch
+
+        from .device import Engine, EngineOptions
+        from .partition import make_grid
+
+        self.torch = torch
+        self.grid = make_grid(d.n, d.m, cfg.grid_i, cfg.grid_j)
+        mask = shard_rows(d.rows, self.grid.row_bounds, sched, rank)
+        self.local_nnz = int(mask.sum())
+        self.stream = torch.cuda.current_stream(device)
+        opts = options or EngineOptions()
+        opts = EngineOptions(exact=False, min_chunk=opts.min_chunk, device=device,
+                             timing=opts.timing, warps_per_sm=opts.warps_per_sm)
+        self.eng = Engine(opts, stream=self.stream.cuda_stream)
+        self.eng.partition(d.rows[mask], d.cols[mask], d.values[mask], d.n, d.m,
+                           cfg.grid_i, cfg.grid_j)
+        self.k, self.kp = cfg.k, (cfg.k + 3) // 4 * 4
+        self.U = torch.zeros((d.n, self.kp), dtype=torch.float32, device=f"cuda:{device}")
+        self.V = torch.zeros((d.m, self.kp), dtype=torch.float32, device=f"cuda:{device}")
+        self.eng.bind_factors(self.U.data_ptr(), self.V.data_ptr(), d.n, d.m, cfg.k, self.kp)
+        self.counts = np.diff(self.eng.offsets)
+
+    def set_factors(self, u, v):
+        self.eng.set_factors(u, v)
+
+    def v_slice(self, j: int):
+        cb = self.grid.col_bounds
+        return self.V[int(cb[j]):int(cb[j + 1])]
+
+    def u_rows(self, rows: range):
+        rb = self.grid.row_bounds
+        return self.U[int(rb[rows.start]):int(rb[rows.stop])]
+
+    def run_batch(self, blocks, g: int, alpha: float, beta: float):
+        ids, off = self.eng.plan_arrays([blocks])
+        sse, bad = self.eng.run_step(ids, off, g, alpha, beta)
+        return sse, bad, ids
+
+
+def _init_dist():
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        dist.init_process_group(backend="nccl")
+    return dist
+
+
+def train_blocked_distributed(d, cfg, *, early_stop: bool = True, options=None,
+                              timing: bool = True):
+    """Multi-GPU train_blocked (fixed inner schedules): every rank calls it with
+    the same dataset and config; rank r uses GPU LOCAL_RANK.  Returns
+    (FactorModel on every rank, ConvergenceTrace, stop_reason)."""
+    import torch
+
+    from .core import (ConvergenceTrace, DivergenceError, FactorModel, TraceStep,
+                       init_factors)
+    from .kernel import divergence
+    from .metrics import RmseAccumulator, finalize, merge
+    from .trainer import resolve_inner_iters
+
+    dist = _init_dist()
+    rank, world = dist.get_rank(), dist.get_world_size()
+    device = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(device)
+    sched = RingSchedule(cfg.grid_i, cfg.grid_j, world)
+    shard = GpuShard(d, cfg, sched, rank, device, options)
+    model0 = init_factors(d.n, d.m, cfg.k, cfg.seed)
+    shard.set_factors(model0.u, model0.v)
+    nb = cfg.grid_i * cfg.grid_j
+    trace = ConvergenceTrace()
+    stop = "max_steps"
+    total_counts = np.zeros(nb, np.int64)
+    cnt = torch.tensor(shard.counts, dtype=torch.int64, device=f"cuda:{device}")
+    dist.all_reduce(cnt)
+    total_counts[:] = cnt.cpu().numpy()
+    for step in range(1, cfg.outer_steps + 1):
+        g = resolve_inner_iters(cfg.inner_schedule, step, 1.0)
+        if g is None:
+            raise NotImplementedError("converge schedules are single-GPU (train_blocked)")
+        t0 = time.perf_counter()
+        sse_all, order, bad_any = run_epoch(sched, shard, rank, dist, step - 1, g, cfg.alpha,
+                                            cfg.beta, nb, cfg.grid_j)
+        red = torch.tensor(sse_all, device=f"cuda:{device}")
+        dist.all_reduce(red)
+        sse_all = red.cpu().numpy()
+        flag = torch.tensor([0 if bad_any is None else 1], device=f"cuda:{device}")
+        dist.all_reduce(flag)
+        if int(flag.item()) or not np.all(np.isfinite(sse_all[order])):
+            b = bad_any[0] if bad_any else int(next(o for o in order
+                                                    if not math.isfinite(sse_all[o])))
+            err = divergence(b // cfg.grid_j, b % cfg.grid_j,
+                             bad_any[1] if bad_any else int(total_counts[b]) - 1,
+                             bad_any[2] if bad_any else g - 1)
+            err.step = step
+            err.partial_trace = trace
+            raise err
+        acc = RmseAccumulator()
+        for b in order:
+            acc = merge(acc, RmseAccumulator(float(sse_all[b]), int(total_counts[b])))
+        train_rmse = finalize(acc)
+        trace.append(TraceStep(step, train_rmse, None,
+                               time.perf_counter() - t0 if timing else 0.0, g, 0))
+        if early_stop:
+            if acc.count == 0:
+                stop = "converged"
+                break
+            if len(trace) >= 2 and trace.steps[-2].train_rmse - train_rmse < cfg.delta:
+                stop = "converged"
+                break
+    # gather the model: V from its holders, U row slabs from their owners
+    sync_all_v(sched, rank, shard.v_slice, dist)
+    for r in range(world):
+        rows = sched.rows_of(r)
+        if len(rows):
+            dist.broadcast(shard.u_rows(rows), src=r)
+    torch.cuda.synchronize()
+    u, v = shard.eng.get_factors()
+    return FactorModel(u, v), trace, stop
+
+
+def bench_main(args):
+    """bench.py --gpus N under torchrun: strong scaling of the C4 epoch."""
+    import json
+
+    import torch
+
+    from . import workloads
+    from .core import RatingsDataset, TrainConfig, init_factors
+    from .device import EngineOptions
+
+    dist = _init_dist()
+    rank, world = dist.get_rank(), dist.get_world_size()
+    device = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(device)
+    w = workloads.CONFIGS[args.config]
+    t_gen = time.perf_counter()
+    if args.config == "C1":
+        r, c, v = workloads.ml100k_standin()
+    else:
+        r, c, v = workloads.lowrank(w.n, w.m, args.nnz or w.nnz, seed=w.seed)
+    t_gen = time.perf_counter() - t_gen
+    d = RatingsDataset(w.n, w.m, r, c, v)
+    nnz = len(d)
+    cfg = TrainConfig(k=w.k, alpha=w.alpha, beta=w.beta, grid_i=w.grid, grid_j=w.grid,
+                      seed=w.seed)
+    sched = RingSchedule(w.grid, w.grid, world)
+    shard = GpuShard(d, cfg, sched, rank, device, EngineOptions(timing=False))
+    del r, c, v
+    m0 = init_factors(w.n, w.m, w.k, w.seed)
+    shard.set_factors(m0.u, m0.v)
+    del m0
+    stream = shard.stream
+
+    def epoch(step0):
+        run_epoch(sched, shard, rank, dist, step0, 1, w.alpha, w.beta, w.grid * w.grid, w.grid)
+
+    step = 0
+    for _ in range(args.warmup):
+        epoch(step % w.grid)
+        step += 1
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        epoch(step % w.grid)
+        step += 1
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{device}")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    total_ms = float(ms.item())
+    if rank == 0:
+        line = {
+            "metric": "SGD rating-updates/sec (epoch)", "value": nnz * args.steps / (total_ms / 1e3),
+            "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (workloads.lowrank)",
+            "config": {"workload": w.description, "n": w.n, "m": w.m, "nnz": nnz, "k": w.k,
+                       "grid": f"{w.grid}x{w.grid}",
+                       "parallelism": f"U-resident/V-rotating x{world} (NCCL P2P)",
+                       "l2": "inputs larger than L2"},
+            "e2e": None, "gen_seconds": t_gen,
+        }
+        print(json.dumps(line))
+    dist.destroy_process_group()

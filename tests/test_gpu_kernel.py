@@ -129,7 +129,7 @@ def test_slices_alias_the_model(dense32):
     blocked = bm.partition(dense32, 4, 4)
     model = bm.init_factors(32, 32, 2, seed=0)
     block = blocked.block(2, 3)
-    task = bm.task_from_block(block, model, 0.1, 0.0, 1)
+    task = bm.task_from_block(block, model, 1e-4, 0.0, 1)
     before = model.u.copy()
     bm.sgd_block(task)
     assert not np.array_equal(model.u, before)
