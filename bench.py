@@ -218,7 +218,8 @@ def run_ours(args):
     # ---- device-resident epochs
     stream = torch.cuda.current_stream()
     # the engine launches on torch's current stream so torch events bracket the work
-    eng2 = bm.Engine(bm.EngineOptions(device=dev, fused=not args.unfused),
+    fused = True if args.fused else (False if args.unfused else None)
+    eng2 = bm.Engine(bm.EngineOptions(device=dev, fused=fused),
                      stream=stream.cuda_stream)
     eng2.partition(d.rows, d.cols, d.values, w.n, w.m, w.grid, w.grid)
     m0 = bm.init_factors(w.n, w.m, w.k, w.seed)
@@ -280,8 +281,8 @@ def run_ours(args):
                         "init upload, K epochs, D2H model"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": None, "peak_kind": hbm_kind,
-                     "kernel": ("sgd_fast_kernel<32,1>" if args.unfused else
-                                "epoch_fast_kernel<32,1> (sweeps + SSE, fused)"),
+                     "kernel": ("epoch_fast_kernel (sweeps + SSE fused)" if args.fused else
+                                "sgd_fast_kernel<8,4> (stratum sweep)"),
                      "alg_bytes_per_launch": alg_per_launch, "avg_launch_ms": sgd_launch_ms,
                      "sgd_share_of_step": st["sgd_ms"] / total_ms,
                      "sse_ms_per_step": st["sse_ms"] / args.steps},
@@ -304,7 +305,9 @@ def main():
     ap.add_argument("--nnz", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--unfused", action="store_true",
-                    help="one launch per stratum sweep / SSE pass (default: one per epoch)")
+                    help="force one launch per stratum sweep / SSE pass")
+    ap.add_argument("--fused", action="store_true",
+                    help="force one cooperative launch per epoch (default: auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-batches", type=int, default=None,
                     help="strata per CPU sample (default: the whole epoch)")

@@ -53,9 +53,12 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      (bounds per-block concurrency on small blocks; 256).
  *   "timing"     0/1   record CUDA events around every kernel launch.
  *   "warps_per_sm" int resident-warp target used to size chunks (0 = occupancy).
- *   "fused"      0/1   1 = one cooperative launch per outer step (all strata,
- *                      sweeps and SSE passes separated by grid barriers;
- *                      default); 0 = one launch per stratum sweep / SSE pass. */
+ *   "fused"      -1/0/1  1 = one cooperative launch per outer step (all
+ *                      strata, sweeps and SSE passes separated by grid
+ *                      barriers); 0 = one launch per stratum sweep / SSE pass;
+ *                      -1 = auto (default): fused when a stratum holds at most
+ *                      "fused_max_batch" ratings (2^21), i.e. when launches
+ *                      dominate. */
 int bgmf_set_option(bgmf_ctx* ctx, const char* key, double value);
 
 /* Bucket the ratings into the I x J block grid on the GPU.
@@ -122,6 +125,16 @@ int bgmf_holdout_set(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                      const double* vals, const uint8_t* cold, int64_t count,
                      double fallback);
 int bgmf_holdout_sse(bgmf_ctx* ctx, double* sse_out);
+
+/* Out-of-core mode (C5; PAPER.md:190,196,294 -- data larger than HBM): move the
+ * partitioned ratings to pinned host memory and keep only `nslots` device
+ * slots of `slot_ratings` ratings each (12 B per rating).  Every later
+ * bgmf_run_step streams each stratum's blocks through the slot ring on a side
+ * stream while the previous piece computes; factors stay resident.  A slot
+ * must hold the largest block.  Fast mode, fixed schedules. */
+int bgmf_stream_ratings(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
+/* Rating bytes streamed host->device since the context was created. */
+int bgmf_stream_stats(bgmf_ctx* ctx, double* h2d_bytes);
 
 /* Accumulated kernel time since the last reset (requires "timing"=1):
  * out[0] sgd ms, out[1] sse ms, out[2] sgd launches, out[3] sse launches,

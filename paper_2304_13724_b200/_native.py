@@ -52,6 +52,8 @@ SIGNATURES = {
     "bgmf_holdout_set": (_i, [_ctx, _i64p, _i64p, _f64p, _u8p, _l, _d]),
     "bgmf_holdout_sse": (_i, [_ctx, _f64p]),
     "bgmf_kernel_stats": (_i, [_ctx, _f64p, _i]),
+    "bgmf_stream_ratings": (_i, [_ctx, _l, _i]),
+    "bgmf_stream_stats": (_i, [_ctx, _f64p]),
     "bgmf_sgd_sweeps": (_i, [_i64p, _i64p, _f64p, _l, _f64p, _l, _f64p, _l, _i, _d, _d, _i,
                              _f64p, _f64p, _i64p, _i64p]),
     "bgmf_sgd_converge": (_i, [_i64p, _i64p, _f64p, _l, _f64p, _l, _f64p, _l, _i, _d, _d, _d,

@@ -55,7 +55,8 @@ struct bgmf_ctx {
   int min_chunk = 256;
   bool timing = false;
   int warps_per_sm = 0;
-  bool fused = true;   // one cooperative launch per outer step
+  int fused = -1;      // 1: one cooperative launch per step, 0: per stratum, -1 auto
+  int64_t fused_max_batch = 1 << 21;  // auto: fuse when a stratum has <= 2M ratings
 
   // grid + partition
   int64_t n = 0, m = 0, nnz = 0;
@@ -96,6 +97,20 @@ struct bgmf_ctx {
   double* d_partials = nullptr;          // eval partial sums
   double* h_scalar = nullptr;            // pinned
 
+  // out-of-core streaming (stream.cu)
+  bool streaming = false;
+  int nslots = 0;
+  int64_t slot_cap = 0;                  // ratings per device slot
+  int32_t* h_lrow = nullptr;             // pinned, partitioned order
+  int32_t* h_lcol = nullptr;
+  float* h_val = nullptr;
+  uint32_t* h_order = nullptr;
+  std::vector<int32_t*> s_lrow, s_lcol;  // device slots
+  std::vector<float*> s_val;
+  std::vector<cudaEvent_t> ev_copied, ev_consumed;
+  cudaStream_t copy_stream = nullptr;
+  double h2d_bytes = 0;                  // streamed this context (stats)
+
   // timing
   std::vector<bgmf::TimedLaunch> events;
   size_t events_used = 0;
@@ -133,6 +148,16 @@ int run_step_converge_fast(bgmf_ctx* ctx, const int32_t* plan, const int32_t* ba
 int train_sse_fast(bgmf_ctx* ctx, double* out);
 int train_sse_exact(bgmf_ctx* ctx, double* out);
 int ensure_step_scratch(bgmf_ctx* ctx, size_t nwork);
+int64_t fast_groups(bgmf_ctx* ctx);
+int launch_piece(bgmf_ctx* ctx, const BlockWork* d_work, int nwork, int chunks,
+                 const int32_t* lrow, const int32_t* lcol, const float* val, int iters,
+                 float alpha, float beta, double ratings);
+
+// stream.cu -- out-of-core: ratings in pinned host memory, device slot ring
+int stream_enable(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
+void stream_free(bgmf_ctx* ctx);
+int run_step_stream(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off, int nbatch,
+                    int iters, float alpha, float beta);
 // single-block exact kernel used by the stateless drop-ins
 int block_exact(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const double* vals,
                 int64_t count, double* u, int64_t u_rows, double* v, int64_t v_rows, int k,

@@ -216,6 +216,7 @@ void bgmf_destroy(bgmf_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_factors(c);
   free_holdout(c);
+  stream_free(c);
   cudaFree(c->d_lrow); cudaFree(c->d_lcol); cudaFree(c->d_val); cudaFree(c->d_val64);
   cudaFree(c->d_order); cudaFree(c->d_sse); cudaFree(c->d_bad); cudaFree(c->d_work);
   cudaFree(c->d_partials);
@@ -235,7 +236,8 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "min_chunk")) c->min_chunk = value < 1 ? 1 : (int)value;
   else if (!strcmp(key, "timing")) c->timing = value != 0.0;
   else if (!strcmp(key, "warps_per_sm")) c->warps_per_sm = value < 0 ? 0 : (int)value;
-  else if (!strcmp(key, "fused")) c->fused = value != 0.0;
+  else if (!strcmp(key, "fused")) c->fused = value < 0 ? -1 : (value != 0.0 ? 1 : 0);
+  else if (!strcmp(key, "fused_max_batch")) c->fused_max_batch = (int64_t)value;
   else return fail(c, BGMF_ERR_ARG, std::string("unknown option ") + key);
   return BGMF_OK;
 }
@@ -244,6 +246,7 @@ int bgmf_partition(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const 
                    int64_t nnz, int64_t n, int64_t m, int grid_i, int grid_j) {
   if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
   cudaSetDevice(c->device);
+  if (c->streaming) stream_free(c);
   // the step scratch is sized by the grid
   cudaFree(c->d_sse); cudaFreeHost(c->h_sse); cudaFree(c->d_bad); cudaFreeHost(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
@@ -258,6 +261,13 @@ int bgmf_partition_export(bgmf_ctx* c, int64_t* offsets, int64_t* order, int32_t
   if (offsets) memcpy(offsets, c->h_offsets.data(), c->h_offsets.size() * 8);
   const int64_t n = c->nnz;
   if (n == 0) return BGMF_OK;
+  if (c->streaming) {  // the ratings live in pinned host memory
+    if (lrows) memcpy(lrows, c->h_lrow, n * 4);
+    if (lcols) memcpy(lcols, c->h_lcol, n * 4);
+    if (order)
+      for (int64_t i = 0; i < n; ++i) order[i] = (int64_t)c->h_order[i];
+    return BGMF_OK;
+  }
   if (lrows) BGMF_CK(c, cudaMemcpyAsync(lrows, c->d_lrow, n * 4, cudaMemcpyDeviceToHost, c->stream));
   if (lcols) BGMF_CK(c, cudaMemcpyAsync(lcols, c->d_lcol, n * 4, cudaMemcpyDeviceToHost, c->stream));
   if (order) {
@@ -345,8 +355,12 @@ int bgmf_run_step(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, in
   int rc = check_step_ready(c);
   if (rc) return rc;
   cudaSetDevice(c->device);
-  rc = c->exact ? run_step_exact(c, plan, batch_off, nbatch, inner_iters, alpha, beta)
-                : run_step_fast(c, plan, batch_off, nbatch, inner_iters, (float)alpha, (float)beta);
+  if (c->exact)
+    rc = run_step_exact(c, plan, batch_off, nbatch, inner_iters, alpha, beta);
+  else if (c->streaming)
+    rc = run_step_stream(c, plan, batch_off, nbatch, inner_iters, (float)alpha, (float)beta);
+  else
+    rc = run_step_fast(c, plan, batch_off, nbatch, inner_iters, (float)alpha, (float)beta);
   if (rc) return rc;
   const int nb = c->I * c->J;
   for (int b = 0; b < nb; ++b) sse_out[b] = c->h_sse[b];
@@ -365,6 +379,8 @@ int bgmf_run_step_converge(bgmf_ctx* c, const int32_t* plan, const int32_t* batc
   int rc = check_step_ready(c);
   if (rc) return rc;
   cudaSetDevice(c->device);
+  if (c->streaming)
+    return fail(c, BGMF_ERR_STATE, "converge schedules are not supported while streaming");
   rc = c->exact ? run_step_converge_exact(c, plan, batch_off, nbatch, tol, cap, alpha, beta,
                                           iters_out, capped_out)
                 : run_step_converge_fast(c, plan, batch_off, nbatch, tol, cap, alpha, beta,
@@ -383,6 +399,17 @@ int bgmf_train_sse(bgmf_ctx* c, double* sse_out) {
   cudaSetDevice(c->device);
   rc = ensure_step_scratch(c, 1);
   if (rc) return rc;
+  if (c->streaming) {  // zero sweeps: every block's SSE of the current factors
+    const int nb = c->I * c->J;
+    std::vector<int32_t> plan(nb), off{0, nb};
+    for (int b = 0; b < nb; ++b) plan[b] = b;
+    rc = run_step_stream(c, plan.data(), off.data(), 1, 0, 0.f, 0.f);
+    if (rc) return rc;
+    double acc = 0.0;
+    for (int b = 0; b < nb; ++b) acc += c->h_sse[b];
+    *sse_out = acc;
+    return BGMF_OK;
+  }
   return c->exact ? train_sse_exact(c, sse_out) : train_sse_fast(c, sse_out);
 }
 
@@ -433,6 +460,18 @@ int bgmf_holdout_sse(bgmf_ctx* c, double* sse_out) {
                         c->hfallback, c->hcount, sse_out);
   return eval_sse_f32(c, c->d_hrow, c->d_hcol, c->d_hval, c->d_hcold, c->hfallback, c->hcount,
                       sse_out);
+}
+
+int bgmf_stream_ratings(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  cudaSetDevice(c->device);
+  return stream_enable(c, slot_ratings, nslots);
+}
+
+int bgmf_stream_stats(bgmf_ctx* c, double* h2d_bytes) {
+  if (!c || !h2d_bytes) return fail(c, BGMF_ERR_ARG, "NULL argument");
+  *h2d_bytes = c->h2d_bytes;
+  return BGMF_OK;
 }
 
 int bgmf_kernel_stats(bgmf_ctx* c, double* out5, int reset) {

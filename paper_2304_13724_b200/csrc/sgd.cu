@@ -298,6 +298,28 @@ sse_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
   if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
 }
 
+// Out-of-line copies of the two walks for the persistent kernel: register
+// allocation is then per phase (no spills from keeping both live), and the
+// call costs once per chunk.
+template <int L, int V4>
+__device__ __noinline__ void sweep_chunk(const Chunk& ch, int maxlen,
+                                         const int32_t* __restrict__ lrow,
+                                         const int32_t* __restrict__ lcol,
+                                         const float* __restrict__ val, float* U, float* V,
+                                         int kp, float alpha, float beta, int iter,
+                                         unsigned long long* bad) {
+  walk_chunk<L, V4, true>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter, bad);
+}
+
+template <int L, int V4>
+__device__ __noinline__ double sse_chunk(const Chunk& ch, int maxlen,
+                                         const int32_t* __restrict__ lrow,
+                                         const int32_t* __restrict__ lcol,
+                                         const float* __restrict__ val, float* U, float* V,
+                                         int kp) {
+  return walk_chunk<L, V4, false>(ch, maxlen, lrow, lcol, val, U, V, kp, 0.f, 0.f, 0, nullptr);
+}
+
 // Whole outer step in one cooperative launch: for every batch, `iters`
 // sweeps, then the per-block SSE, separated by grid-wide barriers (a stratum
 // must finish before its SSE, and the SSE before the next stratum touches the
@@ -326,7 +348,7 @@ epoch_fast_kernel(const BlockWork* __restrict__ work, const BatchDesc* __restric
         const Chunk ch = locate_chunk(w, bd.nw, bd.chunks, base + lane / L);
         const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
         if (maxlen > 0)
-          walk_chunk<L, V4, true>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, it, bad);
+          sweep_chunk<L, V4>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, it, bad);
       }
       grid.sync();
     }
@@ -335,8 +357,7 @@ epoch_fast_kernel(const BlockWork* __restrict__ work, const BatchDesc* __restric
       const int len = (int)(ch.end - ch.begin);
       const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
       if (maxlen == 0) continue;
-      const double acc =
-          walk_chunk<L, V4, false>(ch, maxlen, lrow, lcol, val, U, V, kp, 0.f, 0.f, 0, nullptr);
+      const double acc = sse_chunk<L, V4>(ch, maxlen, lrow, lcol, val, U, V, kp);
       if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
     }
     if (t + 1 < nbatch) grid.sync();
@@ -453,21 +474,27 @@ Shape shape_for(int kp) {
 
 #define BGMF_SHAPES(X) X(1, 1) X(1, 2) X(1, 4) X(2, 4) X(4, 4) X(8, 4) X(16, 4) X(32, 4)
 
-void launch_fast(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, const BlockWork* w,
-                 int nwork, int total, bgmf_ctx* c, float a, float b, int it) {
+void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, const BlockWork* w,
+                     int nwork, int total, const int32_t* lrow, const int32_t* lcol,
+                     const float* val, bgmf_ctx* c, float a, float b, int it) {
 #define BGMF_CASE(LL, VV)                                                                     \
   if (sh.L == LL && sh.V4 == VV) {                                                            \
     if (sweep)                                                                                \
-      sgd_fast_kernel<LL, VV><<<grid, 256, 0, s>>>(w, nwork, total, c->d_lrow, c->d_lcol,     \
-                                                   c->d_val, c->d_u, c->d_v, c->kp, a, b, it, \
-                                                   c->d_bad);                                 \
+      sgd_fast_kernel<LL, VV><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val, c->d_u,  \
+                                                   c->d_v, c->kp, a, b, it, c->d_bad);        \
     else                                                                                      \
-      sse_fast_kernel<LL, VV><<<grid, 256, 0, s>>>(w, nwork, total, c->d_lrow, c->d_lcol,     \
-                                                   c->d_val, c->d_u, c->d_v, c->kp, c->d_sse); \
+      sse_fast_kernel<LL, VV><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val, c->d_u,  \
+                                                   c->d_v, c->kp, c->d_sse);                  \
     return;                                                                                   \
   }
   BGMF_SHAPES(BGMF_CASE)
 #undef BGMF_CASE
+}
+
+void launch_fast(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, const BlockWork* w,
+                 int nwork, int total, bgmf_ctx* c, float a, float b, int it) {
+  launch_fast_ptr(sweep, sh, grid, s, w, nwork, total, c->d_lrow, c->d_lcol, c->d_val, c, a, b,
+                  it);
 }
 
 const void* epoch_kernel_ptr(const Shape& sh) {
@@ -592,7 +619,11 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, in
   const int gpw = 32 / sh.L;
   const int nb = c->I * c->J;
   const void* ep = epoch_kernel_ptr(sh);
-  const int ctas_per_sm = c->fused ? resident_ctas(c, ep) : resident_ctas(c, sweep_kernel_ptr(sh));
+  // fused = -1 (auto): the persistent kernel pays off when launches dominate
+  // (small strata); big strata run faster as separate sweep / SSE launches.
+  const int64_t per_batch = nbatch > 0 ? c->nnz / nbatch : c->nnz;
+  const bool fused = c->fused > 0 || (c->fused < 0 && per_batch <= c->fused_max_batch);
+  const int ctas_per_sm = fused ? resident_ctas(c, ep) : resident_ctas(c, sweep_kernel_ptr(sh));
   const int64_t groups = (int64_t)c->num_sms * ctas_per_sm * 8 * gpw;
   std::vector<BatchRange> ranges;
   int rc = build_work(c, plan, batch_off, nbatch, groups, ranges);
@@ -612,7 +643,7 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, in
                                cudaMemcpyHostToDevice, s));
   BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, s));
   BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
-  if (c->fused && max_chunks > 0) {
+  if (fused && max_chunks > 0) {
     BGMF_CK(c, cudaMemcpyAsync(bdesc, hb.data(), sizeof(BatchDesc) * nbatch,
                                cudaMemcpyHostToDevice, s));
     const int need = (max_chunks + gpw * 8 - 1) / (gpw * 8);
@@ -660,6 +691,34 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, in
   BGMF_CK(c, cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, s));
   BGMF_CK(c, cudaStreamSynchronize(s));
   if (c->timing) harvest_timing(c);
+  return BGMF_OK;
+}
+
+int64_t fast_groups(bgmf_ctx* c) { return sweep_groups(c, shape_for(c->kp)); }
+
+// Sweeps (`iters` launches) + SSE launch for one piece of a batch whose
+// ratings live at (lrow, lcol, val) -- the streaming path's unit of work.
+int launch_piece(bgmf_ctx* c, const BlockWork* d_work, int nwork, int chunks,
+                 const int32_t* lrow, const int32_t* lcol, const float* val, int iters,
+                 float alpha, float beta, double ratings) {
+  if (chunks == 0) return BGMF_OK;
+  const Shape sh = shape_for(c->kp);
+  const int gpw = 32 / sh.L;
+  const int warps = (chunks + gpw - 1) / gpw;
+  const dim3 grid((warps + 7) / 8);
+  for (int it = 0; it < iters; ++it) {
+    TimedLaunch* slot = nullptr;
+    if (c->timing) record_begin(c, 0, ratings * (12.0 + 16.0 * c->k), &slot);
+    launch_fast_ptr(true, sh, grid, c->stream, d_work, nwork, chunks, lrow, lcol, val, c, alpha,
+                    beta, it);
+    if (slot) record_end(c, slot);
+  }
+  TimedLaunch* slot = nullptr;
+  if (c->timing) record_begin(c, 1, 0.0, &slot);
+  launch_fast_ptr(false, sh, grid, c->stream, d_work, nwork, chunks, lrow, lcol, val, c, alpha,
+                  beta, 0);
+  if (slot) record_end(c, slot);
+  BGMF_CK(c, cudaGetLastError());
   return BGMF_OK;
 }
 
@@ -758,6 +817,8 @@ int run_step_converge_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batc
   std::vector<double> sse_final(nb, 0.0);
   for (int b = 0; b < nb; ++b) { iters_out[b] = 0; capped_out[b] = 0; }
   unsigned long long best = kNoBad;
+  int rc0 = ensure_step_scratch(c, (size_t)batch_off[nbatch]);
+  if (rc0) return rc0;
   BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
   const int gpw = 32 / sh.L;
   for (int t = 0; t < nbatch; ++t) {

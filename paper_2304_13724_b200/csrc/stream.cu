@@ -1,0 +1,205 @@
+// stream.cu -- out-of-core epoch: the partitioned ratings live in pinned host
+// memory and stream through a ring of device slots (the
+// paper's motivating case).  Factors stay resident.
+//
+// A step is cut into "pieces": consecutive blocks of one batch whose ratings
+// fit one slot.  Blocks of a batch own disjoint U/V slices, so any grouping
+// of a batch's blocks into sequential pieces is the same algorithm, and a
+// block's post-sweep SSE can run right after its own sweep.  Piece p uses slot
+// p % nslots: a side stream copies piece p+1.. (H2D from pinned memory, one
+// memcpy per block and array) while the compute stream sweeps piece p;
+// events order "slot copied" -> "sweep" -> "slot free for the next copy".
+
+#include <cstring>
+
+#include "bgmf_internal.cuh"
+
+namespace bgmf {
+
+void stream_free(bgmf_ctx* c) {
+  for (auto p : c->s_lrow) cudaFree(p);
+  for (auto p : c->s_lcol) cudaFree(p);
+  for (auto p : c->s_val) cudaFree(p);
+  for (auto e : c->ev_copied) cudaEventDestroy(e);
+  for (auto e : c->ev_consumed) cudaEventDestroy(e);
+  c->s_lrow.clear(); c->s_lcol.clear(); c->s_val.clear();
+  c->ev_copied.clear(); c->ev_consumed.clear();
+  if (c->h_lrow) cudaFreeHost(c->h_lrow);
+  if (c->h_lcol) cudaFreeHost(c->h_lcol);
+  if (c->h_val) cudaFreeHost(c->h_val);
+  if (c->h_order) cudaFreeHost(c->h_order);
+  c->h_lrow = c->h_lcol = nullptr;
+  c->h_val = nullptr;
+  c->h_order = nullptr;
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  c->copy_stream = nullptr;
+  c->streaming = false;
+  c->nslots = 0;
+  c->slot_cap = 0;
+}
+
+int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
+  if (!c->partitioned) return fail(c, BGMF_ERR_STATE, "bgmf_partition has not been called");
+  if (c->exact) return fail(c, BGMF_ERR_STATE, "streaming is fast-mode only");
+  if (c->streaming) return fail(c, BGMF_ERR_STATE, "already streaming");
+  if (nslots < 2 || nslots > 8) return fail(c, BGMF_ERR_ARG, "nslots must be in [2, 8]");
+  int64_t max_block = 0;
+  for (size_t b = 0; b + 1 < c->h_offsets.size(); ++b) {
+    const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
+    if (cnt > max_block) max_block = cnt;
+  }
+  if (slot_ratings < max_block || slot_ratings < 1)
+    return fail(c, BGMF_ERR_ARG, "slot smaller than the largest block (" +
+                                     std::to_string(max_block) + " ratings)");
+  const size_t N = (size_t)(c->nnz > 0 ? c->nnz : 1);
+  cudaStream_t s = c->stream;
+  BGMF_CK(c, cudaMallocHost(&c->h_lrow, N * 4));
+  BGMF_CK(c, cudaMallocHost(&c->h_lcol, N * 4));
+  BGMF_CK(c, cudaMallocHost(&c->h_val, N * 4));
+  BGMF_CK(c, cudaMallocHost(&c->h_order, N * 4));
+  if (c->nnz > 0) {
+    BGMF_CK(c, cudaMemcpyAsync(c->h_lrow, c->d_lrow, c->nnz * 4, cudaMemcpyDeviceToHost, s));
+    BGMF_CK(c, cudaMemcpyAsync(c->h_lcol, c->d_lcol, c->nnz * 4, cudaMemcpyDeviceToHost, s));
+    BGMF_CK(c, cudaMemcpyAsync(c->h_val, c->d_val, c->nnz * 4, cudaMemcpyDeviceToHost, s));
+    BGMF_CK(c, cudaMemcpyAsync(c->h_order, c->d_order, c->nnz * 4, cudaMemcpyDeviceToHost, s));
+  }
+  BGMF_CK(c, cudaStreamSynchronize(s));
+  cudaFree(c->d_lrow); cudaFree(c->d_lcol); cudaFree(c->d_val); cudaFree(c->d_order);
+  c->d_lrow = c->d_lcol = nullptr;
+  c->d_val = nullptr;
+  c->d_order = nullptr;
+  c->slot_cap = slot_ratings;
+  c->nslots = nslots;
+  for (int i = 0; i < nslots; ++i) {
+    int32_t *a = nullptr, *b = nullptr;
+    float* v = nullptr;
+    BGMF_CK(c, cudaMalloc(&a, (size_t)slot_ratings * 4));
+    BGMF_CK(c, cudaMalloc(&b, (size_t)slot_ratings * 4));
+    BGMF_CK(c, cudaMalloc(&v, (size_t)slot_ratings * 4));
+    c->s_lrow.push_back(a);
+    c->s_lcol.push_back(b);
+    c->s_val.push_back(v);
+    cudaEvent_t e1, e2;
+    BGMF_CK(c, cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    BGMF_CK(c, cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+    c->ev_copied.push_back(e1);
+    c->ev_consumed.push_back(e2);
+  }
+  BGMF_CK(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  c->streaming = true;
+  return BGMF_OK;
+}
+
+namespace {
+
+struct Piece {
+  int w0, nw, chunks;  // work-table range
+  int slot;
+  double ratings;
+};
+
+}  // namespace
+
+int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
+                    int iters, float alpha, float beta) {
+  cudaStream_t s = c->stream, cs = c->copy_stream;
+  const int nb = c->I * c->J;
+  const int64_t groups = fast_groups(c);
+  const int total = batch_off[nbatch];
+  int rc = ensure_step_scratch(c, (size_t)total);
+  if (rc) return rc;
+
+  // 1. cut every batch into pieces that fit a slot; slot-relative work items
+  std::vector<Piece> pieces;
+  std::vector<int> piece_first_q;  // first plan position of each piece
+  int w = 0;
+  for (int t = 0; t < nbatch; ++t) {
+    int q = batch_off[t];
+    while (q < batch_off[t + 1]) {
+      // greedy: take blocks while they fit
+      int q_end = q;
+      int64_t fill = 0, piece_nnz = 0;
+      int nonempty = 0;
+      while (q_end < batch_off[t + 1]) {
+        const int b = plan[q_end];
+        if (b < 0 || b >= nb) return fail(c, BGMF_ERR_ARG, "plan block id out of range");
+        const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
+        if (fill + cnt > c->slot_cap) break;
+        fill += cnt;
+        nonempty += cnt > 0;
+        ++q_end;
+      }
+      piece_nnz = fill;
+      const int64_t slots = groups - nonempty > 0 ? groups - nonempty : 1;
+      int64_t cl = (piece_nnz + slots - 1) / slots;
+      if (cl < c->min_chunk) cl = c->min_chunk;
+      Piece pc{w, 0, 0, (int)(pieces.size() % c->nslots), 0.0};
+      int64_t off = 0;
+      for (int qq = q; qq < q_end; ++qq) {
+        const int b = plan[qq];
+        const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
+        if (cnt == 0) continue;
+        const int64_t bl = cl < cnt ? cl : cnt;
+        BlockWork& bw = c->h_work[w++];
+        bw.begin = off;
+        bw.end = off + cnt;
+        bw.row_start = c->row_bounds[b / c->J];
+        bw.col_start = c->col_bounds[b % c->J];
+        bw.chunk_len = (int32_t)bl;
+        bw.first_chunk = pc.chunks;
+        bw.block_id = b;
+        bw.pos = qq;
+        pc.chunks += (int)((cnt + bl - 1) / bl);
+        pc.ratings += (double)cnt;
+        off += cnt;
+      }
+      pc.nw = w - pc.w0;
+      pieces.push_back(pc);
+      piece_first_q.push_back(q);
+      q = q_end;
+    }
+  }
+  if (w > 0)
+    BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * w,
+                               cudaMemcpyHostToDevice, s));
+  BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, s));
+  BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+  // the copy stream must not overwrite a slot before the work table is in place
+  cudaEvent_t ready;
+  BGMF_CK(c, cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  BGMF_CK(c, cudaEventRecord(ready, s));
+  BGMF_CK(c, cudaStreamWaitEvent(cs, ready, 0));
+
+  // 2. pipeline: copy piece p on the side stream, compute it on the main one
+  for (size_t p = 0; p < pieces.size(); ++p) {
+    const Piece& pc = pieces[p];
+    const int sl = pc.slot;
+    if (p >= (size_t)c->nslots) BGMF_CK(c, cudaStreamWaitEvent(cs, c->ev_consumed[sl], 0));
+    for (int i = 0; i < pc.nw; ++i) {
+      const BlockWork& bw = c->h_work[pc.w0 + i];
+      const int64_t src = c->h_offsets[bw.block_id];
+      const int64_t cnt = bw.end - bw.begin;
+      BGMF_CK(c, cudaMemcpyAsync(c->s_lrow[sl] + bw.begin, c->h_lrow + src, cnt * 4,
+                                 cudaMemcpyHostToDevice, cs));
+      BGMF_CK(c, cudaMemcpyAsync(c->s_lcol[sl] + bw.begin, c->h_lcol + src, cnt * 4,
+                                 cudaMemcpyHostToDevice, cs));
+      BGMF_CK(c, cudaMemcpyAsync(c->s_val[sl] + bw.begin, c->h_val + src, cnt * 4,
+                                 cudaMemcpyHostToDevice, cs));
+      c->h2d_bytes += 12.0 * (double)cnt;
+    }
+    BGMF_CK(c, cudaEventRecord(c->ev_copied[sl], cs));
+    BGMF_CK(c, cudaStreamWaitEvent(s, c->ev_copied[sl], 0));
+    rc = launch_piece(c, c->d_work + pc.w0, pc.nw, pc.chunks, c->s_lrow[sl], c->s_lcol[sl],
+                      c->s_val[sl], iters, alpha, beta, pc.ratings);
+    if (rc) { cudaEventDestroy(ready); return rc; }
+    BGMF_CK(c, cudaEventRecord(c->ev_consumed[sl], s));
+  }
+  BGMF_CK(c, cudaMemcpyAsync(c->h_sse, c->d_sse, sizeof(double) * nb, cudaMemcpyDeviceToHost, s));
+  BGMF_CK(c, cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, s));
+  BGMF_CK(c, cudaStreamSynchronize(s));
+  cudaEventDestroy(ready);
+  if (c->timing) harvest_timing(c);
+  return BGMF_OK;
+}
+
+}  // namespace bgmf

@@ -34,8 +34,14 @@ class EngineOptions:
                blocks, which keeps the lossless-Hogwild drift far below 1e-3).
     device     CUDA ordinal; default $BGMF_DEVICE, else $LOCAL_RANK, else 0.
     timing     record CUDA events around every kernel launch.
-    fused      one cooperative launch per outer step (default) instead of one
-               launch per stratum sweep / SSE pass.
+    fused      True: one cooperative launch per outer step; False: one launch
+               per stratum sweep / SSE pass; None (default): fused only for
+               small strata (<= 2M ratings), where launch latency dominates.
+    device_rating_budget
+               bytes of HBM the ratings may use (None: all resident).  When
+               the partition is larger, it moves to pinned host memory and
+               every step streams it through ``stream_slots`` device slots
+               (out-of-core mode, 12 B per rating per slot entry).
     """
 
     exact: bool = False
@@ -43,7 +49,9 @@ class EngineOptions:
     device: int | None = None
     timing: bool = False
     warps_per_sm: int = 0
-    fused: bool = True
+    fused: bool | None = None
+    device_rating_budget: int | None = None
+    stream_slots: int = 3
 
 
 def default_device() -> int:
@@ -67,7 +75,8 @@ class Engine:
         self._opt("min_chunk", float(self.options.min_chunk))
         self._opt("timing", 1.0 if self.options.timing else 0.0)
         self._opt("warps_per_sm", float(self.options.warps_per_sm))
-        self._opt("fused", 1.0 if self.options.fused else 0.0)
+        f = self.options.fused
+        self._opt("fused", -1.0 if f is None else (1.0 if f else 0.0))
         self.n = self.m = self.nnz = 0
         self.I = self.J = 0
         self.k = 0
@@ -105,6 +114,21 @@ class Engine:
         off = np.zeros(grid_i * grid_j + 1, np.int64)
         self._check(self._L.bgmf_partition_export(self._h, N.ptr(off, N._i64p), None, None, None))
         self.offsets = off
+        self.streaming = False
+        budget = self.options.device_rating_budget
+        if budget is not None and 12 * self.nnz > budget:
+            slots = self.options.stream_slots
+            self.stream(int(budget // (12 * slots)), slots)
+
+    def stream(self, slot_ratings: int, nslots: int = 3):
+        """Out-of-core mode: ratings to pinned host memory, `nslots` device slots."""
+        self._check(self._L.bgmf_stream_ratings(self._h, int(slot_ratings), int(nslots)))
+        self.streaming = True
+
+    def streamed_bytes(self) -> float:
+        out = ctypes.c_double()
+        self._check(self._L.bgmf_stream_stats(self._h, ctypes.byref(out)))
+        return out.value
 
     def export_partition(self):
         """(offsets, order, local rows, local cols) as int64 host arrays."""

@@ -9,20 +9,28 @@ OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
 lscpu > $OUT/lscpu.txt 2>&1
+free -g > $OUT/free.txt 2>&1
+B="python bench.py"
 for w in $WHAT; do
   case $w in
     smoke) timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" ;;
     tests) timeout 1500 python -m pytest tests -m "gpu and not slow" -q -rA > $OUT/tests_gpu.log 2>&1; echo "tests rc=$?" ;;
     slow) timeout 1500 python -m pytest tests -m "slow" -q -rA -s > $OUT/tests_slow.log 2>&1; echo "slow rc=$?" ;;
-    bench) timeout 900 python bench.py --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" ;;
-    benchu) timeout 900 python bench.py --steps 10 --warmup 3 --unfused --no-e2e --no-cpu-baseline > $OUT/bench_unfused.json 2> $OUT/bench_unfused.err; echo "benchu rc=$?" ;;
-    benchc3) timeout 900 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_c3.json 2> $OUT/bench_c3.err; echo "benchc3 rc=$?" ;;
+    bench) timeout 900 $B --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" ;;
+    benchu) timeout 900 $B --steps 10 --warmup 3 --unfused --no-e2e --no-cpu-baseline > $OUT/bench_unfused.json 2> $OUT/bench_unfused.err; echo "benchu rc=$?" ;;
+    benchf) timeout 900 $B --steps 10 --warmup 3 --fused --no-e2e --no-cpu-baseline > $OUT/bench_fused.json 2> $OUT/bench_fused.err; echo "benchf rc=$?" ;;
+    small)
+      for c in C1 C2 C3; do
+        for f in "" "--fused" "--unfused"; do
+          timeout 600 $B --config $c --steps 20 --warmup 3 $f --no-e2e --no-cpu-baseline >> $OUT/bench_small.jsonl 2>> $OUT/bench_small.err
+        done
+      done; echo "small rc=$?" ;;
     ncu)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-        --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
+        --log-file $OUT/launches.csv $B --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
       echo "ncu-list rc=$?"
-      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"epoch_fast_kernel|sgd_fast_kernel" -s 2 -c 1 \
-        -o $OUT/sgd_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1
+      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"sgd_fast_kernel|sse_fast_kernel|epoch_fast_kernel" -s 4 -c 2 \
+        -o $OUT/sgd_full $B --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1
       echo "ncu-full rc=$?" ;;
   esac
 done

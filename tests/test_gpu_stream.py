@@ -1,0 +1,63 @@
+"""Out-of-core mode: ratings in pinned host memory, streamed
+through a ring of device slots each step.  Same algorithm as the in-core
+path -- checked against the oracle per epoch (1e-3 absolute) with budgets
+that force many pieces per stratum, plus streamed-byte accounting."""
+
+import numpy as np
+import pytest
+
+import paper_2304_13724_b200 as bm
+from oracle import oracle as O
+from paper_2304_13724_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-3
+
+
+def _c2_like(nnz=400_000):
+    r, c, v = workloads.lowrank(6040, 3706, nnz, seed=3)
+    return bm.RatingsDataset(6040, 3706, r, c, v)
+
+
+@pytest.mark.parametrize("budget_frac,slots", [(0.05, 2), (0.2, 3), (0.5, 4)])
+def test_stream_matches_oracle(budget_frac, slots):
+    d = _c2_like()
+    tr, te = bm.split(d, 0.2, seed=0)
+    cfg = bm.TrainConfig(k=32, outer_steps=5, grid_i=8, grid_j=8)
+    opts = bm.EngineOptions(device_rating_budget=int(12 * len(tr) * budget_frac),
+                            stream_slots=slots)
+    blocked = bm.partition(tr, 8, 8, options=opts)
+    assert blocked.engine.streaming
+    res = bm.train_blocked(tr, cfg, te, early_stop=False, timing=False, blocked=blocked)
+    _, _, otr, _ = O.train_blocked(tr.n, tr.m, tr.rows, tr.cols, tr.values, k=32, outer_steps=5,
+                                   grid_i=8, grid_j=8, test=(te.rows, te.cols, te.values),
+                                   early_stop=False, nthreads=8)
+    dtr = np.abs(np.array([s.train_rmse for s in res.trace]) - [s["train_rmse"] for s in otr])
+    dte = np.abs(np.array([s.test_rmse for s in res.trace]) - [s["test_rmse"] for s in otr])
+    assert dtr.max() <= TOL and dte.max() <= TOL
+    # every epoch streams every rating once (+ the adaptive/none extra passes: none here)
+    assert blocked.engine.streamed_bytes() == pytest.approx(12.0 * len(tr) * 5)
+
+
+def test_stream_partition_export_and_sse_only_pass():
+    d = _c2_like(100_000)
+    ref = O.partition(d.rows, d.cols, d.values, d.n, d.m, 4, 4)
+    b = bm.partition(d, 4, 4, options=bm.EngineOptions(device_rating_budget=12 * 40_000))
+    assert b.engine.streaming
+    assert np.array_equal(b._rows, ref["rows"]) and np.array_equal(b._values, ref["values"])
+    # adaptive schedule needs RMSE_0: the zero-sweep streamed SSE pass
+    cfg = bm.TrainConfig(k=16, outer_steps=3, grid_i=4, grid_j=4, alpha=1e-3,
+                         inner_schedule=bm.AdaptiveDecreasing(4))
+    res = bm.train_blocked(d, cfg, early_stop=False, blocked=b)
+    u, v, otr, _ = O.train_blocked(d.n, d.m, d.rows, d.cols, d.values, k=16, outer_steps=3,
+                                   alpha=1e-3, grid_i=4, grid_j=4, schedule="adaptive:4",
+                                   early_stop=False, nthreads=8)
+    assert [s.inner_iters for s in res.trace] == [s["inner_iters"] for s in otr]
+    got = np.array([s.train_rmse for s in res.trace])
+    assert np.abs(got - [s["train_rmse"] for s in otr]).max() <= TOL
+
+
+def test_stream_rejects_slot_smaller_than_a_block():
+    d = _c2_like(50_000)
+    with pytest.raises(ValueError, match="largest block"):
+        bm.partition(d, 2, 2, options=bm.EngineOptions(device_rating_budget=12 * 3000))
