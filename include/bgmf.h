@@ -71,6 +71,18 @@ int bgmf_partition(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                    const double* vals, int64_t nnz, int64_t n, int64_t m,
                    int grid_i, int grid_j);
 
+/* Benchmark / test inputs (not part of the reference path): generate the
+ * synthetic low-rank workload of paper_2304_13724_b200/workloads.py
+ * (Feistel-sampled cells -- identical integers to workloads.feistel_cells --
+ * and counter-based normals for the values) directly on the device and
+ * partition it as bgmf_partition would.  Used for C5 (2e9 ratings), whose
+ * host-side generation is impractical. */
+int bgmf_synth_partition(bgmf_ctx* ctx, int64_t n, int64_t m, int64_t nnz,
+                         uint64_t seed, int grid_i, int grid_j);
+/* Same generator, ratings [start, start+nnz) copied to host arrays. */
+int bgmf_synth(int64_t n, int64_t m, int64_t nnz, int64_t start, uint64_t seed,
+               int64_t* rows, int64_t* cols, double* vals);
+
 /* Copy the partition back (any pointer may be NULL):
  *   offsets[I*J+1]    BlockedDataset._offsets            (partition.py:134-136)
  *   order[nnz]        source index of each sorted entry (values = vals[order],
@@ -86,6 +98,14 @@ int bgmf_set_factors(bgmf_ctx* ctx, const double* u, const double* v,
                      int64_t n, int64_t m, int k);
 /* Download the factors into caller fp64 buffers (n x k, m x k). */
 int bgmf_get_factors(bgmf_ctx* ctx, double* u, double* v);
+
+/* init_factors on the device (core.py:179-193), bit-identical to numpy:
+ * draws of the PCG64 stream whose seeded 128-bit (state, inc) -- numpy's
+ * default_rng(seed).bit_generator.state -- are passed as hi/lo halves;
+ * u = draws[0 : n*k] / sqrt(k), v = the next m*k draws / sqrt(k). */
+int bgmf_init_factors(bgmf_ctx* ctx, uint64_t state_hi, uint64_t state_lo,
+                      uint64_t inc_hi, uint64_t inc_lo, int64_t n, int64_t m,
+                      int k);
 
 /* Use caller-owned device factor buffers (fp32, row stride kp >= k, kp % 4 ==
  * 0, zero padding) instead of context-owned ones -- e.g. torch tensors that

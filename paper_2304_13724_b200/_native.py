@@ -42,8 +42,12 @@ SIGNATURES = {
     "bgmf_set_option": (_i, [_ctx, ctypes.c_char_p, _d]),
     "bgmf_partition": (_i, [_ctx, _i64p, _i64p, _f64p, _l, _l, _l, _i, _i]),
     "bgmf_partition_export": (_i, [_ctx, _i64p, _i64p, _i32p, _i32p]),
+    "bgmf_synth_partition": (_i, [_ctx, _l, _l, _l, ctypes.c_uint64, _i, _i]),
+    "bgmf_synth": (_i, [_l, _l, _l, _l, ctypes.c_uint64, _i64p, _i64p, _f64p]),
     "bgmf_set_factors": (_i, [_ctx, _f64p, _f64p, _l, _l, _i]),
     "bgmf_get_factors": (_i, [_ctx, _f64p, _f64p]),
+    "bgmf_init_factors": (_i, [_ctx, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                               ctypes.c_uint64, _l, _l, _i]),
     "bgmf_bind_factors": (_i, [_ctx, _vp, _vp, _l, _l, _i, _i]),
     "bgmf_run_step": (_i, [_ctx, _i32p, _i32p, _i, _i, _d, _d, _f64p, _i64p]),
     "bgmf_run_step_converge": (_i, [_ctx, _i32p, _i32p, _i, _d, _l, _d, _d, _f64p, _i64p,

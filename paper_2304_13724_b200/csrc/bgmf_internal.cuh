@@ -132,7 +132,12 @@ int cuda_fail(bgmf_ctx* ctx, cudaError_t e, const char* what);
 
 // partition.cu
 int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
-                     const double* vals, int64_t nnz, int64_t n, int64_t m, int I, int J);
+                     const double* vals, int64_t nnz, int64_t n, int64_t m, int I, int J,
+                     bool dev_in = false);
+
+// synth.cu (benchmark / test input generator)
+int synth_lowrank_device(bgmf_ctx* ctx, int64_t n, int64_t m, int64_t nnz, int64_t start,
+                         uint64_t seed, int64_t* rows, int64_t* cols, double* vals);
 
 // sgd.cu
 int run_step_fast(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
@@ -163,6 +168,10 @@ int block_exact(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const d
                 int64_t count, double* u, int64_t u_rows, double* v, int64_t v_rows, int k,
                 double alpha, double beta, int mode, int iters, double tol, int64_t cap,
                 double* out6);
+
+// init.cu
+int init_factors_device(bgmf_ctx* ctx, uint64_t shi, uint64_t slo, uint64_t ihi, uint64_t ilo,
+                        int64_t n, int64_t m, int k);
 
 // eval.cu
 int eval_sse_f32(bgmf_ctx* ctx, const int32_t* rows, const int32_t* cols, const float* vals,

@@ -253,6 +253,52 @@ int bgmf_partition(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const 
   return partition_device(c, rows, cols, vals, nnz, n, m, grid_i, grid_j);
 }
 
+int bgmf_synth_partition(bgmf_ctx* c, int64_t n, int64_t m, int64_t nnz, uint64_t seed,
+                         int grid_i, int grid_j) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (n < 1 || m < 1 || nnz < 0 || (uint64_t)nnz > (uint64_t)n * (uint64_t)m)
+    return fail(c, BGMF_ERR_ARG, "bad synthetic shape");
+  cudaSetDevice(c->device);
+  if (c->streaming) stream_free(c);
+  cudaFree(c->d_sse); cudaFreeHost(c->h_sse); cudaFree(c->d_bad); cudaFreeHost(c->h_bad);
+  c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
+  const size_t N = (size_t)(nnz > 0 ? nnz : 1);
+  int64_t *r = nullptr, *q = nullptr;
+  double* v = nullptr;
+  cudaError_t e = cudaMalloc(&r, N * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&q, N * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&v, N * 8);
+  if (e != cudaSuccess) { cudaFree(r); cudaFree(q); cudaFree(v); return cuda_fail(c, e, "synth alloc"); }
+  int rc = synth_lowrank_device(c, n, m, nnz, 0, seed, r, q, v);
+  if (rc) { cudaFree(r); cudaFree(q); cudaFree(v); return rc; }
+  return partition_device(c, r, q, v, nnz, n, m, grid_i, grid_j, /*dev_in=*/true);
+}
+
+int bgmf_synth(int64_t n, int64_t m, int64_t nnz, int64_t start, uint64_t seed, int64_t* rows,
+               int64_t* cols, double* vals) {
+  int rc;
+  bgmf_ctx* c = scratch_ctx(&rc);
+  if (!c) return rc;
+  if (nnz <= 0) return BGMF_OK;
+  int64_t *r = nullptr, *q = nullptr;
+  double* v = nullptr;
+  cudaError_t e = cudaMalloc(&r, nnz * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&q, nnz * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&v, nnz * 8);
+  if (e == cudaSuccess) {
+    rc = synth_lowrank_device(c, n, m, nnz, start, seed, r, q, v);
+    if (!rc) {
+      e = cudaMemcpy(rows, r, nnz * 8, cudaMemcpyDeviceToHost);
+      if (e == cudaSuccess) e = cudaMemcpy(cols, q, nnz * 8, cudaMemcpyDeviceToHost);
+      if (e == cudaSuccess) e = cudaMemcpy(vals, v, nnz * 8, cudaMemcpyDeviceToHost);
+    }
+  }
+  cudaFree(r); cudaFree(q); cudaFree(v);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "bgmf_synth");
+  if (rc) { g_err = c->err; return rc; }
+  return BGMF_OK;
+}
+
 int bgmf_partition_export(bgmf_ctx* c, int64_t* offsets, int64_t* order, int32_t* lrows,
                           int32_t* lcols) {
   if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
@@ -307,6 +353,34 @@ int bgmf_set_factors(bgmf_ctx* c, const double* u, const double* v, int64_t n, i
   }
   int rc = upload_rows(c, u, c->d_u, n, k, c->kp);
   if (!rc) rc = upload_rows(c, v, c->d_v, m, k, c->kp);
+  if (rc) return rc;
+  c->have_factors = true;
+  return BGMF_OK;
+}
+
+int bgmf_init_factors(bgmf_ctx* c, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                      uint64_t inc_lo, int64_t n, int64_t m, int k) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (k < 1 || n < 1 || m < 1) return fail(c, BGMF_ERR_ARG, "n, m, k must all be >= 1");
+  if (c->partitioned && (n != c->n || m != c->m))
+    return fail(c, BGMF_ERR_ARG, "factor shapes do not match the partitioned dataset");
+  cudaSetDevice(c->device);
+  if (c->exact) {
+    free_factors(c);
+    c->k = k; c->kp = k;
+    BGMF_CK(c, cudaMalloc(&c->d_u64, (size_t)n * k * 8));
+    BGMF_CK(c, cudaMalloc(&c->d_v64, (size_t)m * k * 8));
+  } else {
+    const int kp = (k + 3) / 4 * 4;
+    if (kp > 512) return fail(c, BGMF_ERR_ARG, "fast mode supports k <= 512 (use exact mode)");
+    if (!(c->bound && c->k == k)) {
+      free_factors(c);
+      c->k = k; c->kp = kp;
+      BGMF_CK(c, cudaMalloc(&c->d_u, (size_t)n * kp * 4));
+      BGMF_CK(c, cudaMalloc(&c->d_v, (size_t)m * kp * 4));
+    }
+  }
+  int rc = init_factors_device(c, state_hi, state_lo, inc_hi, inc_lo, n, m, k);
   if (rc) return rc;
   c->have_factors = true;
   return BGMF_OK;

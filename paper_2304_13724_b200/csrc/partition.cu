@@ -253,8 +253,11 @@ void free_dev(T*& p) {
 
 }  // namespace
 
+// dev_in: rows/cols/vals are device buffers whose ownership passes to this
+// call (freed as soon as they are consumed); otherwise host arrays.
 int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
-                     const double* vals, int64_t nnz, int64_t n, int64_t m, int I, int J) {
+                     const double* vals, int64_t nnz, int64_t n, int64_t m, int I, int J,
+                     bool dev_in) {
   if (n < 1 || m < 1) return fail(ctx, BGMF_ERR_ARG, "n and m must be >= 1");
   if (I < 1 || I > n) return fail(ctx, BGMF_ERR_ARG, "grid_i must be in [1, n]");
   if (J < 1 || J > m) return fail(ctx, BGMF_ERR_ARG, "grid_j must be in [1, m]");
@@ -301,14 +304,20 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
     if (_e != cudaSuccess) { rc = cuda_fail(ctx, _e, #call); cleanup(); return rc; } \
   } while (0)
 
-  PCK(cudaMalloc(&d_rows, N * 8));
-  PCK(cudaMalloc(&d_cols, N * 8));
-  PCK(cudaMalloc(&d_vin, N * 8));
+  if (dev_in) {
+    d_rows = const_cast<int64_t*>(rows);
+    d_cols = const_cast<int64_t*>(cols);
+    d_vin = const_cast<double*>(vals);
+  } else {
+    PCK(cudaMalloc(&d_rows, N * 8));
+    PCK(cudaMalloc(&d_cols, N * 8));
+    PCK(cudaMalloc(&d_vin, N * 8));
+  }
   PCK(cudaMalloc(&ka, N * 8));
   PCK(cudaMalloc(&ia, N * 4));
   PCK(cudaMalloc(&d_bad, 8));
   PCK(cudaMalloc(&d_off, (nb + 1) * 8));
-  if (nnz > 0) {
+  if (nnz > 0 && !dev_in) {
     PCK(cudaMemcpyAsync(d_rows, rows, nnz * 8, cudaMemcpyHostToDevice, s));
     PCK(cudaMemcpyAsync(d_cols, cols, nnz * 8, cudaMemcpyHostToDevice, s));
     PCK(cudaMemcpyAsync(d_vin, vals, nnz * 8, cudaMemcpyHostToDevice, s));
@@ -323,10 +332,17 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   PCK(cudaMemcpyAsync(&hbad, d_bad, 8, cudaMemcpyDeviceToHost, s));
   PCK(cudaStreamSynchronize(s));
   if (hbad != ~0ull) {
+    int64_t br = 0, bc = 0;
+    if (dev_in) {
+      cudaMemcpy(&br, d_rows + hbad, 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&bc, d_cols + hbad, 8, cudaMemcpyDeviceToHost);
+    } else {
+      br = rows[hbad];
+      bc = cols[hbad];
+    }
     char buf[160];
     snprintf(buf, sizeof buf, "entry %lld: index (%lld, %lld) outside %lldx%lld matrix",
-             (long long)hbad, (long long)rows[hbad], (long long)cols[hbad], (long long)n,
-             (long long)m);
+             (long long)hbad, (long long)br, (long long)bc, (long long)n, (long long)m);
     cleanup();
     return fail(ctx, BGMF_ERR_DATA, buf);
   }

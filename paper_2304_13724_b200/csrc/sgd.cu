@@ -83,22 +83,30 @@ __device__ __forceinline__ Chunk locate_chunk(const BlockWork* __restrict__ work
   return ch;
 }
 
-// Per-thread masks: lanes past the padded row (kp < 4*L*V4) do nothing.
-template <int L, int V4>
+// Lane geometry of a group.  kMask: the padded row kp is narrower than the
+// group's 4*L*V4 floats, so some lanes/vectors sit past the row and are
+// predicated off (only for odd k; k = 32/64/128 run unmasked).
+template <int L, int V4, bool kMask>
 struct Lanes {
   int gl, gbase;
-  bool on[V4];
+  bool on_[V4];
   __device__ __forceinline__ Lanes(int kp) {
     const int lane = threadIdx.x & 31;
     gl = lane & (L - 1);
     gbase = lane & ~(L - 1);
 #pragma unroll
-    for (int q = 0; q < V4; ++q) on[q] = 4 * (q * L + gl) < kp;
+    for (int q = 0; q < V4; ++q) on_[q] = !kMask || 4 * (q * L + gl) < kp;
   }
+  __device__ __forceinline__ bool on(int q) const { return !kMask || on_[q]; }
   __device__ __forceinline__ int off(int q) const { return 4 * (q * L + gl); }
 };
 
 __device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ float2 lo2(const float4& a) { return make_float2(a.x, a.y); }
+__device__ __forceinline__ float2 hi2(const float4& a) { return make_float2(a.z, a.w); }
+__device__ __forceinline__ float4 cat4(const float2& a, const float2& b) {
+  return make_float4(a.x, a.y, b.x, b.y);
+}
 
 // L2-coherent 128-bit load (the factors are written by other SMs during the
 // kernel; ld.global.cg never returns a stale L1 line).
@@ -106,20 +114,29 @@ __device__ __forceinline__ float4 ld_cg(const float* p) {
   return __ldcg(reinterpret_cast<const float4*>(p));
 }
 
-template <int L, int V4>
-__device__ __forceinline__ void load_row(float4 (&dst)[V4], const float* row, const Lanes<L, V4>& ln) {
+template <int V4, class LN>
+__device__ __forceinline__ void load_row(float4 (&dst)[V4], const float* row, const LN& ln) {
 #pragma unroll
-  for (int q = 0; q < V4; ++q) dst[q] = ln.on[q] ? ld_cg(row + ln.off(q)) : zero4();
+  for (int q = 0; q < V4; ++q) dst[q] = ln.on(q) ? ld_cg(row + ln.off(q)) : zero4();
 }
 
-// Write a finished user run back with a plain store.  (A run shared with a
-// neighbour chunk is never stored: its per-rating deltas went out as reds.)
-template <int L, int V4>
-__device__ __forceinline__ void store_row(float* row, const float4 (&u)[V4],
-                                          const Lanes<L, V4>& ln) {
+template <int V4, class LN>
+__device__ __forceinline__ void store_row(float* row, const float4 (&u)[V4], const LN& ln) {
 #pragma unroll
   for (int q = 0; q < V4; ++q)
-    if (ln.on[q]) *reinterpret_cast<float4*>(row + ln.off(q)) = u[q];
+    if (ln.on(q)) *reinterpret_cast<float4*>(row + ln.off(q)) = u[q];
+}
+
+// partial dot of the lane's slice with packed FFMA2 (two fp32 lanes per op)
+template <int V4>
+__device__ __forceinline__ float dot_slice(const float4 (&u)[V4], const float4 (&v)[V4]) {
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int q = 0; q < V4; ++q) {
+    acc = __ffma2_rn(lo2(u[q]), lo2(v[q]), acc);
+    acc = __ffma2_rn(hi2(u[q]), hi2(v[q]), acc);
+  }
+  return acc.x + acc.y;
 }
 
 // Software-pipelined walk over one chunk.  While rating t is computed, the
@@ -128,16 +145,18 @@ __device__ __forceinline__ void store_row(float* row, const float4 (&u)[V4],
 // -- so is its U row.  kSweep: SGD update; else: accumulate (x - u.v)^2.
 // A user run that continues into a neighbour chunk ("shared") applies each
 // rating's U delta with red.add as it goes; an interior run is stored once.
+// The update is the reference's  u += a(2e v - b u),  v += a(2e u_old - b v)
+// evaluated as t = 2ae*v - ab*u (FFMA2 of an FMUL2) and u + t, in packed fp32.
 // All lanes of the warp execute the same trip count (maxlen) so the shuffles
 // stay converged; groups past their chunk end are predicated off.
-template <int L, int V4, bool kSweep>
+template <int L, int V4, bool kMask, bool kSweep>
 __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
                                              const int32_t* __restrict__ lrow,
                                              const int32_t* __restrict__ lcol,
                                              const float* __restrict__ val, float* U, float* V,
                                              int kp, float alpha, float beta, int iter,
                                              unsigned long long* bad) {
-  const Lanes<L, V4> ln(kp);
+  const Lanes<L, V4, kMask> ln(kp);
   const int len = (int)(ch.end - ch.begin);
   float* Ub = U + ch.row_start * kp;
   float* Vb = V + ch.col_start * kp;
@@ -165,8 +184,8 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
   float x = __shfl_sync(kFull, xA, ln.gbase);
   float4 u[V4], v[V4];
   if (len > 0) {
-    load_row<L, V4>(u, Ub + (int64_t)r * kp, ln);
-    load_row<L, V4>(v, Vb + (int64_t)c * kp, ln);
+    load_row<V4>(u, Ub + (int64_t)r * kp, ln);
+    load_row<V4>(v, Vb + (int64_t)c * kp, ln);
   } else {
 #pragma unroll
     for (int q = 0; q < V4; ++q) u[q] = v[q] = zero4();
@@ -174,7 +193,8 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
   bool shared = kSweep && (r == first_row || r == last_row);
   bool dead = false;
   double acc = 0.0;
-  const float two_a = 2.0f * alpha, ab = alpha * beta;
+  const float two_a = 2.0f * alpha;
+  const float2 nab = make_float2(-alpha * beta, -alpha * beta);
 
   for (int t0 = 0; t0 < maxlen; t0 += L) {
 #pragma unroll 1
@@ -190,18 +210,10 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
       const bool nvalid = t + 1 < len && !dead;
       const bool newrun = nvalid && rn != r;
       float4 vn[V4], un[V4];
-      if (nvalid) load_row<L, V4>(vn, Vb + (int64_t)cn * kp, ln);
-      if (newrun) load_row<L, V4>(un, Ub + (int64_t)rn * kp, ln);
+      if (nvalid) load_row<V4>(vn, Vb + (int64_t)cn * kp, ln);
+      if (newrun) load_row<V4>(un, Ub + (int64_t)rn * kp, ln);
 
-      float dot = 0.f;
-#pragma unroll
-      for (int q = 0; q < V4; ++q) {
-        dot = fmaf(u[q].x, v[q].x, dot);
-        dot = fmaf(u[q].y, v[q].y, dot);
-        dot = fmaf(u[q].z, v[q].z, dot);
-        dot = fmaf(u[q].w, v[q].w, dot);
-      }
-      dot = group_sum<L>(dot);
+      const float dot = group_sum<L>(dot_slice<V4>(u, v));
       const float e = x - dot;
       if (valid) {
         if (!kSweep) {
@@ -212,32 +224,27 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
           dead = true;
         } else {
           const float g = two_a * e;
+          const float2 g2 = make_float2(g, g);
           float* vp = Vb + (int64_t)c * kp;
           float* up = Ub + (int64_t)r * kp;
 #pragma unroll
           for (int q = 0; q < V4; ++q) {
-            float4 dv, du;
-            dv.x = g * u[q].x - ab * v[q].x;
-            dv.y = g * u[q].y - ab * v[q].y;
-            dv.z = g * u[q].z - ab * v[q].z;
-            dv.w = g * u[q].w - ab * v[q].w;
-            du.x = g * v[q].x - ab * u[q].x;
-            du.y = g * v[q].y - ab * u[q].y;
-            du.z = g * v[q].z - ab * u[q].z;
-            du.w = g * v[q].w - ab * u[q].w;
-            u[q].x += du.x;
-            u[q].y += du.y;
-            u[q].z += du.z;
-            u[q].w += du.w;
-            if (ln.on[q]) {
-              red_add_v4(vp + ln.off(q), dv);
-              if (shared) red_add_v4(up + ln.off(q), du);
+            const float2 ul = lo2(u[q]), uh = hi2(u[q]), vl = lo2(v[q]), vh = hi2(v[q]);
+            // dv = 2ae*u_old - ab*v ; du = 2ae*v - ab*u_old
+            const float2 dvl = __ffma2_rn(g2, ul, __fmul2_rn(nab, vl));
+            const float2 dvh = __ffma2_rn(g2, uh, __fmul2_rn(nab, vh));
+            const float2 dul = __ffma2_rn(g2, vl, __fmul2_rn(nab, ul));
+            const float2 duh = __ffma2_rn(g2, vh, __fmul2_rn(nab, uh));
+            u[q] = cat4(__fadd2_rn(ul, dul), __fadd2_rn(uh, duh));
+            if (ln.on(q)) {
+              red_add_v4(vp + ln.off(q), cat4(dvl, dvh));
+              if (shared) red_add_v4(up + ln.off(q), cat4(dul, duh));
             }
           }
         }
       }
       if (kSweep && valid && !dead && !shared && (newrun || !nvalid))
-        store_row<L, V4>(Ub + (int64_t)r * kp, u, ln);
+        store_row<V4>(Ub + (int64_t)r * kp, u, ln);
       if (newrun) {
 #pragma unroll
         for (int q = 0; q < V4; ++q) u[q] = un[q];
@@ -263,7 +270,7 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
   return acc;
 }
 
-template <int L, int V4>
+template <int L, int V4, bool kMask>
 __global__ void __launch_bounds__(256, 2)
 sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
@@ -275,13 +282,13 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
   const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
   const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
   if (maxlen == 0) return;
-  walk_chunk<L, V4, true>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter, bad);
+  walk_chunk<L, V4, kMask, true>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter, bad);
 }
 
 // Post-sweep SSE of each block: sum over the chunk of (x - u.v)^2 in fp64,
 // one atomicAdd per group into sse[block_id].
-template <int L, int V4>
-__global__ void __launch_bounds__(256)
+template <int L, int V4, bool kMask>
+__global__ void __launch_bounds__(256, 2)
 sse_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
                 const float* __restrict__ val, const float* __restrict__ U,
@@ -293,31 +300,32 @@ sse_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
   const int len = (int)(ch.end - ch.begin);
   const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
   if (maxlen == 0) return;
-  const double acc = walk_chunk<L, V4, false>(ch, maxlen, lrow, lcol, val, const_cast<float*>(U),
-                                              const_cast<float*>(V), kp, 0.f, 0.f, 0, nullptr);
+  const double acc = walk_chunk<L, V4, kMask, false>(ch, maxlen, lrow, lcol, val,
+                                                     const_cast<float*>(U), const_cast<float*>(V),
+                                                     kp, 0.f, 0.f, 0, nullptr);
   if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
 }
 
 // Out-of-line copies of the two walks for the persistent kernel: register
-// allocation is then per phase (no spills from keeping both live), and the
-// call costs once per chunk.
-template <int L, int V4>
+// allocation is then per phase, and the call costs once per chunk.
+template <int L, int V4, bool kMask>
 __device__ __noinline__ void sweep_chunk(const Chunk& ch, int maxlen,
                                          const int32_t* __restrict__ lrow,
                                          const int32_t* __restrict__ lcol,
                                          const float* __restrict__ val, float* U, float* V,
                                          int kp, float alpha, float beta, int iter,
                                          unsigned long long* bad) {
-  walk_chunk<L, V4, true>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter, bad);
+  walk_chunk<L, V4, kMask, true>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter, bad);
 }
 
-template <int L, int V4>
+template <int L, int V4, bool kMask>
 __device__ __noinline__ double sse_chunk(const Chunk& ch, int maxlen,
                                          const int32_t* __restrict__ lrow,
                                          const int32_t* __restrict__ lcol,
                                          const float* __restrict__ val, float* U, float* V,
                                          int kp) {
-  return walk_chunk<L, V4, false>(ch, maxlen, lrow, lcol, val, U, V, kp, 0.f, 0.f, 0, nullptr);
+  return walk_chunk<L, V4, kMask, false>(ch, maxlen, lrow, lcol, val, U, V, kp, 0.f, 0.f, 0,
+                                         nullptr);
 }
 
 // Whole outer step in one cooperative launch: for every batch, `iters`
@@ -328,7 +336,7 @@ struct BatchDesc {
   int w0, nw, chunks, pad;
 };
 
-template <int L, int V4>
+template <int L, int V4, bool kMask>
 __global__ void __launch_bounds__(256, 2)
 epoch_fast_kernel(const BlockWork* __restrict__ work, const BatchDesc* __restrict__ batches,
                   int nbatch, int iters, const int32_t* __restrict__ lrow,
@@ -348,7 +356,7 @@ epoch_fast_kernel(const BlockWork* __restrict__ work, const BatchDesc* __restric
         const Chunk ch = locate_chunk(w, bd.nw, bd.chunks, base + lane / L);
         const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
         if (maxlen > 0)
-          sweep_chunk<L, V4>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, it, bad);
+          sweep_chunk<L, V4, kMask>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, it, bad);
       }
       grid.sync();
     }
@@ -357,7 +365,7 @@ epoch_fast_kernel(const BlockWork* __restrict__ work, const BatchDesc* __restric
       const int len = (int)(ch.end - ch.begin);
       const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
       if (maxlen == 0) continue;
-      const double acc = sse_chunk<L, V4>(ch, maxlen, lrow, lcol, val, U, V, kp);
+      const double acc = sse_chunk<L, V4, kMask>(ch, maxlen, lrow, lcol, val, U, V, kp);
       if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
     }
     if (t + 1 < nbatch) grid.sync();
@@ -472,19 +480,27 @@ Shape shape_for(int kp) {
   return {L, 4};
 }
 
-#define BGMF_SHAPES(X) X(1, 1) X(1, 2) X(1, 4) X(2, 4) X(4, 4) X(8, 4) X(16, 4) X(32, 4)
+#define BGMF_SHAPES(X)                                                                      \
+  X(1, 1, true) X(1, 2, true) X(1, 4, true) X(2, 4, true) X(4, 4, true) X(8, 4, true)       \
+  X(16, 4, true) X(32, 4, true) X(1, 1, false) X(1, 2, false) X(1, 4, false) X(2, 4, false) \
+  X(4, 4, false) X(8, 4, false) X(16, 4, false) X(32, 4, false)
+
+// kp == 4*L*V4: every lane owns a full slice of the row, no predication
+inline bool needs_mask(const Shape& sh, int kp) { return 4 * sh.L * sh.V4 != kp; }
 
 void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, const BlockWork* w,
                      int nwork, int total, const int32_t* lrow, const int32_t* lcol,
                      const float* val, bgmf_ctx* c, float a, float b, int it) {
-#define BGMF_CASE(LL, VV)                                                                     \
-  if (sh.L == LL && sh.V4 == VV) {                                                            \
+  const bool mk = needs_mask(sh, c->kp);
+#define BGMF_CASE(LL, VV, MM)                                                                 \
+  if (sh.L == LL && sh.V4 == VV && mk == MM) {                                                \
     if (sweep)                                                                                \
-      sgd_fast_kernel<LL, VV><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val, c->d_u,  \
-                                                   c->d_v, c->kp, a, b, it, c->d_bad);        \
+      sgd_fast_kernel<LL, VV, MM><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val,      \
+                                                       c->d_u, c->d_v, c->kp, a, b, it,       \
+                                                       c->d_bad);                             \
     else                                                                                      \
-      sse_fast_kernel<LL, VV><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val, c->d_u,  \
-                                                   c->d_v, c->kp, c->d_sse);                  \
+      sse_fast_kernel<LL, VV, MM><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val,      \
+                                                       c->d_u, c->d_v, c->kp, c->d_sse);      \
     return;                                                                                   \
   }
   BGMF_SHAPES(BGMF_CASE)
@@ -497,17 +513,21 @@ void launch_fast(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, const B
                   it);
 }
 
-const void* epoch_kernel_ptr(const Shape& sh) {
-#define BGMF_EP(LL, VV) \
-  if (sh.L == LL && sh.V4 == VV) return reinterpret_cast<const void*>(&epoch_fast_kernel<LL, VV>);
+const void* epoch_kernel_ptr(const Shape& sh, int kp) {
+  const bool mk = needs_mask(sh, kp);
+#define BGMF_EP(LL, VV, MM)                            \
+  if (sh.L == LL && sh.V4 == VV && mk == MM)           \
+    return reinterpret_cast<const void*>(&epoch_fast_kernel<LL, VV, MM>);
   BGMF_SHAPES(BGMF_EP)
 #undef BGMF_EP
   return nullptr;
 }
 
-const void* sweep_kernel_ptr(const Shape& sh) {
-#define BGMF_SW(LL, VV) \
-  if (sh.L == LL && sh.V4 == VV) return reinterpret_cast<const void*>(&sgd_fast_kernel<LL, VV>);
+const void* sweep_kernel_ptr(const Shape& sh, int kp) {
+  const bool mk = needs_mask(sh, kp);
+#define BGMF_SW(LL, VV, MM)                            \
+  if (sh.L == LL && sh.V4 == VV && mk == MM)           \
+    return reinterpret_cast<const void*>(&sgd_fast_kernel<LL, VV, MM>);
   BGMF_SHAPES(BGMF_SW)
 #undef BGMF_SW
   return nullptr;
@@ -582,7 +602,7 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
 }
 
 int64_t sweep_groups(bgmf_ctx* c, const Shape& sh) {
-  return (int64_t)c->num_sms * resident_ctas(c, sweep_kernel_ptr(sh)) * 8 * (32 / sh.L);
+  return (int64_t)c->num_sms * resident_ctas(c, sweep_kernel_ptr(sh, c->kp)) * 8 * (32 / sh.L);
 }
 
 }  // namespace
@@ -618,12 +638,12 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, in
   const Shape sh = shape_for(c->kp);
   const int gpw = 32 / sh.L;
   const int nb = c->I * c->J;
-  const void* ep = epoch_kernel_ptr(sh);
+  const void* ep = epoch_kernel_ptr(sh, c->kp);
   // fused = -1 (auto): the persistent kernel pays off when launches dominate
   // (small strata); big strata run faster as separate sweep / SSE launches.
   const int64_t per_batch = nbatch > 0 ? c->nnz / nbatch : c->nnz;
   const bool fused = c->fused > 0 || (c->fused < 0 && per_batch <= c->fused_max_batch);
-  const int ctas_per_sm = fused ? resident_ctas(c, ep) : resident_ctas(c, sweep_kernel_ptr(sh));
+  const int ctas_per_sm = fused ? resident_ctas(c, ep) : resident_ctas(c, sweep_kernel_ptr(sh, c->kp));
   const int64_t groups = (int64_t)c->num_sms * ctas_per_sm * 8 * gpw;
   std::vector<BatchRange> ranges;
   int rc = build_work(c, plan, batch_off, nbatch, groups, ranges);

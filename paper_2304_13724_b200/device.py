@@ -149,6 +149,16 @@ class Engine:
                                              u.shape[0], v.shape[0], u.shape[1]))
         self.k = u.shape[1]
 
+    def init_factors(self, n: int, m: int, k: int, seed: int):
+        """init_factors(n, m, k, seed) generated on the device: the PCG64
+        stream of numpy's default_rng(seed), bit-identical (core.py:179-193)."""
+        st = np.random.default_rng(seed).bit_generator.state["state"]
+        s, inc = int(st["state"]), int(st["inc"])
+        mask = (1 << 64) - 1
+        self._check(self._L.bgmf_init_factors(self._h, s >> 64, s & mask, inc >> 64, inc & mask,
+                                              n, m, k))
+        self.k = k
+
     def bind_factors(self, u_ptr: int, v_ptr: int, n: int, m: int, k: int, kp: int):
         self._check(self._L.bgmf_bind_factors(self._h, ctypes.c_void_p(u_ptr),
                                               ctypes.c_void_p(v_ptr), n, m, k, kp))

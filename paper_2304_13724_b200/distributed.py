@@ -186,8 +186,7 @@ def train_blocked_distributed(d, cfg, *, early_stop: bool = True, options=None,
     (FactorModel on every rank, ConvergenceTrace, stop_reason)."""
     import torch
 
-    from .core import (ConvergenceTrace, DivergenceError, FactorModel, TraceStep,
-                       init_factors)
+    from .core import ConvergenceTrace, FactorModel, TraceStep
     from .kernel import divergence
     from .metrics import RmseAccumulator, finalize, merge
     from .trainer import resolve_inner_iters
@@ -198,8 +197,7 @@ def train_blocked_distributed(d, cfg, *, early_stop: bool = True, options=None,
     torch.cuda.set_device(device)
     sched = RingSchedule(cfg.grid_i, cfg.grid_j, world)
     shard = GpuShard(d, cfg, sched, rank, device, options)
-    model0 = init_factors(d.n, d.m, cfg.k, cfg.seed)
-    shard.set_factors(model0.u, model0.v)
+    shard.eng.init_factors(d.n, d.m, cfg.k, cfg.seed)
     nb = cfg.grid_i * cfg.grid_j
     trace = ConvergenceTrace()
     stop = "max_steps"
@@ -259,7 +257,7 @@ def bench_main(args):
     import torch
 
     from . import workloads
-    from .core import RatingsDataset, TrainConfig, init_factors
+    from .core import RatingsDataset, TrainConfig
     from .device import EngineOptions
 
     dist = _init_dist()
@@ -280,9 +278,7 @@ def bench_main(args):
     sched = RingSchedule(w.grid, w.grid, world)
     shard = GpuShard(d, cfg, sched, rank, device, EngineOptions(timing=False))
     del r, c, v
-    m0 = init_factors(w.n, w.m, w.k, w.seed)
-    shard.set_factors(m0.u, m0.v)
-    del m0
+    shard.eng.init_factors(w.n, w.m, w.k, w.seed)
     stream = shard.stream
 
     def epoch(step0):

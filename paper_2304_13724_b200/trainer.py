@@ -92,8 +92,9 @@ def train_blocked(d: RatingsDataset, cfg: TrainConfig, test: Optional[RatingsDat
             or blocked.dataset is not d:
         raise ValueError("blocked must partition d with cfg's grid")
     eng = blocked.engine
-    model0 = init_factors(d.n, d.m, cfg.k, cfg.seed)
-    eng.set_factors(model0.u, model0.v)
+    # init_factors(n, m, k, seed) generated in HBM: numpy's PCG64 stream
+    # reproduced bit-for-bit on the device (no 2*(n+m)*k*8-byte upload)
+    eng.init_factors(d.n, d.m, cfg.k, cfg.seed)
 
     evaluator = HoldoutEvaluator(d, test) if test is not None and len(test) > 0 else None
     if evaluator is not None:
@@ -104,7 +105,8 @@ def train_blocked(d: RatingsDataset, cfg: TrainConfig, test: Optional[RatingsDat
     adaptive = isinstance(sched, AdaptiveDecreasing)
     hist = [math.sqrt(eng.train_sse() / len(d))] if adaptive and len(d) else [0.0]
     counts = np.diff(eng.offsets)
-    hooks = _HookTasks(blocked, model0, cfg) if block_hook is not None else None
+    hooks = (_HookTasks(blocked, init_factors(d.n, d.m, cfg.k, cfg.seed), cfg)
+             if block_hook is not None else None)
 
     trace = ConvergenceTrace()
     stop: StopReason = "max_steps"
