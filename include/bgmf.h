@@ -57,8 +57,8 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      strata, sweeps and SSE passes separated by grid
  *                      barriers); 0 = one launch per stratum sweep / SSE pass;
  *                      -1 = auto (default): fused when a stratum holds at most
- *                      "fused_max_batch" ratings (2^21), i.e. when launches
- *                      dominate. */
+ *                      "fused_max_batch" ratings (default 0: measured on B200,
+ *                      the per-stratum launches win at every config size). */
 int bgmf_set_option(bgmf_ctx* ctx, const char* key, double value);
 
 /* Bucket the ratings into the I x J block grid on the GPU.

@@ -56,7 +56,7 @@ struct bgmf_ctx {
   bool timing = false;
   int warps_per_sm = 0;
   int fused = -1;      // 1: one cooperative launch per step, 0: per stratum, -1 auto
-  int64_t fused_max_batch = 1 << 21;  // auto: fuse when a stratum has <= 2M ratings
+  int64_t fused_max_batch = 0;  // auto: fuse when a stratum has <= this many ratings
 
   // grid + partition
   int64_t n = 0, m = 0, nnz = 0;

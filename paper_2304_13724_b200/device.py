@@ -34,9 +34,10 @@ class EngineOptions:
                blocks, which keeps the lossless-Hogwild drift far below 1e-3).
     device     CUDA ordinal; default $BGMF_DEVICE, else $LOCAL_RANK, else 0.
     timing     record CUDA events around every kernel launch.
-    fused      True: one cooperative launch per outer step; False: one launch
-               per stratum sweep / SSE pass; None (default): fused only for
-               small strata (<= 2M ratings), where launch latency dominates.
+    fused      True: one cooperative launch per outer step (grid barriers
+               between strata); False: one launch per stratum sweep / SSE
+               pass; None (default): the library's choice (per-stratum
+               launches -- faster at every config measured on B200).
     device_rating_budget
                bytes of HBM the ratings may use (None: all resident).  When
                the partition is larger, it moves to pinned host memory and

@@ -25,6 +25,8 @@ for w in $WHAT; do
           timeout 600 $B --config $c --steps 20 --warmup 3 $f --no-e2e --no-cpu-baseline >> $OUT/bench_small.jsonl 2>> $OUT/bench_small.err
         done
       done; echo "small rc=$?" ;;
+    c5s) timeout 900 $B --config C5 --nnz 200000000 --steps 3 --warmup 3 --budget-gb 0.5 > $OUT/bench_c5_small.json 2> $OUT/bench_c5_small.err; echo "c5s rc=$?" ;;
+    c5) timeout 1500 $B --config C5 --steps 3 --warmup 3 > $OUT/bench_c5.json 2> $OUT/bench_c5.err; echo "c5 rc=$?" ;;
     ncu)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file $OUT/launches.csv $B --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
