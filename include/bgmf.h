@@ -53,6 +53,9 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      (bounds per-block concurrency on small blocks; 256).
  *   "timing"     0/1   record CUDA events around every kernel launch.
  *   "warps_per_sm" int resident-warp target used to size chunks (0 = occupancy).
+ *   "bulk_red"   0/1   1 = each rating's V-row delta leaves through the TMA
+ *                      engine (cp.reduce.async.bulk add.f32 from a shared-
+ *                      memory ring; default); 0 = per-lane red.global.add.v4.
  *   "fused"      -1/0/1  1 = one cooperative launch per outer step (all
  *                      strata, sweeps and SSE passes separated by grid
  *                      barriers); 0 = one launch per stratum sweep / SSE pass;

@@ -42,6 +42,33 @@ __device__ __forceinline__ void red_add_v4(float* p, float4 d) {
                : "memory");
 }
 
+// Bulk asynchronous reduction (TMA engine): global[dst .. dst+bytes) +=
+// shared[src ..], fp32 adds performed at L2.  Issued by one lane for a whole
+// V-row delta, it replaces that group's per-lane REDG traffic through L1TEX.
+__device__ __forceinline__ void bulk_red_add(float* gdst, const float* ssrc, unsigned bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
+                   gdst),
+               "r"(s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// smem ring of V-row deltas per group for the bulk path
+constexpr int kBulkBufs = 4;
+
 __device__ __forceinline__ int find_work(const BlockWork* __restrict__ work, int nwork, int c) {
   int lo = 0, hi = nwork - 1;  // last w with first_chunk <= c
   while (lo < hi) {
@@ -149,14 +176,16 @@ __device__ __forceinline__ float dot_slice(const float4 (&u)[V4], const float4 (
 // evaluated as t = 2ae*v - ab*u (FFMA2 of an FMUL2) and u + t, in packed fp32.
 // All lanes of the warp execute the same trip count (maxlen) so the shuffles
 // stay converged; groups past their chunk end are predicated off.
-template <int L, int V4, bool kMask, bool kSweep>
+template <int L, int V4, bool kMask, bool kSweep, bool kBulk = false>
 __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
                                              const int32_t* __restrict__ lrow,
                                              const int32_t* __restrict__ lcol,
                                              const float* __restrict__ val, float* U, float* V,
                                              int kp, float alpha, float beta, int iter,
-                                             unsigned long long* bad) {
+                                             unsigned long long* bad,
+                                             float* sbuf = nullptr) {
   const Lanes<L, V4, kMask> ln(kp);
+  int nbulk = 0;  // bulk ops issued by this group (ring position)
   const int len = (int)(ch.end - ch.begin);
   float* Ub = U + ch.row_start * kp;
   float* Vb = V + ch.col_start * kp;
@@ -237,11 +266,30 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
             const float2 duh = __ffma2_rn(g2, vh, __fmul2_rn(nab, uh));
             u[q] = cat4(__fadd2_rn(ul, dul), __fadd2_rn(uh, duh));
             if (ln.on(q)) {
-              red_add_v4(vp + ln.off(q), cat4(dvl, dvh));
+              if (kBulk)
+                *reinterpret_cast<float4*>(sbuf + (nbulk % kBulkBufs) * kp + ln.off(q)) =
+                    cat4(dvl, dvh);
+              else
+                red_add_v4(vp + ln.off(q), cat4(dvl, dvh));
               if (shared) red_add_v4(up + ln.off(q), cat4(dul, duh));
             }
           }
         }
+      }
+      if (kSweep && kBulk) {
+        // the group's V delta is in its smem slot: one lane hands the whole
+        // row to the TMA engine (bulk reduce-add at L2)
+        const bool issue = valid && !dead;
+        fence_async_smem();
+        __syncwarp();
+        if (issue && ln.gl == 0) {
+          bulk_red_add(Vb + (int64_t)c * kp, sbuf + (nbulk % kBulkBufs) * kp, (unsigned)kp * 4u);
+          bulk_commit();
+        }
+        if (issue) ++nbulk;
+        // before the next write into the ring, its oldest slot must be read
+        if (ln.gl == 0) bulk_wait_read<kBulkBufs - 1>();
+        __syncwarp();
       }
       if (kSweep && valid && !dead && !shared && (newrun || !nvalid))
         store_row<V4>(Ub + (int64_t)r * kp, u, ln);
@@ -267,22 +315,28 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
       xB = __ldg(val + ch.begin + nb);
     }
   }
+  if (kSweep && kBulk && ln.gl == 0) bulk_wait_all();
   return acc;
 }
 
-template <int L, int V4, bool kMask>
+template <int L, int V4, bool kMask, bool kBulk>
 __global__ void __launch_bounds__(256, 2)
 sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
                 const float* __restrict__ val, float* __restrict__ U, float* __restrict__ V,
                 int kp, float alpha, float beta, int iter, unsigned long long* __restrict__ bad) {
   constexpr int GPW = 32 / L;
+  extern __shared__ float4 smem_rows[];
   const int lane = threadIdx.x & 31;
   const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
   const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
   if (maxlen == 0) return;
-  walk_chunk<L, V4, kMask, true>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter, bad);
+  // this group's delta ring: kBulkBufs rows of kp floats
+  float* sbuf = reinterpret_cast<float*>(smem_rows) +
+                (size_t)((threadIdx.x >> 5) * GPW + lane / L) * kBulkBufs * kp;
+  walk_chunk<L, V4, kMask, true, kBulk>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter,
+                                        bad, sbuf);
 }
 
 // Post-sweep SSE of each block: sum over the chunk of (x - u.v)^2 in fp64,
@@ -488,16 +542,25 @@ Shape shape_for(int kp) {
 // kp == 4*L*V4: every lane owns a full slice of the row, no predication
 inline bool needs_mask(const Shape& sh, int kp) { return 4 * sh.L * sh.V4 != kp; }
 
+// dynamic smem of the bulk sweep: kBulkBufs delta rows per group
+size_t bulk_smem(bgmf_ctx* c, const Shape& sh) {
+  return (size_t)(256 / sh.L) * kBulkBufs * c->kp * sizeof(float);
+}
+
 void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, const BlockWork* w,
                      int nwork, int total, const int32_t* lrow, const int32_t* lcol,
                      const float* val, bgmf_ctx* c, float a, float b, int it) {
   const bool mk = needs_mask(sh, c->kp);
 #define BGMF_CASE(LL, VV, MM)                                                                 \
   if (sh.L == LL && sh.V4 == VV && mk == MM) {                                                \
-    if (sweep)                                                                                \
-      sgd_fast_kernel<LL, VV, MM><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val,      \
-                                                       c->d_u, c->d_v, c->kp, a, b, it,       \
-                                                       c->d_bad);                             \
+    if (sweep && c->bulk_red) {                                                               \
+      cudaFuncSetAttribute(&sgd_fast_kernel<LL, VV, MM, true>,                               \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem(c, sh)); \
+      sgd_fast_kernel<LL, VV, MM, true><<<grid, 256, bulk_smem(c, sh), s>>>(                  \
+          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad);       \
+    } else if (sweep)                                                                         \
+      sgd_fast_kernel<LL, VV, MM, false><<<grid, 256, 0, s>>>(                                \
+          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad);       \
     else                                                                                      \
       sse_fast_kernel<LL, VV, MM><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val,      \
                                                        c->d_u, c->d_v, c->kp, c->d_sse);      \
@@ -523,21 +586,23 @@ const void* epoch_kernel_ptr(const Shape& sh, int kp) {
   return nullptr;
 }
 
-const void* sweep_kernel_ptr(const Shape& sh, int kp) {
+const void* sweep_kernel_ptr(const Shape& sh, int kp, bool bulk) {
   const bool mk = needs_mask(sh, kp);
-#define BGMF_SW(LL, VV, MM)                            \
-  if (sh.L == LL && sh.V4 == VV && mk == MM)           \
-    return reinterpret_cast<const void*>(&sgd_fast_kernel<LL, VV, MM>);
+#define BGMF_SW(LL, VV, MM)                                                             \
+  if (sh.L == LL && sh.V4 == VV && mk == MM)                                            \
+    return bulk ? reinterpret_cast<const void*>(&sgd_fast_kernel<LL, VV, MM, true>)     \
+                : reinterpret_cast<const void*>(&sgd_fast_kernel<LL, VV, MM, false>);
   BGMF_SHAPES(BGMF_SW)
 #undef BGMF_SW
   return nullptr;
 }
 
 // Resident 256-thread CTAs per SM of a kernel (the one-wave capacity).
-int resident_ctas(bgmf_ctx* c, const void* fn) {
+int resident_ctas(bgmf_ctx* c, const void* fn, size_t smem = 0) {
   if (c->warps_per_sm > 0) return (c->warps_per_sm + 7) / 8;
+  if (smem > 0) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int blocks = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 256, smem);
   return blocks > 0 ? blocks : 1;
 }
 
@@ -602,7 +667,7 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
 }
 
 int64_t sweep_groups(bgmf_ctx* c, const Shape& sh) {
-  return (int64_t)c->num_sms * resident_ctas(c, sweep_kernel_ptr(sh, c->kp)) * 8 * (32 / sh.L);
+  return (int64_t)c->num_sms * resident_ctas(c, sweep_kernel_ptr(sh, c->kp, c->bulk_red), c->bulk_red ? bulk_smem(c, sh) : 0) * 8 * (32 / sh.L);
 }
 
 }  // namespace
@@ -643,7 +708,7 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, in
   // (small strata); big strata run faster as separate sweep / SSE launches.
   const int64_t per_batch = nbatch > 0 ? c->nnz / nbatch : c->nnz;
   const bool fused = c->fused > 0 || (c->fused < 0 && per_batch <= c->fused_max_batch);
-  const int ctas_per_sm = fused ? resident_ctas(c, ep) : resident_ctas(c, sweep_kernel_ptr(sh, c->kp));
+  const int ctas_per_sm = fused ? resident_ctas(c, ep) : resident_ctas(c, sweep_kernel_ptr(sh, c->kp, c->bulk_red), c->bulk_red ? bulk_smem(c, sh) : 0);
   const int64_t groups = (int64_t)c->num_sms * ctas_per_sm * 8 * gpw;
   std::vector<BatchRange> ranges;
   int rc = build_work(c, plan, batch_off, nbatch, groups, ranges);

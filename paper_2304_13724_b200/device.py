@@ -38,6 +38,9 @@ class EngineOptions:
                between strata); False: one launch per stratum sweep / SSE
                pass; None (default): the library's choice (per-stratum
                launches -- faster at every config measured on B200).
+    bulk_red   V-row deltas leave through the TMA engine as bulk reduce-adds
+               from a shared-memory ring (default) instead of per-lane
+               red.global.add.v4.f32 (the L1TEX-bound variant).
     device_rating_budget
                bytes of HBM the ratings may use (None: all resident).  When
                the partition is larger, it moves to pinned host memory and
@@ -52,6 +55,7 @@ class EngineOptions:
     warps_per_sm: int = 0
     fused: bool | None = None
     device_rating_budget: int | None = None
+    bulk_red: bool = True
     stream_slots: int = 3
 
 
@@ -76,6 +80,7 @@ class Engine:
         self._opt("min_chunk", float(self.options.min_chunk))
         self._opt("timing", 1.0 if self.options.timing else 0.0)
         self._opt("warps_per_sm", float(self.options.warps_per_sm))
+        self._opt("bulk_red", 1.0 if self.options.bulk_red else 0.0)
         f = self.options.fused
         self._opt("fused", -1.0 if f is None else (1.0 if f else 0.0))
         self.n = self.m = self.nnz = 0

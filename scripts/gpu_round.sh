@@ -17,6 +17,7 @@ for w in $WHAT; do
     tests) timeout 1500 python -m pytest tests -m "gpu and not slow" -q -rA > $OUT/tests_gpu.log 2>&1; echo "tests rc=$?" ;;
     slow) timeout 1500 python -m pytest tests -m "slow" -q -rA -s > $OUT/tests_slow.log 2>&1; echo "slow rc=$?" ;;
     bench) timeout 900 $B --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" ;;
+    benchnb) timeout 900 $B --steps 10 --warmup 3 --no-bulk --no-e2e --no-cpu-baseline > $OUT/bench_nobulk.json 2> $OUT/bench_nobulk.err; echo "benchnb rc=$?" ;;
     benchu) timeout 900 $B --steps 10 --warmup 3 --unfused --no-e2e --no-cpu-baseline > $OUT/bench_unfused.json 2> $OUT/bench_unfused.err; echo "benchu rc=$?" ;;
     benchf) timeout 900 $B --steps 10 --warmup 3 --fused --no-e2e --no-cpu-baseline > $OUT/bench_fused.json 2> $OUT/bench_fused.err; echo "benchf rc=$?" ;;
     small)
