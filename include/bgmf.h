@@ -55,7 +55,10 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *   "warps_per_sm" int resident-warp target used to size chunks (0 = occupancy).
  *   "bulk_red"   0/1   1 = each rating's V-row delta leaves through the TMA
  *                      engine (cp.reduce.async.bulk add.f32 from a shared-
- *                      memory ring; default); 0 = per-lane red.global.add.v4.
+ *                      memory ring); 0 = per-lane red.global.add.v4 (default,
+ *                      measured faster: both bound by the SM->L2 interface).
+ *   "sse_wide"   0/1   1 = post-sweep SSE with several ratings' rows in flight
+ *                      per group (default); 0 = the sweep's pipelined walk.
  *   "fused"      -1/0/1  1 = one cooperative launch per outer step (all
  *                      strata, sweeps and SSE passes separated by grid
  *                      barriers); 0 = one launch per stratum sweep / SSE pass;

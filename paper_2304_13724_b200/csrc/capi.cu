@@ -238,6 +238,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "warps_per_sm")) c->warps_per_sm = value < 0 ? 0 : (int)value;
   else if (!strcmp(key, "fused")) c->fused = value < 0 ? -1 : (value != 0.0 ? 1 : 0);
   else if (!strcmp(key, "bulk_red")) c->bulk_red = value != 0.0;
+  else if (!strcmp(key, "sse_wide")) c->sse_wide = value != 0.0;
   else if (!strcmp(key, "fused_max_batch")) c->fused_max_batch = (int64_t)value;
   else return fail(c, BGMF_ERR_ARG, std::string("unknown option ") + key);
   return BGMF_OK;

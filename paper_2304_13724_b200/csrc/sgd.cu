@@ -360,6 +360,70 @@ sse_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
   if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
 }
 
+// Post-sweep SSE, wide form: no update dependency, so each group keeps D
+// ratings' U and V rows in flight at once (D x the memory-level parallelism of
+// the sweep walk).  Its own (L, V4) shape: 8 floats per lane.  U and V are
+// read-only during this kernel, so both go through the L1 (__ldg): a user's
+// run re-reads its U row from L1.  One fp64 atomicAdd per group per block.
+template <int L, int V4, bool kMask, int D>
+__global__ void __launch_bounds__(256, 2)
+sse_wide_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
+                const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
+                const float* __restrict__ val, const float* __restrict__ U,
+                const float* __restrict__ V, int kp, double* __restrict__ sse) {
+  constexpr int GPW = 32 / L;
+  static_assert(L % D == 0, "D must divide L");
+  const int lane = threadIdx.x & 31;
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
+  const int len = (int)(ch.end - ch.begin);
+  const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
+  if (maxlen == 0) return;
+  const Lanes<L, V4, kMask> ln(kp);
+  const float* Ub = U + ch.row_start * kp;
+  const float* Vb = V + ch.col_start * kp;
+  double acc = 0.0;
+  for (int t0 = 0; t0 < maxlen; t0 += L) {
+    int r_l = 0, c_l = 0;
+    float x_l = 0.f;
+    if (t0 + ln.gl < len) {
+      r_l = __ldg(lrow + ch.begin + t0 + ln.gl);
+      c_l = __ldg(lcol + ch.begin + t0 + ln.gl);
+      x_l = __ldg(val + ch.begin + t0 + ln.gl);
+    }
+#pragma unroll 1
+    for (int j0 = 0; j0 < L; j0 += D) {
+      float4 uu[D][V4], vv[D][V4];
+      float x[D];
+      bool ok[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int r = __shfl_sync(kFull, r_l, ln.gbase + j0 + d);
+        const int c = __shfl_sync(kFull, c_l, ln.gbase + j0 + d);
+        x[d] = __shfl_sync(kFull, x_l, ln.gbase + j0 + d);
+        ok[d] = t0 + j0 + d < len;
+#pragma unroll
+        for (int q = 0; q < V4; ++q) {
+          const bool on = ok[d] && ln.on(q);
+          uu[d][q] = on ? __ldg(reinterpret_cast<const float4*>(Ub + (int64_t)r * kp + ln.off(q)))
+                        : zero4();
+          vv[d][q] = on ? __ldg(reinterpret_cast<const float4*>(Vb + (int64_t)c * kp + ln.off(q)))
+                        : zero4();
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const float dot = group_sum<L>(dot_slice<V4>(uu[d], vv[d]));
+        if (ok[d]) {
+          const double e = (double)x[d] - (double)dot;
+          acc += e * e;
+        }
+      }
+    }
+  }
+  if (ln.gl == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
+}
+
 // Out-of-line copies of the two walks for the persistent kernel: register
 // allocation is then per phase, and the call costs once per chunk.
 template <int L, int V4, bool kMask>
@@ -542,6 +606,44 @@ Shape shape_for(int kp) {
 // kp == 4*L*V4: every lane owns a full slice of the row, no predication
 inline bool needs_mask(const Shape& sh, int kp) { return 4 * sh.L * sh.V4 != kp; }
 
+// SSE pass shape: 8 floats per lane (V4 = 2) unless the row is wider than
+// 32 lanes of that; D = ratings in flight per group.
+Shape sse_shape_for(int kp) {
+  const int f4 = kp / 4;
+  int v4 = 2;
+  while (v4 * 32 < f4) v4 <<= 1;
+  if (f4 < v4) v4 = f4 < 1 ? 1 : (f4 >= 2 ? 2 : 1);
+  int L = 1;
+  while (L * v4 < f4) L <<= 1;
+  return {L, v4};
+}
+
+#define BGMF_SSE_SHAPES(X)                                                              \
+  X(1, 1, 1) X(1, 2, 1) X(2, 2, 2) X(4, 2, 4) X(8, 2, 4) X(16, 2, 4) X(32, 2, 4)        \
+  X(32, 4, 4)
+
+void launch_sse_wide(dim3 /*unused*/, cudaStream_t s, const BlockWork* w, int nwork, int total,
+                     const int32_t* lrow, const int32_t* lcol, const float* val, bgmf_ctx* c) {
+  const Shape sh = sse_shape_for(c->kp);
+  const bool mk = 4 * sh.L * sh.V4 != c->kp;
+  const int gpw = 32 / sh.L;
+  const int warps = (total + gpw - 1) / gpw;
+  const dim3 grid((warps + 7) / 8);
+#define BGMF_SSE(LL, VV, DD)                                                                  \
+  if (sh.L == LL && sh.V4 == VV) {                                                            \
+    if (mk)                                                                                   \
+      sse_wide_kernel<LL, VV, true, DD><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val, \
+                                                             c->d_u, c->d_v, c->kp, c->d_sse); \
+    else                                                                                      \
+      sse_wide_kernel<LL, VV, false, DD><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol,    \
+                                                              val, c->d_u, c->d_v, c->kp,     \
+                                                              c->d_sse);                      \
+    return;                                                                                   \
+  }
+  BGMF_SSE_SHAPES(BGMF_SSE)
+#undef BGMF_SSE
+}
+
 // dynamic smem of the bulk sweep: kBulkBufs delta rows per group
 size_t bulk_smem(bgmf_ctx* c, const Shape& sh) {
   return (size_t)(256 / sh.L) * kBulkBufs * c->kp * sizeof(float);
@@ -561,6 +663,8 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
     } else if (sweep)                                                                         \
       sgd_fast_kernel<LL, VV, MM, false><<<grid, 256, 0, s>>>(                                \
           w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad);       \
+    else if (c->sse_wide)                                                                     \
+      launch_sse_wide(grid, s, w, nwork, total, lrow, lcol, val, c);                          \
     else                                                                                      \
       sse_fast_kernel<LL, VV, MM><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val,      \
                                                        c->d_u, c->d_v, c->kp, c->d_sse);      \

@@ -39,8 +39,10 @@ class EngineOptions:
                pass; None (default): the library's choice (per-stratum
                launches -- faster at every config measured on B200).
     bulk_red   V-row deltas leave through the TMA engine as bulk reduce-adds
-               from a shared-memory ring (default) instead of per-lane
-               red.global.add.v4.f32 (the L1TEX-bound variant).
+               from a shared-memory ring instead of per-lane
+               red.global.add.v4.f32.  Off by default: both are bound by the
+               SM->L2 request interface on B200 and the per-lane form measured
+               ~3% faster (profiles/r01_*).
     device_rating_budget
                bytes of HBM the ratings may use (None: all resident).  When
                the partition is larger, it moves to pinned host memory and
@@ -55,7 +57,7 @@ class EngineOptions:
     warps_per_sm: int = 0
     fused: bool | None = None
     device_rating_budget: int | None = None
-    bulk_red: bool = True
+    bulk_red: bool = False
     stream_slots: int = 3
 
 
