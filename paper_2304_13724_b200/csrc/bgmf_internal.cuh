@@ -55,8 +55,8 @@ struct bgmf_ctx {
   int min_chunk = 256;
   bool timing = false;
   int warps_per_sm = 0;
-  bool bulk_red = true;
-  bool sse_wide = true;  // post-sweep SSE with D ratings in flight per group  // V deltas via TMA bulk reduce (cp.reduce.async.bulk)
+  bool bulk_red = false;  // V deltas via TMA bulk reduce (measured slower: SM->L2 bound)
+  bool sse_wide = true;   // post-sweep SSE with D ratings in flight per group
   int fused = -1;      // 1: one cooperative launch per step, 0: per stratum, -1 auto
   int64_t fused_max_batch = 0;  // auto: fuse when a stratum has <= this many ratings
 
