@@ -63,6 +63,7 @@ struct bgmf_ctx {
   // grid + partition
   int64_t n = 0, m = 0, nnz = 0;
   int I = 0, J = 0;
+  int rbits = 0, cbits = 0;              // bits of a block-local row / col index
   std::vector<int64_t> row_bounds, col_bounds, h_offsets;
   bool partitioned = false;
   int32_t* d_lrow = nullptr;
@@ -103,10 +104,15 @@ struct bgmf_ctx {
   bool streaming = false;
   int nslots = 0;
   int64_t slot_cap = 0;                  // ratings per device slot
-  int32_t* h_lrow = nullptr;             // pinned, partitioned order
-  int32_t* h_lcol = nullptr;
+  // pinned host copy of the partition, blocks laid out so that every batch
+  // of the rotating plan is contiguous (diagonals when I == J); packed
+  // 4-byte (lrow << cbits | lcol) records when they fit (8 B per rating)
+  bool packed = false;
+  int32_t* h_lrow = nullptr;             // or the packed records
+  int32_t* h_lcol = nullptr;             // unused when packed
   float* h_val = nullptr;
   uint32_t* h_order = nullptr;
+  std::vector<int64_t> h_pos;            // host start of each block
   std::vector<int32_t*> s_lrow, s_lcol;  // device slots
   std::vector<float*> s_val;
   std::vector<cudaEvent_t> ev_copied, ev_consumed;
@@ -158,11 +164,12 @@ int ensure_step_scratch(bgmf_ctx* ctx, size_t nwork);
 int64_t fast_groups(bgmf_ctx* ctx);
 int launch_piece(bgmf_ctx* ctx, const BlockWork* d_work, int nwork, int chunks,
                  const int32_t* lrow, const int32_t* lcol, const float* val, int iters,
-                 float alpha, float beta, double ratings);
+                 float alpha, float beta, double ratings, int cbits);
 
 // stream.cu -- out-of-core: ratings in pinned host memory, device slot ring
 int stream_enable(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
 void stream_free(bgmf_ctx* ctx);
+int stream_export(bgmf_ctx* ctx, int64_t* order, int32_t* lrows, int32_t* lcols);
 int run_step_stream(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off, int nbatch,
                     int iters, float alpha, float beta);
 // single-block exact kernel used by the stateless drop-ins

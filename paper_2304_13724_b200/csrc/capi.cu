@@ -309,13 +309,7 @@ int bgmf_partition_export(bgmf_ctx* c, int64_t* offsets, int64_t* order, int32_t
   if (offsets) memcpy(offsets, c->h_offsets.data(), c->h_offsets.size() * 8);
   const int64_t n = c->nnz;
   if (n == 0) return BGMF_OK;
-  if (c->streaming) {  // the ratings live in pinned host memory
-    if (lrows) memcpy(lrows, c->h_lrow, n * 4);
-    if (lcols) memcpy(lcols, c->h_lcol, n * 4);
-    if (order)
-      for (int64_t i = 0; i < n; ++i) order[i] = (int64_t)c->h_order[i];
-    return BGMF_OK;
-  }
+  if (c->streaming) return stream_export(c, order, lrows, lcols);  // pinned host copy
   if (lrows) BGMF_CK(c, cudaMemcpyAsync(lrows, c->d_lrow, n * 4, cudaMemcpyDeviceToHost, c->stream));
   if (lcols) BGMF_CK(c, cudaMemcpyAsync(lcols, c->d_lcol, n * 4, cudaMemcpyDeviceToHost, c->stream));
   if (order) {

@@ -280,6 +280,7 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
 
   cudaStream_t s = ctx->stream;
   ctx->n = n; ctx->m = m; ctx->I = I; ctx->J = J; ctx->nnz = nnz;
+  ctx->rbits = rbits; ctx->cbits = cbits;
   ctx->row_bounds.assign(I + 1, 0);
   ctx->col_bounds.assign(J + 1, 0);
   for (int p = 0; p < I; ++p) ctx->row_bounds[p + 1] = ctx->row_bounds[p] + rbase + (p < rextra);

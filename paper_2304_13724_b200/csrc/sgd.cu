@@ -129,6 +129,29 @@ struct Lanes {
 };
 
 __device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+// Rating triple of entry i.  cbits < 0: SoA int32 row / int32 col arrays;
+// cbits >= 0: packed 4-byte (row << cbits | col) records in `lrow` (the
+// out-of-core stream format, 8 B per rating with the fp32 value).
+__device__ __forceinline__ void load_triple(const int32_t* __restrict__ lrow,
+                                            const int32_t* __restrict__ lcol,
+                                            const float* __restrict__ val, int cbits, int64_t i,
+                                            int& r, int& c, float& x) {
+  if (cbits < 0) {
+    r = __ldg(lrow + i);
+    c = __ldg(lcol + i);
+  } else {
+    const uint32_t rc = (uint32_t)__ldg(lrow + i);
+    r = (int)(rc >> cbits);
+    c = (int)(rc & ((1u << cbits) - 1u));
+  }
+  x = __ldg(val + i);
+}
+
+__device__ __forceinline__ int load_rowidx(const int32_t* __restrict__ lrow, int cbits,
+                                           int64_t i) {
+  return cbits < 0 ? __ldg(lrow + i) : (int)((uint32_t)__ldg(lrow + i) >> cbits);
+}
 __device__ __forceinline__ float2 lo2(const float4& a) { return make_float2(a.x, a.y); }
 __device__ __forceinline__ float2 hi2(const float4& a) { return make_float2(a.z, a.w); }
 __device__ __forceinline__ float4 cat4(const float2& a, const float2& b) {
@@ -182,7 +205,7 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
                                              const int32_t* __restrict__ lcol,
                                              const float* __restrict__ val, float* U, float* V,
                                              int kp, float alpha, float beta, int iter,
-                                             unsigned long long* bad,
+                                             unsigned long long* bad, int cbits = -1,
                                              float* sbuf = nullptr) {
   const Lanes<L, V4, kMask> ln(kp);
   int nbulk = 0;  // bulk ops issued by this group (ring position)
@@ -191,23 +214,16 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
   float* Vb = V + ch.col_start * kp;
   int first_row = -1, last_row = -1;
   if (kSweep && len > 0) {
-    const int fr = __ldg(lrow + ch.begin), lr = __ldg(lrow + ch.end - 1);
-    if (ch.begin > ch.bbeg && __ldg(lrow + ch.begin - 1) == fr) first_row = fr;
-    if (ch.end < ch.bend && __ldg(lrow + ch.end) == lr) last_row = lr;
+    const int fr = load_rowidx(lrow, cbits, ch.begin);
+    const int lr = load_rowidx(lrow, cbits, ch.end - 1);
+    if (ch.begin > ch.bbeg && load_rowidx(lrow, cbits, ch.begin - 1) == fr) first_row = fr;
+    if (ch.end < ch.bend && load_rowidx(lrow, cbits, ch.end) == lr) last_row = lr;
   }
   // triple batches A (current) and B (next)
   int rA = 0, cA = 0, rB = 0, cB = 0;
   float xA = 0.f, xB = 0.f;
-  if (ln.gl < len) {
-    rA = __ldg(lrow + ch.begin + ln.gl);
-    cA = __ldg(lcol + ch.begin + ln.gl);
-    xA = __ldg(val + ch.begin + ln.gl);
-  }
-  if (L + ln.gl < len) {
-    rB = __ldg(lrow + ch.begin + L + ln.gl);
-    cB = __ldg(lcol + ch.begin + L + ln.gl);
-    xB = __ldg(val + ch.begin + L + ln.gl);
-  }
+  if (ln.gl < len) load_triple(lrow, lcol, val, cbits, ch.begin + ln.gl, rA, cA, xA);
+  if (L + ln.gl < len) load_triple(lrow, lcol, val, cbits, ch.begin + L + ln.gl, rB, cB, xB);
   int r = __shfl_sync(kFull, rA, ln.gbase);
   int c = __shfl_sync(kFull, cA, ln.gbase);
   float x = __shfl_sync(kFull, xA, ln.gbase);
@@ -309,11 +325,7 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
     // advance the triple batches
     rA = rB; cA = cB; xA = xB;
     const int nb = t0 + 2 * L + ln.gl;
-    if (nb < len) {
-      rB = __ldg(lrow + ch.begin + nb);
-      cB = __ldg(lcol + ch.begin + nb);
-      xB = __ldg(val + ch.begin + nb);
-    }
+    if (nb < len) load_triple(lrow, lcol, val, cbits, ch.begin + nb, rB, cB, xB);
   }
   if (kSweep && kBulk && ln.gl == 0) bulk_wait_all();
   return acc;
@@ -324,7 +336,8 @@ __global__ void __launch_bounds__(256, 2)
 sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
                 const float* __restrict__ val, float* __restrict__ U, float* __restrict__ V,
-                int kp, float alpha, float beta, int iter, unsigned long long* __restrict__ bad) {
+                int kp, float alpha, float beta, int iter, unsigned long long* __restrict__ bad,
+                int cbits) {
   constexpr int GPW = 32 / L;
   extern __shared__ float4 smem_rows[];
   const int lane = threadIdx.x & 31;
@@ -336,7 +349,7 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
   float* sbuf = reinterpret_cast<float*>(smem_rows) +
                 (size_t)((threadIdx.x >> 5) * GPW + lane / L) * kBulkBufs * kp;
   walk_chunk<L, V4, kMask, true, kBulk>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter,
-                                        bad, sbuf);
+                                        bad, cbits, sbuf);
 }
 
 // Post-sweep SSE of each block: sum over the chunk of (x - u.v)^2 in fp64,
@@ -346,7 +359,7 @@ __global__ void __launch_bounds__(256, 2)
 sse_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
                 const float* __restrict__ val, const float* __restrict__ U,
-                const float* __restrict__ V, int kp, double* __restrict__ sse) {
+                const float* __restrict__ V, int kp, double* __restrict__ sse, int cbits) {
   constexpr int GPW = 32 / L;
   const int lane = threadIdx.x & 31;
   const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -356,7 +369,7 @@ sse_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
   if (maxlen == 0) return;
   const double acc = walk_chunk<L, V4, kMask, false>(ch, maxlen, lrow, lcol, val,
                                                      const_cast<float*>(U), const_cast<float*>(V),
-                                                     kp, 0.f, 0.f, 0, nullptr);
+                                                     kp, 0.f, 0.f, 0, nullptr, cbits);
   if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
 }
 
@@ -370,7 +383,7 @@ __global__ void __launch_bounds__(256, 2)
 sse_wide_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
                 const float* __restrict__ val, const float* __restrict__ U,
-                const float* __restrict__ V, int kp, double* __restrict__ sse) {
+                const float* __restrict__ V, int kp, double* __restrict__ sse, int cbits) {
   constexpr int GPW = 32 / L;
   static_assert(L % D == 0, "D must divide L");
   const int lane = threadIdx.x & 31;
@@ -386,11 +399,7 @@ sse_wide_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
   for (int t0 = 0; t0 < maxlen; t0 += L) {
     int r_l = 0, c_l = 0;
     float x_l = 0.f;
-    if (t0 + ln.gl < len) {
-      r_l = __ldg(lrow + ch.begin + t0 + ln.gl);
-      c_l = __ldg(lcol + ch.begin + t0 + ln.gl);
-      x_l = __ldg(val + ch.begin + t0 + ln.gl);
-    }
+    if (t0 + ln.gl < len) load_triple(lrow, lcol, val, cbits, ch.begin + t0 + ln.gl, r_l, c_l, x_l);
 #pragma unroll 1
     for (int j0 = 0; j0 < L; j0 += D) {
       float4 uu[D][V4], vv[D][V4];
@@ -622,8 +631,9 @@ Shape sse_shape_for(int kp) {
   X(1, 1, 1) X(1, 2, 1) X(2, 2, 2) X(4, 2, 4) X(8, 2, 4) X(16, 2, 4) X(32, 2, 4)        \
   X(32, 4, 4)
 
-void launch_sse_wide(dim3 /*unused*/, cudaStream_t s, const BlockWork* w, int nwork, int total,
-                     const int32_t* lrow, const int32_t* lcol, const float* val, bgmf_ctx* c) {
+void launch_sse_wide(cudaStream_t s, const BlockWork* w, int nwork, int total,
+                     const int32_t* lrow, const int32_t* lcol, const float* val, bgmf_ctx* c,
+                     int cbits) {
   const Shape sh = sse_shape_for(c->kp);
   const bool mk = 4 * sh.L * sh.V4 != c->kp;
   const int gpw = 32 / sh.L;
@@ -633,11 +643,12 @@ void launch_sse_wide(dim3 /*unused*/, cudaStream_t s, const BlockWork* w, int nw
   if (sh.L == LL && sh.V4 == VV) {                                                            \
     if (mk)                                                                                   \
       sse_wide_kernel<LL, VV, true, DD><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val, \
-                                                             c->d_u, c->d_v, c->kp, c->d_sse); \
+                                                             c->d_u, c->d_v, c->kp, c->d_sse, \
+                                                             cbits);                          \
     else                                                                                      \
       sse_wide_kernel<LL, VV, false, DD><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol,    \
                                                               val, c->d_u, c->d_v, c->kp,     \
-                                                              c->d_sse);                      \
+                                                              c->d_sse, cbits);               \
     return;                                                                                   \
   }
   BGMF_SSE_SHAPES(BGMF_SSE)
@@ -651,7 +662,7 @@ size_t bulk_smem(bgmf_ctx* c, const Shape& sh) {
 
 void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, const BlockWork* w,
                      int nwork, int total, const int32_t* lrow, const int32_t* lcol,
-                     const float* val, bgmf_ctx* c, float a, float b, int it) {
+                     const float* val, bgmf_ctx* c, float a, float b, int it, int cbits = -1) {
   const bool mk = needs_mask(sh, c->kp);
 #define BGMF_CASE(LL, VV, MM)                                                                 \
   if (sh.L == LL && sh.V4 == VV && mk == MM) {                                                \
@@ -659,15 +670,15 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
       cudaFuncSetAttribute(&sgd_fast_kernel<LL, VV, MM, true>,                               \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem(c, sh)); \
       sgd_fast_kernel<LL, VV, MM, true><<<grid, 256, bulk_smem(c, sh), s>>>(                  \
-          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad);       \
+          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
     } else if (sweep)                                                                         \
       sgd_fast_kernel<LL, VV, MM, false><<<grid, 256, 0, s>>>(                                \
-          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad);       \
+          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
     else if (c->sse_wide)                                                                     \
-      launch_sse_wide(grid, s, w, nwork, total, lrow, lcol, val, c);                          \
+      launch_sse_wide(s, w, nwork, total, lrow, lcol, val, c, cbits);                          \
     else                                                                                      \
       sse_fast_kernel<LL, VV, MM><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val,      \
-                                                       c->d_u, c->d_v, c->kp, c->d_sse);      \
+                                                       c->d_u, c->d_v, c->kp, c->d_sse, cbits);      \
     return;                                                                                   \
   }
   BGMF_SHAPES(BGMF_CASE)
@@ -889,7 +900,7 @@ int64_t fast_groups(bgmf_ctx* c) { return sweep_groups(c, shape_for(c->kp)); }
 // ratings live at (lrow, lcol, val) -- the streaming path's unit of work.
 int launch_piece(bgmf_ctx* c, const BlockWork* d_work, int nwork, int chunks,
                  const int32_t* lrow, const int32_t* lcol, const float* val, int iters,
-                 float alpha, float beta, double ratings) {
+                 float alpha, float beta, double ratings, int cbits) {
   if (chunks == 0) return BGMF_OK;
   const Shape sh = shape_for(c->kp);
   const int gpw = 32 / sh.L;
@@ -899,13 +910,13 @@ int launch_piece(bgmf_ctx* c, const BlockWork* d_work, int nwork, int chunks,
     TimedLaunch* slot = nullptr;
     if (c->timing) record_begin(c, 0, ratings * (12.0 + 16.0 * c->k), &slot);
     launch_fast_ptr(true, sh, grid, c->stream, d_work, nwork, chunks, lrow, lcol, val, c, alpha,
-                    beta, it);
+                    beta, it, cbits);
     if (slot) record_end(c, slot);
   }
   TimedLaunch* slot = nullptr;
   if (c->timing) record_begin(c, 1, 0.0, &slot);
   launch_fast_ptr(false, sh, grid, c->stream, d_work, nwork, chunks, lrow, lcol, val, c, alpha,
-                  beta, 0);
+                  beta, 0, cbits);
   if (slot) record_end(c, slot);
   BGMF_CK(c, cudaGetLastError());
   return BGMF_OK;

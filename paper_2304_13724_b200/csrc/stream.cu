@@ -2,13 +2,20 @@
 // memory and stream through a ring of device slots (the
 // paper's motivating case).  Factors stay resident.
 //
+// Host layout.  For square grids the host copy is re-laid out by diagonal:
+// batch t of step s is the diagonal d = (s + t) mod P (blocks ((j+d) mod P, j),
+// j ascending -- exactly plan_step's order), so every batch, and every piece
+// of it, is ONE contiguous range: one cudaMemcpyAsync per array per piece.
+// When a block-local (row, col) fits 32 bits the records are packed as
+// (row << cbits | col) + fp32 value: 8 B per rating instead of 12 over PCIe.
+//
 // A step is cut into "pieces": consecutive blocks of one batch whose ratings
 // fit one slot.  Blocks of a batch own disjoint U/V slices, so any grouping
 // of a batch's blocks into sequential pieces is the same algorithm, and a
 // block's post-sweep SSE can run right after its own sweep.  Piece p uses slot
-// p % nslots: a side stream copies piece p+1.. (H2D from pinned memory, one
-// memcpy per block and array) while the compute stream sweeps piece p;
-// events order "slot copied" -> "sweep" -> "slot free for the next copy".
+// p % nslots: a side stream copies piece p+1.. (H2D from pinned memory) while
+// the compute stream sweeps piece p; events order "slot copied" -> "sweep" ->
+// "slot free for the next copy".
 
 #include <cstring>
 
@@ -31,37 +38,81 @@ void stream_free(bgmf_ctx* c) {
   c->h_lrow = c->h_lcol = nullptr;
   c->h_val = nullptr;
   c->h_order = nullptr;
+  c->h_pos.clear();
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   c->copy_stream = nullptr;
   c->streaming = false;
+  c->packed = false;
   c->nslots = 0;
   c->slot_cap = 0;
 }
+
+namespace {
+
+__global__ void pack_records(const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
+                             int64_t n, int cbits, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)(((uint32_t)lrow[i] << cbits) | (uint32_t)lcol[i]);
+}
+
+}  // namespace
 
 int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
   if (!c->partitioned) return fail(c, BGMF_ERR_STATE, "bgmf_partition has not been called");
   if (c->exact) return fail(c, BGMF_ERR_STATE, "streaming is fast-mode only");
   if (c->streaming) return fail(c, BGMF_ERR_STATE, "already streaming");
   if (nslots < 2 || nslots > 8) return fail(c, BGMF_ERR_ARG, "nslots must be in [2, 8]");
+  const int nb = c->I * c->J;
   int64_t max_block = 0;
-  for (size_t b = 0; b + 1 < c->h_offsets.size(); ++b) {
+  for (int b = 0; b < nb; ++b) {
     const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
     if (cnt > max_block) max_block = cnt;
   }
   if (slot_ratings < max_block || slot_ratings < 1)
     return fail(c, BGMF_ERR_ARG, "slot smaller than the largest block (" +
                                      std::to_string(max_block) + " ratings)");
-  const size_t N = (size_t)(c->nnz > 0 ? c->nnz : 1);
   cudaStream_t s = c->stream;
+  c->packed = c->rbits + c->cbits <= 32;
+  // host block order: diagonals of the rotating plan for square grids
+  std::vector<int> order;
+  order.reserve(nb);
+  if (c->I == c->J) {
+    for (int d = 0; d < c->I; ++d)
+      for (int j = 0; j < c->J; ++j) order.push_back(((j + d) % c->I) * c->J + j);
+  } else {
+    for (int b = 0; b < nb; ++b) order.push_back(b);
+  }
+  c->h_pos.assign(nb, 0);
+  int64_t pos = 0;
+  for (int b : order) {
+    c->h_pos[b] = pos;
+    pos += c->h_offsets[b + 1] - c->h_offsets[b];
+  }
+  const size_t N = (size_t)(c->nnz > 0 ? c->nnz : 1);
   BGMF_CK(c, cudaMallocHost(&c->h_lrow, N * 4));
-  BGMF_CK(c, cudaMallocHost(&c->h_lcol, N * 4));
+  if (!c->packed) BGMF_CK(c, cudaMallocHost(&c->h_lcol, N * 4));
   BGMF_CK(c, cudaMallocHost(&c->h_val, N * 4));
   BGMF_CK(c, cudaMallocHost(&c->h_order, N * 4));
-  if (c->nnz > 0) {
-    BGMF_CK(c, cudaMemcpyAsync(c->h_lrow, c->d_lrow, c->nnz * 4, cudaMemcpyDeviceToHost, s));
-    BGMF_CK(c, cudaMemcpyAsync(c->h_lcol, c->d_lcol, c->nnz * 4, cudaMemcpyDeviceToHost, s));
-    BGMF_CK(c, cudaMemcpyAsync(c->h_val, c->d_val, c->nnz * 4, cudaMemcpyDeviceToHost, s));
-    BGMF_CK(c, cudaMemcpyAsync(c->h_order, c->d_order, c->nnz * 4, cudaMemcpyDeviceToHost, s));
+  if (c->packed && c->nnz > 0) {  // pack in place of the (no longer needed) lrow
+    int32_t* rec = nullptr;
+    BGMF_CK(c, cudaMalloc(&rec, N * 4));
+    pack_records<<<c->num_sms * 8, 256, 0, s>>>(c->d_lrow, c->d_lcol, c->nnz, c->cbits, rec);
+    BGMF_CK(c, cudaGetLastError());
+    BGMF_CK(c, cudaStreamSynchronize(s));
+    cudaFree(c->d_lrow);
+    c->d_lrow = rec;
+  }
+  for (int b : order) {  // D2H block by block into the diagonal layout
+    const int64_t lo = c->h_offsets[b], cnt = c->h_offsets[b + 1] - lo, dst = c->h_pos[b];
+    if (cnt == 0) continue;
+    BGMF_CK(c, cudaMemcpyAsync(c->h_lrow + dst, c->d_lrow + lo, cnt * 4, cudaMemcpyDeviceToHost, s));
+    if (!c->packed)
+      BGMF_CK(c, cudaMemcpyAsync(c->h_lcol + dst, c->d_lcol + lo, cnt * 4, cudaMemcpyDeviceToHost,
+                                 s));
+    BGMF_CK(c, cudaMemcpyAsync(c->h_val + dst, c->d_val + lo, cnt * 4, cudaMemcpyDeviceToHost, s));
+    BGMF_CK(c, cudaMemcpyAsync(c->h_order + dst, c->d_order + lo, cnt * 4, cudaMemcpyDeviceToHost,
+                               s));
   }
   BGMF_CK(c, cudaStreamSynchronize(s));
   cudaFree(c->d_lrow); cudaFree(c->d_lcol); cudaFree(c->d_val); cudaFree(c->d_order);
@@ -74,7 +125,7 @@ int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
     int32_t *a = nullptr, *b = nullptr;
     float* v = nullptr;
     BGMF_CK(c, cudaMalloc(&a, (size_t)slot_ratings * 4));
-    BGMF_CK(c, cudaMalloc(&b, (size_t)slot_ratings * 4));
+    if (!c->packed) BGMF_CK(c, cudaMalloc(&b, (size_t)slot_ratings * 4));
     BGMF_CK(c, cudaMalloc(&v, (size_t)slot_ratings * 4));
     c->s_lrow.push_back(a);
     c->s_lcol.push_back(b);
@@ -87,6 +138,27 @@ int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
   }
   BGMF_CK(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
   c->streaming = true;
+  return BGMF_OK;
+}
+
+// Host copies for bgmf_partition_export while streaming (partitioned order).
+int stream_export(bgmf_ctx* c, int64_t* order, int32_t* lrows, int32_t* lcols) {
+  const int nb = c->I * c->J;
+  const uint32_t cmask = c->cbits >= 32 ? 0xFFFFFFFFu : ((1u << c->cbits) - 1u);
+  for (int b = 0; b < nb; ++b) {
+    const int64_t lo = c->h_offsets[b], cnt = c->h_offsets[b + 1] - lo, src = c->h_pos[b];
+    for (int64_t i = 0; i < cnt; ++i) {
+      if (c->packed) {
+        const uint32_t rc = (uint32_t)c->h_lrow[src + i];
+        if (lrows) lrows[lo + i] = (int32_t)(rc >> c->cbits);
+        if (lcols) lcols[lo + i] = (int32_t)(rc & cmask);
+      } else {
+        if (lrows) lrows[lo + i] = c->h_lrow[src + i];
+        if (lcols) lcols[lo + i] = c->h_lcol[src + i];
+      }
+      if (order) order[lo + i] = (int64_t)c->h_order[src + i];
+    }
+  }
   return BGMF_OK;
 }
 
@@ -111,14 +183,12 @@ int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, 
 
   // 1. cut every batch into pieces that fit a slot; slot-relative work items
   std::vector<Piece> pieces;
-  std::vector<int> piece_first_q;  // first plan position of each piece
   int w = 0;
   for (int t = 0; t < nbatch; ++t) {
     int q = batch_off[t];
     while (q < batch_off[t + 1]) {
-      // greedy: take blocks while they fit
       int q_end = q;
-      int64_t fill = 0, piece_nnz = 0;
+      int64_t fill = 0;
       int nonempty = 0;
       while (q_end < batch_off[t + 1]) {
         const int b = plan[q_end];
@@ -129,9 +199,8 @@ int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, 
         nonempty += cnt > 0;
         ++q_end;
       }
-      piece_nnz = fill;
       const int64_t slots = groups - nonempty > 0 ? groups - nonempty : 1;
-      int64_t cl = (piece_nnz + slots - 1) / slots;
+      int64_t cl = (fill + slots - 1) / slots;
       if (cl < c->min_chunk) cl = c->min_chunk;
       Piece pc{w, 0, 0, (int)(pieces.size() % c->nslots), 0.0};
       int64_t off = 0;
@@ -155,7 +224,6 @@ int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, 
       }
       pc.nw = w - pc.w0;
       pieces.push_back(pc);
-      piece_first_q.push_back(q);
       q = q_end;
     }
   }
@@ -170,27 +238,44 @@ int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, 
   BGMF_CK(c, cudaEventRecord(ready, s));
   BGMF_CK(c, cudaStreamWaitEvent(cs, ready, 0));
 
+  // one H2D per array for a run of host-contiguous blocks
+  auto copy_run = [&](int sl, int64_t dst, int64_t src, int64_t cnt) -> int {
+    BGMF_CK(c, cudaMemcpyAsync(c->s_lrow[sl] + dst, c->h_lrow + src, cnt * 4,
+                               cudaMemcpyHostToDevice, cs));
+    if (!c->packed)
+      BGMF_CK(c, cudaMemcpyAsync(c->s_lcol[sl] + dst, c->h_lcol + src, cnt * 4,
+                                 cudaMemcpyHostToDevice, cs));
+    BGMF_CK(c, cudaMemcpyAsync(c->s_val[sl] + dst, c->h_val + src, cnt * 4,
+                               cudaMemcpyHostToDevice, cs));
+    c->h2d_bytes += (c->packed ? 8.0 : 12.0) * (double)cnt;
+    return BGMF_OK;
+  };
+
   // 2. pipeline: copy piece p on the side stream, compute it on the main one
   for (size_t p = 0; p < pieces.size(); ++p) {
     const Piece& pc = pieces[p];
     const int sl = pc.slot;
     if (p >= (size_t)c->nslots) BGMF_CK(c, cudaStreamWaitEvent(cs, c->ev_consumed[sl], 0));
+    int64_t run_dst = 0, run_src = -1, run_cnt = 0;
     for (int i = 0; i < pc.nw; ++i) {
       const BlockWork& bw = c->h_work[pc.w0 + i];
-      const int64_t src = c->h_offsets[bw.block_id];
+      const int64_t src = c->h_pos[bw.block_id];
       const int64_t cnt = bw.end - bw.begin;
-      BGMF_CK(c, cudaMemcpyAsync(c->s_lrow[sl] + bw.begin, c->h_lrow + src, cnt * 4,
-                                 cudaMemcpyHostToDevice, cs));
-      BGMF_CK(c, cudaMemcpyAsync(c->s_lcol[sl] + bw.begin, c->h_lcol + src, cnt * 4,
-                                 cudaMemcpyHostToDevice, cs));
-      BGMF_CK(c, cudaMemcpyAsync(c->s_val[sl] + bw.begin, c->h_val + src, cnt * 4,
-                                 cudaMemcpyHostToDevice, cs));
-      c->h2d_bytes += 12.0 * (double)cnt;
+      if (run_src >= 0 && src == run_src + run_cnt && bw.begin == run_dst + run_cnt) {
+        run_cnt += cnt;  // extends the contiguous run
+        continue;
+      }
+      if (run_src >= 0 && (rc = copy_run(sl, run_dst, run_src, run_cnt))) break;
+      run_dst = bw.begin;
+      run_src = src;
+      run_cnt = cnt;
     }
+    if (!rc && run_src >= 0) rc = copy_run(sl, run_dst, run_src, run_cnt);
+    if (rc) { cudaEventDestroy(ready); return rc; }
     BGMF_CK(c, cudaEventRecord(c->ev_copied[sl], cs));
     BGMF_CK(c, cudaStreamWaitEvent(s, c->ev_copied[sl], 0));
     rc = launch_piece(c, c->d_work + pc.w0, pc.nw, pc.chunks, c->s_lrow[sl], c->s_lcol[sl],
-                      c->s_val[sl], iters, alpha, beta, pc.ratings);
+                      c->s_val[sl], iters, alpha, beta, pc.ratings, c->packed ? c->cbits : -1);
     if (rc) { cudaEventDestroy(ready); return rc; }
     BGMF_CK(c, cudaEventRecord(c->ev_consumed[sl], s));
   }

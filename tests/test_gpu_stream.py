@@ -35,8 +35,9 @@ def test_stream_matches_oracle(budget_frac, slots):
     dtr = np.abs(np.array([s.train_rmse for s in res.trace]) - [s["train_rmse"] for s in otr])
     dte = np.abs(np.array([s.test_rmse for s in res.trace]) - [s["test_rmse"] for s in otr])
     assert dtr.max() <= TOL and dte.max() <= TOL
-    # every epoch streams every rating once (+ the adaptive/none extra passes: none here)
-    assert blocked.engine.streamed_bytes() == pytest.approx(12.0 * len(tr) * 5)
+    # every epoch streams every rating once, as packed 8-byte records
+    # (block-local row << cbits | col, fp32 value)
+    assert blocked.engine.streamed_bytes() == pytest.approx(8.0 * len(tr) * 5)
 
 
 def test_stream_partition_export_and_sse_only_pass():
