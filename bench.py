@@ -221,7 +221,8 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     # the engine launches on torch's current stream so torch events bracket the work
     fused = True if args.fused else (False if args.unfused else None)
-    eng2 = bm.Engine(bm.EngineOptions(device=dev, fused=fused, bulk_red=not args.no_bulk),
+    eng2 = bm.Engine(bm.EngineOptions(device=dev, fused=fused, bulk_red=args.bulk,
+                                      sse_wide=args.sse_wide),
                      stream=stream.cuda_stream)
     eng2.partition(d.rows, d.cols, d.values, w.n, w.m, w.grid, w.grid)
     eng2.init_factors(w.n, w.m, w.k, w.seed)
@@ -410,8 +411,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--unfused", action="store_true",
                     help="force one launch per stratum sweep / SSE pass")
-    ap.add_argument("--no-bulk", action="store_true",
-                    help="per-lane red.global.add for V deltas instead of TMA bulk reduce")
+    ap.add_argument("--bulk", action="store_true",
+                    help="V deltas via TMA bulk reduce instead of per-lane red.global.add")
+    ap.add_argument("--sse-wide", action="store_true",
+                    help="post-sweep SSE with 4 ratings in flight per group")
     ap.add_argument("--fused", action="store_true",
                     help="force one cooperative launch per epoch (default: auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -58,7 +58,8 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      memory ring); 0 = per-lane red.global.add.v4 (default,
  *                      measured faster: both bound by the SM->L2 interface).
  *   "sse_wide"   0/1   1 = post-sweep SSE with several ratings' rows in flight
- *                      per group (default); 0 = the sweep's pipelined walk.
+ *                      per group; 0 = the sweep's pipelined walk (default,
+ *                      measured faster on C4).
  *   "fused"      -1/0/1  1 = one cooperative launch per outer step (all
  *                      strata, sweeps and SSE passes separated by grid
  *                      barriers); 0 = one launch per stratum sweep / SSE pass;

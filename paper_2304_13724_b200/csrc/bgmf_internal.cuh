@@ -56,7 +56,7 @@ struct bgmf_ctx {
   bool timing = false;
   int warps_per_sm = 0;
   bool bulk_red = false;  // V deltas via TMA bulk reduce (measured slower: SM->L2 bound)
-  bool sse_wide = true;   // post-sweep SSE with D ratings in flight per group
+  bool sse_wide = false;  // post-sweep SSE with D ratings in flight (measured slower)
   int fused = -1;      // 1: one cooperative launch per step, 0: per stratum, -1 auto
   int64_t fused_max_batch = 0;  // auto: fuse when a stratum has <= this many ratings
 

@@ -43,6 +43,8 @@ class EngineOptions:
                red.global.add.v4.f32.  Off by default: both are bound by the
                SM->L2 request interface on B200 and the per-lane form measured
                ~3% faster (profiles/r01_*).
+    sse_wide   post-sweep SSE with 4 ratings' rows in flight per group
+               (measured slower than the pipelined walk on C4; off).
     device_rating_budget
                bytes of HBM the ratings may use (None: all resident).  When
                the partition is larger, it moves to pinned host memory and
@@ -58,6 +60,7 @@ class EngineOptions:
     fused: bool | None = None
     device_rating_budget: int | None = None
     bulk_red: bool = False
+    sse_wide: bool = False
     stream_slots: int = 3
 
 
@@ -83,6 +86,7 @@ class Engine:
         self._opt("timing", 1.0 if self.options.timing else 0.0)
         self._opt("warps_per_sm", float(self.options.warps_per_sm))
         self._opt("bulk_red", 1.0 if self.options.bulk_red else 0.0)
+        self._opt("sse_wide", 1.0 if self.options.sse_wide else 0.0)
         f = self.options.fused
         self._opt("fused", -1.0 if f is None else (1.0 if f else 0.0))
         self.n = self.m = self.nnz = 0

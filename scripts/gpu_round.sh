@@ -17,7 +17,20 @@ for w in $WHAT; do
     tests) timeout 1500 python -m pytest tests -m "gpu and not slow" -q -rA > $OUT/tests_gpu.log 2>&1; echo "tests rc=$?" ;;
     slow) timeout 1500 python -m pytest tests -m "slow" -q -rA -s > $OUT/tests_slow.log 2>&1; echo "slow rc=$?" ;;
     bench) timeout 900 $B --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" ;;
-    benchnb) timeout 900 $B --steps 10 --warmup 3 --no-bulk --no-e2e --no-cpu-baseline > $OUT/bench_nobulk.json 2> $OUT/bench_nobulk.err; echo "benchnb rc=$?" ;;
+    benchx) for f in "--bulk" "--sse-wide"; do timeout 900 $B --steps 10 --warmup 3 $f --no-e2e --no-cpu-baseline >> $OUT/bench_variants.jsonl 2>> $OUT/bench_variants.err; done; echo "benchx rc=$?" ;;
+    h2d) timeout 300 python -c "
+import torch,time
+for mb in (64,256,1024,4096):
+    a=torch.empty(mb<<20,dtype=torch.uint8).pin_memory(); b=torch.empty(mb<<20,dtype=torch.uint8,device='cuda')
+    b.copy_(a,non_blocking=True); torch.cuda.synchronize()
+    e0=torch.cuda.Event(enable_timing=True); e1=torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5): b.copy_(a,non_blocking=True)
+    e1.record(); torch.cuda.synchronize(); print('h2d',mb,'MB',5*mb/1024/(e0.elapsed_time(e1)/1e3),'GB/s')
+    e0.record()
+    for _ in range(5): a.copy_(b,non_blocking=True)
+    e1.record(); torch.cuda.synchronize(); print('d2h',mb,'MB',5*mb/1024/(e0.elapsed_time(e1)/1e3),'GB/s')
+" > $OUT/h2d.txt 2>&1; nvidia-smi -q | grep -iA3 "pcie gen\|link width" >> $OUT/h2d.txt; echo "h2d rc=$?" ;;
     benchu) timeout 900 $B --steps 10 --warmup 3 --unfused --no-e2e --no-cpu-baseline > $OUT/bench_unfused.json 2> $OUT/bench_unfused.err; echo "benchu rc=$?" ;;
     benchf) timeout 900 $B --steps 10 --warmup 3 --fused --no-e2e --no-cpu-baseline > $OUT/bench_fused.json 2> $OUT/bench_fused.err; echo "benchf rc=$?" ;;
     small)
