@@ -58,6 +58,8 @@ struct bgmf_ctx {
   bool bulk_red = false;  // V deltas via TMA bulk reduce (measured slower: SM->L2 bound)
   bool sse_wide = false;  // post-sweep SSE with D ratings in flight (measured slower)
   int fused = -1;      // 1: one cooperative launch per step, 0: per stratum, -1 auto
+  int groups_key = -1;                // sweep_groups() cache
+  int64_t groups_cache = 0;
   int64_t fused_max_batch = 0;  // auto: fuse when a stratum has <= this many ratings
 
   // grid + partition

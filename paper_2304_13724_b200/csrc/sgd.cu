@@ -667,8 +667,13 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
 #define BGMF_CASE(LL, VV, MM)                                                                 \
   if (sh.L == LL && sh.V4 == VV && mk == MM) {                                                \
     if (sweep && c->bulk_red) {                                                               \
-      cudaFuncSetAttribute(&sgd_fast_kernel<LL, VV, MM, true>,                               \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem(c, sh)); \
+      static int smem_set = 0;                                                                \
+      if (smem_set < (int)bulk_smem(c, sh)) {                                                 \
+        cudaFuncSetAttribute(&sgd_fast_kernel<LL, VV, MM, true>,                             \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
+                             (int)bulk_smem(c, sh));                                          \
+        smem_set = (int)bulk_smem(c, sh);                                                     \
+      }                                                                                       \
       sgd_fast_kernel<LL, VV, MM, true><<<grid, 256, bulk_smem(c, sh), s>>>(                  \
           w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
     } else if (sweep)                                                                         \
@@ -781,8 +786,18 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
   return BGMF_OK;
 }
 
+// One-wave capacity of the sweep kernel in worker groups (cached: the
+// occupancy query and the smem attribute are host calls that must stay out of
+// the per-piece path so the copy stream can run ahead).
 int64_t sweep_groups(bgmf_ctx* c, const Shape& sh) {
-  return (int64_t)c->num_sms * resident_ctas(c, sweep_kernel_ptr(sh, c->kp, c->bulk_red), c->bulk_red ? bulk_smem(c, sh) : 0) * 8 * (32 / sh.L);
+  const int key = (c->warps_per_sm * 4096 + c->kp) * 2 + (c->bulk_red ? 1 : 0);
+  if (c->groups_key != key) {
+    const size_t smem = c->bulk_red ? bulk_smem(c, sh) : 0;
+    const int ctas = resident_ctas(c, sweep_kernel_ptr(sh, c->kp, c->bulk_red), smem);
+    c->groups_cache = (int64_t)c->num_sms * ctas * 8 * (32 / sh.L);
+    c->groups_key = key;
+  }
+  return c->groups_cache;
 }
 
 }  // namespace
@@ -823,8 +838,9 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, in
   // (small strata); big strata run faster as separate sweep / SSE launches.
   const int64_t per_batch = nbatch > 0 ? c->nnz / nbatch : c->nnz;
   const bool fused = c->fused > 0 || (c->fused < 0 && per_batch <= c->fused_max_batch);
-  const int ctas_per_sm = fused ? resident_ctas(c, ep) : resident_ctas(c, sweep_kernel_ptr(sh, c->kp, c->bulk_red), c->bulk_red ? bulk_smem(c, sh) : 0);
-  const int64_t groups = (int64_t)c->num_sms * ctas_per_sm * 8 * gpw;
+  const int ctas_per_sm = fused ? resident_ctas(c, ep) : 0;
+  const int64_t groups =
+      fused ? (int64_t)c->num_sms * ctas_per_sm * 8 * gpw : sweep_groups(c, sh);
   std::vector<BatchRange> ranges;
   int rc = build_work(c, plan, batch_off, nbatch, groups, ranges);
   if (rc) return rc;
