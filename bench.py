@@ -187,7 +187,7 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or os.environ.get("BGMF_FORCE_DIST"):
         from paper_2304_13724_b200 import distributed as D
 
         return D.bench_main(args)
@@ -208,10 +208,12 @@ def run_ours(args):
         bm.train_blocked(d, bm.TrainConfig(k=w.k, grid_i=w.grid, grid_j=w.grid, outer_steps=1),
                          early_stop=False)  # warm the CUDA context / allocator
         torch.cuda.synchronize()
+        os.environ["BGMF_PROFILE"] = "1"  # phase breakdown on stderr
         t0 = time.perf_counter()
         res = bm.train_blocked(d, cfg, early_stop=False)
         torch.cuda.synchronize()
         t_e2e = time.perf_counter() - t0
+        del os.environ["BGMF_PROFILE"]
         e2e_val = nnz * args.steps / t_e2e
         h2d = (nnz * 24 + (w.n + w.m) * w.k * 8) / args.steps
         d2h = ((w.n + w.m) * w.k * 8 + args.steps * w.grid * w.grid * 8) / args.steps

@@ -290,6 +290,8 @@ def bench_main(args):
         step += 1
     torch.cuda.synchronize()
     dist.barrier()
+    shard.eng.set_timing(True)
+    shard.eng.kernel_stats(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
@@ -297,13 +299,25 @@ def bench_main(args):
         step += 1
     e1.record(stream)
     torch.cuda.synchronize()
+    st = shard.eng.kernel_stats(reset=True)
     ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{device}")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     dist.barrier()
     total_ms = float(ms.item())
     if rank == 0:
+        hbm = 6553.0
+        try:
+            import json as _j
+
+            hbm = float(_j.load(open(os.path.join(os.path.dirname(os.path.dirname(
+                os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"])
+        except Exception:
+            pass
+        launch_ms = st["sgd_ms"] / max(st["sgd_launches"], 1)
+        achieved = st["sgd_alg_bytes"] / max(st["sgd_launches"], 1) / (launch_ms / 1e3) / 1e9
         line = {
-            "metric": "SGD rating-updates/sec (epoch)", "value": nnz * args.steps / (total_ms / 1e3),
+            "metric": "SGD rating-updates/sec (epoch)",
+            "value": nnz * args.steps / (total_ms / 1e3),
             "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (workloads.lowrank)",
@@ -311,7 +325,12 @@ def bench_main(args):
                        "grid": f"{w.grid}x{w.grid}",
                        "parallelism": f"U-resident/V-rotating x{world} (NCCL P2P)",
                        "l2": "inputs larger than L2"},
-            "e2e": None, "gen_seconds": t_gen,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None,
+                         "kernel": "sgd_fast_kernel (rank 0)"},
+            "e2e": None, "cpu_baseline": None,
+            "gpu_launches": int(st["sgd_launches"] + st["sse_launches"]),
+            "gen_seconds": t_gen,
         }
         print(json.dumps(line))
     dist.destroy_process_group()

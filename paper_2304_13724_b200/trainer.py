@@ -11,6 +11,8 @@ and only the P^2 per-block SSEs come back.
 from __future__ import annotations
 
 import math
+import os
+import sys
 import time
 from dataclasses import dataclass
 from typing import Callable, Literal, Optional
@@ -86,8 +88,11 @@ def train_blocked(d: RatingsDataset, cfg: TrainConfig, test: Optional[RatingsDat
     of ``d`` with the same grid.  ``cfg.workers`` is ignored: concurrency is
     the GPU's.
     """
+    prof = _Phases() if os.environ.get("BGMF_PROFILE") else None
     if blocked is None:
         blocked = BlockedDataset(d, make_grid(d.n, d.m, cfg.grid_i, cfg.grid_j), options)
+    if prof:
+        prof.mark("partition (H2D + GPU sort)")
     elif (blocked.grid.grid_i, blocked.grid.grid_j) != (cfg.grid_i, cfg.grid_j) \
             or blocked.dataset is not d:
         raise ValueError("blocked must partition d with cfg's grid")
@@ -95,6 +100,8 @@ def train_blocked(d: RatingsDataset, cfg: TrainConfig, test: Optional[RatingsDat
     # init_factors(n, m, k, seed) generated in HBM: numpy's PCG64 stream
     # reproduced bit-for-bit on the device (no 2*(n+m)*k*8-byte upload)
     eng.init_factors(d.n, d.m, cfg.k, cfg.seed)
+    if prof:
+        prof.mark("init_factors (device PCG64)")
 
     evaluator = HoldoutEvaluator(d, test) if test is not None and len(test) > 0 else None
     if evaluator is not None:
@@ -140,8 +147,30 @@ def train_blocked(d: RatingsDataset, cfg: TrainConfig, test: Optional[RatingsDat
             if len(trace) >= 2 and trace.steps[-2].train_rmse - train_rmse < cfg.delta:
                 stop = "converged"
                 break
+    if prof:
+        prof.mark(f"{len(trace)} epochs")
     u, v = eng.get_factors()
+    if prof:
+        prof.mark("get_factors (D2H)")
+        prof.report()
     return TrainResult(model=FactorModel(u, v), trace=trace, stop_reason=stop)
+
+
+class _Phases:
+    """BGMF_PROFILE=1: wall time of train_blocked's phases on stderr."""
+
+    def __init__(self):
+        self.t = time.perf_counter()
+        self.rows = []
+
+    def mark(self, what):
+        now = time.perf_counter()
+        self.rows.append((what, now - self.t))
+        self.t = now
+
+    def report(self):
+        for what, dt in self.rows:
+            print(f"[bgmf] {what:32s} {dt * 1e3:9.2f} ms", file=sys.stderr)
 
 
 def _run_step(eng, batches, g, tol, cfg, counts, hooks, block_hook):
