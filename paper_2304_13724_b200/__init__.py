@@ -10,8 +10,8 @@ library or the GPU is missing.
 
 Not provided (outside the hot path): the CMF/CPMF baseline
 trainers, the verification-only gradient kernels (batch_gradient_block,
-block_objective, block_gradients), sweep_budget/auto_splits, file
-formats / persistence, CLI and plots.
+block_objective, block_gradients), sweep_budget/auto_splits, CLI and plots.
+File formats and model / trace persistence are host helpers (data.py).
 """
 
 from ._native import CudaError, NativeUnavailable
@@ -19,7 +19,8 @@ from .core import (AdaptiveDecreasing, Constant, ConvergeEachBlock, ConvergenceT
                    DataError, Decreasing, DivergenceError, FactorModel, IncreasingEvery,
                    InnerSchedule, RatingsDataset, RatingTriple, TraceStep, TrainConfig,
                    format_schedule, init_factors, parse_schedule, validate_dataset)
-from .data import SyntheticSpec, gen_synthetic, split
+from .data import (FORMATS, SyntheticSpec, gen_synthetic, load, load_model, read_trace,
+                   save_dataset, save_model, split, write_trace)
 from .device import Engine, EngineOptions
 from .kernel import BlockStats, BlockTask, block_sse, sgd_block, task_from_block
 from .metrics import HoldoutEvaluator, RmseAccumulator, finalize, merge, rmse, test_rmse
@@ -29,6 +30,7 @@ from .scheduler import Batch, StepPlan, format_plan, plan_step, validate_plan
 from .trainer import TrainResult, resolve_inner_iters, train_blocked
 
 __all__ = [
+    "FORMATS", "load", "load_model", "read_trace", "save_dataset", "save_model", "write_trace",
     "AdaptiveDecreasing", "Batch", "Block", "BlockedDataset", "BlockGrid", "BlockStats",
     "BlockTask", "Constant", "ConvergeEachBlock", "ConvergenceTrace", "CudaError", "DataError",
     "Decreasing", "DivergenceError", "Engine", "EngineOptions", "FactorModel",

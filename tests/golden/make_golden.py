@@ -212,6 +212,24 @@ def traces():
     return meta
 
 
+def io_cases():
+    """Byte-exact outputs of the reference's writers (data_io.py:193-309)."""
+    import io as _io
+
+    d = bm.gen_synthetic(bm.SyntheticSpec(7, 5, 1, 5, seed=2, density=0.6))
+    cfg = bm.TrainConfig(k=3, outer_steps=3, grid_i=2, grid_j=2, alpha=1e-2)
+    tr, te = bm.split(d, 0.3, seed=1)
+    res = bm.train_blocked(tr, cfg, te, early_stop=False, timing=False)
+    buf_m, buf_t, buf_d = _io.StringIO(), _io.StringIO(), _io.StringIO()
+    bm.save_model(res.model, buf_m)
+    bm.write_trace(res.trace, buf_t, config={"k": 3, "grid": "2x2", "schedule": "const:1"})
+    bm.save_dataset(d, buf_d)
+    return dict(model=buf_m.getvalue(), trace=buf_t.getvalue(), dataset=buf_d.getvalue(),
+                rows=d.rows.tolist(), cols=d.cols.tolist(), values=d.values.tolist(),
+                u=res.model.u.tolist(), v=res.model.v.tolist(),
+                train=[s.train_rmse for s in res.trace], test=[s.test_rmse for s in res.trace])
+
+
 def main():
     kernel_cases()
     meta = dict(
@@ -219,6 +237,7 @@ def main():
         partition=partition_cases(),
         plans=plans(),
         traces=traces(),
+        io=io_cases(),
         hand=dict(
             rmse_hand=bm.rmse(bm.FactorModel(np.array([[1.0], [2.0]]), np.array([[1.0], [2.0]])),
                               bm.RatingsDataset.from_triples(2, 2, [(0, 0, 4.0), (1, 1, 8.0)])),

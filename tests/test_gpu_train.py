@@ -216,3 +216,19 @@ def test_c4_one_epoch_properties():
     tr = [s.train_rmse for s in res.trace]
     assert all(math.isfinite(x) for x in tr) and tr[1] < tr[0]
     assert np.all(np.isfinite(res.model.u)) and np.all(np.isfinite(res.model.v))
+
+
+def test_exact_run_saves_reference_bytes(golden):
+    """Exact mode end to end: the saved model file is byte-identical to the
+    reference's save_model output for the same run (data_io.py:221-227)."""
+    import io as _io
+
+    g = golden["io"]
+    d = bm.gen_synthetic(bm.SyntheticSpec(7, 5, 1, 5, seed=2, density=0.6))
+    tr, te = bm.split(d, 0.3, seed=1)
+    cfg = bm.TrainConfig(k=3, outer_steps=3, grid_i=2, grid_j=2, alpha=1e-2)
+    res = bm.train_blocked(tr, cfg, te, early_stop=False, timing=False, options=EXACT)
+    buf = _io.StringIO()
+    bm.save_model(res.model, buf)
+    assert buf.getvalue() == g["model"]
+    assert [s.train_rmse for s in res.trace] == g["train"]
