@@ -41,6 +41,7 @@ for mb in (64,256,1024,4096):
       done; echo "small rc=$?" ;;
     c5s) timeout 900 $B --config C5 --nnz 200000000 --steps 3 --warmup 3 --budget-gb 0.5 > $OUT/bench_c5_small.json 2> $OUT/bench_c5_small.err; echo "c5s rc=$?" ;;
     c5) timeout 1500 $B --config C5 --steps 3 --warmup 3 > $OUT/bench_c5.json 2> $OUT/bench_c5.err; echo "c5 rc=$?" ;;
+    probe) timeout 300 python scripts/h2d_probe.py > $OUT/h2d_probe.txt 2>&1; echo "probe rc=$?" ;;
     dist1) BGMF_FORCE_DIST=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 5 --warmup 3 > $OUT/bench_dist1.json 2> $OUT/bench_dist1.err; echo "dist1 rc=$?" ;;
     ncu)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
