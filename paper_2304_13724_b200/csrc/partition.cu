@@ -35,14 +35,15 @@ __device__ __forceinline__ int64_t slab_start(int64_t s, int64_t base, int64_t e
   return s * base + (s < extra ? s : extra);
 }
 
-__global__ void make_keys(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols,
+template <typename IT>
+__global__ void make_keys(const IT* __restrict__ rows, const IT* __restrict__ cols,
                           int64_t nnz, int64_t n, int64_t m, int64_t rbase, int64_t rextra,
                           int64_t cbase, int64_t cextra, int J, int rbits, int cbits,
                           uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
                           unsigned long long* __restrict__ bad) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = rows[i], c = cols[i];
+    const int64_t r = (int64_t)rows[i], c = (int64_t)cols[i];
     idx[i] = (uint32_t)i;
     if (r < 0 || r >= n || c < 0 || c >= m) {
       atomicMin(bad, (unsigned long long)i);
@@ -221,8 +222,9 @@ __global__ void block_offsets(const uint64_t* __restrict__ keys, int64_t n, int 
   off[b] = lo;
 }
 
+template <typename VT>
 __global__ void decode(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
-                       const double* __restrict__ vin, int64_t n, int cbits, uint64_t rmask,
+                       const VT* __restrict__ vin, int64_t n, int cbits, uint64_t rmask,
                        uint64_t cmask, int32_t* __restrict__ lrow, int32_t* __restrict__ lcol,
                        float* __restrict__ val, double* __restrict__ val64,
                        uint32_t* __restrict__ order) {
@@ -233,9 +235,9 @@ __global__ void decode(const uint64_t* __restrict__ keys, const uint32_t* __rest
     lrow[i] = (int32_t)((k >> cbits) & rmask);
     lcol[i] = (int32_t)(k & cmask);
     order[i] = o;
-    const double x = vin[o];
+    const VT x = vin[o];
     val[i] = (float)x;
-    if (val64) val64[i] = x;
+    if (val64) val64[i] = (double)x;
   }
 }
 
@@ -252,6 +254,70 @@ void free_dev(T*& p) {
 }
 
 }  // namespace
+
+// Host -> device upload of the dataset through pinned staging buffers: the
+// int64 indices are narrowed to int32 (and range-checked) and, in fast mode,
+// the fp64 values to fp32 by OpenMP threads while the previous chunk's DMA is
+// in flight -- 12 instead of 24 bytes per rating cross PCIe, and the copy is
+// not limited by the driver's single-threaded pageable staging (~11 GB/s on
+// the B200 hosts, profiles/r01_h2d_probe.txt).  Returns the first entry whose
+// index is outside n x m (or -1).
+int64_t staged_upload(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
+                      const double* vals, int64_t nnz, int64_t n, int64_t m, int32_t* d_r,
+                      int32_t* d_c, void* d_v, bool v64, int* rc) {
+  constexpr int64_t kChunk = 1 << 22;  // ratings per staging buffer
+  const int64_t chunk = nnz < kChunk ? nnz : kChunk;
+  const size_t vb = v64 ? 8 : 4;
+  const size_t per = (size_t)chunk * (8 + vb);
+  char* stage[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  *rc = BGMF_OK;
+  for (int b = 0; b < 2; ++b) {
+    cudaError_t e = cudaMallocHost(&stage[b], per);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      *rc = cuda_fail(ctx, e, "staging alloc");
+      for (int q = 0; q < 2; ++q) {
+        if (stage[q]) cudaFreeHost(stage[q]);
+        if (done[q]) cudaEventDestroy(done[q]);
+      }
+      return -1;
+    }
+  }
+  int64_t first_bad = INT64_MAX;
+  int k = 0;
+  for (int64_t i0 = 0; i0 < nnz; i0 += chunk, ++k) {
+    const int b = k & 1;
+    const int64_t cnt = nnz - i0 < chunk ? nnz - i0 : chunk;
+    if (k >= 2) cudaEventSynchronize(done[b]);  // the DMA that last read this buffer
+    int32_t* sr = reinterpret_cast<int32_t*>(stage[b]);
+    int32_t* sc = sr + chunk;
+    char* sv = reinterpret_cast<char*>(sc + chunk);
+    int64_t bad = INT64_MAX;
+#pragma omp parallel for schedule(static) reduction(min : bad)
+    for (int64_t i = 0; i < cnt; ++i) {
+      const int64_t r = rows[i0 + i], c = cols[i0 + i];
+      if (r < 0 || r >= n || c < 0 || c >= m) bad = i0 + i < bad ? i0 + i : bad;
+      sr[i] = (int32_t)r;
+      sc[i] = (int32_t)c;
+      if (v64) reinterpret_cast<double*>(sv)[i] = vals[i0 + i];
+      else reinterpret_cast<float*>(sv)[i] = (float)vals[i0 + i];
+    }
+    if (bad < first_bad) first_bad = bad;
+    cudaMemcpyAsync(d_r + i0, sr, cnt * 4, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(d_c + i0, sc, cnt * 4, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(static_cast<char*>(d_v) + i0 * vb, sv, cnt * vb, cudaMemcpyHostToDevice,
+                    ctx->stream);
+    cudaEventRecord(done[b], ctx->stream);
+  }
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) *rc = cuda_fail(ctx, e, "staged upload");
+  for (int b = 0; b < 2; ++b) {
+    cudaFreeHost(stage[b]);
+    cudaEventDestroy(done[b]);
+  }
+  return first_bad == INT64_MAX ? -1 : first_bad;
+}
 
 // dev_in: rows/cols/vals are device buffers whose ownership passes to this
 // call (freed as soon as they are consumed); otherwise host arrays.
@@ -305,33 +371,52 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
     if (_e != cudaSuccess) { rc = cuda_fail(ctx, _e, #call); cleanup(); return rc; } \
   } while (0)
 
+  // host input with 32-bit dimensions: narrowed staged upload (int32 indices,
+  // fp32 values unless exact mode needs the fp64 ones)
+  const bool narrow = !dev_in && n <= INT32_MAX && m <= INT32_MAX;
+  const bool v32 = narrow && !ctx->exact;
   if (dev_in) {
     d_rows = const_cast<int64_t*>(rows);
     d_cols = const_cast<int64_t*>(cols);
     d_vin = const_cast<double*>(vals);
   } else {
-    PCK(cudaMalloc(&d_rows, N * 8));
-    PCK(cudaMalloc(&d_cols, N * 8));
-    PCK(cudaMalloc(&d_vin, N * 8));
+    PCK(cudaMalloc(&d_rows, N * (narrow ? 4 : 8)));
+    PCK(cudaMalloc(&d_cols, N * (narrow ? 4 : 8)));
+    PCK(cudaMalloc(&d_vin, N * (v32 ? 4 : 8)));
   }
   PCK(cudaMalloc(&ka, N * 8));
   PCK(cudaMalloc(&ia, N * 4));
   PCK(cudaMalloc(&d_bad, 8));
   PCK(cudaMalloc(&d_off, (nb + 1) * 8));
-  if (nnz > 0 && !dev_in) {
+  int64_t host_bad = -1;
+  if (nnz > 0 && narrow) {
+    int urc = BGMF_OK;
+    host_bad = staged_upload(ctx, rows, cols, vals, nnz, n, m,
+                             reinterpret_cast<int32_t*>(d_rows),
+                             reinterpret_cast<int32_t*>(d_cols), d_vin, !v32, &urc);
+    if (urc) { cleanup(); return urc; }
+  } else if (nnz > 0 && !dev_in) {
     PCK(cudaMemcpyAsync(d_rows, rows, nnz * 8, cudaMemcpyHostToDevice, s));
     PCK(cudaMemcpyAsync(d_cols, cols, nnz * 8, cudaMemcpyHostToDevice, s));
     PCK(cudaMemcpyAsync(d_vin, vals, nnz * 8, cudaMemcpyHostToDevice, s));
   }
   PCK(cudaMemsetAsync(d_bad, 0xFF, 8, s));
   const int grid = ctx->num_sms * 8;
-  if (nnz > 0)
-    make_keys<<<grid, 256, 0, s>>>(d_rows, d_cols, nnz, n, m, rbase, rextra, cbase, cextra, J,
-                                   rbits, cbits, ka, ia, d_bad);
+  if (nnz > 0 && host_bad < 0) {
+    if (narrow)
+      make_keys<int32_t><<<grid, 256, 0, s>>>(reinterpret_cast<const int32_t*>(d_rows),
+                                              reinterpret_cast<const int32_t*>(d_cols), nnz, n,
+                                              m, rbase, rextra, cbase, cextra, J, rbits, cbits,
+                                              ka, ia, d_bad);
+    else
+      make_keys<int64_t><<<grid, 256, 0, s>>>(d_rows, d_cols, nnz, n, m, rbase, rextra, cbase,
+                                              cextra, J, rbits, cbits, ka, ia, d_bad);
+  }
   PCK(cudaGetLastError());
   unsigned long long hbad = 0;
   PCK(cudaMemcpyAsync(&hbad, d_bad, 8, cudaMemcpyDeviceToHost, s));
   PCK(cudaStreamSynchronize(s));
+  if (host_bad >= 0) hbad = (unsigned long long)host_bad;
   if (hbad != ~0ull) {
     int64_t br = 0, bc = 0;
     if (dev_in) {
@@ -377,7 +462,13 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   PCK(cudaMalloc(&ctx->d_order, N * 4));
   if (ctx->exact) PCK(cudaMalloc(&ctx->d_val64, N * 8));
   if (nnz > 0) {
-    decode<<<grid, 256, 0, s>>>(ka, ia, d_vin, nnz, cbits, (1ull << rbits) - 1,
+    if (v32)
+      decode<float><<<grid, 256, 0, s>>>(ka, ia, reinterpret_cast<const float*>(d_vin), nnz,
+                                         cbits, (1ull << rbits) - 1, (1ull << cbits) - 1,
+                                         ctx->d_lrow, ctx->d_lcol, ctx->d_val, ctx->d_val64,
+                                         ctx->d_order);
+    else
+    decode<double><<<grid, 256, 0, s>>>(ka, ia, d_vin, nnz, cbits, (1ull << rbits) - 1,
                                 (1ull << cbits) - 1, ctx->d_lrow, ctx->d_lcol, ctx->d_val,
                                 ctx->d_val64, ctx->d_order);
   }
