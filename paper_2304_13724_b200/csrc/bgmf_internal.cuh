@@ -145,6 +145,13 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                      const double* vals, int64_t nnz, int64_t n, int64_t m, int I, int J,
                      bool dev_in = false);
 
+// hostio.cu -- host <-> device through the process-wide pinned staging pool
+int64_t staged_upload(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
+                      const double* vals, int64_t nnz, int64_t n, int64_t m, int32_t* d_r,
+                      int32_t* d_c, void* d_v, bool v64, int* rc);
+int download_rows(bgmf_ctx* c, const float* d, double* h, int64_t rows, int k, int kp);
+int upload_rows(bgmf_ctx* c, const double* h, float* d, int64_t rows, int k, int kp);
+
 // synth.cu (benchmark / test input generator)
 int synth_lowrank_device(bgmf_ctx* ctx, int64_t n, int64_t m, int64_t nnz, int64_t start,
                          uint64_t seed, int64_t* rows, int64_t* cols, double* vals);

@@ -56,70 +56,6 @@ void harvest_timing(bgmf_ctx* c) {
 
 namespace {
 
-__global__ void f64_to_f32_rows(const double* __restrict__ src, float* __restrict__ dst,
-                                int64_t rows, int k, int kp) {
-  const int64_t total = rows * kp;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / kp;
-    const int g = (int)(i - r * kp);
-    dst[i] = g < k ? (float)src[r * k + g] : 0.f;
-  }
-}
-
-__global__ void f32_to_f64_rows(const float* __restrict__ src, double* __restrict__ dst,
-                                int64_t rows, int k, int kp) {
-  const int64_t total = rows * k;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / k;
-    const int g = (int)(i - r * k);
-    dst[i] = (double)src[r * kp + g];
-  }
-}
-
-constexpr int64_t kStageRows = 1 << 16;
-
-// fp64 host (rows x k) -> fp32 device (rows x kp) through a staging buffer.
-int upload_rows(bgmf_ctx* c, const double* h, float* d, int64_t rows, int k, int kp) {
-  if (rows == 0) return BGMF_OK;
-  double* stage = nullptr;
-  const int64_t chunk = rows < kStageRows ? rows : kStageRows;
-  BGMF_CK(c, cudaMalloc(&stage, (size_t)chunk * k * 8));
-  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
-    const int64_t nr = rows - r0 < chunk ? rows - r0 : chunk;
-    cudaError_t e = cudaMemcpyAsync(stage, h + r0 * k, (size_t)nr * k * 8,
-                                    cudaMemcpyHostToDevice, c->stream);
-    if (e != cudaSuccess) { cudaFree(stage); return cuda_fail(c, e, "upload_rows"); }
-    f64_to_f32_rows<<<c->num_sms * 4, 256, 0, c->stream>>>(stage, d + r0 * kp, nr, k, kp);
-  }
-  cudaError_t e = cudaStreamSynchronize(c->stream);
-  cudaFree(stage);
-  if (e != cudaSuccess) return cuda_fail(c, e, "upload_rows sync");
-  return BGMF_OK;
-}
-
-// fp32 device rows (stride kp) -> fp64 host (rows x k): one conversion kernel
-// into a device fp64 buffer, then D2H in large pieces (pageable D2H runs at
-// ~21 GB/s on the B200 hosts; per-chunk syncs were the cost before).
-int download_rows(bgmf_ctx* c, const float* d, double* h, int64_t rows, int k, int kp) {
-  if (rows == 0) return BGMF_OK;
-  constexpr int64_t kPiece = 1 << 21;  // rows per D2H piece
-  const int64_t chunk = rows < kPiece ? rows : kPiece;
-  double* stage = nullptr;
-  BGMF_CK(c, cudaMalloc(&stage, (size_t)chunk * k * 8));
-  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
-    const int64_t nr = rows - r0 < chunk ? rows - r0 : chunk;
-    f32_to_f64_rows<<<c->num_sms * 8, 256, 0, c->stream>>>(d + r0 * kp, stage, nr, k, kp);
-    cudaError_t e = cudaMemcpyAsync(h + r0 * k, stage, (size_t)nr * k * 8,
-                                    cudaMemcpyDeviceToHost, c->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    if (e != cudaSuccess) { cudaFree(stage); return cuda_fail(c, e, "download_rows"); }
-  }
-  cudaFree(stage);
-  return BGMF_OK;
-}
-
 void free_factors(bgmf_ctx* c) {
   if (!c->bound) {
     if (c->d_u) cudaFree(c->d_u);

@@ -1,0 +1,181 @@
+// hostio.cu -- host <-> device movement of the dataset and the model.
+//
+// The reference keeps everything in host numpy arrays (ratings int64/int64/
+// fp64, factors fp64: core.py:12-108, 139-176).  The e2e path therefore has
+// to move 24 B per rating in and 8k B per factor row out.  Measured on the
+// B200 hosts (profiles/r01_host_probe.txt, scripts/host_probe.cu):
+//   * pageable cudaMemcpy runs at ~11 GB/s (driver's single-threaded bounce);
+//   * pinned DMA runs at ~55 GB/s, but pinning costs ~1.1 GB/s
+//     (cudaHostRegister / cudaMallocHost), so pinning per call never pays;
+//   * 16 host threads narrow int64 -> int32 at ~100 GB/s (read + write) and
+//     fault fresh pages at 33-70 GB/s.
+// So both directions go through a small process-wide pool of pinned staging
+// buffers, allocated once (like a caching host allocator) and reused by every
+// context: OpenMP threads convert between the reference's host types and the
+// device types in the staging buffer while the DMA engine moves the other one.
+
+#include <omp.h>
+
+#include <mutex>
+
+#include "bgmf_internal.cuh"
+
+namespace bgmf {
+namespace {
+
+constexpr size_t kStageBytes = size_t(16) << 20;  // per buffer
+
+struct StagePool {
+  std::mutex mu;
+  char* buf[2] = {nullptr, nullptr};
+  int device = -1;
+};
+
+StagePool& pool() {
+  static StagePool p;
+  return p;
+}
+
+// Locks the pool and makes sure both pinned buffers exist.
+class Stage {
+ public:
+  explicit Stage(bgmf_ctx* c) : lk_(pool().mu) {
+    StagePool& p = pool();
+    for (int b = 0; b < 2 && !err_; ++b) {
+      if (!p.buf[b]) err_ = cudaMallocHost(&p.buf[b], kStageBytes);
+      if (!err_) err_ = cudaEventCreateWithFlags(&done_[b], cudaEventDisableTiming);
+    }
+    (void)c;
+  }
+  ~Stage() {
+    for (int b = 0; b < 2; ++b)
+      if (done_[b]) cudaEventDestroy(done_[b]);
+  }
+  cudaError_t error() const { return err_; }
+  char* buf(int b) const { return pool().buf[b]; }
+  cudaEvent_t done(int b) const { return done_[b]; }
+
+ private:
+  std::unique_lock<std::mutex> lk_;
+  cudaError_t err_ = cudaSuccess;
+  cudaEvent_t done_[2] = {nullptr, nullptr};
+};
+
+}  // namespace
+
+// Dataset upload for the partitioner (partition.cu): int64 indices narrowed
+// to int32 (and range-checked against n x m), fp64 values narrowed to fp32
+// unless v64 (exact mode keeps them).  12 (16) instead of 24 B per rating
+// cross PCIe.  Returns the first entry whose index is outside n x m, or -1.
+int64_t staged_upload(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
+                      const double* vals, int64_t nnz, int64_t n, int64_t m, int32_t* d_r,
+                      int32_t* d_c, void* d_v, bool v64, int* rc) {
+  *rc = BGMF_OK;
+  Stage st(ctx);
+  if (st.error()) {
+    *rc = cuda_fail(ctx, st.error(), "staging pool");
+    return -1;
+  }
+  const size_t vb = v64 ? 8 : 4;
+  const int64_t chunk = (int64_t)(kStageBytes / (8 + vb));
+  int64_t first_bad = INT64_MAX;
+  int k = 0;
+  for (int64_t i0 = 0; i0 < nnz; i0 += chunk, ++k) {
+    const int b = k & 1;
+    const int64_t cnt = nnz - i0 < chunk ? nnz - i0 : chunk;
+    if (k >= 2) cudaEventSynchronize(st.done(b));  // the DMA that last read this buffer
+    int32_t* sr = reinterpret_cast<int32_t*>(st.buf(b));
+    int32_t* sc = sr + chunk;
+    char* sv = reinterpret_cast<char*>(sc + chunk);
+    int64_t bad = INT64_MAX;
+#pragma omp parallel for schedule(static) reduction(min : bad)
+    for (int64_t i = 0; i < cnt; ++i) {
+      const int64_t r = rows[i0 + i], c = cols[i0 + i];
+      if (r < 0 || r >= n || c < 0 || c >= m) bad = i0 + i < bad ? i0 + i : bad;
+      sr[i] = (int32_t)r;
+      sc[i] = (int32_t)c;
+      if (v64) reinterpret_cast<double*>(sv)[i] = vals[i0 + i];
+      else reinterpret_cast<float*>(sv)[i] = (float)vals[i0 + i];
+    }
+    if (bad < first_bad) first_bad = bad;
+    cudaMemcpyAsync(d_r + i0, sr, cnt * 4, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(d_c + i0, sc, cnt * 4, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(static_cast<char*>(d_v) + i0 * vb, sv, cnt * vb, cudaMemcpyHostToDevice,
+                    ctx->stream);
+    cudaEventRecord(st.done(b), ctx->stream);
+  }
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) *rc = cuda_fail(ctx, e, "staged upload");
+  return first_bad == INT64_MAX ? -1 : first_bad;
+}
+
+// fp32 device rows (stride kp) -> fp64 host rows (stride k), the reference's
+// FactorModel layout.  Piece p is DMA'd into one pinned buffer while the host
+// threads widen piece p-1 out of the other; 4k B per row cross PCIe.
+int download_rows(bgmf_ctx* c, const float* d, double* h, int64_t rows, int k, int kp) {
+  if (rows == 0) return BGMF_OK;
+  Stage st(c);
+  if (st.error()) return cuda_fail(c, st.error(), "staging pool");
+  const int64_t chunk = (int64_t)(kStageBytes / ((size_t)kp * 4));
+  const int64_t np = (rows + chunk - 1) / chunk;
+  auto issue = [&](int64_t p) -> cudaError_t {
+    const int64_t r0 = p * chunk, nr = rows - r0 < chunk ? rows - r0 : chunk;
+    cudaError_t e = cudaMemcpyAsync(st.buf(p & 1), d + r0 * kp, (size_t)nr * kp * 4,
+                                    cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(st.done(p & 1), c->stream);
+    return e;
+  };
+  cudaError_t e = issue(0);
+  for (int64_t p = 0; p < np && e == cudaSuccess; ++p) {
+    e = cudaEventSynchronize(st.done(p & 1));
+    if (e == cudaSuccess && p + 1 < np) e = issue(p + 1);
+    if (e != cudaSuccess) break;
+    const int64_t r0 = p * chunk, nr = rows - r0 < chunk ? rows - r0 : chunk;
+    const float* src = reinterpret_cast<const float*>(st.buf(p & 1));
+    double* dst = h + r0 * k;
+    if (kp == k) {
+      const int64_t tot = nr * k;
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < tot; ++i) dst[i] = (double)src[i];
+    } else {
+#pragma omp parallel for schedule(static)
+      for (int64_t r = 0; r < nr; ++r)
+        for (int j = 0; j < k; ++j) dst[r * k + j] = (double)src[r * kp + j];
+    }
+  }
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(c->stream);
+    return cuda_fail(c, e, "download_rows");
+  }
+  return BGMF_OK;
+}
+
+// fp64 host rows (stride k) -> fp32 device rows (stride kp, zero padding).
+int upload_rows(bgmf_ctx* c, const double* h, float* d, int64_t rows, int k, int kp) {
+  if (rows == 0) return BGMF_OK;
+  Stage st(c);
+  if (st.error()) return cuda_fail(c, st.error(), "staging pool");
+  const int64_t chunk = (int64_t)(kStageBytes / ((size_t)kp * 4));
+  cudaError_t e = cudaSuccess;
+  int q = 0;
+  for (int64_t r0 = 0; r0 < rows && e == cudaSuccess; r0 += chunk, ++q) {
+    const int b = q & 1;
+    const int64_t nr = rows - r0 < chunk ? rows - r0 : chunk;
+    if (q >= 2) e = cudaEventSynchronize(st.done(b));
+    if (e != cudaSuccess) break;
+    float* dst = reinterpret_cast<float*>(st.buf(b));
+    const double* src = h + r0 * k;
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < nr; ++r)
+      for (int j = 0; j < kp; ++j) dst[r * kp + j] = j < k ? (float)src[r * k + j] : 0.f;
+    e = cudaMemcpyAsync(d + r0 * kp, dst, (size_t)nr * kp * 4, cudaMemcpyHostToDevice,
+                        c->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(st.done(b), c->stream);
+  }
+  cudaError_t e2 = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(c, e, "upload_rows");
+  return BGMF_OK;
+}
+
+}  // namespace bgmf

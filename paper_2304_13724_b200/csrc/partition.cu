@@ -255,70 +255,6 @@ void free_dev(T*& p) {
 
 }  // namespace
 
-// Host -> device upload of the dataset through pinned staging buffers: the
-// int64 indices are narrowed to int32 (and range-checked) and, in fast mode,
-// the fp64 values to fp32 by OpenMP threads while the previous chunk's DMA is
-// in flight -- 12 instead of 24 bytes per rating cross PCIe, and the copy is
-// not limited by the driver's single-threaded pageable staging (~11 GB/s on
-// the B200 hosts, profiles/r01_h2d_probe.txt).  Returns the first entry whose
-// index is outside n x m (or -1).
-int64_t staged_upload(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
-                      const double* vals, int64_t nnz, int64_t n, int64_t m, int32_t* d_r,
-                      int32_t* d_c, void* d_v, bool v64, int* rc) {
-  constexpr int64_t kChunk = 1 << 22;  // ratings per staging buffer
-  const int64_t chunk = nnz < kChunk ? nnz : kChunk;
-  const size_t vb = v64 ? 8 : 4;
-  const size_t per = (size_t)chunk * (8 + vb);
-  char* stage[2] = {nullptr, nullptr};
-  cudaEvent_t done[2] = {nullptr, nullptr};
-  *rc = BGMF_OK;
-  for (int b = 0; b < 2; ++b) {
-    cudaError_t e = cudaMallocHost(&stage[b], per);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
-    if (e != cudaSuccess) {
-      *rc = cuda_fail(ctx, e, "staging alloc");
-      for (int q = 0; q < 2; ++q) {
-        if (stage[q]) cudaFreeHost(stage[q]);
-        if (done[q]) cudaEventDestroy(done[q]);
-      }
-      return -1;
-    }
-  }
-  int64_t first_bad = INT64_MAX;
-  int k = 0;
-  for (int64_t i0 = 0; i0 < nnz; i0 += chunk, ++k) {
-    const int b = k & 1;
-    const int64_t cnt = nnz - i0 < chunk ? nnz - i0 : chunk;
-    if (k >= 2) cudaEventSynchronize(done[b]);  // the DMA that last read this buffer
-    int32_t* sr = reinterpret_cast<int32_t*>(stage[b]);
-    int32_t* sc = sr + chunk;
-    char* sv = reinterpret_cast<char*>(sc + chunk);
-    int64_t bad = INT64_MAX;
-#pragma omp parallel for schedule(static) reduction(min : bad)
-    for (int64_t i = 0; i < cnt; ++i) {
-      const int64_t r = rows[i0 + i], c = cols[i0 + i];
-      if (r < 0 || r >= n || c < 0 || c >= m) bad = i0 + i < bad ? i0 + i : bad;
-      sr[i] = (int32_t)r;
-      sc[i] = (int32_t)c;
-      if (v64) reinterpret_cast<double*>(sv)[i] = vals[i0 + i];
-      else reinterpret_cast<float*>(sv)[i] = (float)vals[i0 + i];
-    }
-    if (bad < first_bad) first_bad = bad;
-    cudaMemcpyAsync(d_r + i0, sr, cnt * 4, cudaMemcpyHostToDevice, ctx->stream);
-    cudaMemcpyAsync(d_c + i0, sc, cnt * 4, cudaMemcpyHostToDevice, ctx->stream);
-    cudaMemcpyAsync(static_cast<char*>(d_v) + i0 * vb, sv, cnt * vb, cudaMemcpyHostToDevice,
-                    ctx->stream);
-    cudaEventRecord(done[b], ctx->stream);
-  }
-  cudaError_t e = cudaStreamSynchronize(ctx->stream);
-  if (e != cudaSuccess) *rc = cuda_fail(ctx, e, "staged upload");
-  for (int b = 0; b < 2; ++b) {
-    cudaFreeHost(stage[b]);
-    cudaEventDestroy(done[b]);
-  }
-  return first_bad == INT64_MAX ? -1 : first_bad;
-}
-
 // dev_in: rows/cols/vals are device buffers whose ownership passes to this
 // call (freed as soon as they are consumed); otherwise host arrays.
 int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
