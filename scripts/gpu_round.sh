@@ -31,6 +31,7 @@ for mb in (64,256,1024,4096):
     for _ in range(5): a.copy_(b,non_blocking=True)
     e1.record(); torch.cuda.synchronize(); print('d2h',mb,'MB',5*mb/1024/(e0.elapsed_time(e1)/1e3),'GB/s')
 " > $OUT/h2d.txt 2>&1; nvidia-smi -q | grep -iA3 "pcie gen\|link width" >> $OUT/h2d.txt; echo "h2d rc=$?" ;;
+    sse) timeout 900 python -m pytest tests/test_gpu_sse.py -q -rA -x > $OUT/tests_sse.log 2>&1; echo "sse rc=$?" ;;
     benchu) timeout 900 $B --steps 10 --warmup 3 --unfused --no-e2e --no-cpu-baseline > $OUT/bench_unfused.json 2> $OUT/bench_unfused.err; echo "benchu rc=$?" ;;
     benchf) timeout 900 $B --steps 10 --warmup 3 --fused --no-e2e --no-cpu-baseline > $OUT/bench_fused.json 2> $OUT/bench_fused.err; echo "benchf rc=$?" ;;
     small)
@@ -43,6 +44,10 @@ for mb in (64,256,1024,4096):
     c5) timeout 1500 $B --config C5 --steps 3 --warmup 3 > $OUT/bench_c5.json 2> $OUT/bench_c5.err; echo "c5 rc=$?" ;;
     probe) timeout 300 python scripts/h2d_probe.py > $OUT/h2d_probe.txt 2>&1; echo "probe rc=$?" ;;
     dist1) BGMF_FORCE_DIST=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 5 --warmup 3 > $OUT/bench_dist1.json 2> $OUT/bench_dist1.err; echo "dist1 rc=$?" ;;
+    ncuk) # one kernel, full set + source: NCU_K=<regex> NCU_ARGS=<bench args>
+      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"${NCU_K}" -s ${NCU_S:-4} -c 1 \
+        -o $OUT/k_full $B --steps 1 --warmup 3 --no-e2e --no-cpu-baseline ${NCU_ARGS:-} > $OUT/ncu_k.log 2>&1
+      echo "ncuk rc=$?" ;;
     ncu)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file $OUT/launches.csv $B --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
