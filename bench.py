@@ -213,6 +213,7 @@ def run_ours(args):
         res = bm.train_blocked(d, cfg, early_stop=False)
         torch.cuda.synchronize()
         t_e2e = time.perf_counter() - t0
+        print(f"[bgmf] e2e wall (train_blocked + sync)  {t_e2e * 1e3:9.2f} ms", file=sys.stderr)
         del os.environ["BGMF_PROFILE"]
         e2e_val = nnz * args.steps / t_e2e
         h2d = (nnz * 24 + (w.n + w.m) * w.k * 8) / args.steps
@@ -268,6 +269,8 @@ def run_ours(args):
     except Exception:
         pass
 
+    l2 = l2_ceiling(dev, w, st, sgd_launch_ms, nnz, args)
+
     cpu = None
     if not args.no_cpu_baseline and rank == 0:
         threads = min(os.cpu_count() or 1, w.grid)
@@ -303,7 +306,8 @@ def run_ours(args):
                                 "sgd_fast_kernel<8,4> (stratum sweep)"),
                      "alg_bytes_per_launch": alg_per_launch, "avg_launch_ms": sgd_launch_ms,
                      "sgd_share_of_step": st["sgd_ms"] / total_ms,
-                     "sse_ms_per_step": st["sse_ms"] / args.steps},
+                     "sse_ms_per_step": st["sse_ms"] / args.steps,
+                     "l2_ceiling": l2},
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
         "gpu_launches": int(round(launches_per_step * args.steps)),
@@ -311,6 +315,32 @@ def run_ours(args):
         "gen_seconds": t_gen,
     }
     print(json.dumps(line))
+
+
+def l2_ceiling(dev, w, st, sgd_launch_ms, nnz, args):
+    """The sweep's real limiter: random V-row reads + V-row reduce-adds at the
+    SM->L2 interface.  bgmf_probe_l2 issues exactly that traffic (no math) on
+    an L2-resident m x 128 matrix; the sweep's rows/s over the probe's is how
+    close the kernel sits to that ceiling (the HBM roofline above counts
+    bytes that never reach DRAM)."""
+    if w.k != 128:
+        return None
+    import ctypes
+
+    from paper_2304_13724_b200 import _native as N
+
+    L = N.load()
+    ms = ctypes.c_double()
+    ratings = 50_000_000
+    N.check(L.bgmf_probe_l2(dev, w.m, ratings, 1, 2, ctypes.byref(ms)))
+    probe = ratings / (ms.value / 1e3)
+    per_launch = nnz * 1.0 / max(st["sgd_launches"] / args.steps, 1)
+    achieved = per_launch / (sgd_launch_ms / 1e3)
+    return {"bound": "sm_l2_interface (red.global.add.v4.f32 + ld.global.cg of 512 B rows)",
+            "probe": "bgmf_probe_l2 mode 1: random 512 B row read + 512 B row reduce-add, "
+                     f"{w.m} x 128 fp32 L2-resident, 2 x 256-thread CTAs/SM",
+            "probe_rows_per_s": probe, "achieved_rows_per_s": achieved,
+            "frac": achieved / probe, "unit": "rating updates (rows)/s"}
 
 
 def run_out_of_core(args, dev):

@@ -206,6 +206,15 @@ int bgmf_sse(const double* u, int64_t n, const double* v, int64_t m, int k,
              const int64_t* rows, const int64_t* cols, const double* vals,
              const uint8_t* cold, double fallback, int64_t count, double* sse);
 
+/* Measurement only (no reference counterpart): the SM<->L2 ceiling of the
+ * sweep's access pattern on `device` -- `ratings` random 512-byte rows of an
+ * L2-resident rows x 128 fp32 matrix, read (mode 0), read + reduce-added into
+ * other random rows (mode 1, the sweep's V traffic) or reduce-added only
+ * (mode 2), groups of 8 lanes, 256-thread CTAs x ctas_per_sm per SM.  Best
+ * kernel time of 3 timed launches in *ms_out. */
+int bgmf_probe_l2(int device, int64_t rows, int64_t ratings, int mode,
+                  int ctas_per_sm, double* ms_out);
+
 #ifdef __cplusplus
 }
 #endif

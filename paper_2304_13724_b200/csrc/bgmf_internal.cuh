@@ -130,6 +130,19 @@ struct bgmf_ctx {
 
 namespace bgmf {
 
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync)
+// whose release threshold bgmf_create raises to "never": a second train call
+// reuses the first one's pages instead of re-mapping GBs through the driver
+// (cudaMalloc/cudaFree of the partition temporaries cost 2-500 ms per call on
+// the B200 hosts, profiles/r01_e2e_phases.txt).
+template <class T>
+inline cudaError_t dmalloc(T** p, size_t bytes, cudaStream_t s) {
+  return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, s);
+}
+inline void dfree(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+
 // error helpers --------------------------------------------------------
 int fail(bgmf_ctx* ctx, int code, const std::string& msg);
 int cuda_fail(bgmf_ctx* ctx, cudaError_t e, const char* what);
@@ -139,6 +152,10 @@ int cuda_fail(bgmf_ctx* ctx, cudaError_t e, const char* what);
     cudaError_t _e = (call);                                 \
     if (_e != cudaSuccess) return bgmf::cuda_fail((ctx), _e, #call); \
   } while (0)
+
+// BGMF_PROFILE=1: stream-synchronised wall-clock marks on stderr (host
+// phases of the e2e path); free when the variable is unset.
+void prof_mark(bgmf_ctx* ctx, const char* what);
 
 // partition.cu
 int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,

@@ -2,7 +2,9 @@
 // include/bgmf.h).  Host-side orchestration only; kernels live in
 // partition.cu / sgd.cu / eval.cu.
 
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -24,6 +26,18 @@ int cuda_fail(bgmf_ctx* ctx, cudaError_t e, const char* what) {
                     cudaGetErrorString(e) + ") in " + what;
   cudaGetLastError();  // clear sticky-free errors
   return fail(ctx, e == cudaErrorMemoryAllocation ? BGMF_ERR_NOMEM : BGMF_ERR_CUDA, msg);
+}
+
+void prof_mark(bgmf_ctx* c, const char* what) {
+  const bool on = getenv("BGMF_PROFILE") != nullptr;
+  if (!on) return;
+  static thread_local std::chrono::steady_clock::time_point last;
+  if (c && c->stream) cudaStreamSynchronize(c->stream);
+  const auto now = std::chrono::steady_clock::now();
+  if (what)
+    fprintf(stderr, "[bgmf]   %-30s %9.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
 }
 
 void record_begin(bgmf_ctx* c, int kind, double bytes, TimedLaunch** slot) {
@@ -58,11 +72,11 @@ namespace {
 
 void free_factors(bgmf_ctx* c) {
   if (!c->bound) {
-    if (c->d_u) cudaFree(c->d_u);
-    if (c->d_v) cudaFree(c->d_v);
+    if (c->d_u) dfree(c->d_u, c->stream);
+    if (c->d_v) dfree(c->d_v, c->stream);
   }
-  if (c->d_u64) cudaFree(c->d_u64);
-  if (c->d_v64) cudaFree(c->d_v64);
+  if (c->d_u64) dfree(c->d_u64, c->stream);
+  if (c->d_v64) dfree(c->d_v64, c->stream);
   c->d_u = c->d_v = nullptr;
   c->d_u64 = c->d_v64 = nullptr;
   c->bound = false;
@@ -70,11 +84,11 @@ void free_factors(bgmf_ctx* c) {
 }
 
 void free_holdout(bgmf_ctx* c) {
-  if (c->d_hrow) cudaFree(c->d_hrow);
-  if (c->d_hcol) cudaFree(c->d_hcol);
-  if (c->d_hval) cudaFree(c->d_hval);
-  if (c->d_hval64) cudaFree(c->d_hval64);
-  if (c->d_hcold) cudaFree(c->d_hcold);
+  if (c->d_hrow) dfree(c->d_hrow, c->stream);
+  if (c->d_hcol) dfree(c->d_hcol, c->stream);
+  if (c->d_hval) dfree(c->d_hval, c->stream);
+  if (c->d_hval64) dfree(c->d_hval64, c->stream);
+  if (c->d_hcold) dfree(c->d_hcold, c->stream);
   c->d_hrow = c->d_hcol = nullptr;
   c->d_hval = nullptr;
   c->d_hval64 = nullptr;
@@ -136,6 +150,13 @@ int bgmf_create(int device, void* stream, bgmf_ctx** out) {
   if (device < 0 || device >= ndev) return fail(nullptr, BGMF_ERR_ARG, "no such CUDA device");
   e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+  {  // keep freed device memory in the pool (see dmalloc)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   auto* c = new bgmf_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
@@ -157,9 +178,10 @@ void bgmf_destroy(bgmf_ctx* c) {
   free_factors(c);
   free_holdout(c);
   stream_free(c);
-  cudaFree(c->d_lrow); cudaFree(c->d_lcol); cudaFree(c->d_val); cudaFree(c->d_val64);
-  cudaFree(c->d_order); cudaFree(c->d_sse); cudaFree(c->d_bad); cudaFree(c->d_work);
-  cudaFree(c->d_partials);
+  dfree(c->d_lrow, c->stream); dfree(c->d_lcol, c->stream); dfree(c->d_val, c->stream); dfree(c->d_val64, c->stream);
+  dfree(c->d_order, c->stream); dfree(c->d_sse, c->stream); dfree(c->d_bad, c->stream); dfree(c->d_work, c->stream);
+  dfree(c->d_partials, c->stream);
+  cudaStreamSynchronize(c->stream);
   if (c->h_work) cudaFreeHost(c->h_work);
   if (c->h_sse) cudaFreeHost(c->h_sse);
   if (c->h_bad) cudaFreeHost(c->h_bad);
@@ -190,7 +212,7 @@ int bgmf_partition(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const 
   cudaSetDevice(c->device);
   if (c->streaming) stream_free(c);
   // the step scratch is sized by the grid
-  cudaFree(c->d_sse); cudaFreeHost(c->h_sse); cudaFree(c->d_bad); cudaFreeHost(c->h_bad);
+  dfree(c->d_sse, c->stream); cudaFreeHost(c->h_sse); dfree(c->d_bad, c->stream); cudaFreeHost(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
   return partition_device(c, rows, cols, vals, nnz, n, m, grid_i, grid_j);
 }
@@ -202,17 +224,17 @@ int bgmf_synth_partition(bgmf_ctx* c, int64_t n, int64_t m, int64_t nnz, uint64_
     return fail(c, BGMF_ERR_ARG, "bad synthetic shape");
   cudaSetDevice(c->device);
   if (c->streaming) stream_free(c);
-  cudaFree(c->d_sse); cudaFreeHost(c->h_sse); cudaFree(c->d_bad); cudaFreeHost(c->h_bad);
+  dfree(c->d_sse, c->stream); cudaFreeHost(c->h_sse); dfree(c->d_bad, c->stream); cudaFreeHost(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
   const size_t N = (size_t)(nnz > 0 ? nnz : 1);
   int64_t *r = nullptr, *q = nullptr;
   double* v = nullptr;
-  cudaError_t e = cudaMalloc(&r, N * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&q, N * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&v, N * 8);
-  if (e != cudaSuccess) { cudaFree(r); cudaFree(q); cudaFree(v); return cuda_fail(c, e, "synth alloc"); }
+  cudaError_t e = dmalloc(&r, N * 8, c->stream);
+  if (e == cudaSuccess) e = dmalloc(&q, N * 8, c->stream);
+  if (e == cudaSuccess) e = dmalloc(&v, N * 8, c->stream);
+  if (e != cudaSuccess) { dfree(r, c->stream); dfree(q, c->stream); dfree(v, c->stream); return cuda_fail(c, e, "synth alloc"); }
   int rc = synth_lowrank_device(c, n, m, nnz, 0, seed, r, q, v);
-  if (rc) { cudaFree(r); cudaFree(q); cudaFree(v); return rc; }
+  if (rc) { dfree(r, c->stream); dfree(q, c->stream); dfree(v, c->stream); return rc; }
   return partition_device(c, r, q, v, nnz, n, m, grid_i, grid_j, /*dev_in=*/true);
 }
 
@@ -224,9 +246,9 @@ int bgmf_synth(int64_t n, int64_t m, int64_t nnz, int64_t start, uint64_t seed, 
   if (nnz <= 0) return BGMF_OK;
   int64_t *r = nullptr, *q = nullptr;
   double* v = nullptr;
-  cudaError_t e = cudaMalloc(&r, nnz * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&q, nnz * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&v, nnz * 8);
+  cudaError_t e = dmalloc(&r, nnz * 8, c->stream);
+  if (e == cudaSuccess) e = dmalloc(&q, nnz * 8, c->stream);
+  if (e == cudaSuccess) e = dmalloc(&v, nnz * 8, c->stream);
   if (e == cudaSuccess) {
     rc = synth_lowrank_device(c, n, m, nnz, start, seed, r, q, v);
     if (!rc) {
@@ -235,7 +257,7 @@ int bgmf_synth(int64_t n, int64_t m, int64_t nnz, int64_t start, uint64_t seed, 
       if (e == cudaSuccess) e = cudaMemcpy(vals, v, nnz * 8, cudaMemcpyDeviceToHost);
     }
   }
-  cudaFree(r); cudaFree(q); cudaFree(v);
+  dfree(r, c->stream); dfree(q, c->stream); dfree(v, c->stream);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "bgmf_synth");
   if (rc) { g_err = c->err; return rc; }
   return BGMF_OK;
@@ -271,8 +293,8 @@ int bgmf_set_factors(bgmf_ctx* c, const double* u, const double* v, int64_t n, i
   if (c->exact) {
     free_factors(c);
     c->k = k; c->kp = k;
-    BGMF_CK(c, cudaMalloc(&c->d_u64, (size_t)n * k * 8));
-    BGMF_CK(c, cudaMalloc(&c->d_v64, (size_t)m * k * 8));
+    BGMF_CK(c, dmalloc(&c->d_u64, (size_t)n * k * 8, c->stream));
+    BGMF_CK(c, dmalloc(&c->d_v64, (size_t)m * k * 8, c->stream));
     BGMF_CK(c, cudaMemcpyAsync(c->d_u64, u, (size_t)n * k * 8, cudaMemcpyHostToDevice, c->stream));
     BGMF_CK(c, cudaMemcpyAsync(c->d_v64, v, (size_t)m * k * 8, cudaMemcpyHostToDevice, c->stream));
     BGMF_CK(c, cudaStreamSynchronize(c->stream));
@@ -284,8 +306,8 @@ int bgmf_set_factors(bgmf_ctx* c, const double* u, const double* v, int64_t n, i
   if (!(c->bound && c->k == k)) {
     free_factors(c);
     c->k = k; c->kp = kp;
-    BGMF_CK(c, cudaMalloc(&c->d_u, (size_t)n * kp * 4));
-    BGMF_CK(c, cudaMalloc(&c->d_v, (size_t)m * kp * 4));
+    BGMF_CK(c, dmalloc(&c->d_u, (size_t)n * kp * 4, c->stream));
+    BGMF_CK(c, dmalloc(&c->d_v, (size_t)m * kp * 4, c->stream));
   }
   int rc = upload_rows(c, u, c->d_u, n, k, c->kp);
   if (!rc) rc = upload_rows(c, v, c->d_v, m, k, c->kp);
@@ -304,16 +326,16 @@ int bgmf_init_factors(bgmf_ctx* c, uint64_t state_hi, uint64_t state_lo, uint64_
   if (c->exact) {
     free_factors(c);
     c->k = k; c->kp = k;
-    BGMF_CK(c, cudaMalloc(&c->d_u64, (size_t)n * k * 8));
-    BGMF_CK(c, cudaMalloc(&c->d_v64, (size_t)m * k * 8));
+    BGMF_CK(c, dmalloc(&c->d_u64, (size_t)n * k * 8, c->stream));
+    BGMF_CK(c, dmalloc(&c->d_v64, (size_t)m * k * 8, c->stream));
   } else {
     const int kp = (k + 3) / 4 * 4;
     if (kp > 512) return fail(c, BGMF_ERR_ARG, "fast mode supports k <= 512 (use exact mode)");
     if (!(c->bound && c->k == k)) {
       free_factors(c);
       c->k = k; c->kp = kp;
-      BGMF_CK(c, cudaMalloc(&c->d_u, (size_t)n * kp * 4));
-      BGMF_CK(c, cudaMalloc(&c->d_v, (size_t)m * kp * 4));
+      BGMF_CK(c, dmalloc(&c->d_u, (size_t)n * kp * 4, c->stream));
+      BGMF_CK(c, dmalloc(&c->d_v, (size_t)m * kp * 4, c->stream));
     }
   }
   int rc = init_factors_device(c, state_hi, state_lo, inc_hi, inc_lo, n, m, k);
@@ -440,11 +462,11 @@ int bgmf_holdout_set(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, cons
   }
   std::vector<float> vf(N);
   for (int64_t i = 0; i < count; ++i) vf[i] = (float)vals[i];
-  BGMF_CK(c, cudaMalloc(&c->d_hrow, N * 4));
-  BGMF_CK(c, cudaMalloc(&c->d_hcol, N * 4));
-  BGMF_CK(c, cudaMalloc(&c->d_hval, N * 4));
-  BGMF_CK(c, cudaMalloc(&c->d_hval64, N * 8));
-  BGMF_CK(c, cudaMalloc(&c->d_hcold, N));
+  BGMF_CK(c, dmalloc(&c->d_hrow, N * 4, c->stream));
+  BGMF_CK(c, dmalloc(&c->d_hcol, N * 4, c->stream));
+  BGMF_CK(c, dmalloc(&c->d_hval, N * 4, c->stream));
+  BGMF_CK(c, dmalloc(&c->d_hval64, N * 8, c->stream));
+  BGMF_CK(c, dmalloc(&c->d_hcold, N, c->stream));
   if (count > 0) {
     BGMF_CK(c, cudaMemcpyAsync(c->d_hrow, r.data(), count * 4, cudaMemcpyHostToDevice, c->stream));
     BGMF_CK(c, cudaMemcpyAsync(c->d_hcol, q.data(), count * 4, cudaMemcpyHostToDevice, c->stream));
@@ -571,10 +593,10 @@ int eval_upload(bgmf_ctx* c, EvalBufs& b, const double* u, int64_t n, const doub
     r[i] = (int32_t)rows[i];
     q[i] = (int32_t)cols[i];
   }
-  BGMF_CK(c, cudaMalloc(&b.u, (size_t)n * k * 8));
-  BGMF_CK(c, cudaMalloc(&b.v, (size_t)m * k * 8));
-  BGMF_CK(c, cudaMalloc(&b.r, N * 4));
-  BGMF_CK(c, cudaMalloc(&b.q, N * 4));
+  BGMF_CK(c, dmalloc(&b.u, (size_t)n * k * 8, c->stream));
+  BGMF_CK(c, dmalloc(&b.v, (size_t)m * k * 8, c->stream));
+  BGMF_CK(c, dmalloc(&b.r, N * 4, c->stream));
+  BGMF_CK(c, dmalloc(&b.q, N * 4, c->stream));
   BGMF_CK(c, cudaMemcpyAsync(b.u, u, (size_t)n * k * 8, cudaMemcpyHostToDevice, c->stream));
   BGMF_CK(c, cudaMemcpyAsync(b.v, v, (size_t)m * k * 8, cudaMemcpyHostToDevice, c->stream));
   if (count > 0) {
@@ -596,7 +618,7 @@ int bgmf_predict(const double* u, int64_t n, const double* v, int64_t m, int k,
   rc = eval_upload(c, b, u, n, v, m, k, rows, cols, count);
   if (rc) { g_err = c->err; return rc; }
   if (count == 0) return BGMF_OK;
-  cudaError_t e = cudaMalloc(&b.pred, (size_t)count * 8);
+  cudaError_t e = dmalloc(&b.pred, (size_t)count * 8, c->stream);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMalloc");
   rc = predict_f64(c, b.u, b.v, k, b.r, b.q, count, b.pred);
   if (rc) { g_err = c->err; return rc; }
@@ -617,10 +639,10 @@ int bgmf_sse(const double* u, int64_t n, const double* v, int64_t m, int k, cons
   if (rc) { g_err = c->err; return rc; }
   if (count == 0) { *sse = 0.0; return BGMF_OK; }
   const size_t N = (size_t)count;
-  cudaError_t e = cudaMalloc(&b.vals, N * 8);
+  cudaError_t e = dmalloc(&b.vals, N * 8, c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(b.vals, vals, N * 8, cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess && cold) {
-    e = cudaMalloc(&b.cold, N);
+    e = dmalloc(&b.cold, N, c->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(b.cold, cold, N, cudaMemcpyHostToDevice, c->stream);
   }
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "sse upload");

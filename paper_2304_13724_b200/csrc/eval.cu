@@ -109,7 +109,7 @@ int eval_grid(bgmf_ctx* c) { return c->num_sms * 4; }
 
 int ensure_partials(bgmf_ctx* c) {
   if (!c->d_partials) {
-    BGMF_CK(c, cudaMalloc(&c->d_partials, sizeof(double) * eval_grid(c)));
+    BGMF_CK(c, dmalloc(&c->d_partials, sizeof(double) * eval_grid(c), c->stream));
   }
   return BGMF_OK;
 }

@@ -248,8 +248,8 @@ int bits_for(uint64_t maxval) {  // bits to represent 0..maxval
 }
 
 template <typename T>
-void free_dev(T*& p) {
-  if (p) cudaFree(p);
+void free_dev(T*& p, cudaStream_t s) {
+  if (p) dfree(p, s);
   p = nullptr;
 }
 
@@ -276,8 +276,8 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   if (rbits > 31 || cbits > 31) return fail(ctx, BGMF_ERR_ARG, "block slab wider than 2^31");
 
   // release any previous partition
-  free_dev(ctx->d_lrow); free_dev(ctx->d_lcol); free_dev(ctx->d_val);
-  free_dev(ctx->d_val64); free_dev(ctx->d_order);
+  free_dev(ctx->d_lrow, ctx->stream); free_dev(ctx->d_lcol, ctx->stream); free_dev(ctx->d_val, ctx->stream);
+  free_dev(ctx->d_val64, ctx->stream); free_dev(ctx->d_order, ctx->stream);
   ctx->partitioned = false;
 
   cudaStream_t s = ctx->stream;
@@ -298,8 +298,8 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   unsigned long long* d_bad = nullptr;
   int rc = BGMF_OK;
   auto cleanup = [&]() {
-    free_dev(d_rows); free_dev(d_cols); free_dev(d_vin); free_dev(ka); free_dev(kb);
-    free_dev(ia); free_dev(ib); free_dev(hist); free_dev(tot); free_dev(d_bad); free_dev(d_off);
+    free_dev(d_rows, ctx->stream); free_dev(d_cols, ctx->stream); free_dev(d_vin, ctx->stream); free_dev(ka, ctx->stream); free_dev(kb, ctx->stream);
+    free_dev(ia, ctx->stream); free_dev(ib, ctx->stream); free_dev(hist, ctx->stream); free_dev(tot, ctx->stream); free_dev(d_bad, ctx->stream); free_dev(d_off, ctx->stream);
   };
 #define PCK(call)                                           \
   do {                                                      \
@@ -307,6 +307,7 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
     if (_e != cudaSuccess) { rc = cuda_fail(ctx, _e, #call); cleanup(); return rc; } \
   } while (0)
 
+  prof_mark(ctx, nullptr);
   // host input with 32-bit dimensions: narrowed staged upload (int32 indices,
   // fp32 values unless exact mode needs the fp64 ones)
   const bool narrow = !dev_in && n <= INT32_MAX && m <= INT32_MAX;
@@ -316,14 +317,14 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
     d_cols = const_cast<int64_t*>(cols);
     d_vin = const_cast<double*>(vals);
   } else {
-    PCK(cudaMalloc(&d_rows, N * (narrow ? 4 : 8)));
-    PCK(cudaMalloc(&d_cols, N * (narrow ? 4 : 8)));
-    PCK(cudaMalloc(&d_vin, N * (v32 ? 4 : 8)));
+    PCK(dmalloc(&d_rows, N * (narrow ? 4 : 8), ctx->stream));
+    PCK(dmalloc(&d_cols, N * (narrow ? 4 : 8), ctx->stream));
+    PCK(dmalloc(&d_vin, N * (v32 ? 4 : 8), ctx->stream));
   }
-  PCK(cudaMalloc(&ka, N * 8));
-  PCK(cudaMalloc(&ia, N * 4));
-  PCK(cudaMalloc(&d_bad, 8));
-  PCK(cudaMalloc(&d_off, (nb + 1) * 8));
+  PCK(dmalloc(&ka, N * 8, ctx->stream));
+  PCK(dmalloc(&ia, N * 4, ctx->stream));
+  PCK(dmalloc(&d_bad, 8, ctx->stream));
+  PCK(dmalloc(&d_off, (nb + 1) * 8, ctx->stream));
   int64_t host_bad = -1;
   if (nnz > 0 && narrow) {
     int urc = BGMF_OK;
@@ -336,6 +337,7 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
     PCK(cudaMemcpyAsync(d_cols, cols, nnz * 8, cudaMemcpyHostToDevice, s));
     PCK(cudaMemcpyAsync(d_vin, vals, nnz * 8, cudaMemcpyHostToDevice, s));
   }
+  prof_mark(ctx, "partition: alloc + upload");
   PCK(cudaMemsetAsync(d_bad, 0xFF, 8, s));
   const int grid = ctx->num_sms * 8;
   if (nnz > 0 && host_bad < 0) {
@@ -368,17 +370,18 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
     cleanup();
     return fail(ctx, BGMF_ERR_DATA, buf);
   }
-  free_dev(d_rows);
-  free_dev(d_cols);
+  free_dev(d_rows, ctx->stream);
+  free_dev(d_cols, ctx->stream);
+  prof_mark(ctx, "partition: keys + check");
 
   const int total_bits = rbits + cbits + bbits;
   const int passes = (total_bits + 7) / 8;
   const int64_t ntiles = (nnz + RS_TILE - 1) / RS_TILE;
   if (passes > 0 && nnz > 1) {
-    PCK(cudaMalloc(&kb, N * 8));
-    PCK(cudaMalloc(&ib, N * 4));
-    PCK(cudaMalloc(&hist, (size_t)256 * ntiles * 4));
-    PCK(cudaMalloc(&tot, 256 * 4));
+    PCK(dmalloc(&kb, N * 8, ctx->stream));
+    PCK(dmalloc(&ib, N * 4, ctx->stream));
+    PCK(dmalloc(&hist, (size_t)256 * ntiles * 4, ctx->stream));
+    PCK(dmalloc(&tot, 256 * 4, ctx->stream));
     for (int p = 0; p < passes; ++p) {
       const int shift = 8 * p;
       radix_hist<<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, nnz, shift, ntiles, hist);
@@ -389,14 +392,15 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
       uint64_t* tk = ka; ka = kb; kb = tk;
       uint32_t* ti = ia; ia = ib; ib = ti;
     }
-    free_dev(kb); free_dev(ib); free_dev(hist); free_dev(tot);
+    free_dev(kb, ctx->stream); free_dev(ib, ctx->stream); free_dev(hist, ctx->stream); free_dev(tot, ctx->stream);
   }
+  prof_mark(ctx, "partition: radix sort");
 
-  PCK(cudaMalloc(&ctx->d_lrow, N * 4));
-  PCK(cudaMalloc(&ctx->d_lcol, N * 4));
-  PCK(cudaMalloc(&ctx->d_val, N * 4));
-  PCK(cudaMalloc(&ctx->d_order, N * 4));
-  if (ctx->exact) PCK(cudaMalloc(&ctx->d_val64, N * 8));
+  PCK(dmalloc(&ctx->d_lrow, N * 4, ctx->stream));
+  PCK(dmalloc(&ctx->d_lcol, N * 4, ctx->stream));
+  PCK(dmalloc(&ctx->d_val, N * 4, ctx->stream));
+  PCK(dmalloc(&ctx->d_order, N * 4, ctx->stream));
+  if (ctx->exact) PCK(dmalloc(&ctx->d_val64, N * 8, ctx->stream));
   if (nnz > 0) {
     if (v32)
       decode<float><<<grid, 256, 0, s>>>(ka, ia, reinterpret_cast<const float*>(d_vin), nnz,
@@ -412,7 +416,9 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   PCK(cudaGetLastError());
   PCK(cudaMemcpyAsync(ctx->h_offsets.data(), d_off, (nb + 1) * 8, cudaMemcpyDeviceToHost, s));
   PCK(cudaStreamSynchronize(s));
+  prof_mark(ctx, "partition: decode + offsets");
   cleanup();
+  prof_mark(ctx, "partition: free temporaries");
 #undef PCK
   ctx->partitioned = true;
   return BGMF_OK;

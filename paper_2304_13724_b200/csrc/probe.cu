@@ -1,0 +1,107 @@
+// probe.cu -- the SM<->L2 ceiling of the sweep's access pattern.
+//
+// The sweep (sgd.cu) moves, per rating, one V row in (ld.global.cg, 4k bytes)
+// and one V-row delta out (red.global.add.v4.f32, 4k bytes) against a V block
+// that is L2-resident; its DRAM traffic is ~25x below its algorithmic bytes
+// (profiles/r01_ncu_c4.md), so HBM is not its roofline.  This kernel issues
+// exactly that traffic -- random rows of an L2-resident matrix, k floats per
+// row, groups of L lanes with 16-byte vectors, no arithmetic dependency
+// between rows, several rows in flight per group -- to measure what the SM->L2
+// interface sustains for it on this GPU.  bench.py reports the sweep's
+// achieved row bytes against this measured ceiling next to the HBM roofline.
+
+#include "bgmf_internal.cuh"
+
+namespace bgmf {
+namespace {
+
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+  return x;
+}
+
+// mode 0: read rows; 1: read rows + reduce-add a delta into other rows;
+// 2: reduce-add only.  L = 8 lanes x 4 float4 = 128 floats per row.
+template <int MODE>
+__global__ void __launch_bounds__(256) l2_probe_kernel(float* __restrict__ V, uint32_t rows,
+                                                       int64_t ratings, float* __restrict__ sink) {
+  constexpr int L = 8, V4 = 4, D = 4;
+  const int lane = threadIdx.x & 31, gl = lane & (L - 1);
+  const int64_t group = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / L;
+  const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / L;
+  float acc = 0.f;
+  for (int64_t t0 = group * D; t0 < ratings; t0 += ngroups * D) {
+    float4 v[D][V4];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const uint32_t c = mix32((uint32_t)(t0 + d)) % rows;
+      const float4* row = reinterpret_cast<const float4*>(V + (int64_t)c * (4 * L * V4));
+#pragma unroll
+      for (int q = 0; q < V4; ++q) v[d][q] = MODE == 2 ? make_float4(1e-30f, 0.f, 0.f, 0.f)
+                                                       : __ldcg(row + q * L + gl);
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      if (MODE >= 1) {
+        const uint32_t c = mix32((uint32_t)(t0 + d) ^ 0x9e3779b9u) % rows;
+        float* row = V + (int64_t)c * (4 * L * V4);
+#pragma unroll
+        for (int q = 0; q < V4; ++q) {
+          const float4 z = make_float4(v[d][q].x * 0.f, v[d][q].y * 0.f, v[d][q].z * 0.f,
+                                       v[d][q].w * 0.f);
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + 4 * (q * L + gl)),
+                       "f"(z.x), "f"(z.y), "f"(z.z), "f"(z.w)
+                       : "memory");
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < V4; ++q) acc += v[d][q].x + v[d][q].y + v[d][q].z + v[d][q].w;
+      }
+    }
+  }
+  if (acc == 12345.678f) sink[0] = acc;  // keeps the loads alive
+}
+
+}  // namespace
+}  // namespace bgmf
+
+using namespace bgmf;
+
+extern "C" int bgmf_probe_l2(int device, int64_t rows, int64_t ratings, int mode,
+                             int ctas_per_sm, double* ms_out) {
+  if (!ms_out || rows < 1 || rows > 0x7fffffff || ratings < 1 || mode < 0 || mode > 2)
+    return fail(nullptr, BGMF_ERR_ARG, "bgmf_probe_l2: bad argument");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  float* V = nullptr;
+  float* sink = nullptr;
+  cudaEvent_t a = nullptr, b = nullptr;
+  e = cudaMalloc(&V, (size_t)rows * 128 * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&sink, 4);
+  if (e == cudaSuccess) e = cudaMemset(V, 0, (size_t)rows * 128 * 4);
+  if (e == cudaSuccess) e = cudaEventCreate(&a);
+  if (e == cudaSuccess) e = cudaEventCreate(&b);
+  const dim3 grid(sms * (ctas_per_sm > 0 ? ctas_per_sm : 2));
+  float best = 1e30f;
+  for (int rep = 0; rep < 4 && e == cudaSuccess; ++rep) {
+    cudaEventRecord(a);
+    if (mode == 0) l2_probe_kernel<0><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
+    else if (mode == 1) l2_probe_kernel<1><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
+    else l2_probe_kernel<2><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
+    cudaEventRecord(b);
+    e = cudaEventSynchronize(b);
+    float ms = 0.f;
+    if (e == cudaSuccess) cudaEventElapsedTime(&ms, a, b);
+    if (rep > 0 && ms < best) best = ms;  // rep 0 warms
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  cudaFree(V);
+  cudaFree(sink);
+  if (a) cudaEventDestroy(a);
+  if (b) cudaEventDestroy(b);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "bgmf_probe_l2");
+  *ms_out = best;
+  return BGMF_OK;
+}

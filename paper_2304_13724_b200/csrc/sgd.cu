@@ -805,19 +805,19 @@ int64_t sweep_groups(bgmf_ctx* c, const Shape& sh) {
 int ensure_step_scratch(bgmf_ctx* c, size_t nwork) {
   const int nb = c->I * c->J;
   if (!c->d_sse) {
-    BGMF_CK(c, cudaMalloc(&c->d_sse, sizeof(double) * (nb > 0 ? nb : 1)));
+    BGMF_CK(c, dmalloc(&c->d_sse, sizeof(double) * (nb > 0 ? nb : 1), c->stream));
     BGMF_CK(c, cudaMallocHost(&c->h_sse, sizeof(double) * (nb > 0 ? nb : 1)));
-    BGMF_CK(c, cudaMalloc(&c->d_bad, 8));
+    BGMF_CK(c, dmalloc(&c->d_bad, 8, c->stream));
     BGMF_CK(c, cudaMallocHost(&c->h_bad, 8));
   }
   if (nwork > c->work_cap) {
-    if (c->d_work) cudaFree(c->d_work);
+    if (c->d_work) dfree(c->d_work, c->stream);
     if (c->h_work) cudaFreeHost(c->h_work);
     c->d_work = nullptr;
     c->h_work = nullptr;
     size_t cap = nwork < 64 ? 64 : nwork;
     // device: work table, then exact-mode output slots / batch descriptors
-    BGMF_CK(c, cudaMalloc(&c->d_work, sizeof(BlockWork) * cap * 8));
+    BGMF_CK(c, dmalloc(&c->d_work, sizeof(BlockWork) * cap * 8, c->stream));
     BGMF_CK(c, cudaMallocHost(&c->h_work, sizeof(BlockWork) * cap));
     c->work_cap = cap;
   }
@@ -1196,21 +1196,21 @@ int block_exact(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const dou
   BlockWork* dw = nullptr;
   int rc = BGMF_OK;
   auto cleanup = [&]() {
-    cudaFree(dr); cudaFree(dc); cudaFree(dv); cudaFree(du); cudaFree(dV); cudaFree(dout);
-    cudaFree(dw);
+    dfree(dr, c->stream); dfree(dc, c->stream); dfree(dv, c->stream); dfree(du, c->stream); dfree(dV, c->stream); dfree(dout, c->stream);
+    dfree(dw, c->stream);
   };
 #define XCK(call)                                                                       \
   do {                                                                                  \
     cudaError_t _e = (call);                                                            \
     if (_e != cudaSuccess) { rc = cuda_fail(c, _e, #call); cleanup(); return rc; }      \
   } while (0)
-  XCK(cudaMalloc(&dr, N * 4));
-  XCK(cudaMalloc(&dc, N * 4));
-  XCK(cudaMalloc(&dv, N * 8));
-  XCK(cudaMalloc(&du, (size_t)(u_rows > 0 ? u_rows : 1) * k * 8));
-  XCK(cudaMalloc(&dV, (size_t)(v_rows > 0 ? v_rows : 1) * k * 8));
-  XCK(cudaMalloc(&dout, 8 * 8));
-  XCK(cudaMalloc(&dw, sizeof(BlockWork)));
+  XCK(dmalloc(&dr, N * 4, c->stream));
+  XCK(dmalloc(&dc, N * 4, c->stream));
+  XCK(dmalloc(&dv, N * 8, c->stream));
+  XCK(dmalloc(&du, (size_t)(u_rows > 0 ? u_rows : 1) * k * 8, c->stream));
+  XCK(dmalloc(&dV, (size_t)(v_rows > 0 ? v_rows : 1) * k * 8, c->stream));
+  XCK(dmalloc(&dout, 8 * 8, c->stream));
+  XCK(dmalloc(&dw, sizeof(BlockWork), c->stream));
   BlockWork w{0, count, 0, 0, 0, 0, 0, 0};
   XCK(cudaMemcpyAsync(dw, &w, sizeof w, cudaMemcpyHostToDevice, s));
   if (count > 0) {

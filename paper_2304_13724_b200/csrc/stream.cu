@@ -24,9 +24,10 @@
 namespace bgmf {
 
 void stream_free(bgmf_ctx* c) {
-  for (auto p : c->s_lrow) cudaFree(p);
-  for (auto p : c->s_lcol) cudaFree(p);
-  for (auto p : c->s_val) cudaFree(p);
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  for (auto p : c->s_lrow) dfree(p, c->stream);
+  for (auto p : c->s_lcol) dfree(p, c->stream);
+  for (auto p : c->s_val) dfree(p, c->stream);
   for (auto e : c->ev_copied) cudaEventDestroy(e);
   for (auto e : c->ev_consumed) cudaEventDestroy(e);
   c->s_lrow.clear(); c->s_lcol.clear(); c->s_val.clear();
@@ -96,11 +97,11 @@ int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
   BGMF_CK(c, cudaMallocHost(&c->h_order, N * 4));
   if (c->packed && c->nnz > 0) {  // pack in place of the (no longer needed) lrow
     int32_t* rec = nullptr;
-    BGMF_CK(c, cudaMalloc(&rec, N * 4));
+    BGMF_CK(c, dmalloc(&rec, N * 4, c->stream));
     pack_records<<<c->num_sms * 8, 256, 0, s>>>(c->d_lrow, c->d_lcol, c->nnz, c->cbits, rec);
     BGMF_CK(c, cudaGetLastError());
     BGMF_CK(c, cudaStreamSynchronize(s));
-    cudaFree(c->d_lrow);
+    dfree(c->d_lrow, c->stream);
     c->d_lrow = rec;
   }
   for (int b : order) {  // D2H block by block into the diagonal layout
@@ -115,7 +116,7 @@ int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
                                s));
   }
   BGMF_CK(c, cudaStreamSynchronize(s));
-  cudaFree(c->d_lrow); cudaFree(c->d_lcol); cudaFree(c->d_val); cudaFree(c->d_order);
+  dfree(c->d_lrow, c->stream); dfree(c->d_lcol, c->stream); dfree(c->d_val, c->stream); dfree(c->d_order, c->stream);
   c->d_lrow = c->d_lcol = nullptr;
   c->d_val = nullptr;
   c->d_order = nullptr;
@@ -124,9 +125,9 @@ int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
   for (int i = 0; i < nslots; ++i) {
     int32_t *a = nullptr, *b = nullptr;
     float* v = nullptr;
-    BGMF_CK(c, cudaMalloc(&a, (size_t)slot_ratings * 4));
-    if (!c->packed) BGMF_CK(c, cudaMalloc(&b, (size_t)slot_ratings * 4));
-    BGMF_CK(c, cudaMalloc(&v, (size_t)slot_ratings * 4));
+    BGMF_CK(c, dmalloc(&a, (size_t)slot_ratings * 4, c->stream));
+    if (!c->packed) BGMF_CK(c, dmalloc(&b, (size_t)slot_ratings * 4, c->stream));
+    BGMF_CK(c, dmalloc(&v, (size_t)slot_ratings * 4, c->stream));
     c->s_lrow.push_back(a);
     c->s_lcol.push_back(b);
     c->s_val.push_back(v);

@@ -89,7 +89,8 @@ def train_blocked(d: RatingsDataset, cfg: TrainConfig, test: Optional[RatingsDat
     the GPU's.
     """
     prof = _Phases() if os.environ.get("BGMF_PROFILE") else None
-    if blocked is None:
+    own = blocked is None
+    if own:
         blocked = BlockedDataset(d, make_grid(d.n, d.m, cfg.grid_i, cfg.grid_j), options)
     if prof:
         prof.mark("partition (H2D + GPU sort)")
@@ -152,6 +153,10 @@ def train_blocked(d: RatingsDataset, cfg: TrainConfig, test: Optional[RatingsDat
     u, v = eng.get_factors()
     if prof:
         prof.mark("get_factors (D2H)")
+    if own:  # the partition was made for this call: release its HBM now
+        eng.close()
+    if prof:
+        prof.mark("release device context")
         prof.report()
     return TrainResult(model=FactorModel(u, v), trace=trace, stop_reason=stop)
 
