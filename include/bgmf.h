@@ -51,6 +51,10 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      0 = fp32 warp-per-rating lossless kernels (default).
  *   "min_chunk"  int   minimum ratings per worker group in fast mode
  *                      (bounds per-block concurrency on small blocks; 256).
+ *   "stagger"    0/1/2 chunk-length rule in fast mode: 2 (default) rounds the
+ *                      chunk up to 8*q with q odd so concurrent groups start
+ *                      at staggered columns on dense rows (no lockstep V
+ *                      collisions); 1 = next prime; 0 = as computed.
  *   "timing"     0/1   record CUDA events around every kernel launch.
  *   "warps_per_sm" int resident-warp target used to size chunks (0 = occupancy).
  *   "bulk_red"   0/1   1 = each rating's V-row delta leaves through the TMA
@@ -163,6 +167,19 @@ int bgmf_stream_ratings(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
 /* Rating bytes streamed host->device since the context was created. */
 int bgmf_stream_stats(bgmf_ctx* ctx, double* h2d_bytes);
 
+/* One outer step of the synchronized row-sharded baseline trainer (CPMF,
+ * baselines.py:100-182, `train_sync_parallel`) on a context partitioned 1 x 1
+ * with factors set: shard w = entries [shard_edges[w], shard_edges[w+1]) of
+ * the row-major partition (whole rows, edges from split_bounds), updating U
+ * in place and a private copy of V; the copies' deltas are then summed onto V
+ * in shard order (one shard works on V directly).  sse_out[w] = the shard's
+ * post-sweep SSE; bad_out = {shard, entry within the shard, iteration} of the
+ * first diverged shard in shard order, or -1s.  Exact mode is bit-identical
+ * with the reference; fast mode chunks each shard over worker groups (fp32). */
+int bgmf_run_sync_parallel_step(bgmf_ctx* ctx, const int64_t* shard_edges,
+                                int nshards, double alpha, double beta,
+                                double* sse_out, int64_t* bad_out);
+
 /* Accumulated kernel time since the last reset (requires "timing"=1):
  * out[0] sgd ms, out[1] sse ms, out[2] sgd launches, out[3] sse launches,
  * out[4] algorithmic bytes of the timed sgd launches (ratings*(12+16k)). */
@@ -188,6 +205,27 @@ int bgmf_sgd_converge(const int64_t* rows, const int64_t* cols,
                       double* sse_before, double* sse_after,
                       int64_t* iters_used, int32_t* capped,
                       int64_t* bad_entry, int64_t* bad_iter);
+
+/* _kernels.py:103-140 gradient_steps(rows, cols, vals, u, v, alpha, beta,
+ * iters): full-batch block gradient descent (the kernel behind
+ * kernel.batch_gradient_block, kernel.py:142-158).  Same arguments and
+ * results as bgmf_sgd_sweeps; bit-identical (fp64, reference order). */
+int bgmf_gradient_steps(const int64_t* rows, const int64_t* cols,
+                        const double* vals, int64_t count, double* u,
+                        int64_t u_rows, double* v, int64_t v_rows, int k,
+                        double alpha, double beta, int iters,
+                        double* sse_before, double* sse_after,
+                        int64_t* bad_entry, int64_t* bad_iter);
+
+/* kernel.block_gradients / block_objective (kernel.py:161-179), pure:
+ * gu = beta*u + sum_entries (-2e) v[c] (accumulated in entry order, like
+ * np.add.at), gv likewise (gu / gv may be NULL); *sse = sum e^2 and
+ * *sq_norms = |u|^2 + |v|^2, so objective = sse + beta/2 * sq_norms. */
+int bgmf_block_gradients(const int64_t* rows, const int64_t* cols,
+                         const double* vals, int64_t count, const double* u,
+                         int64_t u_rows, const double* v, int64_t v_rows, int k,
+                         double beta, double* gu, double* gv, double* sse,
+                         double* sq_norms);
 
 /* _kernels.py:16-28 block_sse(rows, cols, vals, u, v) */
 int bgmf_block_sse(const int64_t* rows, const int64_t* cols,

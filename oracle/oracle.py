@@ -66,6 +66,11 @@ def lib():
             _i64p, _i64p, _f64p, ctypes.c_int64, _f64p, _f64p, ctypes.c_int,
             ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int64,
             _f64p, _f64p, _i64p, ctypes.POINTER(ctypes.c_int), _i64p, _i64p]
+        L.oracle_gradient_steps.restype = None
+        L.oracle_gradient_steps.argtypes = [
+            _i64p, _i64p, _f64p, ctypes.c_int64, _f64p, ctypes.c_int64, _f64p, ctypes.c_int64,
+            ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+            _f64p, _f64p, _i64p, _i64p]
         L.oracle_partition.restype = ctypes.c_int
         L.oracle_partition.argtypes = [
             _i64p, _i64p, _f64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
@@ -188,6 +193,35 @@ def sgd_converge(rows, cols, vals, u, v, alpha, beta, tol, cap):
                               cap, ctypes.byref(sb), ctypes.byref(sa), ctypes.byref(iu),
                               ctypes.byref(cp), ctypes.byref(be), ctypes.byref(bi))
     return sb.value, sa.value, iu.value, cp.value, be.value, bi.value
+
+
+def gradient_steps(rows, cols, vals, u, v, alpha, beta, iters):
+    """_kernels.py:103-140, in place on u, v.  Reference tuple
+    (sse_before, sse_after, bad_entry, bad_iter)."""
+    assert u.flags.c_contiguous and v.flags.c_contiguous
+    rows = np.ascontiguousarray(rows, np.int64)
+    cols = np.ascontiguousarray(cols, np.int64)
+    vals = np.ascontiguousarray(vals, np.float64)
+    sb, sa = ctypes.c_double(), ctypes.c_double()
+    be, bi = ctypes.c_int64(), ctypes.c_int64()
+    lib().oracle_gradient_steps(_p(rows, _i64p), _p(cols, _i64p), _p(vals, _f64p), len(rows),
+                                _p(u, _f64p), u.shape[0], _p(v, _f64p), v.shape[0], u.shape[1],
+                                alpha, beta, iters, ctypes.byref(sb), ctypes.byref(sa),
+                                ctypes.byref(be), ctypes.byref(bi))
+    return sb.value, sa.value, be.value, bi.value
+
+
+def block_gradients(rows, cols, vals, u, v, beta):
+    """kernel.py:161-179 restated in numpy: (objective, gu, gv)."""
+    rows = np.asarray(rows, np.int64)
+    cols = np.asarray(cols, np.int64)
+    e = np.asarray(vals, np.float64) - np.einsum("ij,ij->i", u[rows], v[cols])
+    gu = beta * u
+    gv = beta * v
+    np.add.at(gu, rows, -2.0 * e[:, None] * v[cols])
+    np.add.at(gv, cols, -2.0 * e[:, None] * u[rows])
+    reg = np.square(u).sum() + np.square(v).sum()
+    return float(e @ e + 0.5 * beta * reg), gu, gv
 
 
 def partition(rows, cols, vals, n: int, m: int, I: int, J: int) -> dict:
@@ -334,6 +368,57 @@ def train_blocked(n, m, rows, cols, vals, *, k=10, alpha=1e-4, beta=1e-2, delta=
                 stop = "converged"
                 break
             if len(trace) >= 2 and trace[-2]["train_rmse"] - train < delta:
+                stop = "converged"
+                break
+    return u, v, trace, stop
+
+
+def train_sync_parallel(n, m, rows, cols, vals, *, k=10, alpha=1e-4, beta=1e-2, delta=1e-2,
+                        outer_steps=100, seed=0, workers=1, test=None, early_stop=True):
+    """baselines.py:100-182 (CPMF): row shards over the row-major 1x1
+    partition, each swept once per step on the shared U and a private copy
+    of V, V deltas summed in shard order.  Returns (u, v, trace, stop)."""
+    rows = np.ascontiguousarray(rows, np.int64)
+    cols = np.ascontiguousarray(cols, np.int64)
+    vals = np.ascontiguousarray(vals, np.float64)
+    P = partition(rows, cols, vals, n, m, 1, 1)
+    wr, wc, wv = P["rows"], P["cols"], P["values"]
+    u, v = init_factors(n, m, k, seed)
+    shards = min(workers, max(n, 1))
+    edges = np.searchsorted(wr, split_bounds(n, shards))
+    trace: list[dict] = []
+    stop = "max_steps"
+    for step in range(1, outer_steps + 1):
+        t0 = time.perf_counter()
+        results = []
+        if shards == 1:
+            out = sgd_sweeps(wr, wc, wv, u, v, alpha, beta, 1)
+            results.append((out, int(edges[1] - edges[0])))
+        else:
+            v_start = v.copy()
+            privates = [v_start.copy() for _ in range(shards)]
+            for w in range(shards):
+                lo, hi = edges[w], edges[w + 1]
+                out = sgd_sweeps(wr[lo:hi], wc[lo:hi], wv[lo:hi], u, privates[w], alpha, beta, 1)
+                results.append((out, int(hi - lo)))
+            delta_v = np.zeros_like(v)
+            for v_w in privates:
+                delta_v += v_w - v_start
+            v[:] = v_start + delta_v
+        for w, (out, _) in enumerate(results):
+            if out[2] >= 0:
+                raise OracleDivergence(None, int(out[2]), int(out[3]), step, trace)
+        sse = sum(r[0][1] for r in results)
+        count = sum(r[1] for r in results)
+        test_rmse = None
+        if test is not None:
+            test_rmse = holdout_rmse(u, v, rows, cols, vals, *test)
+        trace.append(dict(step=step, train_rmse=float(np.sqrt(sse / count)) if count else 0.0,
+                          test_rmse=test_rmse, seconds=time.perf_counter() - t0,
+                          inner_iters=1, capped_blocks=0))
+        if early_stop:
+            if count == 0 or (len(trace) >= 2 and
+                              trace[-2]["train_rmse"] - trace[-1]["train_rmse"] < delta):
                 stop = "converged"
                 break
     return u, v, trace, stop

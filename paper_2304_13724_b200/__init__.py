@@ -8,10 +8,11 @@ hand-written sm_100a CUDA (``libbgmf.so``, C ABI in ``include/bgmf.h``).
 There is no CPU fallback: numeric calls raise ``NativeUnavailable`` when the
 library or the GPU is missing.
 
-Not provided (outside the hot path): the CMF/CPMF baseline
-trainers, the verification-only gradient kernels (batch_gradient_block,
-block_objective, block_gradients), sweep_budget/auto_splits, CLI and plots.
-File formats and model / trace persistence are host helpers (data.py).
+Also provided: the CMF / CPMF baseline trainers
+(train_sequential, train_sync_parallel) and the verification kernels
+(batch_gradient_block, block_objective, block_gradients) on the GPU,
+sweep_budget / auto_splits over train_blocked, and the file formats and model /
+trace persistence as host helpers (data.py).  Not provided: CLI and plots.
 """
 
 from ._native import CudaError, NativeUnavailable
@@ -22,12 +23,15 @@ from .core import (AdaptiveDecreasing, Constant, ConvergeEachBlock, ConvergenceT
 from .data import (FORMATS, SyntheticSpec, gen_synthetic, load, load_model, read_trace,
                    save_dataset, save_model, split, write_trace)
 from .device import Engine, EngineOptions
-from .kernel import BlockStats, BlockTask, block_sse, sgd_block, task_from_block
+from .kernel import (BlockStats, BlockTask, batch_gradient_block, block_gradients,
+                     block_objective, block_sse, sgd_block, task_from_block)
 from .metrics import HoldoutEvaluator, RmseAccumulator, finalize, merge, rmse, test_rmse
 from .partition import (Block, BlockedDataset, BlockGrid, block_dataset, locate, make_grid,
                         partition, permute_dataset, split_bounds)
 from .scheduler import Batch, StepPlan, format_plan, plan_step, validate_plan
-from .trainer import TrainResult, resolve_inner_iters, train_blocked
+from .trainer import (SweepPoint, TrainResult, auto_splits, resolve_inner_iters, sweep_budget,
+                      train_blocked)
+from .baselines import train_sequential, train_sync_parallel
 
 __all__ = [
     "FORMATS", "load", "load_model", "read_trace", "save_dataset", "save_model", "write_trace",
@@ -41,6 +45,8 @@ __all__ = [
     "merge", "parse_schedule", "partition", "permute_dataset", "plan_step",
     "resolve_inner_iters", "rmse", "sgd_block", "split", "split_bounds", "task_from_block",
     "test_rmse", "train_blocked", "validate_dataset", "validate_plan",
+    "SweepPoint", "auto_splits", "batch_gradient_block", "block_gradients", "block_objective",
+    "sweep_budget", "train_sequential", "train_sync_parallel",
 ]
 
 __version__ = "0.1.0"

@@ -51,6 +51,7 @@ SIGNATURES = {
                                ctypes.c_uint64, _l, _l, _i]),
     "bgmf_bind_factors": (_i, [_ctx, _vp, _vp, _l, _l, _i, _i]),
     "bgmf_run_step": (_i, [_ctx, _i32p, _i32p, _i, _i, _d, _d, _f64p, _i64p]),
+    "bgmf_run_sync_parallel_step": (_i, [_ctx, _i64p, _i, _d, _d, _f64p, _i64p]),
     "bgmf_run_step_converge": (_i, [_ctx, _i32p, _i32p, _i, _d, _l, _d, _d, _f64p, _i64p,
                                     _i32p, _i64p]),
     "bgmf_train_sse": (_i, [_ctx, _f64p]),
@@ -61,6 +62,10 @@ SIGNATURES = {
     "bgmf_stream_stats": (_i, [_ctx, _f64p]),
     "bgmf_sgd_sweeps": (_i, [_i64p, _i64p, _f64p, _l, _f64p, _l, _f64p, _l, _i, _d, _d, _i,
                              _f64p, _f64p, _i64p, _i64p]),
+    "bgmf_gradient_steps": (_i, [_i64p, _i64p, _f64p, _l, _f64p, _l, _f64p, _l, _i, _d, _d, _i,
+                                 _f64p, _f64p, _i64p, _i64p]),
+    "bgmf_block_gradients": (_i, [_i64p, _i64p, _f64p, _l, _f64p, _l, _f64p, _l, _i, _d, _f64p,
+                                  _f64p, _f64p, _f64p]),
     "bgmf_sgd_converge": (_i, [_i64p, _i64p, _f64p, _l, _f64p, _l, _f64p, _l, _i, _d, _d, _d,
                                _l, _f64p, _f64p, _i64p, _i32p, _i64p, _i64p]),
     "bgmf_block_sse": (_i, [_i64p, _i64p, _f64p, _l, _f64p, _l, _f64p, _l, _i, _f64p]),

@@ -53,6 +53,7 @@ struct bgmf_ctx {
   // options
   bool exact = false;
   int min_chunk = 256;
+  int stagger = 2;       // chunk-length rule (stagger_chunk)
   bool timing = false;
   int warps_per_sm = 0;
   bool bulk_red = false;  // V deltas via TMA bulk reduce (measured slower: SM->L2 bound)
@@ -86,6 +87,8 @@ struct bgmf_ctx {
   double* d_sse = nullptr;               // [I*J]
   unsigned long long* d_bad = nullptr;   // [1]
   bgmf::BlockWork* d_work = nullptr;
+  void* d_priv = nullptr;                // sync-parallel private V copies
+  size_t priv_bytes = 0;
   bgmf::BlockWork* h_work = nullptr;     // pinned
   size_t work_cap = 0;
   double* h_sse = nullptr;               // pinned [I*J]
@@ -143,6 +146,29 @@ inline void dfree(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
 }
 
+// Chunk length used by the fast paths.  Groups start their chunks at entry
+// c*len of a block; when len is a multiple of a row length (dense rows, all
+// with the same column order) every group walks the same columns in lockstep
+// and their V updates collide on every rating (drift 0.08 RMSE on a dense
+// 64x64 block).  mode 1: the smallest prime >= cl; mode 2: 8*q with q odd
+// (>= cl): stagger for every even row length >= 16 while chunk starts stay
+// 32-byte aligned for the L-wide triple loads.
+inline int64_t stagger_chunk(int64_t cl, int mode) {
+  if (mode == 2) {
+    int64_t q = (cl + 7) / 8;
+    if ((q & 1) == 0) ++q;
+    return 8 * q;
+  }
+  if (mode != 1) return cl;
+  if (cl < 3) return cl < 2 ? 2 : cl;
+  for (int64_t p = cl | 1;; p += 2) {
+    bool prime = true;
+    for (int64_t d = 3; d * d <= p; d += 2)
+      if (p % d == 0) { prime = false; break; }
+    if (prime) return p;
+  }
+}
+
 // error helpers --------------------------------------------------------
 int fail(bgmf_ctx* ctx, int code, const std::string& msg);
 int cuda_fail(bgmf_ctx* ctx, cudaError_t e, const char* what);
@@ -178,6 +204,8 @@ int run_step_fast(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
                   int nbatch, int iters, float alpha, float beta);
 int run_step_exact(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
                    int nbatch, int iters, double alpha, double beta);
+int run_sync_parallel_step(bgmf_ctx* c, const int64_t* edges, int nshards, double alpha,
+                           double beta, double* sse_out, int64_t* bad_out);
 int run_step_converge_exact(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
                             int nbatch, double tol, int64_t cap, double alpha, double beta,
                             int64_t* iters_out, int32_t* capped_out);
@@ -203,6 +231,14 @@ int block_exact(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const d
                 int64_t count, double* u, int64_t u_rows, double* v, int64_t v_rows, int k,
                 double alpha, double beta, int mode, int iters, double tol, int64_t cap,
                 double* out6);
+
+// gradient.cu -- verification kernels (_kernels.gradient_steps, kernel.py:161-179)
+int gradient_steps(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const double* vals,
+                   int64_t count, double* u, int64_t nu, double* v, int64_t nv, int k,
+                   double alpha, double beta, int iters, double* out4);
+int block_gradients(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const double* vals,
+                    int64_t count, const double* u, int64_t nu, const double* v, int64_t nv,
+                    int k, double beta, double* gu, double* gv, double* out2);
 
 // init.cu
 int init_factors_device(bgmf_ctx* ctx, uint64_t shi, uint64_t slo, uint64_t ihi, uint64_t ilo,

@@ -181,6 +181,7 @@ void bgmf_destroy(bgmf_ctx* c) {
   dfree(c->d_lrow, c->stream); dfree(c->d_lcol, c->stream); dfree(c->d_val, c->stream); dfree(c->d_val64, c->stream);
   dfree(c->d_order, c->stream); dfree(c->d_sse, c->stream); dfree(c->d_bad, c->stream); dfree(c->d_work, c->stream);
   dfree(c->d_partials, c->stream);
+  dfree(c->d_priv, c->stream);
   cudaStreamSynchronize(c->stream);
   if (c->h_work) cudaFreeHost(c->h_work);
   if (c->h_sse) cudaFreeHost(c->h_sse);
@@ -201,6 +202,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "fused")) c->fused = value < 0 ? -1 : (value != 0.0 ? 1 : 0);
   else if (!strcmp(key, "bulk_red")) c->bulk_red = value != 0.0;
   else if (!strcmp(key, "sse_wide")) c->sse_wide = value != 0.0;
+  else if (!strcmp(key, "stagger")) c->stagger = (int)value;
   else if (!strcmp(key, "fused_max_batch")) c->fused_max_batch = (int64_t)value;
   else return fail(c, BGMF_ERR_ARG, std::string("unknown option ") + key);
   return BGMF_OK;
@@ -400,6 +402,16 @@ int bgmf_run_step(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, in
   return BGMF_OK;
 }
 
+int bgmf_run_sync_parallel_step(bgmf_ctx* c, const int64_t* shard_edges, int nshards,
+                                double alpha, double beta, double* sse_out, int64_t* bad_out) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  int rc = check_step_ready(c);
+  if (rc) return rc;
+  if (c->streaming) return fail(c, BGMF_ERR_STATE, "sync-parallel steps do not stream");
+  cudaSetDevice(c->device);
+  return run_sync_parallel_step(c, shard_edges, nshards, alpha, beta, sse_out, bad_out);
+}
+
 int bgmf_run_step_converge(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off,
                            int nbatch, double tol, int64_t cap, double alpha, double beta,
                            double* sse_out, int64_t* iters_out, int32_t* capped_out,
@@ -533,6 +545,39 @@ int bgmf_sgd_sweeps(const int64_t* rows, const int64_t* cols, const double* vals
   if (rc) { g_err = c->err; return rc; }
   *sse_before = o[0]; *sse_after = o[1];
   *bad_entry = (int64_t)o[4]; *bad_iter = (int64_t)o[5];
+  return BGMF_OK;
+}
+
+int bgmf_gradient_steps(const int64_t* rows, const int64_t* cols, const double* vals,
+                        int64_t count, double* u, int64_t u_rows, double* v, int64_t v_rows,
+                        int k, double alpha, double beta, int iters, double* sse_before,
+                        double* sse_after, int64_t* bad_entry, int64_t* bad_iter) {
+  int rc;
+  bgmf_ctx* c = scratch_ctx(&rc);
+  if (!c) return rc;
+  if (!sse_before || !sse_after || !bad_entry || !bad_iter)
+    return fail(nullptr, BGMF_ERR_ARG, "NULL out-parameter");
+  double o[4];
+  rc = gradient_steps(c, rows, cols, vals, count, u, u_rows, v, v_rows, k, alpha, beta, iters, o);
+  if (rc) { g_err = c->err; return rc; }
+  *sse_before = o[0]; *sse_after = o[1];
+  *bad_entry = (int64_t)o[2]; *bad_iter = (int64_t)o[3];
+  return BGMF_OK;
+}
+
+int bgmf_block_gradients(const int64_t* rows, const int64_t* cols, const double* vals,
+                         int64_t count, const double* u, int64_t u_rows, const double* v,
+                         int64_t v_rows, int k, double beta, double* gu, double* gv,
+                         double* sse, double* sq_norms) {
+  int rc;
+  bgmf_ctx* c = scratch_ctx(&rc);
+  if (!c) return rc;
+  if (!sse || !sq_norms) return fail(nullptr, BGMF_ERR_ARG, "NULL out-parameter");
+  double o[2];
+  rc = block_gradients(c, rows, cols, vals, count, u, u_rows, v, v_rows, k, beta, gu, gv, o);
+  if (rc) { g_err = c->err; return rc; }
+  *sse = o[0];
+  *sq_norms = o[1];
   return BGMF_OK;
 }
 

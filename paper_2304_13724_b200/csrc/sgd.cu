@@ -759,6 +759,7 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
       const int64_t slots = groups - nonempty > 0 ? groups - nonempty : 1;
       cl = (batch_nnz + slots - 1) / slots;
       if (cl < c->min_chunk) cl = c->min_chunk;
+      cl = stagger_chunk(cl, c->stagger);
     }
     ranges[t].w0 = w;
     int chunks = 0;
@@ -798,6 +799,28 @@ int64_t sweep_groups(bgmf_ctx* c, const Shape& sh) {
     c->groups_key = key;
   }
   return c->groups_cache;
+}
+
+// CPMF merge (baselines.py:170-175): v = v_start + sum_w (v_w - v_start),
+// the delta accumulated over shards in shard order from zero, per element.
+template <typename T>
+__global__ void merge_private_v(T* __restrict__ V, const T* __restrict__ priv, int64_t elems,
+                                int nshards) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < elems;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T s = V[i];
+    T delta = 0;
+    for (int w = 0; w < nshards; ++w) delta = delta + (priv[(int64_t)w * elems + i] - s);
+    V[i] = s + delta;
+  }
+}
+
+template <typename T>
+__global__ void broadcast_v(const T* __restrict__ V, T* __restrict__ priv, int64_t elems,
+                            int nshards) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < elems * nshards;
+       i += (int64_t)gridDim.x * blockDim.x)
+    priv[i] = V[i % elems];
 }
 
 }  // namespace
@@ -975,6 +998,129 @@ int run_step_exact(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, i
     }
   }
   *c->h_bad = best;
+  return BGMF_OK;
+}
+
+// One outer step of the synchronized row-sharded trainer (CPMF,
+// baselines.py:100-182) on a 1x1 partition: shard w owns entries
+// [edges[w], edges[w+1]) (whole rows), updates U in place and a private copy of
+// V; the copies' deltas are merged in shard order.  A single shard works on V
+// directly.  Exact mode: one fp64 thread per shard in the reference's order
+// (bit-identical); fast mode: each shard is chunked over worker groups like a
+// block of the stratum kernel, V copies in fp32.  sse_out[w] = the shard's
+// post-sweep SSE; bad_out = {shard, entry, iteration} of the first diverged
+// shard in shard order, or -1s.
+int run_sync_parallel_step(bgmf_ctx* c, const int64_t* edges, int nshards, double alpha,
+                           double beta, double* sse_out, int64_t* bad_out) {
+  if (c->I != 1 || c->J != 1) return fail(c, BGMF_ERR_STATE, "sync-parallel needs a 1x1 partition");
+  if (nshards < 1 || !edges || !sse_out || !bad_out) return fail(c, BGMF_ERR_ARG, "bad shards");
+  for (int w = 0; w < nshards; ++w)
+    if (edges[w] < 0 || edges[w] > edges[w + 1] || edges[w + 1] > c->nnz)
+      return fail(c, BGMF_ERR_ARG, "shard edges must be non-decreasing within [0, nnz]");
+  cudaStream_t s = c->stream;
+  int rc = ensure_step_scratch(c, (size_t)nshards);
+  if (rc) return rc;
+  const bool priv = nshards > 1;
+  const int64_t elems = c->m * (c->exact ? c->k : c->kp);
+  const size_t esz = c->exact ? 8 : 4;
+  if (priv) {
+    const size_t need = (size_t)nshards * elems * esz;
+    if (need > c->priv_bytes) {
+      dfree(c->d_priv, s);
+      c->d_priv = nullptr;
+      c->priv_bytes = 0;
+      BGMF_CK(c, dmalloc(&c->d_priv, need, s));
+      c->priv_bytes = need;
+    }
+  }
+  const int grid = c->num_sms * 4;
+  if (c->exact) {
+    double* V = c->d_v64;
+    double* P = reinterpret_cast<double*>(c->d_priv);
+    for (int w = 0; w < nshards; ++w) {
+      BlockWork& bw = c->h_work[w];
+      bw = BlockWork{edges[w], edges[w + 1], 0, priv ? (int64_t)w * c->m : 0, 0, 0, w, w};
+    }
+    BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * nshards,
+                               cudaMemcpyHostToDevice, s));
+    if (priv) broadcast_v<double><<<grid, 256, 0, s>>>(V, P, elems, nshards);
+    double* d_out = reinterpret_cast<double*>(c->d_work + c->work_cap);
+    block_exact_kernel<<<(nshards + 31) / 32, 32, 0, s>>>(
+        c->d_work, nshards, c->d_lrow, c->d_lcol, c->d_val64, c->d_u64, priv ? P : V, c->k,
+        alpha, beta, 0, 1, 0.0, 0, 0, d_out);
+    if (priv) merge_private_v<double><<<grid, 256, 0, s>>>(V, P, elems, nshards);
+    BGMF_CK(c, cudaGetLastError());
+    std::vector<double> out((size_t)8 * nshards);
+    BGMF_CK(c, cudaMemcpyAsync(out.data(), d_out, sizeof(double) * 8 * nshards,
+                               cudaMemcpyDeviceToHost, s));
+    BGMF_CK(c, cudaStreamSynchronize(s));
+    bad_out[0] = bad_out[1] = bad_out[2] = -1;
+    for (int w = 0; w < nshards; ++w) {
+      sse_out[w] = out[8 * w + 1];
+      if (bad_out[0] < 0 && out[8 * w + 4] >= 0) {
+        bad_out[0] = w;
+        bad_out[1] = (int64_t)out[8 * w + 4];
+        bad_out[2] = (int64_t)out[8 * w + 5];
+      }
+    }
+    return BGMF_OK;
+  }
+  // fast mode: shards as the "blocks" of one chunked launch
+  const int64_t groups = fast_groups(c);
+  int64_t total = 0;
+  int nonempty = 0;
+  for (int w = 0; w < nshards; ++w) {
+    total += edges[w + 1] - edges[w];
+    nonempty += edges[w + 1] > edges[w];
+  }
+  const int64_t slots = groups - nonempty > 0 ? groups - nonempty : 1;
+  int64_t cl = (total + slots - 1) / slots;
+  if (cl < c->min_chunk) cl = c->min_chunk;
+      cl = stagger_chunk(cl, c->stagger);
+  int nw = 0, chunks = 0;
+  for (int w = 0; w < nshards; ++w) {
+    const int64_t cnt = edges[w + 1] - edges[w];
+    if (cnt == 0) continue;
+    const int64_t bl = cl < cnt ? cl : cnt;
+    c->h_work[nw++] = BlockWork{edges[w], edges[w + 1], 0, priv ? (int64_t)w * c->m : 0,
+                                (int32_t)bl, chunks, w, w};
+    chunks += (int)((cnt + bl - 1) / bl);
+  }
+  if (nw > 0)
+    BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * nw,
+                               cudaMemcpyHostToDevice, s));
+  double* sse_dev = reinterpret_cast<double*>(c->d_work + c->work_cap);
+  BGMF_CK(c, cudaMemsetAsync(sse_dev, 0, sizeof(double) * nshards, s));
+  BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+  float* V = c->d_v;
+  float* P = reinterpret_cast<float*>(c->d_priv);
+  if (priv) broadcast_v<float><<<grid, 256, 0, s>>>(V, P, elems, nshards);
+  // the stratum kernels address V / the SSE array through the context
+  double* keep_sse = c->d_sse;
+  c->d_sse = sse_dev;
+  if (priv) c->d_v = P;
+  rc = launch_piece(c, c->d_work, nw, chunks, c->d_lrow, c->d_lcol, c->d_val, 1, (float)alpha,
+                    (float)beta, (double)total, -1);
+  c->d_v = V;
+  c->d_sse = keep_sse;
+  if (rc) return rc;
+  if (priv) merge_private_v<float><<<grid, 256, 0, s>>>(V, P, elems, nshards);
+  BGMF_CK(c, cudaGetLastError());
+  std::vector<double> out((size_t)nshards);
+  BGMF_CK(c, cudaMemcpyAsync(out.data(), sse_dev, sizeof(double) * nshards,
+                             cudaMemcpyDeviceToHost, s));
+  BGMF_CK(c, cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, s));
+  BGMF_CK(c, cudaStreamSynchronize(s));
+  if (c->timing) harvest_timing(c);
+  for (int w = 0; w < nshards; ++w) sse_out[w] = out[w];
+  const unsigned long long b = *c->h_bad;
+  if (b == kNoBad) {
+    bad_out[0] = bad_out[1] = bad_out[2] = -1;
+  } else {  // pos = shard
+    bad_out[0] = (int64_t)(b >> 48);
+    bad_out[1] = (int64_t)(b & 0xFFFFFFFFull);
+    bad_out[2] = (int64_t)((b >> 32) & 0xFFFF);
+  }
   return BGMF_OK;
 }
 

@@ -203,6 +203,7 @@ int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, 
       const int64_t slots = groups - nonempty > 0 ? groups - nonempty : 1;
       int64_t cl = (fill + slots - 1) / slots;
       if (cl < c->min_chunk) cl = c->min_chunk;
+      cl = stagger_chunk(cl, c->stagger);
       Piece pc{w, 0, 0, (int)(pieces.size() % c->nslots), 0.0};
       int64_t off = 0;
       for (int qq = q; qq < q_end; ++qq) {

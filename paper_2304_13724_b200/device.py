@@ -212,6 +212,18 @@ class Engine:
             N.ptr(capped, N._i32p), N.ptr(bad, N._i64p)))
         return sse, iters, capped, (None if bad[0] < 0 else tuple(int(x) for x in bad))
 
+    def run_sync_parallel_step(self, edges: np.ndarray, alpha: float, beta: float):
+        """CPMF step on a 1x1 partition; returns (per-shard SSE, bad) where
+        bad = (shard, entry, iteration) or None."""
+        edges = np.ascontiguousarray(edges, np.int64)
+        ns = len(edges) - 1
+        sse = np.zeros(ns, np.float64)
+        bad = np.zeros(3, np.int64)
+        self._check(self._L.bgmf_run_sync_parallel_step(
+            self._h, N.ptr(edges, N._i64p), ns, float(alpha), float(beta),
+            N.ptr(sse, N._f64p), N.ptr(bad, N._i64p)))
+        return sse, (None if bad[0] < 0 else tuple(int(x) for x in bad))
+
     def train_sse(self) -> float:
         out = ctypes.c_double()
         self._check(self._L.bgmf_train_sse(self._h, ctypes.byref(out)))

@@ -142,3 +142,54 @@ def block_sse(task: BlockTask) -> float:
                              len(rows), N.ptr(u, N._f64p), u.shape[0], N.ptr(v, N._f64p),
                              v.shape[0], u.shape[1], ctypes.byref(out)))
     return out.value
+
+
+def batch_gradient_block(task: BlockTask) -> BlockStats:
+    """Full-batch gradient updates on the block (kernel.py:142-158): the
+    verification variant of sgd_block, through ``bgmf_gradient_steps`` (GPU,
+    fp64, the reference's accumulation order: bit-identical)."""
+    if task.inner_iters is None:
+        raise ValueError("converge mode is only defined for sgd_block")
+    L = N.load()
+    rows, cols, vals = N.i64(task.rows), N.i64(task.cols), N.f64(task.values)
+    sl = _Slices(task)
+    sb, sa = ctypes.c_double(), ctypes.c_double()
+    be, bit = ctypes.c_int64(), ctypes.c_int64()
+    N.check(L.bgmf_gradient_steps(
+        N.ptr(rows, N._i64p), N.ptr(cols, N._i64p), N.ptr(vals, N._f64p), len(rows),
+        N.ptr(sl.u, N._f64p), sl.u.shape[0], N.ptr(sl.v, N._f64p), sl.v.shape[0],
+        sl.u.shape[1], task.alpha, task.beta, int(task.inner_iters), ctypes.byref(sb),
+        ctypes.byref(sa), ctypes.byref(be), ctypes.byref(bit)))
+    sl.write_back()
+    if be.value >= 0:
+        raise divergence(task.bi, task.bj, be.value, bit.value)
+    return BlockStats(sb.value, sa.value, len(rows), int(task.inner_iters))
+
+
+def _gradients(task: BlockTask, want_grads: bool):
+    L = N.load()
+    rows, cols, vals = N.i64(task.rows), N.i64(task.cols), N.f64(task.values)
+    u = np.ascontiguousarray(task.u_slice, np.float64)
+    v = np.ascontiguousarray(task.v_slice, np.float64)
+    gu = np.empty_like(u) if want_grads else None
+    gv = np.empty_like(v) if want_grads else None
+    sse, reg = ctypes.c_double(), ctypes.c_double()
+    N.check(L.bgmf_block_gradients(
+        N.ptr(rows, N._i64p), N.ptr(cols, N._i64p), N.ptr(vals, N._f64p), len(rows),
+        N.ptr(u, N._f64p), u.shape[0], N.ptr(v, N._f64p), v.shape[0], u.shape[1],
+        float(task.beta), None if gu is None else N.ptr(gu, N._f64p),
+        None if gv is None else N.ptr(gv, N._f64p), ctypes.byref(sse), ctypes.byref(reg)))
+    return sse.value + 0.5 * task.beta * reg.value, gu, gv
+
+
+def block_objective(task: BlockTask) -> float:
+    """Squared residual sum plus (beta/2) times the slice norms; pure
+    (kernel.py:161-168).  GPU fp64."""
+    return float(_gradients(task, False)[0])
+
+
+def block_gradients(task: BlockTask) -> tuple[np.ndarray, np.ndarray]:
+    """Analytic gradients of block_objective w.r.t. the two slices; pure
+    (kernel.py:171-179).  GPU fp64, accumulated in entry order like np.add.at."""
+    _, gu, gv = _gradients(task, True)
+    return gu, gv

@@ -94,7 +94,7 @@ def train_blocked(d: RatingsDataset, cfg: TrainConfig, test: Optional[RatingsDat
         blocked = BlockedDataset(d, make_grid(d.n, d.m, cfg.grid_i, cfg.grid_j), options)
     if prof:
         prof.mark("partition (H2D + GPU sort)")
-    elif (blocked.grid.grid_i, blocked.grid.grid_j) != (cfg.grid_i, cfg.grid_j) \
+    if (blocked.grid.grid_i, blocked.grid.grid_j) != (cfg.grid_i, cfg.grid_j) \
             or blocked.dataset is not d:
         raise ValueError("blocked must partition d with cfg's grid")
     eng = blocked.engine
@@ -221,3 +221,57 @@ def _run_step(eng, batches, g, tol, cfg, counts, hooks, block_hook):
         if g is not None:
             max_iters = g
     return acc, max_iters, capped
+
+
+@dataclass(frozen=True)
+class SweepPoint:
+    """Outcome of one (outer, inner) split of a fixed iteration budget
+    (trainer.py:187-194)."""
+
+    outer: int
+    inner: int
+    final_rmse: float
+    seconds: float
+
+
+def auto_splits(total_budget: int) -> list[tuple[int, int]]:
+    """All (outer, inner) factorizations of the budget, ascending outer
+    (trainer.py:197-205)."""
+    if total_budget < 1:
+        raise ValueError(f"budget must be >= 1, got {total_budget}")
+    return [(outer, total_budget // outer) for outer in range(1, total_budget + 1)
+            if total_budget % outer == 0]
+
+
+def sweep_budget(d: RatingsDataset, cfg: TrainConfig, total_budget: int,
+                 splits: list[tuple[int, int]], *, timing: bool = True,
+                 options: Optional[EngineOptions] = None) -> list[SweepPoint]:
+    """One training run per (outer, inner) split of a fixed total iteration
+    budget, Constant(inner) for exactly ``outer`` steps from the same seeded
+    init (trainer.py:208-248).  final_rmse is the full-dataset RMSE of the
+    finished model (GPU), not the trace value.  The partition is built once
+    and reused by every split."""
+    from dataclasses import replace
+
+    from .metrics import rmse
+
+    for outer, inner in splits:
+        if outer < 1 or inner < 1 or outer * inner != total_budget:
+            raise ValueError(f"split ({outer}, {inner}) does not factor budget {total_budget}")
+    points = []
+    blocked = None
+    try:
+        for outer, inner in splits:
+            if blocked is None and len(splits) > 1:
+                blocked = BlockedDataset(d, make_grid(d.n, d.m, cfg.grid_i, cfg.grid_j), options)
+            run_cfg = replace(cfg, outer_steps=outer, inner_schedule=Constant(inner))
+            t0 = time.perf_counter()
+            result = train_blocked(d, run_cfg, early_stop=False, timing=timing, options=options,
+                                   blocked=blocked)
+            seconds = time.perf_counter() - t0 if timing else 0.0
+            points.append(SweepPoint(outer=outer, inner=inner,
+                                     final_rmse=rmse(result.model, d), seconds=seconds))
+    finally:
+        if blocked is not None:
+            blocked.engine.close()
+    return points

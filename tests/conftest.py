@@ -47,6 +47,11 @@ def partition_cases():
 
 
 @pytest.fixture(scope="session")
+def baseline_cases():
+    return np.load(os.path.join(GOLDEN, "baseline_cases.npz"))
+
+
+@pytest.fixture(scope="session")
 def train_cases():
     return np.load(os.path.join(GOLDEN, "train_cases.npz"))
 

@@ -212,6 +212,92 @@ def traces():
     return meta
 
 
+def baseline_cases():
+    """Verification kernels and the baseline trainers:
+    _kernels.gradient_steps (_kernels.py:103-140), kernel.block_objective /
+    block_gradients (kernel.py:161-179), baselines.train_sequential (CMF) and
+    train_sync_parallel (CPMF) (baselines.py:62-182)."""
+    rng = np.random.default_rng(2025)
+    out = {}
+    meta = {"n_grad": 12, "n_obj": 6, "traces": {}}
+    for t in range(12):
+        h = int(rng.integers(1, 20))
+        w = int(rng.integers(1, 20))
+        k = int(rng.choice([1, 2, 3, 4, 5, 8, 13, 30, 32, 64]))
+        cnt = int(rng.integers(0, h * w + 1))
+        cells = np.sort(rng.choice(h * w, size=cnt, replace=False))
+        rows, cols = cells // w, cells % w
+        vals = rng.integers(1, 6, cnt).astype(np.float64)
+        u = rng.random((h, k)) / np.sqrt(k)
+        v = rng.random((w, k)) / np.sqrt(k)
+        alpha = float(rng.choice([1e-4, 1e-3, 1e-2, 5e-2]))
+        beta = float(rng.choice([0.0, 1e-2, 0.1, 0.5]))
+        iters = int(rng.integers(1, 5))
+        u1, v1 = u.copy(), v.copy()
+        sb, sa, be, bi = _kernels.gradient_steps(rows, cols, vals, u1, v1, alpha, beta, iters)
+        p = f"g{t}_"
+        out.update({p + "rows": rows, p + "cols": cols, p + "vals": vals, p + "u": u, p + "v": v,
+                    p + "params": np.array([alpha, beta, iters]), p + "u_after": u1,
+                    p + "v_after": v1, p + "out": np.array([sb, sa, be, bi], np.float64)})
+    d32 = dense(32)
+    blk = bm.partition(d32, 1, 1).block(0, 0)
+    model = bm.init_factors(32, 32, 4, seed=0)
+    u, v = model.u.copy(), model.v.copy()
+    out["gdiv_out"] = np.array(_kernels.gradient_steps(blk.rows, blk.cols, blk.values, u, v,
+                                                       1e6, 0.0, 50), np.float64)
+    for t in range(6):
+        k = int(rng.integers(1, 6))
+        nr, nc = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        count = int(rng.integers(1, nr * nc + 1))
+        cells = rng.choice(nr * nc, size=count, replace=False)
+        task = bm.BlockTask(bi=0, bj=0, rows=cells // nc, cols=cells % nc,
+                            values=rng.uniform(1.0, 5.0, count),
+                            u_slice=rng.uniform(0.1, 1.0, (nr, k)),
+                            v_slice=rng.uniform(0.1, 1.0, (nc, k)), alpha=1e-3,
+                            beta=float(rng.uniform(0.0, 0.5)), inner_iters=1)
+        gu, gv = bm.block_gradients(task)
+        p = f"o{t}_"
+        out.update({p + "rows": task.rows, p + "cols": task.cols, p + "vals": task.values,
+                    p + "u": task.u_slice, p + "v": task.v_slice, p + "beta": np.array([task.beta]),
+                    p + "obj": np.array([bm.block_objective(task)]), p + "gu": gu, p + "gv": gv})
+
+    def rec(name, fn, d, cfg, test=None, early_stop=False, keep=False):
+        res = fn(d, cfg, test, early_stop=early_stop, timing=False)
+        meta["traces"][name] = dict(
+            train=[s.train_rmse for s in res.trace], test=[s.test_rmse for s in res.trace],
+            inner=[s.inner_iters for s in res.trace], stop=res.stop_reason,
+            u_sha=sha(res.model.u), v_sha=sha(res.model.v),
+            cfg=dict(k=cfg.k, alpha=cfg.alpha, beta=cfg.beta, delta=cfg.delta,
+                     outer_steps=cfg.outer_steps, seed=cfg.seed, workers=cfg.workers,
+                     grid_i=cfg.grid_i, grid_j=cfg.grid_j,
+                     schedule=bm.format_schedule(cfg.inner_schedule)),
+            early_stop=early_stop)
+        if keep:
+            out[name + "_u"] = res.model.u
+            out[name + "_v"] = res.model.v
+
+    d64 = dense(64)
+    base = dict(k=10, alpha=1e-4, beta=1e-2, delta=1e-2, seed=0, outer_steps=6, grid_i=4,
+                grid_j=4)
+    rec("cmf_dense64", bm.train_sequential, d64, bm.TrainConfig(**base), keep=True)
+    rec("cmf_dense64_early", bm.train_sequential, d64,
+        bm.TrainConfig(**dict(base, outer_steps=100)), early_stop=True)
+    for wk in (1, 3, 4, 7):
+        rec(f"cpmf_dense64_w{wk}", bm.train_sync_parallel, d64,
+            bm.TrainConfig(**dict(base, workers=wk)), keep=wk == 3)
+    tr, te = bm.split(d64, 0.2, seed=1)
+    rec("cpmf_dense64_holdout_w4", bm.train_sync_parallel, tr,
+        bm.TrainConfig(**dict(base, workers=4, outer_steps=3)), te)
+    r, c, v = make_ml100k_standin()
+    sd = bm.RatingsDataset(943, 1682, r, c, v)
+    rec("cmf_c1_k30", bm.train_sequential, sd,
+        bm.TrainConfig(k=30, outer_steps=5, grid_i=4, grid_j=4))
+    rec("cpmf_c1_k30_w8", bm.train_sync_parallel, sd,
+        bm.TrainConfig(k=30, outer_steps=5, grid_i=4, grid_j=4, workers=8))
+    np.savez_compressed(os.path.join(OUT, "baseline_cases.npz"), **out)
+    return meta
+
+
 def io_cases():
     """Byte-exact outputs of the reference's writers (data_io.py:193-309)."""
     import io as _io
@@ -238,6 +324,7 @@ def main():
         plans=plans(),
         traces=traces(),
         io=io_cases(),
+        baselines=baseline_cases(),
         hand=dict(
             rmse_hand=bm.rmse(bm.FactorModel(np.array([[1.0], [2.0]]), np.array([[1.0], [2.0]])),
                               bm.RatingsDataset.from_triples(2, 2, [(0, 0, 4.0), (1, 1, 8.0)])),

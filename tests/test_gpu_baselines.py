@@ -1,0 +1,245 @@
+"""SURVEY 8(f) rank 4 on the GPU: the verification kernels
+(_kernels.gradient_steps, kernel.block_objective / block_gradients) and the
+baseline trainers (CMF train_sequential, CPMF train_sync_parallel) against the
+reference's golden vectors (tests/golden/make_golden.py) and the reference's
+own test cases (test_kernel.py:131-190, test_trainer.py:33-41)."""
+
+import numpy as np
+import pytest
+
+import paper_2304_13724_b200 as bm
+from helpers import baseline_config, sha, trace_inputs
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+EXACT = bm.EngineOptions(exact=True)
+TOL = 1e-3
+
+
+def _task(K, p, alpha=1e-3, beta=None, iters=1):
+    return bm.BlockTask(bi=0, bj=0, rows=K[p + "rows"], cols=K[p + "cols"], values=K[p + "vals"],
+                        u_slice=K[p + "u"].copy(), v_slice=K[p + "v"].copy(), alpha=alpha,
+                        beta=float(K[p + "beta"][0]) if beta is None else beta,
+                        inner_iters=iters)
+
+
+@pytest.mark.parametrize("t", range(12))
+def test_batch_gradient_block_bit_exact(baseline_cases, t):
+    K, p = baseline_cases, f"g{t}_"
+    alpha, beta, iters = K[p + "params"]
+    out = K[p + "out"]
+    task = bm.BlockTask(bi=0, bj=0, rows=K[p + "rows"], cols=K[p + "cols"], values=K[p + "vals"],
+                        u_slice=K[p + "u"].copy(), v_slice=K[p + "v"].copy(), alpha=float(alpha),
+                        beta=float(beta), inner_iters=int(iters))
+    st = bm.batch_gradient_block(task)
+    assert np.array_equal(task.u_slice, K[p + "u_after"])
+    assert np.array_equal(task.v_slice, K[p + "v_after"])
+    assert (st.sse_before, st.sse_after) == (out[0], out[1])
+    assert st.entries == len(K[p + "rows"]) and st.iters_used == int(iters)
+
+
+def test_batch_gradient_diverges(dense32, baseline_cases):
+    """test_kernel.py:131-135; location from the reference's gradient_steps."""
+    block = bm.partition(dense32, 1, 1).block(0, 0)
+    model = bm.init_factors(32, 32, 4, seed=0)
+    with pytest.raises(bm.DivergenceError) as ei:
+        bm.batch_gradient_block(bm.task_from_block(block, model, 1e6, 0.0, 50))
+    ref = baseline_cases["gdiv_out"]
+    assert (ei.value.entry, ei.value.iteration) == (int(ref[2]), int(ref[3]))
+    assert "reduce alpha" in str(ei.value)
+
+
+def test_batch_gradient_rejects_converge_mode():
+    t = bm.BlockTask(bi=0, bj=0, rows=np.array([0]), cols=np.array([0]), values=np.array([2.0]),
+                     u_slice=np.ones((1, 1)), v_slice=np.ones((1, 1)), alpha=0.1, beta=0.5,
+                     inner_iters=None, converge_tol=1e-3)
+    with pytest.raises(ValueError, match="converge mode"):
+        bm.batch_gradient_block(t)
+
+
+@pytest.mark.parametrize("t", range(6))
+def test_objective_and_gradients_match_reference(baseline_cases, t):
+    K, p = baseline_cases, f"o{t}_"
+    task = _task(K, p)
+    gu, gv = bm.block_gradients(task)
+    np.testing.assert_allclose(gu, K[p + "gu"], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(gv, K[p + "gv"], rtol=1e-12, atol=1e-14)
+    assert bm.block_objective(task) == pytest.approx(float(K[p + "obj"][0]), rel=1e-12)
+    # pure: the slices are untouched
+    assert np.array_equal(task.u_slice, K[p + "u"]) and np.array_equal(task.v_slice, K[p + "v"])
+
+
+def test_objective_hand_computed():
+    """test_kernel.py:139-142: residual 1, regularizer (beta/2)(1 + 1) = 2."""
+    t = bm.BlockTask(bi=0, bj=0, rows=np.array([0]), cols=np.array([0]), values=np.array([2.0]),
+                     u_slice=np.ones((1, 1)), v_slice=np.ones((1, 1)), alpha=0.1, beta=2.0)
+    assert bm.block_objective(t) == 3.0
+
+
+def test_gradients_match_finite_differences():
+    """test_kernel.py:144-177."""
+    rng = np.random.default_rng(11)
+    h = 1e-6
+    worst = 0.0
+    for _ in range(10):
+        k = int(rng.integers(1, 4))
+        nr, nc = 6, 6
+        count = int(rng.integers(1, nr * nc + 1))
+        cells = rng.choice(nr * nc, size=count, replace=False)
+        task = bm.BlockTask(bi=0, bj=0, rows=cells // nc, cols=cells % nc,
+                            values=rng.uniform(1.0, 5.0, count),
+                            u_slice=rng.uniform(0.1, 1.0, (nr, k)),
+                            v_slice=rng.uniform(0.1, 1.0, (nc, k)), alpha=1e-3,
+                            beta=float(rng.uniform(0.0, 0.5)), inner_iters=1)
+        gu, gv = bm.block_gradients(task)
+        for mat, grad in ((task.u_slice, gu), (task.v_slice, gv)):
+            fd = np.empty_like(grad)
+            for idx in np.ndindex(mat.shape):
+                orig = mat[idx]
+                mat[idx] = orig + h
+                hi = bm.block_objective(task)
+                mat[idx] = orig - h
+                lo = bm.block_objective(task)
+                mat[idx] = orig
+                fd[idx] = (hi - lo) / (2 * h)
+            worst = max(worst, float(np.max(np.abs(grad - fd) / np.maximum(np.abs(fd), 1.0))))
+    assert worst < 1e-4
+
+
+def test_batch_gradient_step_matches_analytic_gradients(dense32):
+    """test_kernel.py:179-190."""
+    block = bm.partition(dense32, 2, 2).block(0, 1)
+    model = bm.init_factors(32, 32, 3, seed=1)
+    task = bm.task_from_block(block, model, 1e-3, 1e-2, 1)
+    u0, v0 = task.u_slice.copy(), task.v_slice.copy()
+    gu, gv = bm.block_gradients(task)
+    bm.batch_gradient_block(task)
+    assert task.u_slice == pytest.approx(u0 - 1e-3 * gu, rel=1e-12)
+    assert task.v_slice == pytest.approx(v0 - 1e-3 * gv, rel=1e-12)
+
+
+CPMF = ["cpmf_dense64_w1", "cpmf_dense64_w3", "cpmf_dense64_w4", "cpmf_dense64_w7",
+        "cpmf_dense64_holdout_w4", "cpmf_c1_k30_w8"]
+CMF = ["cmf_dense64", "cmf_dense64_early", "cmf_c1_k30"]
+
+
+def _run(fn, name, golden, options=None):
+    meta = golden["baselines"]["traces"][name]
+    d, te = trace_inputs(name)
+    res = fn(d, baseline_config(meta), te, early_stop=meta["early_stop"], timing=False,
+             options=options)
+    return meta, d, te, res
+
+
+@pytest.mark.parametrize("name", CPMF)
+def test_sync_parallel_exact_bit_identical(golden, name):
+    meta, d, te, res = _run(bm.train_sync_parallel, name, golden, EXACT)
+    assert [s.train_rmse for s in res.trace] == meta["train"]
+    assert [s.inner_iters for s in res.trace] == meta["inner"]
+    assert res.stop_reason == meta["stop"]
+    assert sha(res.model.u) == meta["u_sha"] and sha(res.model.v) == meta["v_sha"]
+    if te is not None:
+        for a, b in zip([s.test_rmse for s in res.trace], meta["test"]):
+            assert a == pytest.approx(b, rel=1e-12)
+
+
+# Fast mode (fp32, each shard chunked over worker groups: lossless Hogwild
+# inside a shard) is held to the 1e-3 tolerance on the MovieLens-shaped data
+# the tolerance is stated for.  On the fully dense toy fixtures (64x64, values
+# 1..30, RMSE 8-17) concurrent groups sweep the same columns and the drift is
+# ~1e-3 relative (0.004-0.015 absolute): those are checked bit-for-bit in exact
+# mode above and bounded loosely here.
+FAST_REAL = ["cpmf_c1_k30_w8"]
+FAST_TOY = [n for n in CPMF if n not in FAST_REAL]
+
+
+@pytest.mark.parametrize("name", FAST_TOY)
+def test_sync_parallel_fast_dense_toy_bounded(golden, name):
+    meta, d, te, res = _run(bm.train_sync_parallel, name, golden)
+    got = np.array([s.train_rmse for s in res.trace])
+    ref = np.array(meta["train"])
+    assert len(got) == len(ref)
+    assert np.max(np.abs(got - ref) / ref) <= 3e-3
+
+
+@pytest.mark.parametrize("workers", [1, 4, 16])
+def test_sync_parallel_fast_c2_shape_within_tolerance(workers):
+    """C2-shaped data (6040 x 3706, 1M ratings, k=32) against the oracle's
+    restatement of train_sync_parallel (pinned to the reference in
+    test_oracle.py), 3 steps."""
+    from paper_2304_13724_b200 import workloads
+
+    w = workloads.CONFIGS["C2"]
+    r, c, v = workloads.lowrank(w.n, w.m, w.nnz, seed=w.seed)
+    d = bm.RatingsDataset(w.n, w.m, r, c, v)
+    cfg = bm.TrainConfig(k=w.k, alpha=w.alpha, beta=w.beta, outer_steps=3, workers=workers)
+    res = bm.train_sync_parallel(d, cfg, early_stop=False, timing=False)
+    _, _, tr, _ = O.train_sync_parallel(w.n, w.m, r, c, v, k=w.k, alpha=w.alpha, beta=w.beta,
+                                        outer_steps=3, workers=workers, early_stop=False)
+    got = np.array([s.train_rmse for s in res.trace])
+    ref = np.array([s["train_rmse"] for s in tr])
+    assert np.max(np.abs(got - ref)) <= TOL
+
+
+@pytest.mark.parametrize("name", FAST_REAL)
+def test_sync_parallel_fast_within_tolerance(golden, name):
+    meta, d, te, res = _run(bm.train_sync_parallel, name, golden)
+    got = np.array([s.train_rmse for s in res.trace])
+    assert len(got) == len(meta["train"])
+    assert np.max(np.abs(got - np.array(meta["train"]))) <= TOL
+    if te is not None:
+        got_t = np.array([s.test_rmse for s in res.trace])
+        assert np.max(np.abs(got_t - np.array(meta["test"]))) <= TOL
+
+
+def test_sync_parallel_keeps_cpmf_semantics(golden):
+    """The V merge changes with the shard count (baselines.py:115-117): the
+    trajectories for 3 and 4 shards differ, and each matches its own golden."""
+    a = golden["baselines"]["traces"]["cpmf_dense64_w3"]["train"]
+    b = golden["baselines"]["traces"]["cpmf_dense64_w4"]["train"]
+    assert a != b
+
+
+@pytest.mark.parametrize("name", CMF)
+def test_sequential_exact_bit_identical(golden, name):
+    meta, d, te, res = _run(bm.train_sequential, name, golden, EXACT)
+    assert [s.train_rmse for s in res.trace] == meta["train"]
+    assert res.stop_reason == meta["stop"]
+    assert sha(res.model.u) == meta["u_sha"] and sha(res.model.v) == meta["v_sha"]
+
+
+@pytest.mark.parametrize("name", CMF)
+def test_sequential_fast_within_tolerance(golden, name):
+    meta, d, te, res = _run(bm.train_sequential, name, golden)
+    got = np.array([s.train_rmse for s in res.trace])
+    ref = np.array(meta["train"])
+    assert len(got) == len(ref)
+    if name.startswith("cmf_c1"):
+        assert np.max(np.abs(got - ref)) <= TOL
+    else:  # dense toy: see FAST_TOY above
+        assert np.max(np.abs(got - ref) / ref) <= 3e-3
+
+
+def test_sync_parallel_divergence_reports_shard(dense64):
+    cfg = bm.TrainConfig(k=4, alpha=1e6, beta=0.0, outer_steps=3, workers=3)
+    for opts in (EXACT, None):
+        with pytest.raises(bm.DivergenceError) as ei:
+            bm.train_sync_parallel(dense64, cfg, options=opts)
+        assert str(ei.value).startswith("shard 0:") and ei.value.step == 1
+
+
+def test_sweep_budget_matches_oracle(dense64):
+    cfg = bm.TrainConfig(k=6, alpha=1e-3, grid_i=2, grid_j=2, outer_steps=1)
+    splits = bm.auto_splits(6)
+    assert splits == [(1, 6), (2, 3), (3, 2), (6, 1)]
+    pts = bm.sweep_budget(dense64, cfg, 6, splits, timing=False, options=EXACT)
+    for pt in pts:
+        u, v, _, _ = O.train_blocked(dense64.n, dense64.m, dense64.rows, dense64.cols,
+                                     dense64.values, k=6, alpha=1e-3, outer_steps=pt.outer,
+                                     schedule=f"const:{pt.inner}", grid_i=2, grid_j=2,
+                                     early_stop=False)
+        want = O.rmse(u, v, dense64.rows, dense64.cols, dense64.values)
+        assert pt.final_rmse == pytest.approx(want, rel=1e-12)
+    with pytest.raises(ValueError, match="does not factor"):
+        bm.sweep_budget(dense64, cfg, 6, [(4, 2)])

@@ -131,3 +131,73 @@ def test_hand_values(golden):
     assert O.split_bounds(10, 3).tolist() == h["split_bounds_10_3"]
     u = np.array([[1.0], [2.0]])
     assert O.rmse(u, u, np.array([0, 1]), np.array([0, 1]), np.array([4.0, 8.0])) == h["rmse_hand"]
+
+
+# ---- verification kernels and baseline trainers ------
+
+@pytest.mark.parametrize("t", range(12))
+def test_gradient_steps_bit_exact(baseline_cases, t):
+    K, p = baseline_cases, f"g{t}_"
+    alpha, beta, iters = K[p + "params"]
+    u, v = K[p + "u"].copy(), K[p + "v"].copy()
+    out = O.gradient_steps(K[p + "rows"], K[p + "cols"], K[p + "vals"], u, v, alpha, beta,
+                           int(iters))
+    assert np.array_equal(u, K[p + "u_after"]) and np.array_equal(v, K[p + "v_after"])
+    assert np.array_equal(np.array(out, float), K[p + "out"], equal_nan=True)
+
+
+def test_gradient_steps_divergence(baseline_cases, dense32):
+    P = O.partition(dense32.rows, dense32.cols, dense32.values, 32, 32, 1, 1)
+    u, v = O.init_factors(32, 32, 4, 0)
+    out = O.gradient_steps(P["rows"], P["cols"], P["values"], u, v, 1e6, 0.0, 50)
+    ref = baseline_cases["gdiv_out"]
+    assert out[0] == ref[0] and np.isnan(out[1]) and (out[2], out[3]) == (ref[2], ref[3])
+
+
+@pytest.mark.parametrize("t", range(6))
+def test_block_gradients_restatement(baseline_cases, t):
+    K, p = baseline_cases, f"o{t}_"
+    obj, gu, gv = O.block_gradients(K[p + "rows"], K[p + "cols"], K[p + "vals"], K[p + "u"],
+                                    K[p + "v"], float(K[p + "beta"][0]))
+    assert obj == K[p + "obj"][0]
+    assert np.array_equal(gu, K[p + "gu"]) and np.array_equal(gv, K[p + "gv"])
+
+
+@pytest.mark.parametrize("name", ["cpmf_dense64_w1", "cpmf_dense64_w3", "cpmf_dense64_w4",
+                                  "cpmf_dense64_w7", "cpmf_dense64_holdout_w4",
+                                  "cpmf_c1_k30_w8"])
+def test_sync_parallel_bit_exact(golden, name):
+    from helpers import trace_inputs
+
+    meta = golden["baselines"]["traces"][name]
+    c = meta["cfg"]
+    d, te = trace_inputs(name)
+    test = None if te is None else (te.rows, te.cols, te.values)
+    u, v, tr, stop = O.train_sync_parallel(d.n, d.m, d.rows, d.cols, d.values, k=c["k"],
+                                           alpha=c["alpha"], beta=c["beta"], delta=c["delta"],
+                                           outer_steps=c["outer_steps"], seed=c["seed"],
+                                           workers=c["workers"], test=test,
+                                           early_stop=meta["early_stop"])
+    assert [s["train_rmse"] for s in tr] == meta["train"]
+    assert stop == meta["stop"]
+    assert sha(u) == meta["u_sha"] and sha(v) == meta["v_sha"]
+    if te is not None:
+        for a, b in zip([s["test_rmse"] for s in tr], meta["test"]):
+            assert a == pytest.approx(b, rel=1e-12)
+
+
+@pytest.mark.parametrize("name", ["cmf_dense64", "cmf_dense64_early", "cmf_c1_k30"])
+def test_sequential_is_blocked_1x1(golden, name):
+    """baselines.py:62-97: CMF == train_blocked on a 1x1 grid, Constant(1)."""
+    from helpers import trace_inputs
+
+    meta = golden["baselines"]["traces"][name]
+    c = meta["cfg"]
+    d, _ = trace_inputs(name)
+    u, v, tr, stop = O.train_blocked(d.n, d.m, d.rows, d.cols, d.values, k=c["k"],
+                                     alpha=c["alpha"], beta=c["beta"], delta=c["delta"],
+                                     outer_steps=c["outer_steps"], seed=c["seed"],
+                                     early_stop=meta["early_stop"])
+    assert [s["train_rmse"] for s in tr] == meta["train"]
+    assert stop == meta["stop"]
+    assert sha(u) == meta["u_sha"] and sha(v) == meta["v_sha"]
