@@ -51,6 +51,11 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      0 = fp32 warp-per-rating lossless kernels (default).
  *   "min_chunk"  int   minimum ratings per worker group in fast mode
  *                      (bounds per-block concurrency on small blocks; 256).
+ *   "sparse_min_chunk" int  floor of the per-group chunk on sparse blocks
+ *                      (density <= 1/8), where concurrency per block is
+ *                      instead capped at "col_ratio" (0.6) x block columns
+ *                      (default 32; 0 = always min_chunk).
+ *   "col_ratio"  float see sparse_min_chunk.
  *   "stagger"    0/1/2 chunk-length rule in fast mode: 2 (default) rounds the
  *                      chunk up to 8*q with q odd so concurrent groups start
  *                      at staggered columns on dense rows (no lockstep V

@@ -731,6 +731,32 @@ struct BatchRange {
   int w0, nw, chunks;
 };
 
+// Per-block chunk length of the fast paths.  cl = the batch's one-wave
+// length (ceil(batch nnz / free groups)); the floor bounds how many groups
+// sweep one block at once (lossless Hogwild: reads of a V row are stale by the
+// other groups' in-flight updates to it):
+//   * sparse blocks (density <= 1/8): at most col_ratio * cols groups, i.e.
+//     about one concurrent update per two V rows, floor sparse_min_chunk --
+//     C1/C2-sized blocks get 8x/4.5x the groups min_chunk allowed (C4 and
+//     C3 are unchanged: their one-wave length is already above the floor);
+//   * dense blocks: the conservative min_chunk floor (dense rows share their
+//     column order, so concurrent groups collide far more often).
+// Then stagger_chunk.
+int64_t block_chunk(bgmf_ctx* c, int b, int64_t cnt, int64_t cl) {
+  const int bi = b / c->J, bj = b % c->J;
+  const int64_t rows = c->row_bounds[bi + 1] - c->row_bounds[bi];
+  const int64_t cols = c->col_bounds[bj + 1] - c->col_bounds[bj];
+  int64_t floor_len = c->min_chunk;
+  if (c->sparse_min_chunk > 0 && cnt * 8 <= rows * cols) {
+    const double cap = c->col_ratio * (double)cols;  // max concurrent groups
+    floor_len = (int64_t)std::ceil((double)cnt / (cap > 1.0 ? cap : 1.0));
+    if (floor_len < c->sparse_min_chunk) floor_len = c->sparse_min_chunk;
+  }
+  int64_t bl = cl > floor_len ? cl : floor_len;
+  bl = stagger_chunk(bl, c->stagger);
+  return bl < cnt ? bl : cnt;
+}
+
 // Chunking: each batch's ratings are cut into equal chunks, at most `groups`
 // of them (groups = worker groups resident in one wave; 0 = one chunk per
 // block, the exact path).  chunk = ceil(batch_nnz / (groups - B)) so the
@@ -758,8 +784,6 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
     if (groups > 0) {
       const int64_t slots = groups - nonempty > 0 ? groups - nonempty : 1;
       cl = (batch_nnz + slots - 1) / slots;
-      if (cl < c->min_chunk) cl = c->min_chunk;
-      cl = stagger_chunk(cl, c->stagger);
     }
     ranges[t].w0 = w;
     int chunks = 0;
@@ -769,7 +793,7 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
       const int64_t beg = c->h_offsets[b], end = c->h_offsets[b + 1];
       const int64_t cnt = end - beg;
       if (cnt == 0) continue;
-      const int64_t bl = cl < cnt ? cl : cnt;
+      const int64_t bl = groups > 0 ? block_chunk(c, b, cnt, cl) : cnt;
       BlockWork& bw = c->h_work[w++];
       bw.begin = beg;
       bw.end = end;
