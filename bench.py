@@ -190,7 +190,7 @@ def run_ours(args):
     if world > 1 or os.environ.get("BGMF_FORCE_DIST"):
         from paper_2304_13724_b200 import distributed as D
 
-        return D.bench_main(args)
+        return D.bench_main(args, ClockSampler)
     torch.cuda.set_device(local)
     dev = torch.cuda.current_device()
     if args.config == "C5":

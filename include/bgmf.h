@@ -87,6 +87,15 @@ int bgmf_partition(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                    const double* vals, int64_t nnz, int64_t n, int64_t m,
                    int grid_i, int grid_j);
 
+/* bgmf_partition of the entries whose row lies in [row_lo, row_hi) only (the
+ * rest are range-checked and dropped while the host threads narrow the
+ * upload): a multi-GPU rank's U-row shard, without a host-side gather.  The
+ * grid is still the full n x m one; exported `order` indices refer to the
+ * kept entries in input order. */
+int bgmf_partition_rows(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
+                        const double* vals, int64_t nnz, int64_t n, int64_t m,
+                        int grid_i, int grid_j, int64_t row_lo, int64_t row_hi);
+
 /* Benchmark / test inputs (not part of the reference path): generate the
  * synthetic low-rank workload of paper_2304_13724_b200/workloads.py
  * (Feistel-sampled cells -- identical integers to workloads.feistel_cells --
@@ -171,6 +180,19 @@ int bgmf_holdout_sse(bgmf_ctx* ctx, double* sse_out);
 int bgmf_stream_ratings(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
 /* Rating bytes streamed host->device since the context was created. */
 int bgmf_stream_stats(bgmf_ctx* ctx, double* h2d_bytes);
+
+/* Asynchronous outer step (fast mode), for callers that interleave their own
+ * work between strata -- the multi-GPU ring trainer moves V blocks with NCCL
+ * on the same stream between batches (trainer.py:138-152 barrier analog).
+ * step_begin reserves work-table slots for up to max_blocks block launches
+ * and zeroes the per-block SSEs; each step_batch enqueues its strata (same
+ * arguments as bgmf_run_step) without a host sync; step_end synchronises and
+ * returns sse_out[I*J] (blocks not run: 0) and bad_out = {block id, entry,
+ * iteration} of the first diverged block in submission order, or -1s. */
+int bgmf_step_begin(bgmf_ctx* ctx, int max_blocks);
+int bgmf_step_batch(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
+                    int nbatch, int inner_iters, double alpha, double beta);
+int bgmf_step_end(bgmf_ctx* ctx, double* sse_out, int64_t* bad_out);
 
 /* One outer step of the synchronized row-sharded baseline trainer (CPMF,
  * baselines.py:100-182, `train_sync_parallel`) on a context partitioned 1 x 1

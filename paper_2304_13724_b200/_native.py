@@ -51,6 +51,10 @@ SIGNATURES = {
                                ctypes.c_uint64, _l, _l, _i]),
     "bgmf_bind_factors": (_i, [_ctx, _vp, _vp, _l, _l, _i, _i]),
     "bgmf_run_step": (_i, [_ctx, _i32p, _i32p, _i, _i, _d, _d, _f64p, _i64p]),
+    "bgmf_partition_rows": (_i, [_ctx, _i64p, _i64p, _f64p, _l, _l, _l, _i, _i, _l, _l]),
+    "bgmf_step_begin": (_i, [_ctx, _i]),
+    "bgmf_step_batch": (_i, [_ctx, _i32p, _i32p, _i, _i, _d, _d]),
+    "bgmf_step_end": (_i, [_ctx, _f64p, _i64p]),
     "bgmf_run_sync_parallel_step": (_i, [_ctx, _i64p, _i, _d, _d, _f64p, _i64p]),
     "bgmf_run_step_converge": (_i, [_ctx, _i32p, _i32p, _i, _d, _l, _d, _d, _f64p, _i64p,
                                     _i32p, _i64p]),

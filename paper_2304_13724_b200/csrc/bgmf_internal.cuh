@@ -93,6 +93,9 @@ struct bgmf_ctx {
   size_t priv_bytes = 0;
   bgmf::BlockWork* h_work = nullptr;     // pinned
   size_t work_cap = 0;
+  bool in_step = false;                  // between bgmf_step_begin / _end
+  int w_cursor = 0;                      // next free work-table slot of the step
+  std::vector<int32_t> submitted;        // block id of every step-global plan position
   double* h_sse = nullptr;               // pinned [I*J]
   unsigned long long* h_bad = nullptr;   // pinned [1]
 
@@ -188,12 +191,13 @@ void prof_mark(bgmf_ctx* ctx, const char* what);
 // partition.cu
 int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                      const double* vals, int64_t nnz, int64_t n, int64_t m, int I, int J,
-                     bool dev_in = false);
+                     bool dev_in = false, int64_t row_lo = 0, int64_t row_hi = -1);
 
 // hostio.cu -- host <-> device through the process-wide pinned staging pool
 int64_t staged_upload(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                       const double* vals, int64_t nnz, int64_t n, int64_t m, int32_t* d_r,
-                      int32_t* d_c, void* d_v, bool v64, int* rc);
+                      int32_t* d_c, void* d_v, bool v64, int* rc, int64_t row_lo,
+                      int64_t row_hi, int64_t* kept);
 int download_rows(bgmf_ctx* c, const float* d, double* h, int64_t rows, int k, int kp);
 int upload_rows(bgmf_ctx* c, const double* h, float* d, int64_t rows, int k, int kp);
 
@@ -206,6 +210,10 @@ int run_step_fast(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
                   int nbatch, int iters, float alpha, float beta);
 int run_step_exact(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
                    int nbatch, int iters, double alpha, double beta);
+int step_begin(bgmf_ctx* c, int max_blocks);
+int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch, int iters,
+               float alpha, float beta);
+int step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out);
 int run_sync_parallel_step(bgmf_ctx* c, const int64_t* edges, int nshards, double alpha,
                            double beta, double* sse_out, int64_t* bad_out);
 int run_step_converge_exact(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,

@@ -221,6 +221,17 @@ int bgmf_partition(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const 
   return partition_device(c, rows, cols, vals, nnz, n, m, grid_i, grid_j);
 }
 
+int bgmf_partition_rows(bgmf_ctx* c, const int64_t* rows, const int64_t* cols,
+                        const double* vals, int64_t nnz, int64_t n, int64_t m, int grid_i,
+                        int grid_j, int64_t row_lo, int64_t row_hi) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  cudaSetDevice(c->device);
+  if (c->streaming) stream_free(c);
+  dfree(c->d_sse, c->stream); cudaFreeHost(c->h_sse); dfree(c->d_bad, c->stream); cudaFreeHost(c->h_bad);
+  c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
+  return partition_device(c, rows, cols, vals, nnz, n, m, grid_i, grid_j, false, row_lo, row_hi);
+}
+
 int bgmf_synth_partition(bgmf_ctx* c, int64_t n, int64_t m, int64_t nnz, uint64_t seed,
                          int grid_i, int grid_j) {
   if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
@@ -402,6 +413,32 @@ int bgmf_run_step(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, in
   for (int b = 0; b < nb; ++b) sse_out[b] = c->h_sse[b];
   fill_bad(c, bad_out);
   return BGMF_OK;
+}
+
+int bgmf_step_begin(bgmf_ctx* c, int max_blocks) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  int rc = check_step_ready(c);
+  if (rc) return rc;
+  cudaSetDevice(c->device);
+  return step_begin(c, max_blocks);
+}
+
+int bgmf_step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
+                    int inner_iters, double alpha, double beta) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (!plan || !batch_off || nbatch < 0) return fail(c, BGMF_ERR_ARG, "NULL argument");
+  if (inner_iters < 1 || inner_iters > 65535) return fail(c, BGMF_ERR_ARG, "inner_iters out of range");
+  for (int q = 0; q < batch_off[nbatch]; ++q)
+    if (plan[q] < 0 || plan[q] >= c->I * c->J) return fail(c, BGMF_ERR_ARG, "plan block id out of range");
+  cudaSetDevice(c->device);
+  return step_batch(c, plan, batch_off, nbatch, inner_iters, (float)alpha, (float)beta);
+}
+
+int bgmf_step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (!sse_out || !bad_out) return fail(c, BGMF_ERR_ARG, "NULL argument");
+  cudaSetDevice(c->device);
+  return step_end(c, sse_out, bad_out);
 }
 
 int bgmf_run_sync_parallel_step(bgmf_ctx* c, const int64_t* shard_edges, int nshards,

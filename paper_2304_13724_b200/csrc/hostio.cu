@@ -17,6 +17,7 @@
 #include <omp.h>
 
 #include <mutex>
+#include <vector>
 
 #include "bgmf_internal.cuh"
 
@@ -66,19 +67,27 @@ class Stage {
 // Dataset upload for the partitioner (partition.cu): int64 indices narrowed
 // to int32 (and range-checked against n x m), fp64 values narrowed to fp32
 // unless v64 (exact mode keeps them).  12 (16) instead of 24 B per rating
-// cross PCIe.  Returns the first entry whose index is outside n x m, or -1.
+// cross PCIe.  Only entries with row in [row_lo, row_hi) are kept (compacted
+// in input order; every entry is still range-checked) -- a multi-GPU rank
+// uploads just its row shard without a host-side gather.  *kept = entries
+// uploaded.  Returns the first entry whose index is outside n x m, or -1.
 int64_t staged_upload(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                       const double* vals, int64_t nnz, int64_t n, int64_t m, int32_t* d_r,
-                      int32_t* d_c, void* d_v, bool v64, int* rc) {
+                      int32_t* d_c, void* d_v, bool v64, int* rc, int64_t row_lo,
+                      int64_t row_hi, int64_t* kept) {
   *rc = BGMF_OK;
+  *kept = 0;
   Stage st(ctx);
   if (st.error()) {
     *rc = cuda_fail(ctx, st.error(), "staging pool");
     return -1;
   }
+  const bool filter = row_lo > 0 || row_hi < n;
   const size_t vb = v64 ? 8 : 4;
   const int64_t chunk = (int64_t)(kStageBytes / (8 + vb));
-  int64_t first_bad = INT64_MAX;
+  const int nt = omp_get_max_threads();
+  std::vector<int64_t> tcount((size_t)nt + 1);
+  int64_t first_bad = INT64_MAX, out = 0;
   int k = 0;
   for (int64_t i0 = 0; i0 < nnz; i0 += chunk, ++k) {
     const int b = k & 1;
@@ -87,25 +96,64 @@ int64_t staged_upload(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
     int32_t* sr = reinterpret_cast<int32_t*>(st.buf(b));
     int32_t* sc = sr + chunk;
     char* sv = reinterpret_cast<char*>(sc + chunk);
-    int64_t bad = INT64_MAX;
+    int64_t bad = INT64_MAX, nkeep = cnt;
+    if (!filter) {
 #pragma omp parallel for schedule(static) reduction(min : bad)
-    for (int64_t i = 0; i < cnt; ++i) {
-      const int64_t r = rows[i0 + i], c = cols[i0 + i];
-      if (r < 0 || r >= n || c < 0 || c >= m) bad = i0 + i < bad ? i0 + i : bad;
-      sr[i] = (int32_t)r;
-      sc[i] = (int32_t)c;
-      if (v64) reinterpret_cast<double*>(sv)[i] = vals[i0 + i];
-      else reinterpret_cast<float*>(sv)[i] = (float)vals[i0 + i];
+      for (int64_t i = 0; i < cnt; ++i) {
+        const int64_t r = rows[i0 + i], c = cols[i0 + i];
+        if (r < 0 || r >= n || c < 0 || c >= m) bad = i0 + i < bad ? i0 + i : bad;
+        sr[i] = (int32_t)r;
+        sc[i] = (int32_t)c;
+        if (v64) reinterpret_cast<double*>(sv)[i] = vals[i0 + i];
+        else reinterpret_cast<float*>(sv)[i] = (float)vals[i0 + i];
+      }
+    } else {
+      // pass 1: per-thread counts (static ranges); pass 2: ordered compaction
+      int team = 1;
+#pragma omp parallel reduction(min : bad)
+      {
+        const int t = omp_get_thread_num(), T = omp_get_num_threads();
+        const int64_t lo = cnt * t / T, hi = cnt * (t + 1) / T;
+        int64_t my = 0;
+        for (int64_t i = lo; i < hi; ++i) {
+          const int64_t r = rows[i0 + i], c = cols[i0 + i];
+          if (r < 0 || r >= n || c < 0 || c >= m) bad = i0 + i < bad ? i0 + i : bad;
+          my += r >= row_lo && r < row_hi;
+        }
+        tcount[t + 1] = my;
+#pragma omp barrier
+#pragma omp single
+        {
+          team = T;
+          tcount[0] = 0;
+          for (int q = 0; q < T; ++q) tcount[q + 1] += tcount[q];
+        }
+        int64_t o = tcount[t];
+        for (int64_t i = lo; i < hi; ++i) {
+          const int64_t r = rows[i0 + i];
+          if (r < row_lo || r >= row_hi) continue;
+          sr[o] = (int32_t)r;
+          sc[o] = (int32_t)cols[i0 + i];
+          if (v64) reinterpret_cast<double*>(sv)[o] = vals[i0 + i];
+          else reinterpret_cast<float*>(sv)[o] = (float)vals[i0 + i];
+          ++o;
+        }
+      }
+      nkeep = tcount[team];
     }
     if (bad < first_bad) first_bad = bad;
-    cudaMemcpyAsync(d_r + i0, sr, cnt * 4, cudaMemcpyHostToDevice, ctx->stream);
-    cudaMemcpyAsync(d_c + i0, sc, cnt * 4, cudaMemcpyHostToDevice, ctx->stream);
-    cudaMemcpyAsync(static_cast<char*>(d_v) + i0 * vb, sv, cnt * vb, cudaMemcpyHostToDevice,
-                    ctx->stream);
+    if (nkeep > 0) {
+      cudaMemcpyAsync(d_r + out, sr, nkeep * 4, cudaMemcpyHostToDevice, ctx->stream);
+      cudaMemcpyAsync(d_c + out, sc, nkeep * 4, cudaMemcpyHostToDevice, ctx->stream);
+      cudaMemcpyAsync(static_cast<char*>(d_v) + out * vb, sv, nkeep * vb,
+                      cudaMemcpyHostToDevice, ctx->stream);
+    }
     cudaEventRecord(st.done(b), ctx->stream);
+    out += nkeep;
   }
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) *rc = cuda_fail(ctx, e, "staged upload");
+  *kept = out;
   return first_bad == INT64_MAX ? -1 : first_bad;
 }
 

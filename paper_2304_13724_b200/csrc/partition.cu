@@ -259,7 +259,11 @@ void free_dev(T*& p, cudaStream_t s) {
 // call (freed as soon as they are consumed); otherwise host arrays.
 int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                      const double* vals, int64_t nnz, int64_t n, int64_t m, int I, int J,
-                     bool dev_in) {
+                     bool dev_in, int64_t row_lo, int64_t row_hi) {
+  if (row_hi < 0) row_hi = n;
+  if (row_lo < 0 || row_lo > row_hi || row_hi > n)
+    return fail(ctx, BGMF_ERR_ARG, "row range must satisfy 0 <= row_lo <= row_hi <= n");
+  const bool filter = row_lo > 0 || row_hi < n;
   if (n < 1 || m < 1) return fail(ctx, BGMF_ERR_ARG, "n and m must be >= 1");
   if (I < 1 || I > n) return fail(ctx, BGMF_ERR_ARG, "grid_i must be in [1, n]");
   if (J < 1 || J > m) return fail(ctx, BGMF_ERR_ARG, "grid_j must be in [1, m]");
@@ -311,6 +315,8 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   // host input with 32-bit dimensions: narrowed staged upload (int32 indices,
   // fp32 values unless exact mode needs the fp64 ones)
   const bool narrow = !dev_in && n <= INT32_MAX && m <= INT32_MAX;
+  if (filter && !narrow)
+    return fail(ctx, BGMF_ERR_ARG, "row ranges need host input with 32-bit dimensions");
   const bool v32 = narrow && !ctx->exact;
   if (dev_in) {
     d_rows = const_cast<int64_t*>(rows);
@@ -328,10 +334,14 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   int64_t host_bad = -1;
   if (nnz > 0 && narrow) {
     int urc = BGMF_OK;
+    int64_t kept = nnz;
     host_bad = staged_upload(ctx, rows, cols, vals, nnz, n, m,
                              reinterpret_cast<int32_t*>(d_rows),
-                             reinterpret_cast<int32_t*>(d_cols), d_vin, !v32, &urc);
+                             reinterpret_cast<int32_t*>(d_cols), d_vin, !v32, &urc, row_lo,
+                             row_hi, &kept);
     if (urc) { cleanup(); return urc; }
+    if (host_bad < 0) nnz = kept;  // the partition holds only the kept rows
+    ctx->nnz = nnz;
   } else if (nnz > 0 && !dev_in) {
     PCK(cudaMemcpyAsync(d_rows, rows, nnz * 8, cudaMemcpyHostToDevice, s));
     PCK(cudaMemcpyAsync(d_cols, cols, nnz * 8, cudaMemcpyHostToDevice, s));
@@ -376,10 +386,11 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
 
   const int total_bits = rbits + cbits + bbits;
   const int passes = (total_bits + 7) / 8;
+  const size_t NK = (size_t)(nnz > 0 ? nnz : 1);  // kept entries
   const int64_t ntiles = (nnz + RS_TILE - 1) / RS_TILE;
   if (passes > 0 && nnz > 1) {
-    PCK(dmalloc(&kb, N * 8, ctx->stream));
-    PCK(dmalloc(&ib, N * 4, ctx->stream));
+    PCK(dmalloc(&kb, NK * 8, ctx->stream));
+    PCK(dmalloc(&ib, NK * 4, ctx->stream));
     PCK(dmalloc(&hist, (size_t)256 * ntiles * 4, ctx->stream));
     PCK(dmalloc(&tot, 256 * 4, ctx->stream));
     for (int p = 0; p < passes; ++p) {
@@ -396,11 +407,11 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   }
   prof_mark(ctx, "partition: radix sort");
 
-  PCK(dmalloc(&ctx->d_lrow, N * 4, ctx->stream));
-  PCK(dmalloc(&ctx->d_lcol, N * 4, ctx->stream));
-  PCK(dmalloc(&ctx->d_val, N * 4, ctx->stream));
-  PCK(dmalloc(&ctx->d_order, N * 4, ctx->stream));
-  if (ctx->exact) PCK(dmalloc(&ctx->d_val64, N * 8, ctx->stream));
+  PCK(dmalloc(&ctx->d_lrow, NK * 4, ctx->stream));
+  PCK(dmalloc(&ctx->d_lcol, NK * 4, ctx->stream));
+  PCK(dmalloc(&ctx->d_val, NK * 4, ctx->stream));
+  PCK(dmalloc(&ctx->d_order, NK * 4, ctx->stream));
+  if (ctx->exact) PCK(dmalloc(&ctx->d_val64, NK * 8, ctx->stream));
   if (nnz > 0) {
     if (v32)
       decode<float><<<grid, 256, 0, s>>>(ka, ia, reinterpret_cast<const float*>(d_vin), nnz,

@@ -763,12 +763,12 @@ int64_t block_chunk(bgmf_ctx* c, int b, int64_t cnt, int64_t cl) {
 // per-block rounding can never spill into a second wave.
 int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
                int64_t groups, std::vector<BatchRange>& ranges,
-               const std::vector<char>* active = nullptr) {
+               const std::vector<char>* active = nullptr, int w_base = 0, int pos_base = 0) {
   const int total = batch_off[nbatch];
-  int rc = ensure_step_scratch(c, (size_t)total);
+  int rc = ensure_step_scratch(c, (size_t)(w_base + total));
   if (rc) return rc;
   ranges.assign(nbatch, BatchRange{0, 0, 0});
-  int w = 0;
+  int w = w_base;
   for (int t = 0; t < nbatch; ++t) {
     int64_t batch_nnz = 0;
     int nonempty = 0;
@@ -802,7 +802,7 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
       bw.chunk_len = (int32_t)bl;
       bw.first_chunk = chunks;
       bw.block_id = b;
-      bw.pos = q;
+      bw.pos = pos_base + q;
       chunks += (int)((cnt + bl - 1) / bl);
     }
     ranges[t].nw = w - ranges[t].w0;
@@ -958,6 +958,94 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, in
 }
 
 int64_t fast_groups(bgmf_ctx* c) { return sweep_groups(c, shape_for(c->kp)); }
+
+// ---- asynchronous steps (multi-GPU ring): begin, batches, end ----------
+// The distributed trainer interleaves NCCL V-block moves with the strata of a
+// step; each stratum's kernels are enqueued on the engine stream without a
+// host sync, per-block SSEs accumulate in HBM, and step_end reads them once.
+// Work-table slots are reserved for the whole step at begin (no reallocation
+// while copies are in flight); plan positions are step-global so divergence
+// keeps the reference's "first in plan order" rule.
+int step_begin(bgmf_ctx* c, int max_blocks) {
+  if (c->exact) return fail(c, BGMF_ERR_STATE, "asynchronous steps are fast-mode only");
+  if (c->streaming) return fail(c, BGMF_ERR_STATE, "asynchronous steps do not stream");
+  int rc = ensure_step_scratch(c, (size_t)(max_blocks > 0 ? max_blocks : 1));
+  if (rc) return rc;
+  const int nb = c->I * c->J;
+  BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, c->stream));
+  BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, c->stream));
+  c->in_step = true;
+  c->w_cursor = 0;
+  c->submitted.clear();
+  return BGMF_OK;
+}
+
+int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch, int iters,
+               float alpha, float beta) {
+  if (!c->in_step) return fail(c, BGMF_ERR_STATE, "bgmf_step_begin has not been called");
+  const int total = batch_off[nbatch];
+  if ((size_t)(c->w_cursor + total) > c->work_cap)
+    return fail(c, BGMF_ERR_ARG, "more blocks than reserved by bgmf_step_begin");
+  const Shape sh = shape_for(c->kp);
+  const int gpw = 32 / sh.L;
+  std::vector<BatchRange> ranges;
+  const int pos0 = (int)c->submitted.size();
+  int rc = build_work(c, plan, batch_off, nbatch, sweep_groups(c, sh), ranges, nullptr,
+                      c->w_cursor, pos0);
+  if (rc) return rc;
+  const int w_end = ranges.empty() ? c->w_cursor : ranges.back().w0 + ranges.back().nw;
+  if (w_end > c->w_cursor)
+    BGMF_CK(c, cudaMemcpyAsync(c->d_work + c->w_cursor, c->h_work + c->w_cursor,
+                               sizeof(BlockWork) * (w_end - c->w_cursor), cudaMemcpyHostToDevice,
+                               c->stream));
+  for (int q = 0; q < total; ++q) c->submitted.push_back(plan[q]);
+  for (int t = 0; t < nbatch; ++t) {
+    const BatchRange& r = ranges[t];
+    if (r.chunks == 0) continue;
+    const int warps = (r.chunks + gpw - 1) / gpw;
+    const dim3 grid((warps + 7) / 8);
+    double br = 0;
+    for (int q = 0; q < r.nw; ++q)
+      br += (double)(c->h_work[r.w0 + q].end - c->h_work[r.w0 + q].begin);
+    for (int it = 0; it < iters; ++it) {
+      TimedLaunch* slot = nullptr;
+      if (c->timing) record_begin(c, 0, br * (12.0 + 16.0 * c->k), &slot);
+      launch_fast(true, sh, grid, c->stream, c->d_work + r.w0, r.nw, r.chunks, c, alpha, beta,
+                  it);
+      if (slot) record_end(c, slot);
+    }
+    TimedLaunch* slot = nullptr;
+    if (c->timing) record_begin(c, 1, 0.0, &slot);
+    launch_fast(false, sh, grid, c->stream, c->d_work + r.w0, r.nw, r.chunks, c, alpha, beta, 0);
+    if (slot) record_end(c, slot);
+  }
+  BGMF_CK(c, cudaGetLastError());
+  c->w_cursor = w_end;
+  return BGMF_OK;
+}
+
+int step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out) {
+  if (!c->in_step) return fail(c, BGMF_ERR_STATE, "bgmf_step_begin has not been called");
+  c->in_step = false;
+  const int nb = c->I * c->J;
+  BGMF_CK(c, cudaMemcpyAsync(c->h_sse, c->d_sse, sizeof(double) * nb, cudaMemcpyDeviceToHost,
+                             c->stream));
+  BGMF_CK(c, cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, c->stream));
+  BGMF_CK(c, cudaStreamSynchronize(c->stream));
+  if (c->timing) harvest_timing(c);
+  for (int b = 0; b < nb; ++b) sse_out[b] = c->h_sse[b];
+  const unsigned long long bad = *c->h_bad;
+  if (bad == kNoBad) {
+    bad_out[0] = bad_out[1] = bad_out[2] = -1;
+  } else {
+    const int64_t pos = (int64_t)(bad >> 48);
+    bad_out[0] = pos < (int64_t)c->submitted.size() ? c->submitted[pos] : -1;
+    bad_out[1] = (int64_t)(bad & 0xFFFFFFFFull);
+    bad_out[2] = (int64_t)((bad >> 32) & 0xFFFF);
+  }
+  return BGMF_OK;
+}
+
 
 // Sweeps (`iters` launches) + SSE launch for one piece of a batch whose
 // ratings live at (lrow, lcol, val) -- the streaming path's unit of work.

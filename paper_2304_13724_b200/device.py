@@ -117,15 +117,24 @@ class Engine:
 
     # ------------------------------------------------------------ partition
     def partition(self, rows, cols, values, n: int, m: int, grid_i: int, grid_j: int,
-                  data_error=None):
+                  data_error=None, row_range: tuple[int, int] | None = None):
+        """Partition on the device.  ``row_range=(lo, hi)`` keeps only the
+        entries with lo <= row < hi (a multi-GPU rank's shard)."""
         rows, cols, values = N.i64(rows), N.i64(cols), N.f64(values)
-        self._check(self._L.bgmf_partition(
-            self._h, N.ptr(rows, N._i64p), N.ptr(cols, N._i64p), N.ptr(values, N._f64p),
-            len(rows), n, m, grid_i, grid_j), data_error=data_error)
-        self.n, self.m, self.nnz, self.I, self.J = n, m, len(rows), grid_i, grid_j
+        if row_range is None:
+            self._check(self._L.bgmf_partition(
+                self._h, N.ptr(rows, N._i64p), N.ptr(cols, N._i64p), N.ptr(values, N._f64p),
+                len(rows), n, m, grid_i, grid_j), data_error=data_error)
+        else:
+            self._check(self._L.bgmf_partition_rows(
+                self._h, N.ptr(rows, N._i64p), N.ptr(cols, N._i64p), N.ptr(values, N._f64p),
+                len(rows), n, m, grid_i, grid_j, int(row_range[0]), int(row_range[1])),
+                data_error=data_error)
+        self.I, self.J, self.n, self.m = grid_i, grid_j, n, m
         off = np.zeros(grid_i * grid_j + 1, np.int64)
         self._check(self._L.bgmf_partition_export(self._h, N.ptr(off, N._i64p), None, None, None))
         self.offsets = off
+        self.nnz = int(off[-1])
         self.streaming = False
         budget = self.options.device_rating_budget
         if budget is not None and 12 * self.nnz > budget:
@@ -211,6 +220,24 @@ class Engine:
             int(cap), float(alpha), float(beta), N.ptr(sse, N._f64p), N.ptr(iters, N._i64p),
             N.ptr(capped, N._i32p), N.ptr(bad, N._i64p)))
         return sse, iters, capped, (None if bad[0] < 0 else tuple(int(x) for x in bad))
+
+    def step_begin(self, max_blocks: int):
+        """Asynchronous step (fast mode): reserve ``max_blocks`` block launches."""
+        self._check(self._L.bgmf_step_begin(self._h, int(max_blocks)))
+
+    def step_batch(self, ids: np.ndarray, off: np.ndarray, iters: int, alpha: float,
+                   beta: float):
+        """Enqueue strata (same arrays as run_step); no host synchronisation."""
+        self._check(self._L.bgmf_step_batch(self._h, N.ptr(ids, N._i32p), N.ptr(off, N._i32p),
+                                            len(off) - 1, int(iters), float(alpha),
+                                            float(beta)))
+
+    def step_end(self):
+        """(sse[I*J], bad) with bad = (block id, entry, iteration) or None."""
+        sse = np.zeros(self.I * self.J, np.float64)
+        bad = np.zeros(3, np.int64)
+        self._check(self._L.bgmf_step_end(self._h, N.ptr(sse, N._f64p), N.ptr(bad, N._i64p)))
+        return sse, (None if bad[0] < 0 else tuple(int(x) for x in bad))
 
     def run_sync_parallel_step(self, edges: np.ndarray, alpha: float, beta: float):
         """CPMF step on a 1x1 partition; returns (per-shard SSE, bad) where

@@ -108,19 +108,31 @@ def run_epoch(sched: RingSchedule, shard, rank: int, dist, step0: int, g: int,
     needs, then run the batch's blocks whose rows this rank owns.  Returns
     (local per-block SSE [nb], plan order of block ids, first local divergence
     as (block, entry, iter) or None).  ``shard`` provides ``v_slice(j)`` and
-    ``run_batch(blocks, g, alpha, beta) -> (sse[nb], bad, ids)``."""
+    ``run_batch(blocks, g, alpha, beta)``, which either returns
+    ``(sse[nb], bad, ids)`` (synchronous shards) or None when the shard is
+    asynchronous: then ``begin_epoch(max_blocks)`` / ``end_epoch() -> (sse[nb],
+    bad)`` bracket the step and nothing waits on the host between batches
+    (the GPU shard: V moves and strata are ordered on one CUDA stream)."""
     sse_all = np.zeros(nb, np.float64)
     order: list[int] = []
     bad_any = None
+    begin = getattr(shard, "begin_epoch", None)
+    if begin is not None:
+        begin(nb)
     for batch in sched.batches(step0):
         exchange(sched.transfers_for(batch), rank, shard.v_slice, dist)
         order.extend(bi * J + bj for bi, bj in batch)
         mine = sched.local_blocks(batch, rank)
         if mine:
-            sse, bad, ids = shard.run_batch(mine, g, alpha, beta)
-            sse_all[ids] = sse[ids]
-            if bad is not None and bad_any is None:
-                bad_any = (int(ids[bad[0]]), bad[1], bad[2])
+            res = shard.run_batch(mine, g, alpha, beta)
+            if res is not None:
+                sse, bad, ids = res
+                sse_all[ids] = sse[ids]
+                if bad is not None and bad_any is None:
+                    bad_any = (int(ids[bad[0]]), bad[1], bad[2])
+    end = getattr(shard, "end_epoch", None)
+    if end is not None:
+        sse_all, bad_any = end()
     return sse_all, order, bad_any
 
 
@@ -139,15 +151,18 @@ class GpuShard:
 
         self.torch = torch
         self.grid = make_grid(d.n, d.m, cfg.grid_i, cfg.grid_j)
-        mask = shard_rows(d.rows, self.grid.row_bounds, sched, rank)
-        self.local_nnz = int(mask.sum())
         self.stream = torch.cuda.current_stream(device)
         opts = options or EngineOptions()
         opts = EngineOptions(exact=False, min_chunk=opts.min_chunk, device=device,
                              timing=opts.timing, warps_per_sm=opts.warps_per_sm)
         self.eng = Engine(opts, stream=self.stream.cuda_stream)
-        self.eng.partition(d.rows[mask], d.cols[mask], d.values[mask], d.n, d.m,
-                           cfg.grid_i, cfg.grid_j)
+        # this rank's U row-blocks: the upload keeps only their ratings
+        # (bgmf_partition_rows), no host-side gather of the dataset
+        own = sched.rows_of(rank)
+        rb = self.grid.row_bounds
+        self.eng.partition(d.rows, d.cols, d.values, d.n, d.m, cfg.grid_i, cfg.grid_j,
+                           row_range=(int(rb[own.start]), int(rb[own.stop])))
+        self.local_nnz = self.eng.nnz
         self.k, self.kp = cfg.k, (cfg.k + 3) // 4 * 4
         self.U = torch.zeros((d.n, self.kp), dtype=torch.float32, device=f"cuda:{device}")
         self.V = torch.zeros((d.m, self.kp), dtype=torch.float32, device=f"cuda:{device}")
@@ -165,10 +180,17 @@ class GpuShard:
         rb = self.grid.row_bounds
         return self.U[int(rb[rows.start]):int(rb[rows.stop])]
 
+    def begin_epoch(self, max_blocks: int):
+        self.eng.step_begin(max_blocks)
+
     def run_batch(self, blocks, g: int, alpha: float, beta: float):
+        """Enqueue this rank's blocks of one stratum (no host sync)."""
         ids, off = self.eng.plan_arrays([blocks])
-        sse, bad = self.eng.run_step(ids, off, g, alpha, beta)
-        return sse, bad, ids
+        self.eng.step_batch(ids, off, g, alpha, beta)
+        return None
+
+    def end_epoch(self):
+        return self.eng.step_end()
 
 
 def _init_dist():
@@ -247,11 +269,13 @@ def train_blocked_distributed(d, cfg, *, early_stop: bool = True, options=None,
             dist.broadcast(shard.u_rows(rows), src=r)
     torch.cuda.synchronize()
     u, v = shard.eng.get_factors()
+    shard.eng.close()
     return FactorModel(u, v), trace, stop
 
 
-def bench_main(args):
-    """bench.py --gpus N under torchrun: strong scaling of the C4 epoch."""
+def bench_main(args, clock_sampler=None):
+    """bench.py --gpus N under torchrun: strong scaling of the C4 epoch.
+    ``clock_sampler``: bench.py's nvidia-smi sampler class (rank 0)."""
     import json
 
     import torch
@@ -260,6 +284,13 @@ def bench_main(args):
     from .core import RatingsDataset, TrainConfig
     from .device import EngineOptions
 
+    # NCCL / torch print banners on stdout; the driver reads ONE JSON line
+    # there, so stdout is parked on stderr until that line is written
+    import sys
+
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     dist = _init_dist()
     rank, world = dist.get_rank(), dist.get_world_size()
     device = int(os.environ.get("LOCAL_RANK", rank))
@@ -293,17 +324,51 @@ def bench_main(args):
     shard.eng.set_timing(True)
     shard.eng.kernel_stats(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = None
+    if rank == 0 and clock_sampler is not None:
+        sampler = clock_sampler(device)
+        sampler.__enter__()
+    torch.cuda.synchronize()
+    dist.barrier()
     e0.record(stream)
     for _ in range(args.steps):
         epoch(step % w.grid)
         step += 1
     e1.record(stream)
     torch.cuda.synchronize()
+    dist.barrier()
+    if sampler is not None:
+        sampler.__exit__(None, None, None)
     st = shard.eng.kernel_stats(reset=True)
     ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{device}")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     dist.barrier()
     total_ms = float(ms.item())
+    shard.eng.close()
+    del shard
+
+    # e2e through the public multi-GPU API: host dataset in, host model out
+    e2e = None
+    if not getattr(args, "no_e2e", False):
+        run_cfg = TrainConfig(k=w.k, alpha=w.alpha, beta=w.beta, grid_i=w.grid, grid_j=w.grid,
+                              seed=w.seed, outer_steps=args.steps)
+        train_blocked_distributed(d, TrainConfig(k=w.k, grid_i=w.grid, grid_j=w.grid,
+                                                 outer_steps=1), early_stop=False)  # warm
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        train_blocked_distributed(d, run_cfg, early_stop=False)
+        torch.cuda.synchronize()
+        wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
+                            device=f"cuda:{device}")
+        dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+        t_e2e = float(wall.item())
+        e2e = {"value": nnz * args.steps / t_e2e, "unit": "updates/s",
+               "h2d_bytes_per_step": nnz * 12 / args.steps,
+               "d2h_bytes_per_step": (w.n + w.m) * w.k * 8 * world / args.steps,
+               "what": "train_blocked_distributed(host RatingsDataset) on every rank: each "
+                       "rank uploads its row shard (12 B/rating), trains, gathers the model "
+                       "(NCCL broadcasts) and downloads it; max wall time over ranks"}
     if rank == 0:
         hbm = 6553.0
         try:
@@ -328,9 +393,14 @@ def bench_main(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None,
                          "kernel": "sgd_fast_kernel (rank 0)"},
-            "e2e": None, "cpu_baseline": None,
+            "e2e": e2e, "cpu_baseline": None,
+            "clocks": sampler.summary() if sampler is not None else None,
             "gpu_launches": int(st["sgd_launches"] + st["sse_launches"]),
             "gen_seconds": t_gen,
         }
-        print(json.dumps(line))
+        sys.stdout.flush()
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.destroy_process_group()
+    sys.stdout.flush()
+    os.dup2(json_fd, 1)
+    os.close(json_fd)

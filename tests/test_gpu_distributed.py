@@ -45,3 +45,42 @@ def test_world1_nccl_matches_oracle():
         assert np.isfinite(bm.rmse(model, d))
     finally:
         dist.destroy_process_group()
+
+
+def test_async_step_matches_run_step():
+    """bgmf_step_begin/_batch/_end (the ring trainer's per-stratum path) gives
+    the same per-block SSEs as one bgmf_run_step over the whole plan, and
+    reports divergence by block id in submission order."""
+    r, c, v = workloads.lowrank(6040, 3706, 400_000, seed=9)
+    P = 4
+    plan = bm.plan_step(P, P, 0)
+    outs = []
+    for mode in ("sync", "async"):
+        eng = bm.Engine()
+        eng.partition(r, c, v, 6040, 3706, P, P)
+        eng.init_factors(6040, 3706, 32, 0)
+        if mode == "sync":
+            ids, off = eng.plan_arrays(plan)
+            sse, bad = eng.run_step(ids, off, 1, 1e-3, 1e-2)
+        else:
+            eng.step_begin(P * P)
+            for batch in plan:
+                ids, off = eng.plan_arrays([batch])
+                eng.step_batch(ids, off, 1, 1e-3, 1e-2)
+            sse, bad = eng.step_end()
+        assert bad is None
+        outs.append(sse)
+        eng.close()
+    np.testing.assert_allclose(outs[1], outs[0], rtol=1e-5)
+    eng = bm.Engine()
+    eng.partition(r, c, v, 6040, 3706, P, P)
+    eng.init_factors(6040, 3706, 32, 0)
+    eng.step_begin(P * P)
+    for batch in plan:
+        ids, off = eng.plan_arrays([batch])
+        eng.step_batch(ids, off, 1, 1e9, 0.0)
+    sse, bad = eng.step_end()
+    first = plan.batches[0].blocks[0]
+    assert bad is not None and bad[0] == first[0] * P + first[1]
+    with pytest.raises(RuntimeError, match="step_begin"):
+        eng.step_batch(ids, off, 1, 1e-3, 1e-2)  # no step_begin

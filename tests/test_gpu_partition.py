@@ -135,3 +135,26 @@ def test_c4_full_size_properties():
     assert np.all(np.diff(key) > 0)
     counts = np.bincount(_block_ids(r, c, w.n, w.m, 16, 16), minlength=256)
     assert np.array_equal(np.diff(off), counts)
+
+
+def test_partition_rows_keeps_only_the_row_range():
+    """bgmf_partition_rows == bgmf_partition of the pre-filtered entries
+    (offsets, local coordinates, values), and still range-checks every entry."""
+    g = np.random.default_rng(3)
+    n, m, nnz = 1000, 700, 50_000
+    cells = g.choice(n * m, nnz, replace=False)
+    r, c = cells // m, cells % m
+    v = g.integers(1, 6, nnz).astype(np.float64)
+    for lo, hi in ((0, 1000), (250, 500), (0, 1), (999, 1000), (400, 400)):
+        a, b = bm.Engine(), bm.Engine()
+        a.partition(r, c, v, n, m, 4, 3, row_range=(lo, hi))
+        keep = (r >= lo) & (r < hi)
+        b.partition(r[keep], c[keep], v[keep], n, m, 4, 3)
+        oa, _, ra, ca = a.export_partition()
+        ob, _, rb_, cb = b.export_partition()
+        assert np.array_equal(oa, ob) and a.nnz == int(keep.sum())
+        assert np.array_equal(ra, rb_) and np.array_equal(ca, cb)
+    bad = r.copy()
+    bad[123] = n + 5
+    with pytest.raises(bm.DataError, match="entry 123"):
+        bm.Engine().partition(bad, c, v, n, m, 4, 3, row_range=(0, 10))
