@@ -359,7 +359,8 @@ def run_out_of_core(args, dev):
     w = workloads.CONFIGS["C5"]
     nnz = args.nnz or w.nnz
     stream = torch.cuda.current_stream()
-    eng = bm.Engine(bm.EngineOptions(device=dev, fused=False), stream=stream.cuda_stream)
+    eng = bm.Engine(bm.EngineOptions(device=dev, fused=False, l2_wave_bytes=args.l2_wave_bytes),
+                    stream=stream.cuda_stream)
     t0 = time.perf_counter()
     N.check(eng._L.bgmf_synth_partition(eng._h, w.n, w.m, nnz, w.seed, w.grid, w.grid), eng._h)
     t_part = time.perf_counter() - t0
@@ -467,6 +468,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--budget-gb", type=float, default=1.5,
                     help="C5: device memory for streamed ratings (slots)")
+    ap.add_argument("--l2-wave-bytes", type=int, default=None,
+                    help="V bytes swept at once (library default 48 MiB; 0 = whole strata)")
     ap.add_argument("--ref-batches", type=int, default=None,
                     help="strata per CPU sample (default: the whole epoch)")
     args = ap.parse_args()

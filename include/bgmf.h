@@ -56,6 +56,9 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      instead capped at "col_ratio" (0.6) x block columns
  *                      (default 32; 0 = always min_chunk).
  *   "col_ratio"  float see sparse_min_chunk.
+ *   "l2_wave_bytes" int  fast mode: a stratum whose V blocks exceed this many
+ *                      bytes runs as sequential waves of blocks that fit (so
+ *                      the V traffic stays in L2; default 48 MiB, 0 = off).
  *   "stagger"    0/1/2 chunk-length rule in fast mode: 2 (default) rounds the
  *                      chunk up to 8*q with q odd so concurrent groups start
  *                      at staggered columns on dense rows (no lockstep V

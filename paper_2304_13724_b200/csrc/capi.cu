@@ -205,6 +205,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "stagger")) c->stagger = (int)value;
   else if (!strcmp(key, "sparse_min_chunk")) c->sparse_min_chunk = value < 0 ? 0 : (int)value;
   else if (!strcmp(key, "col_ratio")) c->col_ratio = value > 0 ? value : 0.6;
+  else if (!strcmp(key, "l2_wave_bytes")) c->l2_wave_bytes = value < 0 ? 0 : (int64_t)value;
   else if (!strcmp(key, "fused_max_batch")) c->fused_max_batch = (int64_t)value;
   else return fail(c, BGMF_ERR_ARG, std::string("unknown option ") + key);
   return BGMF_OK;

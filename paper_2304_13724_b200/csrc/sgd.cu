@@ -731,6 +731,33 @@ struct BatchRange {
   int w0, nw, chunks;
 };
 
+// L2-resident waves.  A stratum's blocks are independent, so running it as
+// several sequential sub-batches is the same algorithm.  The sweep's V traffic
+// is L2 traffic only while the V blocks being swept at once fit in L2 (C4:
+// 16 x 570 KB); when a stratum's V set is larger (C5: 64 x 8 MB = 512 MB) every
+// V row read and reduce-add goes to HBM.  Cut each batch into waves whose
+// V blocks total <= l2_wave_bytes (each wave re-chunked to fill the GPU).
+// Returns the refined batch offsets over the same plan array.
+std::vector<int32_t> l2_waves(const bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off,
+                              int nbatch) {
+  std::vector<int32_t> off;
+  off.push_back(batch_off[0]);
+  for (int t = 0; t < nbatch; ++t) {
+    double bytes = 0;
+    for (int q = batch_off[t]; q < batch_off[t + 1]; ++q) {
+      const int bj = plan[q] % c->J;
+      const double vb = (double)(c->col_bounds[bj + 1] - c->col_bounds[bj]) * c->kp * 4.0;
+      if (c->l2_wave_bytes > 0 && bytes > 0 && bytes + vb > (double)c->l2_wave_bytes) {
+        off.push_back(q);
+        bytes = 0;
+      }
+      bytes += vb;
+    }
+    off.push_back(batch_off[t + 1]);
+  }
+  return off;
+}
+
 // Per-block chunk length of the fast paths.  cl = the batch's one-wave
 // length (ceil(batch nnz / free groups)); the floor bounds how many groups
 // sweep one block at once (lossless Hogwild: reads of a V row are stale by the
@@ -874,9 +901,13 @@ int ensure_step_scratch(bgmf_ctx* c, size_t nwork) {
 // One outer step, fast path.  Default: ONE cooperative launch of
 // epoch_fast_kernel for the whole step (grid = one wave of resident CTAs).
 // Option fused=0: per batch, `iters` sgd launches + one sse launch.
-int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
+int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in, int nbatch_in,
                   int iters, float alpha, float beta) {
   cudaStream_t s = c->stream;
+  const std::vector<int32_t> waves = l2_waves(c, plan, batch_off_in, nbatch_in);
+  const bool split = (int)waves.size() - 1 != nbatch_in && c->fused <= 0;
+  const int32_t* batch_off = split ? waves.data() : batch_off_in;
+  const int nbatch = split ? (int)waves.size() - 1 : nbatch_in;
   const Shape sh = shape_for(c->kp);
   const int gpw = 32 / sh.L;
   const int nb = c->I * c->J;
@@ -980,9 +1011,12 @@ int step_begin(bgmf_ctx* c, int max_blocks) {
   return BGMF_OK;
 }
 
-int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch, int iters,
-               float alpha, float beta) {
+int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in, int nbatch_in,
+               int iters, float alpha, float beta) {
   if (!c->in_step) return fail(c, BGMF_ERR_STATE, "bgmf_step_begin has not been called");
+  const std::vector<int32_t> waves = l2_waves(c, plan, batch_off_in, nbatch_in);
+  const int32_t* batch_off = waves.data();
+  const int nbatch = (int)waves.size() - 1;
   const int total = batch_off[nbatch];
   if ((size_t)(c->w_cursor + total) > c->work_cap)
     return fail(c, BGMF_ERR_ARG, "more blocks than reserved by bgmf_step_begin");

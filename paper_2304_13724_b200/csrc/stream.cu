@@ -190,12 +190,18 @@ int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, 
     while (q < batch_off[t + 1]) {
       int q_end = q;
       int64_t fill = 0;
+      double vbytes = 0;
       int nonempty = 0;
       while (q_end < batch_off[t + 1]) {
         const int b = plan[q_end];
         if (b < 0 || b >= nb) return fail(c, BGMF_ERR_ARG, "plan block id out of range");
         const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
         if (fill + cnt > c->slot_cap) break;
+        // one L2-resident wave per piece (l2_waves, sgd.cu)
+        const int bj = b % c->J;
+        const double vb = (double)(c->col_bounds[bj + 1] - c->col_bounds[bj]) * c->kp * 4.0;
+        if (c->l2_wave_bytes > 0 && q_end > q && vbytes + vb > (double)c->l2_wave_bytes) break;
+        vbytes += vb;
         fill += cnt;
         nonempty += cnt > 0;
         ++q_end;

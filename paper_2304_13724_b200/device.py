@@ -45,6 +45,10 @@ class EngineOptions:
                ~3% faster (profiles/r01_*).
     sse_wide   post-sweep SSE with 4 ratings' rows in flight per group
                (measured slower than the pipelined walk on C4; off).
+    l2_wave_bytes
+               V-block bytes swept at once: larger strata run as sequential
+               waves of blocks whose V fits in L2 (None: library default,
+               48 MiB; 0: whole strata).
     device_rating_budget
                bytes of HBM the ratings may use (None: all resident).  When
                the partition is larger, it moves to pinned host memory and
@@ -62,6 +66,7 @@ class EngineOptions:
     bulk_red: bool = False
     sse_wide: bool = False
     stream_slots: int = 3
+    l2_wave_bytes: int | None = None
 
 
 def default_device() -> int:
@@ -87,6 +92,8 @@ class Engine:
         self._opt("warps_per_sm", float(self.options.warps_per_sm))
         self._opt("bulk_red", 1.0 if self.options.bulk_red else 0.0)
         self._opt("sse_wide", 1.0 if self.options.sse_wide else 0.0)
+        if self.options.l2_wave_bytes is not None:
+            self._opt("l2_wave_bytes", float(self.options.l2_wave_bytes))
         f = self.options.fused
         self._opt("fused", -1.0 if f is None else (1.0 if f else 0.0))
         self.n = self.m = self.nnz = 0
