@@ -62,3 +62,21 @@ def test_stream_rejects_slot_smaller_than_a_block():
     d = _c2_like(50_000)
     with pytest.raises(ValueError, match="largest block"):
         bm.partition(d, 2, 2, options=bm.EngineOptions(device_rating_budget=12 * 3000))
+
+
+@pytest.mark.parametrize("streamed", [False, True])
+def test_l2_waves_match_oracle(streamed):
+    """l2_wave_bytes small enough that every stratum runs as one wave per
+    block (in core) / one piece per block (streamed): still the reference
+    algorithm, per-epoch RMSE within 1e-3 of the oracle."""
+    d = _c2_like()
+    cfg = bm.TrainConfig(k=32, outer_steps=4, grid_i=8, grid_j=8)
+    opts = bm.EngineOptions(l2_wave_bytes=1,
+                            device_rating_budget=(12 * len(d) // 2) if streamed else None)
+    blocked = bm.partition(d, 8, 8, options=opts)
+    assert blocked.engine.streaming == streamed
+    res = bm.train_blocked(d, cfg, early_stop=False, timing=False, blocked=blocked)
+    _, _, otr, _ = O.train_blocked(d.n, d.m, d.rows, d.cols, d.values, k=32, outer_steps=4,
+                                   grid_i=8, grid_j=8, early_stop=False, nthreads=8)
+    got = np.array([s.train_rmse for s in res.trace])
+    assert np.abs(got - [s["train_rmse"] for s in otr]).max() <= TOL
