@@ -898,9 +898,11 @@ int ensure_step_scratch(bgmf_ctx* c, size_t nwork) {
   return BGMF_OK;
 }
 
-// One outer step, fast path.  Default: ONE cooperative launch of
-// epoch_fast_kernel for the whole step (grid = one wave of resident CTAs).
-// Option fused=0: per batch, `iters` sgd launches + one sse launch.
+// One outer step, fast path.  Default: per stratum (wave), `iters` sweep
+// launches + one SSE launch, all enqueued without a host sync; one D2H of the
+// per-block SSEs at the end.  fused=1: ONE cooperative launch of
+// epoch_fast_kernel for the whole step (grid barriers between strata;
+// measured slower on B200 at every config, kept as an option).
 int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in, int nbatch_in,
                   int iters, float alpha, float beta) {
   cudaStream_t s = c->stream;
