@@ -70,8 +70,11 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      memory ring); 0 = per-lane red.global.add.v4 (default,
  *                      measured faster: both bound by the SM->L2 interface).
  *   "sse_wide"   0/1   1 = post-sweep SSE with several ratings' rows in flight
- *                      per group; 0 = the sweep's pipelined walk (default,
- *                      measured faster on C4).
+ *                      per group (measured slower on C4).
+ *   "sse_async"  0/1   1 (default) = post-sweep SSE streams the V rows of the
+ *                      next 4 ratings of each group through a per-lane
+ *                      cp.async shared-memory ring; 0 = the sweep's
+ *                      register-pipelined walk (one row in flight).
  *   "fused"      -1/0/1  1 = one cooperative launch per outer step (all
  *                      strata, sweeps and SSE passes separated by grid
  *                      barriers); 0 = one launch per stratum sweep / SSE pass;

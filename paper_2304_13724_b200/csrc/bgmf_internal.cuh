@@ -61,6 +61,7 @@ struct bgmf_ctx {
   int warps_per_sm = 0;
   bool bulk_red = false;  // V deltas via TMA bulk reduce (measured slower: SM->L2 bound)
   bool sse_wide = false;  // post-sweep SSE with D ratings in flight (measured slower)
+  bool sse_async = true;  // post-sweep SSE through a per-lane cp.async ring (sse_async_kernel)
   int fused = -1;      // 1: one cooperative launch per step, 0: per stratum, -1 auto
   int groups_key = -1;                // sweep_groups() cache
   int64_t groups_cache = 0;

@@ -202,6 +202,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "fused")) c->fused = value < 0 ? -1 : (value != 0.0 ? 1 : 0);
   else if (!strcmp(key, "bulk_red")) c->bulk_red = value != 0.0;
   else if (!strcmp(key, "sse_wide")) c->sse_wide = value != 0.0;
+  else if (!strcmp(key, "sse_async")) c->sse_async = value != 0.0;
   else if (!strcmp(key, "stagger")) c->stagger = (int)value;
   else if (!strcmp(key, "sparse_min_chunk")) c->sparse_min_chunk = value < 0 ? 0 : (int)value;
   else if (!strcmp(key, "col_ratio")) c->col_ratio = value > 0 ? value : 0.6;

@@ -170,6 +170,14 @@ __device__ __forceinline__ void load_row(float4 (&dst)[V4], const float* row, co
   for (int q = 0; q < V4; ++q) dst[q] = ln.on(q) ? ld_cg(row + ln.off(q)) : zero4();
 }
 
+// Read-only rows (no writer during the kernel): ld.global.nc.
+template <int V4, class LN>
+__device__ __forceinline__ void load_row_ro(float4 (&dst)[V4], const float* row, const LN& ln) {
+#pragma unroll
+  for (int q = 0; q < V4; ++q)
+    dst[q] = ln.on(q) ? __ldg(reinterpret_cast<const float4*>(row + ln.off(q))) : zero4();
+}
+
 template <int V4, class LN>
 __device__ __forceinline__ void store_row(float* row, const float4 (&u)[V4], const LN& ln) {
 #pragma unroll
@@ -370,6 +378,109 @@ sse_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
   const double acc = walk_chunk<L, V4, kMask, false>(ch, maxlen, lrow, lcol, val,
                                                      const_cast<float*>(U), const_cast<float*>(V),
                                                      kp, 0.f, 0.f, 0, nullptr, cbits);
+  if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
+}
+
+// Post-sweep SSE with the V rows streamed through a per-lane shared-memory
+// ring by cp.async (LDGSTS): each lane copies its own 16-byte slices of the
+// V row of rating t+D while rating t is computed, so D rows per group are in
+// flight with no register cost (the pipelined register walk keeps one; the
+// pass is latency-bound on those reads: profiles/r01_ncu_c4.md).  A lane only
+// reads back what it copied itself, so cp.async.wait_group is the only
+// synchronisation.  U stays in registers for a user's run (next run's row
+// prefetched one rating ahead, as in walk_chunk).  Requires D <= L.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int L, int V4, bool kMask, int D>
+__global__ void __launch_bounds__(256, 2)
+sse_async_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
+                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
+                 const float* __restrict__ val, const float* __restrict__ U,
+                 const float* __restrict__ V, int kp, double* __restrict__ sse, int cbits) {
+  static_assert(D <= L, "the look-ahead must fit the two triple batches");
+  constexpr int GPW = 32 / L;
+  // this lane's D slots of V4 float4, lane-interleaved ([slot][q][thread]) so a
+  // warp's 16-byte accesses hit 32 consecutive bank quads
+  extern __shared__ float4 ring_all[];
+  float4* ring = ring_all + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
+  const int len = (int)(ch.end - ch.begin);
+  const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
+  if (maxlen == 0) return;
+  const Lanes<L, V4, kMask> ln(kp);
+  const float* Ub = U + ch.row_start * kp;
+  const float* Vb = V + ch.col_start * kp;
+  auto issue = [&](int t, int c) {  // V row of rating t -> slot t % D
+    if (t < len) {
+      const float* row = Vb + (int64_t)c * kp;
+      float4* slot = ring + (t % D) * V4 * 256;
+#pragma unroll
+      for (int q = 0; q < V4; ++q)
+        if (ln.on(q)) cp_async16(slot + q * 256, row + ln.off(q));
+    }
+    cp_async_commit();
+  };
+  int rA = 0, cA = 0, rB = 0, cB = 0;
+  float xA = 0.f, xB = 0.f;
+  if (ln.gl < len) load_triple(lrow, lcol, val, cbits, ch.begin + ln.gl, rA, cA, xA);
+  if (L + ln.gl < len) load_triple(lrow, lcol, val, cbits, ch.begin + L + ln.gl, rB, cB, xB);
+#pragma unroll
+  for (int d = 0; d < D; ++d) issue(d, __shfl_sync(kFull, cA, ln.gbase + d));
+  int r = __shfl_sync(kFull, rA, ln.gbase);
+  float4 u[V4], un[V4];
+  if (len > 0) load_row_ro(u, Ub + (int64_t)r * kp, ln);
+  else {
+#pragma unroll
+    for (int q = 0; q < V4; ++q) u[q] = zero4();
+  }
+  double acc = 0.0;
+  for (int t0 = 0; t0 < maxlen; t0 += L) {
+#pragma unroll 1
+    for (int j = 0; j < L; ++j) {
+      const int t = t0 + j;
+      const float x = __shfl_sync(kFull, xA, ln.gbase + j);
+      const bool last_in_batch = (j + 1 == L);
+      const int src = ln.gbase + ((j + 1) & (L - 1));
+      const int rn = __shfl_sync(kFull, last_in_batch ? rB : rA, src);
+      const bool newrun = t + 1 < len && rn != r;
+      if (newrun) load_row_ro(un, Ub + (int64_t)rn * kp, ln);
+      cp_async_wait<D - 1>();  // rating t's slot has landed
+      float4 v[V4];
+      const float4* slot = ring + (t % D) * V4 * 256;
+#pragma unroll
+      for (int q = 0; q < V4; ++q) v[q] = ln.on(q) ? slot[q * 256] : zero4();
+      const float dot = group_sum<L>(dot_slice<V4>(u, v));
+      if (t < len) {
+        const double ed = (double)x - (double)dot;
+        acc += ed * ed;
+      }
+      // refill this slot with rating t + D (from batch A, or B past its edge)
+      const int srcd = ln.gbase + ((j + D) & (L - 1));
+      const int cd = __shfl_sync(kFull, j + D < L ? cA : cB, srcd);
+      issue(t + D, cd);
+      if (newrun) {
+#pragma unroll
+        for (int q = 0; q < V4; ++q) u[q] = un[q];
+      }
+      r = rn;
+    }
+    rA = rB; cA = cB; xA = xB;
+    const int nb = t0 + 2 * L + ln.gl;
+    if (nb < len) load_triple(lrow, lcol, val, cbits, ch.begin + nb, rB, cB, xB);
+  }
+  cp_async_wait<0>();
   if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
 }
 
@@ -655,6 +766,22 @@ void launch_sse_wide(cudaStream_t s, const BlockWork* w, int nwork, int total,
 #undef BGMF_SSE
 }
 
+template <int LL, int VV, bool MM>
+void launch_sse_async(dim3 grid, cudaStream_t s, const BlockWork* w, int nwork, int total,
+                      const int32_t* lrow, const int32_t* lcol, const float* val, bgmf_ctx* c,
+                      int cbits) {
+  constexpr int D = LL < 4 ? LL : 4;
+  const int smem = 256 * D * VV * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(&sse_async_kernel<LL, VV, MM, D>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  sse_async_kernel<LL, VV, MM, D><<<grid, 256, smem, s>>>(w, nwork, total, lrow, lcol, val,
+                                                          c->d_u, c->d_v, c->kp, c->d_sse, cbits);
+}
+
 // dynamic smem of the bulk sweep: kBulkBufs delta rows per group
 size_t bulk_smem(bgmf_ctx* c, const Shape& sh) {
   return (size_t)(256 / sh.L) * kBulkBufs * c->kp * sizeof(float);
@@ -681,6 +808,8 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
           w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
     else if (c->sse_wide)                                                                     \
       launch_sse_wide(s, w, nwork, total, lrow, lcol, val, c, cbits);                          \
+    else if (c->sse_async > 0)                                                                \
+      launch_sse_async<LL, VV, MM>(grid, s, w, nwork, total, lrow, lcol, val, c, cbits);      \
     else                                                                                      \
       sse_fast_kernel<LL, VV, MM><<<grid, 256, 0, s>>>(w, nwork, total, lrow, lcol, val,      \
                                                        c->d_u, c->d_v, c->kp, c->d_sse, cbits);      \

@@ -45,6 +45,9 @@ class EngineOptions:
                ~3% faster (profiles/r01_*).
     sse_wide   post-sweep SSE with 4 ratings' rows in flight per group
                (measured slower than the pipelined walk on C4; off).
+    sse_async  post-sweep SSE with the V rows of the next 4 ratings in flight
+               per group through a per-lane cp.async shared-memory ring
+               (None/True: on; False: the register-pipelined walk).
     l2_wave_bytes
                V-block bytes swept at once: larger strata run as sequential
                waves of blocks whose V fits in L2 (None: library default,
@@ -66,6 +69,7 @@ class EngineOptions:
     bulk_red: bool = False
     sse_wide: bool = False
     stream_slots: int = 3
+    sse_async: bool | None = None
     l2_wave_bytes: int | None = None
 
 
@@ -92,6 +96,7 @@ class Engine:
         self._opt("warps_per_sm", float(self.options.warps_per_sm))
         self._opt("bulk_red", 1.0 if self.options.bulk_red else 0.0)
         self._opt("sse_wide", 1.0 if self.options.sse_wide else 0.0)
+        self._opt("sse_async", 0.0 if self.options.sse_async is False else 1.0)
         if self.options.l2_wave_bytes is not None:
             self._opt("l2_wave_bytes", float(self.options.l2_wave_bytes))
         f = self.options.fused
