@@ -446,6 +446,90 @@ sse_async_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks
     for (int q = 0; q < V4; ++q) u[q] = zero4();
   }
   double acc = 0.0;
+  if (L >= 4) {
+    // two ratings per step: their dot products share one reduce-scatter
+    // (level L/2 splits the pair between the half-groups, then the usual
+    // butterfly), so the shuffle chain is amortised over both.  The pairs of
+    // lanes added are the butterfly's, so every dot is bit-identical to it.
+    constexpr int H = L / 2;
+    const bool upper = (ln.gl & H) != 0;
+    int rcur = len > 0 ? r : -1, rnxt = -1;
+    for (int t0 = 0; t0 < maxlen; t0 += L) {
+#pragma unroll 1
+      for (int j = 0; j < L; j += 2) {
+        const int t = t0 + j;
+        const float x0 = __shfl_sync(kFull, xA, ln.gbase + j);
+        const float x1 = __shfl_sync(kFull, xA, ln.gbase + j + 1);
+        const int r0 = __shfl_sync(kFull, rA, ln.gbase + j);
+        const int r1 = __shfl_sync(kFull, rA, ln.gbase + j + 1);
+        const int r2 = __shfl_sync(kFull, j + 2 < L ? rA : rB, ln.gbase + ((j + 2) & (L - 1)));
+        const int r3 = __shfl_sync(kFull, j + 3 < L ? rA : rB, ln.gbase + ((j + 3) & (L - 1)));
+        cp_async_wait<D - 2>();  // ratings t, t+1 have landed
+        float4 v0[V4], v1[V4];
+        const float4* s0 = ring + (t % D) * V4 * 256;
+        const float4* s1 = ring + ((t + 1) % D) * V4 * 256;
+#pragma unroll
+        for (int q = 0; q < V4; ++q) {
+          v0[q] = ln.on(q) ? s0[q * 256] : zero4();
+          v1[q] = ln.on(q) ? s1[q * 256] : zero4();
+        }
+        // U of rating t, then of t+1: the current run's row, the prefetched
+        // next run's row, or (rarely: two runs starting in one pair) a load now
+        if (t < len && r0 != rcur) {
+          if (r0 == rnxt) {
+#pragma unroll
+            for (int q = 0; q < V4; ++q) u[q] = un[q];
+          } else {
+            load_row_ro(u, Ub + (int64_t)r0 * kp, ln);
+          }
+          rcur = r0;
+          rnxt = -1;
+        }
+        const float p0 = dot_slice<V4>(u, v0);
+        if (t + 1 < len && r1 != rcur) {
+          if (r1 == rnxt) {
+#pragma unroll
+            for (int q = 0; q < V4; ++q) u[q] = un[q];
+          } else {
+            load_row_ro(u, Ub + (int64_t)r1 * kp, ln);
+          }
+          rcur = r1;
+          rnxt = -1;
+        }
+        const float p1 = dot_slice<V4>(u, v1);
+        // request the next run's U row as soon as its start is in view
+        if (rnxt < 0) {
+          const int cand = (t + 2 < len && r2 != rcur) ? r2 : ((t + 3 < len && r3 != rcur) ? r3 : -1);
+          if (cand >= 0) {
+            load_row_ro(un, Ub + (int64_t)cand * kp, ln);
+            rnxt = cand;
+          }
+        }
+        float a = upper ? p1 : p0;
+        const float b = upper ? p0 : p1;
+        a += __shfl_xor_sync(kFull, b, H);
+#pragma unroll
+        for (int o = H / 2; o > 0; o >>= 1) a += __shfl_xor_sync(kFull, a, o);
+        const bool valid = upper ? (t + 1 < len) : (t < len);
+        if (valid) {
+          const double ed = (double)(upper ? x1 : x0) - (double)a;
+          acc += ed * ed;
+        }
+        // refill both slots with ratings t + D, t + D + 1
+        const int cd0 = __shfl_sync(kFull, j + D < L ? cA : cB, ln.gbase + ((j + D) & (L - 1)));
+        const int cd1 =
+            __shfl_sync(kFull, j + D + 1 < L ? cA : cB, ln.gbase + ((j + D + 1) & (L - 1)));
+        issue(t + D, cd0);
+        issue(t + D + 1, cd1);
+      }
+      rA = rB; cA = cB; xA = xB;
+      const int nb = t0 + 2 * L + ln.gl;
+      if (nb < len) load_triple(lrow, lcol, val, cbits, ch.begin + nb, rB, cB, xB);
+    }
+    // only lanes gl == 0 (rating t) and gl == H (rating t+1) hold each sum once
+    if (ln.gl != 0 && ln.gl != H) acc = 0.0;
+    acc += __shfl_xor_sync(kFull, acc, H);
+  } else {
   for (int t0 = 0; t0 < maxlen; t0 += L) {
 #pragma unroll 1
     for (int j = 0; j < L; ++j) {
@@ -479,6 +563,7 @@ sse_async_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks
     rA = rB; cA = cB; xA = xB;
     const int nb = t0 + 2 * L + ln.gl;
     if (nb < len) load_triple(lrow, lcol, val, cbits, ch.begin + nb, rB, cB, xB);
+  }
   }
   cp_async_wait<0>();
   if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
