@@ -269,7 +269,7 @@ def run_ours(args):
     except Exception:
         pass
 
-    l2 = l2_ceiling(dev, w, st, sgd_launch_ms, nnz, args)
+    l2 = None if args.no_l2_probe else l2_ceiling(dev, w, st, sgd_launch_ms, nnz, args)
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0:
@@ -468,6 +468,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--budget-gb", type=float, default=1.5,
                     help="C5: device memory for streamed ratings (slots)")
+    ap.add_argument("--no-l2-probe", action="store_true",
+                    help="skip the SM<->L2 ceiling probe (e.g. under ncu)")
     ap.add_argument("--l2-wave-bytes", type=int, default=None,
                     help="V bytes swept at once (library default 48 MiB; 0 = whole strata)")
     ap.add_argument("--ref-batches", type=int, default=None,

@@ -50,10 +50,10 @@ for mb in (64,256,1024,4096):
       echo "ncuk rc=$?" ;;
     ncu)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-        --log-file $OUT/launches.csv $B --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
+        --log-file $OUT/launches.csv $B --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-l2-probe > $OUT/ncu_bench.log 2>&1
       echo "ncu-list rc=$?"
-      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"sgd_fast_kernel|sse_fast_kernel|epoch_fast_kernel" -s 4 -c 2 \
-        -o $OUT/sgd_full $B --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1
+      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"sgd_fast_kernel|sse_fast_kernel|sse_async_kernel|epoch_fast_kernel" -s 4 -c 2 \
+        -o $OUT/sgd_full $B --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-l2-probe > $OUT/ncu_full.log 2>&1
       echo "ncu-full rc=$?" ;;
   esac
 done
