@@ -187,6 +187,21 @@ int bgmf_stream_ratings(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
 /* Rating bytes streamed host->device since the context was created. */
 int bgmf_stream_stats(bgmf_ctx* ctx, double* h2d_bytes);
 
+/* nsteps outer steps in one call (fast mode, no host decision between them:
+ * train_blocked with early stopping off and a fixed inner schedule).  Step s
+ * runs plan block ids plans[...] cut by batch_offs[...] (both concatenated
+ * over the steps; step s has nbatch[s] batches, nbatch[s] + 1 offsets) with
+ * inner_iters[s] sweeps; sse_out[s * I*J + b] = block b's post-sweep SSE of
+ * step s.  All steps are enqueued back to back with one synchronisation at
+ * the end.  bad_out = {step, block id, entry, iteration} of the first
+ * diverged step, or -1s (later steps' results are then meaningless, as after
+ * the reference's DivergenceError).  step_ms (optional): device time of each
+ * step. */
+int bgmf_run_steps(bgmf_ctx* ctx, int nsteps, const int32_t* plans,
+                   const int32_t* batch_offs, const int32_t* nbatch,
+                   const int32_t* inner_iters, double alpha, double beta,
+                   double* sse_out, int64_t* bad_out, float* step_ms);
+
 /* Asynchronous outer step (fast mode), for callers that interleave their own
  * work between strata -- the multi-GPU ring trainer moves V blocks with NCCL
  * on the same stream between batches (trainer.py:138-152 barrier analog).

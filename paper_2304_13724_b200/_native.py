@@ -52,6 +52,8 @@ SIGNATURES = {
     "bgmf_bind_factors": (_i, [_ctx, _vp, _vp, _l, _l, _i, _i]),
     "bgmf_run_step": (_i, [_ctx, _i32p, _i32p, _i, _i, _d, _d, _f64p, _i64p]),
     "bgmf_partition_rows": (_i, [_ctx, _i64p, _i64p, _f64p, _l, _l, _l, _i, _i, _l, _l]),
+    "bgmf_run_steps": (_i, [_ctx, _i, _i32p, _i32p, _i32p, _i32p, _d, _d, _f64p, _i64p,
+                            ctypes.POINTER(ctypes.c_float)]),
     "bgmf_step_begin": (_i, [_ctx, _i]),
     "bgmf_step_batch": (_i, [_ctx, _i32p, _i32p, _i, _i, _d, _d]),
     "bgmf_step_end": (_i, [_ctx, _f64p, _i64p]),

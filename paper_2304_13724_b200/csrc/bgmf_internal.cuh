@@ -216,6 +216,9 @@ int step_begin(bgmf_ctx* c, int max_blocks);
 int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch, int iters,
                float alpha, float beta);
 int step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out);
+int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs,
+              const int32_t* nbatch, const int32_t* iters, float alpha, float beta,
+              double* sse_out, int64_t* bad_out, float* ms_out);
 int run_sync_parallel_step(bgmf_ctx* c, const int64_t* edges, int nshards, double alpha,
                            double beta, double* sse_out, int64_t* bad_out);
 int run_step_converge_exact(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,

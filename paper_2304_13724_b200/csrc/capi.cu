@@ -174,18 +174,23 @@ int bgmf_create(int device, void* stream, bgmf_ctx** out) {
 void bgmf_destroy(bgmf_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  prof_mark(c, nullptr);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  prof_mark(c, "destroy: sync");
   free_factors(c);
   free_holdout(c);
   stream_free(c);
+  prof_mark(c, "destroy: factors/holdout/stream");
   dfree(c->d_lrow, c->stream); dfree(c->d_lcol, c->stream); dfree(c->d_val, c->stream); dfree(c->d_val64, c->stream);
   dfree(c->d_order, c->stream); dfree(c->d_sse, c->stream); dfree(c->d_bad, c->stream); dfree(c->d_work, c->stream);
   dfree(c->d_partials, c->stream);
   dfree(c->d_priv, c->stream);
   cudaStreamSynchronize(c->stream);
+  prof_mark(c, "destroy: device frees");
   if (c->h_work) cudaFreeHost(c->h_work);
   if (c->h_sse) cudaFreeHost(c->h_sse);
   if (c->h_bad) cudaFreeHost(c->h_bad);
+  prof_mark(nullptr, "destroy: pinned frees");
   for (auto& t : c->events) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -415,6 +420,20 @@ int bgmf_run_step(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, in
   for (int b = 0; b < nb; ++b) sse_out[b] = c->h_sse[b];
   fill_bad(c, bad_out);
   return BGMF_OK;
+}
+
+int bgmf_run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* batch_offs,
+                   const int32_t* nbatch, const int32_t* inner_iters, double alpha, double beta,
+                   double* sse_out, int64_t* bad_out, float* step_ms) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (nsteps < 0 || (nsteps > 0 && (!plans || !batch_offs || !nbatch || !inner_iters ||
+                                    !sse_out)) || !bad_out)
+    return fail(c, BGMF_ERR_ARG, "NULL argument");
+  int rc = check_step_ready(c);
+  if (rc) return rc;
+  cudaSetDevice(c->device);
+  return run_steps(c, nsteps, plans, batch_offs, nbatch, inner_iters, (float)alpha, (float)beta,
+                   sse_out, bad_out, step_ms);
 }
 
 int bgmf_step_begin(bgmf_ctx* c, int max_blocks) {

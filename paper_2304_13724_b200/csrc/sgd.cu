@@ -1274,6 +1274,93 @@ int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in, in
   return BGMF_OK;
 }
 
+// Several outer steps in one call (fixed inner iterations, nothing decided on
+// the host between them -- train_blocked without early stopping): every
+// step's strata are enqueued back to back on the stream, each step writing
+// its own per-block SSE row and divergence word, so the GPU never idles on a
+// host round trip between epochs.  ms_out[s] (optional): CUDA-event time of
+// step s.  bad_out = {step, block id, entry, iteration} of the first diverged
+// step, or -1s.
+int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs,
+              const int32_t* nbatch, const int32_t* iters, float alpha, float beta,
+              double* sse_out, int64_t* bad_out, float* ms_out) {
+  if (c->exact) return fail(c, BGMF_ERR_STATE, "bgmf_run_steps is fast-mode only");
+  if (c->streaming) return fail(c, BGMF_ERR_STATE, "bgmf_run_steps does not stream");
+  const int nb = c->I * c->J;
+  cudaStream_t s = c->stream;
+  int64_t total = 0, plan_pos = 0, off_pos = 0;
+  for (int k = 0; k < nsteps; ++k) {
+    if (nbatch[k] < 0 || iters[k] < 1 || iters[k] > 65535)
+      return fail(c, BGMF_ERR_ARG, "bad step description");
+    const int32_t* off = offs + off_pos;
+    for (int q = 0; q < off[nbatch[k]]; ++q)
+      if (plans[plan_pos + q] < 0 || plans[plan_pos + q] >= nb)
+        return fail(c, BGMF_ERR_ARG, "plan block id out of range");
+    total += off[nbatch[k]];
+    plan_pos += off[nbatch[k]];
+    off_pos += nbatch[k] + 1;
+  }
+  int rc = ensure_step_scratch(c, (size_t)(total > 0 ? total : 1));
+  if (rc) return rc;
+  double* d_sse = nullptr;
+  unsigned long long* d_bad = nullptr;
+  std::vector<cudaEvent_t> ev(ms_out ? (size_t)nsteps + 1 : 0, nullptr);
+  auto cleanup = [&]() {
+    dfree(d_sse, s);
+    dfree(d_bad, s);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+  };
+  cudaError_t e = dmalloc(&d_sse, sizeof(double) * (size_t)nb * (nsteps > 0 ? nsteps : 1), s);
+  if (e == cudaSuccess) e = dmalloc(&d_bad, 8 * (size_t)(nsteps > 0 ? nsteps : 1), s);
+  for (size_t i = 0; i < ev.size() && e == cudaSuccess; ++i) e = cudaEventCreate(&ev[i]);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_sse, 0, sizeof(double) * (size_t)nb * nsteps, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_bad, 0xFF, 8 * (size_t)nsteps, s);
+  if (e != cudaSuccess) { cleanup(); return cuda_fail(c, e, "run_steps setup"); }
+  double* keep_sse = c->d_sse;
+  unsigned long long* keep_bad = c->d_bad;
+  c->in_step = true;
+  c->w_cursor = 0;
+  c->submitted.clear();
+  std::vector<int64_t> pos_end(nsteps);
+  plan_pos = off_pos = 0;
+  if (!ev.empty()) cudaEventRecord(ev[0], s);
+  for (int k = 0; k < nsteps && !rc; ++k) {
+    c->d_sse = d_sse + (size_t)k * nb;  // the stratum kernels address these through c
+    c->d_bad = d_bad + k;
+    const int32_t* off = offs + off_pos;
+    rc = step_batch(c, plans + plan_pos, off, nbatch[k], iters[k], alpha, beta);
+    if (!ev.empty()) cudaEventRecord(ev[k + 1], s);
+    pos_end[k] = (int64_t)c->submitted.size();
+    plan_pos += off[nbatch[k]];
+    off_pos += nbatch[k] + 1;
+  }
+  c->d_sse = keep_sse;
+  c->d_bad = keep_bad;
+  c->in_step = false;
+  if (rc) { cudaStreamSynchronize(s); cleanup(); return rc; }
+  std::vector<unsigned long long> hb((size_t)nsteps);
+  e = cudaMemcpyAsync(sse_out, d_sse, sizeof(double) * (size_t)nb * nsteps, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(hb.data(), d_bad, 8 * (size_t)nsteps, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) { cleanup(); return cuda_fail(c, e, "run_steps"); }
+  for (int k = 0; k < nsteps && ms_out; ++k) cudaEventElapsedTime(&ms_out[k], ev[k], ev[k + 1]);
+  if (c->timing) harvest_timing(c);
+  bad_out[0] = bad_out[1] = bad_out[2] = bad_out[3] = -1;
+  for (int k = 0; k < nsteps; ++k) {
+    if (hb[k] == kNoBad) continue;
+    const int64_t pos = (int64_t)(hb[k] >> 48);
+    bad_out[0] = k;
+    bad_out[1] = pos < (int64_t)c->submitted.size() ? c->submitted[pos] : -1;
+    bad_out[2] = (int64_t)(hb[k] & 0xFFFFFFFFull);
+    bad_out[3] = (int64_t)((hb[k] >> 32) & 0xFFFF);
+    break;
+  }
+  cleanup();
+  return BGMF_OK;
+}
+
 int step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out) {
   if (!c->in_step) return fail(c, BGMF_ERR_STATE, "bgmf_step_begin has not been called");
   c->in_step = false;

@@ -233,6 +233,26 @@ class Engine:
             N.ptr(capped, N._i32p), N.ptr(bad, N._i64p)))
         return sse, iters, capped, (None if bad[0] < 0 else tuple(int(x) for x in bad))
 
+    def run_steps(self, steps, alpha: float, beta: float):
+        """Several outer steps in one call (fast mode): ``steps`` is a list of
+        (ids, off, iters) as for run_step.  Returns (sse[nsteps, I*J],
+        bad = (step, block id, entry, iteration) or None, device ms per step)."""
+        n = len(steps)
+        plans = np.concatenate([np.asarray(i, np.int32) for i, _, _ in steps]) if n else \
+            np.zeros(1, np.int32)
+        offs = np.concatenate([np.asarray(o, np.int32) for _, o, _ in steps]) if n else \
+            np.zeros(1, np.int32)
+        nbatch = np.array([len(o) - 1 for _, o, _ in steps] or [0], np.int32)
+        iters = np.array([int(g) for _, _, g in steps] or [1], np.int32)
+        sse = np.zeros((max(n, 1), self.I * self.J), np.float64)
+        bad = np.zeros(4, np.int64)
+        ms = np.zeros(max(n, 1), np.float32)
+        self._check(self._L.bgmf_run_steps(
+            self._h, n, N.ptr(plans, N._i32p), N.ptr(offs, N._i32p), N.ptr(nbatch, N._i32p),
+            N.ptr(iters, N._i32p), float(alpha), float(beta), N.ptr(sse, N._f64p),
+            N.ptr(bad, N._i64p), ms.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+        return sse[:n], (None if bad[0] < 0 else tuple(int(x) for x in bad)), ms[:n]
+
     def step_begin(self, max_blocks: int):
         """Asynchronous step (fast mode): reserve ``max_blocks`` block launches."""
         self._check(self._L.bgmf_step_begin(self._h, int(max_blocks)))

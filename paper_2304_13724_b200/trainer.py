@@ -118,7 +118,14 @@ def train_blocked(d: RatingsDataset, cfg: TrainConfig, test: Optional[RatingsDat
 
     trace = ConvergenceTrace()
     stop: StopReason = "max_steps"
-    for step in range(1, cfg.outer_steps + 1):
+    batched = (not early_stop and block_hook is None and evaluator is None and not adaptive
+               and not isinstance(sched, ConvergeEachBlock) and not eng.options.exact
+               and not eng.streaming and cfg.outer_steps > 1)
+    if batched:
+        # nothing is decided on the host between steps: enqueue every epoch
+        # in one bgmf_run_steps call (no host round trip between epochs)
+        _run_steps_batched(eng, cfg, sched, counts, trace, timing)
+    for step in range(1, 0 if batched else cfg.outer_steps + 1):
         if adaptive and step >= 2:
             prev, cur = hist[-2], hist[-1]
             ratio = (prev - cur) / prev if prev > 0 else 0.0
@@ -176,6 +183,44 @@ class _Phases:
     def report(self):
         for what, dt in self.rows:
             print(f"[bgmf] {what:32s} {dt * 1e3:9.2f} ms", file=sys.stderr)
+
+
+def _run_steps_batched(eng, cfg, sched, counts, trace, timing):
+    """All outer steps of a fixed-schedule, no-early-stop run in one engine
+    call; the trace (and a DivergenceError at the first diverged step, with
+    the trace before it) as the per-step loop would produce."""
+    steps = []
+    for step in range(1, cfg.outer_steps + 1):
+        g = resolve_inner_iters(sched, step, 1.0)
+        ids, off = eng.plan_arrays(plan_step(cfg.grid_i, cfg.grid_j, step - 1))
+        steps.append((ids, off, g))
+    sse_all, bad, ms = eng.run_steps(steps, cfg.alpha, cfg.beta)
+    for k, (ids, _, g) in enumerate(steps):
+        sse = sse_all[k]
+        pos_bad, entry, it = None, None, None
+        if bad is not None and bad[0] == k:
+            pos_bad = int(np.nonzero(ids == bad[1])[0][0])
+            entry, it = bad[2], bad[3]
+        # the reference also stops at a non-finite post-sweep SSE
+        # (_kernels.py:57-58); the first offender in plan order wins
+        for pos, b in enumerate(ids):
+            if pos_bad is not None and pos >= pos_bad:
+                break
+            if not math.isfinite(sse[b]):
+                pos_bad, entry, it = pos, int(counts[b]) - 1, g - 1
+                break
+        if pos_bad is not None:
+            b = int(ids[pos_bad])
+            exc = divergence(b // cfg.grid_j, b % cfg.grid_j, entry, it)
+            exc.step = k + 1
+            exc.partial_trace = trace
+            raise exc
+        acc = RmseAccumulator()
+        for b in ids:  # submission order, as trainer.py:149-152
+            acc = merge(acc, RmseAccumulator(float(sse[b]), int(counts[b])))
+        trace.append(TraceStep(step=k + 1, train_rmse=finalize(acc), test_rmse=None,
+                               seconds=float(ms[k]) / 1e3 if timing else 0.0, inner_iters=g,
+                               capped_blocks=0))
 
 
 def _run_step(eng, batches, g, tol, cfg, counts, hooks, block_hook):

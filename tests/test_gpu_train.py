@@ -240,3 +240,30 @@ def test_exact_run_saves_reference_bytes(golden):
     bm.save_model(res.model, buf)
     assert buf.getvalue() == g["model"]
     assert [s.train_rmse for s in res.trace] == g["train"]
+
+
+def test_run_steps_batched_matches_per_step_loop():
+    """train_blocked without early stopping enqueues every epoch in one
+    bgmf_run_steps call; the trace must match the per-step loop (early_stop
+    with an unreachable delta) within run-to-run fp32 noise, including a
+    schedule whose inner iterations vary per step, and divergence must be
+    reported at the same step / block.  (delta = 0: the per-step loop would
+    only stop on a rising RMSE, which these 4 epochs never show.)"""
+    r, c, v = workloads.lowrank(6040, 3706, 300_000, seed=4)
+    d = bm.RatingsDataset(6040, 3706, r, c, v)
+    for sched in (bm.Constant(1), bm.Decreasing(3)):
+        cfg = bm.TrainConfig(k=32, outer_steps=4, grid_i=8, grid_j=8, inner_schedule=sched,
+                             delta=0.0)
+        a = bm.train_blocked(d, cfg, early_stop=False, timing=True)
+        b = bm.train_blocked(d, cfg, early_stop=True, timing=True)
+        assert [s.inner_iters for s in a.trace] == [s.inner_iters for s in b.trace]
+        np.testing.assert_allclose([s.train_rmse for s in a.trace],
+                                   [s.train_rmse for s in b.trace], rtol=1e-5)
+        assert all(s.seconds > 0 for s in a.trace)
+    cfg = bm.TrainConfig(k=32, outer_steps=4, grid_i=8, grid_j=8, alpha=1e9, delta=0.0)
+    errs = []
+    for es in (False, True):
+        with pytest.raises(bm.DivergenceError) as ei:
+            bm.train_blocked(d, cfg, early_stop=es)
+        errs.append((ei.value.step, ei.value.block))
+    assert errs[0] == errs[1] and errs[0][0] == 1
