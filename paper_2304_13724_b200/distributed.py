@@ -201,16 +201,20 @@ def _init_dist():
     return dist
 
 
-def train_blocked_distributed(d, cfg, *, early_stop: bool = True, options=None,
+def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, options=None,
                               timing: bool = True):
     """Multi-GPU train_blocked (fixed inner schedules): every rank calls it with
-    the same dataset and config; rank r uses GPU LOCAL_RANK.  Returns
-    (FactorModel on every rank, ConvergenceTrace, stop_reason)."""
+    the same dataset, test set and config; rank r uses GPU LOCAL_RANK.  The
+    per-step test RMSE (HoldoutEvaluator semantics, metrics.py:55-81) is
+    computed where U lives: each rank evaluates the test entries of its own
+    rows after the V blocks are broadcast from their holders, and the SSEs
+    are all-reduced.  Returns (FactorModel on every rank, ConvergenceTrace,
+    stop_reason)."""
     import torch
 
     from .core import ConvergenceTrace, FactorModel, TraceStep
     from .kernel import divergence
-    from .metrics import RmseAccumulator, finalize, merge
+    from .metrics import HoldoutEvaluator, RmseAccumulator, finalize, merge
     from .trainer import resolve_inner_iters
 
     dist = _init_dist()
@@ -220,6 +224,12 @@ def train_blocked_distributed(d, cfg, *, early_stop: bool = True, options=None,
     sched = RingSchedule(cfg.grid_i, cfg.grid_j, world)
     shard = GpuShard(d, cfg, sched, rank, device, options)
     shard.eng.init_factors(d.n, d.m, cfg.k, cfg.seed)
+    evaluator = HoldoutEvaluator(d, test) if test is not None and len(test) > 0 else None
+    if evaluator is not None:
+        t = evaluator.test
+        mine = shard_rows(t.rows, shard.grid.row_bounds, sched, rank)
+        shard.eng.holdout_set(t.rows[mine], t.cols[mine], t.values[mine], evaluator.cold[mine],
+                              evaluator.fallback)
     nb = cfg.grid_i * cfg.grid_j
     trace = ConvergenceTrace()
     stop = "max_steps"
@@ -252,7 +262,14 @@ def train_blocked_distributed(d, cfg, *, early_stop: bool = True, options=None,
         for b in order:
             acc = merge(acc, RmseAccumulator(float(sse_all[b]), int(total_counts[b])))
         train_rmse = finalize(acc)
-        trace.append(TraceStep(step, train_rmse, None,
+        test_rmse = None
+        if evaluator is not None:
+            sync_all_v(sched, rank, shard.v_slice, dist)  # every rank needs all of V
+            hs = torch.tensor([shard.eng.holdout_sse()], dtype=torch.float64,
+                              device=f"cuda:{device}")
+            dist.all_reduce(hs)
+            test_rmse = math.sqrt(float(hs.item()) / len(evaluator.test))
+        trace.append(TraceStep(step, train_rmse, test_rmse,
                                time.perf_counter() - t0 if timing else 0.0, g, 0))
         if early_stop:
             if acc.count == 0:

@@ -34,13 +34,16 @@ def test_world1_nccl_matches_oracle():
     dist.init_process_group("nccl", rank=0, world_size=1)
     try:
         r, c, v = workloads.lowrank(6040, 3706, 500_000, seed=5)
-        d = bm.RatingsDataset(6040, 3706, r, c, v)
+        d, te = bm.split(bm.RatingsDataset(6040, 3706, r, c, v), 0.2, seed=1)
         cfg = bm.TrainConfig(k=32, outer_steps=4, grid_i=8, grid_j=8)
-        model, trace, stop = D.train_blocked_distributed(d, cfg, early_stop=False)
+        model, trace, stop = D.train_blocked_distributed(d, cfg, te, early_stop=False)
         _, _, otr, _ = O.train_blocked(d.n, d.m, d.rows, d.cols, d.values, k=32, outer_steps=4,
-                                       grid_i=8, grid_j=8, early_stop=False, nthreads=8)
+                                       grid_i=8, grid_j=8, early_stop=False, nthreads=8,
+                                       test=(te.rows, te.cols, te.values))
         got = np.array([s.train_rmse for s in trace])
         assert np.abs(got - [s["train_rmse"] for s in otr]).max() <= 1e-3
+        got_t = np.array([s.test_rmse for s in trace])
+        assert np.abs(got_t - [s["test_rmse"] for s in otr]).max() <= 1e-3
         assert stop == "max_steps" and model.u.shape == (6040, 32)
         assert np.isfinite(bm.rmse(model, d))
     finally:
