@@ -59,11 +59,13 @@ __global__ void make_keys(const IT* __restrict__ rows, const IT* __restrict__ co
 }
 
 // Per-tile digit histogram, written digit-major: hist[d * ntiles + tile].
+// RD = buckets per pass (256: 8-bit digits, 512: 9-bit digits).
+template <int RD>
 __global__ void __launch_bounds__(RS_THREADS)
 radix_hist(const uint64_t* __restrict__ keys, int64_t n, int shift, int64_t ntiles,
            uint32_t* __restrict__ hist) {
-  __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
+  __shared__ uint32_t h[RD];
+  for (int d = threadIdx.x; d < RD; d += RS_THREADS) h[d] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * RS_TILE;
@@ -73,13 +75,13 @@ radix_hist(const uint64_t* __restrict__ keys, int64_t n, int shift, int64_t ntil
     const bool valid = i < n;
     const unsigned vm = __ballot_sync(kFull, valid);
     if (valid) {
-      const unsigned d = (unsigned)(keys[i] >> shift) & 0xFFu;
+      const unsigned d = (unsigned)(keys[i] >> shift) & (RD - 1u);
       const unsigned peers = __match_any_sync(vm, d);
       if (lane == __ffs(peers) - 1) atomicAdd(&h[d], (uint32_t)__popc(peers));
     }
   }
   __syncthreads();
-  hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+  for (int d = threadIdx.x; d < RD; d += RS_THREADS) hist[(int64_t)d * ntiles + blockIdx.x] = h[d];
 }
 
 // One CTA per digit: exclusive scan of hist[d * ntiles + 0 .. ntiles) in
@@ -124,21 +126,29 @@ radix_scan_tiles(uint32_t* __restrict__ hist, int64_t ntiles, uint32_t* __restri
 // Stable scatter of one tile.  Warp w owns tile items [w*512, (w+1)*512),
 // walked 32 at a time in order; ranks within a round come from
 // __match_any_sync, across rounds/warps/tiles/digits from the prefix sums.
+template <int RD>
 __global__ void __launch_bounds__(RS_THREADS)
 radix_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
               uint64_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift,
               const uint32_t* __restrict__ hist, int64_t ntiles,
               const uint32_t* __restrict__ totals) {
-  __shared__ uint32_t woff[RS_WARPS][256];
+  constexpr int DPT = RD / RS_THREADS;  // digits per thread
+  __shared__ uint32_t woff[RS_WARPS][RD];
   __shared__ uint32_t wsum[RS_WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tid = threadIdx.x;
 
-  // digit base = exclusive scan of totals (256 threads, one digit each)
-  uint32_t dbase;
+  // digit base = exclusive scan of totals; thread tid owns digits
+  // [tid*DPT, tid*DPT + DPT)
+  uint32_t dbase[DPT];
   {
-    const uint32_t x = totals[tid];
-    uint32_t incl = x;
+    uint32_t x[DPT], mine = 0;
+#pragma unroll
+    for (int q = 0; q < DPT; ++q) {
+      x[q] = totals[tid * DPT + q];
+      mine += x[q];
+    }
+    uint32_t incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(kFull, incl, o);
@@ -146,12 +156,18 @@ radix_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin
     }
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    uint32_t before = 0;
-    for (int w = 0; w < warp; ++w) before += wsum[w];
-    dbase = before + incl - x + hist[(int64_t)tid * ntiles + blockIdx.x];
+    uint32_t run = incl - mine;
+    for (int w = 0; w < warp; ++w) run += wsum[w];
+#pragma unroll
+    for (int q = 0; q < DPT; ++q) {
+      dbase[q] = run + hist[(int64_t)(tid * DPT + q) * ntiles + blockIdx.x];
+      run += x[q];
+    }
   }
 #pragma unroll
-  for (int w = 0; w < RS_WARPS; ++w) woff[w][tid] = 0;
+  for (int w = 0; w < RS_WARPS; ++w)
+#pragma unroll
+    for (int q = 0; q < DPT; ++q) woff[w][tid * DPT + q] = 0;
   __syncthreads();
 
   const int64_t wbase = (int64_t)blockIdx.x * RS_TILE + (int64_t)warp * (32 * RS_ITEMS);
@@ -169,19 +185,20 @@ radix_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin
     const bool valid = wbase + j * 32 + lane < n;
     const unsigned vm = __ballot_sync(kFull, valid);
     if (valid) {
-      const unsigned d = (unsigned)(key[j] >> shift) & 0xFFu;
+      const unsigned d = (unsigned)(key[j] >> shift) & (RD - 1u);
       const unsigned peers = __match_any_sync(vm, d);
       if (lane == __ffs(peers) - 1) woff[warp][d] += (uint32_t)__popc(peers);
     }
     __syncwarp();
   }
   __syncthreads();
-  {
-    uint32_t run = dbase;
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) {
+    uint32_t run = dbase[q];
 #pragma unroll
     for (int w = 0; w < RS_WARPS; ++w) {
-      const uint32_t c = woff[w][tid];
-      woff[w][tid] = run;
+      const uint32_t c = woff[w][tid * DPT + q];
+      woff[w][tid * DPT + q] = run;
       run += c;
     }
   }
@@ -193,7 +210,7 @@ radix_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin
     const unsigned vm = __ballot_sync(kFull, valid);
     unsigned d = 0, peers = 0;
     if (valid) {
-      d = (unsigned)(key[j] >> shift) & 0xFFu;
+      d = (unsigned)(key[j] >> shift) & (RD - 1u);
       peers = __match_any_sync(vm, d);
       const uint32_t p = woff[warp][d] + (uint32_t)__popc(peers & lt);
       kout[p] = key[j];
@@ -384,21 +401,32 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   free_dev(d_cols, ctx->stream);
   prof_mark(ctx, "partition: keys + check");
 
+  // LSD passes: 9-bit digits (512 buckets) when that saves a pass over 8-bit
+  // ones (C4: 34 key bits -> 4 passes instead of 5)
   const int total_bits = rbits + cbits + bbits;
-  const int passes = (total_bits + 7) / 8;
+  const bool wide = (total_bits + 8) / 9 < (total_bits + 7) / 8;
+  const int dbits = wide ? 9 : 8, RD = 1 << dbits;
+  const int passes = (total_bits + dbits - 1) / dbits;
   const size_t NK = (size_t)(nnz > 0 ? nnz : 1);  // kept entries
   const int64_t ntiles = (nnz + RS_TILE - 1) / RS_TILE;
   if (passes > 0 && nnz > 1) {
     PCK(dmalloc(&kb, NK * 8, ctx->stream));
     PCK(dmalloc(&ib, NK * 4, ctx->stream));
-    PCK(dmalloc(&hist, (size_t)256 * ntiles * 4, ctx->stream));
-    PCK(dmalloc(&tot, 256 * 4, ctx->stream));
+    PCK(dmalloc(&hist, (size_t)RD * ntiles * 4, ctx->stream));
+    PCK(dmalloc(&tot, RD * 4, ctx->stream));
     for (int p = 0; p < passes; ++p) {
-      const int shift = 8 * p;
-      radix_hist<<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, nnz, shift, ntiles, hist);
-      radix_scan_tiles<<<256, 1024, 0, s>>>(hist, ntiles, tot);
-      radix_scatter<<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, ia, kb, ib, nnz, shift, hist,
-                                                            ntiles, tot);
+      const int shift = dbits * p;
+      if (wide) {
+        radix_hist<512><<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, nnz, shift, ntiles, hist);
+        radix_scan_tiles<<<512, 1024, 0, s>>>(hist, ntiles, tot);
+        radix_scatter<512><<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, ia, kb, ib, nnz, shift,
+                                                                   hist, ntiles, tot);
+      } else {
+        radix_hist<256><<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, nnz, shift, ntiles, hist);
+        radix_scan_tiles<<<256, 1024, 0, s>>>(hist, ntiles, tot);
+        radix_scatter<256><<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, ia, kb, ib, nnz, shift,
+                                                                   hist, ntiles, tot);
+      }
       PCK(cudaGetLastError());
       uint64_t* tk = ka; ka = kb; kb = tk;
       uint32_t* ti = ia; ia = ib; ib = ti;
