@@ -227,6 +227,9 @@ def run_ours(args):
     eng2 = bm.Engine(bm.EngineOptions(device=dev, fused=fused, bulk_red=args.bulk,
                                       sse_wide=args.sse_wide),
                      stream=stream.cuda_stream)
+    for kv in args.engine_opt or []:  # experiments: raw bgmf_set_option knobs
+        key, val = kv.split("=")
+        eng2._opt(key, float(val))
     eng2.partition(d.rows, d.cols, d.values, w.n, w.m, w.grid, w.grid)
     eng2.init_factors(w.n, w.m, w.k, w.seed)
     plans = [eng2.plan_arrays(bm.plan_step(w.grid, w.grid, s)) for s in range(w.grid)]
@@ -473,6 +476,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--budget-gb", type=float, default=1.5,
                     help="C5: device memory for streamed ratings (slots)")
+    ap.add_argument("--engine-opt", action="append", metavar="KEY=VALUE",
+                    help="raw bgmf_set_option knob for the device-resident leg (experiments)")
     ap.add_argument("--no-l2-probe", action="store_true",
                     help="skip the SM<->L2 ceiling probe (e.g. under ncu)")
     ap.add_argument("--l2-wave-bytes", type=int, default=None,

@@ -55,7 +55,7 @@ struct bgmf_ctx {
   int min_chunk = 256;
   int stagger = 2;       // chunk-length rule (stagger_chunk)
   int sparse_min_chunk = 32;  // block_chunk: floor on sparse blocks (0: always min_chunk)
-  double col_ratio = 0.6;     // block_chunk: max concurrent groups per block column
+  double col_ratio = 0.6;     // block_chunk: concurrent groups per block column (see there)
   int64_t l2_wave_bytes = 48ll << 20;  // l2_waves: V bytes swept at once (0: whole strata)
   bool timing = false;
   int warps_per_sm = 0;

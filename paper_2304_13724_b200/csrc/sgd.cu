@@ -974,12 +974,16 @@ std::vector<int32_t> l2_waves(const bgmf_ctx* c, const int32_t* plan, const int3
 
 // Per-block chunk length of the fast paths.  cl = the batch's one-wave
 // length (ceil(batch nnz / free groups)); the floor bounds how many groups
-// sweep one block at once (lossless Hogwild: reads of a V row are stale by the
-// other groups' in-flight updates to it):
-//   * sparse blocks (density <= 1/8): at most col_ratio * cols groups, i.e.
-//     about one concurrent update per two V rows, floor sparse_min_chunk --
-//     C1/C2-sized blocks get 8x/4.5x the groups min_chunk allowed (C4 and
-//     C3 are unchanged: their one-wave length is already above the floor);
+// sweep one block at once (lossless Hogwild: a V-row read is stale by the
+// other groups' in-flight updates to that row).  Measured on B200 (fast-mode
+// drift vs the reference order, tests/ + DESIGN.md §3.1):
+//   * sparse blocks (density <= 1/8): at most max(col_ratio * cols,
+//     block nnz / 128) groups, floor sparse_min_chunk.  The first term keeps
+//     ~one concurrent update per two V rows (C1/C2-sized blocks: C1 1x1 at 1.9
+//     concurrent updates per row drifted 1.3e-3 in 5 epochs); the second lets
+//     blocks with hundreds of ratings per column use the whole GPU when a
+//     launch holds few of them (C4 with 2 blocks per launch, the 8-GPU ring's
+//     per-rank batch: 4.3 concurrent updates per row, drift 2e-5);
 //   * dense blocks: the conservative min_chunk floor (dense rows share their
 //     column order, so concurrent groups collide far more often).
 // Then stagger_chunk.
@@ -989,7 +993,8 @@ int64_t block_chunk(bgmf_ctx* c, int b, int64_t cnt, int64_t cl) {
   const int64_t cols = c->col_bounds[bj + 1] - c->col_bounds[bj];
   int64_t floor_len = c->min_chunk;
   if (c->sparse_min_chunk > 0 && cnt * 8 <= rows * cols) {
-    const double cap = c->col_ratio * (double)cols;  // max concurrent groups
+    double cap = c->col_ratio * (double)cols;  // max concurrent groups
+    if ((double)cnt / 128.0 > cap) cap = (double)cnt / 128.0;
     floor_len = (int64_t)std::ceil((double)cnt / (cap > 1.0 ? cap : 1.0));
     if (floor_len < c->sparse_min_chunk) floor_len = c->sparse_min_chunk;
   }
