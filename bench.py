@@ -147,7 +147,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    w, r, c, v, _ = make_workload(args.config, args.nnz)
+    nnz = args.nnz
+    if args.config == "C5" and nnz is None:
+        nnz = 20_000_000  # the 2 B-rating C5 set would need 48 GB of host arrays
+    w, r, c, v, _ = make_workload(args.config, nnz)
     threads = min(os.cpu_count() or 1, w.grid)
     ref = CpuReference(w, r, c, v)
     rates = []
@@ -157,7 +160,8 @@ def run_reference(args):
             rates.append(rate)
     value = float(np.median(rates))
     sample = (f"{nb} of {ntot} strata of a {args.config} epoch per step "
-              f"({updates} rating updates), oracle C port, {threads} threads")
+              f"({updates} rating updates of {len(r)} ratings), oracle C port, "
+              f"{threads} threads")
     line = {
         "impl": "reference", "metric": "SGD rating-updates/sec (epoch)", "value": value,
         "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
