@@ -39,10 +39,19 @@ __global__ void __launch_bounds__(256) l2_probe_kernel(float* __restrict__ V, ui
 #pragma unroll
       for (int q = 0; q < V4; ++q) v[d][q] = MODE == 2 ? make_float4(1e-30f, 0.f, 0.f, 0.f)
                                                        : __ldcg(row + q * L + gl);
+      if (MODE == 3) {  // a second, independent row read (the SSE's) per rating
+        const uint32_t c2 = mix32((uint32_t)(t0 + d) ^ 0x5bd1e995u) % rows;
+        const float4* row2 = reinterpret_cast<const float4*>(V + (int64_t)c2 * (4 * L * V4));
+#pragma unroll
+        for (int q = 0; q < V4; ++q) {
+          const float4 w = __ldcg(row2 + q * L + gl);
+          v[d][q].x += w.x; v[d][q].y += w.y; v[d][q].z += w.z; v[d][q].w += w.w;
+        }
+      }
     }
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      if (MODE >= 1) {
+      if (MODE == 1 || MODE == 2 || MODE == 3) {
         const uint32_t c = mix32((uint32_t)(t0 + d) ^ 0x9e3779b9u) % rows;
         float* row = V + (int64_t)c * (4 * L * V4);
 #pragma unroll
@@ -69,7 +78,7 @@ using namespace bgmf;
 
 extern "C" int bgmf_probe_l2(int device, int64_t rows, int64_t ratings, int mode,
                              int ctas_per_sm, double* ms_out) {
-  if (!ms_out || rows < 1 || rows > 0x7fffffff || ratings < 1 || mode < 0 || mode > 2)
+  if (!ms_out || rows < 1 || rows > 0x7fffffff || ratings < 1 || mode < 0 || mode > 3)
     return fail(nullptr, BGMF_ERR_ARG, "bgmf_probe_l2: bad argument");
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
@@ -89,7 +98,8 @@ extern "C" int bgmf_probe_l2(int device, int64_t rows, int64_t ratings, int mode
     cudaEventRecord(a);
     if (mode == 0) l2_probe_kernel<0><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
     else if (mode == 1) l2_probe_kernel<1><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
-    else l2_probe_kernel<2><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
+    else if (mode == 2) l2_probe_kernel<2><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
+    else l2_probe_kernel<3><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
     cudaEventRecord(b);
     e = cudaEventSynchronize(b);
     float ms = 0.f;

@@ -11,8 +11,8 @@ from paper_2304_13724_b200 import _native as N  # noqa: E402
 L = N.load()
 rows, ratings = 17800, 50_000_000
 out = {}
-for mode, name, bpr in ((0, "read", 512), (1, "read+red", 1024), (2, "red", 512)):
-    for cps in (1, 2, 3, 4):
+for mode, name, bpr in ((0, "read", 512), (1, "read+red", 1024), (2, "red", 512), (3, "2read+red", 1536)):
+    for cps in (2, 4):
         ms = ctypes.c_double()
         N.check(L.bgmf_probe_l2(0, rows, ratings, mode, cps, ctypes.byref(ms)))
         gbs = ratings * bpr / (ms.value / 1e3) / 1e9
