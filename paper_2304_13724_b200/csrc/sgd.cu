@@ -977,13 +977,14 @@ std::vector<int32_t> l2_waves(const bgmf_ctx* c, const int32_t* plan, const int3
 // sweep one block at once (lossless Hogwild: a V-row read is stale by the
 // other groups' in-flight updates to that row).  Measured on B200 (fast-mode
 // drift vs the reference order, tests/ + DESIGN.md §3.1):
-//   * sparse blocks (density <= 1/8): at most max(col_ratio * cols,
-//     block nnz / 128) groups, floor sparse_min_chunk.  The first term keeps
-//     ~one concurrent update per two V rows (C1/C2-sized blocks: C1 1x1 at 1.9
-//     concurrent updates per row drifted 1.3e-3 in 5 epochs); the second lets
-//     blocks with hundreds of ratings per column use the whole GPU when a
-//     launch holds few of them (C4 with 2 blocks per launch, the 8-GPU ring's
-//     per-rank batch: 4.3 concurrent updates per row, drift 2e-5);
+//   * sparse blocks (density <= 1/8): at most cols * max(col_ratio,
+//     (ratings per column - 32) / 80) groups, floor sparse_min_chunk.  The
+//     first term keeps ~one concurrent update per two V rows on blocks with
+//     few ratings per column (C1 1x1, 59 per column: 1.9 concurrent updates
+//     per row drifted 1.3e-3 in 5 epochs); the second lets blocks with
+//     hundreds of ratings per column use the whole GPU when a launch holds few
+//     of them (C4, 351 per column, with 2 blocks per launch as each rank of the
+//     8-GPU ring runs: ~4 concurrent updates per row, drift 2e-5);
 //   * dense blocks: the conservative min_chunk floor (dense rows share their
 //     column order, so concurrent groups collide far more often).
 // Then stagger_chunk.
@@ -993,8 +994,12 @@ int64_t block_chunk(bgmf_ctx* c, int b, int64_t cnt, int64_t cl) {
   const int64_t cols = c->col_bounds[bj + 1] - c->col_bounds[bj];
   int64_t floor_len = c->min_chunk;
   if (c->sparse_min_chunk > 0 && cnt * 8 <= rows * cols) {
-    double cap = c->col_ratio * (double)cols;  // max concurrent groups
-    if ((double)cnt / 128.0 > cap) cap = (double)cnt / 128.0;
+    // max concurrent groups: col_ratio per column, more when the block has many
+    // ratings per column (each stale V read is then a smaller perturbation)
+    const double per_col = (double)cnt / (double)(cols > 0 ? cols : 1);
+    double ratio = (per_col - 32.0) / 80.0;
+    if (ratio < c->col_ratio) ratio = c->col_ratio;
+    const double cap = ratio * (double)cols;
     floor_len = (int64_t)std::ceil((double)cnt / (cap > 1.0 ? cap : 1.0));
     if (floor_len < c->sparse_min_chunk) floor_len = c->sparse_min_chunk;
   }
