@@ -373,6 +373,9 @@ def run_out_of_core(args, dev):
     stream = torch.cuda.current_stream()
     eng = bm.Engine(bm.EngineOptions(device=dev, fused=False, l2_wave_bytes=args.l2_wave_bytes),
                     stream=stream.cuda_stream)
+    for kv in args.engine_opt or []:  # experiments: raw bgmf_set_option knobs
+        key, val = kv.split("=")
+        eng._opt(key, float(val))
     t0 = time.perf_counter()
     N.check(eng._L.bgmf_synth_partition(eng._h, w.n, w.m, nnz, w.seed, w.grid, w.grid), eng._h)
     t_part = time.perf_counter() - t0
