@@ -184,7 +184,8 @@ int grad_upload(bgmf_ctx* c, GradBufs& b, const int64_t* rows, const int64_t* co
   return BGMF_OK;
 }
 
-size_t grad_smem(int k) { return (size_t)k * sizeof(double); }
+// k products, padded: thread 0 reads them back with vectorised shared loads
+size_t grad_smem(int k) { return ((size_t)k + 2) * sizeof(double); }
 
 }  // namespace
 
