@@ -237,8 +237,22 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
     cnt = torch.tensor(shard.counts, dtype=torch.int64, device=f"cuda:{device}")
     dist.all_reduce(cnt)
     total_counts[:] = cnt.cpu().numpy()
+    from .core import AdaptiveDecreasing
+
+    adaptive = isinstance(cfg.inner_schedule, AdaptiveDecreasing)
+    hist = [0.0]
+    if adaptive and int(total_counts.sum()):
+        # RMSE of the initial factors over all ranks' ratings (trainer.py:98-100)
+        s0 = torch.tensor([shard.eng.train_sse()], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(s0)
+        hist = [math.sqrt(float(s0.item()) / int(total_counts.sum()))]
     for step in range(1, cfg.outer_steps + 1):
-        g = resolve_inner_iters(cfg.inner_schedule, step, 1.0)
+        if adaptive and step >= 2:
+            prev, cur = hist[-2], hist[-1]
+            ratio = (prev - cur) / prev if prev > 0 else 0.0
+        else:
+            ratio = 1.0
+        g = resolve_inner_iters(cfg.inner_schedule, step, ratio)
         if g is None:
             raise NotImplementedError("converge schedules are single-GPU (train_blocked)")
         t0 = time.perf_counter()
@@ -271,6 +285,7 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
             test_rmse = math.sqrt(float(hs.item()) / len(evaluator.test))
         trace.append(TraceStep(step, train_rmse, test_rmse,
                                time.perf_counter() - t0 if timing else 0.0, g, 0))
+        hist.append(train_rmse)
         if early_stop:
             if acc.count == 0:
                 stop = "converged"

@@ -87,3 +87,29 @@ def test_async_step_matches_run_step():
     assert bad is not None and bad[0] == first[0] * P + first[1]
     with pytest.raises(RuntimeError, match="step_begin"):
         eng.step_batch(ids, off, 1, 1e-3, 1e-2)  # no step_begin
+
+
+def test_world1_nccl_adaptive_schedule_matches_oracle():
+    """AdaptiveDecreasing in the ring trainer: the inner-iteration count
+    follows the improvement ratio of the global trace (trainer.py:52-73)."""
+    import torch.distributed as dist
+
+    from paper_2304_13724_b200 import distributed as D
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
+                      WORLD_SIZE="1", LOCAL_RANK="0")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        r, c, v = workloads.lowrank(6040, 3706, 300_000, seed=7)
+        d = bm.RatingsDataset(6040, 3706, r, c, v)
+        cfg = bm.TrainConfig(k=32, outer_steps=4, grid_i=8, grid_j=8, alpha=1e-3,
+                             inner_schedule=bm.AdaptiveDecreasing(4))
+        _, trace, _ = D.train_blocked_distributed(d, cfg, early_stop=False)
+        _, _, otr, _ = O.train_blocked(d.n, d.m, d.rows, d.cols, d.values, k=32, outer_steps=4,
+                                       alpha=1e-3, grid_i=8, grid_j=8, schedule="adaptive:4",
+                                       early_stop=False, nthreads=8)
+        assert [s.inner_iters for s in trace] == [s["inner_iters"] for s in otr]
+        got = np.array([s.train_rmse for s in trace])
+        assert np.abs(got - [s["train_rmse"] for s in otr]).max() <= 1e-3
+    finally:
+        dist.destroy_process_group()
