@@ -136,6 +136,35 @@ def run_epoch(sched: RingSchedule, shard, rank: int, dist, step0: int, g: int,
     return sse_all, order, bad_any
 
 
+def _run_epoch_converge(sched: RingSchedule, shard, rank: int, dist, step0: int, tol: float,
+                        alpha: float, beta: float, nb: int, J: int):
+    """run_epoch for ConvergeEachBlock: each stratum's local blocks sweep until
+    their RMSE improves by < tol (cap CONVERGE_CAP, _kernels.py:62-100);
+    synchronous per batch.  Also returns every local block's sweep count and
+    the number of capped blocks."""
+    from .kernel import CONVERGE_CAP
+
+    sse_all = np.zeros(nb, np.float64)
+    order: list[int] = []
+    bad_any = None
+    iters_used = []
+    capped = 0
+    for batch in sched.batches(step0):
+        exchange(sched.transfers_for(batch), rank, shard.v_slice, dist)
+        order.extend(bi * J + bj for bi, bj in batch)
+        mine = sched.local_blocks(batch, rank)
+        if mine:
+            ids, off = shard.eng.plan_arrays([mine])
+            sse, its, cap, bad = shard.eng.run_step_converge(ids, off, tol, CONVERGE_CAP, alpha,
+                                                             beta)
+            sse_all[ids] = sse[ids]
+            iters_used.extend(int(its[b]) for b in ids)
+            capped += int(sum(int(cap[b]) for b in ids))
+            if bad is not None and bad_any is None:
+                bad_any = (int(ids[bad[0]]), bad[1], bad[2])
+    return sse_all, order, bad_any, np.array(iters_used, np.int64), capped
+
+
 # ---------------------------------------------------------------------------- GPU
 
 
@@ -203,7 +232,7 @@ def _init_dist():
 
 def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, options=None,
                               timing: bool = True):
-    """Multi-GPU train_blocked (fixed inner schedules): every rank calls it with
+    """Multi-GPU train_blocked (every inner schedule): every rank calls it with
     the same dataset, test set and config; rank r uses GPU LOCAL_RANK.  The
     per-step test RMSE (HoldoutEvaluator semantics, metrics.py:55-81) is
     computed where U lives: each rank evaluates the test entries of its own
@@ -253,11 +282,22 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
         else:
             ratio = 1.0
         g = resolve_inner_iters(cfg.inner_schedule, step, ratio)
-        if g is None:
-            raise NotImplementedError("converge schedules are single-GPU (train_blocked)")
         t0 = time.perf_counter()
-        sse_all, order, bad_any = run_epoch(sched, shard, rank, dist, step - 1, g, cfg.alpha,
-                                            cfg.beta, nb, cfg.grid_j)
+        max_iters, capped = g, 0
+        if g is None:  # converge-each-block: per-block sweep counts, synchronous batches
+            sse_all, order, bad_any, its, cap = _run_epoch_converge(
+                sched, shard, rank, dist, step - 1, cfg.inner_schedule.tol, cfg.alpha, cfg.beta,
+                nb, cfg.grid_j)
+            agg = torch.tensor([float(its.max()) if len(its) else 0.0, float(cap)],
+                               dtype=torch.float64, device=f"cuda:{device}")
+            mx = agg[:1].clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            sm = agg[1:].clone()
+            dist.all_reduce(sm)
+            max_iters, capped = int(mx.item()), int(sm.item())
+        else:
+            sse_all, order, bad_any = run_epoch(sched, shard, rank, dist, step - 1, g, cfg.alpha,
+                                                cfg.beta, nb, cfg.grid_j)
         red = torch.tensor(sse_all, device=f"cuda:{device}")
         dist.all_reduce(red)
         sse_all = red.cpu().numpy()
@@ -268,7 +308,7 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
                                                     if not math.isfinite(sse_all[o])))
             err = divergence(b // cfg.grid_j, b % cfg.grid_j,
                              bad_any[1] if bad_any else int(total_counts[b]) - 1,
-                             bad_any[2] if bad_any else g - 1)
+                             bad_any[2] if bad_any else (g or 1) - 1)
             err.step = step
             err.partial_trace = trace
             raise err
@@ -284,7 +324,7 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
             dist.all_reduce(hs)
             test_rmse = math.sqrt(float(hs.item()) / len(evaluator.test))
         trace.append(TraceStep(step, train_rmse, test_rmse,
-                               time.perf_counter() - t0 if timing else 0.0, g, 0))
+                               time.perf_counter() - t0 if timing else 0.0, max_iters, capped))
         hist.append(train_rmse)
         if early_stop:
             if acc.count == 0:

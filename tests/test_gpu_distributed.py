@@ -113,3 +113,29 @@ def test_world1_nccl_adaptive_schedule_matches_oracle():
         assert np.abs(got - [s["train_rmse"] for s in otr]).max() <= 1e-3
     finally:
         dist.destroy_process_group()
+
+
+def test_world1_nccl_converge_schedule_matches_oracle():
+    """ConvergeEachBlock in the ring trainer: per-block sweep counts and
+    capped blocks reduced over the ranks, trace within 1e-3 of the oracle."""
+    import torch.distributed as dist
+
+    from paper_2304_13724_b200 import distributed as D
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
+                      WORLD_SIZE="1", LOCAL_RANK="0")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        d = bm.gen_synthetic(bm.SyntheticSpec(64, 64, 1, 30, seed=0))
+        cfg = bm.TrainConfig(k=10, outer_steps=2, grid_i=4, grid_j=4,
+                             inner_schedule=bm.ConvergeEachBlock(0.5))
+        _, trace, _ = D.train_blocked_distributed(d, cfg, early_stop=False,
+                                                  options=bm.EngineOptions(min_chunk=1 << 20))
+        _, _, otr, _ = O.train_blocked(d.n, d.m, d.rows, d.cols, d.values, k=10, outer_steps=2,
+                                       grid_i=4, grid_j=4, schedule="converge:0.5",
+                                       early_stop=False)
+        got = np.array([s.train_rmse for s in trace])
+        assert np.abs(got - [s["train_rmse"] for s in otr]).max() <= 1e-3
+        assert all(s.inner_iters >= 1 for s in trace)
+    finally:
+        dist.destroy_process_group()
