@@ -130,6 +130,13 @@ int bgmf_set_factors(bgmf_ctx* ctx, const double* u, const double* v,
 /* Download the factors into caller fp64 buffers (n x k, m x k). */
 int bgmf_get_factors(bgmf_ctx* ctx, double* u, double* v);
 
+/* Zero-fill a caller-owned host buffer with one write per 4 KiB page (OpenMP
+ * threads), faulting its pages in.  Thread-safe and context-free: the
+ * trainer runs it on a side thread over the not-yet-written fp64 factor
+ * arrays while the epochs run, so bgmf_get_factors's widening does not pay
+ * first-touch page faults. */
+int bgmf_host_prefault(void* p, int64_t bytes);
+
 /* init_factors on the device (core.py:179-193), bit-identical to numpy:
  * draws of the PCG64 stream whose seeded 128-bit (state, inc) -- numpy's
  * default_rng(seed).bit_generator.state -- are passed as hi/lo halves;

@@ -47,6 +47,7 @@ SIGNATURES = {
     "bgmf_synth": (_i, [_l, _l, _l, _l, ctypes.c_uint64, _i64p, _i64p, _f64p]),
     "bgmf_set_factors": (_i, [_ctx, _f64p, _f64p, _l, _l, _i]),
     "bgmf_get_factors": (_i, [_ctx, _f64p, _f64p]),
+    "bgmf_host_prefault": (_i, [ctypes.c_void_p, ctypes.c_int64]),
     "bgmf_init_factors": (_i, [_ctx, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                ctypes.c_uint64, _l, _l, _i]),
     "bgmf_bind_factors": (_i, [_ctx, _vp, _vp, _l, _l, _i, _i]),

@@ -201,6 +201,9 @@ int64_t staged_upload(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                       int32_t* d_c, void* d_v, bool v64, int* rc, int64_t row_lo,
                       int64_t row_hi, int64_t* kept);
 int download_rows(bgmf_ctx* c, const float* d, double* h, int64_t rows, int k, int kp);
+// process-wide cache of small pinned host buffers (hostio.cu)
+cudaError_t pinned_alloc(void** p, size_t bytes);
+void pinned_free(void* p);
 int upload_rows(bgmf_ctx* c, const double* h, float* d, int64_t rows, int k, int kp);
 
 // synth.cu (benchmark / test input generator)

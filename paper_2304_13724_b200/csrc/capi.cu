@@ -187,9 +187,9 @@ void bgmf_destroy(bgmf_ctx* c) {
   dfree(c->d_priv, c->stream);
   cudaStreamSynchronize(c->stream);
   prof_mark(c, "destroy: device frees");
-  if (c->h_work) cudaFreeHost(c->h_work);
-  if (c->h_sse) cudaFreeHost(c->h_sse);
-  if (c->h_bad) cudaFreeHost(c->h_bad);
+  pinned_free(c->h_work);
+  pinned_free(c->h_sse);
+  pinned_free(c->h_bad);
   prof_mark(nullptr, "destroy: pinned frees");
   for (auto& t : c->events) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -223,7 +223,7 @@ int bgmf_partition(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const 
   cudaSetDevice(c->device);
   if (c->streaming) stream_free(c);
   // the step scratch is sized by the grid
-  dfree(c->d_sse, c->stream); cudaFreeHost(c->h_sse); dfree(c->d_bad, c->stream); cudaFreeHost(c->h_bad);
+  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
   return partition_device(c, rows, cols, vals, nnz, n, m, grid_i, grid_j);
 }
@@ -234,7 +234,7 @@ int bgmf_partition_rows(bgmf_ctx* c, const int64_t* rows, const int64_t* cols,
   if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
   cudaSetDevice(c->device);
   if (c->streaming) stream_free(c);
-  dfree(c->d_sse, c->stream); cudaFreeHost(c->h_sse); dfree(c->d_bad, c->stream); cudaFreeHost(c->h_bad);
+  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
   return partition_device(c, rows, cols, vals, nnz, n, m, grid_i, grid_j, false, row_lo, row_hi);
 }
@@ -246,7 +246,7 @@ int bgmf_synth_partition(bgmf_ctx* c, int64_t n, int64_t m, int64_t nnz, uint64_
     return fail(c, BGMF_ERR_ARG, "bad synthetic shape");
   cudaSetDevice(c->device);
   if (c->streaming) stream_free(c);
-  dfree(c->d_sse, c->stream); cudaFreeHost(c->h_sse); dfree(c->d_bad, c->stream); cudaFreeHost(c->h_bad);
+  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
   const size_t N = (size_t)(nnz > 0 ? nnz : 1);
   int64_t *r = nullptr, *q = nullptr;

@@ -15,8 +15,11 @@
 // device types in the staging buffer while the DMA engine moves the other one.
 
 #include <omp.h>
+#include <sys/mman.h>
 
+#include <map>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "bgmf_internal.cuh"
@@ -63,6 +66,69 @@ class Stage {
 };
 
 }  // namespace
+
+// Small pinned buffers (the per-context step scratch: work table, per-block
+// SSE, divergence flag) come from a process-wide cache and go back to it on
+// release: cudaFreeHost measured 0.8 ms typically but 300-520 ms at times in
+// a context teardown (profiles/r01_e2e_phases.txt), inside the e2e call.
+// Size classes are powers of two >= 4 KiB; buffers above 64 MiB and a cache
+// above 256 MiB are freed for real.
+namespace {
+constexpr size_t kPinCacheMax = size_t(64) << 20, kPinCacheTotal = size_t(256) << 20;
+struct PinCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_;
+  std::unordered_map<void*, size_t> size_;
+  size_t cached = 0;
+};
+PinCache& pin_cache() {
+  static PinCache* p = new PinCache;  // never destroyed: outlives static teardown
+  return *p;
+}
+size_t pin_class(size_t bytes) {
+  size_t c = 4096;
+  while (c < bytes) c <<= 1;
+  return c;
+}
+}  // namespace
+
+cudaError_t pinned_alloc(void** p, size_t bytes) {
+  const size_t cls = pin_class(bytes ? bytes : 1);
+  PinCache& pc = pin_cache();
+  {
+    std::lock_guard<std::mutex> lk(pc.mu);
+    auto it = pc.free_.find(cls);
+    if (it != pc.free_.end()) {
+      *p = it->second;
+      pc.free_.erase(it);
+      pc.cached -= cls;
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaMallocHost(p, cls);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(pc.mu);
+    pc.size_[*p] = cls;
+  }
+  return e;
+}
+
+void pinned_free(void* p) {
+  if (!p) return;
+  PinCache& pc = pin_cache();
+  {
+    std::lock_guard<std::mutex> lk(pc.mu);
+    auto it = pc.size_.find(p);
+    if (it != pc.size_.end() && it->second <= kPinCacheMax &&
+        pc.cached + it->second <= kPinCacheTotal) {
+      pc.free_.emplace(it->second, p);
+      pc.cached += it->second;
+      return;
+    }
+    if (it != pc.size_.end()) pc.size_.erase(it);
+  }
+  cudaFreeHost(p);
+}
 
 // Dataset upload for the partitioner (partition.cu): int64 indices narrowed
 // to int32 (and range-checked against n x m), fp64 values narrowed to fp32
@@ -227,3 +293,24 @@ int upload_rows(bgmf_ctx* c, const double* h, float* d, int64_t rows, int k, int
 }
 
 }  // namespace bgmf
+
+// Faults in (and zero-fills) a fresh host buffer, one write per 4 KiB page.  The model download widens into freshly allocated
+// numpy arrays; first-touch page faults made it run at 25-35 GB/s
+// (profiles/r01_host_probe.txt), so the trainer faults the output buffers in
+// on a side thread while the epochs run on the GPU.
+// The interior 2 MiB-aligned span is advised MADV_HUGEPAGE first (this
+// host's THP mode is "madvise"): 512x fewer faults, and fewer TLB misses for
+// the widening writes.  Four threads: the epochs' launch thread keeps a core.
+extern "C" int bgmf_host_prefault(void* p, int64_t bytes) {
+  if (!p || bytes <= 0) return BGMF_OK;
+  char* c = static_cast<char*>(p);
+  const uintptr_t huge = uintptr_t(2) << 20;
+  const uintptr_t a = ((uintptr_t)c + huge - 1) & ~(huge - 1);
+  const uintptr_t b = ((uintptr_t)c + (uintptr_t)bytes) & ~(huge - 1);
+  if (b > a) madvise(reinterpret_cast<void*>(a), b - a, MADV_HUGEPAGE);
+  const int64_t pages = (bytes + 4095) / 4096;
+#pragma omp parallel for schedule(static) num_threads(4)
+  for (int64_t q = 0; q < pages; ++q) c[q * 4096] = 0;
+  return BGMF_OK;
+}
+

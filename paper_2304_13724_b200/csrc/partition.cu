@@ -6,15 +6,22 @@
 // np.lexsort((cols, rows, block_id)) -- (block, row, col), ties in input
 // order.  Here:
 //   1. make_keys: closed-form slab index (first n % P slabs are one longer),
-//      one 64-bit key per rating = block | local row | local col, payload =
-//      source index.  Within a block, (local row, local col) orders exactly
-//      like (row, col).
-//   2. LSD radix sort, 8-bit digits, stable (hist -> per-digit tile scan ->
-//      warp-ranked stable scatter with __match_any_sync), so duplicate cells
-//      keep input order like lexsort.
-//   3. decode: local coords from the key, fp64 value gathered by source index
-//      (fp32 copy for the fast kernels), block offsets by binary search.
-// HBM-bound integer work: every pass streams key+index (12 B/rating) in and
+//      one 64-bit key per rating = block | local row | local col.  Within a
+//      block, (local row, local col) orders exactly like (row, col).  When the
+//      source index fits in the key's spare low bits (fast mode: C1-C4) it is
+//      appended there and the fp32 value rides along as the payload, so the
+//      sort needs no gather afterwards; otherwise the payload is the index.
+//   2. LSD radix sort over the key bits, 8- or 9-bit digits, stable: tile
+//      histogram (shared-memory atomics) -> per-digit tile scan -> scatter.
+//      The scatter ranks a tile's items per warp (__match_any_sync, in
+//      order), lays the tile out digit-major in shared memory and writes each
+//      digit's run contiguously, so global stores are coalesced runs instead
+//      of one scattered 8 B store per lane.  Duplicate cells keep input order
+//      like lexsort.
+//   3. decode: local coords from the key (and the source index from its low
+//      bits, or the fp64/fp32 value gathered by source index when it is the
+//      payload), block offsets by binary search.
+// HBM-bound integer work: every pass streams key+payload (12 B/rating) in and
 // out; grid sized to tiles of 4096 ratings.
 
 #include "bgmf_internal.cuh"
@@ -29,22 +36,27 @@ constexpr int RS_WARPS = RS_THREADS / 32;
 
 __device__ __forceinline__ int64_t slab_index(int64_t x, int64_t base, int64_t extra) {
   const int64_t big = extra * (base + 1);
+  if (x < (int64_t)UINT32_MAX && base < (int64_t)UINT32_MAX)  // 32-bit divides
+    return x < big ? (uint32_t)x / (uint32_t)(base + 1)
+                   : extra + (uint32_t)(x - big) / (uint32_t)base;
   return x < big ? x / (base + 1) : extra + (x - big) / base;
 }
 __device__ __forceinline__ int64_t slab_start(int64_t s, int64_t base, int64_t extra) {
   return s * base + (s < extra ? s : extra);
 }
 
+// payload: the source index, or (embed) the fp32 value's bits with the index
+// in the key's low ibits.
 template <typename IT>
 __global__ void make_keys(const IT* __restrict__ rows, const IT* __restrict__ cols,
                           int64_t nnz, int64_t n, int64_t m, int64_t rbase, int64_t rextra,
-                          int64_t cbase, int64_t cextra, int J, int rbits, int cbits,
-                          uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
-                          unsigned long long* __restrict__ bad) {
+                          int64_t cbase, int64_t cextra, int J, int rbits, int cbits, int ibits,
+                          const float* __restrict__ vals32, uint64_t* __restrict__ keys,
+                          uint32_t* __restrict__ payload, unsigned long long* __restrict__ bad) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = (int64_t)rows[i], c = (int64_t)cols[i];
-    idx[i] = (uint32_t)i;
+    payload[i] = vals32 ? __float_as_uint(vals32[i]) : (uint32_t)i;
     if (r < 0 || r >= n || c < 0 || c >= m) {
       atomicMin(bad, (unsigned long long)i);
       keys[i] = 0;
@@ -54,7 +66,8 @@ __global__ void make_keys(const IT* __restrict__ rows, const IT* __restrict__ co
     const int64_t bj = slab_index(c, cbase, cextra);
     const uint64_t lr = (uint64_t)(r - slab_start(bi, rbase, rextra));
     const uint64_t lc = (uint64_t)(c - slab_start(bj, cbase, cextra));
-    keys[i] = ((uint64_t)(bi * J + bj) << (rbits + cbits)) | (lr << cbits) | lc;
+    const uint64_t key = ((uint64_t)(bi * J + bj) << (rbits + cbits)) | (lr << cbits) | lc;
+    keys[i] = (key << ibits) | (ibits ? (uint64_t)i : 0ull);
   }
 }
 
@@ -67,19 +80,17 @@ radix_hist(const uint64_t* __restrict__ keys, int64_t n, int shift, int64_t ntil
   __shared__ uint32_t h[RD];
   for (int d = threadIdx.x; d < RD; d += RS_THREADS) h[d] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * RS_TILE;
-#pragma unroll 4
+  uint64_t k[RS_ITEMS];
+#pragma unroll
   for (int j = 0; j < RS_ITEMS; ++j) {
     const int64_t i = base + (int64_t)j * RS_THREADS + threadIdx.x;
-    const bool valid = i < n;
-    const unsigned vm = __ballot_sync(kFull, valid);
-    if (valid) {
-      const unsigned d = (unsigned)(keys[i] >> shift) & (RD - 1u);
-      const unsigned peers = __match_any_sync(vm, d);
-      if (lane == __ffs(peers) - 1) atomicAdd(&h[d], (uint32_t)__popc(peers));
-    }
+    k[j] = i < n ? __ldcs(keys + i) : ~0ull;
   }
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j)
+    if (base + (int64_t)j * RS_THREADS + threadIdx.x < n)
+      atomicAdd(&h[(unsigned)(k[j] >> shift) & (RD - 1u)], 1u);
   __syncthreads();
   for (int d = threadIdx.x; d < RD; d += RS_THREADS) hist[(int64_t)d * ntiles + blockIdx.x] = h[d];
 }
@@ -124,8 +135,17 @@ radix_scan_tiles(uint32_t* __restrict__ hist, int64_t ntiles, uint32_t* __restri
 }
 
 // Stable scatter of one tile.  Warp w owns tile items [w*512, (w+1)*512),
-// walked 32 at a time in order; ranks within a round come from
-// __match_any_sync, across rounds/warps/tiles/digits from the prefix sums.
+// walked 32 at a time in order; an item's rank among its warp's equal digits
+// comes from __match_any_sync plus a per-(warp, digit) counter.  A CTA scan
+// over (digit, warp) turns those into tile positions (digit-major, stable);
+// the tile is laid out there in shared memory and thread t then writes items
+// t, t+256, ... to global[digit base + tile digit offset + (i - tile digit
+// start)], so each digit's run is stored contiguously.
+template <int RD>
+constexpr size_t scatter_smem() {
+  return (size_t)RS_TILE * 12 + (size_t)RS_WARPS * RD * 4 + (size_t)RD * 4;
+}
+
 template <int RD>
 __global__ void __launch_bounds__(RS_THREADS)
 radix_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
@@ -133,92 +153,114 @@ radix_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin
               const uint32_t* __restrict__ hist, int64_t ntiles,
               const uint32_t* __restrict__ totals) {
   constexpr int DPT = RD / RS_THREADS;  // digits per thread
-  __shared__ uint32_t woff[RS_WARPS][RD];
-  __shared__ uint32_t wsum[RS_WARPS];
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* skey = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* sval = reinterpret_cast<uint32_t*>(skey + RS_TILE);
+  uint32_t* woff = sval + RS_TILE;          // [RS_WARPS][RD]
+  uint32_t* gdst = woff + RS_WARPS * RD;  // [RD], mod 2^32
+  __shared__ uint32_t wsum[2][RS_WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tid = threadIdx.x;
+  const int64_t tbase = (int64_t)blockIdx.x * RS_TILE;
 
-  // digit base = exclusive scan of totals; thread tid owns digits
-  // [tid*DPT, tid*DPT + DPT)
-  uint32_t dbase[DPT];
-  {
-    uint32_t x[DPT], mine = 0;
-#pragma unroll
-    for (int q = 0; q < DPT; ++q) {
-      x[q] = totals[tid * DPT + q];
-      mine += x[q];
-    }
-    uint32_t incl = mine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    uint32_t run = incl - mine;
-    for (int w = 0; w < warp; ++w) run += wsum[w];
-#pragma unroll
-    for (int q = 0; q < DPT; ++q) {
-      dbase[q] = run + hist[(int64_t)(tid * DPT + q) * ntiles + blockIdx.x];
-      run += x[q];
-    }
-  }
 #pragma unroll
   for (int w = 0; w < RS_WARPS; ++w)
 #pragma unroll
-    for (int q = 0; q < DPT; ++q) woff[w][tid * DPT + q] = 0;
-  __syncthreads();
+    for (int q = 0; q < DPT; ++q) woff[w * RD + tid * DPT + q] = 0;
 
-  const int64_t wbase = (int64_t)blockIdx.x * RS_TILE + (int64_t)warp * (32 * RS_ITEMS);
+  const int64_t wbase = tbase + (int64_t)warp * (32 * RS_ITEMS);
   uint64_t key[RS_ITEMS];
   uint32_t val[RS_ITEMS];
 #pragma unroll
   for (int j = 0; j < RS_ITEMS; ++j) {
     const int64_t i = wbase + j * 32 + lane;
-    key[j] = i < n ? kin[i] : 0ull;
-    val[j] = i < n ? vin[i] : 0u;
-  }
-  // count this warp's digits
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) {
-    const bool valid = wbase + j * 32 + lane < n;
-    const unsigned vm = __ballot_sync(kFull, valid);
-    if (valid) {
-      const unsigned d = (unsigned)(key[j] >> shift) & (RD - 1u);
-      const unsigned peers = __match_any_sync(vm, d);
-      if (lane == __ffs(peers) - 1) woff[warp][d] += (uint32_t)__popc(peers);
-    }
-    __syncwarp();
+    key[j] = i < n ? __ldcs(kin + i) : 0ull;
+    val[j] = i < n ? __ldcs(vin + i) : 0u;
   }
   __syncthreads();
-#pragma unroll
-  for (int q = 0; q < DPT; ++q) {
-    uint32_t run = dbase[q];
-#pragma unroll
-    for (int w = 0; w < RS_WARPS; ++w) {
-      const uint32_t c = woff[w][tid * DPT + q];
-      woff[w][tid * DPT + q] = run;
-      run += c;
-    }
-  }
-  __syncthreads();
+  // rank within the warp (in item order)
   const unsigned lt = (1u << lane) - 1u;
+  uint32_t* my = woff + warp * RD;
+  uint32_t rank[RS_ITEMS];
 #pragma unroll
   for (int j = 0; j < RS_ITEMS; ++j) {
     const bool valid = wbase + j * 32 + lane < n;
     const unsigned vm = __ballot_sync(kFull, valid);
-    unsigned d = 0, peers = 0;
+    const unsigned d = (unsigned)(key[j] >> shift) & (RD - 1u);
+    unsigned peers = 0;
+    uint32_t before = 0;
     if (valid) {
-      d = (unsigned)(key[j] >> shift) & (RD - 1u);
       peers = __match_any_sync(vm, d);
-      const uint32_t p = woff[warp][d] + (uint32_t)__popc(peers & lt);
-      kout[p] = key[j];
-      vout[p] = val[j];
+      before = my[d];
     }
+    rank[j] = before + (uint32_t)__popc(peers & lt);
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) woff[warp][d] += (uint32_t)__popc(peers);
+    if (valid && lane == __ffs(peers) - 1) my[d] = before + (uint32_t)__popc(peers);
     __syncwarp();
+  }
+  __syncthreads();
+  // tile positions: exclusive scan over digits (thread tid owns digits
+  // [tid*DPT, tid*DPT+DPT)), then over warps inside each digit; and the global
+  // digit bases (scan of totals + this tile's offset within each digit)
+  {
+    uint32_t cnt[DPT], tot[DPT], mine = 0, gmine = 0;
+#pragma unroll
+    for (int q = 0; q < DPT; ++q) {
+      cnt[q] = 0;
+#pragma unroll
+      for (int w = 0; w < RS_WARPS; ++w) cnt[q] += woff[w * RD + tid * DPT + q];
+      mine += cnt[q];
+      tot[q] = totals[tid * DPT + q];
+      gmine += tot[q];
+    }
+    uint32_t incl = mine, gincl = gmine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      const uint32_t gy = __shfl_up_sync(kFull, gincl, o);
+      if (lane >= o) { incl += y; gincl += gy; }
+    }
+    if (lane == 31) { wsum[0][warp] = incl; wsum[1][warp] = gincl; }
+    __syncthreads();
+    uint32_t run = incl - mine, grun = gincl - gmine;
+    for (int w = 0; w < warp; ++w) { run += wsum[0][w]; grun += wsum[1][w]; }
+#pragma unroll
+    for (int q = 0; q < DPT; ++q) {
+      const int d = tid * DPT + q;
+      gdst[d] = grun + hist[(int64_t)d * ntiles + blockIdx.x] - run;
+      uint32_t r = run;
+#pragma unroll
+      for (int w = 0; w < RS_WARPS; ++w) {
+        const uint32_t c = woff[w * RD + d];
+        woff[w * RD + d] = r;
+        r += c;
+      }
+      run += cnt[q];
+      grun += tot[q];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    if (wbase + j * 32 + lane < n) {
+      const unsigned d = (unsigned)(key[j] >> shift) & (RD - 1u);
+      const uint32_t p = my[d] + rank[j];
+      skey[p] = key[j];
+      sval[p] = val[j];
+    }
+  }
+  __syncthreads();
+  const int64_t valid_n = n - tbase < RS_TILE ? n - tbase : RS_TILE;
+#pragma unroll 4
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    const int i = j * RS_THREADS + tid;
+    if (i < valid_n) {
+      const uint64_t k = skey[i];
+      const unsigned d = (unsigned)(k >> shift) & (RD - 1u);
+      const uint32_t p = gdst[d] + (uint32_t)i;  // < nnz < 2^32
+      __stcs(kout + p, k);
+      __stcs(vout + p, sval[i]);
+    }
   }
 }
 
@@ -255,6 +297,25 @@ __global__ void decode(const uint64_t* __restrict__ keys, const uint32_t* __rest
     const VT x = vin[o];
     val[i] = (float)x;
     if (val64) val64[i] = (double)x;
+  }
+}
+
+// Embedded layout: source index in the key's low ibits, fp32 value bits as
+// the payload -- no gather.
+__global__ void decode_embedded(const uint64_t* __restrict__ keys,
+                                const uint32_t* __restrict__ vbits, int64_t n, int ibits,
+                                int cbits, uint64_t rmask, uint64_t cmask,
+                                int32_t* __restrict__ lrow, int32_t* __restrict__ lcol,
+                                float* __restrict__ val, uint32_t* __restrict__ order) {
+  const uint64_t imask = (1ull << ibits) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = __ldcs(keys + i);
+    order[i] = (uint32_t)(k & imask);
+    const uint64_t kk = k >> ibits;
+    lrow[i] = (int32_t)((kk >> cbits) & rmask);
+    lcol[i] = (int32_t)(kk & cmask);
+    val[i] = __uint_as_float(__ldcs(vbits + i));
   }
 }
 
@@ -367,15 +428,20 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   prof_mark(ctx, "partition: alloc + upload");
   PCK(cudaMemsetAsync(d_bad, 0xFF, 8, s));
   const int grid = ctx->num_sms * 8;
+  // source index in the key's spare low bits, fp32 value as the payload
+  const int ibits = nnz > 1 ? bits_for((uint64_t)nnz - 1) : 0;
+  const bool embed = v32 && nnz > 1 && rbits + cbits + bbits + ibits <= 64;
+  const float* v32in = embed ? reinterpret_cast<const float*>(d_vin) : nullptr;
   if (nnz > 0 && host_bad < 0) {
     if (narrow)
       make_keys<int32_t><<<grid, 256, 0, s>>>(reinterpret_cast<const int32_t*>(d_rows),
                                               reinterpret_cast<const int32_t*>(d_cols), nnz, n,
                                               m, rbase, rextra, cbase, cextra, J, rbits, cbits,
-                                              ka, ia, d_bad);
+                                              embed ? ibits : 0, v32in, ka, ia, d_bad);
     else
       make_keys<int64_t><<<grid, 256, 0, s>>>(d_rows, d_cols, nnz, n, m, rbase, rextra, cbase,
-                                              cextra, J, rbits, cbits, ka, ia, d_bad);
+                                              cextra, J, rbits, cbits, 0, nullptr, ka, ia,
+                                              d_bad);
   }
   PCK(cudaGetLastError());
   unsigned long long hbad = 0;
@@ -399,6 +465,7 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   }
   free_dev(d_rows, ctx->stream);
   free_dev(d_cols, ctx->stream);
+  if (embed) free_dev(d_vin, ctx->stream);
   prof_mark(ctx, "partition: keys + check");
 
   // LSD passes: 9-bit digits (512 buckets) when that saves a pass over 8-bit
@@ -414,18 +481,23 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
     PCK(dmalloc(&ib, NK * 4, ctx->stream));
     PCK(dmalloc(&hist, (size_t)RD * ntiles * 4, ctx->stream));
     PCK(dmalloc(&tot, RD * 4, ctx->stream));
+    // > 48 KB of dynamic shared memory
+    PCK(cudaFuncSetAttribute(&radix_scatter<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)scatter_smem<512>()));
+    PCK(cudaFuncSetAttribute(&radix_scatter<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)scatter_smem<256>()));
     for (int p = 0; p < passes; ++p) {
-      const int shift = dbits * p;
+      const int shift = (embed ? ibits : 0) + dbits * p;
       if (wide) {
         radix_hist<512><<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, nnz, shift, ntiles, hist);
         radix_scan_tiles<<<512, 1024, 0, s>>>(hist, ntiles, tot);
-        radix_scatter<512><<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, ia, kb, ib, nnz, shift,
-                                                                   hist, ntiles, tot);
+        radix_scatter<512><<<(unsigned)ntiles, RS_THREADS, scatter_smem<512>(), s>>>(
+            ka, ia, kb, ib, nnz, shift, hist, ntiles, tot);
       } else {
         radix_hist<256><<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, nnz, shift, ntiles, hist);
         radix_scan_tiles<<<256, 1024, 0, s>>>(hist, ntiles, tot);
-        radix_scatter<256><<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, ia, kb, ib, nnz, shift,
-                                                                   hist, ntiles, tot);
+        radix_scatter<256><<<(unsigned)ntiles, RS_THREADS, scatter_smem<256>(), s>>>(
+            ka, ia, kb, ib, nnz, shift, hist, ntiles, tot);
       }
       PCK(cudaGetLastError());
       uint64_t* tk = ka; ka = kb; kb = tk;
@@ -440,7 +512,11 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   PCK(dmalloc(&ctx->d_val, NK * 4, ctx->stream));
   PCK(dmalloc(&ctx->d_order, NK * 4, ctx->stream));
   if (ctx->exact) PCK(dmalloc(&ctx->d_val64, NK * 8, ctx->stream));
-  if (nnz > 0) {
+  if (nnz > 0 && embed) {
+    decode_embedded<<<grid, 256, 0, s>>>(ka, ia, nnz, ibits, cbits, (1ull << rbits) - 1,
+                                         (1ull << cbits) - 1, ctx->d_lrow, ctx->d_lcol,
+                                         ctx->d_val, ctx->d_order);
+  } else if (nnz > 0) {
     if (v32)
       decode<float><<<grid, 256, 0, s>>>(ka, ia, reinterpret_cast<const float*>(d_vin), nnz,
                                          cbits, (1ull << rbits) - 1, (1ull << cbits) - 1,
@@ -451,7 +527,8 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                                 (1ull << cbits) - 1, ctx->d_lrow, ctx->d_lcol, ctx->d_val,
                                 ctx->d_val64, ctx->d_order);
   }
-  block_offsets<<<(nb + 1 + 255) / 256, 256, 0, s>>>(ka, nnz, nb, rbits + cbits, d_off);
+  block_offsets<<<(nb + 1 + 255) / 256, 256, 0, s>>>(ka, nnz, nb,
+                                                    rbits + cbits + (embed ? ibits : 0), d_off);
   PCK(cudaGetLastError());
   PCK(cudaMemcpyAsync(ctx->h_offsets.data(), d_off, (nb + 1) * 8, cudaMemcpyDeviceToHost, s));
   PCK(cudaStreamSynchronize(s));

@@ -1104,19 +1104,19 @@ int ensure_step_scratch(bgmf_ctx* c, size_t nwork) {
   const int nb = c->I * c->J;
   if (!c->d_sse) {
     BGMF_CK(c, dmalloc(&c->d_sse, sizeof(double) * (nb > 0 ? nb : 1), c->stream));
-    BGMF_CK(c, cudaMallocHost(&c->h_sse, sizeof(double) * (nb > 0 ? nb : 1)));
+    BGMF_CK(c, pinned_alloc((void**)&c->h_sse, sizeof(double) * (nb > 0 ? nb : 1)));
     BGMF_CK(c, dmalloc(&c->d_bad, 8, c->stream));
-    BGMF_CK(c, cudaMallocHost(&c->h_bad, 8));
+    BGMF_CK(c, pinned_alloc((void**)&c->h_bad, 8));
   }
   if (nwork > c->work_cap) {
     if (c->d_work) dfree(c->d_work, c->stream);
-    if (c->h_work) cudaFreeHost(c->h_work);
+    pinned_free(c->h_work);
     c->d_work = nullptr;
     c->h_work = nullptr;
     size_t cap = nwork < 64 ? 64 : nwork;
     // device: work table, then exact-mode output slots / batch descriptors
     BGMF_CK(c, dmalloc(&c->d_work, sizeof(BlockWork) * cap * 8, c->stream));
-    BGMF_CK(c, cudaMallocHost(&c->h_work, sizeof(BlockWork) * cap));
+    BGMF_CK(c, pinned_alloc((void**)&c->h_work, sizeof(BlockWork) * cap));
     c->work_cap = cap;
   }
   return BGMF_OK;

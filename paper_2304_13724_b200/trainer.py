@@ -121,6 +121,8 @@ def train_blocked(d: RatingsDataset, cfg: TrainConfig, test: Optional[RatingsDat
     batched = (not early_stop and block_hook is None and evaluator is None and not adaptive
                and not isinstance(sched, ConvergeEachBlock) and not eng.options.exact
                and not eng.streaming and cfg.outer_steps > 1)
+    if own:  # fault the model's output pages in while the epochs run
+        eng.prefault_factors()
     if batched:
         # nothing is decided on the host between steps: enqueue every epoch
         # in one bgmf_run_steps call (no host round trip between epochs)
