@@ -158,3 +158,29 @@ def test_partition_rows_keeps_only_the_row_range():
     bad[123] = n + 5
     with pytest.raises(bm.DataError, match="entry 123"):
         bm.Engine().partition(bad, c, v, n, m, 4, 3, row_range=(0, 10))
+
+
+@pytest.mark.parametrize("options", [None, bm.EngineOptions(exact=True)], ids=["fast", "exact"])
+@pytest.mark.parametrize("shape", [(6040, 3706, 8, 8), (6040, 3706, 2, 3),
+                                   (2**31 - 1, 2**30, 1, 1), (2**31 - 1, 2**31 - 1, 3, 2)],
+                         ids=["c2-embedded", "c2-8bit", "wide-1x1", "wide-3x2"])
+def test_key_layouts_match_oracle(shape, options):
+    """Both sort layouts: the source index in the key's spare low bits with
+    the fp32 value as payload (fast mode, key + index <= 64 bits) and the
+    index as payload with a gather (exact mode, or keys too wide: 2^31-row
+    matrices), with duplicate cells, against the oracle's lexsort order."""
+    n, m, I, J = shape
+    g = np.random.default_rng(n % 1000 + I)
+    nnz = 60_000
+    r = g.integers(0, n, nnz)
+    c = g.integers(0, m, nnz)
+    dup, at = g.integers(0, nnz, 5_000), g.integers(0, nnz, 5_000)
+    r[at], c[at] = r[dup], c[dup]  # repeated cells keep input order
+    v = g.integers(1, 6, nnz).astype(np.float64) + g.random(nnz)
+    ref = O.partition(r, c, v, n, m, I, J)
+    b = bm.partition(bm.RatingsDataset(n, m, r, c, v), I, J, options)
+    assert np.array_equal(b._offsets, ref["offsets"])
+    assert np.array_equal(b._rows, ref["rows"])
+    assert np.array_equal(b._cols, ref["cols"])
+    assert np.array_equal(b._values, ref["values"])
+    assert np.array_equal(b.order, np.lexsort((c, r, _block_ids(r, c, n, m, I, J))))
