@@ -201,3 +201,27 @@ def test_sequential_is_blocked_1x1(golden, name):
     assert [s["train_rmse"] for s in tr] == meta["train"]
     assert stop == meta["stop"]
     assert sha(u) == meta["u_sha"] and sha(v) == meta["v_sha"]
+
+
+@pytest.mark.parametrize("shape", [(2**31 - 1, 2**31 - 1, 3, 2), (2**31 - 1, 2**30, 1, 1),
+                                   (100, 70, 3, 4)])
+def test_partition_wide_matrices_match_lexsort(shape):
+    """The oracle's packed 64-bit key overflows for 2^31-wide matrices; it
+    then falls back to a stable comparison sort -- still np.lexsort's order
+    (partition.py:124), duplicates in input order."""
+    n, m, I, J = shape
+    g = np.random.default_rng(3)
+    r, c = g.integers(0, n, 20_000), g.integers(0, m, 20_000)
+    dup, at = g.integers(0, 20_000, 2_000), g.integers(0, 20_000, 2_000)
+    r[at], c[at] = r[dup], c[dup]
+    v = g.random(20_000)
+    ref = O.partition(r, c, v, n, m, I, J)
+    rb, cb = O.split_bounds(n, I), O.split_bounds(m, J)
+    bi = np.searchsorted(rb, r, side="right") - 1
+    bj = np.searchsorted(cb, c, side="right") - 1
+    order = np.lexsort((c, r, bi * J + bj))
+    assert np.array_equal(ref["values"], v[order])
+    assert np.array_equal(ref["rows"], r[order] - rb[bi[order]])
+    assert np.array_equal(ref["cols"], c[order] - cb[bj[order]])
+    assert np.array_equal(ref["offsets"], np.concatenate(([0], np.cumsum(
+        np.bincount(bi * J + bj, minlength=I * J)))))
