@@ -303,7 +303,9 @@ int bgmf_sse(const double* u, int64_t n, const double* v, int64_t m, int k,
  * sweep's access pattern on `device` -- `ratings` random 512-byte rows of an
  * L2-resident rows x 128 fp32 matrix, read (mode 0), read + reduce-added into
  * other random rows (mode 1, the sweep's V traffic) or reduce-added only
- * (mode 2), groups of 8 lanes, 256-thread CTAs x ctas_per_sm per SM.  Best
+ * (mode 2), two reads + one reduce (mode 3), or even warps mode 1 and odd
+ * warps mode 0 over as many rows again (mode 4), groups of 8 lanes,
+ * 256-thread CTAs x ctas_per_sm per SM.  Best
  * kernel time of 3 timed launches in *ms_out. */
 int bgmf_probe_l2(int device, int64_t rows, int64_t ratings, int mode,
                   int ctas_per_sm, double* ms_out);

@@ -21,15 +21,39 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
 }
 
 // mode 0: read rows; 1: read rows + reduce-add a delta into other rows;
-// 2: reduce-add only.  L = 8 lanes x 4 float4 = 128 floats per row.
+// 2: reduce-add only; 3: two reads + one reduce per rating; 4: even warps do
+// mode 1 over `ratings`, odd warps mode 0 over another `ratings` (a sweep and
+// an SSE sharing the SMs).  L = 8 lanes x 4 float4 = 128 floats per row.
+template <int MODE>
+__device__ __forceinline__ void l2_probe_body(float* __restrict__ V, uint32_t rows,
+                                              int64_t ratings, int64_t group, int64_t ngroups,
+                                              int gl, float& acc);
+
 template <int MODE>
 __global__ void __launch_bounds__(256) l2_probe_kernel(float* __restrict__ V, uint32_t rows,
                                                        int64_t ratings, float* __restrict__ sink) {
-  constexpr int L = 8, V4 = 4, D = 4;
+  constexpr int L = 8;
   const int lane = threadIdx.x & 31, gl = lane & (L - 1);
-  const int64_t group = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / L;
-  const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / L;
   float acc = 0.f;
+  if (MODE == 4) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t group = (gw >> 1) * (32 / L) + lane / L;
+    const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / L / 2;
+    if (gw & 1) l2_probe_body<0>(V, rows, ratings, group, ngroups, gl, acc);
+    else l2_probe_body<1>(V, rows, ratings, group, ngroups, gl, acc);
+  } else {
+    const int64_t group = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / L;
+    const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / L;
+    l2_probe_body<MODE>(V, rows, ratings, group, ngroups, gl, acc);
+  }
+  if (acc == 12345.678f) sink[0] = acc;  // keeps the loads alive
+}
+
+template <int MODE>
+__device__ __forceinline__ void l2_probe_body(float* __restrict__ V, uint32_t rows,
+                                              int64_t ratings, int64_t group, int64_t ngroups,
+                                              int gl, float& acc) {
+  constexpr int L = 8, V4 = 4, D = 4;
   for (int64_t t0 = group * D; t0 < ratings; t0 += ngroups * D) {
     float4 v[D][V4];
 #pragma unroll
@@ -68,7 +92,6 @@ __global__ void __launch_bounds__(256) l2_probe_kernel(float* __restrict__ V, ui
       }
     }
   }
-  if (acc == 12345.678f) sink[0] = acc;  // keeps the loads alive
 }
 
 }  // namespace
@@ -78,7 +101,7 @@ using namespace bgmf;
 
 extern "C" int bgmf_probe_l2(int device, int64_t rows, int64_t ratings, int mode,
                              int ctas_per_sm, double* ms_out) {
-  if (!ms_out || rows < 1 || rows > 0x7fffffff || ratings < 1 || mode < 0 || mode > 3)
+  if (!ms_out || rows < 1 || rows > 0x7fffffff || ratings < 1 || mode < 0 || mode > 4)
     return fail(nullptr, BGMF_ERR_ARG, "bgmf_probe_l2: bad argument");
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
@@ -99,7 +122,8 @@ extern "C" int bgmf_probe_l2(int device, int64_t rows, int64_t ratings, int mode
     if (mode == 0) l2_probe_kernel<0><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
     else if (mode == 1) l2_probe_kernel<1><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
     else if (mode == 2) l2_probe_kernel<2><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
-    else l2_probe_kernel<3><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
+    else if (mode == 3) l2_probe_kernel<3><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
+    else l2_probe_kernel<4><<<grid, 256>>>(V, (uint32_t)rows, ratings, sink);
     cudaEventRecord(b);
     e = cudaEventSynchronize(b);
     float ms = 0.f;

@@ -1,5 +1,5 @@
 """Warp-stall samples per CUDA source line (ncu source page, cuda,sass view).
-Usage: python scripts/ncu_lines.py report.ncu-rep [N]"""
+Usage: python scripts/ncu_lines.py report.ncu-rep [N] [kernel-regex]"""
 import csv
 import subprocess
 import sys
@@ -7,7 +7,8 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+flt = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, *flt, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout.splitlines()
 per = defaultdict(int)
 src = {}
