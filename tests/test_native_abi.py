@@ -60,3 +60,15 @@ def test_errors_without_context_are_reported():
     assert L.bgmf_last_error(None)
     ctx = ctypes.c_void_p()
     assert L.bgmf_create(-1, None, ctypes.byref(ctx)) != 0
+
+
+def test_host_prefault_zero_fills_without_a_gpu():
+    """bgmf_host_prefault is host-only (no CUDA call): it faults in and
+    zero-fills one byte per 4 KiB page of a caller buffer."""
+    import numpy as np
+
+    lib = N.load()
+    a = np.full(3 * 1024 * 1024 + 123, 7, np.uint8)  # spans 2 MiB pages, ragged tail
+    assert lib.bgmf_host_prefault(a.ctypes.data, a.nbytes) == 0
+    assert (a[::4096] == 0).all()
+    assert lib.bgmf_host_prefault(None, 0) == 0
