@@ -1012,9 +1012,16 @@ int64_t block_chunk(bgmf_ctx* c, int b, int64_t cnt, int64_t cl) {
 // of them (groups = worker groups resident in one wave; 0 = one chunk per
 // block, the exact path).  chunk = ceil(batch_nnz / (groups - B)) so the
 // per-block rounding can never spill into a second wave.
+// sse = true: chunks for the post-sweep SSE, an order-free sum -- one-wave
+// length only, none of block_chunk's concurrency floors (on small strata the
+// sweep's floors leave most of the GPU idle; C1's sweep chunks are ~25
+// ratings long, the SSE's ~3).
+constexpr int64_t kSseMinChunk = 8;
+
 int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
                int64_t groups, std::vector<BatchRange>& ranges,
-               const std::vector<char>* active = nullptr, int w_base = 0, int pos_base = 0) {
+               const std::vector<char>* active = nullptr, int w_base = 0, int pos_base = 0,
+               bool sse = false) {
   const int total = batch_off[nbatch];
   int rc = ensure_step_scratch(c, (size_t)(w_base + total));
   if (rc) return rc;
@@ -1044,7 +1051,9 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
       const int64_t beg = c->h_offsets[b], end = c->h_offsets[b + 1];
       const int64_t cnt = end - beg;
       if (cnt == 0) continue;
-      const int64_t bl = groups > 0 ? block_chunk(c, b, cnt, cl) : cnt;
+      int64_t bl = cnt;
+      if (groups > 0 && !sse) bl = block_chunk(c, b, cnt, cl);
+      else if (groups > 0) bl = std::min(cnt, std::max(cl, kSseMinChunk));
       BlockWork& bw = c->h_work[w++];
       bw.begin = beg;
       bw.end = end;
@@ -1145,10 +1154,17 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in,
   const int ctas_per_sm = fused ? resident_ctas(c, ep) : 0;
   const int64_t groups =
       fused ? (int64_t)c->num_sms * ctas_per_sm * 8 * gpw : sweep_groups(c, sh);
-  std::vector<BatchRange> ranges;
-  int rc = build_work(c, plan, batch_off, nbatch, groups, ranges);
+  std::vector<BatchRange> ranges, sranges;
+  int rc = ensure_step_scratch(c, 2 * (size_t)batch_off[nbatch]);  // sweep + SSE tables
+  if (rc) return rc;
+  rc = build_work(c, plan, batch_off, nbatch, groups, ranges);
   if (rc) return rc;
   const int nw = ranges.empty() ? 0 : ranges.back().w0 + ranges.back().nw;
+  if (!fused) {
+    rc = build_work(c, plan, batch_off, nbatch, groups, sranges, nullptr, nw, 0, true);
+    if (rc) return rc;
+  }
+  const int nw_all = sranges.empty() ? nw : sranges.back().w0 + sranges.back().nw;
   BatchDesc* bdesc = reinterpret_cast<BatchDesc*>(c->d_work + c->work_cap);
   std::vector<BatchDesc> hb(nbatch > 0 ? nbatch : 1);
   int max_chunks = 0;
@@ -1158,8 +1174,8 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in,
     if (ranges[t].chunks > max_chunks) max_chunks = ranges[t].chunks;
   }
   for (int q = 0; q < nw; ++q) ratings += (double)(c->h_work[q].end - c->h_work[q].begin);
-  if (nw > 0)
-    BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * nw,
+  if (nw_all > 0)
+    BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * nw_all,
                                cudaMemcpyHostToDevice, s));
   BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, s));
   BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
@@ -1200,9 +1216,11 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in,
         launch_fast(true, sh, grid, s, w, r.nw, r.chunks, c, alpha, beta, it);
         if (slot) record_end(c, slot);
       }
+      const BatchRange& sr = sranges[t];
+      const dim3 sgrid(((sr.chunks + gpw - 1) / gpw + 7) / 8);
       TimedLaunch* slot = nullptr;
       if (c->timing) record_begin(c, 1, 0.0, &slot);
-      launch_fast(false, sh, grid, s, w, r.nw, r.chunks, c, alpha, beta, 0);
+      launch_fast(false, sh, sgrid, s, c->d_work + sr.w0, sr.nw, sr.chunks, c, alpha, beta, 0);
       if (slot) record_end(c, slot);
     }
   }
@@ -1226,7 +1244,8 @@ int64_t fast_groups(bgmf_ctx* c) { return sweep_groups(c, shape_for(c->kp)); }
 int step_begin(bgmf_ctx* c, int max_blocks) {
   if (c->exact) return fail(c, BGMF_ERR_STATE, "asynchronous steps are fast-mode only");
   if (c->streaming) return fail(c, BGMF_ERR_STATE, "asynchronous steps do not stream");
-  int rc = ensure_step_scratch(c, (size_t)(max_blocks > 0 ? max_blocks : 1));
+  // each submitted block takes a sweep and an SSE work entry
+  int rc = ensure_step_scratch(c, 2 * (size_t)(max_blocks > 0 ? max_blocks : 1));
   if (rc) return rc;
   const int nb = c->I * c->J;
   BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, c->stream));
@@ -1244,16 +1263,20 @@ int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in, in
   const int32_t* batch_off = waves.data();
   const int nbatch = (int)waves.size() - 1;
   const int total = batch_off[nbatch];
-  if ((size_t)(c->w_cursor + total) > c->work_cap)
+  if ((size_t)(c->w_cursor + 2 * total) > c->work_cap)
     return fail(c, BGMF_ERR_ARG, "more blocks than reserved by bgmf_step_begin");
   const Shape sh = shape_for(c->kp);
   const int gpw = 32 / sh.L;
-  std::vector<BatchRange> ranges;
+  std::vector<BatchRange> ranges, sranges;
   const int pos0 = (int)c->submitted.size();
   int rc = build_work(c, plan, batch_off, nbatch, sweep_groups(c, sh), ranges, nullptr,
                       c->w_cursor, pos0);
   if (rc) return rc;
-  const int w_end = ranges.empty() ? c->w_cursor : ranges.back().w0 + ranges.back().nw;
+  const int w_mid = ranges.empty() ? c->w_cursor : ranges.back().w0 + ranges.back().nw;
+  rc = build_work(c, plan, batch_off, nbatch, sweep_groups(c, sh), sranges, nullptr, w_mid,
+                  pos0, true);
+  if (rc) return rc;
+  const int w_end = sranges.empty() ? w_mid : sranges.back().w0 + sranges.back().nw;
   if (w_end > c->w_cursor)
     BGMF_CK(c, cudaMemcpyAsync(c->d_work + c->w_cursor, c->h_work + c->w_cursor,
                                sizeof(BlockWork) * (w_end - c->w_cursor), cudaMemcpyHostToDevice,
@@ -1274,9 +1297,12 @@ int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in, in
                   it);
       if (slot) record_end(c, slot);
     }
+    const BatchRange& sr = sranges[t];
+    const dim3 sgrid(((sr.chunks + gpw - 1) / gpw + 7) / 8);
     TimedLaunch* slot = nullptr;
     if (c->timing) record_begin(c, 1, 0.0, &slot);
-    launch_fast(false, sh, grid, c->stream, c->d_work + r.w0, r.nw, r.chunks, c, alpha, beta, 0);
+    launch_fast(false, sh, sgrid, c->stream, c->d_work + sr.w0, sr.nw, sr.chunks, c, alpha,
+                beta, 0);
     if (slot) record_end(c, slot);
   }
   BGMF_CK(c, cudaGetLastError());
@@ -1310,7 +1336,7 @@ int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs
     plan_pos += off[nbatch[k]];
     off_pos += nbatch[k] + 1;
   }
-  int rc = ensure_step_scratch(c, (size_t)(total > 0 ? total : 1));
+  int rc = ensure_step_scratch(c, 2 * (size_t)(total > 0 ? total : 1));  // sweep + SSE tables
   if (rc) return rc;
   double* d_sse = nullptr;
   unsigned long long* d_bad = nullptr;
