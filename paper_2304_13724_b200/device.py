@@ -102,6 +102,10 @@ class Engine:
             self._opt("l2_wave_bytes", float(self.options.l2_wave_bytes))
         f = self.options.fused
         self._opt("fused", -1.0 if f is None else (1.0 if f else 0.0))
+        # experiments only: raw bgmf_set_option knobs, "key=value,key=value"
+        for kv in filter(None, os.environ.get("BGMF_ENGINE_OPTS", "").split(",")):
+            key, val = kv.split("=")
+            self._opt(key.strip(), float(val))
         self.n = self.m = self.nnz = 0
         self.I = self.J = 0
         self.k = 0
