@@ -246,13 +246,20 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
     from .metrics import HoldoutEvaluator, RmseAccumulator, finalize, merge
     from .trainer import resolve_inner_iters
 
+    from .trainer import _Phases
+
     dist = _init_dist()
     rank, world = dist.get_rank(), dist.get_world_size()
     device = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(device)
+    prof = _Phases() if os.environ.get("BGMF_PROFILE") and rank == 0 else None
     sched = RingSchedule(cfg.grid_i, cfg.grid_j, world)
     shard = GpuShard(d, cfg, sched, rank, device, options)
     shard.eng.init_factors(d.n, d.m, cfg.k, cfg.seed)
+    shard.eng.prefault_factors()  # the model's host pages fault in while the epochs run
+    if prof:
+        torch.cuda.synchronize()
+        prof.mark("shard: partition + factors")
     evaluator = HoldoutEvaluator(d, test) if test is not None and len(test) > 0 else None
     if evaluator is not None:
         t = evaluator.test
@@ -333,15 +340,26 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
             if len(trace) >= 2 and trace.steps[-2].train_rmse - train_rmse < cfg.delta:
                 stop = "converged"
                 break
+    if prof:
+        torch.cuda.synchronize()
+        prof.mark(f"{len(trace)} epochs")
     # gather the model: V from its holders, U row slabs from their owners
-    sync_all_v(sched, rank, shard.v_slice, dist)
-    for r in range(world):
-        rows = sched.rows_of(r)
-        if len(rows):
-            dist.broadcast(shard.u_rows(rows), src=r)
+    if world > 1:
+        sync_all_v(sched, rank, shard.v_slice, dist)
+        for r in range(world):
+            rows = sched.rows_of(r)
+            if len(rows):
+                dist.broadcast(shard.u_rows(rows), src=r)
     torch.cuda.synchronize()
+    if prof:
+        prof.mark("gather (NCCL)")
     u, v = shard.eng.get_factors()
+    if prof:
+        prof.mark("get_factors (D2H)")
     shard.eng.close()
+    if prof:
+        prof.mark("close")
+        prof.report()
     return FactorModel(u, v), trace, stop
 
 
