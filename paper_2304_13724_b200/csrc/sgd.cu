@@ -29,6 +29,8 @@
 
 #include <cmath>
 
+#include <atomic>
+
 #include "bgmf_internal.cuh"
 
 namespace bgmf {
@@ -857,11 +859,12 @@ void launch_sse_async(dim3 grid, cudaStream_t s, const BlockWork* w, int nwork, 
                       int cbits) {
   constexpr int D = LL < 4 ? LL : 4;
   const int smem = 256 * D * VV * 16;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_set{0};  // one bit per device: attributes are per context
+  const uint64_t bit = 1ull << (c->device & 63);
+  if (!(attr_set.load() & bit)) {
     cudaFuncSetAttribute(&sse_async_kernel<LL, VV, MM, D>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+    attr_set.fetch_or(bit);
   }
   sse_async_kernel<LL, VV, MM, D><<<grid, 256, smem, s>>>(w, nwork, total, lrow, lcol, val,
                                                           c->d_u, c->d_v, c->kp, c->d_sse, cbits);
@@ -879,13 +882,9 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
 #define BGMF_CASE(LL, VV, MM)                                                                 \
   if (sh.L == LL && sh.V4 == VV && mk == MM) {                                                \
     if (sweep && c->bulk_red) {                                                               \
-      static int smem_set = 0;                                                                \
-      if (smem_set < (int)bulk_smem(c, sh)) {                                                 \
-        cudaFuncSetAttribute(&sgd_fast_kernel<LL, VV, MM, true>,                             \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
-                             (int)bulk_smem(c, sh));                                          \
-        smem_set = (int)bulk_smem(c, sh);                                                     \
-      }                                                                                       \
+      cudaFuncSetAttribute(&sgd_fast_kernel<LL, VV, MM, true>,                               \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,                       \
+                           (int)bulk_smem(c, sh));                                            \
       sgd_fast_kernel<LL, VV, MM, true><<<grid, 256, bulk_smem(c, sh), s>>>(                  \
           w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
     } else if (sweep)                                                                         \
