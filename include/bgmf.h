@@ -221,6 +221,12 @@ int bgmf_step_begin(bgmf_ctx* ctx, int max_blocks);
 int bgmf_step_batch(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
                     int nbatch, int inner_iters, double alpha, double beta);
 int bgmf_step_end(bgmf_ctx* ctx, double* sse_out, int64_t* bad_out);
+/* bgmf_step_end without a host round trip (the ring trainer's batched
+ * epochs): the step's per-block SSEs (fp64 [I*J]) and its raw divergence
+ * word go to caller DEVICE memory, stream-ordered; nothing waits.  The word
+ * is all ones when clean, else (plan position in submission order << 48) |
+ * (iteration << 32) | entry. */
+int bgmf_step_end_async(bgmf_ctx* ctx, double* d_sse_out, uint64_t* d_bad_out);
 
 /* One outer step of the synchronized row-sharded baseline trainer (CPMF,
  * baselines.py:100-182, `train_sync_parallel`) on a context partitioned 1 x 1

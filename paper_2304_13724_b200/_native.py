@@ -58,6 +58,7 @@ SIGNATURES = {
     "bgmf_step_begin": (_i, [_ctx, _i]),
     "bgmf_step_batch": (_i, [_ctx, _i32p, _i32p, _i, _i, _d, _d]),
     "bgmf_step_end": (_i, [_ctx, _f64p, _i64p]),
+    "bgmf_step_end_async": (_i, [_ctx, ctypes.c_void_p, ctypes.c_void_p]),
     "bgmf_run_sync_parallel_step": (_i, [_ctx, _i64p, _i, _d, _d, _f64p, _i64p]),
     "bgmf_run_step_converge": (_i, [_ctx, _i32p, _i32p, _i, _d, _l, _d, _d, _f64p, _i64p,
                                     _i32p, _i64p]),

@@ -219,6 +219,7 @@ int step_begin(bgmf_ctx* c, int max_blocks);
 int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch, int iters,
                float alpha, float beta);
 int step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out);
+int step_end_async(bgmf_ctx* c, double* d_sse_out, unsigned long long* d_bad_out);
 int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs,
               const int32_t* nbatch, const int32_t* iters, float alpha, float beta,
               double* sse_out, int64_t* bad_out, float* ms_out);

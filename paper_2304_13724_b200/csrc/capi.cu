@@ -462,6 +462,13 @@ int bgmf_step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out) {
   return step_end(c, sse_out, bad_out);
 }
 
+int bgmf_step_end_async(bgmf_ctx* c, double* d_sse_out, uint64_t* d_bad_out) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  if (!d_sse_out || !d_bad_out) return fail(c, BGMF_ERR_ARG, "NULL argument");
+  cudaSetDevice(c->device);
+  return step_end_async(c, d_sse_out, reinterpret_cast<unsigned long long*>(d_bad_out));
+}
+
 int bgmf_run_sync_parallel_step(bgmf_ctx* c, const int64_t* shard_edges, int nshards,
                                 double alpha, double beta, double* sse_out, int64_t* bad_out) {
   if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
@@ -580,6 +587,10 @@ int bgmf_stream_stats(bgmf_ctx* c, double* h2d_bytes) {
 
 int bgmf_kernel_stats(bgmf_ctx* c, double* out5, int reset) {
   if (!c || !out5) return fail(c, BGMF_ERR_ARG, "NULL argument");
+  if (c->events_used) {  // launches timed since the last synchronising call
+    cudaSetDevice(c->device);
+    harvest_timing(c);
+  }
   out5[0] = c->t_sgd_ms;
   out5[1] = c->t_sse_ms;
   out5[2] = (double)c->n_sgd;

@@ -1419,6 +1419,21 @@ int step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out) {
 }
 
 
+// step_end without a host round trip: the per-block SSEs and the raw
+// divergence word are copied (stream-ordered) into caller device memory, so a
+// caller can keep enqueueing steps and collectives and read every step's
+// results once.  The word is pack_bad(plan position in submission order,
+// iteration, entry) or kNoBad; the caller maps positions to blocks.
+int step_end_async(bgmf_ctx* c, double* d_sse_out, unsigned long long* d_bad_out) {
+  if (!c->in_step) return fail(c, BGMF_ERR_STATE, "bgmf_step_begin has not been called");
+  c->in_step = false;
+  const int nb = c->I * c->J;
+  BGMF_CK(c, cudaMemcpyAsync(d_sse_out, c->d_sse, sizeof(double) * nb, cudaMemcpyDeviceToDevice,
+                             c->stream));
+  BGMF_CK(c, cudaMemcpyAsync(d_bad_out, c->d_bad, 8, cudaMemcpyDeviceToDevice, c->stream));
+  return BGMF_OK;
+}
+
 // Sweeps (`iters` launches) + SSE launch for one piece of a batch whose
 // ratings live at (lrow, lcol, val) -- the streaming path's unit of work.
 int launch_piece(bgmf_ctx* c, const BlockWork* d_work, int nwork, int chunks,

@@ -297,6 +297,12 @@ class Engine:
         self._check(self._L.bgmf_step_end(self._h, N.ptr(sse, N._f64p), N.ptr(bad, N._i64p)))
         return sse, (None if bad[0] < 0 else tuple(int(x) for x in bad))
 
+    def step_end_async(self, d_sse: int, d_bad: int):
+        """End the step without a host sync: per-block SSEs (fp64 [I*J]) and
+        the raw divergence word to the device addresses given."""
+        self._check(self._L.bgmf_step_end_async(self._h, ctypes.c_void_p(d_sse),
+                                                ctypes.c_void_p(d_bad)))
+
     def run_sync_parallel_step(self, edges: np.ndarray, alpha: float, beta: float):
         """CPMF step on a 1x1 partition; returns (per-shard SSE, bad) where
         bad = (shard, entry, iteration) or None."""

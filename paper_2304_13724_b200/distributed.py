@@ -136,6 +136,59 @@ def run_epoch(sched: RingSchedule, shard, rank: int, dist, step0: int, g: int,
     return sse_all, order, bad_any
 
 
+def _run_epochs_batched(sched: RingSchedule, shard, rank: int, dist, cfg, nb: int,
+                        device: int, timing: bool):
+    """Every outer step of a run with a fixed inner schedule, no early
+    stopping and no holdout set, without a host round trip between steps:
+    each step's per-block SSEs and divergence word stay in HBM
+    (bgmf_step_end_async) and are all-reduced there (NCCL, ordered on the
+    engine stream), so the host keeps enqueueing V moves and strata while the
+    GPUs work; every step's results are read once at the end.  Returns, per
+    step, (global sse[nb], plan order, local divergence as (block, entry,
+    iter) or None, any rank diverged, inner iterations, seconds)."""
+    import torch
+
+    from .trainer import resolve_inner_iters
+
+    S, J = cfg.outer_steps, cfg.grid_j
+    dev = f"cuda:{device}"
+    sse = torch.zeros((S, nb), dtype=torch.float64, device=dev)
+    bad = torch.full((S,), -1, dtype=torch.int64, device=dev)  # all ones = clean
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(S + 1)] if timing else None
+    if ev:
+        ev[0].record(shard.stream)
+    orders, subs, gs = [], [], []
+    for k in range(S):
+        g = resolve_inner_iters(cfg.inner_schedule, k + 1, 1.0)
+        order: list[int] = []
+        shard.begin_epoch(nb)
+        for batch in sched.batches(k):
+            exchange(sched.transfers_for(batch), rank, shard.v_slice, dist)
+            order.extend(bi * J + bj for bi, bj in batch)
+            mine = sched.local_blocks(batch, rank)
+            if mine:
+                shard.run_batch(mine, g, cfg.alpha, cfg.beta)
+        subs.append(shard.end_epoch_async(sse[k], bad[k]))
+        dist.all_reduce(sse[k])
+        orders.append(order)
+        gs.append(g)
+        if ev:
+            ev[k + 1].record(shard.stream)
+    flag = (bad != -1).to(torch.int64)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+    sse_h, bad_h, flag_h = sse.cpu().numpy(), bad.cpu().numpy(), flag.cpu().numpy()
+    out = []
+    for k in range(S):
+        local = None
+        if int(bad_h[k]) != -1:
+            w = int(bad_h[k]) & 0xFFFFFFFFFFFFFFFF
+            pos, it, entry = w >> 48, (w >> 32) & 0xFFFF, w & 0xFFFFFFFF
+            local = (subs[k][pos] if pos < len(subs[k]) else -1, entry, it)
+        secs = ev[k].elapsed_time(ev[k + 1]) / 1e3 if ev else 0.0
+        out.append((sse_h[k], orders[k], local, bool(flag_h[k]), gs[k], secs))
+    return out
+
+
 def _run_epoch_converge(sched: RingSchedule, shard, rank: int, dist, step0: int, tol: float,
                         alpha: float, beta: float, nb: int, J: int):
     """run_epoch for ConvergeEachBlock: each stratum's local blocks sweep until
@@ -181,6 +234,9 @@ class GpuShard:
         self.torch = torch
         self.grid = make_grid(d.n, d.m, cfg.grid_i, cfg.grid_j)
         self.stream = torch.cuda.current_stream(device)
+        if self.stream.cuda_stream == 0:
+            raise RuntimeError("GpuShard needs a non-default current stream (torch.cuda.stream(...)):"
+                               " its kernels, the NCCL V moves and torch ops must share it")
         opts = options or EngineOptions()
         opts = EngineOptions(exact=False, min_chunk=opts.min_chunk, device=device,
                              timing=opts.timing, warps_per_sm=opts.warps_per_sm)
@@ -211,15 +267,23 @@ class GpuShard:
 
     def begin_epoch(self, max_blocks: int):
         self.eng.step_begin(max_blocks)
+        self.submitted: list[tuple[int, int]] = []
 
     def run_batch(self, blocks, g: int, alpha: float, beta: float):
         """Enqueue this rank's blocks of one stratum (no host sync)."""
         ids, off = self.eng.plan_arrays([blocks])
         self.eng.step_batch(ids, off, g, alpha, beta)
+        self.submitted.extend(int(b) for b in ids)
         return None
 
     def end_epoch(self):
         return self.eng.step_end()
+
+    def end_epoch_async(self, sse_row, bad_cell):
+        """End the step into device tensors (no host sync); returns the
+        step's block ids in submission order (to decode the divergence word)."""
+        self.eng.step_end_async(sse_row.data_ptr(), bad_cell.data_ptr())
+        return list(self.submitted)
 
 
 def _init_dist():
@@ -241,17 +305,26 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
     stop_reason)."""
     import torch
 
-    from .core import ConvergenceTrace, FactorModel, TraceStep
-    from .kernel import divergence
-    from .metrics import HoldoutEvaluator, RmseAccumulator, finalize, merge
-    from .trainer import resolve_inner_iters
-
-    from .trainer import _Phases
-
     dist = _init_dist()
     rank, world = dist.get_rank(), dist.get_world_size()
     device = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(device)
+    # the engine's kernels, the NCCL V moves and the torch ops must share ONE
+    # stream (NCCL orders against torch's current stream; a context created on
+    # the legacy default stream would get its own non-blocking stream)
+    with torch.cuda.stream(torch.cuda.Stream(device)):
+        return _train_ring(d, cfg, test, early_stop, options, timing, dist, rank, world, device)
+
+
+def _train_ring(d, cfg, test, early_stop, options, timing, dist, rank, world, device):
+    """train_blocked_distributed's body, on the rank's training stream."""
+    import torch
+
+    from .core import ConvergenceTrace, FactorModel, TraceStep
+    from .kernel import divergence
+    from .metrics import HoldoutEvaluator, RmseAccumulator, finalize, merge
+    from .trainer import _Phases, resolve_inner_iters
+
     prof = _Phases() if os.environ.get("BGMF_PROFILE") and rank == 0 else None
     sched = RingSchedule(cfg.grid_i, cfg.grid_j, world)
     shard = GpuShard(d, cfg, sched, rank, device, options)
@@ -282,6 +355,12 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
         s0 = torch.tensor([shard.eng.train_sse()], dtype=torch.float64, device=f"cuda:{device}")
         dist.all_reduce(s0)
         hist = [math.sqrt(float(s0.item()) / int(total_counts.sum()))]
+    from .core import ConvergeEachBlock
+
+    batched = (not early_stop and evaluator is None and not adaptive
+               and not isinstance(cfg.inner_schedule, ConvergeEachBlock) and cfg.outer_steps > 1)
+    pre = (_run_epochs_batched(sched, shard, rank, dist, cfg, nb, device, timing)
+           if batched else None)
     for step in range(1, cfg.outer_steps + 1):
         if adaptive and step >= 2:
             prev, cur = hist[-2], hist[-1]
@@ -291,7 +370,10 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
         g = resolve_inner_iters(cfg.inner_schedule, step, ratio)
         t0 = time.perf_counter()
         max_iters, capped = g, 0
-        if g is None:  # converge-each-block: per-block sweep counts, synchronous batches
+        if pre is not None:  # already run: this step's results
+            sse_all, order, bad_any, any_bad, g, secs = pre[step - 1]
+            max_iters = g
+        elif g is None:  # converge-each-block: per-block sweep counts, synchronous batches
             sse_all, order, bad_any, its, cap = _run_epoch_converge(
                 sched, shard, rank, dist, step - 1, cfg.inner_schedule.tol, cfg.alpha, cfg.beta,
                 nb, cfg.grid_j)
@@ -305,12 +387,14 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
         else:
             sse_all, order, bad_any = run_epoch(sched, shard, rank, dist, step - 1, g, cfg.alpha,
                                                 cfg.beta, nb, cfg.grid_j)
-        red = torch.tensor(sse_all, device=f"cuda:{device}")
-        dist.all_reduce(red)
-        sse_all = red.cpu().numpy()
-        flag = torch.tensor([0 if bad_any is None else 1], device=f"cuda:{device}")
-        dist.all_reduce(flag)
-        if int(flag.item()) or not np.all(np.isfinite(sse_all[order])):
+        if pre is None:
+            red = torch.tensor(sse_all, device=f"cuda:{device}")
+            dist.all_reduce(red)
+            sse_all = red.cpu().numpy()
+            flag = torch.tensor([0 if bad_any is None else 1], device=f"cuda:{device}")
+            dist.all_reduce(flag)
+            any_bad = bool(int(flag.item()))
+        if any_bad or not np.all(np.isfinite(sse_all[order])):
             b = bad_any[0] if bad_any else int(next(o for o in order
                                                     if not math.isfinite(sse_all[o])))
             err = divergence(b // cfg.grid_j, b % cfg.grid_j,
@@ -330,8 +414,8 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
                               device=f"cuda:{device}")
             dist.all_reduce(hs)
             test_rmse = math.sqrt(float(hs.item()) / len(evaluator.test))
-        trace.append(TraceStep(step, train_rmse, test_rmse,
-                               time.perf_counter() - t0 if timing else 0.0, max_iters, capped))
+        seconds = (secs if pre is not None else time.perf_counter() - t0) if timing else 0.0
+        trace.append(TraceStep(step, train_rmse, test_rmse, seconds, max_iters, capped))
         hist.append(train_rmse)
         if early_stop:
             if acc.count == 0:
@@ -397,18 +481,19 @@ def bench_main(args, clock_sampler=None):
     cfg = TrainConfig(k=w.k, alpha=w.alpha, beta=w.beta, grid_i=w.grid, grid_j=w.grid,
                       seed=w.seed)
     sched = RingSchedule(w.grid, w.grid, world)
+    torch.cuda.set_stream(torch.cuda.Stream(device))  # one stream: kernels + NCCL (GpuShard)
     shard = GpuShard(d, cfg, sched, rank, device, EngineOptions(timing=False))
     del r, c, v
     shard.eng.init_factors(w.n, w.m, w.k, w.seed)
     stream = shard.stream
 
-    def epoch(step0):
-        run_epoch(sched, shard, rank, dist, step0, 1, w.alpha, w.beta, w.grid * w.grid, w.grid)
+    from dataclasses import replace
 
-    step = 0
-    for _ in range(args.warmup):
-        epoch(step % w.grid)
-        step += 1
+    def epochs(n):  # the trainer's batched loop: no host round trip between epochs
+        _run_epochs_batched(sched, shard, rank, dist, replace(cfg, outer_steps=n),
+                            w.grid * w.grid, device, False)
+
+    epochs(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
     shard.eng.set_timing(True)
@@ -421,9 +506,7 @@ def bench_main(args, clock_sampler=None):
     torch.cuda.synchronize()
     dist.barrier()
     e0.record(stream)
-    for _ in range(args.steps):
-        epoch(step % w.grid)
-        step += 1
+    epochs(args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()

@@ -139,3 +139,31 @@ def test_world1_nccl_converge_schedule_matches_oracle():
         assert all(s.inner_iters >= 1 for s in trace)
     finally:
         dist.destroy_process_group()
+
+
+def test_gpu_shard_refuses_the_legacy_default_stream():
+    """The ring's ordering (sweep -> NCCL send of its V block -> recv -> next
+    sweep) holds only if the engine, NCCL and torch share one stream; on the
+    legacy default stream the engine would run on a private stream."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_13724_b200 import distributed as D
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
+                      WORLD_SIZE="1", LOCAL_RANK="0")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        d = bm.gen_synthetic(bm.SyntheticSpec(64, 64, 1, 30, seed=0))
+        cfg = bm.TrainConfig(k=8, outer_steps=1, grid_i=4, grid_j=4)
+        sched = D.RingSchedule(4, 4, 1)
+        with torch.cuda.stream(torch.cuda.default_stream(0)):
+            with pytest.raises(RuntimeError, match="non-default"):
+                D.GpuShard(d, cfg, sched, 0, 0)
+        s = torch.cuda.Stream(0)
+        with torch.cuda.stream(s):
+            shard = D.GpuShard(d, cfg, sched, 0, 0)
+            assert shard.stream.cuda_stream == s.cuda_stream
+            shard.eng.close()
+    finally:
+        dist.destroy_process_group()
