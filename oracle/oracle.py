@@ -268,9 +268,21 @@ def run_step(P: dict, u, v, step0: int, iters: int, alpha: float, beta: float,
     return sse, bad, int(pos), batches, ids
 
 
+def predict(u, v, rows, cols, chunk: int = 1 << 20) -> np.ndarray:
+    """core.py:163-165 (einsum over gathered rows), evaluated in row chunks:
+    each prediction is the same per-row dot, but the gathers stay at chunk x k
+    instead of materialising nnz x k fp64 twice (2 x 102 GB at C4)."""
+    out = np.empty(len(rows), np.float64)
+    for s in range(0, len(rows), chunk):
+        e = min(len(rows), s + chunk)
+        out[s:e] = np.einsum("ij,ij->i", u[rows[s:e]], v[cols[s:e]])
+    return out
+
+
 def rmse(u, v, rows, cols, vals) -> float:
-    """metrics.py:39-52 (gather + einsum + numpy pairwise sum)."""
-    err = vals - np.einsum("ij,ij->i", u[rows], v[cols])
+    """metrics.py:39-52 (predictions, then numpy's pairwise sum over the whole
+    squared-error vector)."""
+    err = vals - predict(u, v, rows, cols)
     return float(np.sqrt(np.sum(np.square(err)) / len(vals)))
 
 
@@ -285,7 +297,7 @@ def holdout_rmse(u, v, train_rows, train_cols, train_vals, test_rows, test_cols,
     cs[train_cols] = True
     cold = ~(rs[test_rows] & cs[test_cols])
     fb = float(train_vals.mean()) if len(train_vals) else 0.0
-    pred = np.einsum("ij,ij->i", u[test_rows], v[test_cols])
+    pred = predict(u, v, test_rows, test_cols)
     pred[cold] = fb
     err = test_vals - pred
     return float(np.sqrt(np.sum(np.square(err)) / len(test_vals)))

@@ -97,6 +97,14 @@ struct bgmf_ctx {
   size_t work_cap = 0;
   bool in_step = false;                  // between bgmf_step_begin / _end
   int w_cursor = 0;                      // next free work-table slot of the step
+  int w_limit = 0;                       // end of the step's half of the work table
+  // steps ended with bgmf_step_end_async alternate between the two halves of
+  // the pinned work table; ws_done[h] marks the end of the last step that
+  // used half h (its H2D copies read the pinned table when the stream gets
+  // there, so the half is rewritten only after that event)
+  int ws_half = 0;
+  cudaEvent_t ws_done[2] = {nullptr, nullptr};
+  bool ws_pending[2] = {false, false};
   std::vector<int32_t> submitted;        // block id of every step-global plan position
   double* h_sse = nullptr;               // pinned [I*J]
   unsigned long long* h_bad = nullptr;   // pinned [1]
@@ -220,6 +228,8 @@ int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
                float alpha, float beta);
 int step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out);
 int step_end_async(bgmf_ctx* c, double* d_sse_out, unsigned long long* d_bad_out);
+// wait until no asynchronous step's work-table copy is pending (sgd.cu)
+void drain_async_steps(bgmf_ctx* c);
 int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs,
               const int32_t* nbatch, const int32_t* iters, float alpha, float beta,
               double* sse_out, int64_t* bad_out, float* ms_out);

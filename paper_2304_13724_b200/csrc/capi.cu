@@ -176,6 +176,8 @@ void bgmf_destroy(bgmf_ctx* c) {
   cudaSetDevice(c->device);
   prof_mark(c, nullptr);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (int h = 0; h < 2; ++h)
+    if (c->ws_done[h]) cudaEventDestroy(c->ws_done[h]);
   prof_mark(c, "destroy: sync");
   free_factors(c);
   free_holdout(c);

@@ -1022,6 +1022,7 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
                const std::vector<char>* active = nullptr, int w_base = 0, int pos_base = 0,
                bool sse = false) {
   const int total = batch_off[nbatch];
+  if (!c->in_step) drain_async_steps(c);  // synchronous callers rewrite the table from 0
   int rc = ensure_step_scratch(c, (size_t)(w_base + total));
   if (rc) return rc;
   ranges.assign(nbatch, BatchRange{0, 0, 0});
@@ -1243,15 +1244,42 @@ int64_t fast_groups(bgmf_ctx* c) { return sweep_groups(c, shape_for(c->kp)); }
 int step_begin(bgmf_ctx* c, int max_blocks) {
   if (c->exact) return fail(c, BGMF_ERR_STATE, "asynchronous steps are fast-mode only");
   if (c->streaming) return fail(c, BGMF_ERR_STATE, "asynchronous steps do not stream");
-  // each submitted block takes a sweep and an SSE work entry
-  int rc = ensure_step_scratch(c, 2 * (size_t)(max_blocks > 0 ? max_blocks : 1));
+  // each submitted block takes a sweep and an SSE work entry; the table is
+  // split in two halves used by alternate steps (see ws_done)
+  const size_t need = 2 * (size_t)(max_blocks > 0 ? max_blocks : 1);
+  if (2 * need > c->work_cap) drain_async_steps(c);  // about to reallocate the table
+  int rc = ensure_step_scratch(c, 2 * need);
   if (rc) return rc;
+  const int h = c->ws_half ^= 1;
+  if (c->ws_pending[h]) {
+    BGMF_CK(c, cudaEventSynchronize(c->ws_done[h]));
+    c->ws_pending[h] = false;
+  }
+  const int half = (int)(c->work_cap / 2);
   const int nb = c->I * c->J;
   BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, c->stream));
   BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, c->stream));
   c->in_step = true;
-  c->w_cursor = 0;
+  c->w_cursor = h * half;
+  c->w_limit = h * half + half;
   c->submitted.clear();
+  return BGMF_OK;
+}
+
+void drain_async_steps(bgmf_ctx* c) {
+  for (int h = 0; h < 2; ++h)
+    if (c->ws_pending[h]) {
+      cudaEventSynchronize(c->ws_done[h]);
+      c->ws_pending[h] = false;
+    }
+}
+
+// End of a step's use of its work-table half (stream-ordered marker).
+static int mark_half_done(bgmf_ctx* c) {
+  const int h = c->ws_half;
+  if (!c->ws_done[h]) BGMF_CK(c, cudaEventCreateWithFlags(&c->ws_done[h], cudaEventDisableTiming));
+  BGMF_CK(c, cudaEventRecord(c->ws_done[h], c->stream));
+  c->ws_pending[h] = true;
   return BGMF_OK;
 }
 
@@ -1262,7 +1290,7 @@ int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in, in
   const int32_t* batch_off = waves.data();
   const int nbatch = (int)waves.size() - 1;
   const int total = batch_off[nbatch];
-  if ((size_t)(c->w_cursor + 2 * total) > c->work_cap)
+  if (c->w_cursor + 2 * total > c->w_limit)
     return fail(c, BGMF_ERR_ARG, "more blocks than reserved by bgmf_step_begin");
   const Shape sh = shape_for(c->kp);
   const int gpw = 32 / sh.L;
@@ -1321,6 +1349,7 @@ int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs
               double* sse_out, int64_t* bad_out, float* ms_out) {
   if (c->exact) return fail(c, BGMF_ERR_STATE, "bgmf_run_steps is fast-mode only");
   if (c->streaming) return fail(c, BGMF_ERR_STATE, "bgmf_run_steps does not stream");
+  drain_async_steps(c);
   const int nb = c->I * c->J;
   cudaStream_t s = c->stream;
   int64_t total = 0, plan_pos = 0, off_pos = 0;
@@ -1356,6 +1385,7 @@ int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs
   unsigned long long* keep_bad = c->d_bad;
   c->in_step = true;
   c->w_cursor = 0;
+  c->w_limit = (int)c->work_cap;
   c->submitted.clear();
   std::vector<int64_t> pos_end(nsteps);
   plan_pos = off_pos = 0;
@@ -1399,6 +1429,7 @@ int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs
 int step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out) {
   if (!c->in_step) return fail(c, BGMF_ERR_STATE, "bgmf_step_begin has not been called");
   c->in_step = false;
+  if (int rc = mark_half_done(c)) return rc;
   const int nb = c->I * c->J;
   BGMF_CK(c, cudaMemcpyAsync(c->h_sse, c->d_sse, sizeof(double) * nb, cudaMemcpyDeviceToHost,
                              c->stream));
@@ -1427,6 +1458,7 @@ int step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out) {
 int step_end_async(bgmf_ctx* c, double* d_sse_out, unsigned long long* d_bad_out) {
   if (!c->in_step) return fail(c, BGMF_ERR_STATE, "bgmf_step_begin has not been called");
   c->in_step = false;
+  if (int rc = mark_half_done(c)) return rc;
   const int nb = c->I * c->J;
   BGMF_CK(c, cudaMemcpyAsync(d_sse_out, c->d_sse, sizeof(double) * nb, cudaMemcpyDeviceToDevice,
                              c->stream));

@@ -167,3 +167,39 @@ def test_gpu_shard_refuses_the_legacy_default_stream():
             shard.eng.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_world1_nccl_batched_epochs_match_oracle_and_divergence():
+    """Fixed schedule, no early stop, no holdout: the epochs run back to back
+    with device-resident SSEs (bgmf_step_end_async); trace within 1e-3 of the
+    oracle, per-step seconds from CUDA events.  A diverging run raises the
+    same DivergenceError (step, block) batched and per step."""
+    import torch.distributed as dist
+
+    from paper_2304_13724_b200 import distributed as D
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0",
+                      WORLD_SIZE="1", LOCAL_RANK="0")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        r, c, v = workloads.lowrank(6040, 3706, 400_000, seed=7)
+        d = bm.RatingsDataset(6040, 3706, r, c, v)
+        cfg = bm.TrainConfig(k=32, outer_steps=5, grid_i=8, grid_j=8,
+                             inner_schedule=bm.IncreasingEvery(2, 3))
+        model, trace, stop = D.train_blocked_distributed(d, cfg, early_stop=False)
+        _, _, otr, _ = O.train_blocked(d.n, d.m, d.rows, d.cols, d.values, k=32, outer_steps=5,
+                                       grid_i=8, grid_j=8, early_stop=False, nthreads=8,
+                                       schedule="inc:2,3")
+        got = np.array([s.train_rmse for s in trace])
+        assert np.abs(got - [s["train_rmse"] for s in otr]).max() <= 1e-3
+        assert [s.inner_iters for s in trace] == [s["inner_iters"] for s in otr]
+        assert all(s.seconds > 0 for s in trace) and stop == "max_steps"
+        bad = bm.TrainConfig(k=32, outer_steps=3, grid_i=8, grid_j=8, alpha=1e9)
+        errs = []
+        for es in (False, True):  # batched, then per step
+            with pytest.raises(bm.DivergenceError) as ei:
+                D.train_blocked_distributed(d, bad, early_stop=es)
+            errs.append((ei.value.step, ei.value.block))
+        assert errs[0] == errs[1] and errs[0][0] == 1
+    finally:
+        dist.destroy_process_group()
