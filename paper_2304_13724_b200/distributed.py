@@ -245,8 +245,12 @@ class GpuShard:
         # (bgmf_partition_rows), no host-side gather of the dataset
         own = sched.rows_of(rank)
         rb = self.grid.row_bounds
+        t0 = time.perf_counter()
         self.eng.partition(d.rows, d.cols, d.values, d.n, d.m, cfg.grid_i, cfg.grid_j,
                            row_range=(int(rb[own.start]), int(rb[own.stop])))
+        if os.environ.get("BGMF_PROFILE"):
+            print(f"[bgmf]   shard partition call {1e3 * (time.perf_counter() - t0):.2f} ms",
+                  file=__import__("sys").stderr)
         self.local_nnz = self.eng.nnz
         self.k, self.kp = cfg.k, (cfg.k + 3) // 4 * 4
         self.U = torch.zeros((d.n, self.kp), dtype=torch.float32, device=f"cuda:{device}")
@@ -328,11 +332,14 @@ def _train_ring(d, cfg, test, early_stop, options, timing, dist, rank, world, de
     prof = _Phases() if os.environ.get("BGMF_PROFILE") and rank == 0 else None
     sched = RingSchedule(cfg.grid_i, cfg.grid_j, world)
     shard = GpuShard(d, cfg, sched, rank, device, options)
-    shard.eng.init_factors(d.n, d.m, cfg.k, cfg.seed)
-    shard.eng.prefault_factors()  # the model's host pages fault in while the epochs run
     if prof:
         torch.cuda.synchronize()
-        prof.mark("shard: partition + factors")
+        prof.mark("shard: partition + U/V buffers")
+    shard.eng.init_factors(d.n, d.m, cfg.k, cfg.seed)
+    if prof:
+        torch.cuda.synchronize()
+        prof.mark("init_factors")
+    shard.eng.prefault_factors()  # the model's host pages fault in while the epochs run
     evaluator = HoldoutEvaluator(d, test) if test is not None and len(test) > 0 else None
     if evaluator is not None:
         t = evaluator.test
