@@ -74,17 +74,52 @@ class RingSchedule:
         return [(bi, bj) for bi, bj in batch if self.owner(bi) == rank]
 
 
+def _staged(dist, t) -> bool:
+    """CUDA tensor on a non-NCCL process group (gloo: several ranks sharing one
+    GPU in tests): collectives go through host copies."""
+    return getattr(t, "is_cuda", False) and dist.get_backend() != "nccl"
+
+
+def _all_reduce(dist, t, op=None) -> None:
+    op = dist.ReduceOp.SUM if op is None else op
+    if _staged(dist, t):
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op)
+
+
+def _broadcast(dist, t, src: int) -> None:
+    if _staged(dist, t):
+        h = t.cpu()
+        dist.broadcast(h, src=src)
+        t.copy_(h)
+    else:
+        dist.broadcast(t, src=src)
+
+
 def exchange(moves, rank: int, v_slice, dist) -> None:
-    """Run one batch's V moves: isend what this rank holds, irecv what it needs."""
-    ops = []
+    """Run one batch's V moves: isend what this rank holds, irecv what it needs.
+    On NCCL the moves are ordered on the current stream (no host wait); on gloo
+    with CUDA tensors they are staged through host buffers."""
+    ops, back = [], []
     for mv in moves:
         if mv.src == rank:
-            ops.append(dist.P2POp(dist.isend, v_slice(mv.col), mv.dst))
+            t = v_slice(mv.col)
+            ops.append(dist.P2POp(dist.isend, t.cpu() if _staged(dist, t) else t, mv.dst))
         elif mv.dst == rank:
-            ops.append(dist.P2POp(dist.irecv, v_slice(mv.col), mv.src))
+            t = v_slice(mv.col)
+            if _staged(dist, t):
+                h = t.new_empty(t.shape, device="cpu")
+                back.append((t, h))
+                t = h
+            ops.append(dist.P2POp(dist.irecv, t, mv.src))
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()
+    for t, h in back:
+        t.copy_(h)
 
 
 def sync_all_v(sched: RingSchedule, rank: int, v_slice, dist) -> None:
@@ -92,7 +127,7 @@ def sync_all_v(sched: RingSchedule, rank: int, v_slice, dist) -> None:
     for j in range(sched.J):
         src = sched.holder[j]
         if src is not None:
-            dist.broadcast(v_slice(j), src=src)
+            _broadcast(dist, v_slice(j), src)
 
 
 def shard_rows(rows: np.ndarray, row_bounds: np.ndarray, sched: RingSchedule, rank: int):
@@ -169,13 +204,13 @@ def _run_epochs_batched(sched: RingSchedule, shard, rank: int, dist, cfg, nb: in
             if mine:
                 shard.run_batch(mine, g, cfg.alpha, cfg.beta)
         subs.append(shard.end_epoch_async(sse[k], bad[k]))
-        dist.all_reduce(sse[k])
+        _all_reduce(dist, sse[k])
         orders.append(order)
         gs.append(g)
         if ev:
             ev[k + 1].record(shard.stream)
     flag = (bad != -1).to(torch.int64)
-    dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+    _all_reduce(dist, flag, dist.ReduceOp.MAX)
     sse_h, bad_h, flag_h = sse.cpu().numpy(), bad.cpu().numpy(), flag.cpu().numpy()
     out = []
     for k in range(S):
@@ -293,8 +328,8 @@ class GpuShard:
 def _init_dist():
     import torch.distributed as dist
 
-    if not dist.is_initialized():
-        dist.init_process_group(backend="nccl")
+    if not dist.is_initialized():  # BGMF_DIST_BACKEND=gloo: tests, ranks sharing a GPU
+        dist.init_process_group(backend=os.environ.get("BGMF_DIST_BACKEND", "nccl"))
     return dist
 
 
@@ -311,7 +346,7 @@ def train_blocked_distributed(d, cfg, test=None, *, early_stop: bool = True, opt
 
     dist = _init_dist()
     rank, world = dist.get_rank(), dist.get_world_size()
-    device = int(os.environ.get("LOCAL_RANK", rank))
+    device = int(os.environ.get("BGMF_DEVICE", os.environ.get("LOCAL_RANK", rank)))
     torch.cuda.set_device(device)
     # the engine's kernels, the NCCL V moves and the torch ops must share ONE
     # stream (NCCL orders against torch's current stream; a context created on
@@ -351,7 +386,7 @@ def _train_ring(d, cfg, test, early_stop, options, timing, dist, rank, world, de
     stop = "max_steps"
     total_counts = np.zeros(nb, np.int64)
     cnt = torch.tensor(shard.counts, dtype=torch.int64, device=f"cuda:{device}")
-    dist.all_reduce(cnt)
+    _all_reduce(dist, cnt)
     total_counts[:] = cnt.cpu().numpy()
     from .core import AdaptiveDecreasing
 
@@ -360,7 +395,7 @@ def _train_ring(d, cfg, test, early_stop, options, timing, dist, rank, world, de
     if adaptive and int(total_counts.sum()):
         # RMSE of the initial factors over all ranks' ratings (trainer.py:98-100)
         s0 = torch.tensor([shard.eng.train_sse()], dtype=torch.float64, device=f"cuda:{device}")
-        dist.all_reduce(s0)
+        _all_reduce(dist, s0)
         hist = [math.sqrt(float(s0.item()) / int(total_counts.sum()))]
     from .core import ConvergeEachBlock
 
@@ -387,19 +422,19 @@ def _train_ring(d, cfg, test, early_stop, options, timing, dist, rank, world, de
             agg = torch.tensor([float(its.max()) if len(its) else 0.0, float(cap)],
                                dtype=torch.float64, device=f"cuda:{device}")
             mx = agg[:1].clone()
-            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            _all_reduce(dist, mx, dist.ReduceOp.MAX)
             sm = agg[1:].clone()
-            dist.all_reduce(sm)
+            _all_reduce(dist, sm)
             max_iters, capped = int(mx.item()), int(sm.item())
         else:
             sse_all, order, bad_any = run_epoch(sched, shard, rank, dist, step - 1, g, cfg.alpha,
                                                 cfg.beta, nb, cfg.grid_j)
         if pre is None:
             red = torch.tensor(sse_all, device=f"cuda:{device}")
-            dist.all_reduce(red)
+            _all_reduce(dist, red)
             sse_all = red.cpu().numpy()
             flag = torch.tensor([0 if bad_any is None else 1], device=f"cuda:{device}")
-            dist.all_reduce(flag)
+            _all_reduce(dist, flag)
             any_bad = bool(int(flag.item()))
         if any_bad or not np.all(np.isfinite(sse_all[order])):
             b = bad_any[0] if bad_any else int(next(o for o in order
@@ -419,7 +454,7 @@ def _train_ring(d, cfg, test, early_stop, options, timing, dist, rank, world, de
             sync_all_v(sched, rank, shard.v_slice, dist)  # every rank needs all of V
             hs = torch.tensor([shard.eng.holdout_sse()], dtype=torch.float64,
                               device=f"cuda:{device}")
-            dist.all_reduce(hs)
+            _all_reduce(dist, hs)
             test_rmse = math.sqrt(float(hs.item()) / len(evaluator.test))
         seconds = (secs if pre is not None else time.perf_counter() - t0) if timing else 0.0
         trace.append(TraceStep(step, train_rmse, test_rmse, seconds, max_iters, capped))
@@ -440,7 +475,7 @@ def _train_ring(d, cfg, test, early_stop, options, timing, dist, rank, world, de
         for r in range(world):
             rows = sched.rows_of(r)
             if len(rows):
-                dist.broadcast(shard.u_rows(rows), src=r)
+                _broadcast(dist, shard.u_rows(rows), r)
     torch.cuda.synchronize()
     if prof:
         prof.mark("gather (NCCL)")
