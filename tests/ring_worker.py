@@ -20,6 +20,16 @@ def main(out_path: str, case: str) -> None:
     test = None
     if case == "holdout":
         d, test = bm.split(d, 0.2, seed=3)
+    if case.startswith("diverge"):  # every rank must raise the same step
+        cfg = bm.TrainConfig(k=32, outer_steps=3, grid_i=8, grid_j=8, alpha=1e9)
+        try:
+            D.train_blocked_distributed(d, cfg, early_stop=case.endswith("es"))
+            err = None
+        except bm.DivergenceError as e:
+            err = {"step": e.step, "block": list(e.block) if e.block else None,
+                   "partial": len(e.partial_trace)}
+        json.dump(err, open(f"{out_path}.{os.environ['RANK']}", "w"))
+        return
     sched = {"const": bm.Constant(1), "inc": bm.IncreasingEvery(2, 3),
              "converge": bm.ConvergeEachBlock(0.5), "holdout": bm.Constant(1)}[case]
     cfg = bm.TrainConfig(k=32, outer_steps=4, grid_i=8, grid_j=8, inner_schedule=sched)

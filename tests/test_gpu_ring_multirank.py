@@ -29,6 +29,15 @@ def _port():
         return s.getsockname()[1]
 
 
+def _launch(world: int, case: str, out) -> None:
+    env = dict(os.environ, BGMF_DIST_BACKEND="gloo", BGMF_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           os.path.join(ROOT, "tests", "ring_worker.py"), str(out), case]
+    p = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+
+
 def _run(world: int, case: str, tmp_path) -> dict:
     out = tmp_path / f"ring_{world}_{case}.json"
     env = dict(os.environ, BGMF_DIST_BACKEND="gloo", BGMF_DEVICE="0")
@@ -69,3 +78,16 @@ def test_ring_ranks_share_one_gpu_match_oracle(world, case, tmp_path):
     # the gathered model is the trained one: its full-set RMSE sits at the
     # last epoch's trace value (post-sweep SSEs) up to the last epoch's drift
     assert abs(got["rmse"] - got["train"][-1]) < 0.05
+
+
+@pytest.mark.parametrize("case", ["diverge", "diverge-es"], ids=["batched", "per-step"])
+def test_ring_divergence_raises_on_every_rank(case, tmp_path):
+    """alpha = 1e9 blows up in step 1: every rank raises DivergenceError at
+    step 1 (batched epochs and per-step loop) with a block of the grid."""
+    out = tmp_path / "div.json"
+    _launch(2, case, out)
+    errs = [json.load(open(f"{out}.{r}")) for r in range(2)]
+    for e in errs:
+        assert e is not None and e["step"] == 1 and e["partial"] == 0
+        assert e["block"] is not None and 0 <= e["block"][0] < 8 and 0 <= e["block"][1] < 8
+
