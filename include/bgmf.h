@@ -305,6 +305,29 @@ int bgmf_sse(const double* u, int64_t n, const double* v, int64_t m, int k,
              const int64_t* rows, const int64_t* cols, const double* vals,
              const uint8_t* cold, double fallback, int64_t count, double* sse);
 
+/* Peer transport of the multi-GPU ring (no reference counterpart; replaces
+ * an NCCL send/recv pair per V-block move, distributed.py).  Ranks map each
+ * other's V buffers and flag words once through CUDA IPC (also between
+ * processes sharing one GPU); a move is then a copy straight into the
+ * receiver's rows plus a release-store of a sequence number into its flag,
+ * and the receiver's stream waits (acquire) for that number before its next
+ * sweep -- all stream-ordered, no host round trip per batch.
+ *   bgmf_peer_alloc  -- zeroed, IPC-exportable device memory owned by ctx
+ *                       (freed by bgmf_destroy);
+ *   bgmf_peer_handle -- BGMF_PEER_HANDLE_BYTES of IPC handle for such a base;
+ *   bgmf_peer_open   -- map a peer's handle (unmapped by bgmf_destroy);
+ *   bgmf_peer_push   -- on ctx's stream: copy `bytes` src -> dst (a peer
+ *                       address), then *peer_flag = value (system scope);
+ *   bgmf_peer_wait   -- on ctx's stream: block later work until *flag >= value
+ *                       (wrap-safe comparison). */
+#define BGMF_PEER_HANDLE_BYTES 64
+int bgmf_peer_alloc(bgmf_ctx* ctx, int64_t bytes, void** out);
+int bgmf_peer_handle(bgmf_ctx* ctx, void* base, uint8_t* handle_out);
+int bgmf_peer_open(bgmf_ctx* ctx, const uint8_t* handle, void** out);
+int bgmf_peer_push(bgmf_ctx* ctx, void* dst, const void* src, int64_t bytes,
+                   uint32_t* peer_flag, uint32_t value);
+int bgmf_peer_wait(bgmf_ctx* ctx, const uint32_t* flag, uint32_t value);
+
 /* Measurement only (no reference counterpart): the SM<->L2 ceiling of the
  * sweep's access pattern on `device` -- `ratings` random 512-byte rows of an
  * L2-resident rows x 128 fp32 matrix, read (mode 0), read + reduce-added into

@@ -59,6 +59,12 @@ SIGNATURES = {
     "bgmf_step_batch": (_i, [_ctx, _i32p, _i32p, _i, _i, _d, _d]),
     "bgmf_step_end": (_i, [_ctx, _f64p, _i64p]),
     "bgmf_step_end_async": (_i, [_ctx, ctypes.c_void_p, ctypes.c_void_p]),
+    "bgmf_peer_alloc": (_i, [_ctx, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "bgmf_peer_handle": (_i, [_ctx, ctypes.c_void_p, ctypes.c_char_p]),
+    "bgmf_peer_open": (_i, [_ctx, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "bgmf_peer_push": (_i, [_ctx, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                            ctypes.c_void_p, ctypes.c_uint32]),
+    "bgmf_peer_wait": (_i, [_ctx, ctypes.c_void_p, ctypes.c_uint32]),
     "bgmf_run_sync_parallel_step": (_i, [_ctx, _i64p, _i, _d, _d, _f64p, _i64p]),
     "bgmf_run_step_converge": (_i, [_ctx, _i32p, _i32p, _i, _d, _l, _d, _d, _f64p, _i64p,
                                     _i32p, _i64p]),

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -81,6 +82,8 @@ struct bgmf_ctx {
 
   // factors
   int k = 0, kp = 0;
+  // peer transport (peer.cu): IPC-exportable buffers and mapped peer buffers
+  std::vector<void*> peer_owned, peer_opened;
   bool have_factors = false, bound = false;
   float* d_u = nullptr;
   float* d_v = nullptr;
@@ -230,6 +233,8 @@ int step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out);
 int step_end_async(bgmf_ctx* c, double* d_sse_out, unsigned long long* d_bad_out);
 // wait until no asynchronous step's work-table copy is pending (sgd.cu)
 void drain_async_steps(bgmf_ctx* c);
+// unmap peer buffers, free IPC-exportable ones (peer.cu)
+void peer_release(bgmf_ctx* c);
 int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs,
               const int32_t* nbatch, const int32_t* iters, float alpha, float beta,
               double* sse_out, int64_t* bad_out, float* ms_out);

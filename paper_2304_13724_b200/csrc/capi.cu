@@ -178,6 +178,7 @@ void bgmf_destroy(bgmf_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (int h = 0; h < 2; ++h)
     if (c->ws_done[h]) cudaEventDestroy(c->ws_done[h]);
+  peer_release(c);
   prof_mark(c, "destroy: sync");
   free_factors(c);
   free_holdout(c);

@@ -303,6 +303,31 @@ class Engine:
         self._check(self._L.bgmf_step_end_async(self._h, ctypes.c_void_p(d_sse),
                                                 ctypes.c_void_p(d_bad)))
 
+    # ------------------------------------------------------------ peer transport
+    def peer_alloc(self, nbytes: int) -> int:
+        """Zeroed IPC-exportable device memory owned by this context."""
+        p = ctypes.c_void_p()
+        self._check(self._L.bgmf_peer_alloc(self._h, int(nbytes), ctypes.byref(p)))
+        return int(p.value)
+
+    def peer_handle(self, base: int) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        self._check(self._L.bgmf_peer_handle(self._h, ctypes.c_void_p(base), buf))
+        return buf.raw
+
+    def peer_open(self, handle: bytes) -> int:
+        p = ctypes.c_void_p()
+        self._check(self._L.bgmf_peer_open(self._h, handle, ctypes.byref(p)))
+        return int(p.value)
+
+    def peer_push(self, dst: int, src: int, nbytes: int, peer_flag: int, value: int):
+        self._check(self._L.bgmf_peer_push(self._h, ctypes.c_void_p(dst), ctypes.c_void_p(src),
+                                           int(nbytes), ctypes.c_void_p(peer_flag),
+                                           value & 0xFFFFFFFF))
+
+    def peer_wait(self, flag: int, value: int):
+        self._check(self._L.bgmf_peer_wait(self._h, ctypes.c_void_p(flag), value & 0xFFFFFFFF))
+
     def run_sync_parallel_step(self, edges: np.ndarray, alpha: float, beta: float):
         """CPMF step on a 1x1 partition; returns (per-shard SSE, bad) where
         bad = (shard, entry, iteration) or None."""

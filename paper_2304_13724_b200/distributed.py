@@ -155,7 +155,7 @@ def run_epoch(sched: RingSchedule, shard, rank: int, dist, step0: int, g: int,
     if begin is not None:
         begin(nb)
     for batch in sched.batches(step0):
-        exchange(sched.transfers_for(batch), rank, shard.v_slice, dist)
+        _move_v(sched.transfers_for(batch), rank, shard, dist)
         order.extend(bi * J + bj for bi, bj in batch)
         mine = sched.local_blocks(batch, rank)
         if mine:
@@ -198,7 +198,7 @@ def _run_epochs_batched(sched: RingSchedule, shard, rank: int, dist, cfg, nb: in
         order: list[int] = []
         shard.begin_epoch(nb)
         for batch in sched.batches(k):
-            exchange(sched.transfers_for(batch), rank, shard.v_slice, dist)
+            _move_v(sched.transfers_for(batch), rank, shard, dist)
             order.extend(bi * J + bj for bi, bj in batch)
             mine = sched.local_blocks(batch, rank)
             if mine:
@@ -238,7 +238,7 @@ def _run_epoch_converge(sched: RingSchedule, shard, rank: int, dist, step0: int,
     iters_used = []
     capped = 0
     for batch in sched.batches(step0):
-        exchange(sched.transfers_for(batch), rank, shard.v_slice, dist)
+        _move_v(sched.transfers_for(batch), rank, shard, dist)
         order.extend(bi * J + bj for bi, bj in batch)
         mine = sched.local_blocks(batch, rank)
         if mine:
@@ -256,11 +256,80 @@ def _run_epoch_converge(sched: RingSchedule, shard, rank: int, dist, step0: int,
 # ---------------------------------------------------------------------------- GPU
 
 
+class _DeviceArray:
+    """A raw device allocation seen by torch (``torch.as_tensor``) through
+    ``__cuda_array_interface__``; the memory stays owned by the engine."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 2, "strides": None}
+
+
+class _PeerLinks:
+    """The ring's V moves over peer memory (csrc/peer.cu): every rank maps the
+    other ranks' V buffers and flag words once (CUDA IPC handles exchanged with
+    all_gather_object); a move src -> dst is a copy into dst's V rows plus a
+    release-store of the link's sequence number into dst's flag[src], and dst's
+    stream waits for that number before its next sweep."""
+
+    def __init__(self, eng, vptr: int, kp: int, col_bounds, dist):
+        self.eng, self.vptr, self.kp, self.cb = eng, vptr, kp, col_bounds
+        world, rank = dist.get_world_size(), dist.get_rank()
+        self.rank = rank
+        self.flags = eng.peer_alloc(4 * world)  # flags[s]: moves s -> me done
+        mine = (eng.peer_handle(vptr), eng.peer_handle(self.flags))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine)
+        self.peer_v, self.peer_flags = {}, {}
+        for r in range(world):
+            if r != rank:
+                self.peer_v[r] = eng.peer_open(allh[r][0])
+                self.peer_flags[r] = eng.peer_open(allh[r][1])
+        self.sent = [0] * world
+        self.got = [0] * world
+        dist.barrier()  # every rank's flags are zero and mapped before any move
+
+    def move(self, moves) -> None:
+        """One batch's moves: all pushes first, then the waits (a wait blocks
+        the stream; pushing after it could deadlock two ranks)."""
+        for mv in moves:
+            if mv.src == self.rank:
+                self.sent[mv.dst] += 1
+                lo, hi = int(self.cb[mv.col]), int(self.cb[mv.col + 1])
+                off, nbytes = lo * self.kp * 4, (hi - lo) * self.kp * 4
+                self.eng.peer_push(self.peer_v[mv.dst] + off, self.vptr + off, nbytes,
+                                   self.peer_flags[mv.dst] + 4 * self.rank, self.sent[mv.dst])
+        for mv in moves:
+            if mv.dst == self.rank:
+                self.got[mv.src] += 1
+                self.eng.peer_wait(self.flags + 4 * mv.src, self.got[mv.src])
+
+
+def _transport(world: int) -> str:
+    """V-move transport of the ring: "peer" (default: IPC-mapped peer memory,
+    csrc/peer.cu) or "dist" (torch.distributed P2P); BGMF_RING_TRANSPORT picks."""
+    if world <= 1:
+        return "dist"  # nothing moves
+    t = os.environ.get("BGMF_RING_TRANSPORT", "peer")
+    return "dist" if t in ("dist", "nccl") else t
+
+
+def _move_v(moves, rank: int, shard, dist) -> None:
+    """A batch's V moves: over peer memory when the shard has links, else
+    through torch.distributed (NCCL P2P, or gloo staged through the host)."""
+    peer = getattr(shard, "peer", None)
+    if peer is not None:
+        peer.move(moves)
+    else:
+        exchange(moves, rank, shard.v_slice, dist)
+
+
 class GpuShard:
     """This rank's engine: its ratings, full-size U/V buffers (torch-allocated
     so NCCL can move V slices), bound into libbgmf with bgmf_bind_factors."""
 
-    def __init__(self, d, cfg, sched: RingSchedule, rank: int, device: int, options=None):
+    def __init__(self, d, cfg, sched: RingSchedule, rank: int, device: int, options=None,
+                 transport: str = "nccl", dist=None):
         import torch
 
         from .device import Engine, EngineOptions
@@ -289,7 +358,15 @@ class GpuShard:
         self.local_nnz = self.eng.nnz
         self.k, self.kp = cfg.k, (cfg.k + 3) // 4 * 4
         self.U = torch.zeros((d.n, self.kp), dtype=torch.float32, device=f"cuda:{device}")
-        self.V = torch.zeros((d.m, self.kp), dtype=torch.float32, device=f"cuda:{device}")
+        self.peer = None
+        if transport == "peer":  # else "dist": torch.distributed P2P (NCCL, or staged gloo)
+            # V in IPC-exportable memory; peers write moved blocks straight into it
+            vptr = self.eng.peer_alloc(d.m * self.kp * 4)
+            self.V = torch.as_tensor(_DeviceArray(vptr, (d.m, self.kp), "<f4"),
+                                     device=f"cuda:{device}")
+            self.peer = _PeerLinks(self.eng, vptr, self.kp, self.grid.col_bounds, dist)
+        else:
+            self.V = torch.zeros((d.m, self.kp), dtype=torch.float32, device=f"cuda:{device}")
         self.eng.bind_factors(self.U.data_ptr(), self.V.data_ptr(), d.n, d.m, cfg.k, self.kp)
         self.counts = np.diff(self.eng.offsets)
 
@@ -366,7 +443,7 @@ def _train_ring(d, cfg, test, early_stop, options, timing, dist, rank, world, de
 
     prof = _Phases() if os.environ.get("BGMF_PROFILE") and rank == 0 else None
     sched = RingSchedule(cfg.grid_i, cfg.grid_j, world)
-    shard = GpuShard(d, cfg, sched, rank, device, options)
+    shard = GpuShard(d, cfg, sched, rank, device, options, _transport(world), dist)
     if prof:
         torch.cuda.synchronize()
         prof.mark("shard: partition + U/V buffers")
@@ -482,6 +559,9 @@ def _train_ring(d, cfg, test, early_stop, options, timing, dist, rank, world, de
     u, v = shard.eng.get_factors()
     if prof:
         prof.mark("get_factors (D2H)")
+    if shard.peer is not None:  # no rank unmaps/frees while a peer could still touch it
+        torch.cuda.synchronize()
+        dist.barrier()
     shard.eng.close()
     if prof:
         prof.mark("close")
@@ -524,7 +604,8 @@ def bench_main(args, clock_sampler=None):
                       seed=w.seed)
     sched = RingSchedule(w.grid, w.grid, world)
     torch.cuda.set_stream(torch.cuda.Stream(device))  # one stream: kernels + NCCL (GpuShard)
-    shard = GpuShard(d, cfg, sched, rank, device, EngineOptions(timing=False))
+    shard = GpuShard(d, cfg, sched, rank, device, EngineOptions(timing=False), _transport(world),
+                     dist)
     del r, c, v
     shard.eng.init_factors(w.n, w.m, w.k, w.seed)
     stream = shard.stream

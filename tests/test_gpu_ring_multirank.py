@@ -1,7 +1,8 @@
 """The GPU ring trainer (U-resident / V-rotating, distributed.py) at world
 sizes 2 and 4 on the ONE GPU of this box: ranks share the device over gloo
-(NCCL refuses two ranks on one GPU), with every V move, broadcast and
-all-reduce staged through host memory.  What runs on the GPU is the real
+(NCCL refuses two ranks on one GPU): V moves go through IPC-mapped peer
+memory (the default transport, csrc/peer.cu) or torch.distributed P2P staged
+through the host; broadcasts and all-reduces are staged through the host.  What runs on the GPU is the real
 multi-rank path -- row-sharded uploads (bgmf_partition_rows), bound torch
 factor buffers, per-batch V rotation between ranks, asynchronous steps,
 the final U/V gather -- checked against the oracle's single-process trace."""
@@ -29,8 +30,9 @@ def _port():
         return s.getsockname()[1]
 
 
-def _launch(world: int, case: str, out) -> None:
-    env = dict(os.environ, BGMF_DIST_BACKEND="gloo", BGMF_DEVICE="0")
+def _launch(world: int, case: str, out, transport: str = "peer") -> None:
+    env = dict(os.environ, BGMF_DIST_BACKEND="gloo", BGMF_DEVICE="0",
+               BGMF_RING_TRANSPORT=transport)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
            os.path.join(ROOT, "tests", "ring_worker.py"), str(out), case]
@@ -38,14 +40,9 @@ def _launch(world: int, case: str, out) -> None:
     assert p.returncode == 0, p.stderr[-3000:]
 
 
-def _run(world: int, case: str, tmp_path) -> dict:
-    out = tmp_path / f"ring_{world}_{case}.json"
-    env = dict(os.environ, BGMF_DIST_BACKEND="gloo", BGMF_DEVICE="0")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
-           os.path.join(ROOT, "tests", "ring_worker.py"), str(out), case]
-    p = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0, p.stderr[-3000:]
+def _run(world: int, case: str, tmp_path, transport: str = "peer") -> dict:
+    out = tmp_path / f"ring_{world}_{case}_{transport}.json"
+    _launch(world, case, out, transport)
     return json.load(open(out))
 
 
@@ -64,10 +61,14 @@ def _oracle(case: str):
     return otr
 
 
-@pytest.mark.parametrize("world,case", [(2, "const"), (4, "const"), (2, "inc"),
-                                        (2, "converge"), (3, "holdout")])
-def test_ring_ranks_share_one_gpu_match_oracle(world, case, tmp_path):
-    got = _run(world, case, tmp_path)
+@pytest.mark.parametrize("world,case,transport",
+                         [(2, "const", "peer"), (4, "const", "peer"), (2, "inc", "peer"),
+                          (2, "converge", "peer"), (3, "holdout", "peer"),
+                          (2, "const", "dist"), (3, "holdout", "dist")])
+def test_ring_ranks_share_one_gpu_match_oracle(world, case, transport, tmp_path):
+    """transport "peer": V moves through IPC-mapped peer memory (the default);
+    "dist": torch.distributed P2P (staged through the host on gloo)."""
+    got = _run(world, case, tmp_path, transport)
     otr = _oracle(case)
     assert np.abs(np.array(got["train"]) - [s["train_rmse"] for s in otr]).max() <= 1e-3
     if case == "holdout":
