@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import math
 import os
+import sys
 import time
 from dataclasses import dataclass
 
@@ -325,11 +326,13 @@ def _move_v(moves, rank: int, shard, dist) -> None:
 
 
 class GpuShard:
-    """This rank's engine: its ratings, full-size U/V buffers (torch-allocated
-    so NCCL can move V slices), bound into libbgmf with bgmf_bind_factors."""
+    """This rank's engine: its ratings and full-size U/V buffers, bound into
+    libbgmf with bgmf_bind_factors.  U is a torch tensor; V too for the "dist"
+    transport (NCCL moves V slices), or IPC-exportable engine memory seen as a
+    torch tensor for the "peer" transport (peers write moved blocks into it)."""
 
     def __init__(self, d, cfg, sched: RingSchedule, rank: int, device: int, options=None,
-                 transport: str = "nccl", dist=None):
+                 transport: str = "dist", dist=None):
         import torch
 
         from .device import Engine, EngineOptions
@@ -340,7 +343,7 @@ class GpuShard:
         self.stream = torch.cuda.current_stream(device)
         if self.stream.cuda_stream == 0:
             raise RuntimeError("GpuShard needs a non-default current stream (torch.cuda.stream(...)):"
-                               " its kernels, the NCCL V moves and torch ops must share it")
+                               " its kernels, the V moves and torch ops must share it")
         opts = options or EngineOptions()
         opts = EngineOptions(exact=False, min_chunk=opts.min_chunk, device=device,
                              timing=opts.timing, warps_per_sm=opts.warps_per_sm)
@@ -354,7 +357,7 @@ class GpuShard:
                            row_range=(int(rb[own.start]), int(rb[own.stop])))
         if os.environ.get("BGMF_PROFILE"):
             print(f"[bgmf]   shard partition call {1e3 * (time.perf_counter() - t0):.2f} ms",
-                  file=__import__("sys").stderr)
+                  file=sys.stderr)
         self.local_nnz = self.eng.nnz
         self.k, self.kp = cfg.k, (cfg.k + 3) // 4 * 4
         self.U = torch.zeros((d.n, self.kp), dtype=torch.float32, device=f"cuda:{device}")
@@ -582,8 +585,6 @@ def bench_main(args, clock_sampler=None):
 
     # NCCL / torch print banners on stdout; the driver reads ONE JSON line
     # there, so stdout is parked on stderr until that line is written
-    import sys
-
     sys.stdout.flush()
     json_fd = os.dup(1)
     os.dup2(2, 1)
