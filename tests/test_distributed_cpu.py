@@ -175,3 +175,90 @@ def test_row_ownership_covers_grid():
             assert owned == list(range(I))
             assert all(s.owner(r) == g for g in range(G) for r in s.rows_of(g))
             assert math.ceil(I / G) == s.R
+
+
+class _FakePeerEngine:
+    """Records the peer-transport calls a rank makes (no GPU)."""
+
+    def __init__(self, rank):
+        self.rank, self.calls, self._next = rank, [], 1 << 20
+
+    def peer_alloc(self, nbytes):
+        self._next += 1 << 30
+        return self._next
+
+    def peer_handle(self, base):
+        return f"{self.rank}:{base}".encode()
+
+    def peer_open(self, handle):  # mapping of rank r's base b: 10^12 (r+1) + b
+        r, b = handle.split(b":")
+        return 10 ** 12 * (int(r) + 1) + int(b)
+
+    def peer_push(self, dst, src, nbytes, flag, value):
+        self.calls.append(("push", dst, src, nbytes, flag, value))
+
+    def peer_wait(self, flag, value):
+        self.calls.append(("wait", flag, value))
+
+
+class _FakeDist:
+    def __init__(self, world, rank):
+        self.world, self.rank = world, rank
+
+    def get_world_size(self):
+        return self.world
+
+    def get_rank(self):
+        return self.rank
+
+    def all_gather_object(self, out, obj):  # every rank's handles (same bases per rank)
+        for r in range(self.world):
+            out[r] = tuple(h.replace(f"{self.rank}:".encode(), f"{r}:".encode()) for h in obj)
+
+    def barrier(self):
+        pass
+
+
+@pytest.mark.parametrize("world,P", [(2, 8), (4, 16), (3, 7)])
+def test_peer_links_sequence_and_order(world, P):
+    """The peer transport's host logic over several epochs of the ring: per
+    batch every push precedes every wait (a wait blocks the stream); each push
+    targets the receiver's rows of that column and its flag[sender]; the k-th
+    wait of receiver d on sender s expects exactly the k-th push s -> d."""
+    kp, m = 8, 7 * P + 3
+    cb = bm.split_bounds(m, P)
+    sched = D.RingSchedule(P, P, world)
+    links = []
+    for r in range(world):
+        eng = _FakePeerEngine(r)
+        links.append(D._PeerLinks(eng, 5000, kp, cb, _FakeDist(world, r)))
+    vmap = lambda d: 10 ** 12 * (d + 1) + 5000  # noqa: E731  rank d's V, mapped
+    fmap = lambda d: 10 ** 12 * (d + 1) + links[d].flags  # noqa: E731
+    pushes = {(s, d): [] for s in range(world) for d in range(world)}
+    waits = {(s, d): [] for s in range(world) for d in range(world)}
+    for step0 in range(3):
+        for batch in sched.batches(step0):
+            moves = sched.transfers_for(batch)
+            for r, lk in enumerate(links):
+                n0 = len(lk.eng.calls)
+                lk.move(moves)
+                kinds = [c[0] for c in lk.eng.calls[n0:]]
+                assert kinds == sorted(kinds, key=lambda k: k != "push")  # pushes first
+                for c in lk.eng.calls[n0:]:
+                    if c[0] == "push":
+                        _, dst, src, nbytes, flag, value = c
+                        mv = next(mv for mv in moves if mv.src == r and
+                                  dst == vmap(mv.dst) + int(cb[mv.col]) * kp * 4)
+                        d = mv.dst
+                        assert src - 5000 == dst - vmap(d)  # same rows, sender -> receiver
+                        assert nbytes == int(cb[mv.col + 1] - cb[mv.col]) * kp * 4
+                        assert flag == fmap(d) + 4 * r
+                        pushes[(r, d)].append(value)
+                    else:
+                        _, flag, value = c
+                        s = (flag - lk.flags) // 4
+                        waits[(s, r)].append(value)
+    for key in pushes:
+        assert pushes[key] == list(range(1, len(pushes[key]) + 1))
+        assert waits[key] == pushes[key]
+    assert sum(len(v) for v in pushes.values()) > 0
