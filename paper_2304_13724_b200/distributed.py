@@ -345,6 +345,9 @@ class GpuShard:
             raise RuntimeError("GpuShard needs a non-default current stream (torch.cuda.stream(...)):"
                                " its kernels, the V moves and torch ops must share it")
         opts = options or EngineOptions()
+        if opts.exact:
+            raise ValueError("the multi-GPU ring runs the fast kernels only; exact (fp64, "
+                             "reference-order) training is single-GPU: train_blocked")
         opts = EngineOptions(exact=False, min_chunk=opts.min_chunk, device=device,
                              timing=opts.timing, warps_per_sm=opts.warps_per_sm)
         self.eng = Engine(opts, stream=self.stream.cuda_stream)
