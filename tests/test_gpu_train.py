@@ -267,3 +267,31 @@ def test_run_steps_batched_matches_per_step_loop():
             bm.train_blocked(d, cfg, early_stop=es)
         errs.append((ei.value.step, ei.value.block))
     assert errs[0] == errs[1] and errs[0][0] == 1
+
+
+@pytest.mark.parametrize("sched,spec", [
+    (bm.Constant(2), "const:2"), (bm.IncreasingEvery(2, 3), "inc:2,3"),
+    (bm.Decreasing(3), "dec:3"), (bm.AdaptiveDecreasing(3), "adaptive:3"),
+    (bm.ConvergeEachBlock(0.05), "converge:0.05")], ids=lambda x: str(x)[:12])
+def test_every_schedule_with_holdout_vs_oracle(sched, spec):
+    """C2-shaped data (k=32, 8x8) with an 80/20 split, fast mode, every inner
+    schedule of trainer.py:52-73: per-epoch train and test RMSE within 1e-3 of
+    the oracle, the same inner-iteration counts (and capped blocks for
+    converge, whose per-block sweep counts can differ by one where an
+    improvement sits at the tolerance)."""
+    r, c, v = workloads.lowrank(6040, 3706, 300_000, seed=21)
+    d, te = bm.split(bm.RatingsDataset(6040, 3706, r, c, v), 0.2, seed=2)
+    cfg = bm.TrainConfig(k=32, outer_steps=5, grid_i=8, grid_j=8, inner_schedule=sched)
+    res = bm.train_blocked(d, cfg, te, early_stop=False)
+    _, _, otr, _ = O.train_blocked(d.n, d.m, d.rows, d.cols, d.values, k=32, outer_steps=5,
+                                   grid_i=8, grid_j=8, schedule=spec, early_stop=False,
+                                   test=(te.rows, te.cols, te.values), nthreads=8)
+    dtr = np.abs(np.array([s.train_rmse for s in res.trace]) - [s["train_rmse"] for s in otr])
+    dte = np.abs(np.array([s.test_rmse for s in res.trace]) - [s["test_rmse"] for s in otr])
+    assert dtr.max() <= TOL and dte.max() <= TOL
+    got_it = [s.inner_iters for s in res.trace]
+    want_it = [s["inner_iters"] for s in otr]
+    if spec.startswith("converge"):
+        assert all(abs(a - b) <= 1 for a, b in zip(got_it, want_it))
+    else:
+        assert got_it == want_it
