@@ -795,6 +795,11 @@ Shape shape_for(int kp) {
   // each lane holds up to 4 float4 (16 floats) of the row: several
   // independent groups per warp, few shuffles per rating
   const int f4 = kp / 4;  // float4 per row
+  // rows of 3 * 2^j float4 (k = 24, 48, 96, 192, 384): 3 float4 per lane fit
+  // exactly, where the power-of-two shape would predicate a quarter of the
+  // lanes off (k = 96: SSE 4.2 ms vs 2.6 at k = 64 on C4, scripts/k_sweep.py)
+  if (f4 >= 6 && f4 % 3 == 0 && ((f4 / 3) & (f4 / 3 - 1)) == 0 && f4 / 3 <= 32)
+    return {f4 / 3, 3};
   if (f4 <= 4) {
     int v4 = 1;
     while (v4 < f4) v4 <<= 1;
@@ -808,7 +813,8 @@ Shape shape_for(int kp) {
 #define BGMF_SHAPES(X)                                                                      \
   X(1, 1, true) X(1, 2, true) X(1, 4, true) X(2, 4, true) X(4, 4, true) X(8, 4, true)       \
   X(16, 4, true) X(32, 4, true) X(1, 1, false) X(1, 2, false) X(1, 4, false) X(2, 4, false) \
-  X(4, 4, false) X(8, 4, false) X(16, 4, false) X(32, 4, false)
+  X(4, 4, false) X(8, 4, false) X(16, 4, false) X(32, 4, false) X(2, 3, false)              \
+  X(4, 3, false) X(8, 3, false) X(16, 3, false) X(32, 3, false)
 
 // kp == 4*L*V4: every lane owns a full slice of the row, no predication
 inline bool needs_mask(const Shape& sh, int kp) { return 4 * sh.L * sh.V4 != kp; }

@@ -36,8 +36,8 @@ def _compare(d, cfg, options=None, tol=1e-3):
         assert np.abs(res.model.u - u).max() < 1e-2
 
 
-@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 10, 16, 17, 30, 32, 33, 64, 65, 100, 128, 129,
-                               200, 256, 300, 512])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 10, 16, 17, 24, 30, 32, 33, 48, 64, 65, 96,
+                               100, 128, 129, 192, 200, 256, 300, 384, 512])
 def test_latent_widths(k):
     d = _data(700, 500, 40_000, seed=k)
     _compare(d, bm.TrainConfig(k=k, outer_steps=3, grid_i=4, grid_j=4, alpha=2e-4))
