@@ -792,29 +792,34 @@ struct Shape {
 };
 
 Shape shape_for(int kp) {
-  // each lane holds up to 4 float4 (16 floats) of the row: several
-  // independent groups per warp, few shuffles per rating
+  // A group of L lanes owns one rating; lane gl holds float4s gl, gl+L, ...
+  // of the row (V4 of them), so one warp instruction moves a 16L-byte
+  // contiguous segment of each of 32/L rows.  L >= 4 keeps that segment at 64
+  // bytes or more (two full sectors): with k = 16 on one lane per rating the
+  // sweep ran at half the speed, k = 32 on two lanes 21% slower
+  // (scripts/k_sweep.py, B200).  Beyond that, up to 4 float4 per lane keeps
+  // several independent groups per warp and few shuffles per rating.
   const int f4 = kp / 4;  // float4 per row
   // rows of 3 * 2^j float4 (k = 24, 48, 96, 192, 384): 3 float4 per lane fit
   // exactly, where the power-of-two shape would predicate a quarter of the
-  // lanes off (k = 96: SSE 4.2 ms vs 2.6 at k = 64 on C4, scripts/k_sweep.py)
+  // lanes off (k = 96: SSE 4.2 ms vs 2.6 at k = 64 on C4; k = 24 on 2 lanes of
+  // 3 beats 4 lanes of 2 with one masked: 4.06 vs 4.33 ms)
   if (f4 >= 6 && f4 % 3 == 0 && ((f4 / 3) & (f4 / 3 - 1)) == 0 && f4 / 3 <= 32)
     return {f4 / 3, 3};
-  if (f4 <= 4) {
-    int v4 = 1;
-    while (v4 < f4) v4 <<= 1;
-    return {1, v4};
-  }
-  int L = 1;
-  while (L * 4 < f4) L <<= 1;
-  return {L, 4};
+  if (f4 <= 2) return {f4 < 1 ? 1 : f4, 1};
+  int L = 4;
+  while (L * 4 < f4 && L < 32) L <<= 1;
+  int v4 = 1;
+  while (v4 * L < f4) v4 <<= 1;
+  return {L, v4};
 }
 
-#define BGMF_SHAPES(X)                                                                      \
-  X(1, 1, true) X(1, 2, true) X(1, 4, true) X(2, 4, true) X(4, 4, true) X(8, 4, true)       \
-  X(16, 4, true) X(32, 4, true) X(1, 1, false) X(1, 2, false) X(1, 4, false) X(2, 4, false) \
-  X(4, 4, false) X(8, 4, false) X(16, 4, false) X(32, 4, false) X(2, 3, false)              \
-  X(4, 3, false) X(8, 3, false) X(16, 3, false) X(32, 3, false)
+#define BGMF_SHAPES(X)                                                                    \
+  X(1, 1, false) X(2, 1, false) X(2, 3, false) X(4, 1, true) X(4, 1, false) X(4, 2, true) \
+  X(4, 2, false)                                                                          \
+  X(4, 3, false) X(4, 4, true) X(4, 4, false) X(8, 3, false) X(8, 4, true)                \
+  X(8, 4, false) X(16, 3, false) X(16, 4, true) X(16, 4, false) X(32, 3, false)           \
+  X(32, 4, true) X(32, 4, false)
 
 // kp == 4*L*V4: every lane owns a full slice of the row, no predication
 inline bool needs_mask(const Shape& sh, int kp) { return 4 * sh.L * sh.V4 != kp; }
