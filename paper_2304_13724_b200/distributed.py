@@ -307,11 +307,13 @@ class _PeerLinks:
 
 
 def _transport(world: int) -> str:
-    """V-move transport of the ring: "peer" (default: IPC-mapped peer memory,
-    csrc/peer.cu) or "dist" (torch.distributed P2P); BGMF_RING_TRANSPORT picks."""
+    """V-move transport of the ring: "peer" (IPC-mapped peer memory,
+    csrc/peer.cu; the default when every rank is on this node) or "dist"
+    (torch.distributed P2P: multi-node jobs); BGMF_RING_TRANSPORT overrides."""
     if world <= 1:
         return "dist"  # nothing moves
-    t = os.environ.get("BGMF_RING_TRANSPORT", "peer")
+    single_node = int(os.environ.get("LOCAL_WORLD_SIZE", world)) == world
+    t = os.environ.get("BGMF_RING_TRANSPORT", "peer" if single_node else "dist")
     return "dist" if t in ("dist", "nccl") else t
 
 
