@@ -316,8 +316,10 @@ int bgmf_sse(const double* u, int64_t n, const double* v, int64_t m, int k,
  *                       (freed by bgmf_destroy);
  *   bgmf_peer_handle -- BGMF_PEER_HANDLE_BYTES of IPC handle for such a base;
  *   bgmf_peer_open   -- map a peer's handle (unmapped by bgmf_destroy);
- *   bgmf_peer_push   -- on ctx's stream: copy `bytes` src -> dst (a peer
- *                       address), then *peer_flag = value (system scope);
+ *   bgmf_peer_push   -- on ctx's stream, one kernel: copy `bytes` src -> dst
+ *                       (a peer address; both 16-byte aligned), fence every
+ *                       store system-wide, then *peer_flag = value (release,
+ *                       system scope);
  *   bgmf_peer_wait   -- on ctx's stream: block later work until *flag >= value
  *                       (wrap-safe comparison). */
 #define BGMF_PEER_HANDLE_BYTES 64

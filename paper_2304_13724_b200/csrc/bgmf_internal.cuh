@@ -84,6 +84,7 @@ struct bgmf_ctx {
   int k = 0, kp = 0;
   // peer transport (peer.cu): IPC-exportable buffers and mapped peer buffers
   std::vector<void*> peer_owned, peer_opened;
+  unsigned int* d_push_done = nullptr;  // CTA-completion counter of peer_push_kernel
   bool have_factors = false, bound = false;
   float* d_u = nullptr;
   float* d_v = nullptr;

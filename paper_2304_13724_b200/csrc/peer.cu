@@ -6,10 +6,10 @@
 // flag words once (CUDA IPC: cudaIpcGetMemHandle / cudaIpcOpenMemHandle, which
 // also works between processes sharing one GPU) and the move becomes two
 // stream-ordered operations on the engine stream:
-//   sender:   copy V_j rows straight into the receiver's V_j rows (NVLink
-//             P2P writes; no staging, no NCCL proxy), then a one-thread
-//             kernel stores flag[sender] = seq with release semantics at
-//             system scope;
+//   sender:   one kernel copies V_j rows straight into the receiver's V_j
+//             rows (NVLink P2P writes; no staging, no NCCL proxy) and, once
+//             every CTA's stores are fenced system-wide, release-stores
+//             flag[sender] = seq (system scope);
 //   receiver: a one-warp kernel spins (acquire, system scope) until
 //             flag[sender] >= seq before the next sweep is allowed to run.
 // seq counts the moves sender -> receiver; both sides derive it from the same
@@ -18,14 +18,39 @@
 // a peer's V_j rows only after V_j has travelled away from that peer, and the
 // peer pushed it only after its own kernels on V_j (sweep and SSE) finished.
 
+#include <algorithm>
+
 #include "bgmf_internal.cuh"
 
 namespace bgmf {
 namespace {
 
-__global__ void peer_signal_kernel(unsigned int* flag, unsigned int value) {
+// The move itself: SM stores of the block into the peer's rows (NVLink P2P
+// writes), then the CUDA "last block" pattern at system scope -- every thread
+// fences its stores system-wide before its CTA counts itself done, and the
+// last CTA fences again and release-stores the flag -- so a receiver that
+// acquires the flag sees the whole block (PTX memory model; a copy-engine
+// memcpy followed by a separate flag kernel would rely on stream-completion
+// semantics across devices instead).  `done` is this context's counter, reset
+// by the last CTA for the next (stream-ordered) push.
+__global__ void __launch_bounds__(256)
+peer_push_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int64_t n4,
+                 unsigned char* __restrict__ dst_tail, const unsigned char* __restrict__ src_tail,
+                 int tail, unsigned int* flag, unsigned int value, unsigned int* done) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __ldg(src + i);
+  if (blockIdx.x == 0 && (int)threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
   __threadfence_system();
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(done, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+      *done = 0u;
+    }
+  }
 }
 
 __global__ void peer_wait_kernel(const unsigned int* flag, unsigned int value) {
@@ -86,10 +111,21 @@ extern "C" int bgmf_peer_push(bgmf_ctx* c, void* dst, const void* src, int64_t b
                               uint32_t* peer_flag, uint32_t value) {
   if (!c || !dst || !src || !peer_flag || bytes < 0)
     return fail(c, BGMF_ERR_ARG, "bgmf_peer_push: bad argument");
+  if (((uintptr_t)dst | (uintptr_t)src) & 15)
+    return fail(c, BGMF_ERR_ARG, "bgmf_peer_push: buffers must be 16-byte aligned");
   cudaSetDevice(c->device);
-  if (bytes > 0)
-    BGMF_CK(c, cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, c->stream));
-  peer_signal_kernel<<<1, 1, 0, c->stream>>>(peer_flag, value);
+  if (!c->d_push_done) {
+    BGMF_CK(c, cudaMalloc(&c->d_push_done, sizeof(unsigned int)));
+    BGMF_CK(c, cudaMemsetAsync(c->d_push_done, 0, sizeof(unsigned int), c->stream));
+  }
+  const int64_t n4 = bytes / 16;
+  const int tail = (int)(bytes % 16);
+  int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 2 * (int64_t)c->num_sms);
+  if (blocks < 1) blocks = 1;
+  peer_push_kernel<<<blocks, 256, 0, c->stream>>>(
+      static_cast<float4*>(dst), static_cast<const float4*>(src), n4,
+      static_cast<unsigned char*>(dst) + n4 * 16, static_cast<const unsigned char*>(src) + n4 * 16,
+      tail, peer_flag, value, c->d_push_done);
   BGMF_CK(c, cudaGetLastError());
   return BGMF_OK;
 }
@@ -104,6 +140,8 @@ extern "C" int bgmf_peer_wait(bgmf_ctx* c, const uint32_t* flag, uint32_t value)
 
 namespace bgmf {
 void peer_release(bgmf_ctx* c) {
+  if (c->d_push_done) cudaFree(c->d_push_done);
+  c->d_push_done = nullptr;
   for (void* p : c->peer_opened) cudaIpcCloseMemHandle(p);
   c->peer_opened.clear();
   for (void* p : c->peer_owned) cudaFree(p);
