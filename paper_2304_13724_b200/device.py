@@ -119,6 +119,10 @@ class Engine:
         N.check(rc, self._h, **kw)
 
     def close(self):
+        pre = getattr(self, "_prefault", None)
+        if pre is not None:  # a prefault thread still writing host pages
+            pre[0].join()
+            self._prefault = None
         if getattr(self, "_h", None) is not None and self._h.value:
             self._L.bgmf_destroy(self._h)
             self._h = None
