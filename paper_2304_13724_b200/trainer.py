@@ -97,77 +97,82 @@ def train_blocked(d: RatingsDataset, cfg: TrainConfig, test: Optional[RatingsDat
     if (blocked.grid.grid_i, blocked.grid.grid_j) != (cfg.grid_i, cfg.grid_j) \
             or blocked.dataset is not d:
         raise ValueError("blocked must partition d with cfg's grid")
-    eng = blocked.engine
-    # init_factors(n, m, k, seed) generated in HBM: numpy's PCG64 stream
-    # reproduced bit-for-bit on the device (no 2*(n+m)*k*8-byte upload)
-    eng.init_factors(d.n, d.m, cfg.k, cfg.seed)
-    if prof:
-        prof.mark("init_factors (device PCG64)")
+    try:
+        eng = blocked.engine
+        # init_factors(n, m, k, seed) generated in HBM: numpy's PCG64 stream
+        # reproduced bit-for-bit on the device (no 2*(n+m)*k*8-byte upload)
+        eng.init_factors(d.n, d.m, cfg.k, cfg.seed)
+        if prof:
+            prof.mark("init_factors (device PCG64)")
 
-    evaluator = HoldoutEvaluator(d, test) if test is not None and len(test) > 0 else None
-    if evaluator is not None:
-        t = evaluator.test
-        eng.holdout_set(t.rows, t.cols, t.values, evaluator.cold, evaluator.fallback)
-    sched = cfg.inner_schedule
-    tol = sched.tol if isinstance(sched, ConvergeEachBlock) else 0.0
-    adaptive = isinstance(sched, AdaptiveDecreasing)
-    hist = [math.sqrt(eng.train_sse() / len(d))] if adaptive and len(d) else [0.0]
-    counts = np.diff(eng.offsets)
-    hooks = (_HookTasks(blocked, init_factors(d.n, d.m, cfg.k, cfg.seed), cfg)
-             if block_hook is not None else None)
+        evaluator = HoldoutEvaluator(d, test) if test is not None and len(test) > 0 else None
+        if evaluator is not None:
+            t = evaluator.test
+            eng.holdout_set(t.rows, t.cols, t.values, evaluator.cold, evaluator.fallback)
+        sched = cfg.inner_schedule
+        tol = sched.tol if isinstance(sched, ConvergeEachBlock) else 0.0
+        adaptive = isinstance(sched, AdaptiveDecreasing)
+        hist = [math.sqrt(eng.train_sse() / len(d))] if adaptive and len(d) else [0.0]
+        counts = np.diff(eng.offsets)
+        hooks = (_HookTasks(blocked, init_factors(d.n, d.m, cfg.k, cfg.seed), cfg)
+                 if block_hook is not None else None)
 
-    trace = ConvergenceTrace()
-    stop: StopReason = "max_steps"
-    batched = (not early_stop and block_hook is None and evaluator is None and not adaptive
-               and not isinstance(sched, ConvergeEachBlock) and not eng.options.exact
-               and not eng.streaming and cfg.outer_steps > 1)
-    if own:  # fault the model's output pages in while the epochs run
-        eng.prefault_factors()
-    if batched:
-        # nothing is decided on the host between steps: enqueue every epoch
-        # in one bgmf_run_steps call (no host round trip between epochs)
-        _run_steps_batched(eng, cfg, sched, counts, trace, timing)
-    for step in range(1, 0 if batched else cfg.outer_steps + 1):
-        if adaptive and step >= 2:
-            prev, cur = hist[-2], hist[-1]
-            ratio = (prev - cur) / prev if prev > 0 else 0.0
-        else:
-            ratio = 1.0
-        g = resolve_inner_iters(sched, step, ratio)
-        t0 = time.perf_counter()
-        batches = plan_step(cfg.grid_i, cfg.grid_j, step - 1)
-        try:
-            acc, max_iters, capped = _run_step(eng, batches, g, tol, cfg, counts, hooks,
-                                               block_hook)
-        except DivergenceError as exc:
-            exc.step = step
-            exc.partial_trace = trace
-            raise
-        train_rmse = finalize(acc)
-        test_rmse = (math.sqrt(eng.holdout_sse() / len(evaluator.test))
-                     if evaluator is not None else None)
-        trace.append(TraceStep(step=step, train_rmse=train_rmse, test_rmse=test_rmse,
-                               seconds=time.perf_counter() - t0 if timing else 0.0,
-                               inner_iters=max_iters, capped_blocks=capped))
-        hist.append(train_rmse)
-        if early_stop:
-            if acc.count == 0:
-                stop = "converged"
-                break
-            if len(trace) >= 2 and trace.steps[-2].train_rmse - train_rmse < cfg.delta:
-                stop = "converged"
-                break
-    if prof:
-        prof.mark(f"{len(trace)} epochs")
-    u, v = eng.get_factors()
-    if prof:
-        prof.mark("get_factors (D2H)")
-    if own:  # the partition was made for this call: release its HBM now
-        eng.close()
-    if prof:
-        prof.mark("release device context")
-        prof.report()
-    return TrainResult(model=FactorModel(u, v), trace=trace, stop_reason=stop)
+        trace = ConvergenceTrace()
+        stop: StopReason = "max_steps"
+        batched = (not early_stop and block_hook is None and evaluator is None and not adaptive
+                   and not isinstance(sched, ConvergeEachBlock) and not eng.options.exact
+                   and not eng.streaming and cfg.outer_steps > 1)
+        if own:  # fault the model's output pages in while the epochs run
+            eng.prefault_factors()
+        if batched:
+            # nothing is decided on the host between steps: enqueue every epoch
+            # in one bgmf_run_steps call (no host round trip between epochs)
+            _run_steps_batched(eng, cfg, sched, counts, trace, timing)
+        for step in range(1, 0 if batched else cfg.outer_steps + 1):
+            if adaptive and step >= 2:
+                prev, cur = hist[-2], hist[-1]
+                ratio = (prev - cur) / prev if prev > 0 else 0.0
+            else:
+                ratio = 1.0
+            g = resolve_inner_iters(sched, step, ratio)
+            t0 = time.perf_counter()
+            batches = plan_step(cfg.grid_i, cfg.grid_j, step - 1)
+            try:
+                acc, max_iters, capped = _run_step(eng, batches, g, tol, cfg, counts, hooks,
+                                                   block_hook)
+            except DivergenceError as exc:
+                exc.step = step
+                exc.partial_trace = trace
+                raise
+            train_rmse = finalize(acc)
+            test_rmse = (math.sqrt(eng.holdout_sse() / len(evaluator.test))
+                         if evaluator is not None else None)
+            trace.append(TraceStep(step=step, train_rmse=train_rmse, test_rmse=test_rmse,
+                                   seconds=time.perf_counter() - t0 if timing else 0.0,
+                                   inner_iters=max_iters, capped_blocks=capped))
+            hist.append(train_rmse)
+            if early_stop:
+                if acc.count == 0:
+                    stop = "converged"
+                    break
+                if len(trace) >= 2 and trace.steps[-2].train_rmse - train_rmse < cfg.delta:
+                    stop = "converged"
+                    break
+        if prof:
+            prof.mark(f"{len(trace)} epochs")
+        u, v = eng.get_factors()
+        if prof:
+            prof.mark("get_factors (D2H)")
+        if own:  # the partition was made for this call: release its HBM now
+            eng.close()
+        if prof:
+            prof.mark("release device context")
+            prof.report()
+        return TrainResult(model=FactorModel(u, v), trace=trace, stop_reason=stop)
+    except BaseException:
+        if own:  # a failed call (DivergenceError, interrupt) releases its HBM too
+            blocked.engine.close()
+        raise
 
 
 class _Phases:
