@@ -262,3 +262,19 @@ def test_peer_links_sequence_and_order(world, P):
         assert pushes[key] == list(range(1, len(pushes[key]) + 1))
         assert waits[key] == pushes[key]
     assert sum(len(v) for v in pushes.values()) > 0
+
+
+def test_ring_transport_choice(monkeypatch):
+    """Peer memory by default when every rank is on this node; torch.distributed
+    for multi-node jobs (CUDA IPC is single-node); BGMF_RING_TRANSPORT wins."""
+    for var in ("LOCAL_WORLD_SIZE", "BGMF_RING_TRANSPORT"):
+        monkeypatch.delenv(var, raising=False)
+    assert D._transport(1) == "dist"
+    assert D._transport(8) == "peer"
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "8")
+    assert D._transport(8) == "peer"
+    assert D._transport(16) == "dist"
+    monkeypatch.setenv("BGMF_RING_TRANSPORT", "peer")
+    assert D._transport(16) == "peer"
+    monkeypatch.setenv("BGMF_RING_TRANSPORT", "nccl")
+    assert D._transport(8) == "dist"
