@@ -13,11 +13,12 @@ from oracle import oracle as O  # noqa: E402
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 g = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+scale = int(sys.argv[3]) if len(sys.argv) > 3 else 1  # x dims and x^2 ratings
 fails = 0
 t0 = time.time()
 for i in range(cases):
-    n, m = int(g.integers(1, 3000)), int(g.integers(1, 3000))
-    nnz = int(min(n * m, g.integers(1, 60_000)))
+    n, m = int(g.integers(1, 3000 * scale)), int(g.integers(1, 3000 * scale))
+    nnz = int(min(n * m, g.integers(1, 60_000 * scale * scale)))
     cells = g.choice(n * m, nnz, replace=False)
     r, c = np.divmod(cells, m)
     if g.random() < 0.3 and nnz > 10:  # duplicate cells
