@@ -254,6 +254,12 @@ int64_t fast_groups(bgmf_ctx* ctx);
 int launch_piece(bgmf_ctx* ctx, const BlockWork* d_work, int nwork, int chunks,
                  const int32_t* lrow, const int32_t* lcol, const float* val, int iters,
                  float alpha, float beta, double ratings, int cbits);
+int launch_piece_sweep(bgmf_ctx* ctx, const BlockWork* d_work, int nwork, int chunks,
+                       const int32_t* lrow, const int32_t* lcol, const float* val, float alpha,
+                       float beta, int it, int cbits);
+int run_step_stream_converge(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
+                             int nbatch, double tol, int64_t cap, double alpha, double beta,
+                             int64_t* iters_out, int32_t* capped_out);
 
 // stream.cu -- out-of-core: ratings in pinned host memory, device slot ring
 int stream_enable(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);

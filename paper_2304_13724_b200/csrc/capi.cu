@@ -493,9 +493,9 @@ int bgmf_run_step_converge(bgmf_ctx* c, const int32_t* plan, const int32_t* batc
   int rc = check_step_ready(c);
   if (rc) return rc;
   cudaSetDevice(c->device);
-  if (c->streaming)
-    return fail(c, BGMF_ERR_STATE, "converge schedules are not supported while streaming");
-  rc = c->exact ? run_step_converge_exact(c, plan, batch_off, nbatch, tol, cap, alpha, beta,
+  rc = c->streaming ? run_step_stream_converge(c, plan, batch_off, nbatch, tol, cap, alpha,
+                                                beta, iters_out, capped_out)
+     : c->exact ? run_step_converge_exact(c, plan, batch_off, nbatch, tol, cap, alpha, beta,
                                           iters_out, capped_out)
                 : run_step_converge_fast(c, plan, batch_off, nbatch, tol, cap, alpha, beta,
                                          iters_out, capped_out);

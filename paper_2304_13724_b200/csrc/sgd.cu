@@ -1511,6 +1511,21 @@ int launch_piece(bgmf_ctx* c, const BlockWork* d_work, int nwork, int chunks,
   return BGMF_OK;
 }
 
+// One sweep launch (inner iteration `it`) of a piece -- the streaming
+// converge loop's unit (its SSE measurements use launch_piece with iters 0).
+int launch_piece_sweep(bgmf_ctx* c, const BlockWork* d_work, int nwork, int chunks,
+                       const int32_t* lrow, const int32_t* lcol, const float* val, float alpha,
+                       float beta, int it, int cbits) {
+  if (chunks == 0) return BGMF_OK;
+  const Shape sh = shape_for(c->kp);
+  const int gpw = 32 / sh.L;
+  const dim3 grid(((chunks + gpw - 1) / gpw + 7) / 8);
+  launch_fast_ptr(true, sh, grid, c->stream, d_work, nwork, chunks, lrow, lcol, val, c, alpha,
+                  beta, it, cbits);
+  BGMF_CK(c, cudaGetLastError());
+  return BGMF_OK;
+}
+
 int run_step_exact(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
                    int iters, double alpha, double beta) {
   cudaStream_t s = c->stream;

@@ -173,17 +173,12 @@ struct Piece {
 
 }  // namespace
 
-int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
-                    int iters, float alpha, float beta) {
-  cudaStream_t s = c->stream, cs = c->copy_stream;
+// Cut every batch into pieces that fit a slot (and one L2 wave); slot-relative
+// work items into h_work[0, *w).  Pieces never span batches.
+static int build_pieces(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
+                        std::vector<Piece>& pieces, int* w_out) {
   const int nb = c->I * c->J;
   const int64_t groups = fast_groups(c);
-  const int total = batch_off[nbatch];
-  int rc = ensure_step_scratch(c, (size_t)total);
-  if (rc) return rc;
-
-  // 1. cut every batch into pieces that fit a slot; slot-relative work items
-  std::vector<Piece> pieces;
   int w = 0;
   for (int t = 0; t < nbatch; ++t) {
     int q = batch_off[t];
@@ -235,6 +230,22 @@ int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, 
       q = q_end;
     }
   }
+  *w_out = w;
+  return BGMF_OK;
+}
+
+int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
+                    int iters, float alpha, float beta) {
+  cudaStream_t s = c->stream, cs = c->copy_stream;
+  const int nb = c->I * c->J;
+  const int total = batch_off[nbatch];
+  int rc = ensure_step_scratch(c, (size_t)total);
+  if (rc) return rc;
+  // 1. pieces and their slot-relative work items
+  std::vector<Piece> pieces;
+  int w = 0;
+  if ((rc = build_pieces(c, plan, batch_off, nbatch, pieces, &w))) return rc;
+
   if (w > 0)
     BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * w,
                                cudaMemcpyHostToDevice, s));
@@ -292,6 +303,118 @@ int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, 
   BGMF_CK(c, cudaStreamSynchronize(s));
   cudaEventDestroy(ready);
   if (c->timing) harvest_timing(c);
+  return BGMF_OK;
+}
+
+// ConvergeEachBlock while streaming (_kernels.py:62-100 per block): piece by
+// piece, the piece's ratings are copied into a slot once, then its blocks
+// sweep until their RMSE improves by less than tol (or cap sweeps), each
+// iteration one sweep launch over the still-active blocks plus an SSE
+// measurement read back to the host -- the in-core run_step_converge_fast
+// loop on slot-resident data.  Synchronous (no copy/compute overlap): the
+// per-iteration host decision dominates anyway.
+int run_step_stream_converge(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off,
+                             int nbatch, double tol, int64_t cap, double alpha, double beta,
+                             int64_t* iters_out, int32_t* capped_out) {
+  cudaStream_t s = c->stream;
+  const int nb = c->I * c->J;
+  const int total = batch_off[nbatch];
+  int rc = ensure_step_scratch(c, 2 * (size_t)(total > 0 ? total : 1));
+  if (rc) return rc;
+  std::vector<Piece> pieces;
+  int w = 0;
+  if ((rc = build_pieces(c, plan, batch_off, nbatch, pieces, &w))) return rc;
+  for (int b = 0; b < nb; ++b) { iters_out[b] = 0; capped_out[b] = 0; }
+  std::vector<double> sse_final(nb, 0.0);
+  unsigned long long best = kNoBad;
+  const int cb = c->packed ? c->cbits : -1;
+  BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+  for (const Piece& pc : pieces) {
+    const int sl = 0;
+    for (int i = 0; i < pc.nw; ++i) {  // the piece's blocks into slot 0
+      const BlockWork& bw = c->h_work[pc.w0 + i];
+      const int64_t src = c->h_pos[bw.block_id], cnt = bw.end - bw.begin;
+      BGMF_CK(c, cudaMemcpyAsync(c->s_lrow[sl] + bw.begin, c->h_lrow + src, cnt * 4,
+                                 cudaMemcpyHostToDevice, s));
+      if (!c->packed)
+        BGMF_CK(c, cudaMemcpyAsync(c->s_lcol[sl] + bw.begin, c->h_lcol + src, cnt * 4,
+                                   cudaMemcpyHostToDevice, s));
+      BGMF_CK(c, cudaMemcpyAsync(c->s_val[sl] + bw.begin, c->h_val + src, cnt * 4,
+                                 cudaMemcpyHostToDevice, s));
+      c->h2d_bytes += (c->packed ? 8.0 : 12.0) * (double)cnt;
+    }
+    std::vector<char> active(pc.nw, 1);
+    std::vector<double> prev(pc.nw, 0.0);
+    int n_active = pc.nw;
+    // active blocks' work items (slot offsets unchanged) at h_work[w, ...)
+    auto upload_active = [&](int* nw, int* chunks) -> int {
+      *nw = 0;
+      *chunks = 0;
+      for (int i = 0; i < pc.nw; ++i) {
+        if (!active[i]) continue;
+        BlockWork bw = c->h_work[pc.w0 + i];
+        bw.first_chunk = *chunks;
+        *chunks += (int)((bw.end - bw.begin + bw.chunk_len - 1) / bw.chunk_len);
+        c->h_work[w + (*nw)++] = bw;
+      }
+      if (*nw > 0)
+        BGMF_CK(c, cudaMemcpyAsync(c->d_work + w, c->h_work + w, sizeof(BlockWork) * (*nw),
+                                   cudaMemcpyHostToDevice, s));
+      return BGMF_OK;
+    };
+    auto measure = [&](int nw, int chunks) -> int {  // SSE of the active blocks
+      BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, s));
+      int r2 = launch_piece(c, c->d_work + w, nw, chunks, c->s_lrow[sl], c->s_lcol[sl],
+                            c->s_val[sl], 0, (float)alpha, (float)beta, 0.0, cb);
+      if (r2) return r2;
+      BGMF_CK(c, cudaMemcpyAsync(c->h_sse, c->d_sse, sizeof(double) * nb,
+                                 cudaMemcpyDeviceToHost, s));
+      BGMF_CK(c, cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, s));
+      BGMF_CK(c, cudaStreamSynchronize(s));
+      return BGMF_OK;
+    };
+    int nw = 0, chunks = 0;
+    if ((rc = upload_active(&nw, &chunks)) || (rc = measure(nw, chunks))) return rc;
+    for (int i = 0; i < pc.nw; ++i) {
+      const BlockWork& bw = c->h_work[pc.w0 + i];
+      prev[i] = std::sqrt(c->h_sse[bw.block_id] / (double)(bw.end - bw.begin));
+    }
+    int64_t it = 0;
+    while (n_active > 0 && it < cap) {
+      if ((rc = upload_active(&nw, &chunks))) return rc;
+      if ((rc = launch_piece_sweep(c, c->d_work + w, nw, chunks, c->s_lrow[sl], c->s_lcol[sl],
+                                   c->s_val[sl], (float)alpha, (float)beta, (int)(it & 0xFFFF),
+                                   cb)))
+        return rc;
+      ++it;
+      if ((rc = measure(nw, chunks))) return rc;
+      for (int i = 0; i < pc.nw; ++i) {
+        if (!active[i]) continue;
+        const BlockWork& bw = c->h_work[pc.w0 + i];
+        const int64_t cnt = bw.end - bw.begin;
+        const double cur = c->h_sse[bw.block_id];
+        iters_out[bw.block_id] = it;
+        sse_final[bw.block_id] = cur;
+        const double now = std::sqrt(cur / (double)cnt);
+        if (!std::isfinite(cur)) {
+          const unsigned long long key = pack_bad(bw.pos, it - 1, cnt - 1);
+          if (key < best) best = key;
+          active[i] = 0; --n_active;
+        } else if (prev[i] - now < tol) {
+          active[i] = 0; --n_active;
+        } else {
+          prev[i] = now;
+        }
+      }
+      if (*c->h_bad != kNoBad) break;
+    }
+    for (int i = 0; i < pc.nw; ++i)
+      if (active[i]) capped_out[c->h_work[pc.w0 + i].block_id] = 1;
+    if (*c->h_bad != kNoBad) break;
+  }
+  for (int b = 0; b < nb; ++b) c->h_sse[b] = sse_final[b];
+  if (*c->h_bad < best) best = *c->h_bad;
+  *c->h_bad = best;
   return BGMF_OK;
 }
 

@@ -35,10 +35,12 @@ for i in range(cases):
              "adaptive:2": bm.AdaptiveDecreasing(2),
              "converge:0.05": bm.ConvergeEachBlock(0.05)}[spec]
     exact = g.random() < 0.25
+    # out-of-core: a device budget of a few blocks' ratings (fast mode only)
+    stream = (not exact) and g.random() < 0.25 and nnz >= 1000
     steps = int(g.integers(1, 5))
     d = bm.RatingsDataset(n, m, r, c, v)
     holdout = g.random() < 0.3 and nnz >= 20
-    tag = f"case {i}: n={n} m={m} nnz={nnz} grid={I}x{J} k={k} {spec} exact={exact} holdout={holdout}"
+    tag = f"case {i}: n={n} m={m} nnz={nnz} grid={I}x{J} k={k} {spec} exact={exact} holdout={holdout} stream={stream}"
     try:
         P = O.partition(r, c, v, n, m, I, J)
         b = bm.partition(d, I, J)
@@ -50,8 +52,18 @@ for i in range(cases):
         tr, te = bm.split(d, 0.2, seed=i) if holdout else (d, None)
         if holdout:  # the partition above was of the full set; train on the split
             P = None
-        res = bm.train_blocked(tr, cfg, te, early_stop=False,
-                               options=bm.EngineOptions(exact=True) if exact else None)
+        opts = None
+        if exact:
+            opts = bm.EngineOptions(exact=True)
+        elif stream:
+            per_block = max(1, len(tr) // (I * J))
+            opts = bm.EngineOptions(device_rating_budget=12 * 3 * max(per_block * 3, 64))
+        try:
+            res = bm.train_blocked(tr, cfg, te, early_stop=False, options=opts)
+        except Exception as e:  # noqa: BLE001  a slot smaller than the largest block: skip
+            if stream and "slot" in str(e):
+                continue
+            raise
         ou, ov, otr, _ = O.train_blocked(tr.n, tr.m, tr.rows, tr.cols, tr.values, k=k,
                                          outer_steps=steps, grid_i=I, grid_j=J, alpha=2e-4,
                                          schedule=spec, early_stop=False,

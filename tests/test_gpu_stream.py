@@ -80,3 +80,25 @@ def test_l2_waves_match_oracle(streamed):
                                    grid_i=8, grid_j=8, early_stop=False, nthreads=8)
     got = np.array([s.train_rmse for s in res.trace])
     assert np.abs(got - [s["train_rmse"] for s in otr]).max() <= TOL
+
+
+@pytest.mark.parametrize("tol", [0.05, 0.005])
+def test_stream_converge_schedule_matches_oracle(tol):
+    """ConvergeEachBlock out of core: each piece is copied into a slot once and
+    its blocks sweep until their RMSE improves by less than tol (cap 100);
+    trace within 1e-3 of the oracle, the same per-step sweep counts within one
+    (a block's improvement can sit at the tolerance), capped blocks counted."""
+    d = _c2_like(200_000)
+    cfg = bm.TrainConfig(k=32, outer_steps=3, grid_i=8, grid_j=8,
+                         inner_schedule=bm.ConvergeEachBlock(tol))
+    opts = bm.EngineOptions(device_rating_budget=int(12 * len(d) * 0.1), stream_slots=3)
+    blocked = bm.partition(d, 8, 8, options=opts)
+    assert blocked.engine.streaming
+    res = bm.train_blocked(d, cfg, early_stop=False, timing=False, blocked=blocked)
+    _, _, otr, _ = O.train_blocked(d.n, d.m, d.rows, d.cols, d.values, k=32, outer_steps=3,
+                                   grid_i=8, grid_j=8, schedule=f"converge:{tol}",
+                                   early_stop=False, nthreads=8)
+    dtr = np.abs(np.array([s.train_rmse for s in res.trace]) - [s["train_rmse"] for s in otr])
+    assert dtr.max() <= TOL
+    assert all(abs(a.inner_iters - b["inner_iters"]) <= 1 for a, b in zip(res.trace, otr))
+    assert all(s.inner_iters >= 1 for s in res.trace)
