@@ -209,9 +209,6 @@ __device__ __forceinline__ float dot_slice(const float4 (&u)[V4], const float4 (
 // evaluated as t = 2ae*v - ab*u (FFMA2 of an FMUL2) and u + t, in packed fp32.
 // All lanes of the warp execute the same trip count (maxlen) so the shuffles
 // stay converged; groups past their chunk end are predicated off.
-// shared user runs re-read their U row every kShareRefresh ratings (walk_chunk)
-constexpr int kShareRefresh = 8;
-
 template <int L, int V4, bool kMask, bool kSweep, bool kBulk = false>
 __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
                                              const int32_t* __restrict__ lrow,
@@ -326,11 +323,6 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
 #pragma unroll
         for (int q = 0; q < V4; ++q) u[q] = un[q];
         shared = kSweep && (rn == first_row || rn == last_row);
-      } else if (kSweep && shared && nvalid && ((t + 1) & (kShareRefresh - 1)) == 0) {
-        // a run split across chunks: every group red.adds its u deltas, so the
-        // global row holds all of them; re-read it so a long shared run (a
-        // heavy user) sees the other groups' updates, not only its own
-        load_row<V4>(u, Ub + (int64_t)r * kp, ln);
       }
       if (nvalid) {
 #pragma unroll
@@ -340,6 +332,11 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
       c = cn;
       x = xn;
     }
+    // a run split across chunks: every group red.adds its u deltas, so the
+    // global row holds all of them; re-read it once per triple batch so a long
+    // shared run (a heavy user) sees the other groups' updates, not only its
+    // own (outside the per-rating loop: interior runs pay nothing)
+    if (kSweep && shared && !dead && t0 + L < len) load_row<V4>(u, Ub + (int64_t)r * kp, ln);
     // advance the triple batches
     rA = rB; cA = cB; xA = xB;
     const int nb = t0 + 2 * L + ln.gl;

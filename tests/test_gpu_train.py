@@ -301,7 +301,7 @@ def test_every_schedule_with_holdout_vs_oracle(sched, spec):
 def test_heavy_user_runs_split_across_chunks(n, m, k):
     """A user whose run spans many chunks (here: every rating of a 1-2 row
     dense matrix) is swept by several groups at once; each red.adds its u
-    deltas and re-reads the row every 8 ratings (kShareRefresh), so the run
+    deltas and re-reads the row once per triple batch (every L ratings), so the run
     sees the other groups' updates.  Without the re-read the trace drifted 5%
     (randomised sweep, scripts/fuzz_parity.py); now within the dense-toy bound."""
     g = np.random.default_rng(0)
