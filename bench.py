@@ -24,6 +24,7 @@ Printed JSON (rank 0, one line):
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -215,10 +216,13 @@ def run_ours(args):
         torch.cuda.synchronize()
         os.environ["BGMF_PROFILE"] = "1"  # phase breakdown on stderr
         for _ in range(3):  # median of three calls: host page/THP state varies run to run
+            gc.collect()  # like timeit: no cyclic-GC pass inside the timed call
+            gc.disable()
             t0 = time.perf_counter()
             res = bm.train_blocked(d, cfg, early_stop=False)
             torch.cuda.synchronize()
             walls.append(time.perf_counter() - t0)
+            gc.enable()
             print(f"[bgmf] e2e wall (train_blocked + sync)  {walls[-1] * 1e3:9.2f} ms",
                   file=sys.stderr)
             del res
