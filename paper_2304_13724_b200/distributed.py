@@ -657,12 +657,17 @@ def bench_main(args, clock_sampler=None):
         train_blocked_distributed(d, TrainConfig(k=w.k, grid_i=w.grid, grid_j=w.grid,
                                                  outer_steps=1), early_stop=False)  # warm
         walls = []
+        import gc
+
         for _ in range(3):  # median of three calls (host page state varies run to run)
+            gc.collect()  # like timeit: no cyclic-GC pass inside the timed call
+            gc.disable()
             torch.cuda.synchronize()
             dist.barrier()
             t0 = time.perf_counter()
             train_blocked_distributed(d, run_cfg, early_stop=False)
             torch.cuda.synchronize()
+            gc.enable()
             wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
                                 device=f"cuda:{device}")
             dist.all_reduce(wall, op=dist.ReduceOp.MAX)
