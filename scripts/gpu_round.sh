@@ -43,6 +43,14 @@ for mb in (64,256,1024,4096):
     c5s) timeout 900 $B --config C5 --nnz 200000000 --steps 3 --warmup 3 --budget-gb 0.5 > $OUT/bench_c5_small.json 2> $OUT/bench_c5_small.err; echo "c5s rc=$?" ;;
     c5) timeout 1500 $B --config C5 --steps 3 --warmup 3 > $OUT/bench_c5.json 2> $OUT/bench_c5.err; echo "c5 rc=$?" ;;
     probe) timeout 300 python scripts/h2d_probe.py > $OUT/h2d_probe.txt 2>&1; echo "probe rc=$?" ;;
+    fuzz) # randomised parity sweeps vs the oracle (trainer, baselines, drop-ins, ring)
+      timeout 1500 python scripts/fuzz_parity.py 1500 ${FUZZ_SEED:-1} > $OUT/fuzz_parity.txt 2>&1
+      timeout 900 python scripts/fuzz_more.py 400 ${FUZZ_SEED:-1} > $OUT/fuzz_more.txt 2>&1
+      timeout 900 python scripts/fuzz_kernels.py 500 ${FUZZ_SEED:-1} > $OUT/fuzz_kernels.txt 2>&1
+      timeout 1200 python scripts/fuzz_ring.py 10 ${FUZZ_SEED:-1} > $OUT/fuzz_ring.txt 2>&1
+      echo "fuzz rc=$?" ;;
+    ksweep) timeout 900 python scripts/k_sweep.py > $OUT/k_sweep.txt 2>&1; echo "ksweep rc=$?" ;;
+    rank) timeout 600 python scripts/rank_probe.py 2 > $OUT/rank.txt 2>&1; echo "rank rc=$?" ;;
     dist1) BGMF_FORCE_DIST=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 5 --warmup 3 > $OUT/bench_dist1.json 2> $OUT/bench_dist1.err; echo "dist1 rc=$?" ;;
     ncuk) # one kernel, full set + source: NCU_K=<regex> NCU_ARGS=<bench args>
       timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"${NCU_K}" -s ${NCU_S:-4} -c 1 \
