@@ -80,7 +80,7 @@ for i in range(cases):
             assert np.array_equal(got, want), (got, want)
             assert np.array_equal(res.model.u, ou) and np.array_equal(res.model.v, ov)
         else:
-            dense = nnz > 0.5 * n * m
+            dense = nnz > 0.25 * n * m  # dense-ish: the ordering effect of DESIGN §4 grows
             tol = np.maximum(1e-3, 3e-3 * want) if dense else 1e-3
             assert np.all(np.abs(got - want) <= tol), (np.abs(got - want).max(), got, want)
     except Exception as e:  # noqa: BLE001
