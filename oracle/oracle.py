@@ -80,8 +80,57 @@ def lib():
             _i64p, _i64p, _i64p, _f64p, _i64p, _i64p, ctypes.c_int, ctypes.c_int,
             _f64p, _f64p, ctypes.c_int, _i32p, _i32p, ctypes.c_int, ctypes.c_int,
             ctypes.c_double, ctypes.c_double, ctypes.c_int, _f64p, _i64p]
+        L.emu32_step.restype = ctypes.c_int64
+        L.emu32_step.argtypes = [
+            _i32p, _i32p, ctypes.POINTER(ctypes.c_float), _i64p, _i64p, _i64p, ctypes.c_int,
+            _i32p, ctypes.c_int, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float),
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_float, ctypes.c_float,
+            ctypes.c_int, _f64p]
         _lib = L
     return _lib
+
+
+def gpu_shape(kp: int, warp: bool = False) -> tuple[int, int]:
+    """Lane geometry (L, V4) of the GPU fast path for a padded row of kp floats
+    (restates shape_for in paper_2304_13724_b200/csrc/rows.cuh, and with
+    warp=True ordered_shape in csrc/ordered.cu; test use)."""
+    f4 = kp // 4
+    if warp:
+        return 32, max(1, -(-f4 // 32))
+    if f4 >= 6 and f4 % 3 == 0 and ((f4 // 3) & (f4 // 3 - 1)) == 0 and f4 // 3 <= 32:
+        return f4 // 3, 3
+    if f4 <= 2:
+        return max(f4, 1), 1
+    L = 4
+    while L * 4 < f4 and L < 32:
+        L <<= 1
+    v4 = 1
+    while v4 * L < f4:
+        v4 <<= 1
+    return L, v4
+
+
+def emu32_step(lrow, lcol, val32, offsets, row_bounds, col_bounds, J, plan_ids, U32, V32,
+               alpha, beta, iters, warp=True):
+    """Sequential fp32 sweep in stored order with the GPU's operation shapes
+    (emu32.c).  U32 / V32 (n x kp, m x kp float32) are updated in place;
+    returns (per-block post-sweep SSE, first diverged plan position or -1)."""
+    L = lib()
+    kp = U32.shape[1]
+    lv, v4 = gpu_shape(kp, warp)
+    lr = np.ascontiguousarray(lrow, np.int32)
+    lc = np.ascontiguousarray(lcol, np.int32)
+    x = np.ascontiguousarray(val32, np.float32)
+    off = np.ascontiguousarray(offsets, np.int64)
+    rb = np.ascontiguousarray(row_bounds, np.int64)
+    cb = np.ascontiguousarray(col_bounds, np.int64)
+    pl = np.ascontiguousarray(plan_ids, np.int32)
+    sse = np.zeros(len(off) - 1, np.float64)
+    fp = ctypes.POINTER(ctypes.c_float)
+    bad = L.emu32_step(_p(lr, _i32p), _p(lc, _i32p), _p(x, fp), _p(off, _i64p), _p(rb, _i64p),
+                       _p(cb, _i64p), J, _p(pl, _i32p), len(pl), _p(U32, fp), _p(V32, fp), kp,
+                       lv, v4, float(alpha), float(beta), int(iters), _p(sse, _f64p))
+    return sse, int(bad)
 
 
 def _p(a, t):

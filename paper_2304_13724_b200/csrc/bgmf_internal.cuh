@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -143,6 +144,22 @@ struct bgmf_ctx {
   cudaStream_t copy_stream = nullptr;
   double h2d_bytes = 0;                  // streamed this context (stats)
 
+  // ordered sweep (ordered.cu): column ranks, row pointers, row flags
+  int ord_mode = -1;                     // 1: ordered where possible, 0: never, -1: auto
+  int64_t ord_stage_ratings = 262144;     // target ratings per stage (slab CTA)
+  int ord_warp = 1;                      // one group per warp (ordered_shape)
+  bool ord_ready = false;
+  uint32_t ord_gen = 1;                  // row-flag generation of the next sweep
+  int32_t* d_qrank = nullptr;            // [nnz] rank of the entry within its column
+  int32_t* d_rowptr = nullptr;           // per block: h + 1 row starts (block-relative)
+  std::vector<int64_t> h_rp;             // offset of each block's row pointers
+  uint32_t* d_rflag = nullptr;           // [n] tag of the last visit of each U row
+  uint32_t* d_obar = nullptr;            // per launched block: two barrier counters
+  double* d_opart = nullptr;             // per stage: SSE partial
+  int64_t* d_conv = nullptr;             // per block: converge iters_used, capped
+  int ord_auto_blocks = 8;               // auto: ordered below this many blocks per batch
+  std::map<uint64_t, int> ord_cap;       // (kp, smem) -> co-resident CTAs
+
   // timing
   std::vector<bgmf::TimedLaunch> events;
   size_t events_used = 0;
@@ -260,6 +277,14 @@ int launch_piece_sweep(bgmf_ctx* ctx, const BlockWork* d_work, int nwork, int ch
 int run_step_stream_converge(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off,
                              int nbatch, double tol, int64_t cap, double alpha, double beta,
                              int64_t* iters_out, int32_t* capped_out);
+
+// ordered.cu -- order-faithful stratum sweep (V slabs in shared memory)
+void order_release(bgmf_ctx* ctx);
+int ensure_order_index(bgmf_ctx* ctx);
+bool ordered_block_ok(bgmf_ctx* ctx, int b);
+bool use_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1);
+int run_batch_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1, int pos_base,
+                      int iters, float alpha, float beta, bool conv = false, double tol = 0.0);
 
 // stream.cu -- out-of-core: ratings in pinned host memory, device slot ring
 int stream_enable(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);

@@ -183,6 +183,7 @@ void bgmf_destroy(bgmf_ctx* c) {
   free_factors(c);
   free_holdout(c);
   stream_free(c);
+  order_release(c);
   prof_mark(c, "destroy: factors/holdout/stream");
   dfree(c->d_lrow, c->stream); dfree(c->d_lcol, c->stream); dfree(c->d_val, c->stream); dfree(c->d_val64, c->stream);
   dfree(c->d_order, c->stream); dfree(c->d_sse, c->stream); dfree(c->d_bad, c->stream); dfree(c->d_work, c->stream);
@@ -214,6 +215,11 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "stagger")) c->stagger = (int)value;
   else if (!strcmp(key, "sparse_min_chunk")) c->sparse_min_chunk = value < 0 ? 0 : (int)value;
   else if (!strcmp(key, "col_ratio")) c->col_ratio = value > 0 ? value : 0.6;
+  else if (!strcmp(key, "ordered")) c->ord_mode = value < 0 ? -1 : (value != 0.0 ? 1 : 0);
+  else if (!strcmp(key, "ord_auto_blocks")) c->ord_auto_blocks = (int)value;
+  else if (!strcmp(key, "ord_warp")) c->ord_warp = value != 0.0;
+  else if (!strcmp(key, "ord_stage_ratings"))
+    c->ord_stage_ratings = value < 1 ? 1 : (int64_t)value;
   else if (!strcmp(key, "l2_wave_bytes")) c->l2_wave_bytes = value < 0 ? 0 : (int64_t)value;
   else if (!strcmp(key, "fused_max_batch")) c->fused_max_batch = (int64_t)value;
   else return fail(c, BGMF_ERR_ARG, std::string("unknown option ") + key);

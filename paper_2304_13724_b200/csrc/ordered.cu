@@ -1,0 +1,808 @@
+// ordered.cu -- order-faithful stratum sweep (fast mode, fp32).
+//
+// The reference sweeps a block's entries strictly in stored (row-major)
+// order (reference pkg/src/blockmf/_kernels.py:42-55, partition.py:124).  An
+// update reads and writes exactly one U row and one V row, so ANY execution
+// that applies the updates of every U row in stored order and the updates of
+// every V row in stored order computes the same values as the sequential
+// walk -- bit for bit, given the same arithmetic.  This kernel is such an
+// execution ("slab pipeline"):
+//   * the block's columns are cut into S slabs; CTA s of the block (a
+//     "stage") holds V slab s in shared memory for the whole launch: one TMA
+//     bulk copy (cp.async.bulk) in, one bulk copy out;
+//   * the stage's groups claim the block's rows in increasing order and
+//     apply each row's entries that fall in slab s (ascending columns, u_r
+//     in registers);
+//   * column order: entry i of column c carries its rank q_i (earlier
+//     entries of c in the block, built once per partition by
+//     ensure_order_index); it waits until the column's shared-memory counter
+//     equals q_i and releases q_i + 1 after its update;
+//   * row order: a row visits its slabs in increasing order; each visit waits
+//     until the row's flag (global memory, one word per U row) carries the
+//     tag of the visit before it (previous slab of the row, or the previous
+//     sweep's last slab), reads u_r, and publishes u_r and its own tag.
+// Deadlock freedom: the earliest unfinished entry in stored order has all its
+// predecessors done, and its row is claimed because every stage claims rows
+// in order and all stages of a launch are resident (cooperative launch).
+// Groups of one warp run independently (sub-warp masks; independent thread
+// scheduling guarantees forward progress while a group spins).
+// After the sweeps: a barrier over the block's stages, then the post-sweep
+// SSE (_kernels.py:56) with V still in shared memory, summed in a fixed order
+// (static row assignment, stages in order): the whole step is deterministic.
+
+#include "bgmf_internal.cuh"
+#include "rows.cuh"
+
+namespace bgmf {
+namespace {
+
+constexpr int kOrdThreads = 512;
+constexpr int kOrdMaxBlocks = 96;
+constexpr int kOrdMaxStages = 255;  // the row tag keeps slab + 1 in 8 bits
+constexpr uint32_t kGenLimit = 1u << 24;
+
+struct OrdBlock {
+  int64_t begin;      // first entry of the block in the partition arrays
+  int64_t rp;         // offset of the block's h + 1 row pointers in d_rowptr
+  int64_t row_start;  // U row of local row 0
+  int64_t col_start;  // V row of local column 0
+  int32_t h, w;       // rows / columns of the block
+  int32_t stage0, nstages;
+  int32_t slab_w, block_id;
+  int32_t pos, pad;
+};
+
+// Passed by value (kernel parameter space): the host never has to keep a
+// table alive for launches still queued on the stream.
+struct OrdLaunch {
+  int32_t nblocks, pad;
+  OrdBlock b[kOrdMaxBlocks];
+};
+
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];"
+               : "=r"(v)
+               : "r"((unsigned)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(p)),
+               "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned mb, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(mb), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// First index in [lo, hi) whose column is >= key (columns ascend within a
+// row).  L-ary search: every lane probes one split point per round.
+template <int L>
+__device__ __forceinline__ int group_lower_bound(const int32_t* __restrict__ a, int lo, int hi,
+                                                 int key, int gl, unsigned gmask) {
+  while (hi - lo > L) {
+    const int n = hi - lo;
+    const int p = lo + (int)(((int64_t)(gl + 1) * n) / (L + 1));
+    const unsigned bl = __ballot_sync(gmask, __ldg(a + p) < key) & gmask;
+    const int c = __popc(bl);  // probes below the key: lanes 0 .. c-1
+    const int nlo = c == 0 ? lo : lo + (int)(((int64_t)c * n) / (L + 1)) + 1;
+    const int nhi = c == L ? hi : lo + (int)(((int64_t)(c + 1) * n) / (L + 1));
+    lo = nlo;
+    hi = nhi;
+  }
+  const bool less = lo + gl < hi && __ldg(a + lo + gl) < key;
+  return lo + __popc(__ballot_sync(gmask, less) & gmask);
+}
+
+template <int V4, class LN>
+__device__ __forceinline__ void load_row_l2(float4 (&dst)[V4], const float* row, const LN& ln) {
+#pragma unroll
+  for (int q = 0; q < V4; ++q)
+    dst[q] = ln.on(q) ? __ldcg(reinterpret_cast<const float4*>(row + ln.off(q))) : zero4();
+}
+
+template <int V4, class LN>
+__device__ __forceinline__ void load_row_smem(float4 (&dst)[V4], const float* row, const LN& ln) {
+#pragma unroll
+  for (int q = 0; q < V4; ++q)
+    dst[q] = ln.on(q) ? *reinterpret_cast<const float4*>(row + ln.off(q)) : zero4();
+}
+
+template <int V4, class LN>
+__device__ __forceinline__ void store_row_g(float* row, const float4 (&u)[V4], const LN& ln) {
+#pragma unroll
+  for (int q = 0; q < V4; ++q)
+    if (ln.on(q)) *reinterpret_cast<float4*>(row + ln.off(q)) = u[q];
+}
+
+// Per-launch constants of a stage (one CTA).
+struct Stage {
+  const int32_t* rp;    // block row pointers
+  const int32_t* bcol;  // block entries: local column, value, column rank
+  const float* bval;
+  const int32_t* bq;
+  float* Ub;            // U rows of the block
+  uint32_t* fl;         // row flags of those rows
+  float* sv;            // V slab (shared memory)
+  int* cnt;             // column counters of the slab (shared memory)
+  int h, w, S, st, sw, cs, ce, nc, kp;
+};
+
+// One sweep of this stage's slab (sweep `it` of the launch).
+template <int L, int V4, bool kMask>
+__device__ __forceinline__ void stage_sweep(const Stage& T, int it, uint32_t gen, float alpha,
+                                            float beta, int pos, int* s_next,
+                                            unsigned long long* bad, int* divflag) {
+  const Lanes<L, V4, kMask> ln(T.kp);
+  const unsigned gmask = L == 32 ? kFull : (((1u << L) - 1u) << ln.gbase);
+  const float two_a = 2.0f * alpha;
+  const float2 nab = make_float2(-alpha * beta, -alpha * beta);
+  const int kp = T.kp;
+  __syncthreads();  // this stage's previous sweep / SSE is over
+  for (int i = threadIdx.x; i < T.nc; i += kOrdThreads) T.cnt[i] = 0;
+  if (threadIdx.x == 0) *s_next = 0;
+  __syncthreads();
+  const uint32_t tag_now = ((gen + (uint32_t)it) << 8) | (uint32_t)(T.st + 1);
+  while (true) {
+    int r = 0;
+    if (ln.gl == 0) r = atomicAdd(s_next, 1);
+    r = __shfl_sync(gmask, r, ln.gbase);
+    if (r >= T.h) break;
+    const int rb = __ldg(T.rp + r), re = __ldg(T.rp + r + 1);
+    if (rb == re) continue;
+    int lo = rb, hi = re;
+    if (T.cs > 0) lo = group_lower_bound<L>(T.bcol, rb, re, T.cs, ln.gl, gmask);
+    if (T.ce < T.w) hi = group_lower_bound<L>(T.bcol, lo, re, T.ce, ln.gl, gmask);
+    if (lo == hi) continue;
+    // row order (several stages): the visit before this one published u_r;
+    // one stage: earlier sweeps are ordered by the CTA barrier
+    uint32_t want = 0;
+    if (T.S > 1) {
+      if (lo > rb)
+        want = ((gen + (uint32_t)it) << 8) | (uint32_t)(__ldg(T.bcol + lo - 1) / T.sw + 1);
+      else if (it > 0)
+        want = ((gen + (uint32_t)it - 1u) << 8) | (uint32_t)(__ldg(T.bcol + re - 1) / T.sw + 1);
+    }
+    if (want)
+      while (!__all_sync(gmask, ld_acquire_gpu(T.fl + r) == want)) __nanosleep(20);
+    float4 u[V4];
+    load_row_l2<V4>(u, T.Ub + (int64_t)r * kp, ln);
+    for (int t0 = lo; t0 < hi; t0 += L) {
+      int cA = 0, qA = 0;
+      float xA = 0.f;
+      if (t0 + ln.gl < hi) {
+        cA = __ldg(T.bcol + t0 + ln.gl);
+        xA = __ldg(T.bval + t0 + ln.gl);
+        qA = __ldg(T.bq + t0 + ln.gl);
+      }
+      const int nt = min(L, hi - t0);
+      for (int j = 0; j < nt; ++j) {
+        const int c = __shfl_sync(gmask, cA, ln.gbase + j) - T.cs;
+        const float x = __shfl_sync(gmask, xA, ln.gbase + j);
+        const int q = __shfl_sync(gmask, qA, ln.gbase + j);
+        int* cp = T.cnt + c;
+        // column order: every earlier entry of this column has been applied
+        while (!__all_sync(gmask, ld_acquire_cta(cp) == q)) {
+        }
+        float* vr = T.sv + (size_t)c * kp;
+        float4 v[V4];
+        load_row_smem<V4>(v, vr, ln);
+        const float dot = group_sum_m<L>(dot_slice<V4>(u, v), gmask);
+        const float e = x - dot;
+        if (!isfinite(e) && ln.gl == 0) {
+          atomicMin(bad, pack_bad(pos, it, t0 + j));
+          *divflag = 1;
+        }
+        const float gg = two_a * e;
+        const float2 g2 = make_float2(gg, gg);
+#pragma unroll
+        for (int q4 = 0; q4 < V4; ++q4) {
+          const float2 ul = lo2(u[q4]), uh = hi2(u[q4]), vl = lo2(v[q4]), vh = hi2(v[q4]);
+          // the chunked kernel's operation shapes: dv = 2ae*u_old - ab*v,
+          // du = 2ae*v - ab*u_old, then u + du, v + dv
+          const float2 dvl = __ffma2_rn(g2, ul, __fmul2_rn(nab, vl));
+          const float2 dvh = __ffma2_rn(g2, uh, __fmul2_rn(nab, vh));
+          const float2 dul = __ffma2_rn(g2, vl, __fmul2_rn(nab, ul));
+          const float2 duh = __ffma2_rn(g2, vh, __fmul2_rn(nab, uh));
+          u[q4] = cat4(__fadd2_rn(ul, dul), __fadd2_rn(uh, duh));
+          if (ln.on(q4))
+            *reinterpret_cast<float4*>(vr + ln.off(q4)) =
+                cat4(__fadd2_rn(vl, dvl), __fadd2_rn(vh, dvh));
+        }
+        __syncwarp(gmask);
+        if (ln.gl == 0) st_release_cta(cp, q + 1);
+      }
+    }
+    store_row_g<V4>(T.Ub + (int64_t)r * kp, u, ln);
+    if (T.S > 1) {
+      __threadfence();
+      __syncwarp(gmask);
+      if (ln.gl == 0) st_release_gpu(T.fl + r, tag_now);
+    }
+  }
+}
+
+// This stage's share of the block's post-sweep SSE: rows g, g + NG, ...
+// (static assignment), groups of a warp in order, warps in order.  The total
+// is valid in thread 0.
+template <int L, int V4, bool kMask>
+__device__ __forceinline__ double stage_sse(const Stage& T, double* s_red) {
+  constexpr int NG = kOrdThreads / L;
+  const Lanes<L, V4, kMask> ln(T.kp);
+  const unsigned gmask = L == 32 ? kFull : (((1u << L) - 1u) << ln.gbase);
+  const int kp = T.kp;
+  double acc = 0.0;
+  for (int r = (int)threadIdx.x / L; r < T.h; r += NG) {
+    const int rb = __ldg(T.rp + r), re = __ldg(T.rp + r + 1);
+    if (rb == re) continue;
+    int lo = rb, hi = re;
+    if (T.cs > 0) lo = group_lower_bound<L>(T.bcol, rb, re, T.cs, ln.gl, gmask);
+    if (T.ce < T.w) hi = group_lower_bound<L>(T.bcol, lo, re, T.ce, ln.gl, gmask);
+    if (lo == hi) continue;
+    float4 u[V4];
+    load_row_l2<V4>(u, T.Ub + (int64_t)r * kp, ln);
+    for (int t0 = lo; t0 < hi; t0 += L) {
+      int cA = 0;
+      float xA = 0.f;
+      if (t0 + ln.gl < hi) {
+        cA = __ldg(T.bcol + t0 + ln.gl);
+        xA = __ldg(T.bval + t0 + ln.gl);
+      }
+      const int nt = min(L, hi - t0);
+      for (int j = 0; j < nt; ++j) {
+        const int c = __shfl_sync(gmask, cA, ln.gbase + j) - T.cs;
+        const float x = __shfl_sync(gmask, xA, ln.gbase + j);
+        float4 v[V4];
+        load_row_smem<V4>(v, T.sv + (size_t)c * kp, ln);
+        const float dot = group_sum_m<L>(dot_slice<V4>(u, v), gmask);
+        const double ed = (double)x - (double)dot;
+        acc += ed * ed;
+      }
+    }
+  }
+  __syncwarp();
+  double wsum = 0.0;
+#pragma unroll
+  for (int j = 0; j < 32 / L; ++j) wsum += __shfl_sync(kFull, acc, j * L);
+  __syncthreads();  // s_red may still be read by the previous call's thread 0
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = wsum;
+  __syncthreads();
+  double tot = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kOrdThreads / 32; ++w) tot += s_red[w];
+  return tot;
+}
+
+// Barrier over the block's S stages (all co-resident): barrier number k of
+// the launch completes when the counter reaches (k + 1) * S.
+__device__ __forceinline__ void block_barrier(uint32_t* ctr, int S, uint32_t k) {
+  __syncthreads();
+  if (S > 1) {
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(ctr, 1u);
+      while (ld_acquire_gpu(ctr) < (k + 1u) * (uint32_t)S) __nanosleep(64);
+    }
+    __syncthreads();
+  }
+}
+
+// The block's SSE: every stage's partial, summed in stage order by every
+// stage (the same bits everywhere).  Valid in thread 0.
+template <int L, int V4, bool kMask>
+__device__ __forceinline__ double block_sse_all(const Stage& T, double* s_red, double* part,
+                                                int stage0, uint32_t* ctr, uint32_t& nbar,
+                                                double* s_bcast) {
+  const double mine = stage_sse<L, V4, kMask>(T, s_red);
+  if (T.S == 1) {
+    if (threadIdx.x == 0) *s_bcast = mine;
+    __syncthreads();
+    return *s_bcast;
+  }
+  if (threadIdx.x == 0) part[stage0 + T.st] = mine;
+  block_barrier(ctr, T.S, nbar++);
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    for (int s2 = 0; s2 < T.S; ++s2) sum += __ldcg(part + stage0 + s2);
+    *s_bcast = sum;
+  }
+  __syncthreads();
+  return *s_bcast;
+}
+
+// conv = 0: `iters` sweeps, then the post-sweep SSE (sgd_sweeps,
+// _kernels.py:31-59).  conv = 1: ConvergeEachBlock on the device
+// (sgd_converge, _kernels.py:62-100): sse_before, then sweeps until the
+// block's RMSE improvement drops below tol or `iters` (the cap) sweeps ran;
+// iters_used / capped per block to conv_out[2 * block_id + 0 / 1].
+template <int L, int V4, bool kMask>
+__global__ void __launch_bounds__(kOrdThreads, 1)
+ordered_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restrict__ lcol,
+               const float* __restrict__ val, const int32_t* __restrict__ qrank,
+               const int32_t* __restrict__ rowptr, float* __restrict__ U, float* __restrict__ V,
+               int kp, float alpha, float beta, int iters, uint32_t gen,
+               uint32_t* __restrict__ rflag, uint32_t* __restrict__ bar,
+               double* __restrict__ part, double* __restrict__ sse,
+               unsigned long long* __restrict__ bad, int conv, double tol,
+               int64_t* __restrict__ conv_out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ int s_next;
+  __shared__ int s_div;
+  __shared__ double s_red[kOrdThreads / 32];
+  __shared__ double s_bcast;
+  __shared__ __align__(8) unsigned long long s_mbar;
+
+  int bi = 0;
+  {
+    int lo = 0, hi = P.nblocks - 1;  // last block with stage0 <= blockIdx.x
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.b[mid].stage0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    bi = lo;
+  }
+  const OrdBlock B = P.b[bi];
+  Stage T;
+  T.S = B.nstages;
+  T.st = (int)blockIdx.x - B.stage0;
+  T.sw = B.slab_w;
+  T.cs = T.st * T.sw;
+  T.ce = min(T.cs + T.sw, B.w);
+  T.nc = T.ce - T.cs;
+  T.h = B.h;
+  T.w = B.w;
+  T.kp = kp;
+  T.rp = rowptr + B.rp;
+  T.bcol = lcol + B.begin;
+  T.bval = val + B.begin;
+  T.bq = qrank + B.begin;
+  T.Ub = U + B.row_start * kp;
+  T.fl = rflag + B.row_start;
+  T.sv = reinterpret_cast<float*>(smem);
+  T.cnt = reinterpret_cast<int*>(T.sv + (size_t)T.sw * kp);
+  uint32_t* ctr = bar + 3 * bi;      // barrier counter, arrivals at the end, divergence
+  const unsigned bytes = (unsigned)T.nc * (unsigned)kp * 4u;
+  float* gv = V + (B.col_start + T.cs) * kp;
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
+  const unsigned sva = (unsigned)__cvta_generic_to_shared(T.sv);
+
+  // V slab -> shared memory (TMA bulk copy, completion on an mbarrier)
+  if (threadIdx.x == 0) {
+    s_div = 0;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bytes > 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            sva),
+        "l"(gv), "r"(bytes), "r"(mb)
+        : "memory");
+  }
+  if (bytes > 0)
+    while (!mbar_try_wait(mb, 0)) {
+    }
+
+  uint32_t nbar = 0;
+  int swept = 0;
+  double sse_now = 0.0;
+  const double cntd = (double)(__ldg(T.rp + T.h));  // entries of the block
+  if (!conv) {
+    for (int it = 0; it < iters; ++it)
+      stage_sweep<L, V4, kMask>(T, it, gen, alpha, beta, B.pos, &s_next, bad, &s_div);
+    swept = iters;
+    if (swept > 0) block_barrier(ctr, T.S, nbar++);  // every stage done: U is final
+  } else {
+    // sse_before, then sweep -> SSE -> improvement test, all on the device
+    sse_now = block_sse_all<L, V4, kMask>(T, s_red, part, B.stage0, ctr, nbar, &s_bcast);
+    double rmse_prev = sqrt(sse_now / cntd);
+    bool capped = true;
+    while (swept < iters) {
+      stage_sweep<L, V4, kMask>(T, swept, gen, alpha, beta, B.pos, &s_next, bad, &s_div);
+      ++swept;
+      __syncthreads();
+      if (threadIdx.x == 0 && s_div && T.S > 1) atomicOr(ctr + 2, 1u);
+      block_barrier(ctr, T.S, nbar++);
+      // a non-finite residual anywhere in the block ends its loop
+      if (threadIdx.x == 0) s_bcast = (double)(T.S > 1 ? ld_acquire_gpu(ctr + 2) : 0u) + (double)s_div;
+      __syncthreads();
+      const bool diverged = s_bcast != 0.0;
+      __syncthreads();
+      if (diverged) { capped = false; break; }
+      sse_now = block_sse_all<L, V4, kMask>(T, s_red, part, B.stage0, ctr, nbar, &s_bcast);
+      if (!isfinite(sse_now)) {  // _kernels.py:88-89: (count - 1, iters - 1)
+        if (threadIdx.x == 0 && T.st == 0)
+          atomicMin(bad, pack_bad(B.pos, swept - 1, (int64_t)cntd - 1));
+        capped = false;
+        break;
+      }
+      const double rmse_now = sqrt(sse_now / cntd);
+      if (rmse_prev - rmse_now < tol) { capped = false; break; }
+      rmse_prev = rmse_now;
+    }
+    if (threadIdx.x == 0 && T.st == 0) {
+      conv_out[2 * B.block_id] = swept;
+      conv_out[2 * B.block_id + 1] = capped ? 1 : 0;
+    }
+  }
+
+  // V slab back to global memory (TMA bulk store)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0 && bytes > 0 && swept > 0) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gv),
+                 "r"(sva), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  if (!conv) sse_now = block_sse_all<L, V4, kMask>(T, s_red, part, B.stage0, ctr, nbar, &s_bcast);
+  if (threadIdx.x == 0) {
+    if (T.st == 0) sse[B.block_id] = sse_now;
+    if (T.S > 1) {
+      // the last stage out resets the block's counters for the next launch
+      const unsigned done = atomicAdd(ctr + 1, 1u);
+      if (done == (unsigned)T.S - 1) {
+        ctr[0] = 0u;
+        ctr[1] = 0u;
+        ctr[2] = 0u;
+      }
+    }
+    if (bytes > 0 && swept > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
+// ---- order index (once per partition) ---------------------------------
+__device__ __forceinline__ int block_of(const int64_t* __restrict__ off, int nb, int64_t i) {
+  int lo = 0, hi = nb - 1;  // last b with off[b] <= i
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= i) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void rank_keys(const int32_t* __restrict__ lcol, const int64_t* __restrict__ off,
+                          int nb, int64_t n, int cbits, uint64_t* __restrict__ keys,
+                          uint32_t* __restrict__ idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = ((uint64_t)block_of(off, nb, i) << cbits) | (uint32_t)lcol[i];
+    idx[i] = (uint32_t)i;
+  }
+}
+
+// keys sorted by (block, column), stable: a run's first position per key
+__global__ void rank_heads(const uint64_t* __restrict__ keys, int64_t n,
+                           uint32_t* __restrict__ first) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    if (p == 0 || keys[p - 1] != keys[p]) first[keys[p]] = (uint32_t)p;
+}
+
+__global__ void rank_scatter(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                             const uint32_t* __restrict__ first, int64_t n,
+                             int32_t* __restrict__ q) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    q[idx[p]] = (int32_t)((uint32_t)p - first[keys[p]]);
+}
+
+// Row pointers of every block (relative to the block's first entry): the
+// entry that starts row r (or the first entry after an empty run of rows)
+// writes the pointers of the rows it closes.
+__global__ void row_pointers(const int32_t* __restrict__ lrow, const int64_t* __restrict__ off,
+                             const int64_t* __restrict__ rpo, int nb, int64_t n,
+                             int32_t* __restrict__ rowptr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = block_of(off, nb, i);
+    const int64_t beg = off[b], end = off[b + 1];
+    const int r = lrow[i];
+    const int prev = i > beg ? lrow[i - 1] : -1;
+    int32_t* rp = rowptr + rpo[b];
+    for (int rr = prev + 1; rr <= r; ++rr) rp[rr] = (int32_t)(i - beg);
+    if (i == end - 1) {
+      const int h = (int)(rpo[b + 1] - rpo[b] - 1);
+      for (int rr = r + 1; rr <= h; ++rr) rp[rr] = (int32_t)(end - beg);
+    }
+  }
+}
+
+// Shape of the ordered kernel's groups.  warp = 1: one group per warp (L =
+// 32, up to 4 float4 per lane), so a group spinning on a column counter or a
+// row flag never shares its warp with the group it waits for.
+Shape ordered_shape(int kp, int warp) {
+  if (!warp) return shape_for(kp);
+  const int f4 = kp / 4;
+  int v4 = 1;
+  while (32 * v4 < f4) ++v4;
+  return {32, v4};
+}
+
+#define BGMF_ORD_SHAPES(X)                                                              \
+  BGMF_SHAPES(X) X(32, 1, true) X(32, 1, false) X(32, 2, true) X(32, 2, false) X(32, 3, true)
+
+#define BGMF_ORD(LL, VV, MM)                                           \
+  if (sh.L == LL && sh.V4 == VV && mk == MM)                           \
+    return reinterpret_cast<const void*>(&ordered_kernel<LL, VV, MM>);
+const void* ordered_kernel_ptr(int kp, int warp) {
+  const Shape sh = ordered_shape(kp, warp);
+  const bool mk = needs_mask(sh, kp);
+  BGMF_ORD_SHAPES(BGMF_ORD)
+  return nullptr;
+}
+#undef BGMF_ORD
+
+size_t slab_smem(int cols, int kp) { return (size_t)cols * ((size_t)kp * 4 + 4); }
+
+// Largest dynamic shared memory a CTA may ask for (static smem aside).
+size_t smem_budget(bgmf_ctx* c) {
+  static int optin = 0;
+  if (!optin) cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+  const size_t stat = 1024;  // s_next, s_red, s_mbar + slack
+  return optin > (int)stat ? (size_t)optin - stat : 0;
+}
+
+// co-resident CTAs of the ordered kernel with `smem` bytes of dynamic smem
+int ordered_capacity(bgmf_ctx* c, size_t smem) {
+  const void* fn = ordered_kernel_ptr(c->kp, c->ord_warp);
+  if (!fn) return 0;
+  const uint64_t key = ((uint64_t)c->kp << 33) | ((uint64_t)c->ord_warp << 32) | (uint64_t)smem;
+  auto it = c->ord_cap.find(key);
+  if (it != c->ord_cap.end()) return it->second;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_budget(c));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kOrdThreads, smem);
+  c->ord_cap[key] = per_sm * c->num_sms;
+  return per_sm * c->num_sms;
+}
+
+}  // namespace
+
+void order_release(bgmf_ctx* c) {
+  dfree(c->d_qrank, c->stream);
+  dfree(c->d_rowptr, c->stream);
+  dfree(c->d_rflag, c->stream);
+  dfree(c->d_obar, c->stream);
+  dfree(c->d_conv, c->stream);
+  c->d_conv = nullptr;
+  dfree(c->d_opart, c->stream);
+  c->d_qrank = c->d_rowptr = nullptr;
+  c->d_rflag = c->d_obar = nullptr;
+  c->d_opart = nullptr;
+  c->h_rp.clear();
+  c->ord_ready = false;
+}
+
+int sort_pairs_device(bgmf_ctx* ctx, uint64_t** keys, uint32_t** vals, int64_t n, int bits);
+
+// Column ranks and row pointers of the resident partition (once per
+// partition; ~24 B per rating of temporaries).
+int ensure_order_index(bgmf_ctx* c) {
+  if (c->ord_ready) return BGMF_OK;
+  if (!c->partitioned) return fail(c, BGMF_ERR_STATE, "no partition");
+  cudaStream_t s = c->stream;
+  const int nb = c->I * c->J;
+  const int64_t n = c->nnz;
+  c->h_rp.assign(nb + 1, 0);
+  for (int b = 0; b < nb; ++b) {
+    const int bi = b / c->J;
+    c->h_rp[b + 1] = c->h_rp[b] + (c->row_bounds[bi + 1] - c->row_bounds[bi]) + 1;
+  }
+  int bbits = 0;
+  while (bbits < 31 && (1ll << bbits) < nb) ++bbits;
+  const int key_bits = bbits + c->cbits;
+  int64_t *d_off = nullptr, *d_rpo = nullptr;
+  uint64_t* keys = nullptr;
+  uint32_t *idx = nullptr, *first = nullptr;
+  auto cleanup = [&]() {
+    dfree(d_off, s); dfree(d_rpo, s); dfree(keys, s); dfree(idx, s); dfree(first, s);
+  };
+  const size_t N = (size_t)(n > 0 ? n : 1);
+  cudaError_t e = dmalloc(&c->d_qrank, N * 4, s);
+  if (e == cudaSuccess) e = dmalloc(&c->d_rowptr, (size_t)c->h_rp[nb] * 4, s);
+  if (e == cudaSuccess) e = dmalloc(&c->d_rflag, (size_t)(c->n > 0 ? c->n : 1) * 4, s);
+  if (e == cudaSuccess) e = dmalloc(&c->d_obar, (size_t)3 * kOrdMaxBlocks * 4, s);
+  if (e == cudaSuccess) e = dmalloc(&c->d_conv, (size_t)2 * (nb > 0 ? nb : 1) * 8, s);
+  if (e == cudaSuccess) e = dmalloc(&c->d_opart, (size_t)8192 * 8, s);
+  if (e == cudaSuccess) e = dmalloc(&d_off, (size_t)(nb + 1) * 8, s);
+  if (e == cudaSuccess) e = dmalloc(&d_rpo, (size_t)(nb + 1) * 8, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_rflag, 0, (size_t)(c->n > 0 ? c->n : 1) * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_obar, 0, (size_t)3 * kOrdMaxBlocks * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_rowptr, 0, (size_t)c->h_rp[nb] * 4, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_off, c->h_offsets.data(), (size_t)(nb + 1) * 8, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_rpo, c->h_rp.data(), (size_t)(nb + 1) * 8, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && n > 0) e = dmalloc(&keys, N * 8, s);
+  if (e == cudaSuccess && n > 0) e = dmalloc(&idx, N * 4, s);
+  if (e == cudaSuccess && n > 0) e = dmalloc(&first, ((size_t)nb << c->cbits) * 4, s);
+  if (e != cudaSuccess) {
+    cleanup();
+    order_release(c);
+    return cuda_fail(c, e, "ensure_order_index");
+  }
+  const int grid = c->num_sms * 8;
+  if (n > 0) {
+    rank_keys<<<grid, 256, 0, s>>>(c->d_lcol, d_off, nb, n, c->cbits, keys, idx);
+    int rc = sort_pairs_device(c, &keys, &idx, n, key_bits);
+    if (rc) { cleanup(); order_release(c); return rc; }
+    rank_heads<<<grid, 256, 0, s>>>(keys, n, first);
+    rank_scatter<<<grid, 256, 0, s>>>(keys, idx, first, n, c->d_qrank);
+    row_pointers<<<grid, 256, 0, s>>>(c->d_lrow, d_off, d_rpo, nb, n, c->d_rowptr);
+  }
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cleanup();
+  if (e != cudaSuccess) { order_release(c); return cuda_fail(c, e, "ensure_order_index"); }
+  c->ord_gen = 1;
+  c->ord_ready = true;
+  return BGMF_OK;
+}
+
+// Can the ordered kernel take block b (its V block in <= kOrdMaxStages
+// slabs that each fit a CTA, all of them co-resident, row pointers in int32)?
+bool ordered_block_ok(bgmf_ctx* c, int b) {
+  if (c->exact || c->streaming || !ordered_kernel_ptr(c->kp, c->ord_warp)) return false;
+  const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
+  if (cnt >= INT32_MAX) return false;
+  const int64_t w = c->col_bounds[b % c->J + 1] - c->col_bounds[b % c->J];
+  const int64_t per = (int64_t)(smem_budget(c) / ((size_t)c->kp * 4 + 4));
+  if (per < 1) return false;
+  const int64_t smin = (w + per - 1) / per;
+  if (smin > kOrdMaxStages) return false;
+  const int cap = ordered_capacity(c, slab_smem((int)((w + smin - 1) / smin), c->kp));
+  return smin <= cap;
+}
+
+// One batch (stratum, or part of one) through the ordered kernel: `iters`
+// sweeps and the post-sweep SSE of every block in plan[q0 .. q1) (plan
+// positions pos_base + q), as few cooperative launches as co-residency
+// allows.  The caller has checked ordered_block_ok for every block.
+int run_batch_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, int pos_base,
+                      int iters, float alpha, float beta, bool conv, double tol) {
+  int rc = ensure_order_index(c);
+  if (rc) return rc;
+  cudaStream_t s = c->stream;
+  const void* fn = ordered_kernel_ptr(c->kp, c->ord_warp);
+  const size_t budget = smem_budget(c);
+  const int64_t per = (int64_t)(budget / ((size_t)c->kp * 4 + 4));
+  struct Item { int b, pos, S, sw; size_t smem; };
+  std::vector<Item> items;
+  int nonempty = 0;
+  for (int q = q0; q < q1; ++q)
+    nonempty += c->h_offsets[plan[q] + 1] > c->h_offsets[plan[q]];
+  for (int q = q0; q < q1; ++q) {
+    const int b = plan[q];
+    const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
+    if (cnt == 0) continue;  // its SSE stays 0
+    const int64_t w = c->col_bounds[b % c->J + 1] - c->col_bounds[b % c->J];
+    const int64_t smin = (w + per - 1) / per;
+    // stages: enough for the slab to fit; more while the stratum leaves SMs
+    // idle, at ~ord_stage_ratings ratings per stage (a row then visits more
+    // slabs: each visit moves u_r through L2)
+    int64_t S = (cnt + c->ord_stage_ratings - 1) / c->ord_stage_ratings;
+    const int64_t fill = c->num_sms / (nonempty > 0 ? nonempty : 1);
+    if (S > fill) S = fill;
+    if (S < smin) S = smin;
+    if (S > w) S = w;
+    if (S > kOrdMaxStages) S = kOrdMaxStages;
+    if (S < 1) S = 1;
+    const int64_t swd = (w + S - 1) / S;
+    S = (w + swd - 1) / swd;  // no empty slab
+    items.push_back({b, pos_base + q, (int)S, (int)swd, slab_smem((int)swd, c->kp)});
+  }
+  size_t i = 0;
+  while (i < items.size()) {
+    // pack blocks into one launch while every stage stays co-resident
+    OrdLaunch L{};
+    size_t smem = 0;
+    int ctas = 0;
+    size_t j = i;
+    while (j < items.size() && L.nblocks < kOrdMaxBlocks) {
+      const size_t sm2 = std::max(smem, items[j].smem);
+      if (ctas + items[j].S > ordered_capacity(c, sm2) && L.nblocks > 0) break;
+      const int b = items[j].b;
+      OrdBlock& ob = L.b[L.nblocks++];
+      const int bi = b / c->J, bj = b % c->J;
+      ob.begin = c->h_offsets[b];
+      ob.rp = c->h_rp[b];
+      ob.row_start = c->row_bounds[bi];
+      ob.col_start = c->col_bounds[bj];
+      ob.h = (int32_t)(c->row_bounds[bi + 1] - c->row_bounds[bi]);
+      ob.w = (int32_t)(c->col_bounds[bj + 1] - c->col_bounds[bj]);
+      ob.stage0 = ctas;
+      ob.nstages = items[j].S;
+      ob.slab_w = items[j].sw;
+      ob.block_id = b;
+      ob.pos = items[j].pos;
+      ctas += items[j].S;
+      smem = sm2;
+      ++j;
+    }
+    if (ctas > ordered_capacity(c, smem) || ctas > 8192)
+      return fail(c, BGMF_ERR_STATE, "ordered sweep: block does not fit the GPU");
+    if (c->ord_gen + (uint32_t)iters + 1u >= kGenLimit) {
+      BGMF_CK(c, cudaMemsetAsync(c->d_rflag, 0, (size_t)c->n * 4, s));
+      c->ord_gen = 1;
+    }
+    uint32_t gen = c->ord_gen;
+    c->ord_gen += (uint32_t)(iters > 0 ? iters : 1);  // converge: iters = the cap
+    double ratings = 0;
+    for (size_t t = i; t < j; ++t)
+      ratings += (double)(c->h_offsets[items[t].b + 1] - c->h_offsets[items[t].b]);
+    const int32_t* lcol = c->d_lcol;
+    const float* val = c->d_val;
+    const int32_t* qr = c->d_qrank;
+    const int32_t* rpp = c->d_rowptr;
+    float* U = c->d_u;
+    float* V = c->d_v;
+    int kp = c->kp, its = iters;
+    uint32_t* rfl = c->d_rflag;
+    uint32_t* bar = c->d_obar;
+    double* part = c->d_opart;
+    double* sse = c->d_sse;
+    unsigned long long* bad = c->d_bad;
+    int cv = conv ? 1 : 0;
+    int64_t* cout = c->d_conv;
+    void* args[] = {&L, &lcol, &val, &qr, &rpp, &U, &V, &kp, &alpha, &beta, &its, &gen,
+                    &rfl, &bar, &part, &sse, &bad, &cv, &tol, &cout};
+    TimedLaunch* slot = nullptr;
+    if (c->timing) record_begin(c, 0, ratings * iters * (12.0 + 16.0 * c->k), &slot);
+    BGMF_CK(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)budget));
+    BGMF_CK(c, cudaLaunchCooperativeKernel(fn, dim3(ctas), dim3(kOrdThreads), args, smem, s));
+    if (slot) record_end(c, slot);
+    i = j;
+  }
+  return BGMF_OK;
+}
+
+// Ordered routing of one batch: mode 1 = every block the kernel can take;
+// -1 (auto) = the same; 0 = never.  All blocks of the batch must qualify.
+// Routing of one batch.  ord_mode 1: ordered whenever every block fits;
+// 0: never; -1 (auto): ordered when it fits and the chunked sweep's
+// concurrency would distort the reference order -- fewer than
+// ord_auto_blocks non-empty blocks in the batch (each block then gets
+// hundreds to thousands of concurrent chunks, rows split across many of
+// them: every fast-mode drift past 1e-3 found by the randomised sweeps,
+// DESIGN.md section 4) or a dense block (> 1/8 of its cells rated: rows share
+// their columns and concurrent chunks collide on every V row).
+bool use_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1) {
+  if (c->ord_mode == 0 || c->exact || c->streaming) return false;
+  int nonempty = 0;
+  bool dense = false;
+  for (int q = q0; q < q1; ++q) {
+    const int b = plan[q];
+    const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
+    if (cnt == 0) continue;
+    ++nonempty;
+    const int64_t h = c->row_bounds[b / c->J + 1] - c->row_bounds[b / c->J];
+    const int64_t w = c->col_bounds[b % c->J + 1] - c->col_bounds[b % c->J];
+    dense |= cnt * 8 > h * w;
+    if (!ordered_block_ok(c, b)) return false;
+  }
+  if (c->ord_mode > 0) return true;
+  return nonempty < c->ord_auto_blocks || dense;
+}
+
+}  // namespace bgmf

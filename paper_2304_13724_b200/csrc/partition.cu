@@ -333,6 +333,56 @@ void free_dev(T*& p, cudaStream_t s) {
 
 }  // namespace
 
+// Stable LSD radix sort of (key, payload) pairs over key bits [0, bits), with
+// the partitioner's kernels.  *keys / *vals are swapped with the sorted
+// buffers (the caller frees whatever they point to afterwards).  Used by the
+// ordered sweep's column-rank index (ordered.cu).
+int sort_pairs_device(bgmf_ctx* ctx, uint64_t** keys, uint32_t** vals, int64_t n, int bits) {
+  if (n <= 1 || bits <= 0) return BGMF_OK;
+  cudaStream_t s = ctx->stream;
+  const bool wide = (bits + 8) / 9 < (bits + 7) / 8;
+  const int dbits = wide ? 9 : 8, RD = 1 << dbits;
+  const int passes = (bits + dbits - 1) / dbits;
+  const int64_t ntiles = (n + RS_TILE - 1) / RS_TILE;
+  uint64_t* kb = nullptr;
+  uint32_t *ib = nullptr, *hist = nullptr, *tot = nullptr;
+  auto cleanup = [&]() { free_dev(kb, s); free_dev(ib, s); free_dev(hist, s); free_dev(tot, s); };
+  cudaError_t e = dmalloc(&kb, (size_t)n * 8, s);
+  if (e == cudaSuccess) e = dmalloc(&ib, (size_t)n * 4, s);
+  if (e == cudaSuccess) e = dmalloc(&hist, (size_t)RD * ntiles * 4, s);
+  if (e == cudaSuccess) e = dmalloc(&tot, (size_t)RD * 4, s);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(&radix_scatter<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)scatter_smem<512>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(&radix_scatter<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)scatter_smem<256>());
+  if (e != cudaSuccess) { cleanup(); return cuda_fail(ctx, e, "sort_pairs_device"); }
+  uint64_t* ka = *keys;
+  uint32_t* ia = *vals;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = dbits * p;
+    if (wide) {
+      radix_hist<512><<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, n, shift, ntiles, hist);
+      radix_scan_tiles<<<512, 1024, 0, s>>>(hist, ntiles, tot);
+      radix_scatter<512><<<(unsigned)ntiles, RS_THREADS, scatter_smem<512>(), s>>>(
+          ka, ia, kb, ib, n, shift, hist, ntiles, tot);
+    } else {
+      radix_hist<256><<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, n, shift, ntiles, hist);
+      radix_scan_tiles<<<256, 1024, 0, s>>>(hist, ntiles, tot);
+      radix_scatter<256><<<(unsigned)ntiles, RS_THREADS, scatter_smem<256>(), s>>>(
+          ka, ia, kb, ib, n, shift, hist, ntiles, tot);
+    }
+    uint64_t* tk = ka; ka = kb; kb = tk;
+    uint32_t* ti = ia; ia = ib; ib = ti;
+  }
+  e = cudaGetLastError();
+  *keys = ka;
+  *vals = ia;
+  cleanup();  // the spare buffers (kb/ib now hold the other halves)
+  return e == cudaSuccess ? BGMF_OK : cuda_fail(ctx, e, "sort_pairs_device");
+}
+
 // dev_in: rows/cols/vals are device buffers whose ownership passes to this
 // call (freed as soon as they are consumed); otherwise host arrays.
 int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
@@ -357,7 +407,8 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   if (rbits + cbits + bbits > 64) return fail(ctx, BGMF_ERR_ARG, "grid too large for 64-bit keys");
   if (rbits > 31 || cbits > 31) return fail(ctx, BGMF_ERR_ARG, "block slab wider than 2^31");
 
-  // release any previous partition
+  // release any previous partition (and its order index)
+  order_release(ctx);
   free_dev(ctx->d_lrow, ctx->stream); free_dev(ctx->d_lcol, ctx->stream); free_dev(ctx->d_val, ctx->stream);
   free_dev(ctx->d_val64, ctx->stream); free_dev(ctx->d_order, ctx->stream);
   ctx->partitioned = false;

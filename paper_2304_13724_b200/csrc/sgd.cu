@@ -32,6 +32,7 @@
 #include <atomic>
 
 #include "bgmf_internal.cuh"
+#include "rows.cuh"
 
 namespace bgmf {
 namespace {
@@ -80,12 +81,6 @@ __device__ __forceinline__ int find_work(const BlockWork* __restrict__ work, int
   return lo;
 }
 
-template <int L>
-__device__ __forceinline__ float group_sum(float x) {
-#pragma unroll
-  for (int o = L / 2; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
-  return x;
-}
 
 // Chunk geometry shared by the sweep and SSE kernels.
 struct Chunk {
@@ -112,25 +107,6 @@ __device__ __forceinline__ Chunk locate_chunk(const BlockWork* __restrict__ work
   return ch;
 }
 
-// Lane geometry of a group.  kMask: the padded row kp is narrower than the
-// group's 4*L*V4 floats, so some lanes/vectors sit past the row and are
-// predicated off (only for odd k; k = 32/64/128 run unmasked).
-template <int L, int V4, bool kMask>
-struct Lanes {
-  int gl, gbase;
-  bool on_[V4];
-  __device__ __forceinline__ Lanes(int kp) {
-    const int lane = threadIdx.x & 31;
-    gl = lane & (L - 1);
-    gbase = lane & ~(L - 1);
-#pragma unroll
-    for (int q = 0; q < V4; ++q) on_[q] = !kMask || 4 * (q * L + gl) < kp;
-  }
-  __device__ __forceinline__ bool on(int q) const { return !kMask || on_[q]; }
-  __device__ __forceinline__ int off(int q) const { return 4 * (q * L + gl); }
-};
-
-__device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
 // Rating triple of entry i.  cbits < 0: SoA int32 row / int32 col arrays;
 // cbits >= 0: packed 4-byte (row << cbits | col) records in `lrow` (the
@@ -153,11 +129,6 @@ __device__ __forceinline__ void load_triple(const int32_t* __restrict__ lrow,
 __device__ __forceinline__ int load_rowidx(const int32_t* __restrict__ lrow, int cbits,
                                            int64_t i) {
   return cbits < 0 ? __ldg(lrow + i) : (int)((uint32_t)__ldg(lrow + i) >> cbits);
-}
-__device__ __forceinline__ float2 lo2(const float4& a) { return make_float2(a.x, a.y); }
-__device__ __forceinline__ float2 hi2(const float4& a) { return make_float2(a.z, a.w); }
-__device__ __forceinline__ float4 cat4(const float2& a, const float2& b) {
-  return make_float4(a.x, a.y, b.x, b.y);
 }
 
 // L2-coherent 128-bit load (the factors are written by other SMs during the
@@ -187,17 +158,6 @@ __device__ __forceinline__ void store_row(float* row, const float4 (&u)[V4], con
     if (ln.on(q)) *reinterpret_cast<float4*>(row + ln.off(q)) = u[q];
 }
 
-// partial dot of the lane's slice with packed FFMA2 (two fp32 lanes per op)
-template <int V4>
-__device__ __forceinline__ float dot_slice(const float4 (&u)[V4], const float4 (&v)[V4]) {
-  float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int q = 0; q < V4; ++q) {
-    acc = __ffma2_rn(lo2(u[q]), lo2(v[q]), acc);
-    acc = __ffma2_rn(hi2(u[q]), hi2(v[q]), acc);
-  }
-  return acc.x + acc.y;
-}
 
 // Software-pipelined walk over one chunk.  While rating t is computed, the
 // triple of t+1 is already in registers (the next L triples are prefetched a
@@ -792,42 +752,6 @@ __global__ void block_exact_kernel(const BlockWork* __restrict__ work, int nwork
 }
 
 // ------------------------------------------------------------ dispatch
-struct Shape {
-  int L, V4;
-};
-
-Shape shape_for(int kp) {
-  // A group of L lanes owns one rating; lane gl holds float4s gl, gl+L, ...
-  // of the row (V4 of them), so one warp instruction moves a 16L-byte
-  // contiguous segment of each of 32/L rows.  L >= 4 keeps that segment at 64
-  // bytes or more (two full sectors): with k = 16 on one lane per rating the
-  // sweep ran at half the speed, k = 32 on two lanes 21% slower
-  // (scripts/k_sweep.py, B200).  Beyond that, up to 4 float4 per lane keeps
-  // several independent groups per warp and few shuffles per rating.
-  const int f4 = kp / 4;  // float4 per row
-  // rows of 3 * 2^j float4 (k = 24, 48, 96, 192, 384): 3 float4 per lane fit
-  // exactly, where the power-of-two shape would predicate a quarter of the
-  // lanes off (k = 96: SSE 4.2 ms vs 2.6 at k = 64 on C4; k = 24 on 2 lanes of
-  // 3 beats 4 lanes of 2 with one masked: 4.06 vs 4.33 ms)
-  if (f4 >= 6 && f4 % 3 == 0 && ((f4 / 3) & (f4 / 3 - 1)) == 0 && f4 / 3 <= 32)
-    return {f4 / 3, 3};
-  if (f4 <= 2) return {f4 < 1 ? 1 : f4, 1};
-  int L = 4;
-  while (L * 4 < f4 && L < 32) L <<= 1;
-  int v4 = 1;
-  while (v4 * L < f4) v4 <<= 1;
-  return {L, v4};
-}
-
-#define BGMF_SHAPES(X)                                                                    \
-  X(1, 1, false) X(2, 1, false) X(2, 3, false) X(4, 1, true) X(4, 1, false) X(4, 2, true) \
-  X(4, 2, false)                                                                          \
-  X(4, 3, false) X(4, 4, true) X(4, 4, false) X(8, 3, false) X(8, 4, true)                \
-  X(8, 4, false) X(16, 3, false) X(16, 4, true) X(16, 4, false) X(32, 3, false)           \
-  X(32, 4, true) X(32, 4, false)
-
-// kp == 4*L*V4: every lane owns a full slice of the row, no predication
-inline bool needs_mask(const Shape& sh, int kp) { return 4 * sh.L * sh.V4 != kp; }
 
 // SSE pass shape: 8 floats per lane (V4 = 2) unless the row is wider than
 // 32 lanes of that; D = ratings in flight per group.
@@ -1220,6 +1144,11 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in,
     for (int t = 0; t < nbatch; ++t) {
       const BatchRange& r = ranges[t];
       if (r.chunks == 0) continue;
+      if (use_ordered(c, plan, batch_off[t], batch_off[t + 1])) {
+        rc = run_batch_ordered(c, plan, batch_off[t], batch_off[t + 1], 0, iters, alpha, beta);
+        if (rc) return rc;
+        continue;
+      }
       const int warps = (r.chunks + gpw - 1) / gpw;
       const dim3 grid((warps + 7) / 8);
       const BlockWork* w = c->d_work + r.w0;
@@ -1328,6 +1257,11 @@ int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in, in
   for (int t = 0; t < nbatch; ++t) {
     const BatchRange& r = ranges[t];
     if (r.chunks == 0) continue;
+    if (use_ordered(c, plan, batch_off[t], batch_off[t + 1])) {
+      rc = run_batch_ordered(c, plan, batch_off[t], batch_off[t + 1], pos0, iters, alpha, beta);
+      if (rc) return rc;
+      continue;
+    }
     const int warps = (r.chunks + gpw - 1) / gpw;
     const dim3 grid((warps + 7) / 8);
     double br = 0;
@@ -1745,8 +1679,30 @@ int run_step_converge_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batc
   if (rc0) return rc0;
   BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
   const int gpw = 32 / sh.L;
+  std::vector<int64_t> conv((size_t)2 * nb);
   for (int t = 0; t < nbatch; ++t) {
     const int q0 = batch_off[t], q1 = batch_off[t + 1];
+    if (use_ordered(c, plan, q0, q1)) {
+      // the whole per-block converge loop on the device (ordered.cu)
+      const int capi = cap > INT32_MAX ? INT32_MAX : (int)cap;
+      int rc = run_batch_ordered(c, plan, q0, q1, 0, capi, (float)alpha, (float)beta, true, tol);
+      if (rc) return rc;
+      BGMF_CK(c, cudaMemcpyAsync(c->h_sse, c->d_sse, sizeof(double) * nb, cudaMemcpyDeviceToHost,
+                                 s));
+      BGMF_CK(c, cudaMemcpyAsync(conv.data(), c->d_conv, sizeof(int64_t) * 2 * nb,
+                                 cudaMemcpyDeviceToHost, s));
+      BGMF_CK(c, cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, s));
+      BGMF_CK(c, cudaStreamSynchronize(s));
+      for (int q = q0; q < q1; ++q) {
+        const int b = plan[q];
+        if (c->h_offsets[b + 1] == c->h_offsets[b]) continue;
+        sse_final[b] = c->h_sse[b];
+        iters_out[b] = conv[2 * b];
+        capped_out[b] = (int32_t)conv[2 * b + 1];
+      }
+      if (*c->h_bad != kNoBad) break;
+      continue;
+    }
     std::vector<char> active(batch_off[nbatch], 0);
     std::vector<double> prev(nb, 0.0);
     int n_active = 0;

@@ -53,6 +53,11 @@ class EngineOptions:
                V-block bytes swept at once: larger strata run as sequential
                waves of blocks whose V fits in L2 (None: library default,
                48 MiB; 0: whole strata).
+    ordered    None (default): strata whose blocks' V fits the GPU's shared
+               memory run the order-faithful slab sweep (ordered.cu: every U
+               and V row updated in the reference's stored order, fp32,
+               deterministic); True: the same, stated explicitly; False:
+               always the chunked lossless-Hogwild sweep.
     device_rating_budget
                bytes of HBM the ratings may use (None: all resident).  When
                the partition is larger, it moves to pinned host memory and
@@ -72,6 +77,7 @@ class EngineOptions:
     stream_slots: int = 3
     sse_async: bool | None = None
     l2_wave_bytes: int | None = None
+    ordered: bool | None = None
 
 
 def default_device() -> int:
@@ -98,6 +104,8 @@ class Engine:
         self._opt("bulk_red", 1.0 if self.options.bulk_red else 0.0)
         self._opt("sse_wide", 1.0 if self.options.sse_wide else 0.0)
         self._opt("sse_async", 0.0 if self.options.sse_async is False else 1.0)
+        if self.options.ordered is not None:
+            self._opt("ordered", 1.0 if self.options.ordered else 0.0)
         if self.options.l2_wave_bytes is not None:
             self._opt("l2_wave_bytes", float(self.options.l2_wave_bytes))
         f = self.options.fused

@@ -215,10 +215,9 @@ def test_sequential_fast_within_tolerance(golden, name):
     got = np.array([s.train_rmse for s in res.trace])
     ref = np.array(meta["train"])
     assert len(got) == len(ref)
-    if name.startswith("cmf_c1"):
-        assert np.max(np.abs(got - ref)) <= TOL
-    else:  # dense toy: see FAST_TOY above
-        assert np.max(np.abs(got - ref) / ref) <= 3e-3
+    # CMF is BGMF on a 1x1 grid: one block per batch, so the ordered kernel
+    # runs it (stored order, fp32) -- the flat tolerance on every fixture
+    assert np.max(np.abs(got - ref)) <= TOL
 
 
 def test_sync_parallel_divergence_reports_shard(dense64):

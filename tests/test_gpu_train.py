@@ -303,7 +303,9 @@ def test_heavy_user_runs_split_across_chunks(n, m, k):
     dense matrix) is swept by several groups at once; each red.adds its u
     deltas and re-reads the row once per triple batch (every L ratings), so the run
     sees the other groups' updates.  Without the re-read the trace drifted 5%
-    (randomised sweep, scripts/fuzz_parity.py); now within the dense-toy bound."""
+    (randomised sweep, scripts/fuzz_parity.py).  A 1x1 grid is one block per
+    batch, so the auto routing runs it through the ordered kernel (every
+    update in the reference's order): within the flat 1e-3 tolerance."""
     g = np.random.default_rng(0)
     cells = g.choice(n * m, n * m, replace=False)
     r, c = np.divmod(cells, m)
@@ -316,4 +318,4 @@ def test_heavy_user_runs_split_across_chunks(n, m, k):
                                    alpha=2e-4, schedule="const:2", early_stop=False)
     got = np.array([s.train_rmse for s in res.trace])
     want = np.array([s["train_rmse"] for s in otr])
-    assert np.all(np.abs(got - want) <= 3e-3 * want)
+    assert np.all(np.abs(got - want) <= 1e-3), np.abs(got - want).max()
