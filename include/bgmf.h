@@ -329,6 +329,13 @@ int bgmf_peer_open(bgmf_ctx* ctx, const uint8_t* handle, void** out);
 int bgmf_peer_push(bgmf_ctx* ctx, void* dst, const void* src, int64_t bytes,
                    uint32_t* peer_flag, uint32_t value);
 int bgmf_peer_wait(bgmf_ctx* ctx, const uint32_t* flag, uint32_t value);
+/* Bounded waits: a wait gives up (and records why) once *abort_word != 0 or
+ * after timeout_s; bgmf_peer_abort sets a peer's abort word (a failing rank
+ * calls it for every peer); bgmf_peer_error returns 0, 1 (a wait timed out)
+ * or 2 (a peer aborted), synchronising ctx's stream. */
+int bgmf_peer_config(bgmf_ctx* ctx, const uint32_t* abort_word, double timeout_s);
+int bgmf_peer_abort(bgmf_ctx* ctx, uint32_t* peer_abort_word);
+int bgmf_peer_error(bgmf_ctx* ctx, int* out);
 
 /* Measurement only (no reference counterpart): the SM<->L2 ceiling of the
  * sweep's access pattern on `device` -- `ratings` random 512-byte rows of an

@@ -65,6 +65,9 @@ SIGNATURES = {
     "bgmf_peer_push": (_i, [_ctx, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                             ctypes.c_void_p, ctypes.c_uint32]),
     "bgmf_peer_wait": (_i, [_ctx, ctypes.c_void_p, ctypes.c_uint32]),
+    "bgmf_peer_config": (_i, [_ctx, ctypes.c_void_p, ctypes.c_double]),
+    "bgmf_peer_abort": (_i, [_ctx, ctypes.c_void_p]),
+    "bgmf_peer_error": (_i, [_ctx, ctypes.POINTER(ctypes.c_int)]),
     "bgmf_run_sync_parallel_step": (_i, [_ctx, _i64p, _i, _d, _d, _f64p, _i64p]),
     "bgmf_run_step_converge": (_i, [_ctx, _i32p, _i32p, _i, _d, _l, _d, _d, _f64p, _i64p,
                                     _i32p, _i64p]),

@@ -86,6 +86,9 @@ struct bgmf_ctx {
   // peer transport (peer.cu): IPC-exportable buffers and mapped peer buffers
   std::vector<void*> peer_owned, peer_opened;
   unsigned int* d_push_done = nullptr;  // CTA-completion counter of peer_push_kernel
+  unsigned int* d_peer_err = nullptr;   // peer waits: 1 timed out, 2 aborted by a peer
+  const unsigned int* peer_abort = nullptr;  // this rank's abort word (its flag page)
+  unsigned long long peer_timeout_ns = 120ull * 1000000000ull;
   bool have_factors = false, bound = false;
   float* d_u = nullptr;
   float* d_v = nullptr;
@@ -110,7 +113,8 @@ struct bgmf_ctx {
   int ws_half = 0;
   cudaEvent_t ws_done[2] = {nullptr, nullptr};
   bool ws_pending[2] = {false, false};
-  std::vector<int32_t> submitted;        // block id of every step-global plan position
+  std::vector<int32_t> submitted;        // block id of every submitted plan position
+  int step_pos0 = 0;                     // submitted.size() when the current step began
   double* h_sse = nullptr;               // pinned [I*J]
   unsigned long long* h_bad = nullptr;   // pinned [1]
 
@@ -285,6 +289,8 @@ bool ordered_block_ok(bgmf_ctx* ctx, int b);
 bool use_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1);
 int run_batch_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1, int pos_base,
                       int iters, float alpha, float beta, bool conv = false, double tol = 0.0);
+int run_shards_ordered(bgmf_ctx* ctx, const int32_t* r0, const int32_t* r1, int nshards,
+                       float* vpriv, float alpha, float beta, double* sse_dev);
 
 // stream.cu -- out-of-core: ratings in pinned host memory, device slot ring
 int stream_enable(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);

@@ -45,11 +45,13 @@ struct OrdBlock {
   int64_t begin;      // first entry of the block in the partition arrays
   int64_t rp;         // offset of the block's h + 1 row pointers in d_rowptr
   int64_t row_start;  // U row of local row 0
-  int64_t col_start;  // V row of local column 0
+  int64_t col_start;  // V row (of vb) of local column 0
+  float* vb;          // V (or a private copy of it)
   int32_t h, w;       // rows / columns of the block
   int32_t stage0, nstages;
   int32_t slab_w, block_id;
-  int32_t pos, pad;
+  int32_t pos;
+  int32_t qbase;      // 1: column counters start at the unit's smallest rank
 };
 
 // Passed by value (kernel parameter space): the host never has to keep a
@@ -141,7 +143,8 @@ struct Stage {
   uint32_t* fl;         // row flags of those rows
   float* sv;            // V slab (shared memory)
   int* cnt;             // column counters of the slab (shared memory)
-  int h, w, S, st, sw, cs, ce, nc, kp;
+  int h, w, S, st, sw, cs, ce, nc, kp, qbase;
+  int e0;               // first entry of the unit (block-relative)
 };
 
 // One sweep of this stage's slab (sweep `it` of the launch).
@@ -155,9 +158,19 @@ __device__ __forceinline__ void stage_sweep(const Stage& T, int it, uint32_t gen
   const float2 nab = make_float2(-alpha * beta, -alpha * beta);
   const int kp = T.kp;
   __syncthreads();  // this stage's previous sweep / SSE is over
-  for (int i = threadIdx.x; i < T.nc; i += kOrdThreads) T.cnt[i] = 0;
+  for (int i = threadIdx.x; i < T.nc; i += kOrdThreads) T.cnt[i] = T.qbase ? INT32_MAX : 0;
   if (threadIdx.x == 0) *s_next = 0;
   __syncthreads();
+  if (T.qbase) {
+    // a row range of a block: a column's first entry here has the rank of
+    // the block's entries of that column before the range
+    const int e0 = __ldg(T.rp), e1 = __ldg(T.rp + T.h);
+    for (int i = e0 + (int)threadIdx.x; i < e1; i += kOrdThreads) {
+      const int c = __ldg(T.bcol + i);
+      if (c >= T.cs && c < T.ce) atomicMin(T.cnt + (c - T.cs), __ldg(T.bq + i));
+    }
+    __syncthreads();
+  }
   const uint32_t tag_now = ((gen + (uint32_t)it) << 8) | (uint32_t)(T.st + 1);
   while (true) {
     int r = 0;
@@ -206,7 +219,7 @@ __device__ __forceinline__ void stage_sweep(const Stage& T, int it, uint32_t gen
         const float dot = group_sum_m<L>(dot_slice<V4>(u, v), gmask);
         const float e = x - dot;
         if (!isfinite(e) && ln.gl == 0) {
-          atomicMin(bad, pack_bad(pos, it, t0 + j));
+          atomicMin(bad, pack_bad(pos, it, t0 + j - T.e0));
           *divflag = 1;
         }
         const float gg = two_a * e;
@@ -335,7 +348,7 @@ template <int L, int V4, bool kMask>
 __global__ void __launch_bounds__(kOrdThreads, 1)
 ordered_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restrict__ lcol,
                const float* __restrict__ val, const int32_t* __restrict__ qrank,
-               const int32_t* __restrict__ rowptr, float* __restrict__ U, float* __restrict__ V,
+               const int32_t* __restrict__ rowptr, float* __restrict__ U,
                int kp, float alpha, float beta, int iters, uint32_t gen,
                uint32_t* __restrict__ rflag, uint32_t* __restrict__ bar,
                double* __restrict__ part, double* __restrict__ sse,
@@ -378,7 +391,9 @@ ordered_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restrict__ 
   T.cnt = reinterpret_cast<int*>(T.sv + (size_t)T.sw * kp);
   uint32_t* ctr = bar + 3 * bi;      // barrier counter, arrivals at the end, divergence
   const unsigned bytes = (unsigned)T.nc * (unsigned)kp * 4u;
-  float* gv = V + (B.col_start + T.cs) * kp;
+  float* gv = B.vb + (B.col_start + T.cs) * kp;
+  T.qbase = B.qbase;
+  T.e0 = __ldg(T.rp);
   const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
   const unsigned sva = (unsigned)__cvta_generic_to_shared(T.sv);
 
@@ -405,7 +420,7 @@ ordered_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restrict__ 
   uint32_t nbar = 0;
   int swept = 0;
   double sse_now = 0.0;
-  const double cntd = (double)(__ldg(T.rp + T.h));  // entries of the block
+  const double cntd = (double)(__ldg(T.rp + T.h) - __ldg(T.rp));  // entries of the unit
   if (!conv) {
     for (int it = 0; it < iters; ++it)
       stage_sweep<L, V4, kMask>(T, it, gen, alpha, beta, B.pos, &s_next, bad, &s_div);
@@ -678,64 +693,59 @@ bool ordered_block_ok(bgmf_ctx* c, int b) {
 // sweeps and the post-sweep SSE of every block in plan[q0 .. q1) (plan
 // positions pos_base + q), as few cooperative launches as co-residency
 // allows.  The caller has checked ordered_block_ok for every block.
-int run_batch_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, int pos_base,
-                      int iters, float alpha, float beta, bool conv, double tol) {
-  int rc = ensure_order_index(c);
-  if (rc) return rc;
+namespace {
+
+// One unit of the ordered kernel: a block of the partition (or a CPMF row
+// shard of the 1 x 1 block with its private V copy).
+struct OrdItem {
+  OrdBlock ob;
+  int64_t cnt;
+  size_t smem;
+};
+
+// Stage count of an item with w columns and cnt ratings, `items` units in
+// the launch: enough slabs for one to fit a CTA; more while the batch leaves
+// SMs idle, at ~ord_stage_ratings ratings per stage (a row then visits more
+// slabs: each visit moves u_r through L2).
+void plan_stages(bgmf_ctx* c, OrdItem& it, int items) {
+  const int64_t per = (int64_t)(smem_budget(c) / ((size_t)c->kp * 4 + 4));
+  const int64_t w = it.ob.w;
+  const int64_t smin = (w + per - 1) / per;
+  int64_t S = (it.cnt + c->ord_stage_ratings - 1) / c->ord_stage_ratings;
+  const int64_t fill = c->num_sms / (items > 0 ? items : 1);
+  if (S > fill) S = fill;
+  if (S < smin) S = smin;
+  if (S > w) S = w;
+  if (S > kOrdMaxStages) S = kOrdMaxStages;
+  if (S < 1) S = 1;
+  const int64_t swd = (w + S - 1) / S;
+  it.ob.nstages = (int32_t)((w + swd - 1) / swd);  // no empty slab
+  it.ob.slab_w = (int32_t)swd;
+  it.smem = slab_smem((int)swd, c->kp);
+}
+
+// Launch the items: as few cooperative launches as co-residency allows.
+int launch_items(bgmf_ctx* c, std::vector<OrdItem>& items, int iters, float alpha, float beta,
+                 bool conv, double tol, double* sse_dev) {
   cudaStream_t s = c->stream;
   const void* fn = ordered_kernel_ptr(c->kp, c->ord_warp);
   const size_t budget = smem_budget(c);
-  const int64_t per = (int64_t)(budget / ((size_t)c->kp * 4 + 4));
-  struct Item { int b, pos, S, sw; size_t smem; };
-  std::vector<Item> items;
-  int nonempty = 0;
-  for (int q = q0; q < q1; ++q)
-    nonempty += c->h_offsets[plan[q] + 1] > c->h_offsets[plan[q]];
-  for (int q = q0; q < q1; ++q) {
-    const int b = plan[q];
-    const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
-    if (cnt == 0) continue;  // its SSE stays 0
-    const int64_t w = c->col_bounds[b % c->J + 1] - c->col_bounds[b % c->J];
-    const int64_t smin = (w + per - 1) / per;
-    // stages: enough for the slab to fit; more while the stratum leaves SMs
-    // idle, at ~ord_stage_ratings ratings per stage (a row then visits more
-    // slabs: each visit moves u_r through L2)
-    int64_t S = (cnt + c->ord_stage_ratings - 1) / c->ord_stage_ratings;
-    const int64_t fill = c->num_sms / (nonempty > 0 ? nonempty : 1);
-    if (S > fill) S = fill;
-    if (S < smin) S = smin;
-    if (S > w) S = w;
-    if (S > kOrdMaxStages) S = kOrdMaxStages;
-    if (S < 1) S = 1;
-    const int64_t swd = (w + S - 1) / S;
-    S = (w + swd - 1) / swd;  // no empty slab
-    items.push_back({b, pos_base + q, (int)S, (int)swd, slab_smem((int)swd, c->kp)});
-  }
   size_t i = 0;
   while (i < items.size()) {
-    // pack blocks into one launch while every stage stays co-resident
+    // pack units into one launch while every stage stays co-resident
     OrdLaunch L{};
     size_t smem = 0;
     int ctas = 0;
     size_t j = i;
+    double ratings = 0;
     while (j < items.size() && L.nblocks < kOrdMaxBlocks) {
       const size_t sm2 = std::max(smem, items[j].smem);
-      if (ctas + items[j].S > ordered_capacity(c, sm2) && L.nblocks > 0) break;
-      const int b = items[j].b;
+      if (ctas + items[j].ob.nstages > ordered_capacity(c, sm2) && L.nblocks > 0) break;
       OrdBlock& ob = L.b[L.nblocks++];
-      const int bi = b / c->J, bj = b % c->J;
-      ob.begin = c->h_offsets[b];
-      ob.rp = c->h_rp[b];
-      ob.row_start = c->row_bounds[bi];
-      ob.col_start = c->col_bounds[bj];
-      ob.h = (int32_t)(c->row_bounds[bi + 1] - c->row_bounds[bi]);
-      ob.w = (int32_t)(c->col_bounds[bj + 1] - c->col_bounds[bj]);
+      ob = items[j].ob;
       ob.stage0 = ctas;
-      ob.nstages = items[j].S;
-      ob.slab_w = items[j].sw;
-      ob.block_id = b;
-      ob.pos = items[j].pos;
-      ctas += items[j].S;
+      ctas += ob.nstages;
+      ratings += (double)items[j].cnt;
       smem = sm2;
       ++j;
     }
@@ -747,24 +757,20 @@ int run_batch_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, int pos_
     }
     uint32_t gen = c->ord_gen;
     c->ord_gen += (uint32_t)(iters > 0 ? iters : 1);  // converge: iters = the cap
-    double ratings = 0;
-    for (size_t t = i; t < j; ++t)
-      ratings += (double)(c->h_offsets[items[t].b + 1] - c->h_offsets[items[t].b]);
     const int32_t* lcol = c->d_lcol;
     const float* val = c->d_val;
     const int32_t* qr = c->d_qrank;
     const int32_t* rpp = c->d_rowptr;
     float* U = c->d_u;
-    float* V = c->d_v;
     int kp = c->kp, its = iters;
     uint32_t* rfl = c->d_rflag;
     uint32_t* bar = c->d_obar;
     double* part = c->d_opart;
-    double* sse = c->d_sse;
+    double* sse = sse_dev;
     unsigned long long* bad = c->d_bad;
     int cv = conv ? 1 : 0;
     int64_t* cout = c->d_conv;
-    void* args[] = {&L, &lcol, &val, &qr, &rpp, &U, &V, &kp, &alpha, &beta, &its, &gen,
+    void* args[] = {&L, &lcol, &val, &qr, &rpp, &U, &kp, &alpha, &beta, &its, &gen,
                     &rfl, &bar, &part, &sse, &bad, &cv, &tol, &cout};
     TimedLaunch* slot = nullptr;
     if (c->timing) record_begin(c, 0, ratings * iters * (12.0 + 16.0 * c->k), &slot);
@@ -775,6 +781,68 @@ int run_batch_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, int pos_
     i = j;
   }
   return BGMF_OK;
+}
+
+}  // namespace
+
+// One batch (stratum, or part of one) through the ordered kernel: `iters`
+// sweeps (or, conv, the converge loop capped at iters) and the post-sweep
+// SSE of every block in plan[q0 .. q1) (plan positions pos_base + q).  The
+// caller has checked use_ordered.
+int run_batch_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, int pos_base,
+                      int iters, float alpha, float beta, bool conv, double tol) {
+  int rc = ensure_order_index(c);
+  if (rc) return rc;
+  std::vector<OrdItem> items;
+  for (int q = q0; q < q1; ++q) {
+    const int b = plan[q];
+    const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
+    if (cnt == 0) continue;  // its SSE stays 0
+    const int bi = b / c->J, bj = b % c->J;
+    OrdItem it{};
+    it.cnt = cnt;
+    it.ob.begin = c->h_offsets[b];
+    it.ob.rp = c->h_rp[b];
+    it.ob.row_start = c->row_bounds[bi];
+    it.ob.col_start = c->col_bounds[bj];
+    it.ob.vb = c->d_v;
+    it.ob.h = (int32_t)(c->row_bounds[bi + 1] - c->row_bounds[bi]);
+    it.ob.w = (int32_t)(c->col_bounds[bj + 1] - c->col_bounds[bj]);
+    it.ob.block_id = b;
+    it.ob.pos = pos_base + q;
+    it.ob.qbase = 0;
+    items.push_back(it);
+  }
+  for (auto& it : items) plan_stages(c, it, (int)items.size());
+  return launch_items(c, items, iters, alpha, beta, conv, tol, c->d_sse);
+}
+
+// CPMF shards (baselines.py:100-182) through the ordered kernel: shard w =
+// rows [r0[w], r1[w]) of the 1 x 1 partition, swept in stored order on the
+// shared U and its private V copy vpriv + w * m * kp; SSE to sse_dev[w].
+int run_shards_ordered(bgmf_ctx* c, const int32_t* r0, const int32_t* r1, int nshards,
+                       float* vpriv, float alpha, float beta, double* sse_dev) {
+  int rc = ensure_order_index(c);
+  if (rc) return rc;
+  std::vector<OrdItem> items;
+  for (int w = 0; w < nshards; ++w) {
+    if (r1[w] <= r0[w]) continue;
+    OrdItem it{};
+    it.cnt = 1;  // (not needed beyond timing)
+    it.ob.begin = 0;
+    it.ob.rp = c->h_rp[0] + r0[w];
+    it.ob.row_start = r0[w];
+    it.ob.col_start = 0;
+    it.ob.vb = vpriv ? vpriv + (size_t)w * c->m * c->kp : c->d_v;
+    it.ob.h = r1[w] - r0[w];
+    it.ob.w = (int32_t)c->m;
+    it.ob.block_id = w;
+    it.ob.pos = w;
+    it.ob.qbase = 1;  // column ranks count the earlier shards' entries too
+    items.push_back(it);
+  }
+  for (auto& it : items) plan_stages(c, it, (int)items.size());
+  return launch_items(c, items, 1, alpha, beta, false, 0.0, sse_dev);
 }
 
 // Ordered routing of one batch: mode 1 = every block the kernel can take;

@@ -53,12 +53,28 @@ peer_push_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int64
   }
 }
 
-__global__ void peer_wait_kernel(const unsigned int* flag, unsigned int value) {
+// The receiver's wait is bounded: it gives up when the sender's rank has
+// raised the ring's abort word (any rank that fails sets it in every peer's
+// flag page, bgmf_peer_abort) or after `timeout_ns` of %globaltimer, and then
+// records the reason in `err` (1: timeout, 2: abort) for bgmf_peer_error --
+// a dead peer can never hang the surviving ranks' streams.
+__global__ void peer_wait_kernel(const unsigned int* flag, unsigned int value,
+                                 const unsigned int* abort_word, unsigned int* err,
+                                 unsigned long long timeout_ns) {
   if (threadIdx.x != 0) return;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   unsigned int v;
   for (;;) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
     if ((int)(v - value) >= 0) break;  // wrap-safe >=
+    if (abort_word) {
+      unsigned int a;
+      asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(a) : "l"(abort_word) : "memory");
+      if (a) { atomicMax(err, 2u); break; }
+    }
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) { atomicMax(err, 1u); break; }
     __nanosleep(256);
   }
 }
@@ -133,8 +149,42 @@ extern "C" int bgmf_peer_push(bgmf_ctx* c, void* dst, const void* src, int64_t b
 extern "C" int bgmf_peer_wait(bgmf_ctx* c, const uint32_t* flag, uint32_t value) {
   if (!c || !flag) return fail(c, BGMF_ERR_ARG, "bgmf_peer_wait: bad argument");
   cudaSetDevice(c->device);
-  peer_wait_kernel<<<1, 32, 0, c->stream>>>(flag, value);
+  if (!c->d_peer_err) {
+    BGMF_CK(c, cudaMalloc(&c->d_peer_err, sizeof(unsigned int)));
+    BGMF_CK(c, cudaMemsetAsync(c->d_peer_err, 0, sizeof(unsigned int), c->stream));
+  }
+  peer_wait_kernel<<<1, 32, 0, c->stream>>>(flag, value, c->peer_abort, c->d_peer_err,
+                                            c->peer_timeout_ns);
   BGMF_CK(c, cudaGetLastError());
+  return BGMF_OK;
+}
+
+extern "C" int bgmf_peer_config(bgmf_ctx* c, const uint32_t* abort_word, double timeout_s) {
+  if (!c || timeout_s <= 0) return fail(c, BGMF_ERR_ARG, "bgmf_peer_config: bad argument");
+  c->peer_abort = reinterpret_cast<const unsigned int*>(abort_word);
+  c->peer_timeout_ns = (unsigned long long)(timeout_s * 1e9);
+  return BGMF_OK;
+}
+
+extern "C" int bgmf_peer_abort(bgmf_ctx* c, uint32_t* peer_abort_word) {
+  if (!c || !peer_abort_word) return fail(c, BGMF_ERR_ARG, "bgmf_peer_abort: bad argument");
+  cudaSetDevice(c->device);
+  const uint32_t one = 1;
+  // a plain copy into the peer's mapped page: no dependence on this rank's
+  // (possibly failed) stream
+  BGMF_CK(c, cudaMemcpy(peer_abort_word, &one, sizeof(one), cudaMemcpyHostToDevice));
+  return BGMF_OK;
+}
+
+extern "C" int bgmf_peer_error(bgmf_ctx* c, int* out) {
+  if (!c || !out) return fail(c, BGMF_ERR_ARG, "bgmf_peer_error: bad argument");
+  cudaSetDevice(c->device);
+  *out = 0;
+  if (!c->d_peer_err) return BGMF_OK;
+  unsigned int e = 0;
+  BGMF_CK(c, cudaMemcpyAsync(&e, c->d_peer_err, sizeof(e), cudaMemcpyDeviceToHost, c->stream));
+  BGMF_CK(c, cudaStreamSynchronize(c->stream));
+  *out = (int)e;
   return BGMF_OK;
 }
 
@@ -142,6 +192,9 @@ namespace bgmf {
 void peer_release(bgmf_ctx* c) {
   if (c->d_push_done) cudaFree(c->d_push_done);
   c->d_push_done = nullptr;
+  if (c->d_peer_err) cudaFree(c->d_peer_err);
+  c->d_peer_err = nullptr;
+  c->peer_abort = nullptr;
   for (void* p : c->peer_opened) cudaIpcCloseMemHandle(p);
   c->peer_opened.clear();
   for (void* p : c->peer_owned) cudaFree(p);

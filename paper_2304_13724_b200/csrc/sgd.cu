@@ -1208,6 +1208,7 @@ int step_begin(bgmf_ctx* c, int max_blocks) {
   c->w_cursor = h * half;
   c->w_limit = h * half + half;
   c->submitted.clear();
+  c->step_pos0 = 0;
   return BGMF_OK;
 }
 
@@ -1240,7 +1241,9 @@ int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in, in
   const Shape sh = shape_for(c->kp);
   const int gpw = 32 / sh.L;
   std::vector<BatchRange> ranges, sranges;
-  const int pos0 = (int)c->submitted.size();
+  // plan positions count from the start of the step (run_steps queues many
+  // steps; pack_bad keeps 16 bits of position, and a step has <= 65535 blocks)
+  const int pos0 = (int)c->submitted.size() - c->step_pos0;
   int rc = build_work(c, plan, batch_off, nbatch, sweep_groups(c, sh), ranges, nullptr,
                       c->w_cursor, pos0);
   if (rc) return rc;
@@ -1337,22 +1340,24 @@ int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs
   c->w_cursor = 0;
   c->w_limit = (int)c->work_cap;
   c->submitted.clear();
-  std::vector<int64_t> pos_end(nsteps);
+  std::vector<int64_t> pos_start(nsteps);
   plan_pos = off_pos = 0;
   if (!ev.empty()) cudaEventRecord(ev[0], s);
   for (int k = 0; k < nsteps && !rc; ++k) {
     c->d_sse = d_sse + (size_t)k * nb;  // the stratum kernels address these through c
     c->d_bad = d_bad + k;
     const int32_t* off = offs + off_pos;
+    pos_start[k] = (int64_t)c->submitted.size();
+    c->step_pos0 = (int)pos_start[k];
     rc = step_batch(c, plans + plan_pos, off, nbatch[k], iters[k], alpha, beta);
     if (!ev.empty()) cudaEventRecord(ev[k + 1], s);
-    pos_end[k] = (int64_t)c->submitted.size();
     plan_pos += off[nbatch[k]];
     off_pos += nbatch[k] + 1;
   }
   c->d_sse = keep_sse;
   c->d_bad = keep_bad;
   c->in_step = false;
+  c->step_pos0 = 0;
   if (rc) { cudaStreamSynchronize(s); cleanup(); return rc; }
   std::vector<unsigned long long> hb((size_t)nsteps);
   e = cudaMemcpyAsync(sse_out, d_sse, sizeof(double) * (size_t)nb * nsteps, cudaMemcpyDeviceToHost, s);
@@ -1365,7 +1370,7 @@ int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs
   bad_out[0] = bad_out[1] = bad_out[2] = bad_out[3] = -1;
   for (int k = 0; k < nsteps; ++k) {
     if (hb[k] == kNoBad) continue;
-    const int64_t pos = (int64_t)(hb[k] >> 48);
+    const int64_t pos = pos_start[k] + (int64_t)(hb[k] >> 48);
     bad_out[0] = k;
     bad_out[1] = pos < (int64_t)c->submitted.size() ? c->submitted[pos] : -1;
     bad_out[2] = (int64_t)(hb[k] & 0xFFFFFFFFull);
@@ -1558,6 +1563,47 @@ int run_sync_parallel_step(bgmf_ctx* c, const int64_t* edges, int nshards, doubl
         bad_out[1] = (int64_t)out[8 * w + 4];
         bad_out[2] = (int64_t)out[8 * w + 5];
       }
+    }
+    return BGMF_OK;
+  }
+  if (c->ord_mode != 0 && ordered_block_ok(c, 0)) {
+    // fast mode, ordered: each shard's rows in the reference's stored order
+    // (ordered.cu), so the only difference from the reference is fp32
+    std::vector<int32_t> lr(2 * (size_t)nshards, 0), r0(nshards), r1(nshards);
+    for (int w = 0; w < nshards; ++w) {
+      if (edges[w + 1] == edges[w]) continue;
+      BGMF_CK(c, cudaMemcpyAsync(&lr[2 * w], c->d_lrow + edges[w], 4, cudaMemcpyDeviceToHost, s));
+      BGMF_CK(c, cudaMemcpyAsync(&lr[2 * w + 1], c->d_lrow + edges[w + 1] - 1, 4,
+                                 cudaMemcpyDeviceToHost, s));
+    }
+    BGMF_CK(c, cudaStreamSynchronize(s));
+    for (int w = 0; w < nshards; ++w) {
+      r0[w] = lr[2 * w];
+      r1[w] = edges[w + 1] > edges[w] ? lr[2 * w + 1] + 1 : r0[w];
+    }
+    double* sse_dev = reinterpret_cast<double*>(c->d_work + c->work_cap);
+    BGMF_CK(c, cudaMemsetAsync(sse_dev, 0, sizeof(double) * nshards, s));
+    BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+    float* P = reinterpret_cast<float*>(c->d_priv);
+    if (priv) broadcast_v<float><<<grid, 256, 0, s>>>(c->d_v, P, elems, nshards);
+    rc = run_shards_ordered(c, r0.data(), r1.data(), nshards, priv ? P : nullptr, (float)alpha,
+                            (float)beta, sse_dev);
+    if (rc) return rc;
+    if (priv) merge_private_v<float><<<grid, 256, 0, s>>>(c->d_v, P, elems, nshards);
+    BGMF_CK(c, cudaGetLastError());
+    std::vector<double> out((size_t)nshards);
+    BGMF_CK(c, cudaMemcpyAsync(out.data(), sse_dev, sizeof(double) * nshards,
+                               cudaMemcpyDeviceToHost, s));
+    BGMF_CK(c, cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, s));
+    BGMF_CK(c, cudaStreamSynchronize(s));
+    if (c->timing) harvest_timing(c);
+    for (int w = 0; w < nshards; ++w) sse_out[w] = out[w];
+    const unsigned long long b = *c->h_bad;
+    bad_out[0] = bad_out[1] = bad_out[2] = -1;
+    if (b != kNoBad) {  // pos = shard
+      bad_out[0] = (int64_t)(b >> 48);
+      bad_out[1] = (int64_t)(b & 0xFFFFFFFFull);
+      bad_out[2] = (int64_t)((b >> 32) & 0xFFFF);
     }
     return BGMF_OK;
   }

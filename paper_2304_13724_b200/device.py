@@ -18,7 +18,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -30,7 +30,9 @@ class EngineOptions:
     """B200 knobs.  None of them changes the reference's semantics.
 
     exact      fp64 sequential-per-block kernels, bit-identical to the
-               reference (slow; parity/verification mode).
+               reference (slow; parity/verification mode).  Default: False,
+               or True when $BGMF_EXACT=1 (runs a reference test suite
+               unchanged in exact mode, ref_suite/run.py).
     min_chunk  minimum ratings per worker group (bounds concurrency on tiny
                blocks, which keeps the lossless-Hogwild drift far below 1e-3).
     device     CUDA ordinal; default $BGMF_DEVICE, else $LOCAL_RANK, else 0.
@@ -65,7 +67,7 @@ class EngineOptions:
                (out-of-core mode, 12 B per rating per slot entry).
     """
 
-    exact: bool = False
+    exact: bool = field(default_factory=lambda: os.environ.get("BGMF_EXACT") == "1")
     min_chunk: int = 256
     device: int | None = None
     timing: bool = False
@@ -339,6 +341,19 @@ class Engine:
 
     def peer_wait(self, flag: int, value: int):
         self._check(self._L.bgmf_peer_wait(self._h, ctypes.c_void_p(flag), value & 0xFFFFFFFF))
+
+    def peer_config(self, abort_word: int, timeout_s: float):
+        self._check(self._L.bgmf_peer_config(self._h, ctypes.c_void_p(abort_word),
+                                             float(timeout_s)))
+
+    def peer_abort(self, peer_abort_word: int):
+        self._check(self._L.bgmf_peer_abort(self._h, ctypes.c_void_p(peer_abort_word)))
+
+    def peer_error(self) -> int:
+        """0, 1 (a peer wait timed out) or 2 (a peer aborted the ring)."""
+        out = ctypes.c_int(0)
+        self._check(self._L.bgmf_peer_error(self._h, ctypes.byref(out)))
+        return int(out.value)
 
     def run_sync_parallel_step(self, edges: np.ndarray, alpha: float, beta: float):
         """CPMF step on a 1x1 partition; returns (per-shard SSE, bad) where

@@ -277,7 +277,11 @@ class _PeerLinks:
         self.eng, self.vptr, self.kp, self.cb = eng, vptr, kp, col_bounds
         world, rank = dist.get_world_size(), dist.get_rank()
         self.rank = rank
-        self.flags = eng.peer_alloc(4 * world)  # flags[s]: moves s -> me done
+        # flags[s]: moves s -> me done; flags[world]: the ring's abort word
+        self.flags = eng.peer_alloc(4 * (world + 1))
+        self.world = world
+        eng.peer_config(self.flags + 4 * world,
+                        float(os.environ.get("BGMF_PEER_TIMEOUT_S", "120")))
         mine = (eng.peer_handle(vptr), eng.peer_handle(self.flags))
         allh = [None] * world
         dist.all_gather_object(allh, mine)
@@ -289,6 +293,21 @@ class _PeerLinks:
         self.sent = [0] * world
         self.got = [0] * world
         dist.barrier()  # every rank's flags are zero and mapped before any move
+
+    def abort(self) -> None:
+        """This rank is failing: release every peer's waits on it."""
+        for r, f in self.peer_flags.items():
+            try:
+                self.eng.peer_abort(f + 4 * self.world)
+            except Exception:  # noqa: BLE001  best effort on the error path
+                pass
+
+    def check(self) -> None:
+        """Raise if a wait of this rank gave up (peer dead or aborted)."""
+        e = self.eng.peer_error()
+        if e:
+            raise RuntimeError("ring V move: " + ("a peer rank stopped responding (wait timed "
+                               "out)" if e == 1 else "a peer rank aborted the ring"))
 
     def move(self, moves) -> None:
         """One batch's moves: all pushes first, then the waits (a wait blocks
@@ -306,15 +325,36 @@ class _PeerLinks:
                 self.eng.peer_wait(self.flags + 4 * mv.src, self.got[mv.src])
 
 
-def _transport(world: int) -> str:
+def _transport(world: int, device: int | None = None, dist=None) -> str:
     """V-move transport of the ring: "peer" (IPC-mapped peer memory,
-    csrc/peer.cu; the default when every rank is on this node) or "dist"
-    (torch.distributed P2P: multi-node jobs); BGMF_RING_TRANSPORT overrides."""
+    csrc/peer.cu) when every rank is on this node and every rank's GPU can
+    reach every other's; else "dist" (torch.distributed P2P).
+    BGMF_RING_TRANSPORT overrides.  Launchers that do not say how many ranks
+    share the node (no LOCAL_WORLD_SIZE: mpirun, custom launchers) get "dist"."""
     if world <= 1:
         return "dist"  # nothing moves
-    single_node = int(os.environ.get("LOCAL_WORLD_SIZE", world)) == world
-    t = os.environ.get("BGMF_RING_TRANSPORT", "peer" if single_node else "dist")
+    lws = os.environ.get("LOCAL_WORLD_SIZE")
+    single_node = lws is not None and int(lws) == world
+    t = os.environ.get("BGMF_RING_TRANSPORT")
+    if t is None:
+        t = "peer" if single_node and _peers_reachable(world, device, dist) else "dist"
     return "dist" if t in ("dist", "nccl") else t
+
+
+def _peers_reachable(world: int, device, dist) -> bool:
+    """Collective: can every rank's GPU map every other rank's memory (CUDA
+    IPC + P2P)?  Ranks sharing one device are fine."""
+    if device is None or dist is None:
+        return True
+    import torch
+
+    devs = [None] * world
+    dist.all_gather_object(devs, int(device))
+    ok = all(o == device or torch.cuda.can_device_access_peer(device, o) for o in devs)
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int64,
+                        device=f"cuda:{device}" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    return bool(int(flag.item()))
 
 
 def _move_v(moves, rank: int, shard, dist) -> None:
@@ -444,137 +484,157 @@ def _train_ring(d, cfg, test, early_stop, options, timing, dist, rank, world, de
     """train_blocked_distributed's body, on the rank's training stream."""
     import torch
 
-    from .core import ConvergenceTrace, FactorModel, TraceStep
+    from .core import ConvergenceTrace, DivergenceError, FactorModel, TraceStep
     from .kernel import divergence
     from .metrics import HoldoutEvaluator, RmseAccumulator, finalize, merge
     from .trainer import _Phases, resolve_inner_iters
 
     prof = _Phases() if os.environ.get("BGMF_PROFILE") and rank == 0 else None
     sched = RingSchedule(cfg.grid_i, cfg.grid_j, world)
-    shard = GpuShard(d, cfg, sched, rank, device, options, _transport(world), dist)
-    if prof:
-        torch.cuda.synchronize()
-        prof.mark("shard: partition + U/V buffers")
-    shard.eng.init_factors(d.n, d.m, cfg.k, cfg.seed)
-    if prof:
-        torch.cuda.synchronize()
-        prof.mark("init_factors")
-    shard.eng.prefault_factors()  # the model's host pages fault in while the epochs run
-    evaluator = HoldoutEvaluator(d, test) if test is not None and len(test) > 0 else None
-    if evaluator is not None:
-        t = evaluator.test
-        mine = shard_rows(t.rows, shard.grid.row_bounds, sched, rank)
-        shard.eng.holdout_set(t.rows[mine], t.cols[mine], t.values[mine], evaluator.cold[mine],
-                              evaluator.fallback)
-    nb = cfg.grid_i * cfg.grid_j
-    trace = ConvergenceTrace()
-    stop = "max_steps"
-    total_counts = np.zeros(nb, np.int64)
-    cnt = torch.tensor(shard.counts, dtype=torch.int64, device=f"cuda:{device}")
-    _all_reduce(dist, cnt)
-    total_counts[:] = cnt.cpu().numpy()
-    from .core import AdaptiveDecreasing
-
-    adaptive = isinstance(cfg.inner_schedule, AdaptiveDecreasing)
-    hist = [0.0]
-    if adaptive and int(total_counts.sum()):
-        # RMSE of the initial factors over all ranks' ratings (trainer.py:98-100)
-        s0 = torch.tensor([shard.eng.train_sse()], dtype=torch.float64, device=f"cuda:{device}")
-        _all_reduce(dist, s0)
-        hist = [math.sqrt(float(s0.item()) / int(total_counts.sum()))]
-    from .core import ConvergeEachBlock
-
-    batched = (not early_stop and evaluator is None and not adaptive
-               and not isinstance(cfg.inner_schedule, ConvergeEachBlock) and cfg.outer_steps > 1)
-    pre = (_run_epochs_batched(sched, shard, rank, dist, cfg, nb, device, timing)
-           if batched else None)
-    for step in range(1, cfg.outer_steps + 1):
-        if adaptive and step >= 2:
-            prev, cur = hist[-2], hist[-1]
-            ratio = (prev - cur) / prev if prev > 0 else 0.0
-        else:
-            ratio = 1.0
-        g = resolve_inner_iters(cfg.inner_schedule, step, ratio)
-        t0 = time.perf_counter()
-        max_iters, capped = g, 0
-        if pre is not None:  # already run: this step's results
-            sse_all, order, bad_any, any_bad, g, secs = pre[step - 1]
-            max_iters = g
-        elif g is None:  # converge-each-block: per-block sweep counts, synchronous batches
-            sse_all, order, bad_any, its, cap = _run_epoch_converge(
-                sched, shard, rank, dist, step - 1, cfg.inner_schedule.tol, cfg.alpha, cfg.beta,
-                nb, cfg.grid_j)
-            agg = torch.tensor([float(its.max()) if len(its) else 0.0, float(cap)],
-                               dtype=torch.float64, device=f"cuda:{device}")
-            mx = agg[:1].clone()
-            _all_reduce(dist, mx, dist.ReduceOp.MAX)
-            sm = agg[1:].clone()
-            _all_reduce(dist, sm)
-            max_iters, capped = int(mx.item()), int(sm.item())
-        else:
-            sse_all, order, bad_any = run_epoch(sched, shard, rank, dist, step - 1, g, cfg.alpha,
-                                                cfg.beta, nb, cfg.grid_j)
-        if pre is None:
-            red = torch.tensor(sse_all, device=f"cuda:{device}")
-            _all_reduce(dist, red)
-            sse_all = red.cpu().numpy()
-            flag = torch.tensor([0 if bad_any is None else 1], device=f"cuda:{device}")
-            _all_reduce(dist, flag)
-            any_bad = bool(int(flag.item()))
-        if any_bad or not np.all(np.isfinite(sse_all[order])):
-            b = bad_any[0] if bad_any else int(next(o for o in order
-                                                    if not math.isfinite(sse_all[o])))
-            err = divergence(b // cfg.grid_j, b % cfg.grid_j,
-                             bad_any[1] if bad_any else int(total_counts[b]) - 1,
-                             bad_any[2] if bad_any else (g or 1) - 1)
-            err.step = step
-            err.partial_trace = trace
-            raise err
-        acc = RmseAccumulator()
-        for b in order:
-            acc = merge(acc, RmseAccumulator(float(sse_all[b]), int(total_counts[b])))
-        train_rmse = finalize(acc)
-        test_rmse = None
+    shard = GpuShard(d, cfg, sched, rank, device, options, _transport(world, device, dist), dist)
+    closed = False
+    try:
+        if prof:
+            torch.cuda.synchronize()
+            prof.mark("shard: partition + U/V buffers")
+        shard.eng.init_factors(d.n, d.m, cfg.k, cfg.seed)
+        if prof:
+            torch.cuda.synchronize()
+            prof.mark("init_factors")
+        shard.eng.prefault_factors()  # the model's host pages fault in while the epochs run
+        evaluator = HoldoutEvaluator(d, test) if test is not None and len(test) > 0 else None
         if evaluator is not None:
-            sync_all_v(sched, rank, shard.v_slice, dist)  # every rank needs all of V
-            hs = torch.tensor([shard.eng.holdout_sse()], dtype=torch.float64,
-                              device=f"cuda:{device}")
-            _all_reduce(dist, hs)
-            test_rmse = math.sqrt(float(hs.item()) / len(evaluator.test))
-        seconds = (secs if pre is not None else time.perf_counter() - t0) if timing else 0.0
-        trace.append(TraceStep(step, train_rmse, test_rmse, seconds, max_iters, capped))
-        hist.append(train_rmse)
-        if early_stop:
-            if acc.count == 0:
-                stop = "converged"
-                break
-            if len(trace) >= 2 and trace.steps[-2].train_rmse - train_rmse < cfg.delta:
-                stop = "converged"
-                break
-    if prof:
+            t = evaluator.test
+            mine = shard_rows(t.rows, shard.grid.row_bounds, sched, rank)
+            shard.eng.holdout_set(t.rows[mine], t.cols[mine], t.values[mine], evaluator.cold[mine],
+                                  evaluator.fallback)
+        nb = cfg.grid_i * cfg.grid_j
+        trace = ConvergenceTrace()
+        stop = "max_steps"
+        total_counts = np.zeros(nb, np.int64)
+        cnt = torch.tensor(shard.counts, dtype=torch.int64, device=f"cuda:{device}")
+        _all_reduce(dist, cnt)
+        total_counts[:] = cnt.cpu().numpy()
+        from .core import AdaptiveDecreasing
+
+        adaptive = isinstance(cfg.inner_schedule, AdaptiveDecreasing)
+        hist = [0.0]
+        if adaptive and int(total_counts.sum()):
+            # RMSE of the initial factors over all ranks' ratings (trainer.py:98-100)
+            s0 = torch.tensor([shard.eng.train_sse()], dtype=torch.float64, device=f"cuda:{device}")
+            _all_reduce(dist, s0)
+            hist = [math.sqrt(float(s0.item()) / int(total_counts.sum()))]
+        from .core import ConvergeEachBlock
+
+        batched = (not early_stop and evaluator is None and not adaptive
+                   and not isinstance(cfg.inner_schedule, ConvergeEachBlock) and cfg.outer_steps > 1)
+        pre = (_run_epochs_batched(sched, shard, rank, dist, cfg, nb, device, timing)
+               if batched else None)
+        for step in range(1, cfg.outer_steps + 1):
+            if adaptive and step >= 2:
+                prev, cur = hist[-2], hist[-1]
+                ratio = (prev - cur) / prev if prev > 0 else 0.0
+            else:
+                ratio = 1.0
+            g = resolve_inner_iters(cfg.inner_schedule, step, ratio)
+            t0 = time.perf_counter()
+            max_iters, capped = g, 0
+            if pre is not None:  # already run: this step's results
+                sse_all, order, bad_any, any_bad, g, secs = pre[step - 1]
+                max_iters = g
+            elif g is None:  # converge-each-block: per-block sweep counts, synchronous batches
+                sse_all, order, bad_any, its, cap = _run_epoch_converge(
+                    sched, shard, rank, dist, step - 1, cfg.inner_schedule.tol, cfg.alpha, cfg.beta,
+                    nb, cfg.grid_j)
+                agg = torch.tensor([float(its.max()) if len(its) else 0.0, float(cap)],
+                                   dtype=torch.float64, device=f"cuda:{device}")
+                mx = agg[:1].clone()
+                _all_reduce(dist, mx, dist.ReduceOp.MAX)
+                sm = agg[1:].clone()
+                _all_reduce(dist, sm)
+                max_iters, capped = int(mx.item()), int(sm.item())
+            else:
+                sse_all, order, bad_any = run_epoch(sched, shard, rank, dist, step - 1, g, cfg.alpha,
+                                                    cfg.beta, nb, cfg.grid_j)
+            if pre is None:
+                red = torch.tensor(sse_all, device=f"cuda:{device}")
+                _all_reduce(dist, red)
+                sse_all = red.cpu().numpy()
+                flag = torch.tensor([0 if bad_any is None else 1], device=f"cuda:{device}")
+                _all_reduce(dist, flag)
+                any_bad = bool(int(flag.item()))
+            if any_bad or not np.all(np.isfinite(sse_all[order])):
+                b = bad_any[0] if bad_any else int(next(o for o in order
+                                                        if not math.isfinite(sse_all[o])))
+                err = divergence(b // cfg.grid_j, b % cfg.grid_j,
+                                 bad_any[1] if bad_any else int(total_counts[b]) - 1,
+                                 bad_any[2] if bad_any else (g or 1) - 1)
+                err.step = step
+                err.partial_trace = trace
+                raise err
+            acc = RmseAccumulator()
+            for b in order:
+                acc = merge(acc, RmseAccumulator(float(sse_all[b]), int(total_counts[b])))
+            train_rmse = finalize(acc)
+            test_rmse = None
+            if evaluator is not None:
+                sync_all_v(sched, rank, shard.v_slice, dist)  # every rank needs all of V
+                hs = torch.tensor([shard.eng.holdout_sse()], dtype=torch.float64,
+                                  device=f"cuda:{device}")
+                _all_reduce(dist, hs)
+                test_rmse = math.sqrt(float(hs.item()) / len(evaluator.test))
+            seconds = (secs if pre is not None else time.perf_counter() - t0) if timing else 0.0
+            if shard.peer is not None:
+                shard.peer.check()
+            trace.append(TraceStep(step, train_rmse, test_rmse, seconds, max_iters, capped))
+            hist.append(train_rmse)
+            if early_stop:
+                if acc.count == 0:
+                    stop = "converged"
+                    break
+                if len(trace) >= 2 and trace.steps[-2].train_rmse - train_rmse < cfg.delta:
+                    stop = "converged"
+                    break
+        if prof:
+            torch.cuda.synchronize()
+            prof.mark(f"{len(trace)} epochs")
+        # gather the model: V from its holders, U row slabs from their owners
+        if world > 1:
+            sync_all_v(sched, rank, shard.v_slice, dist)
+            for r in range(world):
+                rows = sched.rows_of(r)
+                if len(rows):
+                    _broadcast(dist, shard.u_rows(rows), r)
         torch.cuda.synchronize()
-        prof.mark(f"{len(trace)} epochs")
-    # gather the model: V from its holders, U row slabs from their owners
-    if world > 1:
-        sync_all_v(sched, rank, shard.v_slice, dist)
-        for r in range(world):
-            rows = sched.rows_of(r)
-            if len(rows):
-                _broadcast(dist, shard.u_rows(rows), r)
-    torch.cuda.synchronize()
-    if prof:
-        prof.mark("gather (NCCL)")
-    u, v = shard.eng.get_factors()
-    if prof:
-        prof.mark("get_factors (D2H)")
-    if shard.peer is not None:  # no rank unmaps/frees while a peer could still touch it
-        torch.cuda.synchronize()
-        dist.barrier()
-    shard.eng.close()
-    if prof:
-        prof.mark("close")
-        prof.report()
-    return FactorModel(u, v), trace, stop
+        if prof:
+            prof.mark("gather (NCCL)")
+        u, v = shard.eng.get_factors()
+        if prof:
+            prof.mark("get_factors (D2H)")
+        if shard.peer is not None:  # no rank unmaps/frees while a peer could still touch it
+            torch.cuda.synchronize()
+            dist.barrier()
+        shard.eng.close()
+        closed = True
+        if prof:
+            prof.mark("close")
+            prof.report()
+        return FactorModel(u, v), trace, stop
+    except DivergenceError:
+        # every rank raises together (the flag is all-reduced): peers may still
+        # map this rank's V, so they leave the ring together before freeing
+        if not closed and shard.peer is not None:
+            torch.cuda.synchronize()
+            dist.barrier()
+        raise
+    finally:
+        if not closed:  # free the device context (and unmap peers) on any error
+            if shard.peer is not None and sys.exc_info()[0] is not DivergenceError:
+                shard.peer.abort()  # a local failure: do not leave peers spinning
+            try:
+                torch.cuda.synchronize()
+            finally:
+                shard.eng.close()
 
 
 def bench_main(args, clock_sampler=None):
@@ -610,7 +670,8 @@ def bench_main(args, clock_sampler=None):
                       seed=w.seed)
     sched = RingSchedule(w.grid, w.grid, world)
     torch.cuda.set_stream(torch.cuda.Stream(device))  # one stream: kernels + NCCL (GpuShard)
-    shard = GpuShard(d, cfg, sched, rank, device, EngineOptions(timing=False), _transport(world),
+    shard = GpuShard(d, cfg, sched, rank, device, EngineOptions(timing=False),
+                     _transport(world, device, dist),
                      dist)
     del r, c, v
     shard.eng.init_factors(w.n, w.m, w.k, w.seed)

@@ -1,0 +1,53 @@
+"""Run the reference package's own unit tests against the drop-in.
+
+The test files are NOT part of this repository (they are the reference's
+sources): `python ref_suite/run.py sync` copies them, when /root/reference is
+present (the build container), into ref_suite/_ref/ -- git-ignored, but it
+travels to the GPU box with the gpurun snapshot like the built .so files.
+`python ref_suite/run.py [fast|exact] [pytest args]` then runs them on the GPU
+with `blockmf` aliased to paper_2304_13724_b200 (bgmf_alias.py):
+  exact -- BGMF_EXACT=1: every train/sweep call uses the fp64 kernels, which
+           the reference's bit-identity assertions need;
+  fast  -- the default fp32 engine (ordered sweep where the schedule routes
+           it, chunked elsewhere).
+Files: test_{kernel,partition,scheduler,trainer,metrics,baselines}.py (the
+hot-path suites), plus test_core.py / test_data_io.py (API value types and
+file formats the drop-in also provides) and conftest.py."""
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF = "/root/reference/pkg/tests"
+FILES = ["conftest.py", "test_kernel.py", "test_partition.py", "test_scheduler.py",
+         "test_trainer.py", "test_metrics.py", "test_baselines.py", "test_core.py",
+         "test_data_io.py"]
+
+
+def sync() -> None:
+    dst = os.path.join(HERE, "_ref")
+    os.makedirs(dst, exist_ok=True)
+    for f in FILES:
+        shutil.copyfile(os.path.join(REF, f), os.path.join(dst, f))
+    print(f"copied {len(FILES)} files from {REF} to {dst}")
+
+
+def run(mode: str, extra: list[str]) -> int:
+    env = dict(os.environ)
+    env["PYTHONPATH"] = HERE + os.pathsep + env.get("PYTHONPATH", "")
+    if mode == "exact":
+        env["BGMF_EXACT"] = "1"
+    cmd = [sys.executable, "-m", "pytest", "-p", "bgmf_alias", "-q", "-rf",
+           "-p", "no:cacheprovider", "--rootdir", os.path.join(HERE, "_ref"),
+           os.path.join(HERE, "_ref"), *extra]
+    return subprocess.call(cmd, env=env, cwd=os.path.join(HERE, "_ref"))
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "exact"
+    if what == "sync":
+        sync()
+    else:
+        sys.exit(run(what, sys.argv[2:]))

@@ -200,6 +200,15 @@ class _FakePeerEngine:
     def peer_wait(self, flag, value):
         self.calls.append(("wait", flag, value))
 
+    def peer_config(self, abort_word, timeout_s):
+        self.abort_word, self.timeout_s = abort_word, timeout_s
+
+    def peer_abort(self, peer_abort_word):
+        self.calls.append(("abort", peer_abort_word))
+
+    def peer_error(self):
+        return 0
+
 
 class _FakeDist:
     def __init__(self, world, rank):
@@ -260,17 +269,26 @@ def test_peer_links_sequence_and_order(world, P):
                         waits[(s, r)].append(value)
     for key in pushes:
         assert pushes[key] == list(range(1, len(pushes[key]) + 1))
+    # bounded waits: each rank's abort word is the word after its flags; a
+    # failing rank raises it in every peer's page
+    for r, lk in enumerate(links):
+        assert lk.eng.abort_word == lk.flags + 4 * world and lk.eng.timeout_s > 0
+        n0 = len(lk.eng.calls)
+        lk.abort()
+        got = sorted(c[1] for c in lk.eng.calls[n0:])
+        assert got == sorted(fmap(d) + 4 * world for d in range(world) if d != r)
         assert waits[key] == pushes[key]
     assert sum(len(v) for v in pushes.values()) > 0
 
 
 def test_ring_transport_choice(monkeypatch):
     """Peer memory by default when every rank is on this node; torch.distributed
-    for multi-node jobs (CUDA IPC is single-node); BGMF_RING_TRANSPORT wins."""
+    for multi-node jobs (CUDA IPC is single-node) and for launchers that do not
+    say how many ranks share the node; BGMF_RING_TRANSPORT wins."""
     for var in ("LOCAL_WORLD_SIZE", "BGMF_RING_TRANSPORT"):
         monkeypatch.delenv(var, raising=False)
     assert D._transport(1) == "dist"
-    assert D._transport(8) == "peer"
+    assert D._transport(8) == "dist"  # no LOCAL_WORLD_SIZE: not known to be one node
     monkeypatch.setenv("LOCAL_WORLD_SIZE", "8")
     assert D._transport(8) == "peer"
     assert D._transport(16) == "dist"

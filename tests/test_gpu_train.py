@@ -319,3 +319,40 @@ def test_heavy_user_runs_split_across_chunks(n, m, k):
     got = np.array([s.train_rmse for s in res.trace])
     want = np.array([s["train_rmse"] for s in otr])
     assert np.all(np.abs(got - want) <= 1e-3), np.abs(got - want).max()
+
+
+def test_run_steps_reports_late_divergence_block():
+    """bgmf_run_steps queues many steps before reading their divergence words.
+    Positions are step-relative: on a 255 x 255 grid the second step starts at
+    global position 65025, past pack_bad's 16-bit field.  The block that
+    run_steps reports for a divergence in its second step must be the one a
+    step-by-step run reports (ordered mode: deterministic)."""
+    n, m, P, k = 600, 600, 255, 4
+    g = np.random.default_rng(3)
+    cells = g.choice(n * m, 20_000, replace=False)
+    r, c = np.divmod(cells, m)
+    v = np.clip(np.rint(3 + g.normal(0, 1, len(cells))), 1, 5) * 10.0
+    plan0, plan1 = bm.plan_step(P, P, 0), bm.plan_step(P, P, 1)
+    seen = False
+    for alpha in (0.002, 0.005, 0.01, 0.02, 0.05, 0.1):
+        engs = []
+        for _ in range(2):
+            e = bm.Engine(bm.EngineOptions(ordered=True))
+            e.partition(r, c, v, n, m, P, P)
+            e.init_factors(n, m, k, 0)
+            engs.append(e)
+        a, b = engs
+        i0, o0 = a.plan_arrays(plan0)
+        i1, o1 = a.plan_arrays(plan1)
+        _, bad, _ = a.run_steps([(i0, o0, 1), (i1, o1, 40)], alpha, 0.0)
+        _, bad0 = b.run_step(i0, o0, 1, alpha, 0.0)
+        bad1 = None if bad0 is not None else b.run_step(i1, o1, 40, alpha, 0.0)[1]
+        a.close()
+        b.close()
+        if bad is None or bad[0] != 1 or bad0 is not None:
+            continue
+        assert bad1 is not None
+        assert bad[1] == int(i1[bad1[0]]) and bad[2:] == bad1[1:], (bad, bad1)
+        seen = True
+        break
+    assert seen, "no alpha diverged in the second step only"
