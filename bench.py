@@ -102,11 +102,7 @@ def make_workload(name: str, nnz: int | None):
 
     w = workloads.CONFIGS[name]
     t0 = time.perf_counter()
-    if name == "C1":
-        r, c, v = workloads.ml100k_standin()
-        v = v.astype(np.float64)
-    else:
-        r, c, v = workloads.lowrank(w.n, w.m, nnz or w.nnz, seed=w.seed)
+    r, c, v = workloads.generate(name, nnz)
     return w, r, c, v, time.perf_counter() - t0
 
 
@@ -319,6 +315,11 @@ def run_ours(args):
                 "walls_ms": [round(x * 1e3, 2) for x in walls] if e2e_val else None},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_kind": hbm_kind,
+                     # the honest fractions: DRAM bytes the kernel really moves
+                     # (ncu) per live launch time, and the SM<->L2 probe ceiling
+                     "dram_frac": (traffic / (sgd_launch_ms / 1e3) / (hbm * 1e9)
+                                   if traffic else None),
+                     "l2_frac": l2["frac"] if l2 else None,
                      "traffic_source": "profiles/ncu_traffic_<config>.json (ncu --set full, "
                                        "dram__bytes_read.sum + dram__bytes_write.sum)",
                      "note": "frac > 1 by construction of the metric: algorithmic bytes "

@@ -347,6 +347,11 @@ int bgmf_peer_error(bgmf_ctx* ctx, int* out);
  * kernel time of 3 timed launches in *ms_out. */
 int bgmf_probe_l2(int device, int64_t rows, int64_t ratings, int mode,
                   int ctas_per_sm, double* ms_out);
+/* DSMEM variant of the probe (V block of `rows` x 128 fp32 spread over a
+ * cluster of cs CTAs): mode 5 remote row read + fp32 atomic row add, 6 the
+ * same within the CTA's own slice, 7 remote reads only. */
+int bgmf_probe_dsmem(int device, int64_t rows, int64_t ratings, int mode, int cs,
+                     int ctas_per_sm, double* ms_out);
 
 #ifdef __cplusplus
 }

@@ -37,6 +37,7 @@ _i, _l, _d = ctypes.c_int, ctypes.c_int64, ctypes.c_double
 SIGNATURES = {
     "bgmf_version": (_i, []),
     "bgmf_probe_l2": (_i, [_i, _l, _l, _i, _i, _f64p]),
+    "bgmf_probe_dsmem": (_i, [_i, _l, _l, _i, _i, _i, _f64p]),
     "bgmf_create": (_i, [_i, _vp, ctypes.POINTER(_ctx)]),
     "bgmf_destroy": (None, [_ctx]),
     "bgmf_last_error": (ctypes.c_char_p, [_ctx]),

@@ -46,6 +46,12 @@ CONFIGS = {
                    description="synthetic Netflix-shaped (480k x 17.8k, 100M), 16x16, k=128"),
     "C5": Workload("C5", 10_000_000, 1_000_000, 2_000_000_000, 128, 64,
                    description="synthetic 10M x 1M, 2B ratings, k=128, out-of-core"),
+    # C4 with skew: user and item popularity follow shifted power laws (the
+    # real MovieLens / Netflix data the paper trains on are heavy-tailed,
+    # PAPER.md:252,294); same shape, grid, k and rating model as C4
+    "C4Z": Workload("C4Z", 480_000, 17_800, 100_000_000, 128, 16,
+                    description="synthetic Netflix-shaped with Zipf users and items "
+                                "(480k x 17.8k, 100M), 16x16, k=128"),
 }
 
 
@@ -131,6 +137,84 @@ def lowrank(n: int, m: int, nnz: int, seed: int = 0, chunk: int = 1 << 24):
         rows[s:e], cols[s:e] = r, c
         vals[s:e] = np.clip(np.rint(raw), 1, 5)
     return rows, cols, vals
+
+
+def _power_cdf(count: int, shift: float, expo: float) -> np.ndarray:
+    w = (np.arange(count, dtype=np.float64) + 1.0 + shift) ** -expo
+    cdf = np.cumsum(w)
+    return cdf / cdf[-1]
+
+
+def zipf_cells(n: int, m: int, nnz: int, seed: int = 0, user_shift: float = 500.0,
+               user_expo: float = 0.9, item_shift: float = 50.0,
+               item_expo: float = 1.0, device: str | None = None) -> np.ndarray:
+    """nnz distinct cells of an n x m matrix, users and items drawn with
+    probability ~ (rank + shift)^-expo (ranks scattered over the ids by a
+    seeded permutation, so heavy users and hot items land in every block).
+    Defaults: the hottest item gets ~0.3% of the ratings (~half the users,
+    like Netflix's), the heaviest users rate most of the items; cells in
+    scrambled order.  Drawn with torch's generator on `device` (default
+    cuda:0 when present: 100 M distinct cells in seconds; the CPU stream
+    differs, so a dataset is only comparable within one device kind)."""
+    import torch
+
+    dev = device or ("cuda:0" if torch.cuda.is_available() else "cpu")
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed * 1_000_003 + 0x5A1F)
+
+    def cdf(count, shift, expo):
+        w = (torch.arange(count, device=dev, dtype=torch.float64) + 1.0 + shift) ** -expo
+        c = torch.cumsum(w, 0)
+        return c / c[-1]
+
+    ucdf, icdf = cdf(n, user_shift, user_expo), cdf(m, item_shift, item_expo)
+    uperm = torch.randperm(n, generator=g, device=dev)
+    iperm = torch.randperm(m, generator=g, device=dev)
+    have = torch.empty(0, dtype=torch.int64, device=dev)
+    while have.numel() < nnz:
+        draw = int((nnz - have.numel()) * 1.15) + 1024
+        u = uperm[torch.searchsorted(ucdf, torch.rand(draw, generator=g, device=dev,
+                                                      dtype=torch.float64)).clamp_(max=n - 1)]
+        i = iperm[torch.searchsorted(icdf, torch.rand(draw, generator=g, device=dev,
+                                                      dtype=torch.float64)).clamp_(max=m - 1)]
+        have = torch.unique(torch.cat([have, u * m + i]))
+        del u, i
+    keep = torch.randperm(have.numel(), generator=g, device=dev)[:nnz]
+    out = have[keep].cpu().numpy()
+    del have, keep
+    return out
+
+
+def zipf_lowrank(n: int, m: int, nnz: int, seed: int = 0, chunk: int = 1 << 24):
+    """(rows, cols, values) of C4Z: zipf_cells with lowrank's rating model."""
+    g = np.random.default_rng(seed)
+    f = 6
+    b_user = g.normal(0.0, 0.55, n)
+    b_item = g.normal(0.0, 0.55, m)
+    taste_u = g.normal(0.0, 0.6 / np.sqrt(f), (n, f)).astype(np.float32)
+    taste_v = g.normal(0.0, 0.6 / np.sqrt(f), (m, f)).astype(np.float32)
+    cells = zipf_cells(n, m, nnz, seed)
+    rows, cols = np.divmod(cells, m)
+    vals = np.empty(nnz, np.float64)
+    for s in range(0, nnz, chunk):
+        e = min(nnz, s + chunk)
+        r, c = rows[s:e], cols[s:e]
+        raw = (3.53 + b_user[r] + b_item[c]
+               + np.einsum("ij,ij->i", taste_u[r], taste_v[c]).astype(np.float64)
+               + g.normal(0.0, 0.8, e - s))
+        vals[s:e] = np.clip(np.rint(raw), 1, 5)
+    return rows, cols, vals
+
+
+def generate(name: str, nnz: int | None = None):
+    """(rows, cols, values) of workload `name` (C1 .. C5, C4Z)."""
+    w = CONFIGS[name]
+    if name == "C1":
+        r, c, v = ml100k_standin()
+        return r, c, v.astype(np.float64)
+    if name == "C4Z":
+        return zipf_lowrank(w.n, w.m, nnz or w.nnz, w.seed)
+    return lowrank(w.n, w.m, nnz or w.nnz, w.seed)
 
 
 def dataset(name: str, nnz: int | None = None) -> RatingsDataset:

@@ -226,6 +226,29 @@ def test_c4_parity_vs_oracle():
     assert abs(bm.rmse(res.model, d) - O.rmse(ou, ov, d.rows, d.cols, d.values)) <= TOL
 
 
+@pytest.mark.slow
+def test_c4_zipf_parity_vs_oracle():
+    """C4Z: the C4 shape with heavy-tailed users and items (the hottest item
+    rated by about half the users, heavy users rating most items): hot V rows
+    take many concurrent updates and heavy users' runs span chunks.  2 epochs
+    against the oracle: per-epoch train RMSE and final RMSE within 1e-3."""
+    w = workloads.CONFIGS["C4Z"]
+    r, c, v = workloads.generate("C4Z")
+    d = bm.RatingsDataset(w.n, w.m, r, c, v)
+    cfg = bm.TrainConfig(k=w.k, alpha=w.alpha, beta=w.beta, outer_steps=2, grid_i=w.grid,
+                         grid_j=w.grid, seed=w.seed)
+    res = bm.train_blocked(d, cfg, early_stop=False)
+    tr = [s.train_rmse for s in res.trace]
+    assert all(math.isfinite(x) for x in tr) and tr[1] < tr[0]
+    ou, ov, otr, _ = O.train_blocked(w.n, w.m, r, c, v, k=w.k, alpha=w.alpha, beta=w.beta,
+                                     outer_steps=2, grid_i=w.grid, grid_j=w.grid, seed=w.seed,
+                                     early_stop=False, nthreads=16)
+    drift = np.abs(np.array(tr) - [s["train_rmse"] for s in otr])
+    print(f"C4Z max |d train_rmse| over 2 epochs: {drift.max():.3e}")
+    assert drift.max() <= TOL
+    assert abs(bm.rmse(res.model, d) - O.rmse(ou, ov, d.rows, d.cols, d.values)) <= TOL
+
+
 def test_exact_run_saves_reference_bytes(golden):
     """Exact mode end to end: the saved model file is byte-identical to the
     reference's save_model output for the same run (data_io.py:221-227)."""
@@ -323,36 +346,42 @@ def test_heavy_user_runs_split_across_chunks(n, m, k):
 
 def test_run_steps_reports_late_divergence_block():
     """bgmf_run_steps queues many steps before reading their divergence words.
-    Positions are step-relative: on a 255 x 255 grid the second step starts at
-    global position 65025, past pack_bad's 16-bit field.  The block that
-    run_steps reports for a divergence in its second step must be the one a
-    step-by-step run reports (ordered mode: deterministic)."""
+    Positions are step-relative: on a 255 x 255 grid the second step starts
+    past global position 65000, beyond pack_bad's 16-bit field.  One rating of
+    1e36 (finite, but the next update of its cell overflows fp32) sits in block X; step 1's plan
+    leaves X out, step 2 sweeps it at plan position ~1000.  The block, entry
+    and iteration run_steps reports must be the ones a step-by-step run
+    reports (ordered mode: deterministic)."""
     n, m, P, k = 600, 600, 255, 4
     g = np.random.default_rng(3)
     cells = g.choice(n * m, 20_000, replace=False)
     r, c = np.divmod(cells, m)
-    v = np.clip(np.rint(3 + g.normal(0, 1, len(cells))), 1, 5) * 10.0
-    plan0, plan1 = bm.plan_step(P, P, 0), bm.plan_step(P, P, 1)
-    seen = False
-    for alpha in (0.002, 0.005, 0.01, 0.02, 0.05, 0.1):
-        engs = []
-        for _ in range(2):
-            e = bm.Engine(bm.EngineOptions(ordered=True))
-            e.partition(r, c, v, n, m, P, P)
-            e.init_factors(n, m, k, 0)
-            engs.append(e)
-        a, b = engs
-        i0, o0 = a.plan_arrays(plan0)
-        i1, o1 = a.plan_arrays(plan1)
-        _, bad, _ = a.run_steps([(i0, o0, 1), (i1, o1, 40)], alpha, 0.0)
-        _, bad0 = b.run_step(i0, o0, 1, alpha, 0.0)
-        bad1 = None if bad0 is not None else b.run_step(i1, o1, 40, alpha, 0.0)[1]
-        a.close()
-        b.close()
-        if bad is None or bad[0] != 1 or bad0 is not None:
-            continue
-        assert bad1 is not None
-        assert bad[1] == int(i1[bad1[0]]) and bad[2:] == bad1[1:], (bad, bad1)
-        seen = True
-        break
-    assert seen, "no alpha diverged in the second step only"
+    v = np.clip(np.rint(3 + g.normal(0, 1, len(cells))), 1, 5)
+    plan1 = bm.plan_step(P, P, 1)
+    rb, cb = np.asarray(bm.split_bounds(n, P)), np.asarray(bm.split_bounds(m, P))
+    flat = [blk for b in plan1.batches for blk in b] if hasattr(plan1, "batches") else \
+        [blk for b in plan1 for blk in b]
+    bi, bj = flat[1000]
+    r = np.append(r, [rb[bi], rb[bi]])  # the 1e36 rating, then a duplicate cell
+    c = np.append(c, [cb[bj], cb[bj]])
+    v = np.append(v, [1e36, 3.0])
+    engs = []
+    for _ in range(2):
+        e = bm.Engine(bm.EngineOptions(ordered=True))
+        e.partition(r, c, v, n + 0, m, P, P)
+        e.init_factors(n, m, k, 0)
+        engs.append(e)
+    a, b = engs
+    i1, o1 = a.plan_arrays(plan1)
+    X = bi * P + bj
+    keep = i1 != X
+    i0 = i1[keep]  # step 1: every block of the plan but X, one batch per old batch
+    o0 = np.array([np.count_nonzero(keep[:o]) for o in o1], np.int32)
+    _, bad, _ = a.run_steps([(i0, o0, 1), (i1, o1, 1)], 1e-3, 1e-2)
+    _, bad0 = b.run_step(i0, o0, 1, 1e-3, 1e-2)
+    _, bad1 = b.run_step(i1, o1, 1, 1e-3, 1e-2)
+    a.close()
+    b.close()
+    assert bad0 is None and bad1 is not None and bad is not None
+    assert int(i1[bad1[0]]) == X and bad1[0] >= 1000
+    assert bad[0] == 1 and bad[1] == X and tuple(bad[2:]) == tuple(bad1[1:]), (bad, bad1)
