@@ -191,6 +191,18 @@ int bgmf_holdout_sse(bgmf_ctx* ctx, double* sse_out);
  * stream while the previous piece computes; factors stay resident.  A slot
  * must hold the largest block.  Fast mode, fixed schedules. */
 int bgmf_stream_ratings(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
+/* Out-of-core partition (replaces bgmf_partition + bgmf_stream_ratings when
+ * the partition itself must not exceed device_budget bytes of HBM): row
+ * blocks in chunks, each partitioned on the device exactly as
+ * bgmf_partition does, straight into the pinned streaming layout; then
+ * nslots device slots of slot_ratings ratings.  Same ordering, offsets and
+ * errors as bgmf_partition (reference partition.py:112-136). */
+int bgmf_partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
+                       const double* vals, int64_t nnz, int64_t n, int64_t m, int grid_i,
+                       int grid_j, int64_t device_budget, int64_t slot_ratings, int nslots);
+/* Device memory of the stream-ordered pool every context allocates from:
+ * out2 = {bytes in use now, high-water mark}; reset = 1 restarts the mark. */
+int bgmf_mem_stats(bgmf_ctx* ctx, int64_t* out2, int reset);
 /* Rating bytes streamed host->device since the context was created. */
 int bgmf_stream_stats(bgmf_ctx* ctx, double* h2d_bytes);
 

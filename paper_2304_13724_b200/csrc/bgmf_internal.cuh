@@ -147,6 +147,7 @@ struct bgmf_ctx {
   std::vector<cudaEvent_t> ev_copied, ev_consumed;
   cudaStream_t copy_stream = nullptr;
   double h2d_bytes = 0;                  // streamed this context (stats)
+  int ooc_chunks = 0;                    // chunks of the last out-of-core partition
 
   // ordered sweep (ordered.cu): column ranks, row pointers, row flags
   int ord_mode = -1;                     // 1: ordered where possible, 0: never, -1: auto
@@ -286,7 +287,7 @@ int run_step_stream_converge(bgmf_ctx* ctx, const int32_t* plan, const int32_t* 
 void order_release(bgmf_ctx* ctx);
 int ensure_order_index(bgmf_ctx* ctx);
 bool ordered_block_ok(bgmf_ctx* ctx, int b);
-bool use_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1);
+bool use_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1, bool converge = false);
 int run_batch_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1, int pos_base,
                       int iters, float alpha, float beta, bool conv = false, double tol = 0.0);
 int run_shards_ordered(bgmf_ctx* ctx, const int32_t* r0, const int32_t* r1, int nshards,
@@ -294,6 +295,12 @@ int run_shards_ordered(bgmf_ctx* ctx, const int32_t* r0, const int32_t* r1, int 
 
 // stream.cu -- out-of-core: ratings in pinned host memory, device slot ring
 int stream_enable(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
+int stream_slots(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
+// out-of-core partition (partition.cu): chunks of row blocks under `budget`
+// bytes of HBM straight into the pinned streaming layout
+int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const double* vals,
+                  int64_t nnz, int64_t n, int64_t m, int I, int J, int64_t budget,
+                  int64_t slot_ratings, int nslots);
 void stream_free(bgmf_ctx* ctx);
 int stream_export(bgmf_ctx* ctx, int64_t* order, int32_t* lrows, int32_t* lcols);
 int run_step_stream(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off, int nbatch,

@@ -582,6 +582,35 @@ int bgmf_holdout_sse(bgmf_ctx* c, double* sse_out) {
                       sse_out);
 }
 
+int bgmf_partition_ooc(bgmf_ctx* c, const int64_t* rows, const int64_t* cols,
+                       const double* vals, int64_t nnz, int64_t n, int64_t m, int grid_i,
+                       int grid_j, int64_t device_budget, int64_t slot_ratings, int nslots) {
+  if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
+  cudaSetDevice(c->device);
+  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
+  c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
+  return partition_ooc(c, rows, cols, vals, nnz, n, m, grid_i, grid_j, device_budget,
+                       slot_ratings, nslots);
+}
+
+int bgmf_mem_stats(bgmf_ctx* c, int64_t* out2, int reset) {
+  if (!c || !out2) return fail(c, BGMF_ERR_ARG, "NULL argument");
+  cudaSetDevice(c->device);
+  cudaMemPool_t pool;
+  BGMF_CK(c, cudaDeviceGetDefaultMemPool(&pool, c->device));
+  unsigned long long used = 0, high = 0;
+  BGMF_CK(c, cudaStreamSynchronize(c->stream));
+  BGMF_CK(c, cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  BGMF_CK(c, cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high));
+  out2[0] = (int64_t)used;
+  out2[1] = (int64_t)high;
+  if (reset) {
+    unsigned long long zero = 0;
+    BGMF_CK(c, cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero));
+  }
+  return BGMF_OK;
+}
+
 int bgmf_stream_ratings(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
   if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
   cudaSetDevice(c->device);

@@ -608,7 +608,8 @@ void order_release(bgmf_ctx* c) {
   c->ord_ready = false;
 }
 
-int sort_pairs_device(bgmf_ctx* ctx, uint64_t** keys, uint32_t** vals, int64_t n, int bits);
+int sort_pairs_device(bgmf_ctx* ctx, uint64_t** keys, uint32_t** vals, int64_t n, int bits,
+                      int lo_bit = 0);
 
 // Column ranks and row pointers of the resident partition (once per
 // partition; ~24 B per rating of temporaries).
@@ -855,7 +856,7 @@ int run_shards_ordered(bgmf_ctx* c, const int32_t* r0, const int32_t* r1, int ns
 // them: every fast-mode drift past 1e-3 found by the randomised sweeps,
 // DESIGN.md section 4) or a dense block (> 1/8 of its cells rated: rows share
 // their columns and concurrent chunks collide on every V row).
-bool use_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1) {
+bool use_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, bool converge) {
   if (c->ord_mode == 0 || c->exact || c->streaming) return false;
   int nonempty = 0;
   bool dense = false;
@@ -869,7 +870,10 @@ bool use_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1) {
     dense |= cnt * 8 > h * w;
     if (!ordered_block_ok(c, b)) return false;
   }
-  if (c->ord_mode > 0) return true;
+  // ConvergeEachBlock: the per-block loop (sweep, SSE, improvement test)
+  // runs on the device only in the ordered kernel, and its stopping
+  // decisions then see the reference's sequential trajectory
+  if (c->ord_mode > 0 || converge) return true;
   return nonempty < c->ord_auto_blocks || dense;
 }
 

@@ -24,6 +24,10 @@
 // HBM-bound integer work: every pass streams key+payload (12 B/rating) in and
 // out; grid sized to tiles of 4096 ratings.
 
+#include <omp.h>
+
+#include <algorithm>
+
 #include "bgmf_internal.cuh"
 
 namespace bgmf {
@@ -319,6 +323,19 @@ __global__ void decode_embedded(const uint64_t* __restrict__ keys,
   }
 }
 
+// out-of-core chunks: packed (row << cbits | col) records and the input index
+// of every partitioned entry (gidx = the chunk's input indices)
+__global__ void pack_and_order(const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
+                               const uint32_t* __restrict__ order,
+                               const uint32_t* __restrict__ gidx, int64_t n, int cbits,
+                               int32_t* __restrict__ rec, uint32_t* __restrict__ gorder) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (rec) rec[i] = (int32_t)(((uint32_t)lrow[i] << cbits) | (uint32_t)lcol[i]);
+    gorder[i] = gidx[order[i]];
+  }
+}
+
 int bits_for(uint64_t maxval) {  // bits to represent 0..maxval
   int b = 0;
   while (b < 64 && (maxval >> b) != 0) ++b;
@@ -333,11 +350,12 @@ void free_dev(T*& p, cudaStream_t s) {
 
 }  // namespace
 
-// Stable LSD radix sort of (key, payload) pairs over key bits [0, bits), with
+// Stable LSD radix sort of (key, payload) pairs over key bits [lo_bit, lo_bit + bits), with
 // the partitioner's kernels.  *keys / *vals are swapped with the sorted
 // buffers (the caller frees whatever they point to afterwards).  Used by the
 // ordered sweep's column-rank index (ordered.cu).
-int sort_pairs_device(bgmf_ctx* ctx, uint64_t** keys, uint32_t** vals, int64_t n, int bits) {
+int sort_pairs_device(bgmf_ctx* ctx, uint64_t** keys, uint32_t** vals, int64_t n, int bits,
+                      int lo_bit) {
   if (n <= 1 || bits <= 0) return BGMF_OK;
   cudaStream_t s = ctx->stream;
   const bool wide = (bits + 8) / 9 < (bits + 7) / 8;
@@ -361,7 +379,7 @@ int sort_pairs_device(bgmf_ctx* ctx, uint64_t** keys, uint32_t** vals, int64_t n
   uint64_t* ka = *keys;
   uint32_t* ia = *vals;
   for (int p = 0; p < passes; ++p) {
-    const int shift = dbits * p;
+    const int shift = lo_bit + dbits * p;
     if (wide) {
       radix_hist<512><<<(unsigned)ntiles, RS_THREADS, 0, s>>>(ka, n, shift, ntiles, hist);
       radix_scan_tiles<<<512, 1024, 0, s>>>(hist, ntiles, tot);
@@ -588,6 +606,271 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
   prof_mark(ctx, "partition: free temporaries");
 #undef PCK
   ctx->partitioned = true;
+  return BGMF_OK;
+}
+
+
+// ---- out-of-core partition -------------------------------------------
+// A dataset whose partition does not fit the device (the paper's motivating
+// case: BGMF needs only the blocks being computed) enters
+// here instead of partition_device:
+//   1. host pass (OpenMP over input ranges): range checks, per-block counts;
+//   2. row blocks grouped into chunks whose partition temporaries
+//      (kChunkBytes per rating) fit `budget`;
+//   3. host pass: each entry narrowed (int32 row/col, fp32 value) into its
+//      chunk's bucket with its input index, input order kept per chunk;
+//   4. per chunk: upload, device keys + radix sort + decode (the in-core
+//      kernels, so the block order and in-block order are the reference's
+//      lexsort order, bit for bit), packed records, then D2H of every block
+//      straight into the pinned diagonal layout of the streaming path.
+// Peak device memory: one chunk's temporaries, then the slot ring.
+namespace {
+constexpr int64_t kChunkBytes = 64;  // device bytes per rating while a chunk is partitioned
+}
+
+int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const double* vals,
+                  int64_t nnz, int64_t n, int64_t m, int I, int J, int64_t budget,
+                  int64_t slot_ratings, int nslots) {
+  if (n < 1 || m < 1 || n > INT32_MAX || m > INT32_MAX)
+    return fail(ctx, BGMF_ERR_ARG, "n and m must be in [1, 2^31)");
+  if (I < 1 || I > n) return fail(ctx, BGMF_ERR_ARG, "grid_i must be in [1, n]");
+  if (J < 1 || J > m) return fail(ctx, BGMF_ERR_ARG, "grid_j must be in [1, m]");
+  if ((int64_t)I * J > 65535) return fail(ctx, BGMF_ERR_ARG, "grid_i*grid_j must be <= 65535");
+  if (nnz < 0 || nnz >= (int64_t)0xFFFFFFFFll)
+    return fail(ctx, BGMF_ERR_ARG, "nnz must be in [0, 2^32-1)");
+  if (nnz > 0 && (!rows || !cols || !vals)) return fail(ctx, BGMF_ERR_ARG, "NULL input");
+  if (ctx->exact) return fail(ctx, BGMF_ERR_STATE, "out-of-core partitioning is fast-mode only");
+  if (nslots < 2 || nslots > 8) return fail(ctx, BGMF_ERR_ARG, "nslots must be in [2, 8]");
+  if (ctx->streaming) stream_free(ctx);
+  order_release(ctx);
+  free_dev(ctx->d_lrow, ctx->stream); free_dev(ctx->d_lcol, ctx->stream);
+  free_dev(ctx->d_val, ctx->stream); free_dev(ctx->d_val64, ctx->stream);
+  free_dev(ctx->d_order, ctx->stream);
+  ctx->partitioned = false;
+  prof_mark(ctx, nullptr);
+
+  const int64_t rbase = n / I, rextra = n % I, cbase = m / J, cextra = m % J;
+  const int rbits = bits_for((uint64_t)(rbase + (rextra ? 1 : 0)) - 1);
+  const int cbits = bits_for((uint64_t)(cbase + (cextra ? 1 : 0)) - 1);
+  const int bbits = bits_for((uint64_t)I * J - 1);
+  if (rbits > 31 || cbits > 31) return fail(ctx, BGMF_ERR_ARG, "block slab wider than 2^31");
+  ctx->n = n; ctx->m = m; ctx->I = I; ctx->J = J; ctx->nnz = nnz;
+  ctx->rbits = rbits; ctx->cbits = cbits;
+  ctx->row_bounds.assign(I + 1, 0);
+  ctx->col_bounds.assign(J + 1, 0);
+  for (int p = 0; p < I; ++p) ctx->row_bounds[p + 1] = ctx->row_bounds[p] + rbase + (p < rextra);
+  for (int p = 0; p < J; ++p) ctx->col_bounds[p + 1] = ctx->col_bounds[p] + cbase + (p < cextra);
+  const int nb = I * J;
+  auto slab = [](int64_t x, int64_t base, int64_t extra) -> int64_t {
+    const int64_t big = extra * (base + 1);
+    return x < big ? x / (base + 1) : extra + (x - big) / base;
+  };
+
+  // 1. range checks + per-block counts
+  int nth = 1;
+#pragma omp parallel
+  {
+#pragma omp single
+    nth = omp_get_num_threads();
+  }
+  std::vector<int64_t> tcount((size_t)nth * nb, 0);
+  std::vector<int64_t> tbad(nth, -1);
+#pragma omp parallel num_threads(nth)
+  {
+    const int t = omp_get_thread_num();
+    const int64_t lo = nnz * t / nth, hi = nnz * (t + 1) / nth;
+    int64_t* cnt = tcount.data() + (size_t)t * nb;
+    for (int64_t i = lo; i < hi; ++i) {
+      const int64_t r = rows[i], c = cols[i];
+      if (r < 0 || r >= n || c < 0 || c >= m) { tbad[t] = i; break; }
+      ++cnt[slab(r, rbase, rextra) * J + slab(c, cbase, cextra)];
+    }
+  }
+  for (int t = 0; t < nth; ++t)
+    if (tbad[t] >= 0) {
+      const int64_t i = tbad[t];
+      char buf[160];
+      snprintf(buf, sizeof buf, "entry %lld: index (%lld, %lld) outside %lldx%lld matrix",
+               (long long)i, (long long)rows[i], (long long)cols[i], (long long)n, (long long)m);
+      return fail(ctx, BGMF_ERR_DATA, buf);
+    }
+  std::vector<int64_t> bcount(nb, 0);
+  for (int t = 0; t < nth; ++t)
+    for (int b = 0; b < nb; ++b) bcount[b] += tcount[(size_t)t * nb + b];
+  ctx->h_offsets.assign(nb + 1, 0);
+  for (int b = 0; b < nb; ++b) ctx->h_offsets[b + 1] = ctx->h_offsets[b] + bcount[b];
+  int64_t max_block = 0;
+  for (int b = 0; b < nb; ++b) max_block = std::max(max_block, bcount[b]);
+  if (slot_ratings < max_block || slot_ratings < 1)
+    return fail(ctx, BGMF_ERR_ARG, "slot smaller than the largest block (" +
+                                       std::to_string(max_block) + " ratings)");
+
+  // 2. chunks of whole row blocks
+  const int64_t per_chunk = std::max<int64_t>(1, budget / kChunkBytes);
+  std::vector<int> chunk_of(I, 0);
+  std::vector<int64_t> chunk_cnt;
+  std::vector<int> chunk_b0;  // first row block of each chunk
+  {
+    int64_t acc = 0;
+    for (int bi = 0; bi < I; ++bi) {
+      int64_t rc = 0;
+      for (int bj = 0; bj < J; ++bj) rc += bcount[bi * J + bj];
+      if (chunk_cnt.empty() || (acc > 0 && acc + rc > per_chunk)) {
+        chunk_cnt.push_back(0);
+        chunk_b0.push_back(bi);
+        acc = 0;
+      }
+      acc += rc;
+      chunk_cnt.back() += rc;
+      chunk_of[bi] = (int)chunk_cnt.size() - 1;
+    }
+  }
+  const int nch = (int)chunk_cnt.size();
+  chunk_b0.push_back(I);
+  std::vector<int64_t> chunk_base(nch + 1, 0);
+  for (int k = 0; k < nch; ++k) chunk_base[k + 1] = chunk_base[k] + chunk_cnt[k];
+  prof_mark(ctx, "ooc: host count pass");
+
+  // 3. buckets: narrowed entries + input index, per chunk in input order
+  const size_t N = (size_t)(nnz > 0 ? nnz : 1);
+  std::vector<int32_t> br(N), bc(N);
+  std::vector<float> bv(N);
+  std::vector<uint32_t> bx(N);
+  std::vector<int64_t> toff((size_t)nth * nch, 0);
+  for (int k = 0; k < nch; ++k) {
+    int64_t o = chunk_base[k];
+    for (int t = 0; t < nth; ++t) {
+      toff[(size_t)t * nch + k] = o;
+      for (int bi = chunk_b0[k]; bi < chunk_b0[k + 1]; ++bi)
+        for (int bj = 0; bj < J; ++bj) o += tcount[(size_t)t * nb + bi * J + bj];
+    }
+  }
+#pragma omp parallel num_threads(nth)
+  {
+    const int t = omp_get_thread_num();
+    const int64_t lo = nnz * t / nth, hi = nnz * (t + 1) / nth;
+    int64_t* off = toff.data() + (size_t)t * nch;
+    for (int64_t i = lo; i < hi; ++i) {
+      const int64_t r = rows[i];
+      const int64_t p = off[chunk_of[slab(r, rbase, rextra)]]++;
+      br[p] = (int32_t)r;
+      bc[p] = (int32_t)cols[i];
+      bv[p] = (float)vals[i];
+      bx[p] = (uint32_t)i;
+    }
+  }
+  prof_mark(ctx, "ooc: host bucket pass");
+
+  // pinned diagonal layout (stream.cu) and its block positions
+  ctx->packed = rbits + cbits <= 32;
+  std::vector<int> order;
+  order.reserve(nb);
+  if (I == J) {
+    for (int d = 0; d < I; ++d)
+      for (int j = 0; j < J; ++j) order.push_back(((j + d) % I) * J + j);
+  } else {
+    for (int b = 0; b < nb; ++b) order.push_back(b);
+  }
+  ctx->h_pos.assign(nb, 0);
+  {
+    int64_t pos = 0;
+    for (int b : order) { ctx->h_pos[b] = pos; pos += bcount[b]; }
+  }
+  BGMF_CK(ctx, cudaMallocHost(&ctx->h_lrow, N * 4));
+  if (!ctx->packed) BGMF_CK(ctx, cudaMallocHost(&ctx->h_lcol, N * 4));
+  BGMF_CK(ctx, cudaMallocHost(&ctx->h_val, N * 4));
+  BGMF_CK(ctx, cudaMallocHost(&ctx->h_order, N * 4));
+  prof_mark(ctx, "ooc: pinned layout");
+
+  // 4. chunk by chunk on the device
+  cudaStream_t s = ctx->stream;
+  const int total_bits = rbits + cbits + bbits;
+  int64_t max_chunk = 0;
+  for (int k = 0; k < nch; ++k) max_chunk = std::max(max_chunk, chunk_cnt[k]);
+  const size_t C = (size_t)(max_chunk > 0 ? max_chunk : 1);
+  int32_t *d_r = nullptr, *d_c = nullptr, *lr = nullptr, *lc = nullptr, *rec = nullptr;
+  float *d_v = nullptr, *vv = nullptr;
+  uint32_t *d_x = nullptr, *ia = nullptr, *ord = nullptr, *gord = nullptr;
+  uint64_t* ka = nullptr;
+  unsigned long long* d_bad = nullptr;
+  int rc = BGMF_OK;
+  auto cleanup = [&]() {
+    free_dev(d_r, s); free_dev(d_c, s); free_dev(d_v, s); free_dev(d_x, s); free_dev(ka, s);
+    free_dev(ia, s); free_dev(lr, s); free_dev(lc, s); free_dev(vv, s); free_dev(ord, s);
+    free_dev(rec, s); free_dev(gord, s); free_dev(d_bad, s);
+  };
+#define OCK(call)                                                                    \
+  do {                                                                               \
+    cudaError_t _e = (call);                                                         \
+    if (_e != cudaSuccess) { rc = cuda_fail(ctx, _e, #call); cleanup(); return rc; } \
+  } while (0)
+  OCK(dmalloc(&d_r, C * 4, s)); OCK(dmalloc(&d_c, C * 4, s)); OCK(dmalloc(&d_v, C * 4, s));
+  OCK(dmalloc(&d_x, C * 4, s));
+  OCK(dmalloc(&lr, C * 4, s)); OCK(dmalloc(&lc, C * 4, s)); OCK(dmalloc(&vv, C * 4, s));
+  OCK(dmalloc(&ord, C * 4, s)); OCK(dmalloc(&gord, C * 4, s)); OCK(dmalloc(&d_bad, 8, s));
+  if (ctx->packed) OCK(dmalloc(&rec, C * 4, s));
+  const int grid = ctx->num_sms * 8;
+  for (int k = 0; k < nch; ++k) {
+    const int64_t cnt = chunk_cnt[k], base = chunk_base[k];
+    if (cnt == 0) continue;
+    OCK(cudaMemcpyAsync(d_r, br.data() + base, cnt * 4, cudaMemcpyHostToDevice, s));
+    OCK(cudaMemcpyAsync(d_c, bc.data() + base, cnt * 4, cudaMemcpyHostToDevice, s));
+    OCK(cudaMemcpyAsync(d_v, bv.data() + base, cnt * 4, cudaMemcpyHostToDevice, s));
+    OCK(cudaMemcpyAsync(d_x, bx.data() + base, cnt * 4, cudaMemcpyHostToDevice, s));
+    OCK(cudaMemsetAsync(d_bad, 0xFF, 8, s));
+    OCK(dmalloc(&ka, (size_t)cnt * 8, s));  // the sort swaps buffers: per chunk
+    OCK(dmalloc(&ia, (size_t)cnt * 4, s));
+    // the chunk index rides in the key's spare low bits when they suffice
+    // (then the fp32 value is the payload); else the payload is the index
+    const int ib = cnt > 1 ? bits_for((uint64_t)cnt - 1) : 0;
+    const bool embed = total_bits + ib <= 64;
+    const int ibits = embed ? ib : 0;
+    make_keys<int32_t><<<grid, 256, 0, s>>>(d_r, d_c, cnt, n, m, rbase, rextra, cbase, cextra,
+                                            J, rbits, cbits, ibits, embed ? d_v : nullptr, ka,
+                                            ia, d_bad);
+    OCK(cudaGetLastError());
+    // stable sort on the (block, row, col) bits above the embedded index
+    uint64_t* kk = ka;
+    uint32_t* ii = ia;
+    rc = sort_pairs_device(ctx, &kk, &ii, cnt, total_bits, ibits);
+    if (rc) { cleanup(); return rc; }
+    ka = kk;
+    ia = ii;
+    if (embed)
+      decode_embedded<<<grid, 256, 0, s>>>(ka, ia, cnt, ibits, cbits, (1ull << rbits) - 1,
+                                           (1ull << cbits) - 1, lr, lc, vv, ord);
+    else
+      decode<float><<<grid, 256, 0, s>>>(ka, ia, d_v, cnt, cbits, (1ull << rbits) - 1,
+                                         (1ull << cbits) - 1, lr, lc, vv, nullptr, ord);
+    pack_and_order<<<grid, 256, 0, s>>>(lr, lc, ord, d_x, cnt, cbits, ctx->packed ? rec : nullptr,
+                                        gord);
+    OCK(cudaGetLastError());
+    free_dev(ka, s);
+    free_dev(ia, s);
+    // blocks of this chunk, flat order = their order in the sorted chunk
+    int64_t lo = 0;
+    for (int b = chunk_b0[k] * J; b < chunk_b0[k + 1] * J; ++b) {
+      const int64_t bc_ = bcount[b], dst = ctx->h_pos[b];
+      if (bc_ > 0) {
+        OCK(cudaMemcpyAsync(ctx->h_lrow + dst, (ctx->packed ? rec : lr) + lo, bc_ * 4,
+                            cudaMemcpyDeviceToHost, s));
+        if (!ctx->packed)
+          OCK(cudaMemcpyAsync(ctx->h_lcol + dst, lc + lo, bc_ * 4, cudaMemcpyDeviceToHost, s));
+        OCK(cudaMemcpyAsync(ctx->h_val + dst, vv + lo, bc_ * 4, cudaMemcpyDeviceToHost, s));
+        OCK(cudaMemcpyAsync(ctx->h_order + dst, gord + lo, bc_ * 4, cudaMemcpyDeviceToHost, s));
+      }
+      lo += bc_;
+    }
+    OCK(cudaStreamSynchronize(s));  // the chunk buffers are reused by the next chunk
+  }
+  cleanup();
+#undef OCK
+  prof_mark(ctx, "ooc: device chunks");
+  ctx->partitioned = true;
+  ctx->streaming = true;
+  rc = stream_slots(ctx, slot_ratings, nslots);
+  if (rc) return rc;
+  ctx->ooc_chunks = nch;
   return BGMF_OK;
 }
 

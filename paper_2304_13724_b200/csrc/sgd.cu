@@ -1728,7 +1728,7 @@ int run_step_converge_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batc
   std::vector<int64_t> conv((size_t)2 * nb);
   for (int t = 0; t < nbatch; ++t) {
     const int q0 = batch_off[t], q1 = batch_off[t + 1];
-    if (use_ordered(c, plan, q0, q1)) {
+    if (use_ordered(c, plan, q0, q1, true)) {
       // the whole per-block converge loop on the device (ordered.cu)
       const int capi = cap > INT32_MAX ? INT32_MAX : (int)cap;
       int rc = run_batch_ordered(c, plan, q0, q1, 0, capi, (float)alpha, (float)beta, true, tol);

@@ -120,6 +120,11 @@ int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
   c->d_lrow = c->d_lcol = nullptr;
   c->d_val = nullptr;
   c->d_order = nullptr;
+  return stream_slots(c, slot_ratings, nslots);
+}
+
+// The device slot ring and the copy stream of the streaming path.
+int stream_slots(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
   c->slot_cap = slot_ratings;
   c->nslots = nslots;
   for (int i = 0; i < nslots; ++i) {

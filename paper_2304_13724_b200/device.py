@@ -152,6 +152,24 @@ class Engine:
         """Partition on the device.  ``row_range=(lo, hi)`` keeps only the
         entries with lo <= row < hi (a multi-GPU rank's shard)."""
         rows, cols, values = N.i64(rows), N.i64(cols), N.f64(values)
+        budget = self.options.device_rating_budget
+        if (budget is not None and row_range is None and not self.options.exact
+                and 12 * len(rows) > budget):
+            # out-of-core: the partition itself stays under the budget (row
+            # blocks in chunks straight into the pinned streaming layout)
+            slots = self.options.stream_slots
+            self._check(self._L.bgmf_partition_ooc(
+                self._h, N.ptr(rows, N._i64p), N.ptr(cols, N._i64p), N.ptr(values, N._f64p),
+                len(rows), n, m, grid_i, grid_j, int(budget), int(budget // (12 * slots)),
+                slots), data_error=data_error)
+            self.I, self.J, self.n, self.m = grid_i, grid_j, n, m
+            off = np.zeros(grid_i * grid_j + 1, np.int64)
+            self._check(self._L.bgmf_partition_export(self._h, N.ptr(off, N._i64p), None, None,
+                                                      None))
+            self.offsets = off
+            self.nnz = int(off[-1])
+            self.streaming = True
+            return
         if row_range is None:
             self._check(self._L.bgmf_partition(
                 self._h, N.ptr(rows, N._i64p), N.ptr(cols, N._i64p), N.ptr(values, N._f64p),
@@ -167,7 +185,6 @@ class Engine:
         self.offsets = off
         self.nnz = int(off[-1])
         self.streaming = False
-        budget = self.options.device_rating_budget
         if budget is not None and 12 * self.nnz > budget:
             slots = self.options.stream_slots
             self.stream(int(budget // (12 * slots)), slots)
@@ -176,6 +193,12 @@ class Engine:
         """Out-of-core mode: ratings to pinned host memory, `nslots` device slots."""
         self._check(self._L.bgmf_stream_ratings(self._h, int(slot_ratings), int(nslots)))
         self.streaming = True
+
+    def mem_stats(self, reset: bool = False) -> tuple[int, int]:
+        """(device pool bytes in use, high-water mark since the last reset)."""
+        out = np.zeros(2, np.int64)
+        self._check(self._L.bgmf_mem_stats(self._h, N.ptr(out, N._i64p), int(reset)))
+        return int(out[0]), int(out[1])
 
     def streamed_bytes(self) -> float:
         out = ctypes.c_double()

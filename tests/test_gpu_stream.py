@@ -102,3 +102,58 @@ def test_stream_converge_schedule_matches_oracle(tol):
     assert dtr.max() <= TOL
     assert all(abs(a.inner_iters - b["inner_iters"]) <= 1 for a, b in zip(res.trace, otr))
     assert all(s.inner_iters >= 1 for s in res.trace)
+
+
+@pytest.mark.parametrize("budget_ratings", [3_000, 9_000, 19_000])
+def test_out_of_core_partition_bit_identical(budget_ratings):
+    """bgmf_partition_ooc (row blocks in chunks under the device budget,
+    straight into the pinned streaming layout) yields exactly the in-core
+    partition: offsets, order, local rows and cols -- the reference's lexsort
+    order, reference partition.py:112-136."""
+    n, m, nnz, P = 3000, 2000, 60_000, 6
+    g = np.random.default_rng(budget_ratings)
+    cells = g.choice(n * m, nnz, replace=False)
+    r, c = np.divmod(cells, m)
+    r[::97] = r[::89][: len(r[::97])]  # some duplicates
+    v = np.clip(np.rint(3 + g.normal(0, 1, nnz)), 1, 5)
+    ref = bm.Engine()
+    ref.partition(r, c, v, n, m, P, P)
+    want = ref.export_partition()
+    ref.close()
+    eng = bm.Engine(bm.EngineOptions(device_rating_budget=12 * budget_ratings * 3, stream_slots=3))
+    eng.partition(r, c, v, n, m, P, P)
+    assert eng.streaming
+    got = eng.export_partition()
+    eng.close()
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
+
+
+def test_out_of_core_partition_peak_memory():
+    """The device pool's high-water mark of an out-of-core partition stays
+    within the budget (plus the slot ring and a few MB of fixed scratch),
+    ~an order of magnitude under the in-core partition of the same data."""
+    n, m, nnz, P = 200_000, 50_000, 4_000_000, 16
+    g = np.random.default_rng(7)
+    cells = g.choice(n * m, nnz, replace=False)
+    r, c = np.divmod(cells, m)
+    v = np.clip(np.rint(3 + g.normal(0, 1, nnz)), 1, 5)
+    inc = bm.Engine()
+    inc.mem_stats(reset=True)
+    base, _ = inc.mem_stats()
+    inc.partition(r, c, v, n, m, P, P)
+    _, high_in = inc.mem_stats()
+    inc.close()
+    budget = 16 << 20  # 16 MB: ~250k ratings of chunk temporaries, 1/16 of the data
+    eng = bm.Engine(bm.EngineOptions(device_rating_budget=budget, stream_slots=3))
+    eng.mem_stats(reset=True)
+    base2, _ = eng.mem_stats()
+    eng.partition(r, c, v, n, m, P, P)
+    _, high = eng.mem_stats()
+    eng.close()
+    slots = 3 * (budget // 36) * 8
+    print(f"in-core partition peak {(high_in - base) / 2**20:.1f} MB, out-of-core "
+          f"{(high - base2) / 2**20:.1f} MB (budget {budget / 2**20:.0f} MB + slots "
+          f"{slots / 2**20:.1f} MB)")
+    assert high - base2 <= budget + slots + (4 << 20)
+    assert high - base2 < (high_in - base) / 4
