@@ -238,6 +238,9 @@ int download_rows(bgmf_ctx* c, const float* d, double* h, int64_t rows, int k, i
 // process-wide cache of small pinned host buffers (hostio.cu)
 cudaError_t pinned_alloc(void** p, size_t bytes);
 void pinned_free(void* p);
+// GB-sized pinned arrays: THP-backed + cudaHostRegister; freed off-thread
+cudaError_t big_pinned_alloc(void** p, size_t bytes);
+void big_pinned_free(void* p);
 int upload_rows(bgmf_ctx* c, const double* h, float* d, int64_t rows, int k, int kp);
 
 // synth.cu (benchmark / test input generator)

@@ -19,6 +19,7 @@
 
 #include <map>
 #include <mutex>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -128,6 +129,69 @@ void pinned_free(void* p) {
     if (it != pc.size_.end()) pc.size_.erase(it);
   }
   cudaFreeHost(p);
+}
+
+// Large pinned host arrays (the out-of-core layout: GBs).  cudaMallocHost
+// pins 4 KiB pages one by one (~2.5 GB/s measured for C5's 24 GB,
+// profiles/r02_*); instead: anonymous memory advised MADV_HUGEPAGE, faulted
+// in by all host threads (one write per 2 MiB page), then cudaHostRegister.
+// Released on a detached thread: unpinning GBs costs seconds the caller
+// does not need to wait for.
+namespace {
+struct BigPinned {
+  std::mutex mu;
+  std::unordered_map<void*, std::pair<void*, size_t>> maps;  // user ptr -> (mmap base, len)
+};
+BigPinned& big_pinned() {
+  static BigPinned* p = new BigPinned;
+  return *p;
+}
+}  // namespace
+
+cudaError_t big_pinned_alloc(void** out, size_t bytes) {
+  const size_t huge = size_t(2) << 20;
+  const size_t len = (bytes + 2 * huge - 1) / huge * huge;
+  void* base = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (base == MAP_FAILED) return cudaErrorMemoryAllocation;
+  char* p = reinterpret_cast<char*>(((uintptr_t)base + huge - 1) / huge * huge);
+  const size_t span = (bytes + huge - 1) / huge * huge;
+  madvise(p, span, MADV_HUGEPAGE);
+  const int64_t pages = (int64_t)(span / huge);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < pages; ++i) p[i * (int64_t)huge] = 0;
+  cudaError_t e = cudaHostRegister(p, span, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    munmap(base, len);
+    return e;
+  }
+  {
+    std::lock_guard<std::mutex> lk(big_pinned().mu);
+    big_pinned().maps[p] = {base, len};
+  }
+  *out = p;
+  return cudaSuccess;
+}
+
+// Frees a big_pinned_alloc buffer (asynchronously) or a cudaMallocHost one.
+void big_pinned_free(void* p) {
+  if (!p) return;
+  std::pair<void*, size_t> m{nullptr, 0};
+  {
+    std::lock_guard<std::mutex> lk(big_pinned().mu);
+    auto it = big_pinned().maps.find(p);
+    if (it != big_pinned().maps.end()) {
+      m = it->second;
+      big_pinned().maps.erase(it);
+    }
+  }
+  if (!m.first) {
+    cudaFreeHost(p);
+    return;
+  }
+  std::thread([p, m]() {
+    cudaHostUnregister(p);
+    munmap(m.first, m.second);
+  }).detach();
 }
 
 // Dataset upload for the partitioner (partition.cu): int64 indices narrowed

@@ -32,10 +32,10 @@ void stream_free(bgmf_ctx* c) {
   for (auto e : c->ev_consumed) cudaEventDestroy(e);
   c->s_lrow.clear(); c->s_lcol.clear(); c->s_val.clear();
   c->ev_copied.clear(); c->ev_consumed.clear();
-  if (c->h_lrow) cudaFreeHost(c->h_lrow);
-  if (c->h_lcol) cudaFreeHost(c->h_lcol);
-  if (c->h_val) cudaFreeHost(c->h_val);
-  if (c->h_order) cudaFreeHost(c->h_order);
+  big_pinned_free(c->h_lrow);
+  big_pinned_free(c->h_lcol);
+  big_pinned_free(c->h_val);
+  big_pinned_free(c->h_order);
   c->h_lrow = c->h_lcol = nullptr;
   c->h_val = nullptr;
   c->h_order = nullptr;
@@ -91,10 +91,10 @@ int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
     pos += c->h_offsets[b + 1] - c->h_offsets[b];
   }
   const size_t N = (size_t)(c->nnz > 0 ? c->nnz : 1);
-  BGMF_CK(c, cudaMallocHost(&c->h_lrow, N * 4));
-  if (!c->packed) BGMF_CK(c, cudaMallocHost(&c->h_lcol, N * 4));
-  BGMF_CK(c, cudaMallocHost(&c->h_val, N * 4));
-  BGMF_CK(c, cudaMallocHost(&c->h_order, N * 4));
+  BGMF_CK(c, big_pinned_alloc((void**)&c->h_lrow, N * 4));
+  if (!c->packed) BGMF_CK(c, big_pinned_alloc((void**)&c->h_lcol, N * 4));
+  BGMF_CK(c, big_pinned_alloc((void**)&c->h_val, N * 4));
+  BGMF_CK(c, big_pinned_alloc((void**)&c->h_order, N * 4));
   if (c->packed && c->nnz > 0) {  // pack in place of the (no longer needed) lrow
     int32_t* rec = nullptr;
     BGMF_CK(c, dmalloc(&rec, N * 4, c->stream));
