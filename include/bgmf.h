@@ -196,10 +196,13 @@ int bgmf_stream_ratings(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
  * blocks in chunks, each partitioned on the device exactly as
  * bgmf_partition does, straight into the pinned streaming layout; then
  * nslots device slots of slot_ratings ratings.  Same ordering, offsets and
- * errors as bgmf_partition (reference partition.py:112-136). */
+ * errors as bgmf_partition (reference partition.py:112-136).  Only rows in
+ * [row_lo, row_hi) are kept (row_hi < 0: n) -- a ring rank's shard, as
+ * bgmf_partition_rows; every entry is still range-checked. */
 int bgmf_partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                        const double* vals, int64_t nnz, int64_t n, int64_t m, int grid_i,
-                       int grid_j, int64_t device_budget, int64_t slot_ratings, int nslots);
+                       int grid_j, int64_t device_budget, int64_t slot_ratings, int nslots,
+                       int64_t row_lo, int64_t row_hi);
 /* Device memory of the stream-ordered pool every context allocates from:
  * out2 = {bytes in use now, high-water mark}; reset = 1 restarts the mark. */
 int bgmf_mem_stats(bgmf_ctx* ctx, int64_t* out2, int reset);

@@ -78,7 +78,8 @@ SIGNATURES = {
     "bgmf_kernel_stats": (_i, [_ctx, _f64p, _i]),
     "bgmf_stream_ratings": (_i, [_ctx, _l, _i]),
     "bgmf_mem_stats": (_i, [_ctx, _i64p, _i]),
-    "bgmf_partition_ooc": (_i, [_ctx, _i64p, _i64p, _f64p, _l, _l, _l, _i, _i, _l, _l, _i]),
+    "bgmf_partition_ooc": (_i, [_ctx, _i64p, _i64p, _f64p, _l, _l, _l, _i, _i, _l, _l, _i, _l,
+                                _l]),
     "bgmf_stream_stats": (_i, [_ctx, _f64p]),
     "bgmf_sgd_sweeps": (_i, [_i64p, _i64p, _f64p, _l, _f64p, _l, _f64p, _l, _i, _d, _d, _i,
                              _f64p, _f64p, _i64p, _i64p]),

@@ -148,6 +148,7 @@ struct bgmf_ctx {
   cudaStream_t copy_stream = nullptr;
   double h2d_bytes = 0;                  // streamed this context (stats)
   int ooc_chunks = 0;                    // chunks of the last out-of-core partition
+  int64_t piece_seq = 0;                 // pieces streamed by asynchronous steps (slot rotation)
 
   // ordered sweep (ordered.cu): column ranks, row pointers, row flags
   int ord_mode = -1;                     // 1: ordered where possible, 0: never, -1: auto
@@ -303,11 +304,13 @@ int stream_slots(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
 // bytes of HBM straight into the pinned streaming layout
 int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const double* vals,
                   int64_t nnz, int64_t n, int64_t m, int I, int J, int64_t budget,
-                  int64_t slot_ratings, int nslots);
+                  int64_t slot_ratings, int nslots, int64_t row_lo = 0, int64_t row_hi = -1);
 void stream_free(bgmf_ctx* ctx);
 int stream_export(bgmf_ctx* ctx, int64_t* order, int32_t* lrows, int32_t* lcols);
 int run_step_stream(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off, int nbatch,
                     int iters, float alpha, float beta);
+int stream_batch(bgmf_ctx* ctx, const int32_t* plan, const int32_t* batch_off, int nbatch,
+                 int iters, float alpha, float beta, int pos0);
 // single-block exact kernel used by the stateless drop-ins
 int block_exact(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const double* vals,
                 int64_t count, double* u, int64_t u_rows, double* v, int64_t v_rows, int k,

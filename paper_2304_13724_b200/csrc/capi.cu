@@ -584,13 +584,14 @@ int bgmf_holdout_sse(bgmf_ctx* c, double* sse_out) {
 
 int bgmf_partition_ooc(bgmf_ctx* c, const int64_t* rows, const int64_t* cols,
                        const double* vals, int64_t nnz, int64_t n, int64_t m, int grid_i,
-                       int grid_j, int64_t device_budget, int64_t slot_ratings, int nslots) {
+                       int grid_j, int64_t device_budget, int64_t slot_ratings, int nslots,
+                       int64_t row_lo, int64_t row_hi) {
   if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
   cudaSetDevice(c->device);
   dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
   return partition_ooc(c, rows, cols, vals, nnz, n, m, grid_i, grid_j, device_budget,
-                       slot_ratings, nslots);
+                       slot_ratings, nslots, row_lo, row_hi);
 }
 
 int bgmf_mem_stats(bgmf_ctx* c, int64_t* out2, int reset) {

@@ -630,7 +630,10 @@ constexpr int64_t kChunkBytes = 64;  // device bytes per rating while a chunk is
 
 int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const double* vals,
                   int64_t nnz, int64_t n, int64_t m, int I, int J, int64_t budget,
-                  int64_t slot_ratings, int nslots) {
+                  int64_t slot_ratings, int nslots, int64_t row_lo, int64_t row_hi) {
+  if (row_hi < 0) row_hi = n;
+  if (row_lo < 0 || row_lo > row_hi || row_hi > n)
+    return fail(ctx, BGMF_ERR_ARG, "row range must satisfy 0 <= row_lo <= row_hi <= n");
   if (n < 1 || m < 1 || n > INT32_MAX || m > INT32_MAX)
     return fail(ctx, BGMF_ERR_ARG, "n and m must be in [1, 2^31)");
   if (I < 1 || I > n) return fail(ctx, BGMF_ERR_ARG, "grid_i must be in [1, n]");
@@ -685,6 +688,7 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
     for (int64_t i = lo; i < hi; ++i) {
       const int64_t r = rows[i], c = cols[i];
       if (r < 0 || r >= n || c < 0 || c >= m) { tbad[t] = i; break; }
+      if (r < row_lo || r >= row_hi) continue;  // another rank's rows (checked, not kept)
       ++cnt[slab(r, rbase, rextra) * J + slab(c, cbase, cextra)];
     }
   }
@@ -701,6 +705,8 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
     for (int b = 0; b < nb; ++b) bcount[b] += tcount[(size_t)t * nb + b];
   ctx->h_offsets.assign(nb + 1, 0);
   for (int b = 0; b < nb; ++b) ctx->h_offsets[b + 1] = ctx->h_offsets[b] + bcount[b];
+  const int64_t kept = ctx->h_offsets[nb];  // entries of rows [row_lo, row_hi)
+  ctx->nnz = kept;
   int64_t max_block = 0;
   for (int b = 0; b < nb; ++b) max_block = std::max(max_block, bcount[b]);
   if (slot_ratings < max_block || slot_ratings < 1)
@@ -738,7 +744,7 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   // in by the host threads, and the chunk uploads below are then DMA at full
   // PCIe rate (a std::vector's single-threaded zero-fill of C5's 32 GB and
   // pageable uploads cost 13 s and 3.5 s)
-  const size_t N = (size_t)(nnz > 0 ? nnz : 1);
+  const size_t N = (size_t)(kept > 0 ? kept : 1);
   struct Bucket {
     int32_t* r = nullptr;
     int32_t* c = nullptr;
@@ -790,6 +796,7 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
     };
     for (int64_t i = lo; i < hi; ++i) {
       const int64_t r = rows[i];
+      if (r < row_lo || r >= row_hi) continue;
       const int k = chunk_of[slab(r, rbase, rextra)];
       const size_t j = (size_t)k * WC + fill[k]++;
       wr[j] = (int32_t)r;

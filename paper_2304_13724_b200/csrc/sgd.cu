@@ -1188,7 +1188,6 @@ int64_t fast_groups(bgmf_ctx* c) { return sweep_groups(c, shape_for(c->kp)); }
 // keeps the reference's "first in plan order" rule.
 int step_begin(bgmf_ctx* c, int max_blocks) {
   if (c->exact) return fail(c, BGMF_ERR_STATE, "asynchronous steps are fast-mode only");
-  if (c->streaming) return fail(c, BGMF_ERR_STATE, "asynchronous steps do not stream");
   // each submitted block takes a sweep and an SSE work entry; the table is
   // split in two halves used by alternate steps (see ws_done)
   const size_t need = 2 * (size_t)(max_blocks > 0 ? max_blocks : 1);
@@ -1232,6 +1231,13 @@ static int mark_half_done(bgmf_ctx* c) {
 int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in, int nbatch_in,
                int iters, float alpha, float beta) {
   if (!c->in_step) return fail(c, BGMF_ERR_STATE, "bgmf_step_begin has not been called");
+  if (c->streaming) {  // out-of-core rank: the batch's pieces through the slot ring
+    const int pos0s = (int)c->submitted.size() - c->step_pos0;
+    int rc = stream_batch(c, plan, batch_off_in, nbatch_in, iters, alpha, beta, pos0s);
+    if (rc) return rc;
+    for (int q = 0; q < batch_off_in[nbatch_in]; ++q) c->submitted.push_back(plan[q]);
+    return BGMF_OK;
+  }
   const std::vector<int32_t> waves = l2_waves(c, plan, batch_off_in, nbatch_in);
   const int32_t* batch_off = waves.data();
   const int nbatch = (int)waves.size() - 1;

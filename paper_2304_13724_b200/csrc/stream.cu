@@ -181,10 +181,11 @@ struct Piece {
 // Cut every batch into pieces that fit a slot (and one L2 wave); slot-relative
 // work items into h_work[0, *w).  Pieces never span batches.
 static int build_pieces(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
-                        std::vector<Piece>& pieces, int* w_out) {
+                        std::vector<Piece>& pieces, int* w_out, int w_base = 0, int pos0 = 0,
+                        int64_t slot_seq = 0) {
   const int nb = c->I * c->J;
   const int64_t groups = fast_groups(c);
-  int w = 0;
+  int w = w_base;
   for (int t = 0; t < nbatch; ++t) {
     int q = batch_off[t];
     while (q < batch_off[t + 1]) {
@@ -210,7 +211,7 @@ static int build_pieces(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_o
       int64_t cl = (fill + slots - 1) / slots;
       if (cl < c->min_chunk) cl = c->min_chunk;
       cl = stagger_chunk(cl, c->stagger);
-      Piece pc{w, 0, 0, (int)(pieces.size() % c->nslots), 0.0};
+      Piece pc{w, 0, 0, (int)((slot_seq + (int64_t)pieces.size()) % c->nslots), 0.0};
       int64_t off = 0;
       for (int qq = q; qq < q_end; ++qq) {
         const int b = plan[qq];
@@ -225,7 +226,7 @@ static int build_pieces(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_o
         bw.chunk_len = (int32_t)bl;
         bw.first_chunk = pc.chunks;
         bw.block_id = b;
-        bw.pos = qq;
+        bw.pos = pos0 + qq;
         pc.chunks += (int)((cnt + bl - 1) / bl);
         pc.ratings += (double)cnt;
         off += cnt;
@@ -308,6 +309,68 @@ int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, 
   BGMF_CK(c, cudaStreamSynchronize(s));
   cudaEventDestroy(ready);
   if (c->timing) harvest_timing(c);
+  return BGMF_OK;
+}
+
+// One batch of an asynchronous step (the multi-GPU ring, sgd.cu step_batch)
+// on a streaming context: the batch's pieces go through the slot ring with the
+// copy stream running ahead, nothing waits on the host.  Work items go to the
+// step's reserved work-table range at c->w_cursor; slots rotate with a
+// context-wide piece counter, and a piece always waits until its slot's
+// previous occupant has been swept (ev_consumed; a no-op for a fresh slot).
+int stream_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
+                 int iters, float alpha, float beta, int pos0) {
+  cudaStream_t s = c->stream, cs = c->copy_stream;
+  std::vector<Piece> pieces;
+  int w_end = c->w_cursor;
+  int rc = build_pieces(c, plan, batch_off, nbatch, pieces, &w_end, c->w_cursor, pos0,
+                        c->piece_seq);
+  if (rc) return rc;
+  if (w_end > c->w_limit)
+    return fail(c, BGMF_ERR_ARG, "more blocks than reserved by bgmf_step_begin");
+  if (w_end > c->w_cursor)
+    BGMF_CK(c, cudaMemcpyAsync(c->d_work + c->w_cursor, c->h_work + c->w_cursor,
+                               sizeof(BlockWork) * (w_end - c->w_cursor), cudaMemcpyHostToDevice,
+                               s));
+  for (const Piece& pc : pieces) {
+    const int sl = pc.slot;
+    BGMF_CK(c, cudaStreamWaitEvent(cs, c->ev_consumed[sl], 0));
+    int64_t run_dst = 0, run_src = -1, run_cnt = 0;
+    auto copy_run = [&](int64_t dst, int64_t src, int64_t cnt) -> int {
+      BGMF_CK(c, cudaMemcpyAsync(c->s_lrow[sl] + dst, c->h_lrow + src, cnt * 4,
+                                 cudaMemcpyHostToDevice, cs));
+      if (!c->packed)
+        BGMF_CK(c, cudaMemcpyAsync(c->s_lcol[sl] + dst, c->h_lcol + src, cnt * 4,
+                                   cudaMemcpyHostToDevice, cs));
+      BGMF_CK(c, cudaMemcpyAsync(c->s_val[sl] + dst, c->h_val + src, cnt * 4,
+                                 cudaMemcpyHostToDevice, cs));
+      c->h2d_bytes += (c->packed ? 8.0 : 12.0) * (double)cnt;
+      return BGMF_OK;
+    };
+    for (int i = 0; i < pc.nw && !rc; ++i) {
+      const BlockWork& bw = c->h_work[pc.w0 + i];
+      const int64_t src = c->h_pos[bw.block_id];
+      const int64_t cnt = bw.end - bw.begin;
+      if (run_src >= 0 && src == run_src + run_cnt && bw.begin == run_dst + run_cnt) {
+        run_cnt += cnt;
+        continue;
+      }
+      if (run_src >= 0) rc = copy_run(run_dst, run_src, run_cnt);
+      run_dst = bw.begin;
+      run_src = src;
+      run_cnt = cnt;
+    }
+    if (!rc && run_src >= 0) rc = copy_run(run_dst, run_src, run_cnt);
+    if (rc) return rc;
+    BGMF_CK(c, cudaEventRecord(c->ev_copied[sl], cs));
+    BGMF_CK(c, cudaStreamWaitEvent(s, c->ev_copied[sl], 0));
+    rc = launch_piece(c, c->d_work + pc.w0, pc.nw, pc.chunks, c->s_lrow[sl], c->s_lcol[sl],
+                      c->s_val[sl], iters, alpha, beta, pc.ratings, c->packed ? c->cbits : -1);
+    if (rc) return rc;
+    BGMF_CK(c, cudaEventRecord(c->ev_consumed[sl], s));
+  }
+  c->piece_seq += (int64_t)pieces.size();
+  c->w_cursor = w_end;
   return BGMF_OK;
 }
 

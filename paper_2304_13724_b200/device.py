@@ -153,15 +153,16 @@ class Engine:
         entries with lo <= row < hi (a multi-GPU rank's shard)."""
         rows, cols, values = N.i64(rows), N.i64(cols), N.f64(values)
         budget = self.options.device_rating_budget
-        if (budget is not None and row_range is None and not self.options.exact
-                and 12 * len(rows) > budget):
+        if (budget is not None and not self.options.exact
+                and 12 * self._kept(rows, row_range) > budget):
             # out-of-core: the partition itself stays under the budget (row
             # blocks in chunks straight into the pinned streaming layout)
             slots = self.options.stream_slots
             self._check(self._L.bgmf_partition_ooc(
                 self._h, N.ptr(rows, N._i64p), N.ptr(cols, N._i64p), N.ptr(values, N._f64p),
                 len(rows), n, m, grid_i, grid_j, int(budget), int(budget // (12 * slots)),
-                slots), data_error=data_error)
+                slots, *(row_range if row_range is not None else (0, -1))),
+                data_error=data_error)
             self.I, self.J, self.n, self.m = grid_i, grid_j, n, m
             off = np.zeros(grid_i * grid_j + 1, np.int64)
             self._check(self._L.bgmf_partition_export(self._h, N.ptr(off, N._i64p), None, None,
@@ -188,6 +189,14 @@ class Engine:
         if budget is not None and 12 * self.nnz > budget:
             slots = self.options.stream_slots
             self.stream(int(budget // (12 * slots)), slots)
+
+    @staticmethod
+    def _kept(rows, row_range) -> int:
+        """Ratings a (row-ranged) partition keeps -- decides out-of-core mode."""
+        if row_range is None:
+            return len(rows)
+        lo, hi = row_range
+        return int(np.count_nonzero((rows >= lo) & (rows < hi)))
 
     def stream(self, slot_ratings: int, nslots: int = 3):
         """Out-of-core mode: ratings to pinned host memory, `nslots` device slots."""

@@ -391,7 +391,9 @@ class GpuShard:
             raise ValueError("the multi-GPU ring runs the fast kernels only; exact (fp64, "
                              "reference-order) training is single-GPU: train_blocked")
         opts = EngineOptions(exact=False, min_chunk=opts.min_chunk, device=device,
-                             timing=opts.timing, warps_per_sm=opts.warps_per_sm)
+                             timing=opts.timing, warps_per_sm=opts.warps_per_sm,
+                             device_rating_budget=opts.device_rating_budget,
+                             stream_slots=opts.stream_slots, ordered=opts.ordered)
         self.eng = Engine(opts, stream=self.stream.cuda_stream)
         # this rank's U row-blocks: the upload keeps only their ratings
         # (bgmf_partition_rows), no host-side gather of the dataset

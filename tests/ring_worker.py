@@ -31,9 +31,16 @@ def main(out_path: str, case: str) -> None:
         json.dump(err, open(f"{out_path}.{os.environ['RANK']}", "w"))
         return
     sched = {"const": bm.Constant(1), "inc": bm.IncreasingEvery(2, 3),
-             "converge": bm.ConvergeEachBlock(0.5), "holdout": bm.Constant(1)}[case]
+             "converge": bm.ConvergeEachBlock(0.5), "holdout": bm.Constant(1),
+             "stream": bm.Constant(1), "stream_inc": bm.IncreasingEvery(2, 3)}[case]
     cfg = bm.TrainConfig(k=32, outer_steps=4, grid_i=8, grid_j=8, inner_schedule=sched)
-    model, trace, stop = D.train_blocked_distributed(d, cfg, test, early_stop=False)
+    # "stream*": every rank out of core -- its row shard partitioned in chunks
+    # under a device budget of ~40k ratings into pinned memory, streamed
+    # through a 3-slot ring inside the asynchronous ring steps
+    opts = (bm.EngineOptions(device_rating_budget=12 * 40_000, stream_slots=3)
+            if case.startswith("stream") else None)
+    model, trace, stop = D.train_blocked_distributed(d, cfg, test, early_stop=False,
+                                                     options=opts)
     if int(os.environ["RANK"]) == 0:
         json.dump({"train": [s.train_rmse for s in trace],
                    "test": [s.test_rmse for s in trace],

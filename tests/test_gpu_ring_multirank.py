@@ -54,7 +54,7 @@ def _oracle(case: str):
         d, te = bm.split(d, 0.2, seed=3)
         test = (te.rows, te.cols, te.values)
     sched = {"const": "const:1", "inc": "inc:2,3", "converge": "converge:0.5",
-             "holdout": "const:1"}[case]
+             "holdout": "const:1", "stream": "const:1", "stream_inc": "inc:2,3"}[case]
     _, _, otr, _ = O.train_blocked(d.n, d.m, d.rows, d.cols, d.values, k=32, outer_steps=4,
                                    grid_i=8, grid_j=8, schedule=sched, early_stop=False,
                                    test=test, nthreads=8)
@@ -64,10 +64,13 @@ def _oracle(case: str):
 @pytest.mark.parametrize("world,case,transport",
                          [(2, "const", "peer"), (4, "const", "peer"), (2, "inc", "peer"),
                           (2, "converge", "peer"), (3, "holdout", "peer"),
-                          (2, "const", "dist"), (3, "holdout", "dist")])
+                          (2, "const", "dist"), (3, "holdout", "dist"),
+                          (2, "stream", "peer"), (3, "stream_inc", "peer"),
+                          (2, "stream", "dist")])
 def test_ring_ranks_share_one_gpu_match_oracle(world, case, transport, tmp_path):
     """transport "peer": V moves through IPC-mapped peer memory (the default);
-    "dist": torch.distributed P2P (staged through the host on gloo)."""
+    "dist": torch.distributed P2P (staged through the host on gloo).  The
+    "stream*" cases run every rank out of core (C5 on several GPUs)."""
     got = _run(world, case, tmp_path, transport)
     otr = _oracle(case)
     assert np.abs(np.array(got["train"]) - [s["train_rmse"] for s in otr]).max() <= 1e-3
