@@ -163,7 +163,8 @@ struct bgmf_ctx {
   uint32_t* d_obar = nullptr;            // per launched block: two barrier counters
   double* d_opart = nullptr;             // per stage: SSE partial
   int64_t* d_conv = nullptr;             // per block: converge iters_used, capped
-  int ord_auto_blocks = 8;               // auto: ordered below this many blocks per batch
+  double ord_row_split = 1.0;            // auto: ordered when chunks < this many mean rows
+  double ord_col_conc = 1.0;             // auto: ... or > this many groups per V row (<= 0: off)
   std::map<uint64_t, int> ord_cap;       // (kp, smem) -> co-resident CTAs
 
   // timing
@@ -277,6 +278,8 @@ int train_sse_fast(bgmf_ctx* ctx, double* out);
 int train_sse_exact(bgmf_ctx* ctx, double* out);
 int ensure_step_scratch(bgmf_ctx* ctx, size_t nwork);
 int64_t fast_groups(bgmf_ctx* ctx);
+bool chunked_splits_rows(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1, double factor,
+                         double max_col_conc);
 int launch_piece(bgmf_ctx* ctx, const BlockWork* d_work, int nwork, int chunks,
                  const int32_t* lrow, const int32_t* lcol, const float* val, int iters,
                  float alpha, float beta, double ratings, int cbits);
@@ -292,6 +295,7 @@ void order_release(bgmf_ctx* ctx);
 int ensure_order_index(bgmf_ctx* ctx);
 bool ordered_block_ok(bgmf_ctx* ctx, int b);
 bool use_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1, bool converge = false);
+bool order_risky(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1);
 int run_batch_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1, int pos_base,
                       int iters, float alpha, float beta, bool conv = false, double tol = 0.0);
 int run_shards_ordered(bgmf_ctx* ctx, const int32_t* r0, const int32_t* r1, int nshards,

@@ -849,15 +849,20 @@ int run_shards_ordered(bgmf_ctx* c, const int32_t* r0, const int32_t* r1, int ns
 // Ordered routing of one batch: mode 1 = every block the kernel can take;
 // -1 (auto) = the same; 0 = never.  All blocks of the batch must qualify.
 // Routing of one batch.  ord_mode 1: ordered whenever every block fits;
-// 0: never; -1 (auto): ordered when it fits and the chunked sweep's
-// concurrency would distort the reference order -- fewer than
-// ord_auto_blocks non-empty blocks in the batch (each block then gets
-// hundreds to thousands of concurrent chunks, rows split across many of
-// them: every fast-mode drift past 1e-3 found by the randomised sweeps,
-// DESIGN.md section 4) or a dense block (> 1/8 of its cells rated: rows share
-// their columns and concurrent chunks collide on every V row).
-bool use_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, bool converge) {
-  if (c->ord_mode == 0 || c->exact || c->streaming) return false;
+// 0: never; -1 (auto): ordered when it fits and the chunked sweep would
+// distort the reference order -- a dense block (> 1/8 of its cells rated:
+// rows share their columns and concurrent chunks collide on every V row),
+// chunks shorter than ord_row_split mean rows of a block, or more than
+// ord_col_conc concurrent groups per V row (chunked_splits_rows).  Every
+// fast-mode drift past 1e-3 in the randomised sweeps
+// was in one of these; C1-C5 single-GPU strata are in none.  Ring ranks set
+// ord_col_conc = 4 (their 2-block launches of C4: ~4 groups per V row,
+// measured within 2e-5 and covered by the ring sweeps).
+// converge: always when it fits.
+// The auto rule's risk test alone (no feasibility): would the chunked sweep
+// of this batch distort the reference order (a dense block, split rows, or
+// too many groups per V row)?
+bool order_risky(bgmf_ctx* c, const int32_t* plan, int q0, int q1) {
   int nonempty = 0;
   bool dense = false;
   for (int q = q0; q < q1; ++q) {
@@ -868,13 +873,21 @@ bool use_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, bool converge
     const int64_t h = c->row_bounds[b / c->J + 1] - c->row_bounds[b / c->J];
     const int64_t w = c->col_bounds[b % c->J + 1] - c->col_bounds[b % c->J];
     dense |= cnt * 8 > h * w;
-    if (!ordered_block_ok(c, b)) return false;
   }
+  return dense || (nonempty > 0 && chunked_splits_rows(c, plan, q0, q1, c->ord_row_split,
+                                                       c->ord_col_conc));
+}
+
+bool use_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, bool converge) {
+  if (c->ord_mode == 0 || c->exact || c->streaming) return false;
+  for (int q = q0; q < q1; ++q)
+    if (c->h_offsets[plan[q] + 1] > c->h_offsets[plan[q]] && !ordered_block_ok(c, plan[q]))
+      return false;
   // ConvergeEachBlock: the per-block loop (sweep, SSE, improvement test)
   // runs on the device only in the ordered kernel, and its stopping
   // decisions then see the reference's sequential trajectory
   if (c->ord_mode > 0 || converge) return true;
-  return nonempty < c->ord_auto_blocks || dense;
+  return order_risky(c, plan, q0, q1);
 }
 
 }  // namespace bgmf

@@ -985,6 +985,11 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
     }
     ranges[t].w0 = w;
     int chunks = 0;
+    // a batch the ordered kernel cannot take although the chunked sweep would
+    // distort the reference order: one chunk (one group, stored order) per block
+    const bool seq = groups > 0 && !sse && !active && c->ord_mode != 0 &&
+                     order_risky(c, plan, batch_off[t], batch_off[t + 1]) &&
+                     !use_ordered(c, plan, batch_off[t], batch_off[t + 1]);
     for (int q = batch_off[t]; q < batch_off[t + 1]; ++q) {
       const int b = plan[q];
       if (active && !(*active)[q]) continue;
@@ -992,7 +997,7 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
       const int64_t cnt = end - beg;
       if (cnt == 0) continue;
       int64_t bl = cnt;
-      if (groups > 0 && !sse) bl = block_chunk(c, b, cnt, cl);
+      if (groups > 0 && !sse && !seq) bl = block_chunk(c, b, cnt, cl);
       else if (groups > 0) bl = std::min(cnt, std::max(cl, kSseMinChunk));
       BlockWork& bw = c->h_work[w++];
       bw.begin = beg;
@@ -1178,6 +1183,42 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in,
 }
 
 int64_t fast_groups(bgmf_ctx* c) { return sweep_groups(c, shape_for(c->kp)); }
+
+// Would the chunked sweep of batch plan[q0 .. q1) distort the reference
+// order beyond what the randomised sweeps showed to be safe?  From the chunk
+// length the sweep would use (build_work / block_chunk), per block: fewer
+// than `factor` mean rows per chunk (groups sweep pieces of the same rows at
+// once, each with a stale copy of u_r merged by red.add), or more than
+// `max_col_conc` concurrent groups per V row.  Every fast-mode drift past
+// 1e-3 the sweeps found was in one of the two.
+bool chunked_splits_rows(bgmf_ctx* c, const int32_t* plan, int q0, int q1, double factor,
+                         double max_col_conc) {
+  const int64_t groups = sweep_groups(c, shape_for(c->kp));
+  int64_t batch_nnz = 0;
+  int nonempty = 0;
+  for (int q = q0; q < q1; ++q) {
+    const int64_t cnt = c->h_offsets[plan[q] + 1] - c->h_offsets[plan[q]];
+    batch_nnz += cnt;
+    nonempty += cnt > 0;
+  }
+  const int64_t slots = groups - nonempty > 0 ? groups - nonempty : 1;
+  const int64_t cl = (batch_nnz + slots - 1) / slots;
+  for (int q = q0; q < q1; ++q) {
+    const int b = plan[q];
+    const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
+    if (cnt == 0) continue;
+    const int64_t bl = block_chunk(c, b, cnt, cl);
+    if (bl >= cnt) continue;  // one chunk: the block is swept sequentially
+    const int64_t h = c->row_bounds[b / c->J + 1] - c->row_bounds[b / c->J];
+    if ((double)bl < factor * (double)cnt / (double)(h > 0 ? h : 1)) return true;
+    // concurrent groups per V row of the block (block_chunk lets blocks with
+    // hundreds of ratings per column run several; max_col_conc <= 0: no cap)
+    const int64_t w = c->col_bounds[b % c->J + 1] - c->col_bounds[b % c->J];
+    const double conc = (double)((cnt + bl - 1) / bl) / (double)(w > 0 ? w : 1);
+    if (max_col_conc > 0 && conc > max_col_conc) return true;
+  }
+  return false;
+}
 
 // ---- asynchronous steps (multi-GPU ring): begin, batches, end ----------
 // The distributed trainer interleaves NCCL V-block moves with the strata of a

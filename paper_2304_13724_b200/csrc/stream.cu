@@ -187,6 +187,12 @@ static int build_pieces(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_o
   const int64_t groups = fast_groups(c);
   int w = w_base;
   for (int t = 0; t < nbatch; ++t) {
+    // the ordered kernel does not stream: where the chunked sweep would
+    // distort the reference order (order_risky) each block is one chunk --
+    // one group walks it in stored order (exact but for the next rating's V
+    // row being read one update early when two consecutive ratings share a
+    // column)
+    const bool seq = c->ord_mode != 0 && order_risky(c, plan, batch_off[t], batch_off[t + 1]);
     int q = batch_off[t];
     while (q < batch_off[t + 1]) {
       int q_end = q;
@@ -217,7 +223,7 @@ static int build_pieces(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_o
         const int b = plan[qq];
         const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
         if (cnt == 0) continue;
-        const int64_t bl = cl < cnt ? cl : cnt;
+        const int64_t bl = seq ? cnt : (cl < cnt ? cl : cnt);
         BlockWork& bw = c->h_work[w++];
         bw.begin = off;
         bw.end = off + cnt;

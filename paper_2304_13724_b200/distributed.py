@@ -395,6 +395,10 @@ class GpuShard:
                              device_rating_budget=opts.device_rating_budget,
                              stream_slots=opts.stream_slots, ordered=opts.ordered)
         self.eng = Engine(opts, stream=self.stream.cuda_stream)
+        # a rank sweeps a stratum's blocks of its own rows (C4 on 8 GPUs: 2
+        # per batch), so the chunked kernel runs more groups per V row than a
+        # whole-stratum launch; csrc/ordered.cu use_ordered
+        self.eng._opt("ord_col_conc", float(os.environ.get("BGMF_RING_COL_CONC", "4")))
         # this rank's U row-blocks: the upload keeps only their ratings
         # (bgmf_partition_rows), no host-side gather of the dataset
         own = sched.rows_of(rank)

@@ -1,7 +1,7 @@
 """Randomised parity sweep (GPU vs the oracle): random shapes, densities,
 duplicates, grids, k and schedules; fast mode within 1e-3 absolute per epoch
 (train and test RMSE), exact mode bit-identical; partition arrays bit-equal.
-Usage: python scripts/fuzz_parity.py [cases] [seed]"""
+Usage: python scripts/fuzz_parity.py [cases] [seed] [scale] [only-case]"""
 import sys
 import time
 
@@ -14,6 +14,7 @@ from oracle import oracle as O  # noqa: E402
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 g = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
 scale = int(sys.argv[3]) if len(sys.argv) > 3 else 1  # x dims and x^2 ratings
+only = int(sys.argv[4]) if len(sys.argv) > 4 else None  # re-run one case (same draws)
 fails = 0
 t0 = time.time()
 for i in range(cases):
@@ -41,6 +42,8 @@ for i in range(cases):
     d = bm.RatingsDataset(n, m, r, c, v)
     holdout = g.random() < 0.3 and nnz >= 20
     tag = f"case {i}: n={n} m={m} nnz={nnz} grid={I}x{J} k={k} {spec} exact={exact} holdout={holdout} stream={stream}"
+    if only is not None and i != only:
+        continue
     try:
         P = O.partition(r, c, v, n, m, I, J)
         b = bm.partition(d, I, J)
