@@ -856,8 +856,9 @@ int run_shards_ordered(bgmf_ctx* c, const int32_t* r0, const int32_t* r1, int ns
 // ord_col_conc concurrent groups per V row (chunked_splits_rows).  Every
 // fast-mode drift past 1e-3 in the randomised sweeps
 // was in one of these; C1-C5 single-GPU strata are in none.  Ring ranks set
-// ord_col_conc = 4 (their 2-block launches of C4: ~4 groups per V row,
-// measured within 2e-5 and covered by the ring sweeps).
+// ord_col_conc = 6 (their 2-block launches of C4 run up to 4.0 groups per V
+// row -- block_chunk's (ratings per column - 32) / 80 -- measured within
+// 2e-5, and the randomised ring sweeps cover worlds 2-4).
 // converge: always when it fits.
 // The auto rule's risk test alone (no feasibility): would the chunked sweep
 // of this batch distort the reference order (a dense block, split rows, or

@@ -398,7 +398,7 @@ class GpuShard:
         # a rank sweeps a stratum's blocks of its own rows (C4 on 8 GPUs: 2
         # per batch), so the chunked kernel runs more groups per V row than a
         # whole-stratum launch; csrc/ordered.cu use_ordered
-        self.eng._opt("ord_col_conc", float(os.environ.get("BGMF_RING_COL_CONC", "4")))
+        self.eng._opt("ord_col_conc", float(os.environ.get("BGMF_RING_COL_CONC", "6")))
         # this rank's U row-blocks: the upload keeps only their ratings
         # (bgmf_partition_rows), no host-side gather of the dataset
         own = sched.rows_of(rank)
