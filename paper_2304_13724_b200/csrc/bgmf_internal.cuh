@@ -137,6 +137,9 @@ struct bgmf_ctx {
   // of the rotating plan is contiguous (diagonals when I == J); packed
   // 4-byte (lrow << cbits | lcol) records when they fit (8 B per rating)
   bool packed = false;
+  bool no_val8 = false;                  // option: keep fp32 values in the streamed records
+  bool val8 = false;                     // values are integers 0..255: 1-byte codes in
+                                         // h_val and the slots (records 5 B instead of 8)
   int32_t* h_lrow = nullptr;             // or the packed records
   int32_t* h_lcol = nullptr;             // unused when packed
   float* h_val = nullptr;
@@ -175,6 +178,14 @@ struct bgmf_ctx {
 };
 
 namespace bgmf {
+
+// The streamed record format as the kernels' `cbits` argument: -1 = SoA
+// int32 row / int32 col / fp32 value; else packed (row << cbits | col) records,
+// bit 8 set when the values are 1-byte codes (val8).
+inline int stream_cbits(const bgmf_ctx* c) {
+  return c->packed ? (c->cbits | (c->val8 ? 0x100 : 0)) : -1;
+}
+inline int64_t val_bytes(const bgmf_ctx* c) { return c->val8 ? 1 : 4; }
 
 // Device memory comes from the device's stream-ordered pool (cudaMallocAsync)
 // whose release threshold bgmf_create raises to "never": a second train call
@@ -304,6 +315,7 @@ int run_shards_ordered(bgmf_ctx* ctx, const int32_t* r0, const int32_t* r1, int 
 // stream.cu -- out-of-core: ratings in pinned host memory, device slot ring
 int stream_enable(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
 int stream_slots(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);
+__global__ void values_to_codes(const float* __restrict__ v, int64_t n, uint8_t* __restrict__ out);
 // out-of-core partition (partition.cu): chunks of row blocks under `budget`
 // bytes of HBM straight into the pinned streaming layout
 int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const double* vals,

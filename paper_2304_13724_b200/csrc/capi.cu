@@ -217,6 +217,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "col_ratio")) c->col_ratio = value > 0 ? value : 0.6;
   else if (!strcmp(key, "ordered")) c->ord_mode = value < 0 ? -1 : (value != 0.0 ? 1 : 0);
   else if (!strcmp(key, "ord_row_split")) c->ord_row_split = value;
+  else if (!strcmp(key, "no_val8")) c->no_val8 = value != 0.0;
   else if (!strcmp(key, "ord_col_conc")) c->ord_col_conc = value;
   else if (!strcmp(key, "ord_warp")) c->ord_warp = value != 0.0;
   else if (!strcmp(key, "ord_stage_ratings"))

@@ -680,6 +680,7 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   }
   std::vector<int64_t> tcount((size_t)nth * nb, 0);
   std::vector<int64_t> tbad(nth, -1);
+  std::vector<char> tnonbyte(nth, 0);  // a value that is not an integer in 0..255
 #pragma omp parallel num_threads(nth)
   {
     const int t = omp_get_thread_num();
@@ -690,6 +691,8 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
       if (r < 0 || r >= n || c < 0 || c >= m) { tbad[t] = i; break; }
       if (r < row_lo || r >= row_hi) continue;  // another rank's rows (checked, not kept)
       ++cnt[slab(r, rbase, rextra) * J + slab(c, cbase, cextra)];
+      const float x = (float)vals[i];
+      if (!(x >= 0.f && x <= 255.f && x == rintf(x))) tnonbyte[t] = 1;
     }
   }
   for (int t = 0; t < nth; ++t)
@@ -809,8 +812,11 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   }
   prof_mark(ctx, "ooc: host bucket pass");
 
-  // pinned diagonal layout (stream.cu) and its block positions
+  // pinned diagonal layout (stream.cu) and its block positions; 1-byte value
+  // codes (5 B records) when every kept value is an integer in 0..255
   ctx->packed = rbits + cbits <= 32;
+  ctx->val8 = ctx->packed && !ctx->no_val8;
+  for (int t = 0; t < nth; ++t) ctx->val8 = ctx->val8 && !tnonbyte[t];
   std::vector<int> order;
   order.reserve(nb);
   if (I == J) {
@@ -826,7 +832,7 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   }
   BGMF_CK(ctx, big_pinned_alloc((void**)&ctx->h_lrow, N * 4));
   if (!ctx->packed) BGMF_CK(ctx, big_pinned_alloc((void**)&ctx->h_lcol, N * 4));
-  BGMF_CK(ctx, big_pinned_alloc((void**)&ctx->h_val, N * 4));
+  BGMF_CK(ctx, big_pinned_alloc((void**)&ctx->h_val, N * val_bytes(ctx)));
   BGMF_CK(ctx, big_pinned_alloc((void**)&ctx->h_order, N * 4));
   prof_mark(ctx, "ooc: pinned layout");
 
@@ -839,13 +845,14 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   int32_t *d_r = nullptr, *d_c = nullptr, *lr = nullptr, *lc = nullptr, *rec = nullptr;
   float *d_v = nullptr, *vv = nullptr;
   uint32_t *d_x = nullptr, *ia = nullptr, *ord = nullptr, *gord = nullptr;
+  uint8_t* codes = nullptr;
   uint64_t* ka = nullptr;
   unsigned long long* d_bad = nullptr;
   int rc = BGMF_OK;
   auto cleanup = [&]() {
     free_dev(d_r, s); free_dev(d_c, s); free_dev(d_v, s); free_dev(d_x, s); free_dev(ka, s);
     free_dev(ia, s); free_dev(lr, s); free_dev(lc, s); free_dev(vv, s); free_dev(ord, s);
-    free_dev(rec, s); free_dev(gord, s); free_dev(d_bad, s);
+    free_dev(rec, s); free_dev(gord, s); free_dev(d_bad, s); free_dev(codes, s);
   };
 #define OCK(call)                                                                    \
   do {                                                                               \
@@ -856,6 +863,7 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   OCK(dmalloc(&d_x, C * 4, s));
   OCK(dmalloc(&lr, C * 4, s)); OCK(dmalloc(&lc, C * 4, s)); OCK(dmalloc(&vv, C * 4, s));
   OCK(dmalloc(&ord, C * 4, s)); OCK(dmalloc(&gord, C * 4, s)); OCK(dmalloc(&d_bad, 8, s));
+  if (ctx->val8) OCK(dmalloc(&codes, C, s));
   if (ctx->packed) OCK(dmalloc(&rec, C * 4, s));
   const int grid = ctx->num_sms * 8;
   for (int k = 0; k < nch; ++k) {
@@ -892,6 +900,7 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
                                          (1ull << cbits) - 1, lr, lc, vv, nullptr, ord);
     pack_and_order<<<grid, 256, 0, s>>>(lr, lc, ord, d_x, cnt, cbits, ctx->packed ? rec : nullptr,
                                         gord);
+    if (ctx->val8) values_to_codes<<<grid, 256, 0, s>>>(vv, cnt, codes);
     OCK(cudaGetLastError());
     free_dev(ka, s);
     free_dev(ia, s);
@@ -904,7 +913,11 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
                             cudaMemcpyDeviceToHost, s));
         if (!ctx->packed)
           OCK(cudaMemcpyAsync(ctx->h_lcol + dst, lc + lo, bc_ * 4, cudaMemcpyDeviceToHost, s));
-        OCK(cudaMemcpyAsync(ctx->h_val + dst, vv + lo, bc_ * 4, cudaMemcpyDeviceToHost, s));
+        if (ctx->val8)
+          OCK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(ctx->h_val) + dst, codes + lo, bc_,
+                              cudaMemcpyDeviceToHost, s));
+        else
+          OCK(cudaMemcpyAsync(ctx->h_val + dst, vv + lo, bc_ * 4, cudaMemcpyDeviceToHost, s));
         OCK(cudaMemcpyAsync(ctx->h_order + dst, gord + lo, bc_ * 4, cudaMemcpyDeviceToHost, s));
       }
       lo += bc_;

@@ -110,7 +110,8 @@ __device__ __forceinline__ Chunk locate_chunk(const BlockWork* __restrict__ work
 
 // Rating triple of entry i.  cbits < 0: SoA int32 row / int32 col arrays;
 // cbits >= 0: packed 4-byte (row << cbits | col) records in `lrow` (the
-// out-of-core stream format, 8 B per rating with the fp32 value).
+// out-of-core stream format, 8 B per rating with the fp32 value), the low 8
+// bits the column bits; bit 8: `val` holds 1-byte integer codes (5 B/rating).
 __device__ __forceinline__ void load_triple(const int32_t* __restrict__ lrow,
                                             const int32_t* __restrict__ lcol,
                                             const float* __restrict__ val, int cbits, int64_t i,
@@ -118,17 +119,20 @@ __device__ __forceinline__ void load_triple(const int32_t* __restrict__ lrow,
   if (cbits < 0) {
     r = __ldg(lrow + i);
     c = __ldg(lcol + i);
+    x = __ldg(val + i);
   } else {
+    const int cb = cbits & 0xFF;
     const uint32_t rc = (uint32_t)__ldg(lrow + i);
-    r = (int)(rc >> cbits);
-    c = (int)(rc & ((1u << cbits) - 1u));
+    r = (int)(rc >> cb);
+    c = (int)(rc & ((1u << cb) - 1u));
+    x = (cbits & 0x100) ? (float)__ldg(reinterpret_cast<const uint8_t*>(val) + i)
+                        : __ldg(val + i);
   }
-  x = __ldg(val + i);
 }
 
 __device__ __forceinline__ int load_rowidx(const int32_t* __restrict__ lrow, int cbits,
                                            int64_t i) {
-  return cbits < 0 ? __ldg(lrow + i) : (int)((uint32_t)__ldg(lrow + i) >> cbits);
+  return cbits < 0 ? __ldg(lrow + i) : (int)((uint32_t)__ldg(lrow + i) >> (cbits & 0xFF));
 }
 
 // L2-coherent 128-bit load (the factors are written by other SMs during the

@@ -57,7 +57,23 @@ __global__ void pack_records(const int32_t* __restrict__ lrow, const int32_t* __
     out[i] = (int32_t)(((uint32_t)lrow[i] << cbits) | (uint32_t)lcol[i]);
 }
 
+// 1-byte value codes: every value an integer in 0..255 (rating scales:
+// MovieLens 1..5, Netflix 1..5), so (float)code is the value bit for bit.
+__global__ void byte_values_check(const float* __restrict__ v, int64_t n, int* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = v[i];
+    if (!(x >= 0.f && x <= 255.f && x == rintf(x))) *bad = 1;
+  }
+}
+
 }  // namespace
+
+__global__ void values_to_codes(const float* __restrict__ v, int64_t n, uint8_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint8_t)v[i];
+}
 
 int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
   if (!c->partitioned) return fail(c, BGMF_ERR_STATE, "bgmf_partition has not been called");
@@ -91,9 +107,30 @@ int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
     pos += c->h_offsets[b + 1] - c->h_offsets[b];
   }
   const size_t N = (size_t)(c->nnz > 0 ? c->nnz : 1);
+  c->val8 = false;
+  if (c->packed && c->nnz > 0) {  // 1-byte value codes when every value allows
+    int* d_bad = nullptr;
+    int h_bad = 0;
+    BGMF_CK(c, dmalloc(&d_bad, sizeof(int), s));
+    BGMF_CK(c, cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+    byte_values_check<<<c->num_sms * 8, 256, 0, s>>>(c->d_val, c->nnz, d_bad);
+    BGMF_CK(c, cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BGMF_CK(c, cudaStreamSynchronize(s));
+    dfree(d_bad, s);
+    c->val8 = h_bad == 0 && !c->no_val8;
+    if (c->val8) {  // codes in place of the fp32 values
+      uint8_t* codes = nullptr;
+      BGMF_CK(c, dmalloc(&codes, N, s));
+      values_to_codes<<<c->num_sms * 8, 256, 0, s>>>(c->d_val, c->nnz, codes);
+      BGMF_CK(c, cudaGetLastError());
+      BGMF_CK(c, cudaStreamSynchronize(s));
+      dfree(c->d_val, s);
+      c->d_val = reinterpret_cast<float*>(codes);
+    }
+  }
   BGMF_CK(c, big_pinned_alloc((void**)&c->h_lrow, N * 4));
   if (!c->packed) BGMF_CK(c, big_pinned_alloc((void**)&c->h_lcol, N * 4));
-  BGMF_CK(c, big_pinned_alloc((void**)&c->h_val, N * 4));
+  BGMF_CK(c, big_pinned_alloc((void**)&c->h_val, N * val_bytes(c)));
   BGMF_CK(c, big_pinned_alloc((void**)&c->h_order, N * 4));
   if (c->packed && c->nnz > 0) {  // pack in place of the (no longer needed) lrow
     int32_t* rec = nullptr;
@@ -111,7 +148,9 @@ int stream_enable(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
     if (!c->packed)
       BGMF_CK(c, cudaMemcpyAsync(c->h_lcol + dst, c->d_lcol + lo, cnt * 4, cudaMemcpyDeviceToHost,
                                  s));
-    BGMF_CK(c, cudaMemcpyAsync(c->h_val + dst, c->d_val + lo, cnt * 4, cudaMemcpyDeviceToHost, s));
+    BGMF_CK(c, cudaMemcpyAsync(reinterpret_cast<char*>(c->h_val) + dst * val_bytes(c),
+                               reinterpret_cast<const char*>(c->d_val) + lo * val_bytes(c),
+                               cnt * val_bytes(c), cudaMemcpyDeviceToHost, s));
     BGMF_CK(c, cudaMemcpyAsync(c->h_order + dst, c->d_order + lo, cnt * 4, cudaMemcpyDeviceToHost,
                                s));
   }
@@ -276,9 +315,10 @@ int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, 
     if (!c->packed)
       BGMF_CK(c, cudaMemcpyAsync(c->s_lcol[sl] + dst, c->h_lcol + src, cnt * 4,
                                  cudaMemcpyHostToDevice, cs));
-    BGMF_CK(c, cudaMemcpyAsync(c->s_val[sl] + dst, c->h_val + src, cnt * 4,
-                               cudaMemcpyHostToDevice, cs));
-    c->h2d_bytes += (c->packed ? 8.0 : 12.0) * (double)cnt;
+    BGMF_CK(c, cudaMemcpyAsync(reinterpret_cast<char*>(c->s_val[sl]) + dst * val_bytes(c),
+                               reinterpret_cast<const char*>(c->h_val) + src * val_bytes(c),
+                               cnt * val_bytes(c), cudaMemcpyHostToDevice, cs));
+    c->h2d_bytes += (double)((c->packed ? 4 : 8) + val_bytes(c)) * (double)cnt;
     return BGMF_OK;
   };
 
@@ -306,7 +346,7 @@ int run_step_stream(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, 
     BGMF_CK(c, cudaEventRecord(c->ev_copied[sl], cs));
     BGMF_CK(c, cudaStreamWaitEvent(s, c->ev_copied[sl], 0));
     rc = launch_piece(c, c->d_work + pc.w0, pc.nw, pc.chunks, c->s_lrow[sl], c->s_lcol[sl],
-                      c->s_val[sl], iters, alpha, beta, pc.ratings, c->packed ? c->cbits : -1);
+                      c->s_val[sl], iters, alpha, beta, pc.ratings, stream_cbits(c));
     if (rc) { cudaEventDestroy(ready); return rc; }
     BGMF_CK(c, cudaEventRecord(c->ev_consumed[sl], s));
   }
@@ -348,9 +388,10 @@ int stream_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int
       if (!c->packed)
         BGMF_CK(c, cudaMemcpyAsync(c->s_lcol[sl] + dst, c->h_lcol + src, cnt * 4,
                                    cudaMemcpyHostToDevice, cs));
-      BGMF_CK(c, cudaMemcpyAsync(c->s_val[sl] + dst, c->h_val + src, cnt * 4,
-                                 cudaMemcpyHostToDevice, cs));
-      c->h2d_bytes += (c->packed ? 8.0 : 12.0) * (double)cnt;
+      BGMF_CK(c, cudaMemcpyAsync(reinterpret_cast<char*>(c->s_val[sl]) + dst * val_bytes(c),
+                                 reinterpret_cast<const char*>(c->h_val) + src * val_bytes(c),
+                                 cnt * val_bytes(c), cudaMemcpyHostToDevice, cs));
+      c->h2d_bytes += (double)((c->packed ? 4 : 8) + val_bytes(c)) * (double)cnt;
       return BGMF_OK;
     };
     for (int i = 0; i < pc.nw && !rc; ++i) {
@@ -371,7 +412,7 @@ int stream_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int
     BGMF_CK(c, cudaEventRecord(c->ev_copied[sl], cs));
     BGMF_CK(c, cudaStreamWaitEvent(s, c->ev_copied[sl], 0));
     rc = launch_piece(c, c->d_work + pc.w0, pc.nw, pc.chunks, c->s_lrow[sl], c->s_lcol[sl],
-                      c->s_val[sl], iters, alpha, beta, pc.ratings, c->packed ? c->cbits : -1);
+                      c->s_val[sl], iters, alpha, beta, pc.ratings, stream_cbits(c));
     if (rc) return rc;
     BGMF_CK(c, cudaEventRecord(c->ev_consumed[sl], s));
   }
@@ -401,7 +442,7 @@ int run_step_stream_converge(bgmf_ctx* c, const int32_t* plan, const int32_t* ba
   for (int b = 0; b < nb; ++b) { iters_out[b] = 0; capped_out[b] = 0; }
   std::vector<double> sse_final(nb, 0.0);
   unsigned long long best = kNoBad;
-  const int cb = c->packed ? c->cbits : -1;
+  const int cb = stream_cbits(c);
   BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
   for (const Piece& pc : pieces) {
     const int sl = 0;
@@ -413,9 +454,11 @@ int run_step_stream_converge(bgmf_ctx* c, const int32_t* plan, const int32_t* ba
       if (!c->packed)
         BGMF_CK(c, cudaMemcpyAsync(c->s_lcol[sl] + bw.begin, c->h_lcol + src, cnt * 4,
                                    cudaMemcpyHostToDevice, s));
-      BGMF_CK(c, cudaMemcpyAsync(c->s_val[sl] + bw.begin, c->h_val + src, cnt * 4,
+      BGMF_CK(c, cudaMemcpyAsync(reinterpret_cast<char*>(c->s_val[sl]) + bw.begin * val_bytes(c),
+                                 reinterpret_cast<const char*>(c->h_val) + src * val_bytes(c),
+                                 cnt * val_bytes(c),
                                  cudaMemcpyHostToDevice, s));
-      c->h2d_bytes += (c->packed ? 8.0 : 12.0) * (double)cnt;
+      c->h2d_bytes += (double)((c->packed ? 4 : 8) + val_bytes(c)) * (double)cnt;
     }
     std::vector<char> active(pc.nw, 1);
     std::vector<double> prev(pc.nw, 0.0);

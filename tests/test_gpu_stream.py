@@ -19,9 +19,12 @@ def _c2_like(nnz=400_000):
     return bm.RatingsDataset(6040, 3706, r, c, v)
 
 
-@pytest.mark.parametrize("budget_frac,slots", [(0.05, 2), (0.2, 3), (0.5, 4)])
-def test_stream_matches_oracle(budget_frac, slots):
+@pytest.mark.parametrize("budget_frac,slots,half", [(0.05, 2, False), (0.2, 3, False),
+                                                    (0.5, 4, False), (0.2, 3, True)])
+def test_stream_matches_oracle(budget_frac, slots, half):
     d = _c2_like()
+    if half:  # half-star ratings: not 1-byte integers, fp32 values in the records
+        d = bm.RatingsDataset(d.n, d.m, d.rows, d.cols, d.values - 0.5)
     tr, te = bm.split(d, 0.2, seed=0)
     cfg = bm.TrainConfig(k=32, outer_steps=5, grid_i=8, grid_j=8)
     opts = bm.EngineOptions(device_rating_budget=int(12 * len(tr) * budget_frac),
@@ -35,9 +38,11 @@ def test_stream_matches_oracle(budget_frac, slots):
     dtr = np.abs(np.array([s.train_rmse for s in res.trace]) - [s["train_rmse"] for s in otr])
     dte = np.abs(np.array([s.test_rmse for s in res.trace]) - [s["test_rmse"] for s in otr])
     assert dtr.max() <= TOL and dte.max() <= TOL
-    # every epoch streams every rating once, as packed 8-byte records
-    # (block-local row << cbits | col, fp32 value)
-    assert blocked.engine.streamed_bytes() == pytest.approx(8.0 * len(tr) * 5)
+    # every epoch streams every rating once, as packed records: block-local
+    # row << cbits | col (4 B) and the value -- a 1-byte code for integer
+    # ratings 0..255, else fp32
+    per = 8.0 if half else 5.0
+    assert blocked.engine.streamed_bytes() == pytest.approx(per * len(tr) * 5)
 
 
 def test_stream_partition_export_and_sse_only_pass():
