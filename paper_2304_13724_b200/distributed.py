@@ -711,6 +711,13 @@ def bench_main(args, clock_sampler=None):
     st = shard.eng.kernel_stats(reset=True)
     ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{device}")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    # every rank's sweep launches (roofline per rank) and launch counts
+    mine = torch.tensor([st["sgd_ms"], float(st["sgd_launches"]), st["sgd_alg_bytes"],
+                         float(st["sse_launches"])], dtype=torch.float64,
+                        device=f"cuda:{device}")
+    per_rank = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(per_rank, mine)
+    per_rank = [t.cpu().tolist() for t in per_rank]
     dist.barrier()
     total_ms = float(ms.item())
     shard.eng.close()
@@ -750,16 +757,34 @@ def bench_main(args, clock_sampler=None):
                        "time over ranks",
                "walls_ms": [round(x * 1e3, 2) for x in walls]}
     if rank == 0:
-        hbm = 6553.0
-        try:
-            import json as _j
+        import json as _j
 
-            hbm = float(_j.load(open(os.path.join(os.path.dirname(os.path.dirname(
-                os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"])
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        hbm, hbm_kind = 6650.0, "fallback (B200_PROFILING.md)"
+        try:
+            hbm = float(_j.load(open(os.path.join(root, "MEASURED_PEAKS.json")))["hbm_gbs"])
+            hbm_kind = "measured (MEASURED_PEAKS.json)"
         except Exception:
             pass
         launch_ms = st["sgd_ms"] / max(st["sgd_launches"], 1)
         achieved = st["sgd_alg_bytes"] / max(st["sgd_launches"], 1) / (launch_ms / 1e3) / 1e9
+        ranks = []
+        for r_, (sms, nl, ab, _) in enumerate(per_rank):
+            lm = sms / max(nl, 1.0)
+            ranks.append({"rank": r_, "avg_launch_ms": lm,
+                          "achieved": ab / max(nl, 1.0) / (lm / 1e3) / 1e9 if lm > 0 else None})
+        # DRAM bytes per sweep launch from the committed single-GPU ncu capture:
+        # the same launch shape only at world 1 (a rank's launches hold 1/world
+        # of a stratum's blocks)
+        traffic = None
+        if world == 1:
+            try:
+                cap = _j.load(open(os.path.join(root, "profiles",
+                                                f"ncu_traffic_{args.config.lower()}.json")))
+                traffic = next(v["dram_bytes_per_launch"] for k, v in cap.items()
+                               if "sgd_fast" in k)
+            except Exception:
+                pass
         line = {
             "metric": "SGD rating-updates/sec (epoch)",
             "value": nnz * args.steps / (total_ms / 1e3),
@@ -771,11 +796,13 @@ def bench_main(args, clock_sampler=None):
                        "parallelism": f"U-resident/V-rotating x{world} (NCCL P2P)",
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None,
-                         "kernel": "sgd_fast_kernel (rank 0)"},
+                         "frac": achieved / hbm, "traffic": traffic, "peak_kind": hbm_kind,
+                         "dram_frac": (traffic / (launch_ms / 1e3) / (hbm * 1e9)
+                                       if traffic else None),
+                         "kernel": "sgd_fast_kernel (rank 0)", "per_rank": ranks},
             "e2e": e2e, "cpu_baseline": None,
             "clocks": sampler.summary() if sampler is not None else None,
-            "gpu_launches": int(st["sgd_launches"] + st["sse_launches"]),
+            "gpu_launches": int(sum(p[1] + p[3] for p in per_rank)),
             "gen_seconds": t_gen,
         }
         sys.stdout.flush()
