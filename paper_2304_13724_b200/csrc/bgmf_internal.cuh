@@ -166,6 +166,7 @@ struct bgmf_ctx {
   uint32_t* d_obar = nullptr;            // per launched block: two barrier counters
   double* d_opart = nullptr;             // per stage: SSE partial
   int64_t* d_conv = nullptr;             // per block: converge iters_used, capped
+  double* d_esq = nullptr;               // exact mode: per-entry squared residuals
   double ord_row_split = 1.0;            // auto: ordered when chunks < this many mean rows
   double ord_col_conc = 1.0;             // auto: ... or > this many groups per V row (<= 0: off)
   std::map<uint64_t, int> ord_cap;       // (kp, smem) -> co-resident CTAs
@@ -308,7 +309,8 @@ bool ordered_block_ok(bgmf_ctx* ctx, int b);
 bool use_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1, bool converge = false);
 bool order_risky(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1);
 int run_batch_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1, int pos_base,
-                      int iters, float alpha, float beta, bool conv = false, double tol = 0.0);
+                      int iters, float alpha, float beta, bool conv = false, double tol = 0.0,
+                      double alpha64 = 0.0, double beta64 = 0.0);
 int run_shards_ordered(bgmf_ctx* ctx, const int32_t* r0, const int32_t* r1, int nshards,
                        float* vpriv, float alpha, float beta, double* sse_dev);
 

@@ -93,6 +93,21 @@ __device__ __forceinline__ bool mbar_try_wait(unsigned mb, unsigned parity) {
   return ok != 0;
 }
 
+// Every wait in these kernels is bounded: a schedule bug or a corrupted
+// index array must fail the launch (an error the host reports), never hang
+// the GPU.  20 s of %globaltimer, checked every 1024 polls.
+struct SpinGuard {
+  unsigned long long t0 = 0;
+  unsigned n = 0;
+  __device__ __forceinline__ void tick() {
+    if ((++n & 1023u) != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (!t0) t0 = t;
+    else if (t - t0 > 20000000000ull) __trap();
+  }
+};
+
 // First index in [lo, hi) whose column is >= key (columns ascend within a
 // row).  L-ary search: every lane probes one split point per round.
 template <int L>
@@ -192,8 +207,10 @@ __device__ __forceinline__ void stage_sweep(const Stage& T, int it, uint32_t gen
       else if (it > 0)
         want = ((gen + (uint32_t)it - 1u) << 8) | (uint32_t)(__ldg(T.bcol + re - 1) / T.sw + 1);
     }
-    if (want)
-      while (!__all_sync(gmask, ld_acquire_gpu(T.fl + r) == want)) __nanosleep(20);
+    if (want) {
+      SpinGuard sg;
+      while (!__all_sync(gmask, ld_acquire_gpu(T.fl + r) == want)) { __nanosleep(20); sg.tick(); }
+    }
     float4 u[V4];
     load_row_l2<V4>(u, T.Ub + (int64_t)r * kp, ln);
     for (int t0 = lo; t0 < hi; t0 += L) {
@@ -211,8 +228,8 @@ __device__ __forceinline__ void stage_sweep(const Stage& T, int it, uint32_t gen
         const int q = __shfl_sync(gmask, qA, ln.gbase + j);
         int* cp = T.cnt + c;
         // column order: every earlier entry of this column has been applied
-        while (!__all_sync(gmask, ld_acquire_cta(cp) == q)) {
-        }
+        SpinGuard sg;
+        while (!__all_sync(gmask, ld_acquire_cta(cp) == q)) sg.tick();
         float* vr = T.sv + (size_t)c * kp;
         float4 v[V4];
         load_row_smem<V4>(v, vr, ln);
@@ -310,7 +327,8 @@ __device__ __forceinline__ void block_barrier(uint32_t* ctr, int S, uint32_t k) 
     if (threadIdx.x == 0) {
       __threadfence();
       atomicAdd(ctr, 1u);
-      while (ld_acquire_gpu(ctr) < (k + 1u) * (uint32_t)S) __nanosleep(64);
+      SpinGuard sg;
+      while (ld_acquire_gpu(ctr) < (k + 1u) * (uint32_t)S) { __nanosleep(64); sg.tick(); }
     }
     __syncthreads();
   }
@@ -413,9 +431,10 @@ ordered_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restrict__ 
         "l"(gv), "r"(bytes), "r"(mb)
         : "memory");
   }
-  if (bytes > 0)
-    while (!mbar_try_wait(mb, 0)) {
-    }
+  if (bytes > 0) {
+    SpinGuard sg;
+    while (!mbar_try_wait(mb, 0)) sg.tick();
+  }
 
   uint32_t nbar = 0;
   int swept = 0;
@@ -474,6 +493,303 @@ ordered_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restrict__ 
     if (T.st == 0) sse[B.block_id] = sse_now;
     if (T.S > 1) {
       // the last stage out resets the block's counters for the next launch
+      const unsigned done = atomicAdd(ctr + 1, 1u);
+      if (done == (unsigned)T.S - 1) {
+        ctr[0] = 0u;
+        ctr[1] = 0u;
+        ctr[2] = 0u;
+      }
+    }
+    if (bytes > 0 && swept > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
+// ---- exact mode: the same schedule in fp64, bit-identical ---------------
+// The ordered schedule applies the updates of every U and V row in stored
+// order, so with the reference's own arithmetic it reproduces the reference
+// bit for bit -- in parallel across rows and columns (round 1's exact kernel
+// walked each block on one thread).  Per rating, lane 0 of the warp runs the
+// residual chain e = x - u0 v0 - u1 v1 - ... with separately rounded fp64
+// products and subtractions (numba fastmath=False, _kernels.py:44-48); the
+// lanes then update the k elements in parallel in the reference's order of
+// operations (u + a(2e v - b u), _kernels.py:51-55).  u_r is staged in the
+// warp's shared-memory row for the row's run, V in the stage's slab.  The
+// post-sweep SSE (_kernels.py:16-28) is a sequential sum: every entry's
+// (x - u.v)^2 is computed in parallel into `esq`, then one thread adds them
+// in stored order.
+__device__ __forceinline__ void exact_stage_sweep(const Stage& T, double* sv, double* urow,
+                                                  const double* __restrict__ bval,
+                                                  double* __restrict__ Ub, int it, uint32_t gen,
+                                                  double alpha, double beta, int pos,
+                                                  int* s_next, unsigned long long* bad,
+                                                  int* divflag) {
+  const int lane = threadIdx.x & 31;
+  const int k = T.kp;
+  double* us = urow + (threadIdx.x >> 5) * k;
+  __syncthreads();
+  for (int i = threadIdx.x; i < T.nc; i += kOrdThreads) T.cnt[i] = T.qbase ? INT32_MAX : 0;
+  if (threadIdx.x == 0) *s_next = 0;
+  __syncthreads();
+  if (T.qbase) {
+    const int e0 = __ldg(T.rp), e1 = __ldg(T.rp + T.h);
+    for (int i = e0 + (int)threadIdx.x; i < e1; i += kOrdThreads) {
+      const int c = __ldg(T.bcol + i);
+      if (c >= T.cs && c < T.ce) atomicMin(T.cnt + (c - T.cs), __ldg(T.bq + i));
+    }
+    __syncthreads();
+  }
+  const uint32_t tag_now = ((gen + (uint32_t)it) << 8) | (uint32_t)(T.st + 1);
+  while (true) {
+    int r = 0;
+    if (lane == 0) r = atomicAdd(s_next, 1);
+    r = __shfl_sync(kFull, r, 0);
+    if (r >= T.h) break;
+    const int rb = __ldg(T.rp + r), re = __ldg(T.rp + r + 1);
+    if (rb == re) continue;
+    int lo = rb, hi = re;
+    if (T.cs > 0) lo = group_lower_bound<32>(T.bcol, rb, re, T.cs, lane, kFull);
+    if (T.ce < T.w) hi = group_lower_bound<32>(T.bcol, lo, re, T.ce, lane, kFull);
+    if (lo == hi) continue;
+    uint32_t want = 0;
+    if (T.S > 1) {
+      if (lo > rb)
+        want = ((gen + (uint32_t)it) << 8) | (uint32_t)(__ldg(T.bcol + lo - 1) / T.sw + 1);
+      else if (it > 0)
+        want = ((gen + (uint32_t)it - 1u) << 8) | (uint32_t)(__ldg(T.bcol + re - 1) / T.sw + 1);
+    }
+    if (want) {
+      SpinGuard sg;
+      while (!__all_sync(kFull, ld_acquire_gpu(T.fl + r) == want)) { __nanosleep(20); sg.tick(); }
+    }
+    double* ug = Ub + (int64_t)r * k;
+    for (int g = lane; g < k; g += 32) us[g] = __ldcg(ug + g);
+    __syncwarp();
+    for (int t0 = lo; t0 < hi; t0 += 32) {
+      int cA = 0, qA = 0;
+      double xA = 0.0;
+      if (t0 + lane < hi) {
+        cA = __ldg(T.bcol + t0 + lane);
+        xA = __ldg(bval + t0 + lane);
+        qA = __ldg(T.bq + t0 + lane);
+      }
+      const int nt = min(32, hi - t0);
+      for (int j = 0; j < nt; ++j) {
+        const int c = __shfl_sync(kFull, cA, j) - T.cs;
+        const double x = __shfl_sync(kFull, xA, j);
+        const int q = __shfl_sync(kFull, qA, j);
+        int* cp = T.cnt + c;
+        SpinGuard sg;
+        while (!__all_sync(kFull, ld_acquire_cta(cp) == q)) sg.tick();
+        double* vs = sv + (size_t)c * k;
+        double e = x;
+        if (lane == 0)
+          for (int g = 0; g < k; ++g) e = __dsub_rn(e, __dmul_rn(us[g], vs[g]));
+        e = __shfl_sync(kFull, e, 0);
+        if (!isfinite(e) && lane == 0) {
+          atomicMin(bad, pack_bad(pos, it, t0 + j - T.e0));
+          *divflag = 1;
+        }
+        const double e2 = __dmul_rn(2.0, e);
+        for (int g = lane; g < k; g += 32) {
+          const double u0 = us[g], v0 = vs[g];
+          us[g] = __dadd_rn(u0, __dmul_rn(alpha, __dsub_rn(__dmul_rn(e2, v0), __dmul_rn(beta, u0))));
+          vs[g] = __dadd_rn(v0, __dmul_rn(alpha, __dsub_rn(__dmul_rn(e2, u0), __dmul_rn(beta, v0))));
+        }
+        __syncwarp();
+        if (lane == 0) st_release_cta(cp, q + 1);
+      }
+    }
+    for (int g = lane; g < k; g += 32) ug[g] = us[g];
+    if (T.S > 1) {
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release_gpu(T.fl + r, tag_now);
+    }
+    __syncwarp();
+  }
+}
+
+// (x - u.v)^2 of every entry of this stage's slab into esq (entry order is
+// irrelevant: the sum below is sequential)
+__device__ __forceinline__ void exact_stage_esq(const Stage& T, const double* sv,
+                                                const double* __restrict__ bval,
+                                                const double* __restrict__ Ub,
+                                                double* __restrict__ besq) {
+  const int lane = threadIdx.x & 31;
+  const int k = T.kp;
+  for (int r = (int)threadIdx.x / 32; r < T.h; r += kOrdThreads / 32) {
+    const int rb = __ldg(T.rp + r), re = __ldg(T.rp + r + 1);
+    if (rb == re) continue;
+    int lo = rb, hi = re;
+    if (T.cs > 0) lo = group_lower_bound<32>(T.bcol, rb, re, T.cs, lane, kFull);
+    if (T.ce < T.w) hi = group_lower_bound<32>(T.bcol, lo, re, T.ce, lane, kFull);
+    const double* ug = Ub + (int64_t)r * k;
+    for (int i = lo + lane; i < hi; i += 32) {
+      const double* vs = sv + (size_t)(__ldg(T.bcol + i) - T.cs) * k;
+      double e = __ldg(bval + i);
+      for (int g = 0; g < k; ++g) e = __dsub_rn(e, __dmul_rn(__ldcg(ug + g), vs[g]));
+      besq[i] = __dmul_rn(e, e);
+    }
+  }
+}
+
+// The block's SSE, summed in stored order by one thread; every stage gets it.
+__device__ __forceinline__ double exact_block_sse(const Stage& T, const double* sv,
+                                                  const double* __restrict__ bval,
+                                                  const double* __restrict__ Ub,
+                                                  double* __restrict__ besq, double* part,
+                                                  int stage0, uint32_t* ctr, uint32_t& nbar,
+                                                  double* s_bcast) {
+  exact_stage_esq(T, sv, bval, Ub, besq);
+  block_barrier(ctr, T.S, nbar++);  // every stage's terms are written
+  if (T.st == 0 && threadIdx.x == 0) {
+    const int e0 = __ldg(T.rp), e1 = __ldg(T.rp + T.h);
+    double s = 0.0;
+    for (int i = e0; i < e1; ++i) s = __dadd_rn(s, __ldcg(besq + i));
+    part[stage0] = s;
+    *s_bcast = s;
+  }
+  if (T.S > 1) {
+    block_barrier(ctr, T.S, nbar++);
+    if (threadIdx.x == 0) *s_bcast = __ldcg(part + stage0);
+  }
+  __syncthreads();
+  return *s_bcast;
+}
+
+__global__ void __launch_bounds__(kOrdThreads, 1)
+ordered_exact_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restrict__ lcol,
+                     const double* __restrict__ val, const int32_t* __restrict__ qrank,
+                     const int32_t* __restrict__ rowptr, double* __restrict__ U, int k,
+                     double alpha, double beta, int iters, uint32_t gen,
+                     uint32_t* __restrict__ rflag, uint32_t* __restrict__ bar,
+                     double* __restrict__ part, double* __restrict__ esq,
+                     double* __restrict__ sse, unsigned long long* __restrict__ bad, int conv,
+                     double tol, int64_t* __restrict__ conv_out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ int s_next;
+  __shared__ int s_div;
+  __shared__ double s_bcast;
+  __shared__ __align__(8) unsigned long long s_mbar;
+  int bi = 0;
+  {
+    int lo = 0, hi = P.nblocks - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.b[mid].stage0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    bi = lo;
+  }
+  const OrdBlock B = P.b[bi];
+  Stage T;
+  T.S = B.nstages;
+  T.st = (int)blockIdx.x - B.stage0;
+  T.sw = B.slab_w;
+  T.cs = T.st * T.sw;
+  T.ce = min(T.cs + T.sw, B.w);
+  T.nc = T.ce - T.cs;
+  T.h = B.h;
+  T.w = B.w;
+  T.kp = k;
+  T.rp = rowptr + B.rp;
+  T.bcol = lcol + B.begin;
+  T.bq = qrank + B.begin;
+  T.fl = rflag + B.row_start;
+  T.qbase = B.qbase;
+  T.e0 = __ldg(T.rp);
+  double* sv = reinterpret_cast<double*>(smem);
+  T.cnt = reinterpret_cast<int*>(sv + (size_t)T.sw * k);
+  double* urow = reinterpret_cast<double*>(smem + (((size_t)T.sw * k * 8 + (size_t)T.sw * 4 + 15) & ~(size_t)15));
+  const double* bval = val + B.begin;
+  double* Ub = U + B.row_start * k;
+  double* besq = esq + B.begin;
+  uint32_t* ctr = bar + 3 * bi;
+  double* gv = reinterpret_cast<double*>(B.vb) + (B.col_start + T.cs) * k;
+  // TMA bulk copies need 16-byte aligned addresses and sizes: rows of odd k
+  // doubles are not, so those slabs move with plain loads / stores
+  const bool bulk = ((reinterpret_cast<uintptr_t>(gv) | ((size_t)T.nc * k * 8)) & 15) == 0;
+  const unsigned bytes = bulk ? (unsigned)T.nc * (unsigned)k * 8u : 0u;
+  if (!bulk)
+    for (int i = threadIdx.x; i < T.nc * k; i += kOrdThreads) sv[i] = __ldcg(gv + i);
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
+  const unsigned sva = (unsigned)__cvta_generic_to_shared(sv);
+  if (threadIdx.x == 0) {
+    s_div = 0;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bytes > 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            sva),
+        "l"(gv), "r"(bytes), "r"(mb)
+        : "memory");
+  }
+  if (bytes > 0) {
+    SpinGuard sg;
+    while (!mbar_try_wait(mb, 0)) sg.tick();
+  }
+  uint32_t nbar = 0;
+  int swept = 0;
+  double sse_now = 0.0;
+  const double cntd = (double)(__ldg(T.rp + T.h) - __ldg(T.rp));
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  if (!conv) {
+    for (int it = 0; it < iters; ++it)
+      exact_stage_sweep(T, sv, urow, bval, Ub, it, gen, alpha, beta, B.pos, &s_next, bad, &s_div);
+    swept = iters;
+    block_barrier(ctr, T.S, nbar++);  // every stage done: U is final
+    sse_now = exact_block_sse(T, sv, bval, Ub, besq, part, B.stage0, ctr, nbar, &s_bcast);
+    if (!isfinite(sse_now) && threadIdx.x == 0 && T.st == 0)  // _kernels.py:56-58
+      atomicMin(bad, pack_bad(B.pos, iters - 1, (int64_t)cntd - 1));
+  } else {
+    sse_now = exact_block_sse(T, sv, bval, Ub, besq, part, B.stage0, ctr, nbar, &s_bcast);
+    double rmse_prev = sqrt(sse_now / cntd);
+    bool capped = true;
+    while (swept < iters) {
+      exact_stage_sweep(T, sv, urow, bval, Ub, swept, gen, alpha, beta, B.pos, &s_next, bad,
+                        &s_div);
+      ++swept;
+      __syncthreads();
+      if (threadIdx.x == 0 && s_div && T.S > 1) atomicOr(ctr + 2, 1u);
+      block_barrier(ctr, T.S, nbar++);
+      if (threadIdx.x == 0) s_bcast = (double)(T.S > 1 ? ld_acquire_gpu(ctr + 2) : 0u) + (double)s_div;
+      __syncthreads();
+      const bool diverged = s_bcast != 0.0;
+      __syncthreads();
+      if (diverged) { capped = false; sse_now = nan; break; }
+      sse_now = exact_block_sse(T, sv, bval, Ub, besq, part, B.stage0, ctr, nbar, &s_bcast);
+      if (!isfinite(sse_now)) {
+        if (threadIdx.x == 0 && T.st == 0)
+          atomicMin(bad, pack_bad(B.pos, swept - 1, (int64_t)cntd - 1));
+        capped = false;
+        break;
+      }
+      const double rmse_now = sqrt(sse_now / cntd);
+      if (rmse_prev - rmse_now < tol) { capped = false; break; }
+      rmse_prev = rmse_now;
+    }
+    if (threadIdx.x == 0 && T.st == 0) {
+      conv_out[2 * B.block_id] = swept;
+      conv_out[2 * B.block_id + 1] = capped ? 1 : 0;
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0 && bytes > 0 && swept > 0) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gv),
+                 "r"(sva), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  if (!bulk && swept > 0)
+    for (int i = threadIdx.x; i < T.nc * k; i += kOrdThreads) gv[i] = sv[i];
+  if (threadIdx.x == 0) {
+    if (T.st == 0) sse[B.block_id] = sse_now;
+    if (T.S > 1) {
       const unsigned done = atomicAdd(ctr + 1, 1u);
       if (done == (unsigned)T.S - 1) {
         ctr[0] = 0u;
@@ -567,7 +883,17 @@ const void* ordered_kernel_ptr(int kp, int warp) {
 }
 #undef BGMF_ORD
 
-size_t slab_smem(int cols, int kp) { return (size_t)cols * ((size_t)kp * 4 + 4); }
+// Shared memory of a stage: the V slab and its column counters; exact mode
+// (fp64 rows of k) adds one staged u row per warp.
+size_t slab_smem(bgmf_ctx* c, int cols) {
+  if (!c->exact) return (size_t)cols * ((size_t)c->kp * 4 + 4);
+  const size_t slab = ((size_t)cols * ((size_t)c->k * 8 + 4) + 15) & ~(size_t)15;
+  return slab + (size_t)(kOrdThreads / 32) * c->k * 8;
+}
+size_t row_bytes(bgmf_ctx* c) { return c->exact ? (size_t)c->k * 8 + 4 : (size_t)c->kp * 4 + 4; }
+size_t fixed_smem(bgmf_ctx* c) {
+  return c->exact ? 16 + (size_t)(kOrdThreads / 32) * c->k * 8 : 0;
+}
 
 // Largest dynamic shared memory a CTA may ask for (static smem aside).
 size_t smem_budget(bgmf_ctx* c) {
@@ -577,11 +903,17 @@ size_t smem_budget(bgmf_ctx* c) {
   return optin > (int)stat ? (size_t)optin - stat : 0;
 }
 
-// co-resident CTAs of the ordered kernel with `smem` bytes of dynamic smem
+const void* stage_kernel_ptr(bgmf_ctx* c) {
+  return c->exact ? reinterpret_cast<const void*>(&ordered_exact_kernel)
+                  : ordered_kernel_ptr(c->kp, c->ord_warp);
+}
+
+// co-resident CTAs of the (fp32 or exact) ordered kernel with `smem` bytes
 int ordered_capacity(bgmf_ctx* c, size_t smem) {
-  const void* fn = ordered_kernel_ptr(c->kp, c->ord_warp);
+  const void* fn = stage_kernel_ptr(c);
   if (!fn) return 0;
-  const uint64_t key = ((uint64_t)c->kp << 33) | ((uint64_t)c->ord_warp << 32) | (uint64_t)smem;
+  const uint64_t key = ((uint64_t)c->kp << 34) | ((uint64_t)c->exact << 33) |
+                       ((uint64_t)c->ord_warp << 32) | (uint64_t)smem;
   auto it = c->ord_cap.find(key);
   if (it != c->ord_cap.end()) return it->second;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_budget(c));
@@ -601,6 +933,8 @@ void order_release(bgmf_ctx* c) {
   dfree(c->d_conv, c->stream);
   c->d_conv = nullptr;
   dfree(c->d_opart, c->stream);
+  dfree(c->d_esq, c->stream);
+  c->d_esq = nullptr;
   c->d_qrank = c->d_rowptr = nullptr;
   c->d_rflag = c->d_obar = nullptr;
   c->d_opart = nullptr;
@@ -678,22 +1012,20 @@ int ensure_order_index(bgmf_ctx* c) {
 // Can the ordered kernel take block b (its V block in <= kOrdMaxStages
 // slabs that each fit a CTA, all of them co-resident, row pointers in int32)?
 bool ordered_block_ok(bgmf_ctx* c, int b) {
-  if (c->exact || c->streaming || !ordered_kernel_ptr(c->kp, c->ord_warp)) return false;
+  if (c->streaming || !stage_kernel_ptr(c)) return false;
   const int64_t cnt = c->h_offsets[b + 1] - c->h_offsets[b];
   if (cnt >= INT32_MAX) return false;
   const int64_t w = c->col_bounds[b % c->J + 1] - c->col_bounds[b % c->J];
-  const int64_t per = (int64_t)(smem_budget(c) / ((size_t)c->kp * 4 + 4));
+  const size_t budget = smem_budget(c);
+  if (budget <= fixed_smem(c)) return false;
+  const int64_t per = (int64_t)((budget - fixed_smem(c)) / row_bytes(c));
   if (per < 1) return false;
   const int64_t smin = (w + per - 1) / per;
   if (smin > kOrdMaxStages) return false;
-  const int cap = ordered_capacity(c, slab_smem((int)((w + smin - 1) / smin), c->kp));
+  const int cap = ordered_capacity(c, slab_smem(c, (int)((w + smin - 1) / smin)));
   return smin <= cap;
 }
 
-// One batch (stratum, or part of one) through the ordered kernel: `iters`
-// sweeps and the post-sweep SSE of every block in plan[q0 .. q1) (plan
-// positions pos_base + q), as few cooperative launches as co-residency
-// allows.  The caller has checked ordered_block_ok for every block.
 namespace {
 
 // One unit of the ordered kernel: a block of the partition (or a CPMF row
@@ -709,7 +1041,7 @@ struct OrdItem {
 // SMs idle, at ~ord_stage_ratings ratings per stage (a row then visits more
 // slabs: each visit moves u_r through L2).
 void plan_stages(bgmf_ctx* c, OrdItem& it, int items) {
-  const int64_t per = (int64_t)(smem_budget(c) / ((size_t)c->kp * 4 + 4));
+  const int64_t per = (int64_t)((smem_budget(c) - fixed_smem(c)) / row_bytes(c));
   const int64_t w = it.ob.w;
   const int64_t smin = (w + per - 1) / per;
   int64_t S = (it.cnt + c->ord_stage_ratings - 1) / c->ord_stage_ratings;
@@ -722,15 +1054,17 @@ void plan_stages(bgmf_ctx* c, OrdItem& it, int items) {
   const int64_t swd = (w + S - 1) / S;
   it.ob.nstages = (int32_t)((w + swd - 1) / swd);  // no empty slab
   it.ob.slab_w = (int32_t)swd;
-  it.smem = slab_smem((int)swd, c->kp);
+  it.smem = slab_smem(c, (int)swd);
 }
 
 // Launch the items: as few cooperative launches as co-residency allows.
 int launch_items(bgmf_ctx* c, std::vector<OrdItem>& items, int iters, float alpha, float beta,
-                 bool conv, double tol, double* sse_dev) {
+                 bool conv, double tol, double* sse_dev, double alpha64 = 0.0,
+                 double beta64 = 0.0) {
   cudaStream_t s = c->stream;
-  const void* fn = ordered_kernel_ptr(c->kp, c->ord_warp);
+  const void* fn = stage_kernel_ptr(c);
   const size_t budget = smem_budget(c);
+  if (c->exact && !c->d_esq) BGMF_CK(c, dmalloc(&c->d_esq, (size_t)(c->nnz > 0 ? c->nnz : 1) * 8, s));
   size_t i = 0;
   while (i < items.size()) {
     // pack units into one launch while every stage stays co-resident
@@ -773,11 +1107,20 @@ int launch_items(bgmf_ctx* c, std::vector<OrdItem>& items, int iters, float alph
     int64_t* cout = c->d_conv;
     void* args[] = {&L, &lcol, &val, &qr, &rpp, &U, &kp, &alpha, &beta, &its, &gen,
                     &rfl, &bar, &part, &sse, &bad, &cv, &tol, &cout};
+    // exact: fp64 values, U and arithmetic (ordered_exact_kernel)
+    const double* val64 = c->d_val64;
+    double* U64 = c->d_u64;
+    int k = c->k;
+    double a64 = alpha64, b64 = beta64;
+    double* esq = c->d_esq;
+    void* args64[] = {&L, &lcol, &val64, &qr, &rpp, &U64, &k, &a64, &b64, &its, &gen,
+                      &rfl, &bar, &part, &esq, &sse, &bad, &cv, &tol, &cout};
     TimedLaunch* slot = nullptr;
     if (c->timing) record_begin(c, 0, ratings * iters * (12.0 + 16.0 * c->k), &slot);
     BGMF_CK(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)budget));
-    BGMF_CK(c, cudaLaunchCooperativeKernel(fn, dim3(ctas), dim3(kOrdThreads), args, smem, s));
+    BGMF_CK(c, cudaLaunchCooperativeKernel(fn, dim3(ctas), dim3(kOrdThreads),
+                                           c->exact ? args64 : args, smem, s));
     if (slot) record_end(c, slot);
     i = j;
   }
@@ -791,7 +1134,8 @@ int launch_items(bgmf_ctx* c, std::vector<OrdItem>& items, int iters, float alph
 // SSE of every block in plan[q0 .. q1) (plan positions pos_base + q).  The
 // caller has checked use_ordered.
 int run_batch_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, int pos_base,
-                      int iters, float alpha, float beta, bool conv, double tol) {
+                      int iters, float alpha, float beta, bool conv, double tol,
+                      double alpha64, double beta64) {
   int rc = ensure_order_index(c);
   if (rc) return rc;
   std::vector<OrdItem> items;
@@ -806,7 +1150,7 @@ int run_batch_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, int pos_
     it.ob.rp = c->h_rp[b];
     it.ob.row_start = c->row_bounds[bi];
     it.ob.col_start = c->col_bounds[bj];
-    it.ob.vb = c->d_v;
+    it.ob.vb = c->exact ? reinterpret_cast<float*>(c->d_v64) : c->d_v;
     it.ob.h = (int32_t)(c->row_bounds[bi + 1] - c->row_bounds[bi]);
     it.ob.w = (int32_t)(c->col_bounds[bj + 1] - c->col_bounds[bj]);
     it.ob.block_id = b;
@@ -815,7 +1159,7 @@ int run_batch_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, int pos_
     items.push_back(it);
   }
   for (auto& it : items) plan_stages(c, it, (int)items.size());
-  return launch_items(c, items, iters, alpha, beta, conv, tol, c->d_sse);
+  return launch_items(c, items, iters, alpha, beta, conv, tol, c->d_sse, alpha64, beta64);
 }
 
 // CPMF shards (baselines.py:100-182) through the ordered kernel: shard w =
@@ -880,7 +1224,13 @@ bool order_risky(bgmf_ctx* c, const int32_t* plan, int q0, int q1) {
 }
 
 bool use_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, bool converge) {
-  if (c->ord_mode == 0 || c->exact || c->streaming) return false;
+  if (c->ord_mode == 0 || c->streaming) return false;
+  if (c->exact) {  // fp64: the ordered schedule is the reference's, bit for bit
+    for (int q = q0; q < q1; ++q)
+      if (c->h_offsets[plan[q] + 1] > c->h_offsets[plan[q]] && !ordered_block_ok(c, plan[q]))
+        return false;
+    return true;
+  }
   for (int q = q0; q < q1; ++q)
     if (c->h_offsets[plan[q] + 1] > c->h_offsets[plan[q]] && !ordered_block_ok(c, plan[q]))
       return false;

@@ -1513,8 +1513,48 @@ int launch_piece_sweep(bgmf_ctx* c, const BlockWork* d_work, int nwork, int chun
   return BGMF_OK;
 }
 
+// Exact mode through the ordered schedule (ordered_exact_kernel): every batch
+// whose blocks fit, bit-identical to the reference and parallel within the
+// block.  Returns 1 (nothing run) when some batch cannot take it.
+static int run_exact_ordered(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off,
+                             int nbatch, int iters, double alpha, double beta, bool conv,
+                             double tol, int64_t cap, int64_t* iters_out, int32_t* capped_out) {
+  for (int t = 0; t < nbatch; ++t)
+    if (!use_ordered(c, plan, batch_off[t], batch_off[t + 1])) return 1;
+  cudaStream_t s = c->stream;
+  const int nb = c->I * c->J;
+  int rc = ensure_step_scratch(c, 1);
+  if (rc) return rc;
+  BGMF_CK(c, cudaMemsetAsync(c->d_sse, 0, sizeof(double) * nb, s));
+  BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
+  const int n_it = conv ? (int)(cap > INT32_MAX ? INT32_MAX : cap) : iters;
+  for (int t = 0; t < nbatch && !rc; ++t)
+    rc = run_batch_ordered(c, plan, batch_off[t], batch_off[t + 1], 0, n_it, (float)alpha,
+                           (float)beta, conv, tol, alpha, beta);
+  if (rc) return rc;
+  std::vector<int64_t> cv(conv ? (size_t)2 * nb : 0);
+  BGMF_CK(c, cudaMemcpyAsync(c->h_sse, c->d_sse, sizeof(double) * nb, cudaMemcpyDeviceToHost, s));
+  BGMF_CK(c, cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, s));
+  if (conv && c->d_conv)
+    BGMF_CK(c, cudaMemcpyAsync(cv.data(), c->d_conv, sizeof(int64_t) * 2 * nb,
+                               cudaMemcpyDeviceToHost, s));
+  BGMF_CK(c, cudaStreamSynchronize(s));
+  if (conv)
+    for (int b = 0; b < nb; ++b) {
+      const bool ne = c->h_offsets[b + 1] > c->h_offsets[b];
+      iters_out[b] = ne ? cv[2 * b] : 0;
+      capped_out[b] = ne ? (int32_t)cv[2 * b + 1] : 0;
+    }
+  return BGMF_OK;
+}
+
 int run_step_exact(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int nbatch,
                    int iters, double alpha, double beta) {
+  {
+    const int rc = run_exact_ordered(c, plan, batch_off, nbatch, iters, alpha, beta, false, 0.0,
+                                     0, nullptr, nullptr);
+    if (rc != 1) return rc;
+  }
   cudaStream_t s = c->stream;
   std::vector<BatchRange> ranges;
   int rc = build_work(c, plan, batch_off, nbatch, 0, ranges);
@@ -1720,6 +1760,11 @@ int run_sync_parallel_step(bgmf_ctx* c, const int64_t* edges, int nshards, doubl
 int run_step_converge_exact(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off,
                             int nbatch, double tol, int64_t cap, double alpha, double beta,
                             int64_t* iters_out, int32_t* capped_out) {
+  {
+    const int rc = run_exact_ordered(c, plan, batch_off, nbatch, 0, alpha, beta, true, tol, cap,
+                                     iters_out, capped_out);
+    if (rc != 1) return rc;
+  }
   cudaStream_t s = c->stream;
   std::vector<BatchRange> ranges;
   int rc = build_work(c, plan, batch_off, nbatch, 0, ranges);

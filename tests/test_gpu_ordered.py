@@ -139,3 +139,31 @@ def test_ordered_converge_on_device_matches_sequential(I, J, stage_ratings):
     eng.close()
     assert np.array_equal(gu.astype(np.float32), U[:, :k])
     assert np.array_equal(gv.astype(np.float32), V[:, :k])
+
+
+@pytest.mark.parametrize("I,J,stage_ratings,iters", [(1, 1, 10**9, 1), (3, 3, 700, 2),
+                                                     (2, 4, 300, 1), (4, 1, 10**9, 3)])
+def test_exact_ordered_bit_identical_to_reference(I, J, stage_ratings, iters):
+    """Exact mode runs the ordered schedule in fp64 with the reference's own
+    operation order (ordered_exact_kernel): factors and per-block SSEs equal the
+    oracle's restatement of the reference (pinned to the reference's golden
+    vectors) bit for bit, for any number of slabs per block."""
+    n, m, nnz, k = 400, 300, 12_000, 12
+    r, c, v = _data(n, m, nnz, 5, dup=0.05)
+    eng = bm.Engine(bm.EngineOptions(exact=True))
+    eng._opt("ord_stage_ratings", float(stage_ratings))
+    eng.partition(r, c, v, n, m, I, J)
+    u0, v0 = O.init_factors(n, m, k, 1)
+    eng.set_factors(u0, v0)
+    P = O.partition(r, c, v, n, m, I, J)
+    ou, ov = u0.copy(), v0.copy()
+    for s in range(3):
+        ids, off = eng.plan_arrays(bm.plan_step(I, J, s))
+        sse, bad = eng.run_step(ids, off, iters, 1e-3, 1e-2)
+        assert bad is None
+        osse, _, pos, _, _ = O.run_step(P, ou, ov, s, iters, 1e-3, 1e-2)
+        assert pos < 0
+        assert np.array_equal(sse, osse), np.abs(sse - osse).max()
+    gu, gv = eng.get_factors()
+    eng.close()
+    assert np.array_equal(gu, ou) and np.array_equal(gv, ov)
