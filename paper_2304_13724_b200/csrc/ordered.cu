@@ -36,7 +36,8 @@
 namespace bgmf {
 namespace {
 
-constexpr int kOrdThreads = 512;
+constexpr int kOrdThreads = 1024;   // fp32 ordered kernel: 32 warps, <= 64 registers
+constexpr int kExactThreads = 512;  // exact (fp64) kernel
 constexpr int kOrdMaxBlocks = 96;
 constexpr int kOrdMaxStages = 255;  // the row tag keeps slab + 1 in 8 bits
 constexpr uint32_t kGenLimit = 1u << 24;
@@ -527,12 +528,12 @@ __device__ __forceinline__ void exact_stage_sweep(const Stage& T, double* sv, do
   const int k = T.kp;
   double* us = urow + (threadIdx.x >> 5) * k;
   __syncthreads();
-  for (int i = threadIdx.x; i < T.nc; i += kOrdThreads) T.cnt[i] = T.qbase ? INT32_MAX : 0;
+  for (int i = threadIdx.x; i < T.nc; i += kExactThreads) T.cnt[i] = T.qbase ? INT32_MAX : 0;
   if (threadIdx.x == 0) *s_next = 0;
   __syncthreads();
   if (T.qbase) {
     const int e0 = __ldg(T.rp), e1 = __ldg(T.rp + T.h);
-    for (int i = e0 + (int)threadIdx.x; i < e1; i += kOrdThreads) {
+    for (int i = e0 + (int)threadIdx.x; i < e1; i += kExactThreads) {
       const int c = __ldg(T.bcol + i);
       if (c >= T.cs && c < T.ce) atomicMin(T.cnt + (c - T.cs), __ldg(T.bq + i));
     }
@@ -617,7 +618,7 @@ __device__ __forceinline__ void exact_stage_esq(const Stage& T, const double* sv
                                                 double* __restrict__ besq) {
   const int lane = threadIdx.x & 31;
   const int k = T.kp;
-  for (int r = (int)threadIdx.x / 32; r < T.h; r += kOrdThreads / 32) {
+  for (int r = (int)threadIdx.x / 32; r < T.h; r += kExactThreads / 32) {
     const int rb = __ldg(T.rp + r), re = __ldg(T.rp + r + 1);
     if (rb == re) continue;
     int lo = rb, hi = re;
@@ -657,7 +658,7 @@ __device__ __forceinline__ double exact_block_sse(const Stage& T, const double* 
   return *s_bcast;
 }
 
-__global__ void __launch_bounds__(kOrdThreads, 1)
+__global__ void __launch_bounds__(kExactThreads, 1)
 ordered_exact_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restrict__ lcol,
                      const double* __restrict__ val, const int32_t* __restrict__ qrank,
                      const int32_t* __restrict__ rowptr, double* __restrict__ U, int k,
@@ -710,7 +711,7 @@ ordered_exact_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restr
   const bool bulk = ((reinterpret_cast<uintptr_t>(gv) | ((size_t)T.nc * k * 8)) & 15) == 0;
   const unsigned bytes = bulk ? (unsigned)T.nc * (unsigned)k * 8u : 0u;
   if (!bulk)
-    for (int i = threadIdx.x; i < T.nc * k; i += kOrdThreads) sv[i] = __ldcg(gv + i);
+    for (int i = threadIdx.x; i < T.nc * k; i += kExactThreads) sv[i] = __ldcg(gv + i);
   const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
   const unsigned sva = (unsigned)__cvta_generic_to_shared(sv);
   if (threadIdx.x == 0) {
@@ -786,7 +787,7 @@ ordered_exact_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restr
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
   if (!bulk && swept > 0)
-    for (int i = threadIdx.x; i < T.nc * k; i += kOrdThreads) gv[i] = sv[i];
+    for (int i = threadIdx.x; i < T.nc * k; i += kExactThreads) gv[i] = sv[i];
   if (threadIdx.x == 0) {
     if (T.st == 0) sse[B.block_id] = sse_now;
     if (T.S > 1) {
@@ -888,11 +889,11 @@ const void* ordered_kernel_ptr(int kp, int warp) {
 size_t slab_smem(bgmf_ctx* c, int cols) {
   if (!c->exact) return (size_t)cols * ((size_t)c->kp * 4 + 4);
   const size_t slab = ((size_t)cols * ((size_t)c->k * 8 + 4) + 15) & ~(size_t)15;
-  return slab + (size_t)(kOrdThreads / 32) * c->k * 8;
+  return slab + (size_t)(kExactThreads / 32) * c->k * 8;
 }
 size_t row_bytes(bgmf_ctx* c) { return c->exact ? (size_t)c->k * 8 + 4 : (size_t)c->kp * 4 + 4; }
 size_t fixed_smem(bgmf_ctx* c) {
-  return c->exact ? 16 + (size_t)(kOrdThreads / 32) * c->k * 8 : 0;
+  return c->exact ? 16 + (size_t)(kExactThreads / 32) * c->k * 8 : 0;
 }
 
 // Largest dynamic shared memory a CTA may ask for (static smem aside).
@@ -918,7 +919,8 @@ int ordered_capacity(bgmf_ctx* c, size_t smem) {
   if (it != c->ord_cap.end()) return it->second;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_budget(c));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kOrdThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c->exact ? kExactThreads : kOrdThreads,
+                                                smem);
   c->ord_cap[key] = per_sm * c->num_sms;
   return per_sm * c->num_sms;
 }
@@ -1119,7 +1121,8 @@ int launch_items(bgmf_ctx* c, std::vector<OrdItem>& items, int iters, float alph
     if (c->timing) record_begin(c, 0, ratings * iters * (12.0 + 16.0 * c->k), &slot);
     BGMF_CK(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)budget));
-    BGMF_CK(c, cudaLaunchCooperativeKernel(fn, dim3(ctas), dim3(kOrdThreads),
+    BGMF_CK(c, cudaLaunchCooperativeKernel(fn, dim3(ctas),
+                                           dim3(c->exact ? kExactThreads : kOrdThreads),
                                            c->exact ? args64 : args, smem, s));
     if (slot) record_end(c, slot);
     i = j;
