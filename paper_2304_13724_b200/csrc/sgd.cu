@@ -87,13 +87,15 @@ struct Chunk {
   int64_t begin, end, bbeg, bend;
   int64_t row_start, col_start;
   int block_id, pos;
+  int w;  // work item
 };
 
 __device__ __forceinline__ Chunk locate_chunk(const BlockWork* __restrict__ work, int nwork,
                                               int total_chunks, int chunk) {
-  Chunk ch{0, 0, 0, 0, 0, 0, 0, 0};
+  Chunk ch{0, 0, 0, 0, 0, 0, 0, 0, -1};
   if (chunk < total_chunks) {
     const int w = find_work(work, nwork, chunk);
+    ch.w = w;
     const BlockWork bw = work[w];
     ch.begin = bw.begin + (int64_t)(chunk - bw.first_chunk) * bw.chunk_len;
     ch.end = min(ch.begin + (int64_t)bw.chunk_len, bw.end);
@@ -372,24 +374,20 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// The SSE walk of one chunk per group (all groups of the warp together:
+// the trip count is the warp's longest chunk).  Returns the group's sum
+// (valid in lane gl == 0).  `ring` = this thread's slice of the cp.async ring.
 template <int L, int V4, bool kMask, int D>
-__global__ void __launch_bounds__(256, 2)
-sse_async_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
-                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
-                 const float* __restrict__ val, const float* __restrict__ U,
-                 const float* __restrict__ V, int kp, double* __restrict__ sse, int cbits) {
+__device__ __forceinline__ double sse_async_walk(const Chunk& ch, const int32_t* __restrict__ lrow,
+                                                 const int32_t* __restrict__ lcol,
+                                                 const float* __restrict__ val,
+                                                 const float* __restrict__ U,
+                                                 const float* __restrict__ V, int kp, int cbits,
+                                                 float4* ring) {
   static_assert(D <= L, "the look-ahead must fit the two triple batches");
-  constexpr int GPW = 32 / L;
-  // this lane's D slots of V4 float4, lane-interleaved ([slot][q][thread]) so a
-  // warp's 16-byte accesses hit 32 consecutive bank quads
-  extern __shared__ float4 ring_all[];
-  float4* ring = ring_all + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
   const int len = (int)(ch.end - ch.begin);
   const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
-  if (maxlen == 0) return;
+  if (maxlen == 0) return 0.0;
   const Lanes<L, V4, kMask> ln(kp);
   const float* Ub = U + ch.row_start * kp;
   const float* Vb = V + ch.col_start * kp;
@@ -537,7 +535,106 @@ sse_async_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks
   }
   }
   cp_async_wait<0>();
-  if ((lane & (L - 1)) == 0 && len > 0) atomicAdd(sse + ch.block_id, acc);
+  return acc;
+}
+
+template <int L, int V4, bool kMask, int D>
+__global__ void __launch_bounds__(256, 2)
+sse_async_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
+                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
+                 const float* __restrict__ val, const float* __restrict__ U,
+                 const float* __restrict__ V, int kp, double* __restrict__ sse, int cbits) {
+  constexpr int GPW = 32 / L;
+  // this lane's D slots of V4 float4, lane-interleaved ([slot][q][thread]) so a
+  // warp's 16-byte accesses hit 32 consecutive bank quads
+  extern __shared__ float4 ring_all[];
+  const int lane = threadIdx.x & 31;
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
+  const double acc = sse_async_walk<L, V4, kMask, D>(ch, lrow, lcol, val, U, V, kp, cbits,
+                                                      ring_all + threadIdx.x);
+  if ((lane & (L - 1)) == 0 && ch.end > ch.begin) atomicAdd(sse + ch.block_id, acc);
+}
+
+// Sweep and post-sweep SSE of a stratum in ONE launch.  Phase 1 is
+// sgd_fast_kernel (one chunk per group, one wave); a group that finishes its
+// chunk counts it into done[w] (after a fence: its V reductions and U stores
+// are visible first).  Phase 2: warps take SSE slots (GPW consecutive SSE
+// chunks of one block) of blocks whose sweep is complete (done[w] equals the
+// block's sweep chunks), from per-block slot counters -- so the SSE of early
+// blocks fills the tail of the sweep of late ones, with no second launch.
+// The SSE is an order-free sum (atomicAdd per group), as in sse_async_kernel.
+// done / next: 2 * nwork counters, zeroed before the launch.
+template <int L, int V4, bool kMask, int D>
+__global__ void __launch_bounds__(256, 2)
+sweep_sse_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
+                 const BlockWork* __restrict__ swork, const int32_t* __restrict__ lrow,
+                 const int32_t* __restrict__ lcol, const float* __restrict__ val,
+                 float* __restrict__ U, float* __restrict__ V, int kp, float alpha, float beta,
+                 int iter, unsigned long long* __restrict__ bad, double* __restrict__ sse,
+                 unsigned* __restrict__ done, int cbits) {
+  constexpr int GPW = 32 / L;
+  extern __shared__ float4 ring_all[];
+  const int lane = threadIdx.x & 31;
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  {
+    const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
+    const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
+    if (maxlen > 0)
+      walk_chunk<L, V4, kMask, true>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter,
+                                     bad, cbits);
+    if ((lane & (L - 1)) == 0 && ch.w >= 0) {
+      __threadfence();
+      atomicAdd(done + ch.w, 1u);
+    }
+  }
+  unsigned* next = done + nwork;
+  const int gl = lane & (L - 1), g = lane / L;
+  unsigned long long t0 = 0;
+  for (unsigned poll = 0;; ++poll) {
+    // lane 0 picks a swept block with unclaimed SSE slots
+    int pick = -1, slot = 0, left = 0;
+    if (lane == 0) {
+      for (int i = 0; i < nwork; ++i) {
+        const int w = (warp + i) % nwork;
+        const BlockWork bw = swork[w];
+        const int nch = (int)((bw.end - bw.begin + bw.chunk_len - 1) / bw.chunk_len);
+        const int slots = (nch + GPW - 1) / GPW;
+        if ((int)*((volatile unsigned*)(next + w)) >= slots) continue;
+        ++left;
+        const BlockWork sw = work[w];
+        const unsigned need = (unsigned)((sw.end - sw.begin + sw.chunk_len - 1) / sw.chunk_len);
+        unsigned d;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(done + w) : "memory");
+        if (d < need) continue;
+        const int got = (int)atomicAdd(next + w, 1u);
+        if (got < slots) { pick = w; slot = got; break; }
+      }
+    }
+    pick = __shfl_sync(kFull, pick, 0);
+    left = __shfl_sync(kFull, left, 0);
+    if (pick < 0) {
+      if (left == 0) break;  // every SSE slot is taken
+      if ((poll & 1023u) == 1023u) {  // bounded: a lost counter must not hang the GPU
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (!t0) t0 = t; else if (t - t0 > 20000000000ull) __trap();
+      }
+      __nanosleep(128);
+      continue;
+    }
+    slot = __shfl_sync(kFull, slot, 0);
+    const BlockWork bw = swork[pick];
+    Chunk ch{0, 0, 0, 0, bw.row_start, bw.col_start, bw.block_id, bw.pos, pick};
+    const int64_t c0 = (int64_t)(slot * GPW + g) * bw.chunk_len;
+    ch.bbeg = bw.begin;
+    ch.bend = bw.end;
+    ch.begin = min(bw.begin + c0, bw.end);
+    ch.end = min(ch.begin + (int64_t)bw.chunk_len, bw.end);
+    const double acc = sse_async_walk<L, V4, kMask, D>(ch, lrow, lcol, val, U, V, kp, cbits,
+                                                        ring_all + threadIdx.x);
+    if (gl == 0 && ch.end > ch.begin) atomicAdd(sse + ch.block_id, acc);
+  }
 }
 
 // Post-sweep SSE, wide form: no update dependency, so each group keeps D
@@ -853,6 +950,31 @@ void launch_fast(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, const B
                   it);
 }
 
+// One stratum's last sweep + its SSE as ONE launch (sweep_sse_kernel), on the
+// sweep's grid; its completion counters (2 per work item) are zeroed first.
+// Returns false when the shape has no fused instance (the caller launches the
+// two kernels).
+bool launch_sweep_sse(const Shape& sh, dim3 grid, cudaStream_t s, const BlockWork* w,
+                      const BlockWork* sw, int nwork, int total, bgmf_ctx* c, float a, float b,
+                      int it) {
+  const bool mk = needs_mask(sh, c->kp);
+  if (cudaMemsetAsync(c->d_fuse, 0, sizeof(unsigned) * 2 * nwork, s) != cudaSuccess) return false;
+#define BGMF_FUSED(LL, VV, MM)                                                                \
+  if (sh.L == LL && sh.V4 == VV && mk == MM) {                                                \
+    constexpr int D = LL < 4 ? LL : 4;                                                        \
+    const int smem = 256 * D * VV * 16;                                                       \
+    cudaFuncSetAttribute(&sweep_sse_kernel<LL, VV, MM, D>,                                    \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                   \
+    sweep_sse_kernel<LL, VV, MM, D><<<grid, 256, smem, s>>>(                                  \
+        w, nwork, total, sw, c->d_lrow, c->d_lcol, c->d_val, c->d_u, c->d_v, c->kp, a, b, it,  \
+        c->d_bad, c->d_sse, c->d_fuse, -1);                                                   \
+    return true;                                                                              \
+  }
+  BGMF_SHAPES(BGMF_FUSED)
+#undef BGMF_FUSED
+  return false;
+}
+
 const void* epoch_kernel_ptr(const Shape& sh, int kp) {
   const bool mk = needs_mask(sh, kp);
 #define BGMF_EP(LL, VV, MM)                            \
@@ -1060,6 +1182,7 @@ __global__ void broadcast_v(const T* __restrict__ V, T* __restrict__ priv, int64
 
 int ensure_step_scratch(bgmf_ctx* c, size_t nwork) {
   const int nb = c->I * c->J;
+  if (!c->d_fuse) BGMF_CK(c, dmalloc(&c->d_fuse, sizeof(unsigned) * 2 * (nb > 64 ? nb : 64), c->stream));
   if (!c->d_sse) {
     BGMF_CK(c, dmalloc(&c->d_sse, sizeof(double) * (nb > 0 ? nb : 1), c->stream));
     BGMF_CK(c, pinned_alloc((void**)&c->h_sse, sizeof(double) * (nb > 0 ? nb : 1)));
@@ -1164,13 +1287,20 @@ int run_step_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in,
       double br = 0;
       for (int q = 0; q < r.nw; ++q)
         br += (double)(c->h_work[r.w0 + q].end - c->h_work[r.w0 + q].begin);
+      const BatchRange& sr = sranges[t];
+      const bool fuse = c->fuse_sse && sr.nw == r.nw && c->sse_async > 0 && !c->sse_wide &&
+                        !c->bulk_red;
+      bool fused_done = false;
       for (int it = 0; it < iters; ++it) {
         TimedLaunch* slot = nullptr;
         if (c->timing) record_begin(c, 0, br * (12.0 + 16.0 * c->k), &slot);
-        launch_fast(true, sh, grid, s, w, r.nw, r.chunks, c, alpha, beta, it);
+        if (fuse && it == iters - 1)  // the last sweep and the SSE: one launch
+          fused_done = launch_sweep_sse(sh, grid, s, w, c->d_work + sr.w0, r.nw, r.chunks, c,
+                                        alpha, beta, it);
+        if (!fused_done) launch_fast(true, sh, grid, s, w, r.nw, r.chunks, c, alpha, beta, it);
         if (slot) record_end(c, slot);
       }
-      const BatchRange& sr = sranges[t];
+      if (fused_done) continue;
       const dim3 sgrid(((sr.chunks + gpw - 1) / gpw + 7) / 8);
       TimedLaunch* slot = nullptr;
       if (c->timing) record_begin(c, 1, 0.0, &slot);
@@ -1321,14 +1451,22 @@ int step_batch(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off_in, in
     double br = 0;
     for (int q = 0; q < r.nw; ++q)
       br += (double)(c->h_work[r.w0 + q].end - c->h_work[r.w0 + q].begin);
+    const BatchRange& sr = sranges[t];
+    const bool fuse = c->fuse_sse && sr.nw == r.nw && c->sse_async > 0 && !c->sse_wide &&
+                      !c->bulk_red;
+    bool fused_done = false;
     for (int it = 0; it < iters; ++it) {
       TimedLaunch* slot = nullptr;
       if (c->timing) record_begin(c, 0, br * (12.0 + 16.0 * c->k), &slot);
-      launch_fast(true, sh, grid, c->stream, c->d_work + r.w0, r.nw, r.chunks, c, alpha, beta,
-                  it);
+      if (fuse && it == iters - 1)  // the last sweep and the SSE: one launch
+        fused_done = launch_sweep_sse(sh, grid, c->stream, c->d_work + r.w0, c->d_work + sr.w0,
+                                      r.nw, r.chunks, c, alpha, beta, it);
+      if (!fused_done)
+        launch_fast(true, sh, grid, c->stream, c->d_work + r.w0, r.nw, r.chunks, c, alpha, beta,
+                    it);
       if (slot) record_end(c, slot);
     }
-    const BatchRange& sr = sranges[t];
+    if (fused_done) continue;
     const dim3 sgrid(((sr.chunks + gpw - 1) / gpw + 7) / 8);
     TimedLaunch* slot = nullptr;
     if (c->timing) record_begin(c, 1, 0.0, &slot);
