@@ -69,6 +69,18 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // smem ring of V-row deltas per group for the bulk path
 constexpr int kBulkBufs = 4;
 
@@ -175,7 +187,13 @@ __device__ __forceinline__ void store_row(float* row, const float4 (&u)[V4], con
 // evaluated as t = 2ae*v - ab*u (FFMA2 of an FMUL2) and u + t, in packed fp32.
 // All lanes of the warp execute the same trip count (maxlen) so the shuffles
 // stay converged; groups past their chunk end are predicated off.
-template <int L, int V4, bool kMask, bool kSweep, bool kBulk = false>
+// MODE 0: plain; 1 (bulk): V deltas through the TMA bulk reduce; 2 (uring):
+// the U row of a run starting UD ratings ahead is requested into a per-lane
+// shared-memory ring by cp.async (sbuf = this thread's slice), so short user
+// runs -- skewed or very sparse blocks, ~1-3 ratings per run -- do not wait a
+// DRAM round trip at every run switch (the register prefetch leads by one
+// rating only).
+template <int L, int V4, bool kMask, bool kSweep, int MODE = 0>
 __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
                                              const int32_t* __restrict__ lrow,
                                              const int32_t* __restrict__ lcol,
@@ -183,6 +201,9 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
                                              int kp, float alpha, float beta, int iter,
                                              unsigned long long* bad, int cbits = -1,
                                              float* sbuf = nullptr) {
+  constexpr bool kBulk = MODE == 1;
+  constexpr bool kURing = MODE == 2 && kSweep && L >= 4;
+  constexpr int UD = L >= 8 ? 4 : 3;  // ring depth (needs UD < L: rows from batches A, B)
   const Lanes<L, V4, kMask> ln(kp);
   int nbulk = 0;  // bulk ops issued by this group (ring position)
   const int len = (int)(ch.end - ch.begin);
@@ -216,6 +237,29 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
   double acc = 0.0;
   const float two_a = 2.0f * alpha;
   const float2 nab = make_float2(-alpha * beta, -alpha * beta);
+  float4* uring = reinterpret_cast<float4*>(sbuf);
+  // row of rating i of the two triple batches (i < 2L), for the ring
+  auto row_at = [&](int i) {
+    const int v = __shfl_sync(kFull, i < L ? rA : rB, ln.gbase + (i & (L - 1)));
+    return v;
+  };
+  auto u_issue = [&](int t, int row, bool start) {  // U row of rating t -> slot t % UD
+    if (t < len && start) {
+      float4* slot = uring + (t % UD) * V4 * 256;
+      const float* src = Ub + (int64_t)row * kp;
+#pragma unroll
+      for (int q = 0; q < V4; ++q)
+        if (ln.on(q)) cp_async16(slot + q * 256, src + ln.off(q));
+    }
+    cp_async_commit();
+  };
+  if (kURing) {
+#pragma unroll
+    for (int d = 1; d <= UD; ++d) {
+      const int rd = row_at(d), rp = row_at(d - 1);
+      u_issue(d, rd, rd != rp);
+    }
+  }
 
   for (int t0 = 0; t0 < maxlen; t0 += L) {
 #pragma unroll 1
@@ -232,7 +276,18 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
       const bool newrun = nvalid && rn != r;
       float4 vn[V4], un[V4];
       if (nvalid) load_row<V4>(vn, Vb + (int64_t)cn * kp, ln);
-      if (newrun) load_row<V4>(un, Ub + (int64_t)rn * kp, ln);
+      if (kURing) {
+        cp_async_wait<UD - 1>();  // rating t+1's U row has landed (when it starts a run)
+        if (newrun) {
+          const float4* slot = uring + ((t + 1) % UD) * V4 * 256;
+#pragma unroll
+          for (int q = 0; q < V4; ++q) un[q] = ln.on(q) ? slot[q * 256] : zero4();
+        }
+        const int ri = row_at(j + 1 + UD), rp = row_at(j + UD);
+        u_issue(t + 1 + UD, ri, ri != rp);
+      } else if (newrun) {
+        load_row<V4>(un, Ub + (int64_t)rn * kp, ln);
+      }
 
       const float dot = group_sum<L>(dot_slice<V4>(u, v));
       const float e = x - dot;
@@ -309,10 +364,11 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
     if (nb < len) load_triple(lrow, lcol, val, cbits, ch.begin + nb, rB, cB, xB);
   }
   if (kSweep && kBulk && ln.gl == 0) bulk_wait_all();
+  if (kURing) cp_async_wait<0>();
   return acc;
 }
 
-template <int L, int V4, bool kMask, bool kBulk>
+template <int L, int V4, bool kMask, int MODE>
 __global__ void __launch_bounds__(256, 2)
 sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
@@ -326,11 +382,13 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
   const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
   const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
   if (maxlen == 0) return;
-  // this group's delta ring: kBulkBufs rows of kp floats
-  float* sbuf = reinterpret_cast<float*>(smem_rows) +
-                (size_t)((threadIdx.x >> 5) * GPW + lane / L) * kBulkBufs * kp;
-  walk_chunk<L, V4, kMask, true, kBulk>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter,
-                                        bad, cbits, sbuf);
+  // bulk: this group's delta ring, kBulkBufs rows of kp floats; uring: this
+  // thread's slice of the U-row ring ([slot][q][thread] float4)
+  float* sbuf = MODE == 2 ? reinterpret_cast<float*>(smem_rows + threadIdx.x)
+                          : reinterpret_cast<float*>(smem_rows) +
+                                (size_t)((threadIdx.x >> 5) * GPW + lane / L) * kBulkBufs * kp;
+  walk_chunk<L, V4, kMask, true, MODE>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter,
+                                       bad, cbits, sbuf);
 }
 
 // Post-sweep SSE of each block: sum over the chunk of (x - u.v)^2 in fp64,
@@ -362,17 +420,6 @@ sse_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
 // reads back what it copied itself, so cp.async.wait_group is the only
 // synchronisation.  U stays in registers for a user's run (next run's row
 // prefetched one rating ahead, as in walk_chunk).  Requires D <= L.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 // The SSE walk of one chunk per group (all groups of the warp together:
 // the trip count is the warp's longest chunk).  Returns the group's sum
@@ -923,13 +970,20 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
 #define BGMF_CASE(LL, VV, MM)                                                                 \
   if (sh.L == LL && sh.V4 == VV && mk == MM) {                                                \
     if (sweep && c->bulk_red) {                                                               \
-      cudaFuncSetAttribute(&sgd_fast_kernel<LL, VV, MM, true>,                               \
+      cudaFuncSetAttribute(&sgd_fast_kernel<LL, VV, MM, 1>,                                  \
                            cudaFuncAttributeMaxDynamicSharedMemorySize,                       \
                            (int)bulk_smem(c, sh));                                            \
-      sgd_fast_kernel<LL, VV, MM, true><<<grid, 256, bulk_smem(c, sh), s>>>(                  \
+      sgd_fast_kernel<LL, VV, MM, 1><<<grid, 256, bulk_smem(c, sh), s>>>(                     \
+          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
+    } else if (sweep && c->u_ring && LL >= 4) {                                               \
+      constexpr int UD = LL >= 8 ? 4 : 3;                                                     \
+      const int sm = 256 * UD * VV * 16;                                                      \
+      cudaFuncSetAttribute(&sgd_fast_kernel<LL, VV, MM, 2>,                                  \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                  \
+      sgd_fast_kernel<LL, VV, MM, 2><<<grid, 256, sm, s>>>(                                   \
           w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
     } else if (sweep)                                                                         \
-      sgd_fast_kernel<LL, VV, MM, false><<<grid, 256, 0, s>>>(                                \
+      sgd_fast_kernel<LL, VV, MM, 0><<<grid, 256, 0, s>>>(                                    \
           w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
     else if (c->sse_wide)                                                                     \
       launch_sse_wide(s, w, nwork, total, lrow, lcol, val, c, cbits);                          \
@@ -989,8 +1043,8 @@ const void* sweep_kernel_ptr(const Shape& sh, int kp, bool bulk) {
   const bool mk = needs_mask(sh, kp);
 #define BGMF_SW(LL, VV, MM)                                                             \
   if (sh.L == LL && sh.V4 == VV && mk == MM)                                            \
-    return bulk ? reinterpret_cast<const void*>(&sgd_fast_kernel<LL, VV, MM, true>)     \
-                : reinterpret_cast<const void*>(&sgd_fast_kernel<LL, VV, MM, false>);
+    return bulk ? reinterpret_cast<const void*>(&sgd_fast_kernel<LL, VV, MM, 1>)        \
+                : reinterpret_cast<const void*>(&sgd_fast_kernel<LL, VV, MM, 0>);
   BGMF_SHAPES(BGMF_SW)
 #undef BGMF_SW
   return nullptr;
