@@ -11,8 +11,10 @@ with `blockmf` aliased to paper_2304_13724_b200 (bgmf_alias.py):
   fast  -- the default fp32 engine (ordered sweep where the schedule routes
            it, chunked elsewhere).
 Files: test_{kernel,partition,scheduler,trainer,metrics,baselines}.py (the
-hot-path suites), plus test_core.py / test_data_io.py (API value types and
-file formats the drop-in also provides) and conftest.py."""
+hot-path suites), test_core.py / test_data_io.py (API value types and file
+formats the drop-in also provides), test_cli.py with the reference's cli.py and
+report.py loaded over the drop-in (the CLI's VARIANTS plug-in path; matplotlib
+is absent here, so figures are placeholder files), and conftest.py."""
 
 import os
 import shutil
@@ -23,7 +25,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REF = "/root/reference/pkg/tests"
 FILES = ["conftest.py", "test_kernel.py", "test_partition.py", "test_scheduler.py",
          "test_trainer.py", "test_metrics.py", "test_baselines.py", "test_core.py",
-         "test_data_io.py"]
+         "test_data_io.py", "test_cli.py"]
+# the reference's CLI and report modules, loaded on top of the drop-in as
+# blockmf.cli / blockmf.report (bgmf_alias.py): its VARIANTS table then holds
+# this package's trainers
+SRC = "/root/reference/pkg/src/blockmf"
+SRC_FILES = ["cli.py", "report.py"]
 
 
 def sync() -> None:
@@ -31,7 +38,9 @@ def sync() -> None:
     os.makedirs(dst, exist_ok=True)
     for f in FILES:
         shutil.copyfile(os.path.join(REF, f), os.path.join(dst, f))
-    print(f"copied {len(FILES)} files from {REF} to {dst}")
+    for f in SRC_FILES:
+        shutil.copyfile(os.path.join(SRC, f), os.path.join(dst, f))
+    print(f"copied {len(FILES) + len(SRC_FILES)} files from {REF}, {SRC} to {dst}")
 
 
 def run(mode: str, extra: list[str]) -> int:
