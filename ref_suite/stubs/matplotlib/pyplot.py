@@ -8,8 +8,8 @@ class _Any:
     def __call__(self, *args, **kwargs):
         return _Any()
 
-    def __iter__(self):
-        return iter([_Any(), _Any()])
+    def __iter__(self):  # `(line,) = ax.plot(...)`: one artist
+        return iter([_Any()])
 
     def savefig(self, path, *args, **kwargs):
         savefig(path)
@@ -29,8 +29,17 @@ def savefig(path, *args, **kwargs):
         f.write(b"placeholder figure (matplotlib absent)\n")
 
 
-def subplots(*args, **kwargs):
-    return _Any(), _Any()
+class _Axes(_Any):
+    def __init__(self, n):
+        self.n = n
+
+    def __iter__(self):  # `fig, (a, b) = plt.subplots(1, 2)`
+        return iter([_Any() for _ in range(self.n)])
+
+
+def subplots(nrows=1, ncols=1, *args, **kwargs):
+    n = nrows * ncols
+    return _Any(), (_Axes(n) if n > 1 else _Any())
 
 
 rcParams = {}
