@@ -64,6 +64,7 @@ struct bgmf_ctx {
   bool bulk_red = false;  // V deltas via TMA bulk reduce (measured slower: SM->L2 bound)
   bool sse_wide = false;  // post-sweep SSE with D ratings in flight (measured slower)
   bool sse_async = true;  // post-sweep SSE through a per-lane cp.async ring (sse_async_kernel)
+  bool pdl = true;        // programmatic dependent launch between sweep / SSE kernels
   bool u_ring = false;    // sweep: U rows of upcoming runs via a cp.async smem ring
   bool fuse_sse = false;  // last sweep + SSE in one launch (sweep_sse_kernel; measured slower)
   unsigned* d_fuse = nullptr;  // sweep_sse_kernel's per-work-item counters

@@ -220,6 +220,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "no_val8")) c->no_val8 = value != 0.0;
   else if (!strcmp(key, "fuse_sse")) c->fuse_sse = value != 0.0;
   else if (!strcmp(key, "u_ring")) c->u_ring = value != 0.0;
+  else if (!strcmp(key, "pdl")) c->pdl = value != 0.0;
   else if (!strcmp(key, "ord_col_conc")) c->ord_col_conc = value;
   else if (!strcmp(key, "ord_warp")) c->ord_warp = value != 0.0;
   else if (!strcmp(key, "ord_stage_ratings"))

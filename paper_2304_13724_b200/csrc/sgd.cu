@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <utility>
 
 #include <atomic>
 
@@ -80,6 +81,16 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+
+// Programmatic dependent launch: a sweep / SSE kernel lets the next one be
+// scheduled as soon as SMs free up (trigger), and waits for the previous
+// grid's completion and memory before touching factors (wait); the work table
+// and ratings it reads first are not written by that grid.  Without the
+// launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // smem ring of V-row deltas per group for the bulk path
 constexpr int kBulkBufs = 4;
@@ -381,7 +392,9 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
   const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
   const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
+  pdl_trigger();
   if (maxlen == 0) return;
+  pdl_wait();
   // bulk: this group's delta ring, kBulkBufs rows of kp floats; uring: this
   // thread's slice of the U-row ring ([slot][q][thread] float4)
   float* sbuf = MODE == 2 ? reinterpret_cast<float*>(smem_rows + threadIdx.x)
@@ -598,6 +611,8 @@ sse_async_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks
   const int lane = threadIdx.x & 31;
   const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
+  pdl_trigger();
+  pdl_wait();
   const double acc = sse_async_walk<L, V4, kMask, D>(ch, lrow, lcol, val, U, V, kp, cbits,
                                                       ring_all + threadIdx.x);
   if ((lane & (L - 1)) == 0 && ch.end > ch.begin) atomicAdd(sse + ch.block_id, acc);
@@ -899,6 +914,23 @@ __global__ void block_exact_kernel(const BlockWork* __restrict__ work, int nwork
   o[1] = s; o[2] = (double)it; o[3] = 1.0;
 }
 
+// <<<>>> with the programmatic-dependent-launch attribute when pdl is set
+template <typename... KArgs, typename... Args>
+void launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, int block, size_t smem, cudaStream_t s,
+              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 // ------------------------------------------------------------ dispatch
 
 // SSE pass shape: 8 floats per lane (V4 = 2) unless the row is wider than
@@ -954,8 +986,8 @@ void launch_sse_async(dim3 grid, cudaStream_t s, const BlockWork* w, int nwork, 
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr_set.fetch_or(bit);
   }
-  sse_async_kernel<LL, VV, MM, D><<<grid, 256, smem, s>>>(w, nwork, total, lrow, lcol, val,
-                                                          c->d_u, c->d_v, c->kp, c->d_sse, cbits);
+  launch_k(c->pdl, &sse_async_kernel<LL, VV, MM, D>, grid, 256, smem, s, w, nwork, total, lrow,
+           lcol, val, (const float*)c->d_u, (const float*)c->d_v, c->kp, c->d_sse, cbits);
 }
 
 // dynamic smem of the bulk sweep: kBulkBufs delta rows per group
@@ -983,8 +1015,8 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
       sgd_fast_kernel<LL, VV, MM, 2><<<grid, 256, sm, s>>>(                                   \
           w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
     } else if (sweep)                                                                         \
-      sgd_fast_kernel<LL, VV, MM, 0><<<grid, 256, 0, s>>>(                                    \
-          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
+      launch_k(c->pdl, &sgd_fast_kernel<LL, VV, MM, 0>, grid, 256, 0, s, w, nwork, total, lrow,   \
+               lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);                    \
     else if (c->sse_wide)                                                                     \
       launch_sse_wide(s, w, nwork, total, lrow, lcol, val, c, cbits);                          \
     else if (c->sse_async > 0)                                                                \
