@@ -26,6 +26,11 @@ struct BlockWork {
   int32_t first_chunk;          // exclusive prefix of chunk counts in batch
   int32_t block_id;             // bi * J + bj
   int32_t pos;                  // position in the step plan
+  // device-side ConvergeEachBlock (run_step_converge_fast): the block's
+  // active flag (its chunks do nothing once it is 0) and the current
+  // iteration; nullptr everywhere else
+  const int32_t* active;
+  const int32_t* iter;
 };
 
 // Divergence record: smaller = earlier in the reference's order
@@ -64,6 +69,10 @@ struct bgmf_ctx {
   bool bulk_red = false;  // V deltas via TMA bulk reduce (measured slower: SM->L2 bound)
   bool sse_wide = false;  // post-sweep SSE with D ratings in flight (measured slower)
   bool sse_async = true;  // post-sweep SSE through a per-lane cp.async ring (sse_async_kernel)
+  bool conv_graph = true;  // ConvergeEachBlock loop as a CUDA-graph WHILE node (chunked path)
+  void* d_cstate = nullptr;  // its per-block state (ConvState, flags, iteration)
+  int cstate_cap = 0;
+  std::map<std::string, cudaGraphExec_t> conv_graphs;  // instantiated converge graphs per batch
   bool pdl = true;        // programmatic dependent launch between sweep / SSE kernels
   bool u_ring = false;    // sweep: U rows of upcoming runs via a cp.async smem ring
   bool fuse_sse = false;  // last sweep + SSE in one launch (sweep_sse_kernel; measured slower)
@@ -277,6 +286,8 @@ int step_end(bgmf_ctx* c, double* sse_out, int64_t* bad_out);
 int step_end_async(bgmf_ctx* c, double* d_sse_out, unsigned long long* d_bad_out);
 // wait until no asynchronous step's work-table copy is pending (sgd.cu)
 void drain_async_steps(bgmf_ctx* c);
+// drop the cached converge graphs (they capture device pointers)
+void conv_graphs_release(bgmf_ctx* c);
 // unmap peer buffers, free IPC-exportable ones (peer.cu)
 void peer_release(bgmf_ctx* c);
 int run_steps(bgmf_ctx* c, int nsteps, const int32_t* plans, const int32_t* offs,

@@ -186,7 +186,7 @@ void bgmf_destroy(bgmf_ctx* c) {
   order_release(c);
   prof_mark(c, "destroy: factors/holdout/stream");
   dfree(c->d_lrow, c->stream); dfree(c->d_lcol, c->stream); dfree(c->d_val, c->stream); dfree(c->d_val64, c->stream);
-  dfree(c->d_order, c->stream); dfree(c->d_fuse, c->stream); dfree(c->d_sse, c->stream); dfree(c->d_bad, c->stream); dfree(c->d_work, c->stream);
+  dfree(c->d_order, c->stream); dfree(c->d_fuse, c->stream); dfree(c->d_cstate, c->stream); conv_graphs_release(c); dfree(c->d_sse, c->stream); dfree(c->d_bad, c->stream); dfree(c->d_work, c->stream);
   dfree(c->d_partials, c->stream);
   dfree(c->d_priv, c->stream);
   cudaStreamSynchronize(c->stream);
@@ -221,6 +221,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "fuse_sse")) c->fuse_sse = value != 0.0;
   else if (!strcmp(key, "u_ring")) c->u_ring = value != 0.0;
   else if (!strcmp(key, "pdl")) c->pdl = value != 0.0;
+  else if (!strcmp(key, "conv_graph")) c->conv_graph = value != 0.0;
   else if (!strcmp(key, "ord_col_conc")) c->ord_col_conc = value;
   else if (!strcmp(key, "ord_warp")) c->ord_warp = value != 0.0;
   else if (!strcmp(key, "ord_stage_ratings"))
@@ -237,7 +238,7 @@ int bgmf_partition(bgmf_ctx* c, const int64_t* rows, const int64_t* cols, const 
   cudaSetDevice(c->device);
   if (c->streaming) stream_free(c);
   // the step scratch is sized by the grid
-  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_fuse, c->stream); c->d_fuse = nullptr; dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
+  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_fuse, c->stream); c->d_fuse = nullptr; dfree(c->d_cstate, c->stream); c->d_cstate = nullptr; c->cstate_cap = 0; conv_graphs_release(c); dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
   return partition_device(c, rows, cols, vals, nnz, n, m, grid_i, grid_j);
 }
@@ -248,7 +249,7 @@ int bgmf_partition_rows(bgmf_ctx* c, const int64_t* rows, const int64_t* cols,
   if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
   cudaSetDevice(c->device);
   if (c->streaming) stream_free(c);
-  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_fuse, c->stream); c->d_fuse = nullptr; dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
+  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_fuse, c->stream); c->d_fuse = nullptr; dfree(c->d_cstate, c->stream); c->d_cstate = nullptr; c->cstate_cap = 0; conv_graphs_release(c); dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
   return partition_device(c, rows, cols, vals, nnz, n, m, grid_i, grid_j, false, row_lo, row_hi);
 }
@@ -260,7 +261,7 @@ int bgmf_synth_partition(bgmf_ctx* c, int64_t n, int64_t m, int64_t nnz, uint64_
     return fail(c, BGMF_ERR_ARG, "bad synthetic shape");
   cudaSetDevice(c->device);
   if (c->streaming) stream_free(c);
-  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_fuse, c->stream); c->d_fuse = nullptr; dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
+  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_fuse, c->stream); c->d_fuse = nullptr; dfree(c->d_cstate, c->stream); c->d_cstate = nullptr; c->cstate_cap = 0; conv_graphs_release(c); dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
   const size_t N = (size_t)(nnz > 0 ? nnz : 1);
   int64_t *r = nullptr, *q = nullptr;
@@ -593,7 +594,7 @@ int bgmf_partition_ooc(bgmf_ctx* c, const int64_t* rows, const int64_t* cols,
                        int64_t row_lo, int64_t row_hi) {
   if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
   cudaSetDevice(c->device);
-  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_fuse, c->stream); c->d_fuse = nullptr; dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
+  dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_fuse, c->stream); c->d_fuse = nullptr; dfree(c->d_cstate, c->stream); c->d_cstate = nullptr; c->cstate_cap = 0; conv_graphs_release(c); dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
   return partition_ooc(c, rows, cols, vals, nnz, n, m, grid_i, grid_j, device_budget,
                        slot_ratings, nslots, row_lo, row_hi);

@@ -1193,8 +1193,6 @@ int run_shards_ordered(bgmf_ctx* c, const int32_t* r0, const int32_t* r1, int ns
   return launch_items(c, items, 1, alpha, beta, false, 0.0, sse_dev);
 }
 
-// Ordered routing of one batch: mode 1 = every block the kernel can take;
-// -1 (auto) = the same; 0 = never.  All blocks of the batch must qualify.
 // Routing of one batch.  ord_mode 1: ordered whenever every block fits;
 // 0: never; -1 (auto): ordered when it fits and the chunked sweep would
 // distort the reference order -- a dense block (> 1/8 of its cells rated:
@@ -1205,8 +1203,11 @@ int run_shards_ordered(bgmf_ctx* c, const int32_t* r0, const int32_t* r1, int ns
 // was in one of these; C1-C5 single-GPU strata are in none.  Ring ranks set
 // ord_col_conc = 6 (their 2-block launches of C4 run up to 4.0 groups per V
 // row -- block_chunk's (ratings per column - 32) / 80 -- measured within
-// 2e-5, and the randomised ring sweeps cover worlds 2-4).
-// converge: always when it fits.
+// 2e-5, and the randomised ring sweeps cover worlds 2-4).  ConvergeEachBlock
+// routes the same way; both paths run its per-block loop on the device (the
+// ordered kernel in-launch, the chunked one as a CUDA-graph WHILE node).
+// Exact mode: always the ordered schedule when it fits (fp64, bit-identical).
+//
 // The auto rule's risk test alone (no feasibility): would the chunked sweep
 // of this batch distort the reference order (a dense block, split rows, or
 // too many groups per V row)?
@@ -1237,10 +1238,8 @@ bool use_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, bool converge
   for (int q = q0; q < q1; ++q)
     if (c->h_offsets[plan[q] + 1] > c->h_offsets[plan[q]] && !ordered_block_ok(c, plan[q]))
       return false;
-  // ConvergeEachBlock: the per-block loop (sweep, SSE, improvement test)
-  // runs on the device only in the ordered kernel, and its stopping
-  // decisions then see the reference's sequential trajectory
-  if (c->ord_mode > 0 || converge) return true;
+  if (c->ord_mode > 0) return true;
+  (void)converge;  // ConvergeEachBlock routes like fixed schedules: both paths loop on the device
   return order_risky(c, plan, q0, q1);
 }
 

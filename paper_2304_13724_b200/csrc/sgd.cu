@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <string>
 #include <utility>
 
 #include <atomic>
@@ -110,12 +111,13 @@ struct Chunk {
   int64_t begin, end, bbeg, bend;
   int64_t row_start, col_start;
   int block_id, pos;
-  int w;  // work item
+  int w;     // work item
+  int iter;  // the work item's device-side iteration, or -1 (the launch's)
 };
 
 __device__ __forceinline__ Chunk locate_chunk(const BlockWork* __restrict__ work, int nwork,
                                               int total_chunks, int chunk) {
-  Chunk ch{0, 0, 0, 0, 0, 0, 0, 0, -1};
+  Chunk ch{0, 0, 0, 0, 0, 0, 0, 0, -1, -1};
   if (chunk < total_chunks) {
     const int w = find_work(work, nwork, chunk);
     ch.w = w;
@@ -128,6 +130,8 @@ __device__ __forceinline__ Chunk locate_chunk(const BlockWork* __restrict__ work
     ch.col_start = bw.col_start;
     ch.block_id = bw.block_id;
     ch.pos = bw.pos;
+    if (bw.active && !*((volatile const int32_t*)bw.active)) ch.end = ch.begin;  // converged
+    ch.iter = bw.iter ? *((volatile const int32_t*)bw.iter) : -1;
   }
   return ch;
 }
@@ -307,7 +311,8 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
           const double ed = (double)x - (double)dot;
           acc += ed * ed;
         } else if (!isfinite(e)) {
-          if (ln.gl == 0) atomicMin(bad, pack_bad(ch.pos, iter, ch.begin + t - ch.bbeg));
+          if (ln.gl == 0)
+            atomicMin(bad, pack_bad(ch.pos, ch.iter >= 0 ? ch.iter : iter, ch.begin + t - ch.bbeg));
           dead = true;
         } else {
           const float g = two_a * e;
@@ -687,7 +692,7 @@ sweep_sse_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks
     }
     slot = __shfl_sync(kFull, slot, 0);
     const BlockWork bw = swork[pick];
-    Chunk ch{0, 0, 0, 0, bw.row_start, bw.col_start, bw.block_id, bw.pos, pick};
+    Chunk ch{0, 0, 0, 0, bw.row_start, bw.col_start, bw.block_id, bw.pos, pick, -1};
     const int64_t c0 = (int64_t)(slot * GPW + g) * bw.chunk_len;
     ch.bbeg = bw.begin;
     ch.bend = bw.end;
@@ -1220,6 +1225,8 @@ int build_work(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off, int n
       bw.first_chunk = chunks;
       bw.block_id = b;
       bw.pos = pos_base + q;
+      bw.active = nullptr;
+      bw.iter = nullptr;
       chunks += (int)((cnt + bl - 1) / bl);
     }
     ranges[t].nw = w - ranges[t].w0;
@@ -2031,6 +2038,254 @@ int run_step_converge_exact(bgmf_ctx* c, const int32_t* plan, const int32_t* bat
 
 // Fast converge mode: per batch, sweep the still-active blocks, measure each
 // block's post-sweep SSE, deactivate blocks whose RMSE improvement < tol.
+// ---- ConvergeEachBlock on the device, chunked kernel -------------------
+// sgd_converge (_kernels.py:62-100) for every block of a batch at once, with
+// no host round trip per sweep: one CUDA graph per batch whose WHILE node
+// repeats [sweep of the active blocks -> their post-sweep SSE -> conv_decide]
+// while any block is active; conv_decide sets the node's condition
+// (cudaGraphSetConditional).  A block's chunks in the work tables point at its
+// active flag (BlockWork::active) and skip themselves once it is 0.
+struct ConvState {
+  double prev;     // RMSE of the last measurement
+  int64_t iters;   // sweeps done
+  int32_t capped;
+  int32_t pad;
+};
+
+namespace {
+
+__global__ void conv_prep(const BlockWork* __restrict__ w, int nw, int32_t* __restrict__ act) {
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) act[i] = w[i].end > w[i].begin ? 1 : 0;
+}
+
+// after the sse_before measurement
+__global__ void conv_init(const BlockWork* __restrict__ w, int nw, double* __restrict__ sse,
+                          ConvState* __restrict__ st, int32_t* __restrict__ act,
+                          int32_t* __restrict__ iter, int64_t cap,
+                          cudaGraphConditionalHandle h) {
+  int any = 0;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) {
+    const double cnt = (double)(w[i].end - w[i].begin);
+    ConvState z{0.0, 0, 0, 0};
+    if (cnt > 0) {
+      z.prev = sqrt(sse[w[i].block_id] / cnt);
+      if (cap > 0) {
+        sse[w[i].block_id] = 0.0;  // the next measurement accumulates here
+        any = 1;
+      } else {
+        z.capped = 1;  // no sweep allowed: sse_after = sse_before, capped
+        act[i] = 0;
+      }
+    }
+    st[i] = z;
+  }
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) {
+    *iter = 0;
+    cudaGraphSetConditional(h, any ? 1u : 0u);
+  }
+}
+
+// after each sweep + SSE of the active blocks: the reference's stopping rule
+__global__ void conv_decide(const BlockWork* __restrict__ w, int nw, double* __restrict__ sse,
+                            ConvState* __restrict__ st, int32_t* __restrict__ act,
+                            int32_t* __restrict__ iter, int64_t cap, double tol,
+                            unsigned long long* __restrict__ bad,
+                            cudaGraphConditionalHandle h) {
+  int any = 0;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) {
+    if (!act[i]) continue;
+    ConvState z = st[i];
+    const int64_t cnt = w[i].end - w[i].begin;
+    const int b = w[i].block_id;
+    ++z.iters;
+    const double s2 = sse[b];
+    if (!isfinite(s2)) {  // _kernels.py:88-89: (count - 1, iters - 1)
+      atomicMin(bad, pack_bad(w[i].pos, z.iters - 1, cnt - 1));
+      act[i] = 0;
+    } else {
+      const double now = sqrt(s2 / (double)cnt);
+      if (z.prev - now < tol) {
+        act[i] = 0;  // converged: sse_after stays
+      } else {
+        z.prev = now;
+        if (z.iters >= cap) {
+          act[i] = 0;
+          z.capped = 1;
+        } else {
+          sse[b] = 0.0;
+          any = 1;
+        }
+      }
+    }
+    st[i] = z;
+  }
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) {
+    ++*iter;
+    // a divergence anywhere ends the step (the trainer raises)
+    cudaGraphSetConditional(h, (any && *bad == kNoBad) ? 1u : 0u);
+  }
+}
+
+}  // namespace
+
+// ConvergeEachBlock for the batches `ts` of a step through the chunked
+// kernels, the loops on the device: ONE graph per step -- for each batch in
+// plan order: prep -> sse_before -> init -> WHILE { sweep, SSE, decide } --
+// launched once and read back once (per-block SSE in d_sse, iterations and
+// capped flags in h_conv, batch-major).  Blocks of different batches are
+// disjoint, so d_sse is zeroed once.
+static int converge_step_graph(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off,
+                               int nbatch, const std::vector<int>& ts, double tol, int64_t cap,
+                               float alpha, float beta, std::vector<ConvState>& h_conv,
+                               std::vector<BlockWork>& items) {
+  cudaStream_t s = c->stream;
+  const Shape sh = shape_for(c->kp);
+  const int gpw = 32 / sh.L;
+  std::vector<BatchRange> rg, srg;
+  // both tables at once: growing the table between the two builds would drop the first
+  int rc = ensure_step_scratch(c, 2 * (size_t)batch_off[nbatch]);
+  if (rc) return rc;
+  rc = build_work(c, plan, batch_off, nbatch, sweep_groups(c, sh), rg);
+  if (rc) return rc;
+  const int nw_all = rg.empty() ? 0 : rg.back().w0 + rg.back().nw;
+  rc = build_work(c, plan, batch_off, nbatch, sweep_groups(c, sh), srg, nullptr, nw_all, 0, true);
+  if (rc) return rc;
+  // device state: per work item (all batches) flags + state, one iteration word per batch
+  const int cap_items = nw_all > 64 ? nw_all : 64;
+  if (!c->d_cstate || c->cstate_cap < cap_items) {
+    dfree(c->d_cstate, s);
+    c->cstate_cap = cap_items;
+    BGMF_CK(c, dmalloc(reinterpret_cast<char**>(&c->d_cstate),
+                       (size_t)c->cstate_cap * (sizeof(ConvState) + 8) + 16, s));
+  }
+  ConvState* st = reinterpret_cast<ConvState*>(c->d_cstate);
+  int32_t* act = reinterpret_cast<int32_t*>(st + c->cstate_cap);
+  int32_t* iters = act + c->cstate_cap;  // [batch]
+  items.clear();
+  for (int t : ts) {
+    const BatchRange& r = rg[t];
+    const BatchRange& sr = srg[t];
+    if (sr.nw != r.nw) return fail(c, BGMF_ERR_STATE, "converge: work tables disagree");
+    for (int q = 0; q < r.nw; ++q) {
+      c->h_work[r.w0 + q].active = act + r.w0 + q;
+      c->h_work[r.w0 + q].iter = iters + t;
+      c->h_work[sr.w0 + q].active = act + r.w0 + q;
+      c->h_work[sr.w0 + q].iter = nullptr;
+      items.push_back(c->h_work[r.w0 + q]);
+    }
+  }
+  if (items.empty()) return BGMF_OK;
+  const int w_end = srg.back().w0 + srg.back().nw;
+  BGMF_CK(c, cudaMemcpyAsync(c->d_work, c->h_work, sizeof(BlockWork) * w_end,
+                             cudaMemcpyHostToDevice, s));
+  // instantiated graphs are cached per step plan, layout and hyper-parameters:
+  // a run of steps cycles through P plans
+  std::string key((const char*)plan, sizeof(int32_t) * batch_off[nbatch]);
+  key.append((const char*)ts.data(), sizeof(int) * ts.size());
+  {
+    const double kv[4] = {(double)alpha, (double)beta, tol, (double)cap};
+    const int64_t lv[9] = {(int64_t)(uintptr_t)c->d_sse, (int64_t)(uintptr_t)c->d_bad,
+                           (int64_t)(uintptr_t)c->d_u,   (int64_t)(uintptr_t)c->d_v,
+                           (int64_t)(uintptr_t)c->d_lrow, (int64_t)(uintptr_t)c->d_val,
+                           (int64_t)(uintptr_t)c->d_work, (int64_t)(uintptr_t)c->d_cstate,
+                           (int64_t)w_end};
+    key.append((const char*)kv, sizeof kv).append((const char*)lv, sizeof lv);
+  }
+  cudaGraphExec_t ge = nullptr;
+  auto hit = c->conv_graphs.find(key);
+  if (hit != c->conv_graphs.end()) {
+    ge = hit->second;
+  } else {
+    cudaStream_t cs = nullptr, cs2 = nullptr;
+    cudaGraph_t g = nullptr;
+    const bool pdl = c->pdl;
+    c->pdl = false;  // plain serialised edges inside the graph
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->d_sse, 0, sizeof(double) * (size_t)c->I * c->J, cs);
+    for (int t : ts) {
+      const BatchRange& r = rg[t];
+      const BatchRange& sr = srg[t];
+      if (e != cudaSuccess || r.nw == 0) continue;
+      cudaStreamCaptureStatus stt;
+      cudaGraph_t cg = nullptr;
+      cudaGraphConditionalHandle h = 0;
+      e = cudaStreamGetCaptureInfo(cs, &stt, nullptr, &cg, nullptr, nullptr);
+      if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault);
+      const dim3 grid(((r.chunks + gpw - 1) / gpw + 7) / 8);
+      const dim3 sgrid(((sr.chunks + gpw - 1) / gpw + 7) / 8);
+      if (e == cudaSuccess) {
+        conv_prep<<<1, 256, 0, cs>>>(c->d_work + r.w0, r.nw, act + r.w0);
+        launch_fast(false, sh, sgrid, cs, c->d_work + sr.w0, sr.nw, sr.chunks, c, alpha, beta, 0);
+        conv_init<<<1, 256, 0, cs>>>(c->d_work + r.w0, r.nw, c->d_sse, st + r.w0, act + r.w0,
+                                     iters + t, cap, h);
+        e = cudaGetLastError();
+      }
+      const cudaGraphNode_t* deps = nullptr;
+      size_t ndeps = 0;
+      if (e == cudaSuccess) e = cudaStreamGetCaptureInfo(cs, &stt, nullptr, &cg, &deps, &ndeps);
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t cond = nullptr;
+      if (e == cudaSuccess) e = cudaGraphAddNode(&cond, cg, deps, ndeps, &cp);
+      if (e == cudaSuccess)
+        e = cudaStreamUpdateCaptureDependencies(cs, &cond, 1, cudaStreamSetCaptureDependencies);
+      if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(cs2, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeRelaxed);
+      if (e == cudaSuccess) {
+        launch_fast(true, sh, grid, cs2, c->d_work + r.w0, r.nw, r.chunks, c, alpha, beta, 0);
+        launch_fast(false, sh, sgrid, cs2, c->d_work + sr.w0, sr.nw, sr.chunks, c, alpha, beta,
+                    0);
+        conv_decide<<<1, 256, 0, cs2>>>(c->d_work + r.w0, r.nw, c->d_sse, st + r.w0, act + r.w0,
+                                        iters + t, cap, tol, c->d_bad, h);
+        e = cudaGetLastError();
+        cudaGraph_t bg = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(cs2, &bg);
+        if (e == cudaSuccess) e = e2;
+      }
+    }
+    {
+      cudaGraph_t gg = nullptr;
+      const cudaError_t e3 = cudaStreamEndCapture(cs, &gg);
+      g = gg;
+      if (e == cudaSuccess) e = e3;
+    }
+    c->pdl = pdl;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (cs) cudaStreamDestroy(cs);
+    if (cs2) cudaStreamDestroy(cs2);
+    if (e != cudaSuccess) {
+      if (ge) cudaGraphExecDestroy(ge);
+      return cuda_fail(c, e, "device-side converge graph");
+    }
+    c->conv_graphs[key] = ge;
+  }
+  BGMF_CK(c, cudaGraphLaunch(ge, s));
+  h_conv.resize(items.size());
+  // state of the step's items, gathered in batch order
+  std::vector<ConvState> all((size_t)(nw_all > 0 ? nw_all : 1));
+  BGMF_CK(c, cudaMemcpyAsync(all.data(), st, sizeof(ConvState) * nw_all, cudaMemcpyDeviceToHost,
+                             s));
+  BGMF_CK(c, cudaStreamSynchronize(s));
+  size_t o = 0;
+  for (int t : ts)
+    for (int q = 0; q < rg[t].nw; ++q) h_conv[o++] = all[rg[t].w0 + q];
+  return BGMF_OK;
+}
+
+void conv_graphs_release(bgmf_ctx* c) {
+  for (auto& kv : c->conv_graphs) cudaGraphExecDestroy(kv.second);
+  c->conv_graphs.clear();
+}
+
 int run_step_converge_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_off,
                            int nbatch, double tol, int64_t cap, double alpha, double beta,
                            int64_t* iters_out, int32_t* capped_out) {
@@ -2048,8 +2303,8 @@ int run_step_converge_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batc
   std::vector<int64_t> conv((size_t)2 * nb);
   for (int t = 0; t < nbatch; ++t) {
     const int q0 = batch_off[t], q1 = batch_off[t + 1];
-    if (use_ordered(c, plan, q0, q1, true)) {
-      // the whole per-block converge loop on the device (ordered.cu)
+    if (use_ordered(c, plan, q0, q1)) {
+      // the whole per-block converge loop on the device, in stored order (ordered.cu)
       const int capi = cap > INT32_MAX ? INT32_MAX : (int)cap;
       int rc = run_batch_ordered(c, plan, q0, q1, 0, capi, (float)alpha, (float)beta, true, tol);
       if (rc) return rc;
@@ -2065,6 +2320,32 @@ int run_step_converge_fast(bgmf_ctx* c, const int32_t* plan, const int32_t* batc
         sse_final[b] = c->h_sse[b];
         iters_out[b] = conv[2 * b];
         capped_out[b] = (int32_t)conv[2 * b + 1];
+      }
+      if (*c->h_bad != kNoBad) break;
+      continue;
+    }
+    if (c->conv_graph && !c->streaming) {  // the loop on the device (converge_step_graph)
+      std::vector<ConvState> hc;
+      std::vector<BlockWork> items;
+      // every remaining batch that also takes the chunked path joins this graph
+      std::vector<int> ts;
+      for (int t2 = t; t2 < nbatch; ++t2) {
+        if (t2 > t && use_ordered(c, plan, batch_off[t2], batch_off[t2 + 1])) break;
+        ts.push_back(t2);
+      }
+      int rc = converge_step_graph(c, plan, batch_off, nbatch, ts, tol, cap, (float)alpha,
+                                   (float)beta, hc, items);
+      if (rc) return rc;
+      t = ts.back();  // the loop's ++t moves past the batches just run
+      BGMF_CK(c, cudaMemcpyAsync(c->h_sse, c->d_sse, sizeof(double) * nb, cudaMemcpyDeviceToHost,
+                                 s));
+      BGMF_CK(c, cudaMemcpyAsync(c->h_bad, c->d_bad, 8, cudaMemcpyDeviceToHost, s));
+      BGMF_CK(c, cudaStreamSynchronize(s));
+      for (size_t q = 0; q < items.size(); ++q) {
+        const int b = items[q].block_id;
+        sse_final[b] = c->h_sse[b];
+        iters_out[b] = hc[q].iters;
+        capped_out[b] = hc[q].capped;
       }
       if (*c->h_bad != kNoBad) break;
       continue;

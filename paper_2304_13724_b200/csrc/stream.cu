@@ -272,6 +272,8 @@ static int build_pieces(bgmf_ctx* c, const int32_t* plan, const int32_t* batch_o
         bw.first_chunk = pc.chunks;
         bw.block_id = b;
         bw.pos = pos0 + qq;
+        bw.active = nullptr;
+        bw.iter = nullptr;
         pc.chunks += (int)((cnt + bl - 1) / bl);
         pc.ratings += (double)cnt;
         off += cnt;

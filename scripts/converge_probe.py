@@ -16,11 +16,12 @@ from paper_2304_13724_b200 import workloads  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+tol = float(sys.argv[3]) if len(sys.argv) > 3 else 0.05
 w = workloads.CONFIGS[name]
 r, c, v = workloads.generate(name)
 d = bm.RatingsDataset(w.n, w.m, r, c, v)
 cfg = bm.TrainConfig(k=w.k, alpha=w.alpha, beta=w.beta, grid_i=w.grid, grid_j=w.grid,
-                     seed=w.seed, outer_steps=epochs, inner_schedule=bm.ConvergeEachBlock(0.05))
+                     seed=w.seed, outer_steps=epochs, inner_schedule=bm.ConvergeEachBlock(tol))
 bm.train_blocked(d, bm.TrainConfig(k=w.k, grid_i=w.grid, grid_j=w.grid, outer_steps=1),
                  early_stop=False)  # warm
 t0 = time.perf_counter()
@@ -29,7 +30,7 @@ wall = time.perf_counter() - t0
 t1 = time.perf_counter()
 _, _, otr, _ = O.train_blocked(w.n, w.m, r, c, v, k=w.k, alpha=w.alpha, beta=w.beta,
                                grid_i=w.grid, grid_j=w.grid, seed=w.seed, outer_steps=epochs,
-                               schedule="converge:0.05", early_stop=False, nthreads=16)
+                               schedule=f"converge:{tol}", early_stop=False, nthreads=16)
 owall = time.perf_counter() - t1
 for s, o in zip(res.trace, otr):
     print(f"{name} step {s.step}: train {s.train_rmse:.6f} (oracle {o['train_rmse']:.6f}, "
