@@ -48,9 +48,11 @@ def run(mode: str, extra: list[str]) -> int:
     env["PYTHONPATH"] = HERE + os.pathsep + env.get("PYTHONPATH", "")
     if mode == "exact":
         env["BGMF_EXACT"] = "1"
+    # explicit test files / node ids narrow the run; else the whole suite
+    picked = [a for a in extra if a.endswith(".py") or "::" in a]
     cmd = [sys.executable, "-m", "pytest", "-p", "bgmf_alias", "-q", "-rf",
            "-p", "no:cacheprovider", "--rootdir", os.path.join(HERE, "_ref"),
-           os.path.join(HERE, "_ref"), *extra]
+           *([] if picked else [os.path.join(HERE, "_ref")]), *extra]
     return subprocess.call(cmd, env=env, cwd=os.path.join(HERE, "_ref"))
 
 
