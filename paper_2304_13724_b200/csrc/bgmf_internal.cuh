@@ -168,7 +168,8 @@ struct bgmf_ctx {
 
   // ordered sweep (ordered.cu): column ranks, row pointers, row flags
   int ord_mode = -1;                     // 1: ordered where possible, 0: never, -1: auto
-  int64_t ord_stage_ratings = 262144;     // target ratings per stage (slab CTA)
+  int64_t ord_stage_ratings = 16384;     // target ratings per stage (slab CTA)
+  int ord_fill_ctas = 1;                 // stages per SM when filling the GPU
   int ord_warp = 1;                      // one group per warp (ordered_shape)
   bool ord_ready = false;
   uint32_t ord_gen = 1;                  // row-flag generation of the next sweep

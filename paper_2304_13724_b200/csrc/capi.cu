@@ -223,6 +223,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "pdl")) c->pdl = value != 0.0;
   else if (!strcmp(key, "conv_graph")) c->conv_graph = value != 0.0;
   else if (!strcmp(key, "ord_col_conc")) c->ord_col_conc = value;
+  else if (!strcmp(key, "ord_fill_ctas")) c->ord_fill_ctas = value < 1 ? 1 : (int)value;
   else if (!strcmp(key, "ord_warp")) c->ord_warp = value != 0.0;
   else if (!strcmp(key, "ord_stage_ratings"))
     c->ord_stage_ratings = value < 1 ? 1 : (int64_t)value;

@@ -1047,7 +1047,8 @@ void plan_stages(bgmf_ctx* c, OrdItem& it, int items) {
   const int64_t w = it.ob.w;
   const int64_t smin = (w + per - 1) / per;
   int64_t S = (it.cnt + c->ord_stage_ratings - 1) / c->ord_stage_ratings;
-  const int64_t fill = c->num_sms / (items > 0 ? items : 1);
+  // co-residency allows ord_fill_ctas stages per SM (1024-thread CTAs: at most 2)
+  const int64_t fill = (int64_t)c->num_sms * c->ord_fill_ctas / (items > 0 ? items : 1);
   if (S > fill) S = fill;
   if (S < smin) S = smin;
   if (S > w) S = w;
