@@ -168,7 +168,7 @@ struct bgmf_ctx {
 
   // ordered sweep (ordered.cu): column ranks, row pointers, row flags
   int ord_mode = -1;                     // 1: ordered where possible, 0: never, -1: auto
-  int64_t ord_stage_ratings = 16384;     // target ratings per stage (slab CTA)
+  int64_t ord_stage_ratings = 1024;      // target ratings per stage (slab CTA)
   int ord_fill_ctas = 1;                 // stages per SM when filling the GPU
   int ord_warp = 1;                      // one group per warp (ordered_shape)
   bool ord_ready = false;
@@ -327,8 +327,9 @@ bool order_risky(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1);
 int run_batch_ordered(bgmf_ctx* ctx, const int32_t* plan, int q0, int q1, int pos_base,
                       int iters, float alpha, float beta, bool conv = false, double tol = 0.0,
                       double alpha64 = 0.0, double beta64 = 0.0);
-int run_shards_ordered(bgmf_ctx* ctx, const int32_t* r0, const int32_t* r1, int nshards,
-                       float* vpriv, float alpha, float beta, double* sse_dev);
+int run_shards_ordered(bgmf_ctx* ctx, const int32_t* r0, const int32_t* r1,
+                       const int64_t* edges, int nshards, float* vpriv, float alpha, float beta,
+                       double* sse_dev);
 
 // stream.cu -- out-of-core: ratings in pinned host memory, device slot ring
 int stream_enable(bgmf_ctx* ctx, int64_t slot_ratings, int nslots);

@@ -1169,15 +1169,15 @@ int run_batch_ordered(bgmf_ctx* c, const int32_t* plan, int q0, int q1, int pos_
 // CPMF shards (baselines.py:100-182) through the ordered kernel: shard w =
 // rows [r0[w], r1[w]) of the 1 x 1 partition, swept in stored order on the
 // shared U and its private V copy vpriv + w * m * kp; SSE to sse_dev[w].
-int run_shards_ordered(bgmf_ctx* c, const int32_t* r0, const int32_t* r1, int nshards,
-                       float* vpriv, float alpha, float beta, double* sse_dev) {
+int run_shards_ordered(bgmf_ctx* c, const int32_t* r0, const int32_t* r1, const int64_t* edges,
+                       int nshards, float* vpriv, float alpha, float beta, double* sse_dev) {
   int rc = ensure_order_index(c);
   if (rc) return rc;
   std::vector<OrdItem> items;
   for (int w = 0; w < nshards; ++w) {
     if (r1[w] <= r0[w]) continue;
     OrdItem it{};
-    it.cnt = 1;  // (not needed beyond timing)
+    it.cnt = edges[w + 1] - edges[w];  // sets the stage count as for a block of that size
     it.ob.begin = 0;
     it.ob.rp = c->h_rp[0] + r0[w];
     it.ob.row_start = r0[w];

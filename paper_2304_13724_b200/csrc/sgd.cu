@@ -1908,8 +1908,8 @@ int run_sync_parallel_step(bgmf_ctx* c, const int64_t* edges, int nshards, doubl
     BGMF_CK(c, cudaMemsetAsync(c->d_bad, 0xFF, 8, s));
     float* P = reinterpret_cast<float*>(c->d_priv);
     if (priv) broadcast_v<float><<<grid, 256, 0, s>>>(c->d_v, P, elems, nshards);
-    rc = run_shards_ordered(c, r0.data(), r1.data(), nshards, priv ? P : nullptr, (float)alpha,
-                            (float)beta, sse_dev);
+    rc = run_shards_ordered(c, r0.data(), r1.data(), edges, nshards, priv ? P : nullptr,
+                            (float)alpha, (float)beta, sse_dev);
     if (rc) return rc;
     if (priv) merge_private_v<float><<<grid, 256, 0, s>>>(c->d_v, P, elems, nshards);
     BGMF_CK(c, cudaGetLastError());
