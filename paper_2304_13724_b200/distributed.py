@@ -351,10 +351,48 @@ def _peers_reachable(world: int, device, dist) -> bool:
     devs = [None] * world
     dist.all_gather_object(devs, int(device))
     ok = all(o == device or torch.cuda.can_device_access_peer(device, o) for o in devs)
+    ok = _all_ok(ok, device, dist)
+    if ok:  # and CUDA IPC itself works here (containers can forbid it)
+        ok = _all_ok(_ipc_probe(world, device, dist), device, dist)
+    return ok
+
+
+def _all_ok(ok: bool, device, dist) -> bool:
+    import torch
+
     flag = torch.tensor([1 if ok else 0], dtype=torch.int64,
                         device=f"cuda:{device}" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     return bool(int(flag.item()))
+
+
+def _ipc_probe(world: int, device, dist) -> bool:
+    """Collective: export a small peer buffer, map every other rank's.  Any
+    failure (on any rank) makes the ring fall back to torch.distributed."""
+    from .device import Engine, EngineOptions
+
+    eng = None
+    ok, handle = True, None
+    try:
+        eng = Engine(EngineOptions(device=device))
+        handle = eng.peer_handle(eng.peer_alloc(256))
+    except Exception:  # noqa: BLE001  probing: any failure means "no peer transport"
+        ok = False
+    allh = [None] * world
+    dist.all_gather_object(allh, handle)
+    if ok:
+        try:
+            for h in allh:
+                if h is None:
+                    ok = False
+                elif h != handle:
+                    eng.peer_open(h)
+        except Exception:  # noqa: BLE001
+            ok = False
+    ok = _all_ok(ok, device, dist)  # nobody closes while a peer may still map it
+    if eng is not None:
+        eng.close()
+    return ok
 
 
 def _move_v(moves, rank: int, shard, dist) -> None:

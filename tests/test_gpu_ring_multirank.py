@@ -31,8 +31,11 @@ def _port():
 
 
 def _launch(world: int, case: str, out, transport: str = "peer") -> None:
-    env = dict(os.environ, BGMF_DIST_BACKEND="gloo", BGMF_DEVICE="0",
-               BGMF_RING_TRANSPORT=transport)
+    env = dict(os.environ, BGMF_DIST_BACKEND="gloo", BGMF_DEVICE="0")
+    if transport == "auto":  # the ring chooses (collective P2P + CUDA-IPC probe)
+        env.pop("BGMF_RING_TRANSPORT", None)
+    else:
+        env["BGMF_RING_TRANSPORT"] = transport
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
            os.path.join(ROOT, "tests", "ring_worker.py"), str(out), case]
@@ -66,7 +69,7 @@ def _oracle(case: str):
                           (2, "converge", "peer"), (3, "holdout", "peer"),
                           (2, "const", "dist"), (3, "holdout", "dist"),
                           (2, "stream", "peer"), (3, "stream_inc", "peer"),
-                          (2, "stream", "dist")])
+                          (2, "stream", "dist"), (2, "const", "auto")])
 def test_ring_ranks_share_one_gpu_match_oracle(world, case, transport, tmp_path):
     """transport "peer": V moves through IPC-mapped peer memory (the default);
     "dist": torch.distributed P2P (staged through the host on gloo).  The
