@@ -77,6 +77,8 @@ struct bgmf_ctx {
   bool u_ring = false;    // sweep: U rows of upcoming runs via a cp.async smem ring
   bool fuse_sse = false;  // last sweep + SSE in one launch (sweep_sse_kernel; measured slower)
   unsigned* d_fuse = nullptr;  // sweep_sse_kernel's per-work-item counters
+  int dyn_split = 1;           // sweep: chunks cut D ways, taken from a ticket counter
+  unsigned* d_dyn = nullptr;   // its two self-resetting counters (allocated at create)
   int fused = -1;      // 1: one cooperative launch per step, 0: per stratum, -1 auto
   int groups_key = -1;                // sweep_groups() cache
   int64_t groups_cache = 0;

@@ -167,6 +167,13 @@ int bgmf_create(int device, void* stream, bgmf_ctx** out) {
     if (e != cudaSuccess) { delete c; return cuda_fail(nullptr, e, "cudaStreamCreate"); }
     c->own_stream = true;
   }
+  e = cudaMalloc(&c->d_dyn, 2 * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(c->d_dyn, 0, 2 * sizeof(unsigned));
+  if (e != cudaSuccess) {
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return cuda_fail(nullptr, e, "cudaMalloc");
+  }
   *out = c;
   return BGMF_OK;
 }
@@ -190,6 +197,7 @@ void bgmf_destroy(bgmf_ctx* c) {
   dfree(c->d_partials, c->stream);
   dfree(c->d_priv, c->stream);
   cudaStreamSynchronize(c->stream);
+  if (c->d_dyn) cudaFree(c->d_dyn);
   prof_mark(c, "destroy: device frees");
   pinned_free(c->h_work);
   pinned_free(c->h_sse);
@@ -220,6 +228,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "no_val8")) c->no_val8 = value != 0.0;
   else if (!strcmp(key, "fuse_sse")) c->fuse_sse = value != 0.0;
   else if (!strcmp(key, "u_ring")) c->u_ring = value != 0.0;
+  else if (!strcmp(key, "dyn_split")) c->dyn_split = value < 1.0 ? 1 : value > 16.0 ? 16 : (int)value;
   else if (!strcmp(key, "pdl")) c->pdl = value != 0.0;
   else if (!strcmp(key, "conv_graph")) c->conv_graph = value != 0.0;
   else if (!strcmp(key, "ord_col_conc")) c->ord_col_conc = value;

@@ -137,6 +137,42 @@ __device__ __forceinline__ Chunk locate_chunk(const BlockWork* __restrict__ work
 }
 
 
+// Dynamic chunking (the sweep's dyn_split option): the static one-wave table
+// (chunk_len, first_chunk per work item, T0 chunks) is cut D ways.  Warp slot s
+// covers GPW consecutive static chunk indices of phase p = s / ceil(T0 / GPW):
+// static chunk j of block w becomes its sub-chunks [p n_w, (p + 1) n_w) of
+// length ceil(chunk_len / D), so within a phase each block has as many groups
+// on it as in the static wave (the per-block concurrency floors still hold)
+// and only the last phase's short chunks form the tail.
+__device__ __forceinline__ Chunk locate_dyn(const BlockWork* __restrict__ work, int nwork,
+                                            int total_chunks, int dyn_d, int slot, int g,
+                                            int gpw) {
+  Chunk ch{0, 0, 0, 0, 0, 0, 0, 0, -1, -1};
+  const int per_phase = (total_chunks + gpw - 1) / gpw;
+  const int p = slot / per_phase;
+  const int j = (slot - p * per_phase) * gpw + g;
+  if (p < dyn_d && j < total_chunks) {
+    const int w = find_work(work, nwork, j);
+    ch.w = w;
+    const BlockWork bw = work[w];
+    const int64_t cnt = bw.end - bw.begin;
+    const int64_t n0 = (cnt + bw.chunk_len - 1) / bw.chunk_len;
+    const int64_t cl = ((int64_t)bw.chunk_len + dyn_d - 1) / dyn_d;
+    const int64_t idx = (int64_t)p * n0 + (j - bw.first_chunk);
+    ch.begin = min(bw.begin + idx * cl, bw.end);
+    ch.end = min(ch.begin + cl, bw.end);
+    ch.bbeg = bw.begin;
+    ch.bend = bw.end;
+    ch.row_start = bw.row_start;
+    ch.col_start = bw.col_start;
+    ch.block_id = bw.block_id;
+    ch.pos = bw.pos;
+    if (bw.active && !*((volatile const int32_t*)bw.active)) ch.end = ch.begin;  // converged
+    ch.iter = bw.iter ? *((volatile const int32_t*)bw.iter) : -1;
+  }
+  return ch;
+}
+
 // Rating triple of entry i.  cbits < 0: SoA int32 row / int32 col arrays;
 // cbits >= 0: packed 4-byte (row << cbits | col) records in `lrow` (the
 // out-of-core stream format, 8 B per rating with the fp32 value), the low 8
@@ -390,23 +426,47 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
                 const float* __restrict__ val, float* __restrict__ U, float* __restrict__ V,
                 int kp, float alpha, float beta, int iter, unsigned long long* __restrict__ bad,
-                int cbits) {
+                int cbits, int dyn_d, unsigned* __restrict__ dyn) {
   constexpr int GPW = 32 / L;
   extern __shared__ float4 smem_rows[];
   const int lane = threadIdx.x & 31;
   const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
-  const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
-  pdl_trigger();
-  if (maxlen == 0) return;
-  pdl_wait();
   // bulk: this group's delta ring, kBulkBufs rows of kp floats; uring: this
   // thread's slice of the U-row ring ([slot][q][thread] float4)
   float* sbuf = MODE == 2 ? reinterpret_cast<float*>(smem_rows + threadIdx.x)
                           : reinterpret_cast<float*>(smem_rows) +
                                 (size_t)((threadIdx.x >> 5) * GPW + lane / L) * kBulkBufs * kp;
-  walk_chunk<L, V4, kMask, true, MODE>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta, iter,
-                                       bad, cbits, sbuf);
+  if (dyn_d <= 1) {
+    const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
+    const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
+    pdl_trigger();
+    if (maxlen == 0) return;
+    pdl_wait();
+    walk_chunk<L, V4, kMask, true, MODE>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta,
+                                         iter, bad, cbits, sbuf);
+    return;
+  }
+  // dynamic: slot = this warp, then nwarps + a ticket from dyn[0] until the
+  // D phases are taken; the last warp out (dyn[1]) zeroes both counters for
+  // the next launch (stream order / griddepcontrol.wait makes that visible)
+  pdl_trigger();
+  pdl_wait();
+  const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
+  const int slots = dyn_d * ((total_chunks + GPW - 1) / GPW);
+  for (int slot = warp; slot < slots;) {
+    const Chunk ch = locate_dyn(work, nwork, total_chunks, dyn_d, slot, lane / L, GPW);
+    const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
+    if (maxlen > 0)
+      walk_chunk<L, V4, kMask, true, MODE>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta,
+                                           iter, bad, cbits, sbuf);
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(dyn, 1u);
+    slot = nwarps + (int)__shfl_sync(kFull, t, 0);
+  }
+  if (lane == 0 && atomicAdd(dyn + 1, 1u) == (unsigned)nwarps - 1u) {
+    dyn[0] = 0u;
+    dyn[1] = 0u;
+  }
 }
 
 // Post-sweep SSE of each block: sum over the chunk of (x - u.v)^2 in fp64,
@@ -1004,6 +1064,7 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
                      int nwork, int total, const int32_t* lrow, const int32_t* lcol,
                      const float* val, bgmf_ctx* c, float a, float b, int it, int cbits = -1) {
   const bool mk = needs_mask(sh, c->kp);
+  const int dd = sweep && c->d_dyn ? c->dyn_split : 1;
 #define BGMF_CASE(LL, VV, MM)                                                                 \
   if (sh.L == LL && sh.V4 == VV && mk == MM) {                                                \
     if (sweep && c->bulk_red) {                                                               \
@@ -1011,17 +1072,19 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
                            cudaFuncAttributeMaxDynamicSharedMemorySize,                       \
                            (int)bulk_smem(c, sh));                                            \
       sgd_fast_kernel<LL, VV, MM, 1><<<grid, 256, bulk_smem(c, sh), s>>>(                     \
-          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
+          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits, dd,    \
+          c->d_dyn);                                                                          \
     } else if (sweep && c->u_ring && LL >= 4) {                                               \
       constexpr int UD = LL >= 8 ? 4 : 3;                                                     \
       const int sm = 256 * UD * VV * 16;                                                      \
       cudaFuncSetAttribute(&sgd_fast_kernel<LL, VV, MM, 2>,                                  \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                  \
       sgd_fast_kernel<LL, VV, MM, 2><<<grid, 256, sm, s>>>(                                   \
-          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);       \
+          w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits, dd,    \
+          c->d_dyn);                                                                          \
     } else if (sweep)                                                                         \
       launch_k(c->pdl, &sgd_fast_kernel<LL, VV, MM, 0>, grid, 256, 0, s, w, nwork, total, lrow,   \
-               lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits);                    \
+               lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits, dd, c->d_dyn);      \
     else if (c->sse_wide)                                                                     \
       launch_sse_wide(s, w, nwork, total, lrow, lcol, val, c, cbits);                          \
     else if (c->sse_async > 0)                                                                \
