@@ -123,6 +123,12 @@ int bgmf_synth(int64_t n, int64_t m, int64_t nnz, int64_t start, uint64_t seed,
 int bgmf_partition_export(bgmf_ctx* ctx, int64_t* offsets, int64_t* order,
                           int32_t* lrows, int32_t* lcols);
 
+/* The device-resident values in partition order, widened to fp64 (fast mode
+ * holds fp32, exact mode fp64): what the kernels read for BlockedDataset._values
+ * (partition.py:131).  Device-resident partitions only (BGMF_ERR_STATE when
+ * the ratings stream from host memory). */
+int bgmf_partition_values(bgmf_ctx* ctx, double* vals);
+
 /* Upload U (n x k) and V (m x k), row-major fp64 as FactorModel.u/.v
  * (core.py:139-176).  Fast mode stores fp32 rows padded to a multiple of 4. */
 int bgmf_set_factors(bgmf_ctx* ctx, const double* u, const double* v,

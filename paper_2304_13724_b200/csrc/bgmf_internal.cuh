@@ -79,6 +79,7 @@ struct bgmf_ctx {
   unsigned* d_fuse = nullptr;  // sweep_sse_kernel's per-work-item counters
   int dyn_split = 1;           // sweep: chunks cut D ways, taken from a ticket counter
   unsigned* d_dyn = nullptr;   // its two self-resetting counters (allocated at create)
+  int snap_cap = 0;            // sweep: chunk edges moved to the end of a run within this many ratings
   int fused = -1;      // 1: one cooperative launch per step, 0: per stratum, -1 auto
   int groups_key = -1;                // sweep_groups() cache
   int64_t groups_cache = 0;

@@ -228,6 +228,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "no_val8")) c->no_val8 = value != 0.0;
   else if (!strcmp(key, "fuse_sse")) c->fuse_sse = value != 0.0;
   else if (!strcmp(key, "u_ring")) c->u_ring = value != 0.0;
+  else if (!strcmp(key, "snap")) c->snap_cap = value < 0.0 ? 0 : value > 4096.0 ? 4096 : (int)value;
   else if (!strcmp(key, "dyn_split")) c->dyn_split = value < 1.0 ? 1 : value > 16.0 ? 16 : (int)value;
   else if (!strcmp(key, "pdl")) c->pdl = value != 0.0;
   else if (!strcmp(key, "conv_graph")) c->conv_graph = value != 0.0;
@@ -328,6 +329,25 @@ int bgmf_partition_export(bgmf_ctx* c, int64_t* offsets, int64_t* order, int32_t
     for (int64_t i = 0; i < n; ++i) order[i] = (int64_t)o[i];
   }
   BGMF_CK(c, cudaStreamSynchronize(c->stream));
+  return BGMF_OK;
+}
+
+int bgmf_partition_values(bgmf_ctx* c, double* vals) {
+  if (!c || !vals) return fail(c, BGMF_ERR_ARG, "ctx or vals is NULL");
+  if (!c->partitioned) return fail(c, BGMF_ERR_STATE, "bgmf_partition has not been called");
+  if (c->streaming) return fail(c, BGMF_ERR_STATE, "the ratings stream from host memory");
+  cudaSetDevice(c->device);
+  const int64_t n = c->nnz;
+  if (n == 0) return BGMF_OK;
+  if (c->d_val64) {
+    BGMF_CK(c, cudaMemcpyAsync(vals, c->d_val64, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    BGMF_CK(c, cudaStreamSynchronize(c->stream));
+    return BGMF_OK;
+  }
+  std::vector<float> f((size_t)n);
+  BGMF_CK(c, cudaMemcpyAsync(f.data(), c->d_val, n * 4, cudaMemcpyDeviceToHost, c->stream));
+  BGMF_CK(c, cudaStreamSynchronize(c->stream));
+  for (int64_t i = 0; i < n; ++i) vals[i] = (double)f[i];
   return BGMF_OK;
 }
 

@@ -200,6 +200,32 @@ __device__ __forceinline__ int load_rowidx(const int32_t* __restrict__ lrow, int
   return cbits < 0 ? __ldg(lrow + i) : (int)((uint32_t)__ldg(lrow + i) >> (cbits & 0xFF));
 }
 
+// Run-aligned chunk edges (the sweep's snap option): a nominal chunk edge P
+// inside a user run moves forward to that run's end when it lies within
+// `cap` entries, so the run is walked by one group (U stays in registers, no
+// per-rating U red.add, no re-reads) instead of being straddled.  A pure
+// function of P: the chunk ending at P and the one starting there agree.
+// Group-parallel (ballots over L entries); all warp lanes execute it.
+template <int L>
+__device__ __forceinline__ int64_t snap_edge(const int32_t* __restrict__ lrow, int cbits,
+                                             int64_t P, int64_t lo, int64_t hi, int cap) {
+  const int lane = threadIdx.x & 31, gl = lane & (L - 1), gbase = lane & ~(L - 1);
+  const bool inside = P > lo && P < hi;
+  const int prev = inside ? load_rowidx(lrow, cbits, P - 1) : 0;
+  bool open = inside && load_rowidx(lrow, cbits, P) == prev;  // P splits a run
+  int64_t out = P;
+  for (int base = 1; base < cap; base += L) {
+    const int64_t i = P + base + gl;
+    const bool edge = open && (i >= hi || load_rowidx(lrow, cbits, min(i, hi - 1)) != prev);
+    const unsigned m = (__ballot_sync(0xffffffffu, edge) >> gbase) & (L == 32 ? 0xffffffffu : ((1u << L) - 1u));
+    if (open && m) {
+      out = min(P + base + (int64_t)(__ffs(m) - 1), hi);
+      open = false;
+    }
+  }
+  return out;  // still open: the run is longer than cap, keep the straddle
+}
+
 // L2-coherent 128-bit load (the factors are written by other SMs during the
 // kernel; ld.global.cg never returns a stale L1 line).
 __device__ __forceinline__ float4 ld_cg(const float* p) {
@@ -426,7 +452,7 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
                 const float* __restrict__ val, float* __restrict__ U, float* __restrict__ V,
                 int kp, float alpha, float beta, int iter, unsigned long long* __restrict__ bad,
-                int cbits, int dyn_d, unsigned* __restrict__ dyn) {
+                int cbits, int dyn_d, unsigned* __restrict__ dyn, int snap) {
   constexpr int GPW = 32 / L;
   extern __shared__ float4 smem_rows[];
   const int lane = threadIdx.x & 31;
@@ -437,7 +463,13 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                           : reinterpret_cast<float*>(smem_rows) +
                                 (size_t)((threadIdx.x >> 5) * GPW + lane / L) * kBulkBufs * kp;
   if (dyn_d <= 1) {
-    const Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
+    Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
+    if (snap > 0) {
+      const int64_t b = snap_edge<L>(lrow, cbits, ch.begin, ch.bbeg, ch.bend, snap);
+      const int64_t e = snap_edge<L>(lrow, cbits, ch.end, ch.bbeg, ch.bend, snap);
+      ch.begin = b;
+      ch.end = max(b, e);
+    }
     const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
     pdl_trigger();
     if (maxlen == 0) return;
@@ -454,7 +486,13 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
   const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
   const int slots = dyn_d * ((total_chunks + GPW - 1) / GPW);
   for (int slot = warp; slot < slots;) {
-    const Chunk ch = locate_dyn(work, nwork, total_chunks, dyn_d, slot, lane / L, GPW);
+    Chunk ch = locate_dyn(work, nwork, total_chunks, dyn_d, slot, lane / L, GPW);
+    if (snap > 0) {
+      const int64_t b = snap_edge<L>(lrow, cbits, ch.begin, ch.bbeg, ch.bend, snap);
+      const int64_t e = snap_edge<L>(lrow, cbits, ch.end, ch.bbeg, ch.bend, snap);
+      ch.begin = b;
+      ch.end = max(b, e);
+    }
     const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
     if (maxlen > 0)
       walk_chunk<L, V4, kMask, true, MODE>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta,
@@ -1065,6 +1103,7 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
                      const float* val, bgmf_ctx* c, float a, float b, int it, int cbits = -1) {
   const bool mk = needs_mask(sh, c->kp);
   const int dd = sweep && c->d_dyn ? c->dyn_split : 1;
+  const int sn = c->snap_cap;
 #define BGMF_CASE(LL, VV, MM)                                                                 \
   if (sh.L == LL && sh.V4 == VV && mk == MM) {                                                \
     if (sweep && c->bulk_red) {                                                               \
@@ -1073,7 +1112,7 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
                            (int)bulk_smem(c, sh));                                            \
       sgd_fast_kernel<LL, VV, MM, 1><<<grid, 256, bulk_smem(c, sh), s>>>(                     \
           w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits, dd,    \
-          c->d_dyn);                                                                          \
+          c->d_dyn, sn);                                                                          \
     } else if (sweep && c->u_ring && LL >= 4) {                                               \
       constexpr int UD = LL >= 8 ? 4 : 3;                                                     \
       const int sm = 256 * UD * VV * 16;                                                      \
@@ -1081,10 +1120,10 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                  \
       sgd_fast_kernel<LL, VV, MM, 2><<<grid, 256, sm, s>>>(                                   \
           w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits, dd,    \
-          c->d_dyn);                                                                          \
+          c->d_dyn, sn);                                                                          \
     } else if (sweep)                                                                         \
       launch_k(c->pdl, &sgd_fast_kernel<LL, VV, MM, 0>, grid, 256, 0, s, w, nwork, total, lrow,   \
-               lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits, dd, c->d_dyn);      \
+               lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits, dd, c->d_dyn, sn); \
     else if (c->sse_wide)                                                                     \
       launch_sse_wide(s, w, nwork, total, lrow, lcol, val, c, cbits);                          \
     else if (c->sse_async > 0)                                                                \

@@ -226,6 +226,12 @@ class Engine:
             N.ptr(lc, N._i32p)))
         return off, order, lr.astype(np.int64), lc.astype(np.int64)
 
+    def partition_values(self) -> np.ndarray:
+        """The device-resident values in partition order, as fp64."""
+        out = np.empty(self.nnz, np.float64)
+        self._check(self._L.bgmf_partition_values(self._h, N.ptr(out, N._f64p)))
+        return out
+
     # ------------------------------------------------------------ factors
     def set_factors(self, u: np.ndarray, v: np.ndarray):
         u, v = N.f64(u), N.f64(v)

@@ -184,3 +184,28 @@ def test_key_layouts_match_oracle(shape, options):
     assert np.array_equal(b._cols, ref["cols"])
     assert np.array_equal(b._values, ref["values"])
     assert np.array_equal(b.order, np.lexsort((c, r, _block_ids(r, c, n, m, I, J))))
+
+
+
+@pytest.mark.parametrize("kind", ["ints", "floats"])
+def test_device_values_are_the_narrowed_inputs(kind):
+    """bgmf_partition_values: the fp32 values the kernels read, in partition
+    order, are the fp64 inputs narrowed (bit-exact, -0.0 kept); indices
+    bit-equal to the oracle.  4 M entries = several staging chunks."""
+    from paper_2304_13724_b200.device import Engine, EngineOptions
+    g = np.random.default_rng(5)
+    n, m, nnz = 480_000, 17_800, 4_000_000
+    r = g.integers(0, n, nnz)
+    c = g.integers(0, m, nnz)
+    v = np.rint(g.uniform(0, 255, nnz)) if kind == "ints" else g.normal(3.0, 2.0, nnz)
+    v[:4] = [-0.0, 0.5, 1e9, 256.0]
+    eng = Engine(EngineOptions())
+    eng.partition(r, c, v, n, m, 8, 8)
+    off, order, lr, lc = eng.export_partition()
+    vals = eng.partition_values()
+    eng.close()
+    assert np.array_equal(vals.view(np.int64),
+                          v[order].astype(np.float32).astype(np.float64).view(np.int64))
+    P = O.partition(r, c, v, n, m, 8, 8)
+    assert np.array_equal(off, P["offsets"])
+    assert np.array_equal(lr, P["rows"]) and np.array_equal(lc, P["cols"])
