@@ -79,6 +79,10 @@ struct bgmf_ctx {
   unsigned* d_fuse = nullptr;  // sweep_sse_kernel's per-work-item counters
   int dyn_split = 1;           // sweep: chunks cut D ways, taken from a ticket counter
   unsigned* d_dyn = nullptr;   // its two self-resetting counters (allocated at create)
+  int u_prefetch = -1;         // sweep/SSE L2 prefetch of upcoming runs' U rows: 1 on, 0 off,
+                               // -1 when runs are short (upf_route)
+  bool upf_on = false;         // resolved for the current partition
+  int64_t upf_key = -1;        // partition the resolution belongs to
   int snap_cap = 0;            // sweep: chunk edges moved to the end of a run within this many ratings
   int fused = -1;      // 1: one cooperative launch per step, 0: per stratum, -1 auto
   int groups_key = -1;                // sweep_groups() cache

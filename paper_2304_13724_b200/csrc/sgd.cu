@@ -226,6 +226,21 @@ __device__ __forceinline__ int64_t snap_edge(const int32_t* __restrict__ lrow, i
   return out;  // still open: the run is longer than cap, keep the straddle
 }
 
+// U-row L2 prefetch (upf; routed by u_prefetch): when a triple batch is loaded, each
+// lane whose rating starts a user run asks the TMA unit to pull that run's U
+// row into L2 (cp.async.bulk.prefetch, no registers, no completion), so the
+// register load at the run switch L..2L ratings later hits L2, not DRAM.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int L>
+__device__ __forceinline__ void prefetch_runs(const float* Ub, int row, int kp, bool valid) {
+  const int gl = (threadIdx.x & 31) & (L - 1);
+  const int prev = __shfl_up_sync(0xffffffffu, row, 1);
+  if (valid && (gl == 0 || prev != row)) prefetch_l2(Ub + (int64_t)row * kp, (unsigned)kp * 4u);
+}
+
 // L2-coherent 128-bit load (the factors are written by other SMs during the
 // kernel; ld.global.cg never returns a stale L1 line).
 __device__ __forceinline__ float4 ld_cg(const float* p) {
@@ -277,7 +292,7 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
                                              const float* __restrict__ val, float* U, float* V,
                                              int kp, float alpha, float beta, int iter,
                                              unsigned long long* bad, int cbits = -1,
-                                             float* sbuf = nullptr) {
+                                             float* sbuf = nullptr, bool upf = false) {
   constexpr bool kBulk = MODE == 1;
   constexpr bool kURing = MODE == 2 && kSweep && L >= 4;
   constexpr int UD = L >= 8 ? 4 : 3;  // ring depth (needs UD < L: rows from batches A, B)
@@ -298,6 +313,7 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
   float xA = 0.f, xB = 0.f;
   if (ln.gl < len) load_triple(lrow, lcol, val, cbits, ch.begin + ln.gl, rA, cA, xA);
   if (L + ln.gl < len) load_triple(lrow, lcol, val, cbits, ch.begin + L + ln.gl, rB, cB, xB);
+  if (upf) prefetch_runs<L>(Ub, rB, kp, L + ln.gl < len);
   int r = __shfl_sync(kFull, rA, ln.gbase);
   int c = __shfl_sync(kFull, cA, ln.gbase);
   float x = __shfl_sync(kFull, xA, ln.gbase);
@@ -440,6 +456,7 @@ __device__ __forceinline__ double walk_chunk(const Chunk& ch, int maxlen,
     rA = rB; cA = cB; xA = xB;
     const int nb = t0 + 2 * L + ln.gl;
     if (nb < len) load_triple(lrow, lcol, val, cbits, ch.begin + nb, rB, cB, xB);
+    if (upf) prefetch_runs<L>(Ub, rB, kp, nb < len);
   }
   if (kSweep && kBulk && ln.gl == 0) bulk_wait_all();
   if (kURing) cp_async_wait<0>();
@@ -452,9 +469,11 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                 const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
                 const float* __restrict__ val, float* __restrict__ U, float* __restrict__ V,
                 int kp, float alpha, float beta, int iter, unsigned long long* __restrict__ bad,
-                int cbits, int dyn_d, unsigned* __restrict__ dyn, int snap) {
+                int cbits, int dyn_d, unsigned* __restrict__ dyn, int flags) {
   constexpr int GPW = 32 / L;
   extern __shared__ float4 smem_rows[];
+  const int snap = flags & 0xFFFF;     // run-aligned chunk edges (0: off)
+  const bool upf = (flags >> 16) & 1;  // U-row L2 prefetch
   const int lane = threadIdx.x & 31;
   const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   // bulk: this group's delta ring, kBulkBufs rows of kp floats; uring: this
@@ -475,7 +494,7 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
     if (maxlen == 0) return;
     pdl_wait();
     walk_chunk<L, V4, kMask, true, MODE>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta,
-                                         iter, bad, cbits, sbuf);
+                                         iter, bad, cbits, sbuf, upf);
     return;
   }
   // dynamic: slot = this warp, then nwarps + a ticket from dyn[0] until the
@@ -496,7 +515,7 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
     const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)(ch.end - ch.begin));
     if (maxlen > 0)
       walk_chunk<L, V4, kMask, true, MODE>(ch, maxlen, lrow, lcol, val, U, V, kp, alpha, beta,
-                                           iter, bad, cbits, sbuf);
+                                           iter, bad, cbits, sbuf, upf);
     unsigned t = 0;
     if (lane == 0) t = atomicAdd(dyn, 1u);
     slot = nwarps + (int)__shfl_sync(kFull, t, 0);
@@ -546,7 +565,7 @@ __device__ __forceinline__ double sse_async_walk(const Chunk& ch, const int32_t*
                                                  const float* __restrict__ val,
                                                  const float* __restrict__ U,
                                                  const float* __restrict__ V, int kp, int cbits,
-                                                 float4* ring) {
+                                                 float4* ring, bool upf = false) {
   static_assert(D <= L, "the look-ahead must fit the two triple batches");
   const int len = (int)(ch.end - ch.begin);
   const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)len);
@@ -568,6 +587,7 @@ __device__ __forceinline__ double sse_async_walk(const Chunk& ch, const int32_t*
   float xA = 0.f, xB = 0.f;
   if (ln.gl < len) load_triple(lrow, lcol, val, cbits, ch.begin + ln.gl, rA, cA, xA);
   if (L + ln.gl < len) load_triple(lrow, lcol, val, cbits, ch.begin + L + ln.gl, rB, cB, xB);
+  if (upf) prefetch_runs<L>(Ub, rB, kp, L + ln.gl < len);
 #pragma unroll
   for (int d = 0; d < D; ++d) issue(d, __shfl_sync(kFull, cA, ln.gbase + d));
   int r = __shfl_sync(kFull, rA, ln.gbase);
@@ -657,6 +677,7 @@ __device__ __forceinline__ double sse_async_walk(const Chunk& ch, const int32_t*
       rA = rB; cA = cB; xA = xB;
       const int nb = t0 + 2 * L + ln.gl;
       if (nb < len) load_triple(lrow, lcol, val, cbits, ch.begin + nb, rB, cB, xB);
+      if (upf) prefetch_runs<L>(Ub, rB, kp, nb < len);
     }
     // only lanes gl == 0 (rating t) and gl == H (rating t+1) hold each sum once
     if (ln.gl != 0 && ln.gl != H) acc = 0.0;
@@ -695,6 +716,7 @@ __device__ __forceinline__ double sse_async_walk(const Chunk& ch, const int32_t*
     rA = rB; cA = cB; xA = xB;
     const int nb = t0 + 2 * L + ln.gl;
     if (nb < len) load_triple(lrow, lcol, val, cbits, ch.begin + nb, rB, cB, xB);
+    if (upf) prefetch_runs<L>(Ub, rB, kp, nb < len);
   }
   }
   cp_async_wait<0>();
@@ -706,7 +728,8 @@ __global__ void __launch_bounds__(256, 2)
 sse_async_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                  const int32_t* __restrict__ lrow, const int32_t* __restrict__ lcol,
                  const float* __restrict__ val, const float* __restrict__ U,
-                 const float* __restrict__ V, int kp, double* __restrict__ sse, int cbits) {
+                 const float* __restrict__ V, int kp, double* __restrict__ sse, int cbits,
+                 int upf) {
   constexpr int GPW = 32 / L;
   // this lane's D slots of V4 float4, lane-interleaved ([slot][q][thread]) so a
   // warp's 16-byte accesses hit 32 consecutive bank quads
@@ -717,7 +740,7 @@ sse_async_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks
   pdl_trigger();
   pdl_wait();
   const double acc = sse_async_walk<L, V4, kMask, D>(ch, lrow, lcol, val, U, V, kp, cbits,
-                                                      ring_all + threadIdx.x);
+                                                      ring_all + threadIdx.x, upf != 0);
   if ((lane & (L - 1)) == 0 && ch.end > ch.begin) atomicAdd(sse + ch.block_id, acc);
 }
 
@@ -1076,6 +1099,8 @@ void launch_sse_wide(cudaStream_t s, const BlockWork* w, int nwork, int total,
 #undef BGMF_SSE
 }
 
+bool upf_route(bgmf_ctx* c);
+
 template <int LL, int VV, bool MM>
 void launch_sse_async(dim3 grid, cudaStream_t s, const BlockWork* w, int nwork, int total,
                       const int32_t* lrow, const int32_t* lcol, const float* val, bgmf_ctx* c,
@@ -1090,7 +1115,8 @@ void launch_sse_async(dim3 grid, cudaStream_t s, const BlockWork* w, int nwork, 
     attr_set.fetch_or(bit);
   }
   launch_k(c->pdl, &sse_async_kernel<LL, VV, MM, D>, grid, 256, smem, s, w, nwork, total, lrow,
-           lcol, val, (const float*)c->d_u, (const float*)c->d_v, c->kp, c->d_sse, cbits);
+           lcol, val, (const float*)c->d_u, (const float*)c->d_v, c->kp, c->d_sse, cbits,
+           upf_route(c) ? 1 : 0);
 }
 
 // dynamic smem of the bulk sweep: kBulkBufs delta rows per group
@@ -1098,12 +1124,34 @@ size_t bulk_smem(bgmf_ctx* c, const Shape& sh) {
   return (size_t)(256 / sh.L) * kBulkBufs * c->kp * sizeof(float);
 }
 
+// u_prefetch routing: the L2 prefetch of the next runs' U rows pays only when
+// nearly every rating starts a user run (C5 shape with 600 M ratings, 0.94
+// ratings per (row, block): sweep 0.268 -> 0.248 ms, +11%) and costs issue
+// slots and L2 bandwidth otherwise (C5 2 B, 3.1: 0.416 -> 0.437 ms; C4, 13:
+// -3%; C3, 18: -5%).  Mean run length = ratings / rows of the non-empty
+// blocks (a ring rank's partition holds only its row blocks).
+constexpr double kUpfMaxRun = 1.5;
+
+bool upf_route(bgmf_ctx* c) {
+  const int64_t key = c->nnz * 8191 + (int64_t)c->I * c->J;
+  if (c->upf_key != key) {
+    double rows = 0.0;
+    for (int b = 0; b < c->I * c->J && b + 1 < (int)c->h_offsets.size(); ++b)
+      if (c->h_offsets[b + 1] > c->h_offsets[b])
+        rows += (double)(c->row_bounds[b / c->J + 1] - c->row_bounds[b / c->J]);
+    const double run = rows > 0.0 ? (double)c->nnz / rows : 0.0;
+    c->upf_on = c->u_prefetch > 0 || (c->u_prefetch < 0 && rows > 0.0 && run < kUpfMaxRun);
+    c->upf_key = key;
+  }
+  return c->upf_on;
+}
+
 void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, const BlockWork* w,
                      int nwork, int total, const int32_t* lrow, const int32_t* lcol,
                      const float* val, bgmf_ctx* c, float a, float b, int it, int cbits = -1) {
   const bool mk = needs_mask(sh, c->kp);
   const int dd = sweep && c->d_dyn ? c->dyn_split : 1;
-  const int sn = c->snap_cap;
+  const int sn = c->snap_cap | (upf_route(c) ? 1 << 16 : 0);
 #define BGMF_CASE(LL, VV, MM)                                                                 \
   if (sh.L == LL && sh.V4 == VV && mk == MM) {                                                \
     if (sweep && c->bulk_red) {                                                               \
