@@ -482,7 +482,18 @@ sgd_fast_kernel(const BlockWork* __restrict__ work, int nwork, int total_chunks,
                           : reinterpret_cast<float*>(smem_rows) +
                                 (size_t)((threadIdx.x >> 5) * GPW + lane / L) * kBulkBufs * kp;
   if (dyn_d <= 1) {
-    Chunk ch = locate_chunk(work, nwork, total_chunks, warp * GPW + lane / L);
+    int cidx = warp * GPW + lane / L;
+    if ((flags >> 17) & 1) {
+      // spread: fewer chunks than the grid's groups (a stratum whose per-block
+      // concurrency floors bind), dealt evenly over the CTAs -- a full wave of
+      // CTAs, so every SM holds the same number of working groups, instead of
+      // the last SMs holding one CTA where the others hold two
+      const int nb = (int)gridDim.x, b = (int)blockIdx.x;
+      const int q = total_chunks / nb, rem = total_chunks % nb;
+      const int lg = (int)(threadIdx.x >> 5) * GPW + lane / L;
+      cidx = lg < q + (b < rem) ? b * q + min(b, rem) + lg : total_chunks;
+    }
+    Chunk ch = locate_chunk(work, nwork, total_chunks, cidx);
     if (snap > 0) {
       const int64_t b = snap_edge<L>(lrow, cbits, ch.begin, ch.bbeg, ch.bend, snap);
       const int64_t e = snap_edge<L>(lrow, cbits, ch.end, ch.bbeg, ch.bend, snap);
@@ -1132,6 +1143,8 @@ size_t bulk_smem(bgmf_ctx* c, const Shape& sh) {
 // blocks (a ring rank's partition holds only its row blocks).
 constexpr double kUpfMaxRun = 1.5;
 
+int64_t sweep_groups(bgmf_ctx* c, const Shape& sh);
+
 bool upf_route(bgmf_ctx* c) {
   const int64_t key = c->nnz * 8191 + (int64_t)c->I * c->J;
   if (c->upf_key != key) {
@@ -1151,7 +1164,16 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
                      const float* val, bgmf_ctx* c, float a, float b, int it, int cbits = -1) {
   const bool mk = needs_mask(sh, c->kp);
   const int dd = sweep && c->d_dyn ? c->dyn_split : 1;
-  const int sn = c->snap_cap | (upf_route(c) ? 1 << 16 : 0);
+  int sn = c->snap_cap | (upf_route(c) ? 1 << 16 : 0);
+  if (sweep && c->spread && dd <= 1 && !c->bulk_red && !c->u_ring) {
+    // a partial wave that would leave some SMs with fewer CTAs than others:
+    // launch the full wave and deal the chunks evenly (sgd_fast_kernel)
+    const int64_t cap = sweep_groups(c, sh) / (8 * (32 / sh.L));
+    if ((int64_t)grid.x > c->num_sms && (int64_t)grid.x * 20 < cap * 19) {
+      grid.x = (unsigned)cap;
+      sn |= 1 << 17;
+    }
+  }
 #define BGMF_CASE(LL, VV, MM)                                                                 \
   if (sh.L == LL && sh.V4 == VV && mk == MM) {                                                \
     if (sweep && c->bulk_red) {                                                               \
