@@ -80,7 +80,26 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      barriers); 0 = one launch per stratum sweep / SSE pass;
  *                      -1 = auto (default): fused when a stratum holds at most
  *                      "fused_max_batch" ratings (default 0: measured on B200,
- *                      the per-stratum launches win at every config size). */
+ *                      the per-stratum launches win at every config size).
+ *   "ordered"    -1/0/1  -1 (default) = route batches whose chunked order would
+ *                      distort the reference (dense blocks, chunks shorter
+ *                      than a row, >1 group per V row) to the ordered stratum
+ *                      kernel (every update in stored order, deterministic);
+ *                      1 = always when it fits; 0 = never.
+ *   "ord_row_split", "ord_col_conc"  float  the routing thresholds above
+ *                      (1.0 / 1.0; ring ranks use ord_col_conc 6).
+ *   "ord_stage_ratings" int, "ord_fill_ctas" int, "ord_warp" 0/1  ordered
+ *                      kernel stage size (1024), CTAs per SM, one group per warp.
+ *   "pdl"        0/1   programmatic dependent launch between sweep and SSE (1).
+ *   "conv_graph" 0/1   ConvergeEachBlock steps as a CUDA graph with device-side
+ *                      while-nodes (1) instead of host-driven sweeps.
+ *   "no_val8"    0/1   streamed ratings never use 1-byte value codes.
+ *   "spread"     0/1   partial sweep waves dealt evenly over a full wave of
+ *                      CTAs (1).
+ *   "u_prefetch" -1/0/1  L2 prefetch of upcoming runs' U rows: -1 (default)
+ *                      when the mean run is < 1.5 ratings, 1 on, 0 off.
+ *   Measured slower and kept off: "fuse_sse",
+ *   "u_ring", "dyn_split" (int D), "snap" (int cap). */
 int bgmf_set_option(bgmf_ctx* ctx, const char* key, double value);
 
 /* Bucket the ratings into the I x J block grid on the GPU.

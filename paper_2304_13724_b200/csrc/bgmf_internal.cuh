@@ -78,7 +78,7 @@ struct bgmf_ctx {
   bool fuse_sse = false;  // last sweep + SSE in one launch (sweep_sse_kernel; measured slower)
   unsigned* d_fuse = nullptr;  // sweep_sse_kernel's per-work-item counters
   int dyn_split = 1;           // sweep: chunks cut D ways, taken from a ticket counter
-  unsigned* d_dyn = nullptr;   // its two self-resetting counters (allocated at create)
+  unsigned* d_dyn = nullptr;   // its two self-resetting counters (allocated with the option)
   int u_prefetch = -1;         // sweep/SSE L2 prefetch of upcoming runs' U rows: 1 on, 0 off,
                                // -1 when runs are short (upf_route)
   bool upf_on = false;         // resolved for the current partition

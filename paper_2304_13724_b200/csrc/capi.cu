@@ -167,13 +167,6 @@ int bgmf_create(int device, void* stream, bgmf_ctx** out) {
     if (e != cudaSuccess) { delete c; return cuda_fail(nullptr, e, "cudaStreamCreate"); }
     c->own_stream = true;
   }
-  e = cudaMalloc(&c->d_dyn, 2 * sizeof(unsigned));
-  if (e == cudaSuccess) e = cudaMemset(c->d_dyn, 0, 2 * sizeof(unsigned));
-  if (e != cudaSuccess) {
-    if (c->own_stream) cudaStreamDestroy(c->stream);
-    delete c;
-    return cuda_fail(nullptr, e, "cudaMalloc");
-  }
   *out = c;
   return BGMF_OK;
 }
@@ -231,7 +224,15 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "u_prefetch")) { c->u_prefetch = value < 0.0 ? -1 : value != 0.0; c->upf_key = -1; }
   else if (!strcmp(key, "spread")) c->spread = value != 0.0;
   else if (!strcmp(key, "snap")) c->snap_cap = value < 0.0 ? 0 : value > 4096.0 ? 4096 : (int)value;
-  else if (!strcmp(key, "dyn_split")) c->dyn_split = value < 1.0 ? 1 : value > 16.0 ? 16 : (int)value;
+  else if (!strcmp(key, "dyn_split")) {
+    c->dyn_split = value < 1.0 ? 1 : value > 16.0 ? 16 : (int)value;
+    if (c->dyn_split > 1 && !c->d_dyn) {  // the ticket counters, zeroed once
+      cudaSetDevice(c->device);
+      cudaError_t e = cudaMalloc(&c->d_dyn, 2 * sizeof(unsigned));
+      if (e == cudaSuccess) e = cudaMemset(c->d_dyn, 0, 2 * sizeof(unsigned));
+      if (e != cudaSuccess) { c->dyn_split = 1; return cuda_fail(c, e, "dyn_split counters"); }
+    }
+  }
   else if (!strcmp(key, "pdl")) c->pdl = value != 0.0;
   else if (!strcmp(key, "conv_graph")) c->conv_graph = value != 0.0;
   else if (!strcmp(key, "ord_col_conc")) c->ord_col_conc = value;
