@@ -207,7 +207,8 @@ def test_c4_parity_vs_oracle():
     """C4 at full size (the headline config: 100M ratings, k=128, 16x16, the
     bench's alpha/beta): 2 epochs through the public API against the oracle's
     fp64 restatement of the reference on the same input -- per-epoch train
-    RMSE within 1e-3, final full-set RMSE within 1e-3, finite model."""
+    RMSE within 1e-3, final full-set RMSE within 1e-3, finite model; exact
+    mode bit-identical (trace, U, V)."""
     w = workloads.CONFIGS["C4"]
     r, c, v = workloads.lowrank(w.n, w.m, w.nnz, seed=w.seed)
     d = bm.RatingsDataset(w.n, w.m, r, c, v)
@@ -224,6 +225,11 @@ def test_c4_parity_vs_oracle():
     print(f"C4 max |d train_rmse| over 2 epochs: {drift.max():.3e}")
     assert drift.max() <= TOL
     assert abs(bm.rmse(res.model, d) - O.rmse(ou, ov, d.rows, d.cols, d.values)) <= TOL
+    # exact mode (fp64, the ordered schedule) at full size: bit-identical to
+    # the reference epoch -- trace and both factor matrices
+    ex = bm.train_blocked(d, cfg, early_stop=False, options=bm.EngineOptions(exact=True))
+    assert [s.train_rmse for s in ex.trace] == [s["train_rmse"] for s in otr]
+    assert np.array_equal(ex.model.u, ou) and np.array_equal(ex.model.v, ov)
 
 
 @pytest.mark.slow
