@@ -518,6 +518,28 @@ ordered_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restrict__ 
 // post-sweep SSE (_kernels.py:16-28) is a sequential sum: every entry's
 // (x - u.v)^2 is computed in parallel into `esq`, then one thread adds them
 // in stored order.
+// e = x - u0 v0 - u1 v1 - ... in the reference's order with separately rounded
+// products (_kernels.py:44-48).  The products do not depend on the chain, so
+// lane g computes u_g v_g for its elements in parallel and every lane runs the
+// subtraction chain over them in g order, the operands broadcast by shuffles
+// that issue ahead of the chain: the serial part is k dependent DADDs, not k
+// shared-memory load pairs + DMUL + DADD on one lane.  Same bits on all lanes.
+__device__ __forceinline__ double exact_residual(double x, const double* us, const double* vs,
+                                                 int k, int lane) {
+  double e = x;
+  for (int j = 0; j * 32 < k; ++j) {
+    const int g = j * 32 + lane;
+    const double p = g < k ? __dmul_rn(us[g], vs[g]) : 0.0;
+    if (k - j * 32 >= 32) {
+#pragma unroll
+      for (int l = 0; l < 32; ++l) e = __dsub_rn(e, __shfl_sync(kFull, p, l));
+    } else {
+      for (int l = 0; l < k - j * 32; ++l) e = __dsub_rn(e, __shfl_sync(kFull, p, l));
+    }
+  }
+  return e;
+}
+
 __device__ __forceinline__ void exact_stage_sweep(const Stage& T, double* sv, double* urow,
                                                   const double* __restrict__ bval,
                                                   double* __restrict__ Ub, int it, uint32_t gen,
@@ -582,10 +604,7 @@ __device__ __forceinline__ void exact_stage_sweep(const Stage& T, double* sv, do
         SpinGuard sg;
         while (!__all_sync(kFull, ld_acquire_cta(cp) == q)) sg.tick();
         double* vs = sv + (size_t)c * k;
-        double e = x;
-        if (lane == 0)
-          for (int g = 0; g < k; ++g) e = __dsub_rn(e, __dmul_rn(us[g], vs[g]));
-        e = __shfl_sync(kFull, e, 0);
+        const double e = exact_residual(x, us, vs, k, lane);
         if (!isfinite(e) && lane == 0) {
           atomicMin(bad, pack_bad(pos, it, t0 + j - T.e0));
           *divflag = 1;
@@ -612,7 +631,7 @@ __device__ __forceinline__ void exact_stage_sweep(const Stage& T, double* sv, do
 
 // (x - u.v)^2 of every entry of this stage's slab into esq (entry order is
 // irrelevant: the sum below is sequential)
-__device__ __forceinline__ void exact_stage_esq(const Stage& T, const double* sv,
+__device__ __forceinline__ void exact_stage_esq(const Stage& T, const double* sv, double* urow,
                                                 const double* __restrict__ bval,
                                                 const double* __restrict__ Ub,
                                                 double* __restrict__ besq) {
@@ -624,31 +643,69 @@ __device__ __forceinline__ void exact_stage_esq(const Stage& T, const double* sv
     int lo = rb, hi = re;
     if (T.cs > 0) lo = group_lower_bound<32>(T.bcol, rb, re, T.cs, lane, kFull);
     if (T.ce < T.w) hi = group_lower_bound<32>(T.bcol, lo, re, T.ce, lane, kFull);
+    if (lo == hi) continue;
+    // the row's u into this warp's shared-memory row, so the per-lane chains
+    // below read it with LDS (unrolled, issued ahead of the DSUB chain)
+    // instead of one dependent L2 load per element
     const double* ug = Ub + (int64_t)r * k;
+    double* us = urow + (threadIdx.x >> 5) * k;
+    __syncwarp();
+    for (int g = lane; g < k; g += 32) us[g] = __ldcg(ug + g);
+    __syncwarp();
     for (int i = lo + lane; i < hi; i += 32) {
       const double* vs = sv + (size_t)(__ldg(T.bcol + i) - T.cs) * k;
       double e = __ldg(bval + i);
-      for (int g = 0; g < k; ++g) e = __dsub_rn(e, __dmul_rn(__ldcg(ug + g), vs[g]));
+#pragma unroll 8
+      for (int g = 0; g < k; ++g) e = __dsub_rn(e, __dmul_rn(us[g], vs[g]));
       besq[i] = __dmul_rn(e, e);
     }
   }
 }
 
 // The block's SSE, summed in stored order by one thread; every stage gets it.
-__device__ __forceinline__ double exact_block_sse(const Stage& T, const double* sv,
+__device__ __forceinline__ double exact_block_sse(const Stage& T, const double* sv, double* urow,
                                                   const double* __restrict__ bval,
                                                   const double* __restrict__ Ub,
                                                   double* __restrict__ besq, double* part,
                                                   int stage0, uint32_t* ctr, uint32_t& nbar,
                                                   double* s_bcast) {
-  exact_stage_esq(T, sv, bval, Ub, besq);
+  exact_stage_esq(T, sv, urow, bval, Ub, besq);
   block_barrier(ctr, T.S, nbar++);  // every stage's terms are written
-  if (T.st == 0 && threadIdx.x == 0) {
+  if (T.st == 0 && threadIdx.x < 32) {
+    // the stored-order sum s += esq[i] (_kernels.py:16-28) by one warp: tiles
+    // of 32 terms loaded coalesced PF tiles ahead, then added in order from
+    // shuffles -- every lane runs the same DADD chain (same bits), which is
+    // then the only serial part (one thread with one L2 load per term before)
+    const int lane = threadIdx.x;
     const int e0 = __ldg(T.rp), e1 = __ldg(T.rp + T.h);
+    constexpr int PF = 8;
+    double buf[PF];
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+      const int i = e0 + p * 32 + lane;
+      buf[p] = i < e1 ? __ldcg(besq + i) : 0.0;
+    }
     double s = 0.0;
-    for (int i = e0; i < e1; ++i) s = __dadd_rn(s, __ldcg(besq + i));
-    part[stage0] = s;
-    *s_bcast = s;
+    for (int t = e0; t < e1; t += 32 * PF) {
+#pragma unroll
+      for (int p = 0; p < PF; ++p) {
+        const int base = t + p * 32;
+        const double cur = buf[p];
+        const int ni = base + PF * 32 + lane;
+        buf[p] = ni < e1 ? __ldcg(besq + ni) : 0.0;
+        const int n = min(32, e1 - base);
+        if (n == 32) {
+#pragma unroll
+          for (int l = 0; l < 32; ++l) s = __dadd_rn(s, __shfl_sync(kFull, cur, l));
+        } else {
+          for (int l = 0; l < n; ++l) s = __dadd_rn(s, __shfl_sync(kFull, cur, l));
+        }
+      }
+    }
+    if (lane == 0) {
+      part[stage0] = s;
+      *s_bcast = s;
+    }
   }
   if (T.S > 1) {
     block_barrier(ctr, T.S, nbar++);
@@ -743,11 +800,11 @@ ordered_exact_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restr
       exact_stage_sweep(T, sv, urow, bval, Ub, it, gen, alpha, beta, B.pos, &s_next, bad, &s_div);
     swept = iters;
     block_barrier(ctr, T.S, nbar++);  // every stage done: U is final
-    sse_now = exact_block_sse(T, sv, bval, Ub, besq, part, B.stage0, ctr, nbar, &s_bcast);
+    sse_now = exact_block_sse(T, sv, urow, bval, Ub, besq, part, B.stage0, ctr, nbar, &s_bcast);
     if (!isfinite(sse_now) && threadIdx.x == 0 && T.st == 0)  // _kernels.py:56-58
       atomicMin(bad, pack_bad(B.pos, iters - 1, (int64_t)cntd - 1));
   } else {
-    sse_now = exact_block_sse(T, sv, bval, Ub, besq, part, B.stage0, ctr, nbar, &s_bcast);
+    sse_now = exact_block_sse(T, sv, urow, bval, Ub, besq, part, B.stage0, ctr, nbar, &s_bcast);
     double rmse_prev = sqrt(sse_now / cntd);
     bool capped = true;
     while (swept < iters) {
@@ -762,7 +819,7 @@ ordered_exact_kernel(const __grid_constant__ OrdLaunch P, const int32_t* __restr
       const bool diverged = s_bcast != 0.0;
       __syncthreads();
       if (diverged) { capped = false; sse_now = nan; break; }
-      sse_now = exact_block_sse(T, sv, bval, Ub, besq, part, B.stage0, ctr, nbar, &s_bcast);
+      sse_now = exact_block_sse(T, sv, urow, bval, Ub, besq, part, B.stage0, ctr, nbar, &s_bcast);
       if (!isfinite(sse_now)) {
         if (threadIdx.x == 0 && T.st == 0)
           atomicMin(bad, pack_bad(B.pos, swept - 1, (int64_t)cntd - 1));
