@@ -277,6 +277,10 @@ void pinned_free(void* p);
 // GB-sized pinned arrays: THP-backed + cudaHostRegister; freed off-thread
 cudaError_t big_pinned_alloc(void** p, size_t bytes);
 void big_pinned_free(void* p);
+void* big_host_alloc(size_t bytes);
+void big_host_free(void* p);
+void big_host_release(void* p, size_t bytes);
+int staged_h2d(bgmf_ctx* ctx, void* dst, const void* src, size_t bytes);
 int upload_rows(bgmf_ctx* c, const double* h, float* d, int64_t rows, int k, int kp);
 
 // synth.cu (benchmark / test input generator)

@@ -627,6 +627,7 @@ int bgmf_partition_ooc(bgmf_ctx* c, const int64_t* rows, const int64_t* cols,
                        int64_t row_lo, int64_t row_hi) {
   if (!c) return fail(nullptr, BGMF_ERR_ARG, "ctx is NULL");
   cudaSetDevice(c->device);
+  prof_mark(c, nullptr);
   dfree(c->d_sse, c->stream); pinned_free(c->h_sse); dfree(c->d_fuse, c->stream); c->d_fuse = nullptr; dfree(c->d_cstate, c->stream); c->d_cstate = nullptr; c->cstate_cap = 0; conv_graphs_release(c); dfree(c->d_bad, c->stream); pinned_free(c->h_bad);
   c->d_sse = nullptr; c->h_sse = nullptr; c->d_bad = nullptr; c->h_bad = nullptr;
   return partition_ooc(c, rows, cols, vals, nnz, n, m, grid_i, grid_j, device_budget,

@@ -17,6 +17,8 @@
 #include <omp.h>
 #include <sys/mman.h>
 
+#include <algorithm>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <thread>
@@ -170,6 +172,80 @@ cudaError_t big_pinned_alloc(void** out, size_t bytes) {
   }
   *out = p;
   return cudaSuccess;
+}
+
+// Large pageable host buffer: THP-backed anonymous memory, faulted in by the
+// writing threads (no zero-fill pass, no pinning).  For data that crosses
+// PCIe once (the out-of-core partition's buckets): staged_h2d moves it, so
+// neither the registration (~24 GB/s) nor the unregistration -- which holds
+// the driver lock for seconds on tens of GB, stalling every CUDA call of the
+// process -- is paid.
+void* big_host_alloc(size_t bytes) {
+  const size_t huge = size_t(2) << 20;
+  const size_t len = (bytes + huge - 1) / huge * huge + huge;
+  void* base = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (base == MAP_FAILED) return nullptr;
+  char* p = reinterpret_cast<char*>(((uintptr_t)base + huge - 1) / huge * huge);
+  madvise(p, len - huge, MADV_HUGEPAGE);
+  {
+    std::lock_guard<std::mutex> lk(big_pinned().mu);
+    big_pinned().maps[p] = {base, len};
+  }
+  return p;
+}
+
+void big_host_free(void* p) {
+  if (!p) return;
+  std::pair<void*, size_t> m{nullptr, 0};
+  {
+    std::lock_guard<std::mutex> lk(big_pinned().mu);
+    auto it = big_pinned().maps.find(p);
+    if (it == big_pinned().maps.end()) return;
+    m = it->second;
+    big_pinned().maps.erase(it);
+  }
+  std::thread([m]() { munmap(m.first, m.second); }).detach();
+}
+
+// Give the physical pages of [p, p + bytes) back (whole 2 MiB pages inside
+// the range only): madvise(MADV_DONTNEED) runs under the mm read lock, so
+// other threads' faults and CUDA calls proceed -- unlike one munmap of tens
+// of GB at the end, which holds the write lock for seconds.
+void big_host_release(void* p, size_t bytes) {
+  const uintptr_t huge = uintptr_t(2) << 20;
+  const uintptr_t a = ((uintptr_t)p + huge - 1) / huge * huge;
+  const uintptr_t e = ((uintptr_t)p + bytes) / huge * huge;
+  if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_DONTNEED);
+}
+
+// Host -> device copy of pageable memory through the process's pinned staging
+// pair: host threads copy piece p+1 into one buffer while the DMA engine moves
+// piece p out of the other (pageable cudaMemcpy runs at ~11 GB/s; this at the
+// pinned PCIe rate when the host copy keeps up).  Stream-ordered on
+// ctx->stream; returns when the last piece has left the staging buffers.
+int staged_h2d(bgmf_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  Stage st(ctx);
+  if (st.error()) return cuda_fail(ctx, st.error(), "staging pool");
+  const char* s = static_cast<const char*>(src);
+  char* d = static_cast<char*>(dst);
+  int k = 0;
+  for (size_t o = 0; o < bytes; o += kStageBytes, ++k) {
+    const int b = k & 1;
+    const size_t n = std::min(kStageBytes, bytes - o);
+    if (k >= 2) cudaEventSynchronize(st.done(b));
+    char* buf = st.buf(b);
+    const int64_t parts = 16;
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < parts; ++q) {
+      const size_t a = n * q / parts, e = n * (q + 1) / parts;
+      memcpy(buf + a, s + o + a, e - a);
+    }
+    cudaError_t e = cudaMemcpyAsync(d + o, buf, n, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(st.done(b), ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "staged H2D");
+  }
+  for (int b = 0; b < 2 && k > 0; ++b) cudaEventSynchronize(st.done(b));
+  return BGMF_OK;
 }
 
 // Frees a big_pinned_alloc buffer (asynchronously) or a cudaMallocHost one.

@@ -28,6 +28,8 @@
 
 #include <algorithm>
 
+#include <thread>
+
 #include "bgmf_internal.cuh"
 
 namespace bgmf {
@@ -650,7 +652,7 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   free_dev(ctx->d_val, ctx->stream); free_dev(ctx->d_val64, ctx->stream);
   free_dev(ctx->d_order, ctx->stream);
   ctx->partitioned = false;
-  prof_mark(ctx, nullptr);
+  prof_mark(ctx, "ooc: release previous state");
 
   const int64_t rbase = n / I, rextra = n % I, cbase = m / J, cextra = m % J;
   const int rbits = bits_for((uint64_t)(rbase + (rextra ? 1 : 0)) - 1);
@@ -743,23 +745,27 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   prof_mark(ctx, "ooc: host count pass");
 
   // 3. buckets: narrowed entries + input index, per chunk in input order
-  // buckets in pinned memory (THP-backed, hostio.cu): no zero-fill, faulted
-  // in by the host threads, and the chunk uploads below are then DMA at full
-  // PCIe rate (a std::vector's single-threaded zero-fill of C5's 32 GB and
-  // pageable uploads cost 13 s and 3.5 s)
+  // buckets in THP-backed pageable memory (hostio.cu big_host_alloc): no
+  // zero-fill (faulted in by the bucket pass's threads), and no pinning --
+  // they cross PCIe once, through the pinned staging pair (staged_h2d).
+  // Pinned buckets cost 1.3 s to register and ~2 s to unregister on C5's
+  // 32 GB, the latter holding the driver lock (a std::vector's zero-fill and
+  // plain pageable uploads cost 13 s and 3.5 s before that).
   const size_t N = (size_t)(kept > 0 ? kept : 1);
   struct Bucket {
     int32_t* r = nullptr;
     int32_t* c = nullptr;
     float* v = nullptr;
     uint32_t* x = nullptr;
-    ~Bucket() { big_pinned_free(r); big_pinned_free(c); big_pinned_free(v); big_pinned_free(x); }
+    ~Bucket() { big_host_free(r); big_host_free(c); big_host_free(v); big_host_free(x); }
   } bk;
-  BGMF_CK(ctx, big_pinned_alloc((void**)&bk.r, N * 4));
-  BGMF_CK(ctx, big_pinned_alloc((void**)&bk.c, N * 4));
-  BGMF_CK(ctx, big_pinned_alloc((void**)&bk.v, N * 4));
-  BGMF_CK(ctx, big_pinned_alloc((void**)&bk.x, N * 4));
-  prof_mark(ctx, "ooc: pinned buckets");
+  bk.r = static_cast<int32_t*>(big_host_alloc(N * 4));
+  bk.c = static_cast<int32_t*>(big_host_alloc(N * 4));
+  bk.v = static_cast<float*>(big_host_alloc(N * 4));
+  bk.x = static_cast<uint32_t*>(big_host_alloc(N * 4));
+  if (!bk.r || !bk.c || !bk.v || !bk.x)
+    return fail(ctx, BGMF_ERR_NOMEM, "out of host memory for the partition buckets");
+  prof_mark(ctx, "ooc: bucket memory");
   int32_t* const br = bk.r;
   int32_t* const bc = bk.c;
   float* const bv = bk.v;
@@ -849,7 +855,9 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   uint64_t* ka = nullptr;
   unsigned long long* d_bad = nullptr;
   int rc = BGMF_OK;
+  std::thread releaser;
   auto cleanup = [&]() {
+    if (releaser.joinable()) releaser.join();
     free_dev(d_r, s); free_dev(d_c, s); free_dev(d_v, s); free_dev(d_x, s); free_dev(ka, s);
     free_dev(ia, s); free_dev(lr, s); free_dev(lc, s); free_dev(vv, s); free_dev(ord, s);
     free_dev(rec, s); free_dev(gord, s); free_dev(d_bad, s); free_dev(codes, s);
@@ -869,10 +877,20 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   for (int k = 0; k < nch; ++k) {
     const int64_t cnt = chunk_cnt[k], base = chunk_base[k];
     if (cnt == 0) continue;
-    OCK(cudaMemcpyAsync(d_r, br + base, cnt * 4, cudaMemcpyHostToDevice, s));
-    OCK(cudaMemcpyAsync(d_c, bc + base, cnt * 4, cudaMemcpyHostToDevice, s));
-    OCK(cudaMemcpyAsync(d_v, bv + base, cnt * 4, cudaMemcpyHostToDevice, s));
-    OCK(cudaMemcpyAsync(d_x, bx + base, cnt * 4, cudaMemcpyHostToDevice, s));
+    if (releaser.joinable()) releaser.join();
+    rc = staged_h2d(ctx, d_r, br + base, cnt * 4);
+    if (!rc) rc = staged_h2d(ctx, d_c, bc + base, cnt * 4);
+    if (!rc) rc = staged_h2d(ctx, d_v, bv + base, cnt * 4);
+    if (!rc) rc = staged_h2d(ctx, d_x, bx + base, cnt * 4);
+    if (rc) { cleanup(); return rc; }
+    // this chunk's bucket slices have crossed: a helper thread returns their
+    // pages while this thread waits on the chunk's sort and layout copies
+    releaser = std::thread([=]() {
+      big_host_release(br + base, cnt * 4);
+      big_host_release(bc + base, cnt * 4);
+      big_host_release(bv + base, cnt * 4);
+      big_host_release(bx + base, cnt * 4);
+    });
     OCK(cudaMemsetAsync(d_bad, 0xFF, 8, s));
     OCK(dmalloc(&ka, (size_t)cnt * 8, s));  // the sort swaps buffers: per chunk
     OCK(dmalloc(&ia, (size_t)cnt * 4, s));
@@ -931,6 +949,7 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   ctx->streaming = true;
   rc = stream_slots(ctx, slot_ratings, nslots);
   if (rc) return rc;
+  prof_mark(ctx, "ooc: stream slots");
   ctx->ooc_chunks = nch;
   return BGMF_OK;
 }

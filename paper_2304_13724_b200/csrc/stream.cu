@@ -188,8 +188,10 @@ int stream_slots(bgmf_ctx* c, int64_t slot_ratings, int nslots) {
 
 // Host copies for bgmf_partition_export while streaming (partitioned order).
 int stream_export(bgmf_ctx* c, int64_t* order, int32_t* lrows, int32_t* lcols) {
+  if (!order && !lrows && !lcols) return BGMF_OK;  // offsets only (the trainer's call)
   const int nb = c->I * c->J;
   const uint32_t cmask = c->cbits >= 32 ? 0xFFFFFFFFu : ((1u << c->cbits) - 1u);
+#pragma omp parallel for schedule(dynamic, 1)
   for (int b = 0; b < nb; ++b) {
     const int64_t lo = c->h_offsets[b], cnt = c->h_offsets[b + 1] - lo, src = c->h_pos[b];
     for (int64_t i = 0; i < cnt; ++i) {

@@ -17,6 +17,8 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
+import time
 import threading
 from dataclasses import dataclass, field
 
@@ -158,15 +160,20 @@ class Engine:
             # out-of-core: the partition itself stays under the budget (row
             # blocks in chunks straight into the pinned streaming layout)
             slots = self.options.stream_slots
+            _t0 = time.perf_counter()
             self._check(self._L.bgmf_partition_ooc(
                 self._h, N.ptr(rows, N._i64p), N.ptr(cols, N._i64p), N.ptr(values, N._f64p),
                 len(rows), n, m, grid_i, grid_j, int(budget), int(budget // (12 * slots)),
                 slots, *(row_range if row_range is not None else (0, -1))),
                 data_error=data_error)
+            _t1 = time.perf_counter()
             self.I, self.J, self.n, self.m = grid_i, grid_j, n, m
             off = np.zeros(grid_i * grid_j + 1, np.int64)
             self._check(self._L.bgmf_partition_export(self._h, N.ptr(off, N._i64p), None, None,
                                                       None))
+            if os.environ.get("BGMF_PROFILE"):
+                print(f"[bgmf]   bgmf_partition_ooc call {1e3 * (_t1 - _t0):9.2f} ms, export "
+                      f"{1e3 * (time.perf_counter() - _t1):9.2f} ms", file=sys.stderr)
             self.offsets = off
             self.nnz = int(off[-1])
             self.streaming = True
