@@ -275,7 +275,7 @@ int download_rows(bgmf_ctx* c, const float* d, double* h, int64_t rows, int k, i
 cudaError_t pinned_alloc(void** p, size_t bytes);
 void pinned_free(void* p);
 // GB-sized pinned arrays: THP-backed + cudaHostRegister; freed off-thread
-cudaError_t big_pinned_alloc(void** p, size_t bytes);
+cudaError_t big_pinned_alloc(void** p, size_t bytes, int threads = 0);
 void big_pinned_free(void* p);
 void* big_host_alloc(size_t bytes);
 void big_host_free(void* p);

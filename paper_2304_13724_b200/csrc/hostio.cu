@@ -150,7 +150,7 @@ BigPinned& big_pinned() {
 }
 }  // namespace
 
-cudaError_t big_pinned_alloc(void** out, size_t bytes) {
+cudaError_t big_pinned_alloc(void** out, size_t bytes, int threads) {
   const size_t huge = size_t(2) << 20;
   const size_t len = (bytes + 2 * huge - 1) / huge * huge;
   void* base = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
@@ -159,7 +159,7 @@ cudaError_t big_pinned_alloc(void** out, size_t bytes) {
   const size_t span = (bytes + huge - 1) / huge * huge;
   madvise(p, span, MADV_HUGEPAGE);
   const int64_t pages = (int64_t)(span / huge);
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) num_threads(threads > 0 ? threads : omp_get_max_threads())
   for (int64_t i = 0; i < pages; ++i) p[i * (int64_t)huge] = 0;
   cudaError_t e = cudaHostRegister(p, span, cudaHostRegisterDefault);
   if (e != cudaSuccess) {

@@ -744,6 +744,33 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   for (int k = 0; k < nch; ++k) chunk_base[k + 1] = chunk_base[k] + chunk_cnt[k];
   prof_mark(ctx, "ooc: host count pass");
 
+  // the pinned diagonal layout (stream.cu) is sized now, so a side thread
+  // maps, faults in and registers it (0.6-1.8 s for C5's 18 GB, mostly the
+  // kernel's page pinning) while the bucket pass below runs; 1-byte value
+  // codes (5 B records) when every kept value is an integer in 0..255
+  ctx->packed = rbits + cbits <= 32;
+  ctx->val8 = ctx->packed && !ctx->no_val8;
+  for (int t = 0; t < nth; ++t) ctx->val8 = ctx->val8 && !tnonbyte[t];
+  struct LayoutPin {
+    std::thread t;
+    cudaError_t err = cudaSuccess;
+    void* p[4] = {nullptr, nullptr, nullptr, nullptr};
+    ~LayoutPin() {
+      if (t.joinable()) t.join();
+      for (void* q : p) big_pinned_free(q);  // still owned: an error path
+    }
+  } lay;
+  {
+    const size_t NL = (size_t)(kept > 0 ? kept : 1);
+    const size_t sz[4] = {NL * 4, ctx->packed ? 0 : NL * 4, NL * val_bytes(ctx), NL * 4};
+    const int dev = ctx->device;
+    lay.t = std::thread([&lay, sz, dev]() {
+      cudaSetDevice(dev);
+      for (int q = 0; q < 4 && lay.err == cudaSuccess; ++q)
+        if (sz[q]) lay.err = big_pinned_alloc(&lay.p[q], sz[q], 4);
+    });
+  }
+
   // 3. buckets: narrowed entries + input index, per chunk in input order
   // buckets in THP-backed pageable memory (hostio.cu big_host_alloc): no
   // zero-fill (faulted in by the bucket pass's threads), and no pinning --
@@ -818,11 +845,7 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
   }
   prof_mark(ctx, "ooc: host bucket pass");
 
-  // pinned diagonal layout (stream.cu) and its block positions; 1-byte value
-  // codes (5 B records) when every kept value is an integer in 0..255
-  ctx->packed = rbits + cbits <= 32;
-  ctx->val8 = ctx->packed && !ctx->no_val8;
-  for (int t = 0; t < nth; ++t) ctx->val8 = ctx->val8 && !tnonbyte[t];
+  // the layout's block positions (diagonal order)
   std::vector<int> order;
   order.reserve(nb);
   if (I == J) {
@@ -836,11 +859,14 @@ int partition_ooc(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols, const
     int64_t pos = 0;
     for (int b : order) { ctx->h_pos[b] = pos; pos += bcount[b]; }
   }
-  BGMF_CK(ctx, big_pinned_alloc((void**)&ctx->h_lrow, N * 4));
-  if (!ctx->packed) BGMF_CK(ctx, big_pinned_alloc((void**)&ctx->h_lcol, N * 4));
-  BGMF_CK(ctx, big_pinned_alloc((void**)&ctx->h_val, N * val_bytes(ctx)));
-  BGMF_CK(ctx, big_pinned_alloc((void**)&ctx->h_order, N * 4));
-  prof_mark(ctx, "ooc: pinned layout");
+  lay.t.join();
+  if (lay.err != cudaSuccess) return cuda_fail(ctx, lay.err, "pinned layout");
+  ctx->h_lrow = static_cast<int32_t*>(lay.p[0]);
+  ctx->h_lcol = static_cast<int32_t*>(lay.p[1]);
+  ctx->h_val = static_cast<float*>(lay.p[2]);
+  ctx->h_order = static_cast<uint32_t*>(lay.p[3]);
+  for (void*& q : lay.p) q = nullptr;  // the context owns them now
+  prof_mark(ctx, "ooc: pinned layout (wait)");
 
   // 4. chunk by chunk on the device
   cudaStream_t s = ctx->stream;
