@@ -50,9 +50,13 @@ def run(mode: str, extra: list[str]) -> int:
         env["BGMF_EXACT"] = "1"
     # explicit test files / node ids narrow the run; else the whole suite
     picked = [a for a in extra if a.endswith(".py") or "::" in a]
+    # plus this repository's own test of the "bgmf-b200" CLI variant
+    # (test_variant_plugin.py), which needs the reference CLI copied by sync
+    ours = [os.path.join(HERE, "test_variant_plugin.py")] \
+        if os.path.exists(os.path.join(HERE, "_ref", "cli.py")) else []
     cmd = [sys.executable, "-m", "pytest", "-p", "bgmf_alias", "-q", "-rf",
            "-p", "no:cacheprovider", "--rootdir", os.path.join(HERE, "_ref"),
-           *([] if picked else [os.path.join(HERE, "_ref")]), *extra]
+           *([] if picked else [os.path.join(HERE, "_ref"), *ours]), *extra]
     return subprocess.call(cmd, env=env, cwd=os.path.join(HERE, "_ref"))
 
 
