@@ -262,7 +262,12 @@ __device__ __forceinline__ void stage_sweep(const Stage& T, int it, uint32_t gen
     }
     store_row_g<V4>(T.Ub + (int64_t)r * kp, u, ln);
     if (T.S > 1) {
-      __threadfence();
+      // publish u_r: the group's stores are ordered before lane 0's release by
+      // the warp barrier (bar.warp.sync orders memory among its threads) and a
+      // release is cumulative over what precedes it -- the pattern of
+      // cooperative groups' grid sync (bar.sync, then one thread's fence and
+      // flag).  One release per visit, no full fence.sc (and its L1
+      // invalidation) on every lane before it.
       __syncwarp(gmask);
       if (ln.gl == 0) st_release_gpu(T.fl + r, tag_now);
     }
@@ -620,8 +625,7 @@ __device__ __forceinline__ void exact_stage_sweep(const Stage& T, double* sv, do
       }
     }
     for (int g = lane; g < k; g += 32) ug[g] = us[g];
-    if (T.S > 1) {
-      __threadfence();
+    if (T.S > 1) {  // publish u_r (the release pattern of ordered_kernel's row visits)
       __syncwarp();
       if (lane == 0) st_release_gpu(T.fl + r, tag_now);
     }
