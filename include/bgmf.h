@@ -98,8 +98,11 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      CTAs (1).
  *   "u_prefetch" -1/0/1  L2 prefetch of upcoming runs' U rows: -1 (default)
  *                      when the mean run is < 1.5 ratings, 1 on, 0 off.
+ *   "u_ring"     -1/0/1  U rows of upcoming runs through a cp.async ring: -1
+ *                      (default) when the partition's ratings-per-user CV > 1
+ *                      (skewed users), 1 on, 0 off.
  *   Measured slower and kept off: "fuse_sse",
- *   "u_ring", "dyn_split" (int D), "snap" (int cap). */
+ *   "dyn_split" (int D), "snap" (int cap). */
 int bgmf_set_option(bgmf_ctx* ctx, const char* key, double value);
 
 /* Bucket the ratings into the I x J block grid on the GPU.

@@ -74,7 +74,9 @@ struct bgmf_ctx {
   int cstate_cap = 0;
   std::map<std::string, cudaGraphExec_t> conv_graphs;  // instantiated converge graphs per batch
   bool pdl = true;        // programmatic dependent launch between sweep / SSE kernels
-  bool u_ring = false;    // sweep: U rows of upcoming runs via a cp.async smem ring
+  int u_ring = -1;        // sweep: U rows of upcoming runs via a cp.async smem ring:
+                          // 1 on, 0 off, -1 when the users are skewed (row_cv)
+  double row_cv = 0.0;    // coefficient of variation of ratings per user (partition)
   bool fuse_sse = false;  // last sweep + SSE in one launch (sweep_sse_kernel; measured slower)
   unsigned* d_fuse = nullptr;  // sweep_sse_kernel's per-work-item counters
   int dyn_split = 1;           // sweep: chunks cut D ways, taken from a ticket counter

@@ -27,6 +27,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include <thread>
 
@@ -405,6 +406,45 @@ int sort_pairs_device(bgmf_ctx* ctx, uint64_t** keys, uint32_t** vals, int64_t n
 
 // dev_in: rows/cols/vals are device buffers whose ownership passes to this
 // call (freed as soon as they are consumed); otherwise host arrays.
+// Skew statistic of a partition (routes the sweep's u_ring, sgd.cu): the
+// coefficient of variation of the ratings per user.  Entries are sorted by
+// (block, row), so a warp's equal rows are neighbours: one atomic per distinct
+// (block, row) run per warp (__match_any_sync), then sum of squares.
+__global__ void row_hist(const int32_t* __restrict__ lrow, const int64_t* __restrict__ off,
+                         int nb, int J, int64_t rbase, int64_t rextra, int64_t nnz,
+                         unsigned* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+       base < nnz; base += warps * 32) {
+    const int64_t i = base + lane;
+    long long grow = -1;
+    if (i < nnz) {
+      int lo = 0, hi = nb - 1;  // last block b with off[b] <= i
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(off + mid) <= i) lo = mid; else hi = mid - 1;
+      }
+      const int64_t bi = lo / J;
+      grow = bi * rbase + min(bi, rextra) + __ldg(lrow + i);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, grow);
+    if (grow >= 0 && lane == __ffs(peers) - 1) atomicAdd(cnt + grow, (unsigned)__popc(peers));
+  }
+}
+
+__global__ void sum_squares(const unsigned* __restrict__ cnt, int64_t n,
+                            unsigned long long* __restrict__ out) {
+  unsigned long long acc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long c = cnt[i];
+    acc += c * c;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
 int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                      const double* vals, int64_t nnz, int64_t n, int64_t m, int I, int J,
                      bool dev_in, int64_t row_lo, int64_t row_hi) {
@@ -602,6 +642,28 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
                                                     rbits + cbits + (embed ? ibits : 0), d_off);
   PCK(cudaGetLastError());
   PCK(cudaMemcpyAsync(ctx->h_offsets.data(), d_off, (nb + 1) * 8, cudaMemcpyDeviceToHost, s));
+  // ratings-per-user skew (ctx->row_cv), reusing the sort's scratch (ia: nnz
+  // x 4 B >= n x 4 B is not guaranteed, so its own n counters)
+  ctx->row_cv = 0.0;
+  if (nnz > 0 && ctx->u_ring < 0) {
+    unsigned* cnt = nullptr;
+    unsigned long long* sq = nullptr;
+    PCK(dmalloc(&cnt, (size_t)n * 4, s));
+    PCK(dmalloc(&sq, 8, s));
+    PCK(cudaMemsetAsync(cnt, 0, (size_t)n * 4, s));
+    PCK(cudaMemsetAsync(sq, 0, 8, s));
+    row_hist<<<grid, 256, 0, s>>>(ctx->d_lrow, d_off, nb, J, rbase, rextra, nnz, cnt);
+    sum_squares<<<grid, 256, 0, s>>>(cnt, n, sq);
+    unsigned long long h_sq = 0;
+    cudaError_t e = cudaMemcpyAsync(&h_sq, sq, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    free_dev(cnt, s);
+    free_dev(sq, s);
+    PCK(e);
+    const double mean = (double)nnz / (double)n;
+    const double var = (double)h_sq / (double)n - mean * mean;
+    ctx->row_cv = var > 0.0 ? std::sqrt(var) / mean : 0.0;
+  }
   PCK(cudaStreamSynchronize(s));
   prof_mark(ctx, "partition: decode + offsets");
   cleanup();

@@ -1145,6 +1145,16 @@ constexpr double kUpfMaxRun = 1.5;
 
 int64_t sweep_groups(bgmf_ctx* c, const Shape& sh);
 
+// u_ring routing: the cp.async ring of upcoming runs' U rows measured +6% on
+// the Zipf-skewed C4Z and -11% on uniform C4, -15% on C5 (DESIGN 3.10c); the
+// partition's ratings-per-user CV separates them (uniform ~0.1, C4Z >> 1).
+// Device-resident partitions only (the out-of-core one computes no CV).
+constexpr double kURingMinCV = 1.0;
+
+bool uring_route(bgmf_ctx* c) {
+  return c->u_ring > 0 || (c->u_ring < 0 && !c->streaming && c->row_cv > kURingMinCV);
+}
+
 bool upf_route(bgmf_ctx* c) {
   const int64_t key = c->nnz * 8191 + (int64_t)c->I * c->J;
   if (c->upf_key != key) {
@@ -1165,7 +1175,8 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
   const bool mk = needs_mask(sh, c->kp);
   const int dd = sweep && c->d_dyn ? c->dyn_split : 1;
   int sn = c->snap_cap | (upf_route(c) ? 1 << 16 : 0);
-  if (sweep && c->spread && dd <= 1 && !c->bulk_red && !c->u_ring) {
+  const bool uring = sweep && uring_route(c);
+  if (sweep && c->spread && dd <= 1 && !c->bulk_red && !uring) {
     // a partial wave that would leave some SMs with fewer CTAs than others:
     // launch the full wave and deal the chunks evenly (sgd_fast_kernel)
     const int64_t cap = sweep_groups(c, sh) / (8 * (32 / sh.L));
@@ -1183,7 +1194,7 @@ void launch_fast_ptr(bool sweep, const Shape& sh, dim3 grid, cudaStream_t s, con
       sgd_fast_kernel<LL, VV, MM, 1><<<grid, 256, bulk_smem(c, sh), s>>>(                     \
           w, nwork, total, lrow, lcol, val, c->d_u, c->d_v, c->kp, a, b, it, c->d_bad, cbits, dd,    \
           c->d_dyn, sn);                                                                          \
-    } else if (sweep && c->u_ring && LL >= 4) {                                               \
+    } else if (uring && LL >= 4) {                                                            \
       constexpr int UD = LL >= 8 ? 4 : 3;                                                     \
       const int sm = 256 * UD * VV * 16;                                                      \
       cudaFuncSetAttribute(&sgd_fast_kernel<LL, VV, MM, 2>,                                  \
