@@ -660,8 +660,11 @@ int partition_device(bgmf_ctx* ctx, const int64_t* rows, const int64_t* cols,
     free_dev(cnt, s);
     free_dev(sq, s);
     PCK(e);
-    const double mean = (double)nnz / (double)n;
-    const double var = (double)h_sq / (double)n - mean * mean;
+    // over the kept rows (a ring rank's shard; the others count 0 and add
+    // nothing to the sum of squares)
+    const double rows_kept = (double)std::max<int64_t>(1, row_hi - row_lo);
+    const double mean = (double)nnz / rows_kept;
+    const double var = (double)h_sq / rows_kept - mean * mean;
     ctx->row_cv = var > 0.0 ? std::sqrt(var) / mean : 0.0;
   }
   PCK(cudaStreamSynchronize(s));
