@@ -86,6 +86,7 @@ struct bgmf_ctx {
   bool upf_on = false;         // resolved for the current partition
   int64_t upf_key = -1;        // partition the resolution belongs to
   bool spread = true;          // sweep: partial waves dealt evenly over a full wave of CTAs
+  bool nt_download = true;     // model download: non-temporal fp64 stores
   int snap_cap = 0;            // sweep: chunk edges moved to the end of a run within this many ratings
   int fused = -1;      // 1: one cooperative launch per step, 0: per stratum, -1 auto
   int groups_key = -1;                // sweep_groups() cache

@@ -223,6 +223,7 @@ int bgmf_set_option(bgmf_ctx* c, const char* key, double value) {
   else if (!strcmp(key, "u_ring")) c->u_ring = value < 0.0 ? -1 : (value != 0.0 ? 1 : 0);
   else if (!strcmp(key, "u_prefetch")) { c->u_prefetch = value < 0.0 ? -1 : value != 0.0; c->upf_key = -1; }
   else if (!strcmp(key, "spread")) c->spread = value != 0.0;
+  else if (!strcmp(key, "nt_download")) c->nt_download = value != 0.0;
   else if (!strcmp(key, "snap")) c->snap_cap = value < 0.0 ? 0 : value > 4096.0 ? 4096 : (int)value;
   else if (!strcmp(key, "dyn_split")) {
     c->dyn_split = value < 1.0 ? 1 : value > 16.0 ? 16 : (int)value;

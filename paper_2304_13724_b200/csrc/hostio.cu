@@ -14,6 +14,7 @@
 // context: OpenMP threads convert between the reference's host types and the
 // device types in the staging buffer while the DMA engine moves the other one.
 
+#include <emmintrin.h>
 #include <omp.h>
 #include <sys/mman.h>
 
@@ -387,7 +388,19 @@ int download_rows(bgmf_ctx* c, const float* d, double* h, int64_t rows, int k, i
     const int64_t r0 = p * chunk, nr = rows - r0 < chunk ? rows - r0 : chunk;
     const float* src = reinterpret_cast<const float*>(st.buf(p & 1));
     double* dst = h + r0 * k;
-    if (kp == k) {
+    if (kp == k && c->nt_download && ((uintptr_t)dst & 15) == 0 && (nr * k) % 2 == 0) {
+      // widen with non-temporal 16-byte stores: the fp64 model is written once
+      // and not read back here, so no read-for-ownership of its lines
+      const int64_t pairs = nr * k / 2;
+#pragma omp parallel
+      {
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < pairs; ++i)
+          _mm_stream_pd(dst + 2 * i, _mm_cvtps_pd(_mm_castsi128_ps(
+                                          _mm_loadl_epi64(reinterpret_cast<const __m128i*>(src + 2 * i)))));
+        _mm_sfence();
+      }
+    } else if (kp == k) {
       const int64_t tot = nr * k;
 #pragma omp parallel for schedule(static)
       for (int64_t i = 0; i < tot; ++i) dst[i] = (double)src[i];
