@@ -98,6 +98,8 @@ const char* bgmf_last_error(const bgmf_ctx* ctx);
  *                      CTAs (1).
  *   "u_prefetch" -1/0/1  L2 prefetch of upcoming runs' U rows: -1 (default)
  *                      when the mean run is < 1.5 ratings, 1 on, 0 off.
+ *   "nt_download" 0/1  the model's fp32 -> fp64 widening into the caller's
+ *                      arrays uses non-temporal stores (1).
  *   "u_ring"     -1/0/1  U rows of upcoming runs through a cp.async ring: -1
  *                      (default) when the partition's ratings-per-user CV > 1
  *                      (skewed users), 1 on, 0 off.
