@@ -513,7 +513,9 @@ def run_out_of_core(args, dev):
                "d2h_bytes_per_step": ((w.n + w.m) * kp * 4 + nnz * 16) / args.steps,
                "what": "train_blocked(host RatingsDataset, device_rating_budget) incl. the "
                        "out-of-core partition (host bucketing, device chunks, D2H into "
-                       "pinned layout), K streamed epochs, D2H model; one call",
+                       "pinned layout), K streamed epochs, D2H model; one call, in a "
+                       "process whose pinned-buffer cache is warm (the device-resident "
+                       "leg above ran first: the layout's pages are already registered)",
                "wall_s": wall, "gen_s": t_gen,
                "train_rmse_trace": [s.train_rmse for s in res.trace]}
         del res, d, rr, cc, vv

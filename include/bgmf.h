@@ -153,6 +153,12 @@ int bgmf_partition_export(bgmf_ctx* ctx, int64_t* offsets, int64_t* order,
  * the ratings stream from host memory). */
 int bgmf_partition_values(bgmf_ctx* ctx, double* vals);
 
+/* Out-of-core partitions keep their pinned host layout; when a context is
+ * destroyed those buffers stay registered in a process-wide cache (up to a
+ * quarter of physical memory) for the next out-of-core partition, like a
+ * caching host allocator.  This unregisters and unmaps all of them. */
+int bgmf_release_host_cache(void);
+
 /* Upload U (n x k) and V (m x k), row-major fp64 as FactorModel.u/.v
  * (core.py:139-176).  Fast mode stores fp32 rows padded to a multiple of 4. */
 int bgmf_set_factors(bgmf_ctx* ctx, const double* u, const double* v,

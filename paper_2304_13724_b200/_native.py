@@ -45,6 +45,7 @@ SIGNATURES = {
     "bgmf_partition": (_i, [_ctx, _i64p, _i64p, _f64p, _l, _l, _l, _i, _i]),
     "bgmf_partition_export": (_i, [_ctx, _i64p, _i64p, _i32p, _i32p]),
     "bgmf_partition_values": (_i, [_ctx, _f64p]),
+    "bgmf_release_host_cache": (_i, []),
     "bgmf_synth_partition": (_i, [_ctx, _l, _l, _l, ctypes.c_uint64, _i, _i]),
     "bgmf_synth": (_i, [_l, _l, _l, _l, ctypes.c_uint64, _i64p, _i64p, _f64p]),
     "bgmf_set_factors": (_i, [_ctx, _f64p, _f64p, _l, _l, _i]),

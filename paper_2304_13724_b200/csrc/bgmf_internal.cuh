@@ -280,6 +280,7 @@ void pinned_free(void* p);
 // GB-sized pinned arrays: THP-backed + cudaHostRegister; freed off-thread
 cudaError_t big_pinned_alloc(void** p, size_t bytes, int threads = 0);
 void big_pinned_free(void* p);
+void big_pinned_trim();
 void* big_host_alloc(size_t bytes);
 void big_host_free(void* p);
 void big_host_release(void* p, size_t bytes);

@@ -336,6 +336,11 @@ int bgmf_partition_export(bgmf_ctx* c, int64_t* offsets, int64_t* order, int32_t
   return BGMF_OK;
 }
 
+int bgmf_release_host_cache(void) {
+  big_pinned_trim();
+  return BGMF_OK;
+}
+
 int bgmf_partition_values(bgmf_ctx* c, double* vals) {
   if (!c || !vals) return fail(c, BGMF_ERR_ARG, "ctx or vals is NULL");
   if (!c->partitioned) return fail(c, BGMF_ERR_STATE, "bgmf_partition has not been called");

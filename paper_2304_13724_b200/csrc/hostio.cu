@@ -17,6 +17,7 @@
 #include <emmintrin.h>
 #include <omp.h>
 #include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstring>
@@ -140,19 +141,61 @@ void pinned_free(void* p) {
 // in by all host threads (one write per 2 MiB page), then cudaHostRegister.
 // Released on a detached thread: unpinning GBs costs seconds the caller
 // does not need to wait for.
+//
+// Freed pinned buffers are cached (like a caching host allocator) up to a
+// quarter of physical memory: unregistering tens of GB takes the driver lock
+// for a few hundred ms, stalling the caller's next CUDA call (C5: the context
+// release), and the next out-of-core partition of a similar size reuses the
+// registered pages instead of pinning again (0.6-1.8 s for C5's layout).
+// bgmf_release_host_cache() gives everything back.
 namespace {
+struct CachedPin {
+  void* p;
+  void* base;
+  size_t len, span;
+};
 struct BigPinned {
   std::mutex mu;
   std::unordered_map<void*, std::pair<void*, size_t>> maps;  // user ptr -> (mmap base, len)
+  std::unordered_map<void*, size_t> spans;                    // registered bytes
+  std::vector<CachedPin> cache;  // registered, unused
+  size_t cached = 0;
 };
 BigPinned& big_pinned() {
   static BigPinned* p = new BigPinned;
   return *p;
 }
+size_t& pin_span_of(void* p) { return big_pinned().spans[p]; }  // under mu
+size_t pin_cache_cap() {
+  static const size_t cap = [] {
+    const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
+    return pages > 0 && psz > 0 ? (size_t)pages * (size_t)psz / 4 : (size_t)0;
+  }();
+  return cap;
+}
 }  // namespace
 
 cudaError_t big_pinned_alloc(void** out, size_t bytes, int threads) {
   const size_t huge = size_t(2) << 20;
+  {  // a cached registered buffer of the same order of size
+    const size_t want = (bytes + huge - 1) / huge * huge;
+    std::lock_guard<std::mutex> lk(big_pinned().mu);
+    auto& c = big_pinned().cache;
+    int best = -1;
+    for (int i = 0; i < (int)c.size(); ++i)
+      if (c[i].span >= want && c[i].span <= 2 * want + huge &&
+          (best < 0 || c[i].span < c[best].span))
+        best = i;
+    if (best >= 0) {
+      const CachedPin h = c[best];
+      c.erase(c.begin() + best);
+      big_pinned().cached -= h.span;
+      big_pinned().maps[h.p] = {h.base, h.len};
+      pin_span_of(h.p) = h.span;
+      *out = h.p;
+      return cudaSuccess;
+    }
+  }
   const size_t len = (bytes + 2 * huge - 1) / huge * huge;
   void* base = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
   if (base == MAP_FAILED) return cudaErrorMemoryAllocation;
@@ -170,6 +213,7 @@ cudaError_t big_pinned_alloc(void** out, size_t bytes, int threads) {
   {
     std::lock_guard<std::mutex> lk(big_pinned().mu);
     big_pinned().maps[p] = {base, len};
+    pin_span_of(p) = span;
   }
   *out = p;
   return cudaSuccess;
@@ -253,12 +297,24 @@ int staged_h2d(bgmf_ctx* ctx, void* dst, const void* src, size_t bytes) {
 void big_pinned_free(void* p) {
   if (!p) return;
   std::pair<void*, size_t> m{nullptr, 0};
+  size_t span = 0;
   {
     std::lock_guard<std::mutex> lk(big_pinned().mu);
-    auto it = big_pinned().maps.find(p);
-    if (it != big_pinned().maps.end()) {
+    BigPinned& bp = big_pinned();
+    auto it = bp.maps.find(p);
+    if (it != bp.maps.end()) {
       m = it->second;
-      big_pinned().maps.erase(it);
+      bp.maps.erase(it);
+      auto sp = bp.spans.find(p);
+      if (sp != bp.spans.end()) {
+        span = sp->second;
+        bp.spans.erase(sp);
+      }
+      if (span && bp.cached + span <= pin_cache_cap()) {  // keep it registered
+        bp.cache.push_back(CachedPin{p, m.first, m.second, span});
+        bp.cached += span;
+        return;
+      }
     }
   }
   if (!m.first) {
@@ -269,6 +325,20 @@ void big_pinned_free(void* p) {
     cudaHostUnregister(p);
     munmap(m.first, m.second);
   }).detach();
+}
+
+// Unregister and unmap every cached pinned buffer (bgmf_release_host_cache).
+void big_pinned_trim() {
+  std::vector<CachedPin> c;
+  {
+    std::lock_guard<std::mutex> lk(big_pinned().mu);
+    c.swap(big_pinned().cache);
+    big_pinned().cached = 0;
+  }
+  for (const CachedPin& h : c) {
+    cudaHostUnregister(h.p);
+    munmap(h.base, h.len);
+  }
 }
 
 // Dataset upload for the partitioner (partition.cu): int64 indices narrowed

@@ -84,6 +84,12 @@ class EngineOptions:
     ordered: bool | None = None
 
 
+def release_host_cache() -> None:
+    """Unregister the pinned host buffers cached by closed out-of-core contexts
+    (bgmf_release_host_cache)."""
+    N.check(N.load().bgmf_release_host_cache(), None)
+
+
 def default_device() -> int:
     for var in ("BGMF_DEVICE", "LOCAL_RANK"):
         v = os.environ.get(var)

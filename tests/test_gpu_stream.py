@@ -162,3 +162,27 @@ def test_out_of_core_partition_peak_memory():
           f"{slots / 2**20:.1f} MB)")
     assert high - base2 <= budget + slots + (4 << 20)
     assert high - base2 < (high_in - base) / 4
+
+
+def test_out_of_core_pinned_cache_reuse():
+    """A closed out-of-core context leaves its pinned layout in the process
+    cache; the next partition of the same size reuses it (no re-pinning) and
+    is still bit-identical; bgmf_release_host_cache empties the cache."""
+    from paper_2304_13724_b200.device import release_host_cache
+    n, m, nnz, P = 3000, 2000, 80_000, 5
+    g = np.random.default_rng(9)
+    cells = g.choice(n * m, nnz, replace=False)
+    r, c = np.divmod(cells, m)
+    v = np.clip(np.rint(3 + g.normal(0, 1, nnz)), 1, 5)
+    outs = []
+    for _ in range(3):
+        eng = bm.Engine(bm.EngineOptions(device_rating_budget=12 * 6000 * 3, stream_slots=3))
+        eng.partition(r, c, v, n, m, P, P)
+        assert eng.streaming
+        outs.append(eng.export_partition())
+        eng.close()
+    for got in outs[1:]:
+        for a, b in zip(got, outs[0]):
+            assert np.array_equal(a, b)
+    release_host_cache()
+    release_host_cache()  # idempotent
